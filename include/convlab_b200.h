@@ -1,0 +1,140 @@
+/* convlab_b200.h -- the drop-in C ABI of the B200-native kn2row / im2col hot path.
+ *
+ * Plain pointers and sizes only (no torch, no C++ types).  All tensors are fp32.
+ * Device entry points take DEVICE pointers and a cudaStream_t passed as void*.
+ * Layouts are the reference's: input NCHW (N stacked CHW images, tensor.hpp:86-90),
+ * kernels MKKC ((m*k+i)*k+j)*C+c (tensor.hpp:120-125), output NCHW.
+ *
+ * Reference interfaces each entry point replaces (paths under /root/reference/proj/core):
+ *   cl_conv_desc        <- LayerConfig{C,H,W,M,k,stride} (include/convlab/layers.hpp:12-22)
+ *                          + the implicit pad = k/2 of ConvProblem (conv_direct.hpp:7-10)
+ *                          + a batch dimension N (the reference has none)
+ *   cl_method           <- ConvMethod (include/convlab/methods.hpp:15-23)
+ *   cl_conv_plan        <- ConvProblem validation (src/conv_direct.cpp:8-21) + the
+ *                          kn2row_reorder_kernel pre-pack (src/conv_kn2.cpp:28-39), done once
+ *   cl_conv_forward     <- run_method(method, ConvProblem, GemmBackend) (src/methods.cpp:65-88)
+ *   cl_conv_forward_host<- the same call with host buffers (run_method returns a host Tensor3)
+ *   cl_gemm_f32         <- the external-GEMM plugin signature Matrix(MatrixView, MatrixView)
+ *                          registered via register_gemm_backend (include/convlab/gemm.hpp:52-58)
+ *   cl_shift_add_row    <- shift_add, row orientation (src/conv_kn2.cpp:78-118)
+ *   cl_last_error       <- the what() text of the exceptions the reference throws
+ *
+ * Error behaviour mirrors the reference: contract violations (the reference's
+ * std::invalid_argument) return CL_EINVAL; unsupported shapes CL_EUNSUPPORTED; CUDA
+ * failures CL_ECUDA.  cl_last_error() returns the thread-local message of the last failure.
+ * No entry point falls back to the CPU: without a usable sm_100 device they fail.
+ */
+#ifndef CONVLAB_B200_H
+#define CONVLAB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CL_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define CL_API __attribute__((visibility("default")))
+#else
+#define CL_API
+#endif
+
+typedef enum cl_status {
+    CL_OK = 0,
+    CL_EINVAL = 1,        /* contract violation (reference: std::invalid_argument)        */
+    CL_EUNSUPPORTED = 2,  /* valid but not implemented on this path                        */
+    CL_ECUDA = 3,         /* CUDA runtime / driver failure                                 */
+    CL_ENOMEM = 4,        /* device allocation failed (reference: bench.cpp:44-54 message) */
+    CL_ENODEVICE = 5,     /* no sm_100 device visible                                      */
+    CL_EINTERNAL = 6
+} cl_status;
+
+/* GPU conv methods.  The names mirror ConvMethod (methods.cpp:11-33) with a -gpu suffix. */
+typedef enum cl_method {
+    CL_METHOD_AUTO = 0,          /* per-layer selector ("auto")                                      */
+    CL_METHOD_KN2ROW = 1,        /* implicit kn2row: k^2 shifted 1x1 GEMMs fused in one TMEM accumulator */
+    CL_METHOD_KN2ROW_EXPLICIT = 2,/* paper-faithful: one (k^2 M x C).(C x NHW) GEMM + shift-add kernel */
+    CL_METHOD_KN2COL = 3,        /* transposed: one (NHW x C).(C x k^2 M) GEMM + column shift-add      */
+    CL_METHOD_KN2ROW_ACC = 4,    /* accumulating: k^2 shifted GEMM launches summing into the output    */
+    CL_METHOD_IM2COL = 5,        /* baseline: patch matrix (NHW x k^2 C) + one GEMM                     */
+    CL_METHOD_CONV1X1 = 6        /* k == 1 only (CL_EINVAL otherwise, methods.cpp:81-85)                */
+} cl_method;
+
+typedef enum cl_precision {
+    CL_PREC_FP32 = 0,  /* fp32-faithful 3xTF32 (rel-L2 <= 1e-5 vs the fp32 oracle)   */
+    CL_PREC_TF32 = 1   /* single TF32 pass (fast mode, 1e-2 tolerance)              */
+} cl_precision;
+
+typedef struct cl_conv_desc {
+    int32_t n;       /* batch (images)                              */
+    int32_t c;       /* input channels  C                           */
+    int32_t h;       /* input height    H                           */
+    int32_t w;       /* input width     W                           */
+    int32_t m;       /* kernels         M (output channels)         */
+    int32_t k;       /* kernel size (odd, as KernelSet enforces)    */
+    int32_t pad;     /* zero padding; -1 = reference default k/2   */
+    int32_t stride;  /* 1 (the reference rejects others: bench.cpp:90-92) */
+} cl_conv_desc;
+
+typedef struct cl_plan cl_plan;
+
+/* Validates the descriptor, selects method/tile shape, allocates the packed-weight
+ * storage on `device`.  *out_plan is owned by the caller (cl_conv_destroy). */
+CL_API cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision precision, int device,
+                       cl_plan** out_plan);
+
+/* Uploads MKKC weights from a DEVICE pointer: one-time reorder + TF32 hi/lo split. */
+CL_API cl_status cl_conv_set_weights(cl_plan* plan, const float* d_w_mkkc, void* stream);
+
+/* Same, from a HOST pointer (H2D inside; synchronous on `stream`). */
+CL_API cl_status cl_conv_set_weights_host(cl_plan* plan, const float* h_w_mkkc, void* stream);
+
+/* Output spatial size chosen by the plan: P = (H + 2 pad - k)/stride + 1, Q likewise. */
+CL_API cl_status cl_conv_output_dims(const cl_plan* plan, int32_t* p, int32_t* q);
+
+/* Bytes of device scratch cl_conv_forward needs (split input, intermediates, patches). */
+CL_API size_t cl_conv_workspace_bytes(const cl_plan* plan);
+
+/* The method the plan resolved to (auto -> concrete). */
+CL_API cl_method cl_conv_resolved_method(const cl_plan* plan);
+
+/* y[N][M][P][Q] = conv(x[N][C][H][W], w).  d_ws may be NULL: the plan then owns a lazily
+ * allocated workspace.  Asynchronous on `stream`; returns after enqueueing. */
+CL_API cl_status cl_conv_forward(cl_plan* plan, const float* d_x, float* d_y, void* d_ws, void* stream);
+
+/* Host-buffer end-to-end call (the run_method surface): H2D of x, forward, D2H of y,
+ * synchronous.  Host buffers should be pinned for full PCIe bandwidth. */
+CL_API cl_status cl_conv_forward_host(cl_plan* plan, const float* h_x, float* h_y, void* stream);
+
+/* Number of GPU kernel launches the last cl_conv_forward enqueued. */
+CL_API int cl_conv_last_launch_count(const cl_plan* plan);
+
+CL_API void cl_conv_destroy(cl_plan* plan);
+
+/* C[m x n] = A[m x k] . B[k x n], all row-major fp32 DEVICE pointers (the reference's
+ * gemm() contract, gemm.hpp:34-50).  d_ws may be NULL (internal scratch is allocated). */
+CL_API cl_status cl_gemm_f32(int m, int n, int k, const float* d_a, const float* d_b, float* d_c,
+                      cl_precision precision, void* d_ws, size_t ws_bytes, void* stream);
+CL_API size_t cl_gemm_workspace_bytes(int m, int n, int k, cl_precision precision);
+
+/* shift_add (row orientation) on the device: inter[(k^2 M) x (N H W)] -> y NCHW with
+ * output P x Q (pad = k/2 keeps P = H).  Exposed for the decomposition tests. */
+CL_API cl_status cl_shift_add_row(const float* d_inter, float* d_y, int n, int m, int h, int w, int k, int pad,
+                           void* stream);
+
+CL_API const char* cl_last_error(void);
+CL_API const char* cl_method_name(cl_method method);
+CL_API int cl_method_from_name(const char* name, cl_method* out);
+CL_API int cl_abi_version(void);
+
+/* Number of sm_100 devices usable by this library (0 on a CPU-only host). */
+CL_API int cl_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CONVLAB_B200_H */

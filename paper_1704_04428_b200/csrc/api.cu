@@ -1,0 +1,508 @@
+// api.cu -- the extern "C" boundary (include/convlab_b200.h): plans, method dispatch,
+// workspace management, error mapping.  No CPU fallback anywhere: every entry point
+// either enqueues sm_100a kernels or returns an error.
+#include <cstring>
+#include <string>
+
+#include "../../include/convlab_b200.h"
+#include "internal.hpp"
+
+using namespace clb;
+
+namespace {
+
+thread_local std::string g_err;
+
+cl_status fail(cl_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+template <class F>
+cl_status guarded(F&& f) {
+    try {
+        f();
+        return CL_OK;
+    } catch (const Error& e) {
+        return fail((cl_status)e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(CL_ENOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(CL_EINTERNAL, e.what());
+    }
+}
+
+void require(bool ok, const std::string& what) {
+    if (!ok) throw Error(CL_EINVAL, what);
+}
+
+int bn_for(int cols) {
+    const int tiles = (cols + 255) / 256;
+    const int per = (cols + tiles - 1) / tiles;
+    int bn = round_up(per, 16);
+    if (bn < 16) bn = 16;
+    return bn > 256 ? 256 : bn;
+}
+
+}  // namespace
+
+struct cl_plan {
+    cl_conv_desc d{};
+    int P = 0, Q = 0;
+    cl_method requested = CL_METHOD_AUTO, method = CL_METHOD_AUTO;
+    cl_precision prec = CL_PREC_FP32;
+    int planes = 2;
+    int device = 0;
+    int Cp = 0;            // channels padded to the 16-wide K block (kn2 methods)
+    int Kp = 0;            // k*k*C padded (im2col)
+    int bn = 0;
+    float* wpack = nullptr;
+    size_t wpack_bytes = 0;
+    bool weights_set = false;
+    void* own_ws = nullptr;
+    size_t own_ws_bytes = 0;
+    float* host_x = nullptr;   // device staging for cl_conv_forward_host
+    float* host_y = nullptr;
+    int launches = 0;
+};
+
+namespace {
+
+cl_method resolve(const cl_conv_desc& d, cl_method m) {
+    if (m != CL_METHOD_AUTO) return m;
+    // Per-layer selector.  The implicit kernel is the default; tiny-C first layers (VGG
+    // conv1_1, C = 3) waste 13/16 of every 16-channel K block per tap, while im2col packs
+    // all k^2 C taps densely into K (27 -> 32), so it wins there (PAPER.md:484 found a
+    // non-kn2 method best on that layer too).
+    if (d.k > 1 && d.c * 4 <= 16) return CL_METHOD_IM2COL;
+    return CL_METHOD_KN2ROW;
+}
+
+size_t ws_bytes(const cl_plan* p) {
+    const cl_conv_desc& d = p->d;
+    const size_t nhw = (size_t)d.n * d.h * d.w;
+    const size_t npq = (size_t)d.n * p->P * p->Q;
+    const size_t xs = nhw * p->planes * p->Cp * 4;
+    const size_t kk = (size_t)d.k * d.k;
+    switch (p->method) {
+        case CL_METHOD_KN2ROW:
+        case CL_METHOD_CONV1X1:
+        case CL_METHOD_KN2ROW_ACC:
+            return xs;
+        case CL_METHOD_KN2ROW_EXPLICIT:
+        case CL_METHOD_KN2COL:
+            return xs + kk * d.m * nhw * 4;
+        case CL_METHOD_IM2COL:
+            return npq * p->planes * p->Kp * 4;
+        default:
+            return 0;
+    }
+}
+
+void check_device(int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw Error(CL_ENODEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+    }
+    if (device < 0 || device >= count) throw Error(CL_EINVAL, "device index out of range");
+    int major = 0;
+    CLB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10) throw Error(CL_ENODEVICE, "device is not sm_100 (compute capability 10.x required)");
+}
+
+Operand implicit_a(const cl_plan* p, const float* xs) {
+    Operand a;
+    a.mode = LOAD_IM2COL;
+    a.ptr = xs;
+    a.kp = p->Cp;
+    a.planes = p->planes;
+    a.n = p->d.n;
+    a.h = p->d.h;
+    a.w = p->d.w;
+    a.k = p->d.k;
+    a.pad = p->d.pad;
+    return a;
+}
+
+Operand tiled(const float* ptr, long long rows, int taps, int kp, int planes) {
+    Operand o;
+    o.mode = LOAD_TILED;
+    o.ptr = ptr;
+    o.rows = rows;
+    o.taps = taps;
+    o.kp = kp;
+    o.planes = planes;
+    return o;
+}
+
+TcParams base_params(const cl_plan* p) {
+    TcParams t{};
+    t.ksize = p->d.k;
+    t.P = p->P;
+    t.Q = p->Q;
+    t.pad = p->d.pad;
+    return t;
+}
+
+void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
+    const cl_conv_desc& d = p->d;
+    require(p->weights_set, "cl_conv_forward: weights not set (cl_conv_set_weights)");
+    require(x && y, "cl_conv_forward: null tensor");
+    CLB_CUDA(cudaSetDevice(p->device));
+    const size_t need = ws_bytes(p);
+    if (!ws && need) {
+        if (p->own_ws_bytes < need) {
+            if (p->own_ws) cudaFree(p->own_ws);
+            p->own_ws = nullptr;
+            p->own_ws_bytes = 0;
+            if (cudaMalloc(&p->own_ws, need) != cudaSuccess) {
+                cudaGetLastError();
+                throw Error(CL_ENOMEM, "workspace allocation failed: requires " + std::to_string(need) + " bytes");
+            }
+            p->own_ws_bytes = need;
+        }
+        ws = p->own_ws;
+    }
+    const int taps = d.k * d.k;
+    const long long nhw = (long long)d.n * d.h * d.w;
+    const long long npq = (long long)d.n * p->P * p->Q;
+    float* wsf = static_cast<float*>(ws);
+    p->launches = 0;
+
+    switch (p->method) {
+        case CL_METHOD_KN2ROW:
+        case CL_METHOD_CONV1X1:
+        case CL_METHOD_KN2ROW_ACC: {
+            float* xs = wsf;
+            launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
+            ++p->launches;
+            Operand a = implicit_a(p, xs);
+            Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
+            TcParams t = base_params(p);
+            t.rows = (int)npq;
+            t.cols = d.m;
+            t.bn = p->bn;
+            t.b_tap3 = 1;
+            t.epi = EPI_NCHW;
+            t.out = y;
+            t.out_channels = d.m;
+            t.pq_out = p->P * p->Q;
+            if (p->method == CL_METHOD_KN2ROW_ACC) {
+                // k^2 shifted GEMMs, each accumulating into the output (tap 0 overwrites).
+                for (int tap = 0; tap < taps; ++tap) {
+                    t.taps = 1;
+                    t.tap_begin = tap;
+                    t.accumulate = tap > 0;
+                    launch_tc(a, b, t, s);
+                    ++p->launches;
+                }
+            } else {
+                t.taps = taps;
+                t.tap_begin = 0;
+                launch_tc(a, b, t, s);
+                ++p->launches;
+            }
+            break;
+        }
+        case CL_METHOD_KN2ROW_EXPLICIT:
+        case CL_METHOD_KN2COL: {
+            float* xs = wsf;
+            float* inter = wsf + nhw * p->planes * p->Cp;
+            launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
+            ++p->launches;
+            Operand wts = tiled(p->wpack, (long long)taps * d.m, 1, p->Cp, p->planes);
+            Operand pix = tiled(xs, nhw, 1, p->Cp, p->planes);
+            TcParams t = base_params(p);
+            t.taps = 1;
+            t.epi = EPI_ROWMAJOR;
+            t.out = inter;
+            if (p->method == CL_METHOD_KN2ROW_EXPLICIT) {
+                // (k^2 M x C) . (C x NHW): the paper's single kn2row GEMM (conv_kn2.cpp:145-162)
+                t.rows = taps * d.m;
+                t.cols = (int)nhw;
+                t.ld = nhw;
+                t.bn = 256;
+                launch_tc(wts, pix, t, s);
+                ++p->launches;
+                launch_shift_add_row(inter, y, d.n, d.m, d.h, d.w, d.k, d.pad, p->P, p->Q, s);
+            } else {
+                // (NHW x C) . (C x k^2 M): the kn2col GEMM (conv_kn2.cpp:164-183)
+                t.rows = (int)nhw;
+                t.cols = taps * d.m;
+                t.ld = (long long)taps * d.m;
+                t.bn = bn_for(taps * d.m);
+                launch_tc(pix, wts, t, s);
+                ++p->launches;
+                launch_shift_add_col(inter, y, d.n, d.m, d.h, d.w, d.k, d.pad, p->P, p->Q, s);
+            }
+            ++p->launches;
+            break;
+        }
+        case CL_METHOD_IM2COL: {
+            float* pm = wsf;
+            launch_im2col_split(x, pm, d.n, d.c, d.h, d.w, d.k, d.pad, d.stride, p->P, p->Q, p->Kp, p->planes, s);
+            ++p->launches;
+            Operand a = tiled(pm, npq, 1, p->Kp, p->planes);
+            Operand b = tiled(p->wpack, d.m, 1, p->Kp, p->planes);
+            TcParams t = base_params(p);
+            t.rows = (int)npq;
+            t.cols = d.m;
+            t.bn = p->bn;
+            t.taps = 1;
+            t.epi = EPI_NCHW;
+            t.out = y;
+            t.out_channels = d.m;
+            t.pq_out = p->P * p->Q;
+            launch_tc(a, b, t, s);
+            ++p->launches;
+            break;
+        }
+        default:
+            throw Error(CL_EINTERNAL, "unresolved method");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision precision, int device,
+                       cl_plan** out_plan) {
+    return guarded([&] {
+        require(desc && out_plan, "cl_conv_plan: null argument");
+        *out_plan = nullptr;
+        cl_conv_desc d = *desc;
+        require(d.n > 0 && d.c > 0 && d.h > 0 && d.w > 0 && d.m > 0 && d.k > 0,
+                "cl_conv_plan: dimensions must be positive");
+        require(d.k % 2 == 1, "kernel size must be odd, got " + std::to_string(d.k));   // tensor.cpp:64,71
+        if (d.pad < 0) d.pad = d.k / 2;
+        if (d.stride <= 0) d.stride = 1;
+        // ConvProblem's bound k <= min(H,W) + k/2 (conv_direct.cpp:15-20) at the default pad
+        const int bound = (d.h < d.w ? d.h : d.w) + d.k / 2;
+        require(d.pad != d.k / 2 || d.k <= bound,
+                "ConvProblem: kernel size " + std::to_string(d.k) + " exceeds padded image bound " +
+                    std::to_string(bound));
+        require(precision == CL_PREC_FP32 || precision == CL_PREC_TF32, "unknown precision");
+        if (method == CL_METHOD_CONV1X1)
+            require(d.k == 1, "conv1x1 requires a 1x1 kernel, got k = " + std::to_string(d.k));
+        const int P = (d.h + 2 * d.pad - d.k) / d.stride + 1;
+        const int Q = (d.w + 2 * d.pad - d.k) / d.stride + 1;
+        require(P > 0 && Q > 0, "cl_conv_plan: empty output");
+        cl_method m = resolve(d, method);
+        if (d.k == 1 && (m == CL_METHOD_KN2ROW_EXPLICIT || m == CL_METHOD_KN2COL)) m = CL_METHOD_CONV1X1;
+        if (m != CL_METHOD_IM2COL) {
+            if (d.stride != 1) throw Error(CL_EUNSUPPORTED, "kn2 methods support stride 1 only (im2col supports stride)");
+            if (d.pad > 127 || d.k - 1 - d.pad > 128)
+                throw Error(CL_EUNSUPPORTED, "padding outside the TMA im2col bounding-box range");
+            if ((m == CL_METHOD_KN2ROW_EXPLICIT || m == CL_METHOD_KN2COL) && (P != d.h || Q != d.w))
+                throw Error(CL_EUNSUPPORTED, "explicit kn2row/kn2col need same padding (pad = k/2)");
+        }
+        check_device(device);
+        CLB_CUDA(cudaSetDevice(device));
+        auto* p = new cl_plan;
+        p->d = d;
+        p->P = P;
+        p->Q = Q;
+        p->requested = method;
+        p->method = m;
+        p->prec = precision;
+        p->planes = precision == CL_PREC_FP32 ? 2 : 1;
+        p->device = device;
+        p->Cp = round_up(d.c, kBlockK);
+        p->Kp = round_up(d.k * d.k * d.c, kBlockK);
+        p->bn = bn_for(d.m);
+        if (m == CL_METHOD_IM2COL) p->wpack_bytes = (size_t)d.m * p->planes * p->Kp * 4;
+        else p->wpack_bytes = (size_t)d.k * d.k * d.m * p->planes * p->Cp * 4;
+        if (cudaMalloc(&p->wpack, p->wpack_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            delete p;
+            throw Error(CL_ENOMEM, "packed-weight allocation failed");
+        }
+        *out_plan = p;
+    });
+}
+
+cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
+    return guarded([&] {
+        require(p && d_w, "cl_conv_set_weights: null argument");
+        CLB_CUDA(cudaSetDevice(p->device));
+        auto s = static_cast<cudaStream_t>(stream);
+        const cl_conv_desc& d = p->d;
+        if (p->method == CL_METHOD_IM2COL)
+            launch_rows_split(d_w, p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);   // MKKC == M x k^2C
+        else
+            launch_pack_weights(d_w, p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s);
+        p->weights_set = true;
+    });
+}
+
+cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
+    return guarded([&] {
+        require(p && h_w, "cl_conv_set_weights_host: null argument");
+        CLB_CUDA(cudaSetDevice(p->device));
+        auto s = static_cast<cudaStream_t>(stream);
+        const size_t bytes = (size_t)p->d.m * p->d.k * p->d.k * p->d.c * 4;
+        void* dw = nullptr;
+        CLB_CUDA(cudaMallocAsync(&dw, bytes, s));
+        CLB_CUDA(cudaMemcpyAsync(dw, h_w, bytes, cudaMemcpyHostToDevice, s));
+        const cl_conv_desc& d = p->d;
+        if (p->method == CL_METHOD_IM2COL)
+            launch_rows_split(static_cast<float*>(dw), p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);
+        else
+            launch_pack_weights(static_cast<float*>(dw), p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s);
+        CLB_CUDA(cudaFreeAsync(dw, s));
+        CLB_CUDA(cudaStreamSynchronize(s));
+        p->weights_set = true;
+    });
+}
+
+cl_status cl_conv_output_dims(const cl_plan* p, int32_t* P, int32_t* Q) {
+    if (!p || !P || !Q) return fail(CL_EINVAL, "cl_conv_output_dims: null argument");
+    *P = p->P;
+    *Q = p->Q;
+    return CL_OK;
+}
+
+size_t cl_conv_workspace_bytes(const cl_plan* p) { return p ? ws_bytes(p) : 0; }
+
+cl_method cl_conv_resolved_method(const cl_plan* p) { return p ? p->method : CL_METHOD_AUTO; }
+
+cl_status cl_conv_forward(cl_plan* p, const float* d_x, float* d_y, void* d_ws, void* stream) {
+    return guarded([&] {
+        require(p, "cl_conv_forward: null plan");
+        forward(p, d_x, d_y, d_ws, static_cast<cudaStream_t>(stream));
+    });
+}
+
+cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* stream) {
+    return guarded([&] {
+        require(p && h_x && h_y, "cl_conv_forward_host: null argument");
+        CLB_CUDA(cudaSetDevice(p->device));
+        const cl_conv_desc& d = p->d;
+        const size_t xb = (size_t)d.n * d.c * d.h * d.w * 4;
+        const size_t yb = (size_t)d.n * d.m * p->P * p->Q * 4;
+        if (!p->host_x) {
+            if (cudaMalloc(&p->host_x, xb) != cudaSuccess || cudaMalloc(&p->host_y, yb) != cudaSuccess) {
+                cudaGetLastError();
+                throw Error(CL_ENOMEM, "staging allocation failed");
+            }
+        }
+        auto s = static_cast<cudaStream_t>(stream);
+        CLB_CUDA(cudaMemcpyAsync(p->host_x, h_x, xb, cudaMemcpyHostToDevice, s));
+        forward(p, p->host_x, p->host_y, nullptr, s);
+        CLB_CUDA(cudaMemcpyAsync(h_y, p->host_y, yb, cudaMemcpyDeviceToHost, s));
+        CLB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int cl_conv_last_launch_count(const cl_plan* p) { return p ? p->launches : 0; }
+
+void cl_conv_destroy(cl_plan* p) {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    if (p->wpack) cudaFree(p->wpack);
+    if (p->own_ws) cudaFree(p->own_ws);
+    if (p->host_x) cudaFree(p->host_x);
+    if (p->host_y) cudaFree(p->host_y);
+    delete p;
+}
+
+size_t cl_gemm_workspace_bytes(int m, int n, int k, cl_precision precision) {
+    const int planes = precision == CL_PREC_FP32 ? 2 : 1;
+    const size_t kp = (size_t)round_up(k > 0 ? k : 1, kBlockK);
+    return ((size_t)(m > 0 ? m : 0) + (size_t)(n > 0 ? n : 0)) * planes * kp * 4;
+}
+
+cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float* c, cl_precision precision,
+                      void* ws, size_t ws_bytes_, void* stream) {
+    return guarded([&] {
+        require(m > 0 && n > 0 && k > 0, "gemm: dimensions must be positive");
+        require(a && b && c, "gemm: null operand");
+        require(precision == CL_PREC_FP32 || precision == CL_PREC_TF32, "unknown precision");
+        int dev = 0;
+        CLB_CUDA(cudaGetDevice(&dev));
+        check_device(dev);
+        auto s = static_cast<cudaStream_t>(stream);
+        const int planes = precision == CL_PREC_FP32 ? 2 : 1;
+        const int kp = round_up(k, kBlockK);
+        const size_t need = cl_gemm_workspace_bytes(m, n, k, precision);
+        void* own = nullptr;
+        if (!ws) {
+            CLB_CUDA(cudaMallocAsync(&own, need, s));
+            ws = own;
+        } else {
+            require(ws_bytes_ >= need, "gemm: workspace too small");
+        }
+        float* as = static_cast<float*>(ws);
+        float* bs = as + (size_t)m * planes * kp;
+        launch_rows_split(a, as, m, k, kp, planes, s);
+        launch_transpose_split(b, bs, k, n, kp, planes, s);
+        TcParams t{};
+        t.rows = m;
+        t.cols = n;
+        t.bn = bn_for(n);
+        t.taps = 1;
+        t.ksize = 1;
+        t.epi = EPI_ROWMAJOR;
+        t.out = c;
+        t.ld = n;
+        launch_tc(tiled(as, m, 1, kp, planes), tiled(bs, n, 1, kp, planes), t, s);
+        if (own) CLB_CUDA(cudaFreeAsync(own, s));
+    });
+}
+
+cl_status cl_shift_add_row(const float* inter, float* y, int n, int m, int h, int w, int k, int pad, void* stream) {
+    return guarded([&] {
+        require(inter && y && n > 0 && m > 0 && h > 0 && w > 0 && k > 0 && k % 2 == 1, "shift_add: bad arguments");
+        if (pad < 0) pad = k / 2;
+        const int P = h + 2 * pad - k + 1, Q = w + 2 * pad - k + 1;
+        require(P > 0 && Q > 0, "shift_add: empty output");
+        launch_shift_add_row(inter, y, n, m, h, w, k, pad, P, Q, static_cast<cudaStream_t>(stream));
+    });
+}
+
+const char* cl_last_error(void) { return g_err.c_str(); }
+
+const char* cl_method_name(cl_method m) {
+    switch (m) {
+        case CL_METHOD_AUTO: return "auto";
+        case CL_METHOD_KN2ROW: return "kn2row-gpu";
+        case CL_METHOD_KN2ROW_EXPLICIT: return "kn2row-explicit-gpu";
+        case CL_METHOD_KN2COL: return "kn2col-gpu";
+        case CL_METHOD_KN2ROW_ACC: return "kn2row-acc-gpu";
+        case CL_METHOD_IM2COL: return "im2col-gpu";
+        case CL_METHOD_CONV1X1: return "conv1x1-gpu";
+    }
+    return "unknown";
+}
+
+int cl_method_from_name(const char* name, cl_method* out) {
+    if (!name || !out) return 0;
+    for (int m = CL_METHOD_AUTO; m <= CL_METHOD_CONV1X1; ++m) {
+        if (std::strcmp(name, cl_method_name((cl_method)m)) == 0) {
+            *out = (cl_method)m;
+            return 1;
+        }
+    }
+    return 0;
+}
+
+int cl_abi_version(void) { return CL_ABI_VERSION; }
+
+int cl_device_count(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int usable = 0;
+    for (int i = 0; i < count; ++i) {
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, i) == cudaSuccess && major == 10)
+            ++usable;
+    }
+    return usable;
+}
+
+}  // extern "C"

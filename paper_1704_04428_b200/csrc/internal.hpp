@@ -1,0 +1,67 @@
+// internal.hpp -- declarations shared by the CUDA translation units (not part of the ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "tc_conv.cuh"
+
+namespace clb {
+
+// status-carrying exception used inside the library; converted to cl_status at the ABI.
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define CLB_CUDA(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t _e = (expr);                                                                    \
+        if (_e != cudaSuccess)                                                                      \
+            throw ::clb::Error(3, std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+    } while (0)
+
+inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// ---- pre-pass / post-pass kernels (prepass.cu) -------------------------------------------
+// x NCHW fp32 -> xs[n][h][w][planes][Cp] (hi = rna_tf32(x), lo = x - hi; zero for c >= C)
+void launch_nchw_to_nhwc_split(const float* x, float* xs, int N, int C, int HW, int Cp, int planes,
+                               cudaStream_t s);
+// a[rows][K] -> as[rows][planes][Kp]
+void launch_rows_split(const float* a, float* as, long long rows, int K, int Kp, int planes, cudaStream_t s);
+// b[K][cols] -> bs[cols][planes][Kp]
+void launch_transpose_split(const float* b, float* bs, int K, int cols, int Kp, int planes, cudaStream_t s);
+// w MKKC -> wp[tap][M][planes][Cp]
+void launch_pack_weights(const float* w, float* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s);
+// x NCHW -> patches[n p q][planes][Kp], K index (i*k+j)*C + c  (conv_im2.cpp:19-54 order)
+void launch_im2col_split(const float* x, float* pm, int N, int C, int H, int W, int k, int pad, int stride,
+                         int P, int Q, int Kp, int planes, cudaStream_t s);
+// inter[(t*M+m)][N*H*W] -> y NCHW (P x Q)
+void launch_shift_add_row(const float* inter, float* y, int N, int M, int H, int W, int k, int pad, int P,
+                          int Q, cudaStream_t s);
+// inter[N*H*W][k*k*M] -> y NCHW
+void launch_shift_add_col(const float* inter, float* y, int N, int M, int H, int W, int k, int pad, int P,
+                          int Q, cudaStream_t s);
+
+// ---- tcgen05 engine (tc_conv.cu) ---------------------------------------------------------
+struct Operand {
+    int mode = LOAD_TILED;   // LOAD_TILED: 3-D map (K=planes*Kp, rows, taps); LOAD_IM2COL: NHWC 4-D
+    const float* ptr = nullptr;
+    long long rows = 0;      // tiled: rows of the map
+    int taps = 1;            // tiled: 3rd dim
+    int kp = 0;              // padded channel count per plane
+    int planes = 2;
+    // im2col only
+    int n = 0, h = 0, w = 0, k = 1, pad = 0;
+};
+
+void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows);
+void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s);
+int num_sms();
+
+}  // namespace clb

@@ -1,0 +1,256 @@
+// prepass.cu -- HBM-bound layout / split kernels around the tcgen05 engine, and the
+// standalone shift-add kernels of the explicit kn2row / kn2col variants.
+//
+// All are coalesced on both sides (32x32 shared-memory transposes where the layout
+// changes) and grid-stride free: one CTA per 32x32 tile.  None of them does arithmetic
+// beyond the TF32 hi/lo split (hi = cvt.rna.tf32(x), lo = x - hi, exact in fp32).
+#include "internal.hpp"
+
+namespace clb {
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void store_split(float* dst, long long base, int c, int kp, int planes, float v) {
+    const float hi = tf32_rna(v);
+    dst[base + c] = hi;
+    if (planes == 2) dst[base + kp + c] = v - hi;
+}
+
+// ------------------------------------------------------------------ NCHW -> NHWC split ----
+// grid (ceil(HW/32), ceil(Cp/32), N), block (32, 8)
+__global__ void nchw_to_nhwc_split_kernel(const float* __restrict__ x, float* __restrict__ xs, int C, int HW,
+                                          int Cp, int planes) {
+    __shared__ float tile[32][33];
+    const int n = blockIdx.z;
+    const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const float* xn = x + (long long)n * C * HW;
+    for (int cc = threadIdx.y; cc < 32; cc += 8) {
+        const int c = c0 + cc, pix = p0 + threadIdx.x;
+        tile[cc][threadIdx.x] = (c < C && pix < HW) ? __ldg(xn + (long long)c * HW + pix) : 0.0f;
+    }
+    __syncthreads();
+    const long long row_stride = (long long)planes * Cp;
+    for (int pp = threadIdx.y; pp < 32; pp += 8) {
+        const int pix = p0 + pp, c = c0 + threadIdx.x;
+        if (pix < HW && c < Cp)
+            store_split(xs, ((long long)n * HW + pix) * row_stride, c, Cp, planes, tile[threadIdx.x][pp]);
+    }
+}
+
+void launch_nchw_to_nhwc_split(const float* x, float* xs, int N, int C, int HW, int Cp, int planes,
+                               cudaStream_t s) {
+    dim3 grid((HW + 31) / 32, (Cp + 31) / 32, N), block(32, 8);
+    nchw_to_nhwc_split_kernel<<<grid, block, 0, s>>>(x, xs, C, HW, Cp, planes);
+    CLB_CUDA(cudaGetLastError());
+}
+
+// -------------------------------------------------------------------- row-wise split ----
+// grid (ceil(Kp/128), rows), block 128
+__global__ void rows_split_kernel(const float* __restrict__ a, float* __restrict__ as, int K, int Kp,
+                                  int planes) {
+    const long long r = blockIdx.y;
+    const int c = blockIdx.x * 128 + threadIdx.x;
+    if (c >= Kp) return;
+    const float v = c < K ? __ldg(a + r * K + c) : 0.0f;
+    store_split(as, r * planes * Kp, c, Kp, planes, v);
+}
+
+void launch_rows_split(const float* a, float* as, long long rows, int K, int Kp, int planes, cudaStream_t s) {
+    if (rows <= 0) return;
+    for (long long r0 = 0; r0 < rows; r0 += 65535) {
+        const long long nr = rows - r0 < 65535 ? rows - r0 : 65535;
+        dim3 grid((Kp + 127) / 128, (unsigned)nr);
+        rows_split_kernel<<<grid, 128, 0, s>>>(a + r0 * K, as + r0 * planes * Kp, K, Kp, planes);
+    }
+    CLB_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------- transpose + split (B^T) ----
+// b[K][cols] -> bs[cols][planes][Kp]; grid (ceil(cols/32), ceil(Kp/32)), block (32, 8)
+__global__ void transpose_split_kernel(const float* __restrict__ b, float* __restrict__ bs, int K, int cols,
+                                       int Kp, int planes) {
+    __shared__ float tile[32][33];
+    const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    for (int kk = threadIdx.y; kk < 32; kk += 8) {
+        const int kx = k0 + kk, n = n0 + threadIdx.x;
+        tile[kk][threadIdx.x] = (kx < K && n < cols) ? __ldg(b + (long long)kx * cols + n) : 0.0f;
+    }
+    __syncthreads();
+    for (int nn = threadIdx.y; nn < 32; nn += 8) {
+        const int n = n0 + nn, kx = k0 + threadIdx.x;
+        if (n < cols && kx < Kp) store_split(bs, (long long)n * planes * Kp, kx, Kp, planes, tile[threadIdx.x][nn]);
+    }
+}
+
+void launch_transpose_split(const float* b, float* bs, int K, int cols, int Kp, int planes, cudaStream_t s) {
+    dim3 grid((cols + 31) / 32, (Kp + 31) / 32), block(32, 8);
+    transpose_split_kernel<<<grid, block, 0, s>>>(b, bs, K, cols, Kp, planes);
+    CLB_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ weight pre-pack ----
+// kn2row_reorder_kernel (conv_kn2.cpp:28-39) fused with the split:
+//   wp[(i*k+j)][m][plane][c] = split(K[m][i][j][c])
+__global__ void pack_weights_kernel(const float* __restrict__ w, float* __restrict__ wp, int M, int k, int C,
+                                    int Cp, int planes) {
+    const long long total = (long long)k * k * M * Cp;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(e % Cp);
+        const long long tm = e / Cp;
+        const int m = (int)(tm % M);
+        const int t = (int)(tm / M);
+        const float v = c < C ? w[((long long)m * k * k + t) * C + c] : 0.0f;
+        store_split(wp, tm * planes * Cp, c, Cp, planes, v);
+    }
+}
+
+void launch_pack_weights(const float* w, float* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s) {
+    const long long total = (long long)k * k * M * Cp;
+    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    pack_weights_kernel<<<blocks, 256, 0, s>>>(w, wp, M, k, C, Cp, planes);
+    CLB_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------------- im2col ----
+// Patch matrix in the K-major orientation the engine consumes (the im2row shape of
+// conv_im2.cpp:56-85 with im2col's K order (i*k+j)*C+c of conv_im2.cpp:19-54):
+//   pm[pix = (n,p,q)][plane][kk = (i*k+j)*C + c] = x[n][c][p*s-pad+i][q*s-pad+j]  (0 if OOB)
+// grid (ceil(NPQ/32), ceil(Kp/32)), block (32, 8): gather coalesced along pixels, write along K.
+__global__ void im2col_split_kernel(const float* __restrict__ x, float* __restrict__ pm, int C, int H, int W,
+                                    int k, int pad, int stride, int P, int Q, long long npq, int Kp, int planes) {
+    __shared__ float tile[32][33];
+    const long long pix0 = (long long)blockIdx.x * 32;
+    const int k0 = blockIdx.y * 32;
+    const int KC = k * k * C;
+    // this thread's pixel for the gather phase
+    const long long pix = pix0 + threadIdx.x;
+    int n = 0, p = 0, q = 0;
+    if (pix < npq) {
+        n = (int)(pix / ((long long)P * Q));
+        const int rem = (int)(pix - (long long)n * P * Q);
+        p = rem / Q;
+        q = rem - p * Q;
+    }
+    for (int kk = threadIdx.y; kk < 32; kk += 8) {
+        const int kx = k0 + kk;
+        float v = 0.0f;
+        if (pix < npq && kx < KC) {
+            const int c = kx % C, t = kx / C;
+            const int i = t / k, j = t - (t / k) * k;
+            const int sh = p * stride - pad + i, sw = q * stride - pad + j;
+            if (sh >= 0 && sh < H && sw >= 0 && sw < W)
+                v = __ldg(x + (((long long)n * C + c) * H + sh) * W + sw);
+        }
+        tile[kk][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int pp = threadIdx.y; pp < 32; pp += 8) {
+        const long long pr = pix0 + pp;
+        const int kx = k0 + threadIdx.x;
+        if (pr < npq && kx < Kp) store_split(pm, pr * planes * Kp, kx, Kp, planes, tile[threadIdx.x][pp]);
+    }
+}
+
+void launch_im2col_split(const float* x, float* pm, int N, int C, int H, int W, int k, int pad, int stride,
+                         int P, int Q, int Kp, int planes, cudaStream_t s) {
+    const long long npq = (long long)N * P * Q;
+    dim3 grid((unsigned)((npq + 31) / 32), (Kp + 31) / 32), block(32, 8);
+    im2col_split_kernel<<<grid, block, 0, s>>>(x, pm, C, H, W, k, pad, stride, P, Q, npq, Kp, planes);
+    CLB_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------- shift-add ----
+// Row orientation (conv_kn2.cpp:94-118), batched: inter[(t*M+m)][n*H*W + h*W + w].
+// out[n][m][p][q] = sum_{i<k} sum_{j<k} inter[(i*k+j)*M+m][n, p-pad+i, q-pad+j], OOB skipped,
+// i outer / j inner (the reference's accumulation order).  One thread per output element,
+// q fastest -> coalesced loads of each tap row and coalesced stores.
+__global__ void shift_add_row_kernel(const float* __restrict__ inter, float* __restrict__ y, int N, int M,
+                                     int H, int W, int k, int pad, int P, int Q) {
+    const long long total = (long long)N * M * P * Q;
+    const long long ld = (long long)N * H * W;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int q = (int)(e % Q);
+        long long r = e / Q;
+        const int p = (int)(r % P);
+        r /= P;
+        const int m = (int)(r % M);
+        const int n = (int)(r / M);
+        float acc = 0.0f;
+        for (int i = 0; i < k; ++i) {
+            const int sh = p - pad + i;
+            if (sh < 0 || sh >= H) continue;
+            for (int j = 0; j < k; ++j) {
+                const int sw = q - pad + j;
+                if (sw < 0 || sw >= W) continue;
+                acc += __ldg(inter + ((long long)(i * k + j) * M + m) * ld + ((long long)n * H + sh) * W + sw);
+            }
+        }
+        y[e] = acc;
+    }
+}
+
+void launch_shift_add_row(const float* inter, float* y, int N, int M, int H, int W, int k, int pad, int P,
+                          int Q, cudaStream_t s) {
+    const long long total = (long long)N * M * P * Q;
+    const int blocks = (int)((total + 255) / 256 < 148 * 64 ? (total + 255) / 256 : 148 * 64);
+    shift_add_row_kernel<<<blocks, 256, 0, s>>>(inter, y, N, M, H, W, k, pad, P, Q);
+    CLB_CUDA(cudaGetLastError());
+}
+
+// Column orientation (conv_kn2.cpp:120-142), batched: inter[n*H*W + h*W + w][t*M + m].
+// A 32-pixel x 32-channel output tile: gather coalesced along m, transpose through shared
+// memory, store coalesced along pixels into NCHW.  grid (ceil(NPQ/32), ceil(M/32)), block (32,8)
+__global__ void shift_add_col_kernel(const float* __restrict__ inter, float* __restrict__ y, int N, int M,
+                                     int H, int W, int k, int pad, int P, int Q) {
+    __shared__ float tile[32][33];
+    const long long npq = (long long)N * P * Q;
+    const long long pix0 = (long long)blockIdx.x * 32;
+    const int m0 = blockIdx.y * 32;
+    const long long ld = (long long)k * k * M;
+    const int m = m0 + threadIdx.x;
+    for (int pp = threadIdx.y; pp < 32; pp += 8) {
+        const long long pix = pix0 + pp;
+        float acc = 0.0f;
+        if (pix < npq && m < M) {
+            const int n = (int)(pix / ((long long)P * Q));
+            const int rem = (int)(pix - (long long)n * P * Q);
+            const int p = rem / Q, q = rem - (rem / Q) * Q;
+            for (int i = 0; i < k; ++i) {
+                const int sh = p - pad + i;
+                if (sh < 0 || sh >= H) continue;
+                for (int j = 0; j < k; ++j) {
+                    const int sw = q - pad + j;
+                    if (sw < 0 || sw >= W) continue;
+                    acc += __ldg(inter + (((long long)n * H + sh) * W + sw) * ld + (long long)(i * k + j) * M + m);
+                }
+            }
+        }
+        tile[pp][threadIdx.x] = acc;
+    }
+    __syncthreads();
+    for (int mm = threadIdx.y; mm < 32; mm += 8) {
+        const long long pix = pix0 + threadIdx.x;
+        const int mo = m0 + mm;
+        if (pix < npq && mo < M) {
+            const int n = (int)(pix / ((long long)P * Q));
+            const int rem = (int)(pix - (long long)n * P * Q);
+            y[((long long)n * M + mo) * P * Q + rem] = tile[threadIdx.x][mm];
+        }
+    }
+}
+
+void launch_shift_add_col(const float* inter, float* y, int N, int M, int H, int W, int k, int pad, int P,
+                          int Q, cudaStream_t s) {
+    const long long npq = (long long)N * P * Q;
+    dim3 grid((unsigned)((npq + 31) / 32), (M + 31) / 32), block(32, 8);
+    shift_add_col_kernel<<<grid, block, 0, s>>>(inter, y, N, M, H, W, k, pad, P, Q);
+    CLB_CUDA(cudaGetLastError());
+}
+
+}  // namespace clb

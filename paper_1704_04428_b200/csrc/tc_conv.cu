@@ -1,0 +1,107 @@
+// tc_conv.cu -- host side of the tcgen05 engine: TMA tensor-map encoding (tiled and
+// im2col) and the persistent launch.  The kernel itself lives in tc_conv.cuh.
+#include <mutex>
+
+#define CLB_DEFINE_TC_KERNEL 1
+#include "internal.hpp"
+
+namespace clb {
+
+namespace {
+
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+using PFN_encodeIm2col = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled g_tiled = nullptr;
+PFN_encodeIm2col g_im2col = nullptr;
+std::once_flag g_once;
+
+void resolve_driver() {
+    std::call_once(g_once, [] {
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_tiled = reinterpret_cast<PFN_encodeTiled>(fn);
+        fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_im2col = reinterpret_cast<PFN_encodeIm2col>(fn);
+    });
+    if (!g_tiled || !g_im2col) throw Error(3, "cuTensorMapEncode* entry points unavailable (driver too old?)");
+}
+
+}  // namespace
+
+int num_sms() {
+    int dev = 0, n = 0;
+    CLB_CUDA(cudaGetDevice(&dev));
+    CLB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+}
+
+void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows) {
+    resolve_driver();
+    const cuuint64_t kdim = (cuuint64_t)op.planes * op.kp;   // channels per row incl. hi|lo planes
+    CUresult r;
+    if (op.mode == LOAD_IM2COL) {
+        cuuint64_t dims[4] = {kdim, (cuuint64_t)op.w, (cuuint64_t)op.h, (cuuint64_t)op.n};
+        cuuint64_t strides[3] = {kdim * 4, kdim * 4 * op.w, kdim * 4 * op.w * op.h};
+        // Bounding box: lower corner -pad, upper corner pad-(k-1) in W and H, so the
+        // traversal enumerates exactly the P x Q output positions of each image.
+        int lower[2] = {-op.pad, -op.pad};
+        int upper[2] = {op.pad - (op.k - 1), op.pad - (op.k - 1)};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        r = g_im2col(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(op.ptr), dims, strides, lower,
+                     upper, (cuuint32_t)kBlockK, (cuuint32_t)box_rows, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[3] = {kdim, (cuuint64_t)op.rows, (cuuint64_t)op.taps};
+        cuuint64_t strides[2] = {kdim * 4, kdim * 4 * (cuuint64_t)op.rows};
+        cuuint32_t box[3] = {(cuuint32_t)kBlockK, (cuuint32_t)box_rows, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = g_tiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(op.ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS)
+        throw Error(3, "cuTensorMapEncode" + std::string(op.mode == LOAD_IM2COL ? "Im2col" : "Tiled") +
+                           " failed with CUresult " + std::to_string((int)r));
+}
+
+void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s) {
+    if (p.bn % 16 != 0 || p.bn < 16 || p.bn > 256) throw Error(6, "tile N must be a multiple of 16 in [16,256]");
+    if (a.kp != b.kp || a.kp % kBlockK != 0) throw Error(6, "operand K padding mismatch");
+    CUtensorMap ma, mb;
+    encode_operand_map(&ma, a, kTileM);
+    encode_operand_map(&mb, b, p.bn);
+    p.planes = a.planes;
+    p.kblocks = a.kp / kBlockK;
+    p.a_lo = a.kp;
+    p.b_lo = b.kp;
+    p.a_mode = a.mode;
+    p.b_mode = b.mode;
+    p.stages = tc_num_stages(p.bn, p.planes);
+    const int row_tiles = (p.rows + kTileM - 1) / kTileM;
+    p.n_col_tiles = (p.cols + p.bn - 1) / p.bn;
+    p.num_tiles = row_tiles * p.n_col_tiles;
+    if (p.num_tiles <= 0) return;
+    const int smem = tc_smem_bytes(p.bn, p.planes, p.stages);
+    static int configured = 0;
+    if (smem > configured) {
+        CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        configured = 227 * 1024;
+    }
+    const int sms = num_sms();
+    const int grid = p.num_tiles < sms ? p.num_tiles : sms;
+    tc_conv_kernel<<<grid, kThreads, smem, s>>>(ma, mb, p);
+    CLB_CUDA(cudaGetLastError());
+}
+
+}  // namespace clb

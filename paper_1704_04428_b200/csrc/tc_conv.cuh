@@ -1,0 +1,288 @@
+// tc_conv.cuh -- the one tcgen05 contraction engine behind every GPU method.
+//
+//   D[rows x cols] = sum_{tap, cblock}  A_tap[rows x 16ch] . B_tap[cols x 16ch]^T
+//
+// A supplies the 128 D rows of an MMA tile (UMMA M = 128), B the BN columns (UMMA N = BN,
+// a runtime multiple of 16 <= 256).  Both operands are K-major fp32 words holding TF32
+// values, split hi/lo for the fp32-faithful 3xTF32 mode (D += Alo.Bhi + Ahi.Blo + Ahi.Bhi).
+// Each operand is fetched by TMA either as a plain 3-D tile (k, row, tap) or -- the
+// implicit kn2row path -- as a 4-D im2col box over the NHWC input whose per-tap offsets
+// (j, i) shift the 128 output pixels onto their input taps; taps falling outside the image
+// are zero-filled by the TMA unit, which is exactly the reference's "OOB reads discarded"
+// shift-add law (conv_kn2.hpp:50-56, conv_kn2.cpp:94-118).  All k^2 taps accumulate into the
+// same TMEM accumulator, so no k^2-fold intermediate and no patch matrix ever reach HBM.
+//
+// Warp roles (256 threads, persistent, one CTA per SM):
+//   warp 0      : TMA producer (one elected lane)
+//   warp 1      : MMA issuer   (one lane issues tcgen05.mma + tcgen05.commit)
+//   warp 2      : TMEM allocator
+//   warps 4..7  : epilogue (TMEM -> registers -> global), lane quadrant = warp % 4
+// Pipelines: smem stages full/empty (TMA <-> MMA), TMEM accumulators x2 full/empty
+// (MMA <-> epilogue) so tile t's epilogue overlaps tile t+1's main loop.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+
+#include "ptx.cuh"
+
+namespace clb {
+
+enum : int { LOAD_TILED = 0, LOAD_IM2COL = 1 };
+enum : int { EPI_NCHW = 0, EPI_ROWMAJOR = 1 };
+
+constexpr int kTileM = 128;          // UMMA M (D rows per tile)
+constexpr int kBlockK = 16;          // fp32 channels per stage (64 B rows, SWIZZLE_64B)
+constexpr int kRowBytes = kBlockK * 4;
+constexpr int kThreads = 256;
+constexpr int kSmemBudget = 200 * 1024;
+
+struct TcParams {
+    // problem
+    int rows, cols;            // valid D rows / cols
+    int bn;                    // tile N (multiple of 16, <= 256)
+    int n_col_tiles, num_tiles;
+    int taps, tap_begin, ksize;  // K loop: taps [tap_begin, tap_begin+taps), tap t -> (t/ksize, t%ksize)
+    int kblocks;               // 16-channel blocks per tap
+    int planes;                // 2 = 3xTF32 (hi,lo), 1 = TF32 (hi)
+    int stages;
+    int a_mode, b_mode;        // LOAD_TILED / LOAD_IM2COL
+    int a_lo, b_lo;            // K-coordinate offset of the lo plane in each tensor map
+    int a_tap3, b_tap3;        // tiled: pass the tap as 3rd coordinate (weights [tap][M][K])
+    // im2col geometry of the row operand (output pixels)
+    int P, Q, pad;
+    // epilogue
+    int epi;                   // EPI_NCHW (rows = pixels n*P*Q, cols = channels) / EPI_ROWMAJOR
+    int accumulate;            // out += D (accumulating shifted-GEMM variant)
+    float* out;
+    long long ld;              // EPI_ROWMAJOR leading dimension
+    int out_channels;          // EPI_NCHW: channel count of the output tensor
+    int pq_out;                // EPI_NCHW: P*Q
+    unsigned long long* debug; // optional
+};
+
+__host__ __device__ inline int tc_stage_bytes(int bn, int planes) { return planes * (kTileM + bn) * kRowBytes; }
+
+__host__ inline int tc_num_stages(int bn, int planes) {
+    int s = (kSmemBudget - 1024) / tc_stage_bytes(bn, planes);
+    return s > 8 ? 8 : s;
+}
+
+__host__ inline int tc_smem_bytes(int bn, int planes, int stages) {
+    return 1024 /*align slack*/ + stages * tc_stage_bytes(bn, planes) + 256 /*barriers*/;
+}
+
+__host__ __device__ inline uint32_t tmem_cols_for(int bn) {
+    uint32_t need = 2u * (uint32_t)bn, c = 32;
+    while (c < need) c <<= 1;
+    return c;
+}
+
+#ifdef CLB_DEFINE_TC_KERNEL
+__device__ __forceinline__ void load_operand(const CUtensorMap* map, int mode, uint64_t* bar, uint8_t* dst,
+                                             int kcoord, int row0, int tap, int tap3, int ksize, int P, int Q,
+                                             int pad) {
+    if (mode == LOAD_IM2COL) {
+        // row0 = first output pixel (linear over n, p, q)
+        const int PQ = P * Q;
+        const int n = row0 / PQ;
+        const int rem = row0 - n * PQ;
+        const int p = rem / Q;
+        const int q = rem - p * Q;
+        const int i = tap / ksize, j = tap - (tap / ksize) * ksize;
+        tma_load_im2col_4d(map, bar, dst, kcoord, q - pad, p - pad, n, (uint16_t)j, (uint16_t)i);
+    } else {
+        tma_load_3d(map, bar, dst, kcoord, row0, tap3 ? tap : 0);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               const TcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+    const int bn = p.bn;
+    const int planes = p.planes;
+    const int stages = p.stages;
+    const int a_bytes = kTileM * kRowBytes;       // one plane of A per stage
+    const int b_bytes = bn * kRowBytes;           // one plane of B per stage
+    const int stage_bytes = planes * (a_bytes + b_bytes);
+
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + stages;
+    uint64_t* tfull = bars + 2 * stages;
+    uint64_t* tempty = bars + 2 * stages + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 4);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t ncols = tmem_cols_for(bn);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane_id() == 0) {
+        tma_prefetch_desc(&map_a);
+        tma_prefetch_desc(&map_b);
+    }
+    if (warp == 2) {
+        tmem_alloc(tmem_slot, ncols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int k_iters = p.taps * p.kblocks;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer ----
+        if (lane_id() == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t tx = (uint32_t)stage_bytes;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                const int mt = tile / p.n_col_tiles;
+                const int nt = tile - mt * p.n_col_tiles;
+                const int row0 = mt * kTileM;
+                const int col0 = nt * bn;
+                for (int it = 0; it < k_iters; ++it) {
+                    const int tap = p.tap_begin + it / p.kblocks;
+                    const int kc = (it % p.kblocks) * kBlockK;
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    mbar_arrive_expect_tx(&full[stage], tx);
+                    uint8_t* st = smem + stage * stage_bytes;
+                    uint8_t* a_hi = st;
+                    uint8_t* a_lo = st + a_bytes;
+                    uint8_t* b_hi = st + planes * a_bytes;
+                    uint8_t* b_lo = b_hi + b_bytes;
+                    load_operand(&map_a, p.a_mode, &full[stage], a_hi, kc, row0, tap, p.a_tap3, p.ksize, p.P, p.Q,
+                                 p.pad);
+                    load_operand(&map_b, p.b_mode, &full[stage], b_hi, kc, col0, tap, p.b_tap3, p.ksize, p.P, p.Q,
+                                 p.pad);
+                    if (planes == 2) {
+                        load_operand(&map_a, p.a_mode, &full[stage], a_lo, kc + p.a_lo, row0, tap, p.a_tap3, p.ksize,
+                                     p.P, p.Q, p.pad);
+                        load_operand(&map_b, p.b_mode, &full[stage], b_lo, kc + p.b_lo, col0, tap, p.b_tap3, p.ksize,
+                                     p.P, p.Q, p.pad);
+                    }
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------- MMA issuer ----
+        if (lane_id() == 0) {
+            const uint32_t idesc = idesc_tf32(kTileM, (uint32_t)bn);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+                const int acc = local & 1;
+                const uint32_t acc_phase = (uint32_t)(local >> 1) & 1u;
+                mbar_wait(&tempty[acc], acc_phase ^ 1u);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)acc * (ncols / 2);
+                for (int it = 0; it < k_iters; ++it) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + stage * stage_bytes);
+                    const uint32_t a_hi = st, a_lo = st + a_bytes;
+                    const uint32_t b_hi = st + planes * a_bytes, b_lo = b_hi + b_bytes;
+#pragma unroll
+                    for (int ks = 0; ks < kBlockK / 8; ++ks) {
+                        const uint32_t off = ks * 32;   // 8 tf32 = 32 B along K
+                        const uint64_t dah = umma_desc_kmajor(a_hi + off, kRowBytes);
+                        const uint64_t dbh = umma_desc_kmajor(b_hi + off, kRowBytes);
+                        uint32_t accum = (it > 0 || ks > 0) ? 1u : 0u;
+                        if (planes == 2) {
+                            const uint64_t dal = umma_desc_kmajor(a_lo + off, kRowBytes);
+                            const uint64_t dbl = umma_desc_kmajor(b_lo + off, kRowBytes);
+                            mma_tf32_ss(d_tmem, dal, dbh, idesc, accum);   // small cross terms first
+                            mma_tf32_ss(d_tmem, dah, dbl, idesc, 1u);
+                            accum = 1u;
+                        }
+                        mma_tf32_ss(d_tmem, dah, dbh, idesc, accum);
+                    }
+                    mma_commit(&empty[stage]);      // frees the smem stage once these MMAs retire
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                mma_commit(&tfull[acc]);            // accumulator complete -> epilogue
+            }
+        }
+    } else if (warp >= 4) {
+        // --------------------------------------------------------------- epilogue ----
+        const int quad = warp & 3;
+        const int lane = (int)lane_id();
+        int local = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+            const int acc = local & 1;
+            const uint32_t acc_phase = (uint32_t)(local >> 1) & 1u;
+            const int mt = tile / p.n_col_tiles;
+            const int nt = tile - mt * p.n_col_tiles;
+            const int row = mt * kTileM + quad * 32 + lane;
+            const int col0 = nt * bn;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t t_addr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)acc * (ncols / 2);
+            const bool row_ok = row < p.rows;
+            float* dst = nullptr;
+            long long cstride = 1;
+            if (p.epi == EPI_NCHW) {
+                const int n = row / p.pq_out;
+                const int pq = row - n * p.pq_out;
+                dst = p.out + ((long long)n * p.out_channels) * p.pq_out + pq;
+                cstride = p.pq_out;
+            } else {
+                dst = p.out + (long long)row * p.ld;
+                cstride = 1;
+            }
+            for (int c = 0; c < bn; c += 16) {
+                uint32_t r[16];
+                tmem_ld_32x32b_x16(t_addr + (uint32_t)c, r);
+                tmem_ld_wait();
+                if (row_ok) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int col = col0 + c + j;
+                        if (col < p.cols) {
+                            float* o = dst + (long long)col * cstride;
+                            const float v = __uint_as_float(r[j]);
+                            if (p.accumulate) *o += v;
+                            else *o = v;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, ncols);
+    }
+}
+
+#endif  // CLB_DEFINE_TC_KERNEL
+
+}  // namespace clb
