@@ -125,6 +125,16 @@ CL_API size_t cl_gemm_workspace_bytes(int m, int n, int k, cl_precision precisio
 CL_API cl_status cl_shift_add_row(const float* d_inter, float* d_y, int n, int m, int h, int w, int k, int pad,
                            void* stream);
 
+/* Fills d[0..n) with the reference's counter-based generator on the device, bit-identical to
+ * fill_deterministic (tensor.cpp:104-134): d[i] = unit_value(seed, first_index + i) in [-1,1).
+ * Replaces random_tensor3 / random_kernels for device-resident synthetic inputs. */
+CL_API cl_status cl_fill_uniform(float* d, uint64_t n, uint64_t seed, uint64_t first_index, void* stream);
+
+/* Instrumentation: when set, cl_conv_forward records ev_begin (a cudaEvent_t) on the stream
+ * right before its first tcgen05 contraction launch and ev_end right after its last, so the
+ * caller can time the dominant kernel alone with CUDA events.  NULLs disable. */
+CL_API cl_status cl_conv_set_profile_events(cl_plan* plan, void* ev_begin, void* ev_end);
+
 CL_API const char* cl_last_error(void);
 CL_API const char* cl_method_name(cl_method method);
 CL_API int cl_method_from_name(const char* name, cl_method* out);

@@ -64,6 +64,7 @@ struct cl_plan {
     float* host_x = nullptr;   // device staging for cl_conv_forward_host
     float* host_y = nullptr;
     int launches = 0;
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // optional instrumentation
 };
 
 namespace {
@@ -169,6 +170,16 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
     const long long npq = (long long)d.n * p->P * p->Q;
     float* wsf = static_cast<float*>(ws);
     p->launches = 0;
+    bool began = false;
+    auto tc = [&](const Operand& a, const Operand& b, const TcParams& t) {
+        if (p->ev_begin && !began) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
+        began = true;
+        launch_tc(a, b, t, s);
+        ++p->launches;
+    };
+    auto tc_done = [&] {
+        if (p->ev_end) CLB_CUDA(cudaEventRecord(p->ev_end, s));
+    };
 
     switch (p->method) {
         case CL_METHOD_KN2ROW:
@@ -194,15 +205,14 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
                     t.taps = 1;
                     t.tap_begin = tap;
                     t.accumulate = tap > 0;
-                    launch_tc(a, b, t, s);
-                    ++p->launches;
+                    tc(a, b, t);
                 }
             } else {
                 t.taps = taps;
                 t.tap_begin = 0;
-                launch_tc(a, b, t, s);
-                ++p->launches;
+                tc(a, b, t);
             }
+            tc_done();
             break;
         }
         case CL_METHOD_KN2ROW_EXPLICIT:
@@ -223,8 +233,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
                 t.cols = (int)nhw;
                 t.ld = nhw;
                 t.bn = 256;
-                launch_tc(wts, pix, t, s);
-                ++p->launches;
+                tc(wts, pix, t);
+                tc_done();
                 launch_shift_add_row(inter, y, d.n, d.m, d.h, d.w, d.k, d.pad, p->P, p->Q, s);
             } else {
                 // (NHW x C) . (C x k^2 M): the kn2col GEMM (conv_kn2.cpp:164-183)
@@ -232,8 +242,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
                 t.cols = taps * d.m;
                 t.ld = (long long)taps * d.m;
                 t.bn = bn_for(taps * d.m);
-                launch_tc(pix, wts, t, s);
-                ++p->launches;
+                tc(pix, wts, t);
+                tc_done();
                 launch_shift_add_col(inter, y, d.n, d.m, d.h, d.w, d.k, d.pad, p->P, p->Q, s);
             }
             ++p->launches;
@@ -254,8 +264,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
             t.out = y;
             t.out_channels = d.m;
             t.pq_out = p->P * p->Q;
-            launch_tc(a, b, t, s);
-            ++p->launches;
+            tc(a, b, t);
+            tc_done();
             break;
         }
         default:
@@ -460,6 +470,20 @@ cl_status cl_shift_add_row(const float* inter, float* y, int n, int m, int h, in
         require(P > 0 && Q > 0, "shift_add: empty output");
         launch_shift_add_row(inter, y, n, m, h, w, k, pad, P, Q, static_cast<cudaStream_t>(stream));
     });
+}
+
+cl_status cl_fill_uniform(float* d, uint64_t n, uint64_t seed, uint64_t first_index, void* stream) {
+    return guarded([&] {
+        require(d || n == 0, "cl_fill_uniform: null pointer");
+        launch_fill_uniform(d, n, seed, first_index, static_cast<cudaStream_t>(stream));
+    });
+}
+
+cl_status cl_conv_set_profile_events(cl_plan* p, void* ev_begin, void* ev_end) {
+    if (!p) return fail(CL_EINVAL, "cl_conv_set_profile_events: null plan");
+    p->ev_begin = static_cast<cudaEvent_t>(ev_begin);
+    p->ev_end = static_cast<cudaEvent_t>(ev_end);
+    return CL_OK;
 }
 
 const char* cl_last_error(void) { return g_err.c_str(); }

@@ -48,6 +48,9 @@ void launch_shift_add_row(const float* inter, float* y, int N, int M, int H, int
 void launch_shift_add_col(const float* inter, float* y, int N, int M, int H, int W, int k, int pad, int P,
                           int Q, cudaStream_t s);
 
+void launch_fill_uniform(float* d, unsigned long long n, unsigned long long seed,
+                         unsigned long long first, cudaStream_t s);
+
 // ---- tcgen05 engine (tc_conv.cu) ---------------------------------------------------------
 struct Operand {
     int mode = LOAD_TILED;   // LOAD_TILED: 3-D map (K=planes*Kp, rows, taps); LOAD_IM2COL: NHWC 4-D

@@ -253,4 +253,29 @@ void launch_shift_add_col(const float* inter, float* y, int N, int M, int H, int
     CLB_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------------- generator ----
+// rng::unit_value (tensor.cpp:117-123): top 24 bits of splitmix64(seed + (i+1) gamma),
+// scaled by 2^-23 and shifted -- exact in fp32, so bit-identical to the host generator.
+__global__ void fill_uniform_kernel(float* __restrict__ d, unsigned long long n, unsigned long long seed,
+                                    unsigned long long first) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        unsigned long long z = seed + (first + i + 1ull) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const unsigned top = (unsigned)(z >> 40);
+        d[i] = __fsub_rn(__fmul_rn((float)top, 0x1p-23f), 1.0f);
+    }
+}
+
+void launch_fill_uniform(float* d, unsigned long long n, unsigned long long seed, unsigned long long first,
+                         cudaStream_t s) {
+    if (n == 0) return;
+    const unsigned long long want = (n + 255) / 256;
+    const int blocks = (int)(want < 148ull * 32 ? want : 148ull * 32);
+    fill_uniform_kernel<<<blocks, 256, 0, s>>>(d, n, seed, first);
+    CLB_CUDA(cudaGetLastError());
+}
+
 }  // namespace clb

@@ -1,0 +1,65 @@
+// ref_plugin_test.cpp -- TEST: the drop-in at the reference's own plugin point.
+//
+// Registers the B200 GEMM as an external backend of the UNMODIFIED reference library
+// (register_gemm_backend, gemm.hpp:52-58; compiled into oracle/_ref) and runs the
+// reference's own conv_kn2row / conv_im2col / conv_kn2col (conv_kn2.cpp:145-183,
+// conv_im2.cpp:108-132) with it, against the reference oracle conv_mcmk_sum.  The adapter
+// below is exactly the binding shown in INTEGRATION.md.
+#include <cstdio>
+#include <stdexcept>
+#include <cuda_runtime.h>
+
+#include "convlab/conv_direct.hpp"
+#include "convlab/conv_im2.hpp"
+#include "convlab/conv_kn2.hpp"
+#include "convlab/gemm.hpp"
+#include "convlab/methods.hpp"
+#include "convlab_b200.h"
+
+namespace {
+
+convlab::Matrix b200_gemm(convlab::MatrixView a, convlab::MatrixView b) {
+    const std::size_t m = a.rows, k = a.cols, n = b.cols;
+    float *da = nullptr, *db = nullptr, *dc = nullptr;
+    if (cudaMalloc(&da, m * k * 4) || cudaMalloc(&db, k * n * 4) || cudaMalloc(&dc, m * n * 4))
+        throw std::runtime_error("b200 gemm: device allocation failed");
+    cudaMemcpy(da, a.data, m * k * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(db, b.data, k * n * 4, cudaMemcpyHostToDevice);
+    const cl_status s = cl_gemm_f32((int)m, (int)n, (int)k, da, db, dc, CL_PREC_FP32, nullptr, 0, nullptr);
+    convlab::Matrix c(m, n);
+    if (s == CL_OK) cudaMemcpy(c.data().data(), dc, m * n * 4, cudaMemcpyDeviceToHost);
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dc);
+    if (s != CL_OK) throw std::runtime_error(cl_last_error());
+    return c;
+}
+
+}  // namespace
+
+int main() {
+    convlab::register_gemm_backend("b200", b200_gemm);
+    auto backend = convlab::make_backend("b200");
+    if (!backend) return 2;
+    int fails = 0;
+    const struct { std::size_t c, h, w, m, k; } shapes[] = {{3, 6, 5, 4, 3}, {16, 13, 13, 8, 3}, {64, 28, 28, 32, 3},
+                                                            {8, 9, 9, 16, 5}, {32, 7, 7, 64, 1}};
+    for (const auto& s : shapes) {
+        convlab::ConvProblem p(convlab::random_tensor3(s.c, s.h, s.w, convlab::Layout::CHW, convlab::rng::split(5, 0)),
+                               convlab::random_kernels(s.m, s.k, s.c, convlab::KernelLayout::MKKC,
+                                                       convlab::rng::split(5, 1)));
+        const convlab::Tensor3 oracle = convlab::conv_mcmk_sum(p);
+        const auto tol = convlab::scaled_tolerance({1e-5f, 1e-6f}, convlab::max_abs(oracle));
+        for (auto m : {convlab::ConvMethod::Kn2row, convlab::ConvMethod::Kn2col, convlab::ConvMethod::Im2col,
+                       convlab::ConvMethod::Im2row}) {
+            const convlab::Tensor3 out = convlab::run_method(m, p, *backend);
+            const bool ok = convlab::allclose(out, oracle, tol);
+            std::printf("  ref %-8s via b200 GEMM  C=%zu %zux%zu M=%zu k=%zu  max|err|=%.3e  %s\n",
+                        std::string(convlab::to_string(m)).c_str(), s.c, s.h, s.w, s.m, s.k,
+                        convlab::max_abs_diff(out, oracle), ok ? "ok" : "FAIL");
+            fails += !ok;
+        }
+    }
+    std::printf(fails ? "FAILED (%d)\n" : "PASSED\n", fails);
+    return fails ? 1 : 0;
+}

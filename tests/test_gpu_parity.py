@@ -1,0 +1,272 @@
+"""GPU parity: every CUDA method through the C ABI against the CPU oracle (oracle/oracle.c,
+pinned bitwise to the reference in tests/test_oracle.py).
+
+Tolerances (BASELINE.md 3 / north star):
+  fp32-faithful (3xTF32): rel-L2 <= 1e-5 and max|d|/max|ref| <= 1e-4
+  tf32 fast mode        : rel-L2 <= 1e-2
+plus the reference's own allclose verdict (rel 1e-5, abs 1e-6 + 1e-5 max|oracle|) reported.
+Cases follow the reference's tests: the method x shape grid (conv_kn2_test.cpp:242-263),
+border-dominated shapes (acceptance_main.cpp:182-199), delta kernels, per-tap
+decomposition, k=1 routing, one-contraction-per-call, determinism, and a negative control.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FP32_L2, FP32_MAX, TF32_L2 = 1e-5, 1e-4, 1e-2
+METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu"]
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def clb(torch_cuda):
+    import paper_1704_04428_b200 as clb
+    assert clb.lib.cl_device_count() >= 1
+    return clb
+
+
+def _run(clb, torch, method, x, w, precision="fp32", pad=None):
+    y = clb.run_method(method, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), precision, pad=pad)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def _check_fp32(oracle, y, ref, what=""):
+    m = oracle.parity_metrics(y, ref)
+    assert m["finite"], what
+    assert m["rel_l2"] <= FP32_L2 and m["max_rel"] <= FP32_MAX, (what, m)
+    return m
+
+
+GRID = [(k, c, m, hw) for k in (1, 3, 5) for c in (1, 3, 16) for m in (1, 4) for hw in (1, 4, 13)
+        if k <= hw + k // 2]
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_method_shape_grid(oracle, clb, torch_cuda, method):
+    """conv_kn2_test.cpp:242-263 grid, all GPU methods, batch 2."""
+    for k, c, m, hw in GRID:
+        s = k * 31 + c * 7 + m * 3 + hw
+        x, w = oracle.make_problem(2, c, hw, hw, m, k, s)
+        ref = oracle.conv_batch(x, w)
+        y = _run(clb, torch_cuda, method, x, w)
+        _check_fp32(oracle, y, ref, f"{method} k={k} C={c} M={m} HW={hw}")
+
+
+BORDER = [(2, 2, 3), (2, 6, 3), (6, 2, 3), (3, 3, 5), (3, 8, 5), (4, 4, 7), (1, 2, 1), (1, 3, 3), (1, 1, 1)]
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_border_dominated_shapes(oracle, clb, torch_cuda, method):
+    """acceptance_main.cpp:182-199 / conv_kn2_test.cpp:221-231: every pixel touches padding."""
+    for h, w_, k in BORDER:
+        if k > min(h, w_) + k // 2:
+            continue
+        x, w = oracle.make_problem(3, 5, h, w_, 6, k, h * 10 + w_)
+        _check_fp32(oracle, _run(clb, torch_cuda, method, x, w), oracle.conv_batch(x, w), f"{method} {h}x{w_} k{k}")
+
+
+def test_golden_fixtures(oracle, clb, torch_cuda):
+    """The reference's own outputs (tests/golden/ref_outputs.npz) for the implicit kernel."""
+    from tests.golden.make_golden import CASES
+    from tests.test_oracle import GOLDEN
+    g = np.load(GOLDEN)
+    for name, C, H, W, M, k, seed in CASES:
+        x, w = oracle.make_problem(1, C, H, W, M, k, seed)
+        ref = g[f"{name}/direct_sum"][None]
+        for method in ("kn2row-gpu", "im2col-gpu"):
+            y = _run(clb, torch_cuda, method, x, w)
+            m = _check_fp32(oracle, y, ref, f"{method} {name}")
+            assert m["allclose"], (name, method, m)
+
+
+@pytest.mark.parametrize("shape", [
+    # BASELINE layer shapes at reduced batch: every tap count / channel padding / odd width
+    (2, 64, 56, 56, 64, 3),      # C1
+    (2, 96, 27, 27, 256, 5),     # AlexNet conv2
+    (3, 256, 13, 13, 384, 3),    # AlexNet conv3
+    (2, 384, 13, 13, 256, 3),    # AlexNet conv5
+    (1, 3, 224, 224, 64, 3),     # VGG conv1_1 (C=3)
+    (1, 512, 14, 14, 512, 3),    # VGG conv5_x (K = 4608)
+    (4, 16, 28, 28, 32, 5),      # GoogLeNet 3a/5x5
+    (4, 96, 14, 14, 208, 3),     # GoogLeNet 4a/3x3 (M=208)
+    (4, 832, 7, 7, 384, 1),      # GoogLeNet 5b/1x1
+    (4, 48, 7, 7, 128, 5),       # GoogLeNet 5b/5x5
+    (1, 256, 28, 28, 256, 7),    # sweep k7
+    (1, 256, 28, 28, 256, 11),   # sweep k11
+])
+def test_baseline_shapes_implicit(oracle, clb, torch_cuda, shape):
+    N, C, H, W, M, k = shape
+    x, w = oracle.make_problem(N, C, H, W, M, k, sum(shape))
+    ref = oracle.conv_batch(x, w)
+    y = _run(clb, torch_cuda, "auto", x, w)
+    _check_fp32(oracle, y, ref, f"auto {shape}")
+
+
+def test_tf32_fast_mode(oracle, clb, torch_cuda):
+    x, w = oracle.make_problem(2, 64, 20, 20, 96, 3, 3)
+    ref = oracle.conv_batch(x, w)
+    for method in ("kn2row-gpu", "im2col-gpu", "kn2row-explicit-gpu"):
+        m = oracle.parity_metrics(_run(clb, torch_cuda, method, x, w, "tf32"), ref)
+        assert m["rel_l2"] <= TF32_L2, (method, m)
+
+
+def test_nonstandard_padding(oracle, clb, torch_cuda):
+    """pad != k/2 (beyond the reference; oracle = generalised loop nest)."""
+    x, w = oracle.make_problem(2, 16, 11, 9, 24, 3, 4)
+    for pad in (0, 2):
+        ref = oracle.conv_loopnest(x, w, pad, 1)
+        for method in ("kn2row-gpu", "kn2row-acc-gpu", "im2col-gpu"):
+            _check_fp32(oracle, _run(clb, torch_cuda, method, x, w, pad=pad), ref, f"{method} pad={pad}")
+
+
+def test_im2col_stride(oracle, clb, torch_cuda):
+    x, w = oracle.make_problem(2, 8, 15, 15, 16, 3, 9)
+    ref = oracle.conv_loopnest(x, w, 1, 2)
+    y = clb.run_method("im2col-gpu", torch_cuda.from_numpy(x).cuda(), torch_cuda.from_numpy(w).cuda(), stride=2)
+    _check_fp32(oracle, y.cpu().numpy(), ref, "im2col stride 2")
+
+
+def test_delta_kernels_reproduce_input(oracle, clb, torch_cuda):
+    """conv_kn2_test.cpp:148-152: centre-tap identity kernels give the input back (exact:
+    hi+lo of each value is exact and the other taps contribute exact zeros)."""
+    x, _ = oracle.make_problem(2, 3, 5, 5, 3, 3, 137)
+    w = np.zeros((3, 3, 3, 3), np.float32)
+    for m in range(3):
+        w[m, 1, 1, m] = 1.0
+    for method in METHODS:
+        y = _run(clb, torch_cuda, method, x, w)
+        assert np.array_equal(y, x), method
+
+
+def test_k1_routing_and_conv1x1(oracle, clb, torch_cuda):
+    """methods.cpp:75-85: kn2row/kn2col with k=1 take the conv1x1 path; conv1x1 with k!=1 is
+    a contract violation."""
+    import paper_1704_04428_b200._lib as L
+    x, w = oracle.make_problem(2, 20, 6, 7, 9, 1, 135)
+    ref = oracle.conv_batch(x, w)
+    outs = {}
+    for method in ("kn2row-gpu", "kn2col-gpu", "kn2row-explicit-gpu", "conv1x1-gpu"):
+        layer = clb.LayerConfig("k1", 20, 6, 7, 9, 1, batch=2)
+        with clb.ConvPlan(layer, method) as plan:
+            assert plan.method in ("kn2row-gpu", "conv1x1-gpu"), plan.method
+        outs[method] = _run(clb, torch_cuda, method, x, w)
+        _check_fp32(oracle, outs[method], ref, method)
+    assert np.array_equal(outs["kn2col-gpu"], outs["conv1x1-gpu"])
+    with pytest.raises(L.ClInvalid):
+        clb.ConvPlan(clb.LayerConfig("k3", 4, 5, 5, 2, 3), "conv1x1-gpu")
+
+
+def test_one_contraction_per_call(oracle, clb, torch_cuda):
+    """conv_kn2_test.cpp:162-176 (exactly one GEMM per kn2row call), as launch counts."""
+    torch = torch_cuda
+    layer = clb.LayerConfig("l", 3, 6, 6, 2, 3, batch=1)
+    x, w = oracle.make_problem(1, 3, 6, 6, 2, 3, 140)
+    expect = {"kn2row-gpu": 2, "kn2row-explicit-gpu": 3, "kn2col-gpu": 3, "im2col-gpu": 2, "kn2row-acc-gpu": 10}
+    for method, n in expect.items():
+        with clb.ConvPlan(layer, method) as plan:
+            plan.set_weights(torch.from_numpy(w).cuda())
+            plan.forward(torch.from_numpy(x).cuda())
+            torch.cuda.synchronize()
+            assert plan.launch_count() == n, (method, plan.launch_count())
+
+
+def test_explicit_intermediate_decomposes_per_tap(oracle, clb, torch_cuda):
+    """conv_kn2_test.cpp:195-219 on the device: the (k^2 M x HW) product of the explicit
+    path equals, tap by tap, the 1x1 convolution with that tap's kernel slice."""
+    torch = torch_cuda
+    k, M, C, H, W = 3, 2, 3, 5, 5
+    x, w = oracle.make_problem(1, C, H, W, M, k, 146)
+    r = oracle.kn2row_reorder(w)  # (k^2 M) x C
+    inter = clb.gemm(torch.from_numpy(r).cuda(), torch.from_numpy(x[0].reshape(C, H * W)).cuda()).cpu().numpy()
+    for t in range(k * k):
+        i, j = divmod(t, k)
+        one = _run(clb, torch, "conv1x1-gpu", x, np.ascontiguousarray(w[:, i:i + 1, j:j + 1, :]))
+        blk = inter[t * M:(t + 1) * M]
+        # the two contractions put operands in swapped MMA roles, so equality is to rounding
+        assert np.abs(blk - one[0].reshape(M, H * W)).max() <= 1e-6 * max(1.0, np.abs(blk).max()), t
+        assert np.array_equal(blk, oracle.gemm_ref(r, x[0].reshape(C, H * W))[t * M:(t + 1) * M]) or \
+            np.allclose(blk, oracle.gemm_ref(r, x[0].reshape(C, H * W))[t * M:(t + 1) * M], rtol=1e-6, atol=1e-6)
+
+
+def test_device_shift_add_known_answers(oracle, clb, torch_cuda):
+    torch = torch_cuda
+    y = clb.shift_add_row(torch.ones((9, 9), device="cuda"), 1, 1, 3, 3, 3).cpu().numpy()
+    assert y.ravel().tolist() == [4, 6, 4, 6, 9, 6, 4, 6, 4]
+    inter = oracle.fill(9 * 2 * 20, 9).reshape(18, 20)
+    dev = clb.shift_add_row(torch.from_numpy(inter).cuda(), 1, 2, 4, 5, 3).cpu().numpy()
+    assert np.array_equal(dev.reshape(2, 20), oracle.shift_add_row(inter, 3, 2, 4, 5))
+
+
+def test_gemm_against_fp64(oracle, clb, torch_cuda):
+    torch = torch_cuda
+    for m, n, k in ((1, 1, 1), (128, 256, 64), (300, 200, 70), (129, 17, 1000), (64, 1000, 33)):
+        a = oracle.fill(m * k, 1).reshape(m, k)
+        b = oracle.fill(k * n, 2).reshape(k, n)
+        c = clb.gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+        _check_fp32(oracle, c, a.astype(np.float64) @ b.astype(np.float64), f"gemm {m}x{n}x{k}")
+
+
+def test_device_generator_bit_identical(oracle, clb, torch_cuda):
+    from paper_1704_04428_b200 import rng
+    x, w = rng.make_problem(3, 5, 7, 9, 4, 3, seed=11)
+    xh, wh = oracle.make_problem(3, 5, 7, 9, 4, 3, seed=11)
+    assert np.array_equal(x.cpu().numpy().view(np.uint32), xh.view(np.uint32))
+    assert np.array_equal(w.cpu().numpy().view(np.uint32), wh.view(np.uint32))
+
+
+def test_run_to_run_bitwise_determinism(oracle, clb, torch_cuda):
+    """bench.cpp:126-128 nondeterminism check: fixed reduction order within a build."""
+    torch = torch_cuda
+    x, w = oracle.make_problem(4, 64, 28, 28, 128, 3, 5)
+    for method in METHODS:
+        a = _run(clb, torch, method, x, w)
+        b = _run(clb, torch, method, x, w)
+        assert oracle.fnv1a(a) == oracle.fnv1a(b), method
+
+
+def test_negative_control_detects_corruption(oracle, clb, torch_cuda):
+    """bench.hpp:88-90 perturb hook / --corrupt: the parity gate must be able to fail."""
+    x, w = oracle.make_problem(1, 16, 9, 9, 8, 3, 1)
+    ref = oracle.conv_batch(x, w)
+    y = _run(clb, torch_cuda, "kn2row-gpu", x, w)
+    y[0, 3, 4, 4] += 0.5
+    m = oracle.parity_metrics(y, ref)
+    assert not m["allclose"] and m["max_rel"] > FP32_MAX
+
+
+def test_forward_host_matches_device(oracle, clb, torch_cuda):
+    torch = torch_cuda
+    layer = clb.LayerConfig("h", 32, 14, 14, 48, 3, batch=2)
+    x, w = oracle.make_problem(2, 32, 14, 14, 48, 3, 8)
+    with clb.ConvPlan(layer, "kn2row-gpu") as plan:
+        plan.set_weights(torch.from_numpy(w).cuda())
+        yd = plan.forward(torch.from_numpy(x).cuda()).cpu()
+        hy = torch.empty(plan.output_shape()).pin_memory()
+        plan.forward_host(torch.from_numpy(x).pin_memory(), hy)
+    assert torch.equal(yd, hy)
+
+
+def test_full_size_sampled_images(oracle, clb, torch_cuda):
+    """BASELINE full batch sizes: convolve the whole batch on the GPU, check a sample of
+    images (0, N-1 and two seeded picks) against the oracle (images are independent)."""
+    torch = torch_cuda
+    from paper_1704_04428_b200 import rng, workloads
+    for layer in workloads.workload("alexnet")[1:3] + workloads.workload("googlenet")[4:5]:
+        x, w = rng.make_problem(layer.batch, layer.channels, layer.height, layer.width, layer.kernel_count,
+                                layer.kernel_size, seed=2)
+        with clb.ConvPlan(layer, "auto") as plan:
+            plan.set_weights(w)
+            y = plan.forward(x).cpu().numpy()
+        picks = sorted({0, layer.batch - 1, 7 % layer.batch, 61 % layer.batch})
+        xh = x[picks].cpu().numpy()
+        ref = oracle.conv_batch(xh, w.cpu().numpy())
+        _check_fp32(oracle, y[picks], ref, layer.name)

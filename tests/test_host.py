@@ -1,0 +1,189 @@
+"""CPU-side tests: the C-ABI library loads and exports every symbol include/*.h declares,
+host logic mirrors the reference interface, contract violations surface before any device
+work, and the multi-rank sharding/timing logic (gloo, world size 2)."""
+import os
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _declared_symbols():
+    syms = set()
+    for h in (ROOT / "include").glob("*.h"):
+        syms |= set(re.findall(r"CL_API\s+[\w\s\*]+?\b(cl_\w+)\s*\(", h.read_text()))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+    lib = ctypes.CDLL(str(ROOT / "paper_1704_04428_b200" / "libconvlab_b200.so"))
+    syms = _declared_symbols()
+    assert len(syms) >= 19
+    for s in sorted(syms):
+        assert hasattr(lib, s), s
+    from paper_1704_04428_b200 import _lib
+    assert set(_lib.EXPORTS) == syms
+
+
+def test_package_import_fails_loudly_without_library(tmp_path):
+    """No silent fallback: importing the package without the .so raises."""
+    pkg = tmp_path / "paper_1704_04428_b200"
+    pkg.mkdir()
+    for f in (ROOT / "paper_1704_04428_b200").glob("*.py"):
+        (pkg / f.name).write_text(f.read_text())
+    r = subprocess.run([sys.executable, "-c", "import paper_1704_04428_b200"], cwd=tmp_path,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "no CPU fallback" in r.stderr
+
+
+def test_abi_basics_and_errors_without_gpu():
+    import ctypes
+    import paper_1704_04428_b200 as clb
+    from paper_1704_04428_b200 import _lib
+    L = clb.lib
+    assert L.cl_abi_version() == 1
+    for name, v in _lib.METHODS.items():
+        assert L.cl_method_name(v).decode() == name
+        out = ctypes.c_int()
+        assert L.cl_method_from_name(name.encode(), ctypes.byref(out)) == 1 and out.value == v
+    # contract violations are CL_EINVAL (the reference's std::invalid_argument) even without a GPU
+    for bad in (clb.LayerConfig, ):
+        pass
+    cases = [
+        dict(n=1, c=3, h=8, w=8, m=4, k=2, pad=-1, stride=1),   # even k  (tensor.cpp:64)
+        dict(n=1, c=3, h=2, w=2, m=4, k=7, pad=-1, stride=1),   # k > min(H,W)+k/2 (conv_direct.cpp:15-20)
+        dict(n=0, c=3, h=8, w=8, m=4, k=3, pad=-1, stride=1),   # zero dim
+    ]
+    for c in cases:
+        d = _lib.ConvDesc(**c)
+        h = ctypes.c_void_p()
+        assert L.cl_conv_plan(ctypes.byref(d), 1, 0, 0, ctypes.byref(h)) == _lib.CL_EINVAL, c
+        assert L.cl_last_error()
+    d = _lib.ConvDesc(n=1, c=3, h=8, w=8, m=4, k=3, pad=1, stride=1)
+    h = ctypes.c_void_p()
+    assert L.cl_conv_plan(ctypes.byref(d), 6, 0, 0, ctypes.byref(h)) == _lib.CL_EINVAL   # conv1x1 with k=3
+    if L.cl_device_count() == 0:
+        assert L.cl_conv_plan(ctypes.byref(d), 1, 0, 0, ctypes.byref(h)) == _lib.CL_ENODEVICE
+        assert b"no CPU fallback" in L.cl_last_error() or b"device" in L.cl_last_error()
+
+
+def test_method_names_and_lists():
+    import paper_1704_04428_b200 as clb
+    assert clb.parse_method_list("kn2row-gpu,,im2col") == ["kn2row-gpu", "im2col"]
+    with pytest.raises(ValueError, match="unknown method 'x'"):
+        clb.parse_method_list("kn2row,x")
+    with pytest.raises(ValueError, match="empty method list"):
+        clb.parse_method_list(",")
+    assert clb.method_requires_1x1("conv1x1-gpu") and not clb.method_requires_1x1("kn2row-gpu")
+    for m in clb.REFERENCE_METHODS:
+        assert clb.method_from_name(m) == m
+
+
+def test_footprint_matches_reference_closed_forms(oracle):
+    """bench.cpp:58-85 (and the pinned3 golden numbers, tests/data/golden_bench_columns.csv)."""
+    import ctypes
+    import paper_1704_04428_b200 as clb
+    pinned = {("l1", "kn2row"): (768, 432, 9216, 1024), ("l1", "im2col"): (768, 432, 6912, 1024),
+              ("l2", "kn2row"): (1152, 64, 288, 288), ("l3", "im2col"): (280, 600, 7000, 420),
+              ("l3", "kn2col"): (280, 600, 10500, 420), ("l1", "direct-sum"): (768, 432, 0, 1024)}
+    shapes = {"l1": (3, 8, 8, 4, 3), "l2": (8, 6, 6, 2, 1), "l3": (2, 5, 7, 3, 5)}
+    for (ln, m), want in pinned.items():
+        fp = clb.footprint(clb.LayerConfig(ln, *shapes[ln]), m)
+        assert (fp["input_bytes"], fp["kernel_bytes"], fp["intermediate_bytes"], fp["output_bytes"]) == want
+    if oracle.ref_available():
+        R = oracle.ref()
+        out = (ctypes.c_uint64 * 4)()
+        for m in ("kn2row", "kn2col", "im2col", "im2row", "direct-sum", "conv1x1"):
+            for sh in shapes.values():
+                assert R.ref_footprint(m.encode(), *sh, out) == 0
+                fp = clb.footprint(clb.LayerConfig("x", *sh), m)
+                assert list(out) == [fp["input_bytes"], fp["kernel_bytes"], fp["intermediate_bytes"],
+                                     fp["output_bytes"]], (m, sh)
+
+
+def test_network_grammar_and_workloads():
+    import paper_1704_04428_b200 as clb
+    from paper_1704_04428_b200 import workloads
+    ls = clb.parse_network_text("# c\nconv1 3 227 227 96 11 4\nconv2 96 27 27 256 5  # x\nc3 8 5 5 4 3 pad=0 n=7\n")
+    assert [l.name for l in ls] == ["conv1", "conv2", "c3"] and ls[0].stride == 4 and ls[2].pad == 0
+    assert ls[2].batch == 7 and ls[2].out_height == 3
+    for bad in ("a 1 2 3 4", "a 1 2 3 4 2", "a 1 2 0 4 3", "a 1 2 x 4 3", "a 1 1 1 1 1\na 1 1 1 1 1"):
+        with pytest.raises(RuntimeError, match=r"<text>:\d"):
+            clb.parse_network_text(bad)
+    # BASELINE totals
+    assert round(workloads.total_flops(workloads.workload("vgg16")) / 1e9, 3) == 982.184
+    assert round(workloads.total_flops(workloads.workload("c1")) / 1e9, 3) == 0.231
+    assert round(workloads.total_flops(workloads.workload("scale")) / 1e9, 3) == 947.040
+    assert len(workloads.workload("googlenet")) == 9 and len(workloads.workload("alexnet")) == 4
+    assert all(l.batch == 1 for l in workloads.workload("alexnet-b1"))
+
+
+def test_rng_split_matches_reference(oracle):
+    from paper_1704_04428_b200 import rng
+    for s, lane in ((0, 0), (0, 1), (12345, 7), (2 ** 63 + 5, 3)):
+        assert rng.split(s, lane) == oracle.split(s, lane)
+
+
+def test_cpp_facade_host_logic():
+    exe = ROOT / "tests" / "cpp" / "facade_test"
+    if not exe.exists():
+        subprocess.run(["make", "-s", "-C", str(exe.parent)], check=True)
+    r = subprocess.run([str(exe), "cpu"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "PASSED" in r.stdout, r.stdout + r.stderr
+
+
+def test_shard_range_properties():
+    from paper_1704_04428_b200 import dist
+    for total in (1, 7, 256, 1000):
+        for world in (1, 2, 3, 8):
+            rs = [dist.shard_range(total, world, r) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == total
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            sizes = [e - b for b, e in rs]
+            assert max(sizes) - min(sizes) <= 1
+
+
+_WORKER = r'''
+import os, sys, json
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch, torch.distributed as dist_
+from paper_1704_04428_b200 import dist
+from oracle import oracle as O
+info = dist.init("gloo")
+B, C, H, W, M, k = 2, 3, 6, 6, 4, 3
+img = C * H * W
+# rank r's images = images [rB, (r+1)B) of one global reference stream
+x = O.fill(B * img, O.split(0, 0), dist.image_offset(info.rank, B, img)).reshape(B, C, H, W)
+w = O.fill(M * k * k * C, O.split(0, 1)).reshape(M, k, k, C)
+y = O.conv_batch(x, w)
+gathered = [torch.zeros(B, M, H, W) for _ in range(info.world)]
+dist_.all_gather(gathered, torch.from_numpy(y))
+t = dist.max_over_ranks(1.0 + info.rank, info)
+s = dist.sum_over_ranks(10.0, info)
+if info.rank == 0:
+    xg = O.fill(info.world * B * img, O.split(0, 0)).reshape(-1, C, H, W)
+    ok = np.array_equal(torch.cat(gathered).numpy(), O.conv_batch(xg, w))
+    print(json.dumps({"ok": bool(ok), "max": t, "sum": s}))
+dist_.destroy_process_group()
+'''
+
+
+def test_two_rank_gloo_sharding(tmp_path):
+    """The N>1 path on CPU: per-rank generation offsets reproduce the global batch,
+    MAX/SUM reductions behave, results gather to the single-process answer."""
+    script = tmp_path / "worker.py"
+    script.write_text(_WORKER)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29517", str(script), str(ROOT)]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][0]
+    import json
+    res = json.loads(line)
+    assert res == {"ok": True, "max": 2.0, "sum": 20.0}
