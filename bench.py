@@ -255,6 +255,10 @@ def main():
     st_b = [ev() for _ in range(args.steps)]
     st_e = [ev() for _ in range(args.steps)]
     k_ev = [[(ev(), ev()) for _ in plans] for _ in range(args.steps)]
+    for pair in (p for row in k_ev for p in row):   # torch creates CUDA events lazily:
+        pair[0].record(stream)                       # record once so .cuda_event is a live
+        pair[1].record(stream)                       # handle the library can record into
+    torch.cuda.synchronize()
 
     dist.barrier(info)
     torch.cuda.synchronize()

@@ -88,6 +88,9 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s) {
     p.a_mode = a.mode;
     p.b_mode = b.mode;
     p.stages = tc_num_stages(p.bn, p.planes);
+    const int k_iters = p.taps * p.kblocks;
+    if (p.chunk_iters <= 0) p.chunk_iters = kChunkIters;
+    if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
     const int row_tiles = (p.rows + kTileM - 1) / kTileM;
     p.n_col_tiles = (p.cols + p.bn - 1) / p.bn;
     p.num_tiles = row_tiles * p.n_col_tiles;

@@ -12,13 +12,16 @@
 // shift-add law (conv_kn2.hpp:50-56, conv_kn2.cpp:94-118).  All k^2 taps accumulate into the
 // same TMEM accumulator, so no k^2-fold intermediate and no patch matrix ever reach HBM.
 //
-// Warp roles (256 threads, persistent, one CTA per SM):
+// Warp roles (384 threads, persistent, one CTA per SM):
 //   warp 0      : TMA producer (one elected lane)
 //   warp 1      : MMA issuer   (one lane issues tcgen05.mma + tcgen05.commit)
 //   warp 2      : TMEM allocator
-//   warps 4..7  : epilogue (TMEM -> registers -> global), lane quadrant = warp % 4
-// Pipelines: smem stages full/empty (TMA <-> MMA), TMEM accumulators x2 full/empty
-// (MMA <-> epilogue) so tile t's epilogue overlaps tile t+1's main loop.
+//   warps 4..11 : epilogue (TMEM -> fp32 registers -> global); lane quadrant = warp % 4,
+//                 column half = (warp - 4) / 4
+// Pipelines: smem stages full/empty (TMA <-> MMA); two TMEM chunk accumulators full/empty
+// (MMA <-> epilogue).  The epilogue folds each K chunk into registers (fp32, RNE) while
+// the MMA fills the other buffer, and stores a tile after its last chunk, so stores
+// overlap the next tile's main loop.
 #pragma once
 
 #include <cstdint>
@@ -34,8 +37,10 @@ enum : int { EPI_NCHW = 0, EPI_ROWMAJOR = 1 };
 constexpr int kTileM = 128;          // UMMA M (D rows per tile)
 constexpr int kBlockK = 16;          // fp32 channels per stage (64 B rows, SWIZZLE_64B)
 constexpr int kRowBytes = kBlockK * 4;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;             // 4 control warps + 8 epilogue warps
+constexpr int kEpiThreads = 256;
 constexpr int kSmemBudget = 200 * 1024;
+constexpr int kChunkIters = 8;      // 8 x 16 = 128 K-elements per TMEM accumulation chunk
 
 struct TcParams {
     // problem
@@ -46,6 +51,7 @@ struct TcParams {
     int kblocks;               // 16-channel blocks per tap
     int planes;                // 2 = 3xTF32 (hi,lo), 1 = TF32 (hi)
     int stages;
+    int chunk_iters;           // k-iterations per TMEM accumulation chunk
     int a_mode, b_mode;        // LOAD_TILED / LOAD_IM2COL
     int a_lo, b_lo;            // K-coordinate offset of the lo plane in each tensor map
     int a_tap3, b_tap3;        // tiled: pass the tap as 3rd coordinate (weights [tap][M][K])
@@ -126,7 +132,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 128);
+            mbar_init(&tempty[a], kEpiThreads);
         }
         fence_barrier_init();
     }
@@ -145,6 +151,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 
     const int k_iters = p.taps * p.kblocks;
 
+    if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer ----
         if (lane_id() == 0) {
@@ -185,93 +192,130 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer ----
+        // The K loop of a tile is cut into chunks of p.chunk_iters k-iterations; each chunk
+        // accumulates into a fresh TMEM buffer (ping-pong) that the epilogue folds into
+        // fp32 registers.  Tensor-core accumulation rounds every update of the running
+        // fp32 accumulator (error grows ~linearly in K: 7e-9 K measured), so bounding the
+        // chunk to 128 K-elements keeps the 3xTF32 result fp32-faithful for any K.
         if (lane_id() == 0) {
             const uint32_t idesc = idesc_tf32(kTileM, (uint32_t)bn);
             int stage = 0;
             uint32_t phase = 0;
-            int local = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
-                const int acc = local & 1;
-                const uint32_t acc_phase = (uint32_t)(local >> 1) & 1u;
-                mbar_wait(&tempty[acc], acc_phase ^ 1u);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)acc * (ncols / 2);
-                for (int it = 0; it < k_iters; ++it) {
-                    mbar_wait(&full[stage], phase);
+            uint32_t g = 0;   // chunk counter of this CTA
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                for (int c0 = 0; c0 < k_iters; c0 += p.chunk_iters, ++g) {
+                    const int c1 = c0 + p.chunk_iters < k_iters ? c0 + p.chunk_iters : k_iters;
+                    const uint32_t buf = g & 1u;
+                    mbar_wait(&tempty[buf], ((g >> 1) & 1u) ^ 1u);
                     tc_fence_after();
-                    const uint32_t st = smem_u32(smem + stage * stage_bytes);
-                    const uint32_t a_hi = st, a_lo = st + a_bytes;
-                    const uint32_t b_hi = st + planes * a_bytes, b_lo = b_hi + b_bytes;
+                    const uint32_t d_tmem = tmem_base + buf * (ncols / 2);
+                    for (int it = c0; it < c1; ++it) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t st = smem_u32(smem + stage * stage_bytes);
+                        const uint32_t a_hi = st, a_lo = st + a_bytes;
+                        const uint32_t b_hi = st + planes * a_bytes, b_lo = b_hi + b_bytes;
 #pragma unroll
-                    for (int ks = 0; ks < kBlockK / 8; ++ks) {
-                        const uint32_t off = ks * 32;   // 8 tf32 = 32 B along K
-                        const uint64_t dah = umma_desc_kmajor(a_hi + off, kRowBytes);
-                        const uint64_t dbh = umma_desc_kmajor(b_hi + off, kRowBytes);
-                        uint32_t accum = (it > 0 || ks > 0) ? 1u : 0u;
-                        if (planes == 2) {
-                            const uint64_t dal = umma_desc_kmajor(a_lo + off, kRowBytes);
-                            const uint64_t dbl = umma_desc_kmajor(b_lo + off, kRowBytes);
-                            mma_tf32_ss(d_tmem, dal, dbh, idesc, accum);   // small cross terms first
-                            mma_tf32_ss(d_tmem, dah, dbl, idesc, 1u);
-                            accum = 1u;
+                        for (int ks = 0; ks < kBlockK / 8; ++ks) {
+                            const uint32_t off = ks * 32;   // 8 tf32 = 32 B along K
+                            const uint64_t dah = umma_desc_kmajor(a_hi + off, kRowBytes);
+                            const uint64_t dbh = umma_desc_kmajor(b_hi + off, kRowBytes);
+                            uint32_t accum = (it > c0 || ks > 0) ? 1u : 0u;
+                            if (planes == 2) {
+                                const uint64_t dal = umma_desc_kmajor(a_lo + off, kRowBytes);
+                                const uint64_t dbl = umma_desc_kmajor(b_lo + off, kRowBytes);
+                                mma_tf32_ss(d_tmem, dal, dbh, idesc, accum);   // small cross terms first
+                                mma_tf32_ss(d_tmem, dah, dbl, idesc, 1u);
+                                accum = 1u;
+                            }
+                            mma_tf32_ss(d_tmem, dah, dbh, idesc, accum);
                         }
-                        mma_tf32_ss(d_tmem, dah, dbh, idesc, accum);
+                        mma_commit(&empty[stage]);      // frees the smem stage once these MMAs retire
+                        if (++stage == stages) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
                     }
-                    mma_commit(&empty[stage]);      // frees the smem stage once these MMAs retire
-                    if (++stage == stages) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
+                    mma_commit(&tfull[buf]);            // chunk complete -> epilogue
                 }
-                mma_commit(&tfull[acc]);            // accumulator complete -> epilogue
             }
         }
     } else if (warp >= 4) {
         // --------------------------------------------------------------- epilogue ----
+        // 8 warps: lane quadrant = warp % 4 (TMEM access rule), column half = (warp-4)/4.
+        // Each thread owns one D row and up to 128 columns of running fp32 sums.
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
         const int quad = warp & 3;
+        const int half = (warp - 4) >> 2;
         const int lane = (int)lane_id();
-        int local = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
-            const int acc = local & 1;
-            const uint32_t acc_phase = (uint32_t)(local >> 1) & 1u;
+        const int hcols = bn >> 1;                   // multiple of 8 (bn % 16 == 0)
+        const int cbase = half * hcols;
+        uint32_t g = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
             const int mt = tile / p.n_col_tiles;
             const int nt = tile - mt * p.n_col_tiles;
             const int row = mt * kTileM + quad * 32 + lane;
-            const int col0 = nt * bn;
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            const uint32_t t_addr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)acc * (ncols / 2);
-            const bool row_ok = row < p.rows;
-            float* dst = nullptr;
-            long long cstride = 1;
-            if (p.epi == EPI_NCHW) {
-                const int n = row / p.pq_out;
-                const int pq = row - n * p.pq_out;
-                dst = p.out + ((long long)n * p.out_channels) * p.pq_out + pq;
-                cstride = p.pq_out;
-            } else {
-                dst = p.out + (long long)row * p.ld;
-                cstride = 1;
-            }
-            for (int c = 0; c < bn; c += 16) {
-                uint32_t r[16];
-                tmem_ld_32x32b_x16(t_addr + (uint32_t)c, r);
-                tmem_ld_wait();
-                if (row_ok) {
+            const int col0 = nt * bn + cbase;
+            float sum[128];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int col = col0 + c + j;
-                        if (col < p.cols) {
-                            float* o = dst + (long long)col * cstride;
-                            const float v = __uint_as_float(r[j]);
-                            if (p.accumulate) *o += v;
-                            else *o = v;
+            for (int j = 0; j < 128; ++j) sum[j] = 0.0f;
+            for (int c0 = 0; c0 < k_iters; c0 += p.chunk_iters, ++g) {
+                const uint32_t buf = g & 1u;
+                mbar_wait(&tfull[buf], (g >> 1) & 1u);
+                tc_fence_after();
+                const uint32_t t_addr =
+                    tmem_base + ((uint32_t)(quad * 32) << 16) + buf * (ncols / 2) + (uint32_t)cbase;
+#pragma unroll
+                for (int grp = 0; grp < 8; grp += 4) {      // 4 loads (64 columns) in flight
+                    uint32_t r[4][16];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if ((grp + q) * 16 < hcols) tmem_ld_32x32b_x16(t_addr + (uint32_t)((grp + q) * 16), r[q]);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if ((grp + q) * 16 < hcols)
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) sum[(grp + q) * 16 + j] += __uint_as_float(r[q][j]);
+                }
+                tc_fence_before();
+                mbar_arrive(&tempty[buf]);
+            }
+            // ---- store the finished tile ----
+            if (row < p.rows) {
+                if (p.epi == EPI_NCHW) {
+                    const int n = row / p.pq_out;
+                    const int pq = row - n * p.pq_out;
+                    float* dst = p.out + ((long long)n * p.out_channels) * p.pq_out + pq;
+#pragma unroll
+                    for (int j = 0; j < 128; ++j) {
+                        const int col = col0 + j;
+                        if (j < hcols && col < p.cols) {
+                            float* o = dst + (long long)col * p.pq_out;
+                            if (p.accumulate) *o += sum[j];
+                            else *o = sum[j];
+                        }
+                    }
+                } else {
+                    float* dst = p.out + (long long)row * p.ld + col0;
+                    const bool vec = (p.ld % 4 == 0) && !p.accumulate;
+#pragma unroll
+                    for (int j = 0; j < 128; j += 4) {
+                        if (j < hcols) {
+                            if (vec && col0 + j + 3 < p.cols) {
+                                *reinterpret_cast<float4*>(dst + j) = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    if (col0 + j + e < p.cols) {
+                                        if (p.accumulate) dst[j + e] += sum[j + e];
+                                        else dst[j + e] = sum[j + e];
+                                    }
+                            }
                         }
                     }
                 }
             }
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
         }
     }
 
