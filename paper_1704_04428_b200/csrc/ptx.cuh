@@ -59,7 +59,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred P;\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2, 0x989680;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, P;\n\t}\n"
         : "=r"(ok)
         : "r"(addr), "r"(parity)
@@ -67,8 +67,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     return ok != 0;
 }
 
-// Blocking wait on the phase with the given parity.  A watchdog traps after ~4 s so that a
-// protocol bug surfaces as a launch error instead of a hung GPU.
+// Blocking wait on the phase with the given parity.  try_wait WITHOUT a suspend-time hint:
+// with a hint ptxas emits NANOSLEEP.SYNCS <hint> and the waiter oversleeps (measured: 37% of
+// stall samples, tensor pipe 13% busy).  A watchdog traps after ~4 s so that a protocol bug
+// surfaces as a launch error instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     if (mbar_try_wait(addr, parity)) return;
