@@ -79,7 +79,14 @@ cl_method resolve(const cl_conv_desc& d, cl_method m) {
     return CL_METHOD_KN2ROW;
 }
 
-size_t ws_bytes(const cl_plan* p) {
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// Method buffers first, then the stream-K scratch of the tcgen05 engine.
+size_t method_ws_bytes(const cl_plan* p);
+size_t ws_bytes(const cl_plan* p) { return align256(method_ws_bytes(p)) + tc_scratch_bytes(); }
+void* scratch_of(const cl_plan* p, void* ws) { return static_cast<char*>(ws) + align256(method_ws_bytes(p)); }
+
+size_t method_ws_bytes(const cl_plan* p) {
     const cl_conv_desc& d = p->d;
     const size_t nhw = (size_t)d.n * d.h * d.w;
     const size_t npq = (size_t)d.n * p->P * p->Q;
@@ -171,9 +178,11 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
     float* wsf = static_cast<float*>(ws);
     p->launches = 0;
     bool began = false;
-    auto tc = [&](const Operand& a, const Operand& b, const TcParams& t) {
+    void* scratch = scratch_of(p, ws);
+    auto tc = [&](const Operand& a, const Operand& b, TcParams t) {
         if (p->ev_begin && !began) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
         began = true;
+        set_scratch(t, scratch);
         launch_tc(a, b, t, s);
         ++p->launches;
     };
@@ -421,7 +430,7 @@ void cl_conv_destroy(cl_plan* p) {
 size_t cl_gemm_workspace_bytes(int m, int n, int k, cl_precision precision) {
     const int planes = precision == CL_PREC_FP32 ? 2 : 1;
     const size_t kp = (size_t)round_up(k > 0 ? k : 1, kBlockK);
-    return ((size_t)(m > 0 ? m : 0) + (size_t)(n > 0 ? n : 0)) * planes * kp * 4;
+    return align256(((size_t)(m > 0 ? m : 0) + (size_t)(n > 0 ? n : 0)) * planes * kp * 4) + tc_scratch_bytes();
 }
 
 cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float* c, cl_precision precision,
@@ -457,6 +466,7 @@ cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float
         t.epi = EPI_ROWMAJOR;
         t.out = c;
         t.ld = n;
+        set_scratch(t, static_cast<char*>(ws) + align256((size_t)(m + n) * planes * kp * 4));
         launch_tc(tiled(as, m, 1, kp, planes), tiled(bs, n, 1, kp, planes), t, s);
         if (own) CLB_CUDA(cudaFreeAsync(own, s));
     });

@@ -64,7 +64,15 @@ struct Operand {
 };
 
 void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows);
+// p.partials / p.flags must point at tc_scratch_bytes() of device scratch (stream-K fixup).
 void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s);
+constexpr int kMaxGrid = 160;   // >= SM count (148 on B200)
+size_t tc_scratch_bytes();
+// carve the stream-K scratch out of a workspace pointer
+inline void set_scratch(TcParams& t, void* scratch) {
+    t.partials = static_cast<float*>(scratch);
+    t.flags = reinterpret_cast<unsigned*>(static_cast<char*>(scratch) + (size_t)kMaxGrid * kTileM * 256 * sizeof(float));
+}
 int num_sms();
 
 }  // namespace clb

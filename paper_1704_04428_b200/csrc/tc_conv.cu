@@ -95,6 +95,8 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s) {
     p.n_col_tiles = (p.cols + p.bn - 1) / p.bn;
     p.num_tiles = row_tiles * p.n_col_tiles;
     if (p.num_tiles <= 0) return;
+    p.chunks_per_tile = (k_iters + p.chunk_iters - 1) / p.chunk_iters;
+    const long long total_chunks = (long long)p.num_tiles * p.chunks_per_tile;
     const int smem = tc_smem_bytes(p.bn, p.planes, p.stages);
     static int configured = 0;
     if (smem > configured) {
@@ -102,9 +104,30 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s) {
         configured = 227 * 1024;
     }
     const int sms = num_sms();
-    const int grid = p.num_tiles < sms ? p.num_tiles : sms;
-    tc_conv_kernel<<<grid, kThreads, smem, s>>>(ma, mb, p);
-    CLB_CUDA(cudaGetLastError());
+    int grid = total_chunks < sms ? (int)total_chunks : sms;
+    if (grid > kMaxGrid) grid = kMaxGrid;
+    // whole-tile waves for all but the last 1-2 waves; stream-K over the rest
+    const int waves = p.num_tiles / grid;
+    p.dp_tiles = (p.num_tiles % grid == 0) ? p.num_tiles : (waves >= 2 ? (waves - 1) * grid : 0);
+    p.sk_chunks = (p.num_tiles - p.dp_tiles) * p.chunks_per_tile;
+    if (!p.partials || !p.flags) throw Error(6, "stream-K scratch missing");
+    CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));
+    // Cooperative launch: the fixup makes CTAs wait on each other, so all must be resident.
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CLB_CUDA(cudaLaunchKernelEx(&cfg, tc_conv_kernel, ma, mb, p));
+}
+
+size_t tc_scratch_bytes() {
+    return (size_t)kMaxGrid * kTileM * 256 * sizeof(float) + (size_t)kMaxGrid * sizeof(unsigned);
 }
 
 }  // namespace clb

@@ -12,7 +12,13 @@
 // shift-add law (conv_kn2.hpp:50-56, conv_kn2.cpp:94-118).  All k^2 taps accumulate into the
 // same TMEM accumulator, so no k^2-fold intermediate and no patch matrix ever reach HBM.
 //
-// Warp roles (384 threads, persistent, one CTA per SM):
+// Work split (hybrid data-parallel + stream-K): whole tiles round-robin for all but the last
+// 1-2 waves, whose (tile, K-chunk) space is cut into gridDim.x contiguous ranges, so every
+// SM gets the same MMA work regardless of the tile count.  A tile
+// whose chunks straddle CTAs is finished by the CTA holding its FIRST chunk (it processes
+// that piece last); the CTAs holding the later pieces publish fp32 partials + a flag first.
+// Summation order is fixed by the static split -> bitwise run-to-run determinism.
+// Warp roles (384 threads, persistent, one CTA per SM, cooperative launch):
 //   warp 0      : TMA producer (one elected lane)
 //   warp 1      : MMA issuer   (one lane issues tcgen05.mma + tcgen05.commit)
 //   warp 2      : TMEM allocator
@@ -64,8 +70,18 @@ struct TcParams {
     long long ld;              // EPI_ROWMAJOR leading dimension
     int out_channels;          // EPI_NCHW: channel count of the output tensor
     int pq_out;                // EPI_NCHW: P*Q
-    unsigned long long* debug; // optional
+    // stream-K work split (chunk granularity) and its deterministic fixup
+    int chunks_per_tile;       // ceil(k_iters / chunk_iters)
+    int dp_tiles;              // tiles [0, dp_tiles) scheduled whole, round-robin over CTAs
+    int sk_chunks;             // chunks of tiles [dp_tiles, num_tiles), split contiguously (stream-K)
+    float* partials;           // [gridDim.x][128][bn] tile-tail partial sums
+    unsigned* flags;           // [gridDim.x], zeroed before the launch; 1 = partial ready
 };
+
+// Contiguous chunk range of CTA b: [chunk_start(b), chunk_start(b+1)).
+__host__ __device__ inline int chunk_start(int b, int total, int grid) {
+    return (int)(((long long)b * total) / grid);
+}
 
 __host__ __device__ inline int tc_stage_bytes(int bn, int planes) { return planes * (kTileM + bn) * kRowBytes; }
 
@@ -113,6 +129,56 @@ __device__ __forceinline__ void load_operand(const CUtensorMap* map, const Opera
     else
         tma_load_3d(map, bar, dst, kcoord, c.c1, c.tap3 ? tap : 0);
 }
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void epi_bar_sync() {   // the 8 epilogue warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
+
+// A piece = the part of one tile's chunk range [c_lo, c_hi) that falls in this CTA's range.
+struct Piece {
+    int tile, c_lo, c_hi;
+};
+
+// Hybrid data-parallel + stream-K schedule of one CTA: first its share of the whole tiles
+// [0, dp_tiles) round-robin (tile = b, b + grid, ...: neighbouring CTAs work on neighbouring
+// tiles, which keeps the live input window compact in L2), then its contiguous range of the
+// stream-K chunk space covering the remaining 1-2 waves of tiles.
+struct Sched {
+    int b, grid, cpt, dp_tiles, i, n_dp, g, g_end;
+    __device__ Sched(const TcParams& p, int b_, int grid_)
+        : b(b_), grid(grid_), cpt(p.chunks_per_tile), dp_tiles(p.dp_tiles), i(0) {
+        n_dp = dp_tiles / grid;
+        g = chunk_start(b, p.sk_chunks, grid);
+        g_end = chunk_start(b + 1, p.sk_chunks, grid);
+    }
+    __device__ bool next(Piece& pc) {
+        if (i < n_dp) {
+            pc.tile = b + i * grid;
+            pc.c_lo = 0;
+            pc.c_hi = cpt;
+            ++i;
+            return true;
+        }
+        if (g >= g_end) return false;
+        const int t = g / cpt;
+        pc.tile = dp_tiles + t;
+        pc.c_lo = g - t * cpt;
+        const int left = g_end - g;
+        pc.c_hi = (cpt - pc.c_lo) < left ? cpt : pc.c_lo + left;
+        g += pc.c_hi - pc.c_lo;
+        return true;
+    }
+};
 
 __global__ void __launch_bounds__(kThreads, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -162,6 +228,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t tmem_base = *tmem_slot;
 
     const int k_iters = p.taps * p.kblocks;
+    const int cpt = p.chunks_per_tile;
+    const int ci = p.chunk_iters;
 
     if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0) {
@@ -170,85 +238,96 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t tx = (uint32_t)stage_bytes;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-                const int mt = tile / p.n_col_tiles;
-                const int nt = tile - mt * p.n_col_tiles;
+            Sched sch(p, blockIdx.x, gridDim.x);
+            Piece pc;
+            while (sch.next(pc)) {
+                const int mt = pc.tile / p.n_col_tiles;
+                const int nt = pc.tile - mt * p.n_col_tiles;
                 const OperandCoord ca = operand_coord(p.a_mode, p.a_tap3, mt * kTileM, p.P, p.Q, p.pad);
                 const OperandCoord cb = operand_coord(p.b_mode, p.b_tap3, nt * bn, p.P, p.Q, p.pad);
-                int ti = p.tap_begin / p.ksize, tj = p.tap_begin - (p.tap_begin / p.ksize) * p.ksize;
-                for (int tap = p.tap_begin; tap < p.tap_begin + p.taps; ++tap) {
-                    for (int kc = 0; kc < p.kblocks * kBlockK; kc += kBlockK) {
-                        mbar_wait(&empty[stage], phase ^ 1u);
-                        mbar_arrive_expect_tx(&full[stage], tx);
-                        uint8_t* st = smem + stage * stage_bytes;
-                        uint8_t* a_hi = st;
-                        uint8_t* b_hi = st + planes * a_bytes;
-                        load_operand(&map_a, ca, &full[stage], a_hi, kc, tap, ti, tj);
-                        load_operand(&map_b, cb, &full[stage], b_hi, kc, tap, ti, tj);
-                        if (planes == 2) {
-                            load_operand(&map_a, ca, &full[stage], a_hi + a_bytes, kc + p.a_lo, tap, ti, tj);
-                            load_operand(&map_b, cb, &full[stage], b_hi + b_bytes, kc + p.b_lo, tap, ti, tj);
-                        }
-                        if (++stage == stages) {
-                            stage = 0;
-                            phase ^= 1u;
-                        }
+                const int it0 = pc.c_lo * ci;
+                const int it1 = pc.c_hi * ci < k_iters ? pc.c_hi * ci : k_iters;
+                // (tap, channel block) of it0; then walk with counters, no division in the loop
+                int tap = p.tap_begin + it0 / p.kblocks;
+                int kb = it0 - (it0 / p.kblocks) * p.kblocks;
+                int ti = tap / p.ksize, tj = tap - (tap / p.ksize) * p.ksize;
+                for (int it = it0; it < it1; ++it) {
+                    const int kc = kb * kBlockK;
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    mbar_arrive_expect_tx(&full[stage], tx);
+                    uint8_t* a_hi = smem + stage * stage_bytes;
+                    uint8_t* b_hi = a_hi + planes * a_bytes;
+                    load_operand(&map_a, ca, &full[stage], a_hi, kc, tap, ti, tj);
+                    load_operand(&map_b, cb, &full[stage], b_hi, kc, tap, ti, tj);
+                    if (planes == 2) {
+                        load_operand(&map_a, ca, &full[stage], a_hi + a_bytes, kc + p.a_lo, tap, ti, tj);
+                        load_operand(&map_b, cb, &full[stage], b_hi + b_bytes, kc + p.b_lo, tap, ti, tj);
                     }
-                    if (++tj == p.ksize) {
-                        tj = 0;
-                        ++ti;
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                    if (++kb == p.kblocks) {
+                        kb = 0;
+                        ++tap;
+                        if (++tj == p.ksize) {
+                            tj = 0;
+                            ++ti;
+                        }
                     }
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer ----
-        // The K loop of a tile is cut into chunks of p.chunk_iters k-iterations; each chunk
-        // accumulates into a fresh TMEM buffer (ping-pong) that the epilogue folds into
-        // fp32 registers.  Tensor-core accumulation rounds every update of the running
-        // fp32 accumulator (error grows ~linearly in K: 7e-9 K measured), so bounding the
-        // chunk to 128 K-elements keeps the 3xTF32 result fp32-faithful for any K.
+        // The K loop of a tile is cut into chunks of ci k-iterations; each chunk accumulates
+        // into a fresh TMEM buffer (ping-pong) that the epilogue folds into fp32 registers.
+        // Tensor-core accumulation rounds every update of the running fp32 accumulator
+        // (error grows ~linearly in K: 7e-9 K measured), so bounding the chunk to 128
+        // K-elements keeps the 3xTF32 result fp32-faithful for any K.
         if (lane_id() == 0) {
             const uint32_t idesc = idesc_tf32(kTileM, (uint32_t)bn);
             int stage = 0;
             uint32_t phase = 0;
-            uint32_t g = 0;   // chunk counter of this CTA
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-                for (int c0 = 0; c0 < k_iters; c0 += p.chunk_iters, ++g) {
-                    const int c1 = c0 + p.chunk_iters < k_iters ? c0 + p.chunk_iters : k_iters;
-                    const uint32_t buf = g & 1u;
-                    mbar_wait(&tempty[buf], ((g >> 1) & 1u) ^ 1u);
+            uint32_t lg = 0;
+            Sched sch(p, blockIdx.x, gridDim.x);
+            Piece pc;
+            while (sch.next(pc))
+            for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
+                const int c0 = c * ci;
+                const int c1 = c0 + ci < k_iters ? c0 + ci : k_iters;
+                const uint32_t buf = lg & 1u;
+                mbar_wait(&tempty[buf], ((lg >> 1) & 1u) ^ 1u);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + buf * (ncols / 2);
+                for (int it = c0; it < c1; ++it) {
+                    mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t d_tmem = tmem_base + buf * (ncols / 2);
-                    for (int it = c0; it < c1; ++it) {
-                        mbar_wait(&full[stage], phase);
-                        tc_fence_after();
-                        const uint32_t st = smem_u32(smem + stage * stage_bytes);
-                        const uint32_t a_hi = st, a_lo = st + a_bytes;
-                        const uint32_t b_hi = st + planes * a_bytes, b_lo = b_hi + b_bytes;
+                    const uint32_t st = smem_u32(smem + stage * stage_bytes);
+                    const uint32_t a_hi = st, a_lo = st + a_bytes;
+                    const uint32_t b_hi = st + planes * a_bytes, b_lo = b_hi + b_bytes;
 #pragma unroll
-                        for (int ks = 0; ks < kBlockK / 8; ++ks) {
-                            const uint32_t off = ks * 32;   // 8 tf32 = 32 B along K
-                            const uint64_t dah = umma_desc_kmajor(a_hi + off, kRowBytes);
-                            const uint64_t dbh = umma_desc_kmajor(b_hi + off, kRowBytes);
-                            uint32_t accum = (it > c0 || ks > 0) ? 1u : 0u;
-                            if (planes == 2) {
-                                const uint64_t dal = umma_desc_kmajor(a_lo + off, kRowBytes);
-                                const uint64_t dbl = umma_desc_kmajor(b_lo + off, kRowBytes);
-                                mma_tf32_ss(d_tmem, dal, dbh, idesc, accum);   // small cross terms first
-                                mma_tf32_ss(d_tmem, dah, dbl, idesc, 1u);
-                                accum = 1u;
-                            }
-                            mma_tf32_ss(d_tmem, dah, dbh, idesc, accum);
+                    for (int ks = 0; ks < kBlockK / 8; ++ks) {
+                        const uint32_t off = ks * 32;   // 8 tf32 = 32 B along K
+                        const uint64_t dah = umma_desc_kmajor(a_hi + off, kRowBytes);
+                        const uint64_t dbh = umma_desc_kmajor(b_hi + off, kRowBytes);
+                        uint32_t accum = (it > c0 || ks > 0) ? 1u : 0u;
+                        if (planes == 2) {
+                            const uint64_t dal = umma_desc_kmajor(a_lo + off, kRowBytes);
+                            const uint64_t dbl = umma_desc_kmajor(b_lo + off, kRowBytes);
+                            mma_tf32_ss(d_tmem, dal, dbh, idesc, accum);   // small cross terms first
+                            mma_tf32_ss(d_tmem, dah, dbl, idesc, 1u);
+                            accum = 1u;
                         }
-                        mma_commit(&empty[stage]);      // frees the smem stage once these MMAs retire
-                        if (++stage == stages) {
-                            stage = 0;
-                            phase ^= 1u;
-                        }
+                        mma_tf32_ss(d_tmem, dah, dbh, idesc, accum);
                     }
-                    mma_commit(&tfull[buf]);            // chunk complete -> epilogue
+                    mma_commit(&empty[stage]);      // frees the smem stage once these MMAs retire
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
                 }
+                mma_commit(&tfull[buf]);            // chunk complete -> epilogue
             }
         }
     } else if (warp >= 4) {
@@ -261,18 +340,21 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const int lane = (int)lane_id();
         const int hcols = bn >> 1;                   // multiple of 8 (bn % 16 == 0)
         const int cbase = half * hcols;
-        uint32_t g = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-            const int mt = tile / p.n_col_tiles;
-            const int nt = tile - mt * p.n_col_tiles;
-            const int row = mt * kTileM + quad * 32 + lane;
+        const int trow = quad * 32 + lane;           // row within the tile
+        uint32_t lg = 0;
+        Sched sch(p, blockIdx.x, gridDim.x);
+        Piece pc;
+        while (sch.next(pc)) {
+            const int mt = pc.tile / p.n_col_tiles;
+            const int nt = pc.tile - mt * p.n_col_tiles;
+            const int row = mt * kTileM + trow;
             const int col0 = nt * bn + cbase;
             float sum[128];
 #pragma unroll
             for (int j = 0; j < 128; ++j) sum[j] = 0.0f;
-            for (int c0 = 0; c0 < k_iters; c0 += p.chunk_iters, ++g) {
-                const uint32_t buf = g & 1u;
-                mbar_wait(&tfull[buf], (g >> 1) & 1u);
+            for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
+                const uint32_t buf = lg & 1u;
+                mbar_wait(&tfull[buf], (lg >> 1) & 1u);
                 tc_fence_after();
                 const uint32_t t_addr =
                     tmem_base + ((uint32_t)(quad * 32) << 16) + buf * (ncols / 2) + (uint32_t)cbase;
@@ -291,6 +373,38 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[buf]);
+            }
+            if (pc.c_lo > 0) {
+                // ---- tile tail handled by this CTA: publish the partial for the finisher ----
+                float* dst = p.partials + ((long long)blockIdx.x * kTileM + trow) * bn + cbase;
+#pragma unroll
+                for (int j = 0; j < 128; j += 4)
+                    if (j < hcols) *reinterpret_cast<float4*>(dst + j) = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+                __threadfence();
+                epi_bar_sync();
+                if (threadIdx.x == 4 * 32) st_release_u32(&p.flags[blockIdx.x], 1u);
+                continue;
+            }
+            if (pc.c_hi < cpt) {
+                // ---- finisher of a split tile: add the later pieces' partials in CTA order ----
+                const int last = (pc.tile - p.dp_tiles) * cpt + cpt - 1;   // in stream-K chunk space
+                for (int b2 = blockIdx.x + 1; b2 < (int)gridDim.x && chunk_start(b2, p.sk_chunks, gridDim.x) <= last;
+                     ++b2) {
+                    const uint64_t t0 = globaltimer_ns();
+                    while (ld_acquire_u32(&p.flags[b2]) == 0u) {
+                        if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+                    }
+                    const float* src = p.partials + ((long long)b2 * kTileM + trow) * bn + cbase;
+#pragma unroll
+                    for (int j = 0; j < 128; j += 4)
+                        if (j < hcols) {
+                            const float4 v = __ldcg(reinterpret_cast<const float4*>(src + j));
+                            sum[j] += v.x;
+                            sum[j + 1] += v.y;
+                            sum[j + 2] += v.z;
+                            sum[j + 3] += v.w;
+                        }
+                }
             }
             // ---- store the finished tile ----
             if (row < p.rows) {
