@@ -123,7 +123,7 @@ Operand implicit_a(const cl_plan* p, const float* xs) {
     Operand a;
     a.mode = LOAD_IM2COL;
     a.ptr = xs;
-    a.kp = p->Cp;
+    a.kw = p->planes * p->Cp;
     a.planes = p->planes;
     a.n = p->d.n;
     a.h = p->d.h;
@@ -139,7 +139,7 @@ Operand tiled(const float* ptr, long long rows, int taps, int kp, int planes) {
     o.ptr = ptr;
     o.rows = rows;
     o.taps = taps;
-    o.kp = kp;
+    o.kw = planes * kp;
     o.planes = planes;
     return o;
 }
@@ -328,8 +328,8 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         p->prec = precision;
         p->planes = precision == CL_PREC_FP32 ? 2 : 1;
         p->device = device;
-        p->Cp = round_up(d.c, kBlockK);
-        p->Kp = round_up(d.k * d.k * d.c, kBlockK);
+        p->Cp = round_up(d.c, k_granule(p->planes));
+        p->Kp = round_up(d.k * d.k * d.c, k_granule(p->planes));
         p->bn = bn_for(d.m);
         if (m == CL_METHOD_IM2COL) p->wpack_bytes = (size_t)d.m * p->planes * p->Kp * 4;
         else p->wpack_bytes = (size_t)d.k * d.k * d.m * p->planes * p->Cp * 4;
@@ -429,7 +429,7 @@ void cl_conv_destroy(cl_plan* p) {
 
 size_t cl_gemm_workspace_bytes(int m, int n, int k, cl_precision precision) {
     const int planes = precision == CL_PREC_FP32 ? 2 : 1;
-    const size_t kp = (size_t)round_up(k > 0 ? k : 1, kBlockK);
+    const size_t kp = (size_t)round_up(k > 0 ? k : 1, k_granule(planes));
     return align256(((size_t)(m > 0 ? m : 0) + (size_t)(n > 0 ? n : 0)) * planes * kp * 4) + tc_scratch_bytes();
 }
 
@@ -444,7 +444,7 @@ cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float
         check_device(dev);
         auto s = static_cast<cudaStream_t>(stream);
         const int planes = precision == CL_PREC_FP32 ? 2 : 1;
-        const int kp = round_up(k, kBlockK);
+        const int kp = round_up(k, k_granule(planes));
         const size_t need = cl_gemm_workspace_bytes(m, n, k, precision);
         void* own = nullptr;
         if (!ws) {

@@ -27,9 +27,13 @@ struct Error : std::runtime_error {
     } while (0)
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+// channel padding granularity of the split layout
+inline int k_granule(int planes) { return planes == 2 ? 16 : 32; }
 
 // ---- pre-pass / post-pass kernels (prepass.cu) -------------------------------------------
-// x NCHW fp32 -> xs[n][h][w][planes][Cp] (hi = rna_tf32(x), lo = x - hi; zero for c >= C)
+// Split layout of every operand row (k_pad channels): 3xTF32 -> per 16-channel block
+// [hi 16 | lo 16] (row = 2*k_pad words); TF32 -> hi only (row = k_pad words, k_pad % 32 == 0).
+// x NCHW fp32 -> xs[n][h][w][row] (hi = rna_tf32(x), lo = x - hi; zero for c >= C)
 void launch_nchw_to_nhwc_split(const float* x, float* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s);
 // a[rows][K] -> as[rows][planes][Kp]
@@ -57,7 +61,7 @@ struct Operand {
     const float* ptr = nullptr;
     long long rows = 0;      // tiled: rows of the map
     int taps = 1;            // tiled: 3rd dim
-    int kp = 0;              // padded channel count per plane
+    int kw = 0;              // words per row: 2*Cp (3xTF32 hi|lo interleave) or Cp (TF32)
     int planes = 2;
     // im2col only
     int n = 0, h = 0, w = 0, k = 1, pad = 0;

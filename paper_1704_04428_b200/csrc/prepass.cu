@@ -14,10 +14,18 @@ __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float(r);
 }
 
+// Row layout (see internal.hpp): 3xTF32 rows interleave hi|lo per 16-channel block so each
+// 128-byte TMA row carries both halves of 16 channels; TF32 rows hold hi only.
 __device__ __forceinline__ void store_split(float* dst, long long base, int c, int kp, int planes, float v) {
+    (void)kp;
     const float hi = tf32_rna(v);
-    dst[base + c] = hi;
-    if (planes == 2) dst[base + kp + c] = v - hi;
+    if (planes == 2) {
+        const int u = (c >> 4) << 5, w = c & 15;
+        dst[base + u + w] = hi;
+        dst[base + u + 16 + w] = v - hi;
+    } else {
+        dst[base + c] = hi;
+    }
 }
 
 // ------------------------------------------------------------------ NCHW -> NHWC split ----

@@ -47,7 +47,7 @@ int num_sms() {
 
 void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows) {
     resolve_driver();
-    const cuuint64_t kdim = (cuuint64_t)op.planes * op.kp;   // channels per row incl. hi|lo planes
+    const cuuint64_t kdim = (cuuint64_t)op.kw;   // words per row (hi|lo interleaved for 3xTF32)
     CUresult r;
     if (op.mode == LOAD_IM2COL) {
         cuuint64_t dims[4] = {kdim, (cuuint64_t)op.w, (cuuint64_t)op.h, (cuuint64_t)op.n};
@@ -58,16 +58,16 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows) {
         int upper[2] = {op.pad - (op.k - 1), op.pad - (op.k - 1)};
         cuuint32_t estr[4] = {1, 1, 1, 1};
         r = g_im2col(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(op.ptr), dims, strides, lower,
-                     upper, (cuuint32_t)kBlockK, (cuuint32_t)box_rows, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     upper, (cuuint32_t)kRowWords, (cuuint32_t)box_rows, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
         cuuint64_t dims[3] = {kdim, (cuuint64_t)op.rows, (cuuint64_t)op.taps};
         cuuint64_t strides[2] = {kdim * 4, kdim * 4 * (cuuint64_t)op.rows};
-        cuuint32_t box[3] = {(cuuint32_t)kBlockK, (cuuint32_t)box_rows, 1};
+        cuuint32_t box[3] = {(cuuint32_t)kRowWords, (cuuint32_t)box_rows, 1};
         cuuint32_t estr[3] = {1, 1, 1};
         r = g_tiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(op.ptr), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS)
@@ -77,19 +77,17 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows) {
 
 void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s) {
     if (p.bn % 16 != 0 || p.bn < 16 || p.bn > 256) throw Error(6, "tile N must be a multiple of 16 in [16,256]");
-    if (a.kp != b.kp || a.kp % kBlockK != 0) throw Error(6, "operand K padding mismatch");
+    if (a.kw != b.kw || a.kw % kRowWords != 0 || a.planes != b.planes) throw Error(6, "operand K layout mismatch");
     CUtensorMap ma, mb;
     encode_operand_map(&ma, a, kTileM);
     encode_operand_map(&mb, b, p.bn);
     p.planes = a.planes;
-    p.kblocks = a.kp / kBlockK;
-    p.a_lo = a.kp;
-    p.b_lo = b.kp;
+    p.kblocks = a.kw / kRowWords;
     p.a_mode = a.mode;
     p.b_mode = b.mode;
     p.stages = tc_num_stages(p.bn, p.planes);
     const int k_iters = p.taps * p.kblocks;
-    if (p.chunk_iters <= 0) p.chunk_iters = kChunkIters;
+    if (p.chunk_iters <= 0) p.chunk_iters = p.planes == 2 ? kChunkIters : kChunkIters / 2;   // 128 K-elements
     if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
     const int row_tiles = (p.rows + kTileM - 1) / kTileM;
     p.n_col_tiles = (p.cols + p.bn - 1) / p.bn;
@@ -107,8 +105,11 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s) {
     int grid = total_chunks < sms ? (int)total_chunks : sms;
     if (grid > kMaxGrid) grid = kMaxGrid;
     // whole-tile waves for all but the last 1-2 waves; stream-K over the rest
+    // (a last wave that is >= 95% full stays data-parallel: splitting it costs more than it saves)
     const int waves = p.num_tiles / grid;
-    p.dp_tiles = (p.num_tiles % grid == 0) ? p.num_tiles : (waves >= 2 ? (waves - 1) * grid : 0);
+    const int ceil_waves = (p.num_tiles + grid - 1) / grid;
+    const bool balanced = (long long)(ceil_waves * grid - p.num_tiles) * 20 <= (long long)ceil_waves * grid;
+    p.dp_tiles = balanced ? p.num_tiles : (waves >= 2 ? (waves - 1) * grid : 0);
     p.sk_chunks = (p.num_tiles - p.dp_tiles) * p.chunks_per_tile;
     if (!p.partials || !p.flags) throw Error(6, "stream-K scratch missing");
     CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));

@@ -41,8 +41,12 @@ enum : int { LOAD_TILED = 0, LOAD_IM2COL = 1 };
 enum : int { EPI_NCHW = 0, EPI_ROWMAJOR = 1 };
 
 constexpr int kTileM = 128;          // UMMA M (D rows per tile)
-constexpr int kBlockK = 16;          // fp32 channels per stage (64 B rows, SWIZZLE_64B)
-constexpr int kRowBytes = kBlockK * 4;
+// Operand rows are 128-byte units (SWIZZLE_128B, one TMA box per operand per stage):
+//   3xTF32: 16 channels as [hi 0..15 | lo 0..15]   (kBlockK = 16 channels per stage)
+//   TF32  : 32 channels of hi                      (32 channels per stage)
+constexpr int kBlockK = 16;          // channel granularity of the 3xTF32 interleave
+constexpr int kRowWords = 32;
+constexpr int kRowBytes = kRowWords * 4;
 constexpr int kThreads = 384;             // 4 control warps + 8 epilogue warps
 constexpr int kEpiThreads = 256;
 constexpr int kSmemBudget = 200 * 1024;
@@ -55,11 +59,10 @@ struct TcParams {
     int n_col_tiles, num_tiles;
     int taps, tap_begin, ksize;  // K loop: taps [tap_begin, tap_begin+taps), tap t -> (t/ksize, t%ksize)
     int kblocks;               // 16-channel blocks per tap
-    int planes;                // 2 = 3xTF32 (hi,lo), 1 = TF32 (hi)
+    int planes;                // 2 = 3xTF32 (hi|lo interleaved per 16 channels), 1 = TF32 (hi)
     int stages;
     int chunk_iters;           // k-iterations per TMEM accumulation chunk
     int a_mode, b_mode;        // LOAD_TILED / LOAD_IM2COL
-    int a_lo, b_lo;            // K-coordinate offset of the lo plane in each tensor map
     int a_tap3, b_tap3;        // tiled: pass the tap as 3rd coordinate (weights [tap][M][K])
     // im2col geometry of the row operand (output pixels)
     int P, Q, pad;
@@ -83,7 +86,7 @@ __host__ __device__ inline int chunk_start(int b, int total, int grid) {
     return (int)(((long long)b * total) / grid);
 }
 
-__host__ __device__ inline int tc_stage_bytes(int bn, int planes) { return planes * (kTileM + bn) * kRowBytes; }
+__host__ __device__ inline int tc_stage_bytes(int bn, int planes) { return (void)planes, (kTileM + bn) * kRowBytes; }
 
 __host__ inline int tc_num_stages(int bn, int planes) {
     int s = (kSmemBudget - 1024) / tc_stage_bytes(bn, planes);
@@ -157,7 +160,7 @@ struct Sched {
     int b, grid, cpt, dp_tiles, i, n_dp, g, g_end;
     __device__ Sched(const TcParams& p, int b_, int grid_)
         : b(b_), grid(grid_), cpt(p.chunks_per_tile), dp_tiles(p.dp_tiles), i(0) {
-        n_dp = dp_tiles / grid;
+        n_dp = dp_tiles > b ? (dp_tiles - b + grid - 1) / grid : 0;
         g = chunk_start(b, p.sk_chunks, grid);
         g_end = chunk_start(b + 1, p.sk_chunks, grid);
     }
@@ -189,9 +192,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int bn = p.bn;
     const int planes = p.planes;
     const int stages = p.stages;
-    const int a_bytes = kTileM * kRowBytes;       // one plane of A per stage
-    const int b_bytes = bn * kRowBytes;           // one plane of B per stage
-    const int stage_bytes = planes * (a_bytes + b_bytes);
+    const int a_bytes = kTileM * kRowBytes;       // A rows of one stage
+    const int b_bytes = bn * kRowBytes;           // B rows of one stage
+    const int stage_bytes = a_bytes + b_bytes;
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
     uint64_t* full = bars;
@@ -252,17 +255,12 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 int kb = it0 - (it0 / p.kblocks) * p.kblocks;
                 int ti = tap / p.ksize, tj = tap - (tap / p.ksize) * p.ksize;
                 for (int it = it0; it < it1; ++it) {
-                    const int kc = kb * kBlockK;
+                    const int kc = kb * kRowWords;
                     mbar_wait(&empty[stage], phase ^ 1u);
                     mbar_arrive_expect_tx(&full[stage], tx);
-                    uint8_t* a_hi = smem + stage * stage_bytes;
-                    uint8_t* b_hi = a_hi + planes * a_bytes;
-                    load_operand(&map_a, ca, &full[stage], a_hi, kc, tap, ti, tj);
-                    load_operand(&map_b, cb, &full[stage], b_hi, kc, tap, ti, tj);
-                    if (planes == 2) {
-                        load_operand(&map_a, ca, &full[stage], a_hi + a_bytes, kc + p.a_lo, tap, ti, tj);
-                        load_operand(&map_b, cb, &full[stage], b_hi + b_bytes, kc + p.b_lo, tap, ti, tj);
-                    }
+                    uint8_t* a_st = smem + stage * stage_bytes;
+                    load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
+                    load_operand(&map_b, cb, &full[stage], a_st + a_bytes, kc, tap, ti, tj);
                     if (++stage == stages) {
                         stage = 0;
                         phase ^= 1u;
@@ -303,23 +301,30 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 for (int it = c0; it < c1; ++it) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t st = smem_u32(smem + stage * stage_bytes);
-                    const uint32_t a_hi = st, a_lo = st + a_bytes;
-                    const uint32_t b_hi = st + planes * a_bytes, b_lo = b_hi + b_bytes;
+                    const uint32_t a_st = smem_u32(smem + stage * stage_bytes);
+                    const uint32_t b_st = a_st + a_bytes;
+                    if (planes == 2) {
+                        // row = [hi 16 | lo 16]: k-step s (8 tf32 = 32 B) of hi at 32 s, of lo at 64 + 32 s
 #pragma unroll
-                    for (int ks = 0; ks < kBlockK / 8; ++ks) {
-                        const uint32_t off = ks * 32;   // 8 tf32 = 32 B along K
-                        const uint64_t dah = umma_desc_kmajor(a_hi + off, kRowBytes);
-                        const uint64_t dbh = umma_desc_kmajor(b_hi + off, kRowBytes);
-                        uint32_t accum = (it > c0 || ks > 0) ? 1u : 0u;
-                        if (planes == 2) {
-                            const uint64_t dal = umma_desc_kmajor(a_lo + off, kRowBytes);
-                            const uint64_t dbl = umma_desc_kmajor(b_lo + off, kRowBytes);
+                        for (int ks = 0; ks < 2; ++ks) {
+                            const uint32_t off = ks * 32;
+                            const uint64_t dah = umma_desc_kmajor(a_st + off, kRowBytes);
+                            const uint64_t dbh = umma_desc_kmajor(b_st + off, kRowBytes);
+                            const uint64_t dal = umma_desc_kmajor(a_st + 64 + off, kRowBytes);
+                            const uint64_t dbl = umma_desc_kmajor(b_st + 64 + off, kRowBytes);
+                            const uint32_t accum = (it > c0 || ks > 0) ? 1u : 0u;
                             mma_tf32_ss(d_tmem, dal, dbh, idesc, accum);   // small cross terms first
                             mma_tf32_ss(d_tmem, dah, dbl, idesc, 1u);
-                            accum = 1u;
+                            mma_tf32_ss(d_tmem, dah, dbh, idesc, 1u);
                         }
-                        mma_tf32_ss(d_tmem, dah, dbh, idesc, accum);
+                    } else {
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) {
+                            const uint32_t off = ks * 32;
+                            mma_tf32_ss(d_tmem, umma_desc_kmajor(a_st + off, kRowBytes),
+                                        umma_desc_kmajor(b_st + off, kRowBytes), idesc,
+                                        (it > c0 || ks > 0) ? 1u : 0u);
+                        }
                     }
                     mma_commit(&empty[stage]);      // frees the smem stage once these MMAs retire
                     if (++stage == stages) {
