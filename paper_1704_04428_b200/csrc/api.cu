@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" boundary (include/convlab_b200.h): plans, method dispatch,
 // workspace management, error mapping.  No CPU fallback anywhere: every entry point
 // either enqueues sm_100a kernels or returns an error.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -34,6 +35,17 @@ cl_status guarded(F&& f) {
 
 void require(bool ok, const std::string& what) {
     if (!ok) throw Error(CL_EINVAL, what);
+}
+
+// CTA group of the tcgen05 engine: 2 (CTA pair, M = 256) unless CLB_CTA_GROUP=1 (A/B switch
+// for measurements) or the problem has fewer than 256 rows.
+int cta_group_for(long long rows) {
+    static int forced = [] {
+        const char* e = std::getenv("CLB_CTA_GROUP");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced == 1 || forced == 2) return forced;
+    return rows >= 256 ? 2 : 1;
 }
 
 int bn_for(int cols) {
@@ -183,7 +195,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
         if (p->ev_begin && !began) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
         began = true;
         set_scratch(t, scratch);
-        launch_tc(a, b, t, s);
+        launch_tc(a, b, t, s, cta_group_for(t.rows));
         ++p->launches;
     };
     auto tc_done = [&] {
@@ -467,7 +479,7 @@ cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float
         t.out = c;
         t.ld = n;
         set_scratch(t, static_cast<char*>(ws) + align256((size_t)(m + n) * planes * kp * 4));
-        launch_tc(tiled(as, m, 1, kp, planes), tiled(bs, n, 1, kp, planes), t, s);
+        launch_tc(tiled(as, m, 1, kp, planes), tiled(bs, n, 1, kp, planes), t, s, cta_group_for(m));
         if (own) CLB_CUDA(cudaFreeAsync(own, s));
     });
 }

@@ -75,42 +75,48 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows) {
                            " failed with CUresult " + std::to_string((int)r));
 }
 
-void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s) {
+void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cg) {
+    if (cg != 1 && cg != 2) throw Error(6, "cta group must be 1 or 2");
     if (p.bn % 16 != 0 || p.bn < 16 || p.bn > 256) throw Error(6, "tile N must be a multiple of 16 in [16,256]");
     if (a.kw != b.kw || a.kw % kRowWords != 0 || a.planes != b.planes) throw Error(6, "operand K layout mismatch");
     CUtensorMap ma, mb;
     encode_operand_map(&ma, a, kTileM);
-    encode_operand_map(&mb, b, p.bn);
+    encode_operand_map(&mb, b, p.bn / cg);
     p.planes = a.planes;
     p.kblocks = a.kw / kRowWords;
     p.a_mode = a.mode;
     p.b_mode = b.mode;
-    p.stages = tc_num_stages(p.bn, p.planes);
+    p.stages = tc_num_stages(p.bn / cg, p.planes);
     const int k_iters = p.taps * p.kblocks;
     if (p.chunk_iters <= 0) p.chunk_iters = p.planes == 2 ? kChunkIters : kChunkIters / 2;   // 128 K-elements
     if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
-    const int row_tiles = (p.rows + kTileM - 1) / kTileM;
+    const int tile_m = kTileM * cg;
+    const int row_tiles = (p.rows + tile_m - 1) / tile_m;
     p.n_col_tiles = (p.cols + p.bn - 1) / p.bn;
     p.num_tiles = row_tiles * p.n_col_tiles;
     if (p.num_tiles <= 0) return;
     p.chunks_per_tile = (k_iters + p.chunk_iters - 1) / p.chunk_iters;
     const long long total_chunks = (long long)p.num_tiles * p.chunks_per_tile;
-    const int smem = tc_smem_bytes(p.bn, p.planes, p.stages);
-    static int configured = 0;
-    if (smem > configured) {
-        CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        configured = 227 * 1024;
+    const int smem = tc_smem_bytes(p.bn / cg, p.planes, p.stages);
+    static bool configured[3] = {false, false, false};
+    if (!configured[cg]) {
+        if (cg == 2)
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        else
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        configured[cg] = true;
     }
     const int sms = num_sms();
-    int grid = total_chunks < sms ? (int)total_chunks : sms;
-    if (grid > kMaxGrid) grid = kMaxGrid;
+    int units = (sms < kMaxGrid ? sms : kMaxGrid) / cg;      // scheduling units (CTAs or CTA pairs)
+    if (total_chunks < units) units = (int)total_chunks;
     // whole-tile waves for all but the last 1-2 waves; stream-K over the rest
     // (a last wave that is >= 95% full stays data-parallel: splitting it costs more than it saves)
-    const int waves = p.num_tiles / grid;
-    const int ceil_waves = (p.num_tiles + grid - 1) / grid;
-    const bool balanced = (long long)(ceil_waves * grid - p.num_tiles) * 20 <= (long long)ceil_waves * grid;
-    p.dp_tiles = balanced ? p.num_tiles : (waves >= 2 ? (waves - 1) * grid : 0);
+    const int waves = p.num_tiles / units;
+    const int ceil_waves = (p.num_tiles + units - 1) / units;
+    const bool balanced = (long long)(ceil_waves * units - p.num_tiles) * 20 <= (long long)ceil_waves * units;
+    p.dp_tiles = balanced ? p.num_tiles : (waves >= 2 ? (waves - 1) * units : 0);
     p.sk_chunks = (p.num_tiles - p.dp_tiles) * p.chunks_per_tile;
+    const int grid = units * cg;
     if (!p.partials || !p.flags) throw Error(6, "stream-K scratch missing");
     CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));
     // Cooperative launch: the fixup makes CTAs wait on each other, so all must be resident.
@@ -119,12 +125,30 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+    if (cg == 2) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 2;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CLB_CUDA(cudaLaunchKernelEx(&cfg, tc_conv_kernel, ma, mb, p));
+    cfg.numAttrs = na;
+    cudaError_t e = cg == 2 ? cudaLaunchKernelEx(&cfg, tc_conv_kernel<2>, ma, mb, p)
+                            : cudaLaunchKernelEx(&cfg, tc_conv_kernel<1>, ma, mb, p);
+    if (e != cudaSuccess && cg == 2) {
+        // clusters + cooperative not accepted: grid = one pair per SM pair is still all-resident
+        cudaGetLastError();
+        cfg.attrs = attr + 1;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, tc_conv_kernel<2>, ma, mb, p);
+    }
+    CLB_CUDA(e);
 }
 
 size_t tc_scratch_bytes() {

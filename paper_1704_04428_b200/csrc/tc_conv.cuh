@@ -183,6 +183,13 @@ struct Sched {
     }
 };
 
+// CG = 1: one CTA per 128-row tile (tcgen05 cta_group::1).
+// CG = 2: a CTA pair (cluster of 2) per 256-row tile (cta_group::2): each CTA TMA-loads its
+//         128 A rows and HALF of the BN B rows into its own smem, all completion bytes land
+//         on the leader's barrier, the leader issues M=256 MMAs reading both CTAs' smem and
+//         multicasts its commits; each CTA's TMEM holds its 128 D rows.  Per-SM operand
+//         bytes per MMA drop by BN/2 rows (-33% at BN = 256).
+template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const TcParams p) {
@@ -192,9 +199,15 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int bn = p.bn;
     const int planes = p.planes;
     const int stages = p.stages;
+    const int tile_m = kTileM * CG;               // D rows per tile (the pair's rows for CG = 2)
+    const int b_rows = bn / CG;                   // B rows this CTA loads
     const int a_bytes = kTileM * kRowBytes;       // A rows of one stage
-    const int b_bytes = bn * kRowBytes;           // B rows of one stage
+    const int b_bytes = b_rows * kRowBytes;       // B rows of one stage
     const int stage_bytes = a_bytes + b_bytes;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;       // scheduling unit
+    const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
     uint64_t* full = bars;
@@ -213,7 +226,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], kEpiThreads);
+            mbar_init(&tempty[a], CG * kEpiThreads);
         }
         fence_barrier_init();
     }
@@ -222,11 +235,17 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         tma_prefetch_desc(&map_b);
     }
     if (warp == 2) {
-        tmem_alloc(tmem_slot, ncols);
-        tmem_relinquish();
+        if constexpr (CG == 2) {
+            tmem_alloc_2sm(tmem_slot, ncols);
+            tmem_relinquish_2sm();
+        } else {
+            tmem_alloc(tmem_slot, ncols);
+            tmem_relinquish();
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync();   // peer barriers initialised before any remote use
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -240,14 +259,15 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         if (lane_id() == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t tx = (uint32_t)stage_bytes;
-            Sched sch(p, blockIdx.x, gridDim.x);
+            const uint32_t tx = (uint32_t)(CG * stage_bytes);   // both CTAs' bytes land on the leader
+            Sched sch(p, unit, nunits);
             Piece pc;
             while (sch.next(pc)) {
                 const int mt = pc.tile / p.n_col_tiles;
                 const int nt = pc.tile - mt * p.n_col_tiles;
-                const OperandCoord ca = operand_coord(p.a_mode, p.a_tap3, mt * kTileM, p.P, p.Q, p.pad);
-                const OperandCoord cb = operand_coord(p.b_mode, p.b_tap3, nt * bn, p.P, p.Q, p.pad);
+                const OperandCoord ca =
+                    operand_coord(p.a_mode, p.a_tap3, mt * tile_m + (int)rank * kTileM, p.P, p.Q, p.pad);
+                const OperandCoord cb = operand_coord(p.b_mode, p.b_tap3, nt * bn + (int)rank * b_rows, p.P, p.Q, p.pad);
                 const int it0 = pc.c_lo * ci;
                 const int it1 = pc.c_hi * ci < k_iters ? pc.c_hi * ci : k_iters;
                 // (tap, channel block) of it0; then walk with counters, no division in the loop
@@ -257,10 +277,24 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 for (int it = it0; it < it1; ++it) {
                     const int kc = kb * kRowWords;
                     mbar_wait(&empty[stage], phase ^ 1u);
-                    mbar_arrive_expect_tx(&full[stage], tx);
                     uint8_t* a_st = smem + stage * stage_bytes;
-                    load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
-                    load_operand(&map_b, cb, &full[stage], a_st + a_bytes, kc, tap, ti, tj);
+                    if constexpr (CG == 2) {
+                        const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
+                        if (leader) mbar_arrive_expect_tx(&full[stage], tx);
+                        if (ca.mode == LOAD_IM2COL)
+                            tma_load_im2col_4d_2sm(&map_a, lbar, a_st, kc, ca.c1, ca.c2, ca.c3, (uint16_t)tj, (uint16_t)ti);
+                        else
+                            tma_load_3d_2sm(&map_a, lbar, a_st, kc, ca.c1, ca.tap3 ? tap : 0);
+                        if (cb.mode == LOAD_IM2COL)
+                            tma_load_im2col_4d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.c2, cb.c3, (uint16_t)tj,
+                                                   (uint16_t)ti);
+                        else
+                            tma_load_3d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.tap3 ? tap : 0);
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], tx);
+                        load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
+                        load_operand(&map_b, cb, &full[stage], a_st + a_bytes, kc, tap, ti, tj);
+                    }
                     if (++stage == stages) {
                         stage = 0;
                         phase ^= 1u;
@@ -283,13 +317,21 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // Tensor-core accumulation rounds every update of the running fp32 accumulator
         // (error grows ~linearly in K: 7e-9 K measured), so bounding the chunk to 128
         // K-elements keeps the 3xTF32 result fp32-faithful for any K.
-        if (lane_id() == 0) {
-            const uint32_t idesc = idesc_tf32(kTileM, (uint32_t)bn);
+        if (lane_id() == 0 && leader) {
+            const uint32_t idesc = idesc_tf32((uint32_t)tile_m, (uint32_t)bn);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t lg = 0;
-            Sched sch(p, blockIdx.x, gridDim.x);
+            Sched sch(p, unit, nunits);
             Piece pc;
+            auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+                if constexpr (CG == 2) mma_tf32_ss_2sm(d, a, b, idesc, acc);
+                else mma_tf32_ss(d, a, b, idesc, acc);
+            };
+            auto commit = [&](uint64_t* bar) {
+                if constexpr (CG == 2) mma_commit_2sm_mc(bar, (uint16_t)0x3);
+                else mma_commit(bar);
+            };
             while (sch.next(pc))
             for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
                 const int c0 = c * ci;
@@ -313,26 +355,25 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             const uint64_t dal = umma_desc_kmajor(a_st + 64 + off, kRowBytes);
                             const uint64_t dbl = umma_desc_kmajor(b_st + 64 + off, kRowBytes);
                             const uint32_t accum = (it > c0 || ks > 0) ? 1u : 0u;
-                            mma_tf32_ss(d_tmem, dal, dbh, idesc, accum);   // small cross terms first
-                            mma_tf32_ss(d_tmem, dah, dbl, idesc, 1u);
-                            mma_tf32_ss(d_tmem, dah, dbh, idesc, 1u);
+                            mma(d_tmem, dal, dbh, accum);   // small cross terms first
+                            mma(d_tmem, dah, dbl, 1u);
+                            mma(d_tmem, dah, dbh, 1u);
                         }
                     } else {
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks) {
                             const uint32_t off = ks * 32;
-                            mma_tf32_ss(d_tmem, umma_desc_kmajor(a_st + off, kRowBytes),
-                                        umma_desc_kmajor(b_st + off, kRowBytes), idesc,
-                                        (it > c0 || ks > 0) ? 1u : 0u);
+                            mma(d_tmem, umma_desc_kmajor(a_st + off, kRowBytes), umma_desc_kmajor(b_st + off, kRowBytes),
+                                (it > c0 || ks > 0) ? 1u : 0u);
                         }
                     }
-                    mma_commit(&empty[stage]);      // frees the smem stage once these MMAs retire
+                    commit(&empty[stage]);          // frees the smem stage(s) once these MMAs retire
                     if (++stage == stages) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
-                mma_commit(&tfull[buf]);            // chunk complete -> epilogue
+                commit(&tfull[buf]);                // chunk complete -> epilogue(s)
             }
         }
     } else if (warp >= 4) {
@@ -345,14 +386,14 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const int lane = (int)lane_id();
         const int hcols = bn >> 1;                   // multiple of 8 (bn % 16 == 0)
         const int cbase = half * hcols;
-        const int trow = quad * 32 + lane;           // row within the tile
+        const int trow = quad * 32 + lane;           // row within this CTA's 128 rows
         uint32_t lg = 0;
-        Sched sch(p, blockIdx.x, gridDim.x);
+        Sched sch(p, unit, nunits);
         Piece pc;
         while (sch.next(pc)) {
             const int mt = pc.tile / p.n_col_tiles;
             const int nt = pc.tile - mt * p.n_col_tiles;
-            const int row = mt * kTileM + trow;
+            const int row = mt * tile_m + (int)rank * kTileM + trow;
             const int col0 = nt * bn + cbase;
             float sum[128];
 #pragma unroll
@@ -377,7 +418,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             for (int j = 0; j < 16; ++j) sum[(grp + q) * 16 + j] += __uint_as_float(r[q][j]);
                 }
                 tc_fence_before();
-                mbar_arrive(&tempty[buf]);
+                if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[buf]), 0));
+                else mbar_arrive(&tempty[buf]);
             }
             if (pc.c_lo > 0) {
                 // ---- tile tail handled by this CTA: publish the partial for the finisher ----
@@ -391,15 +433,15 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 continue;
             }
             if (pc.c_hi < cpt) {
-                // ---- finisher of a split tile: add the later pieces' partials in CTA order ----
+                // ---- finisher of a split tile: add the later pieces' partials in unit order ----
                 const int last = (pc.tile - p.dp_tiles) * cpt + cpt - 1;   // in stream-K chunk space
-                for (int b2 = blockIdx.x + 1; b2 < (int)gridDim.x && chunk_start(b2, p.sk_chunks, gridDim.x) <= last;
-                     ++b2) {
+                for (int u2 = unit + 1; u2 < nunits && chunk_start(u2, p.sk_chunks, nunits) <= last; ++u2) {
+                    const int slot = u2 * CG + (int)rank;
                     const uint64_t t0 = globaltimer_ns();
-                    while (ld_acquire_u32(&p.flags[b2]) == 0u) {
+                    while (ld_acquire_u32(&p.flags[slot]) == 0u) {
                         if (globaltimer_ns() - t0 > 4000000000ull) __trap();
                     }
-                    const float* src = p.partials + ((long long)b2 * kTileM + trow) * bn + cbase;
+                    const float* src = p.partials + ((long long)slot * kTileM + trow) * bn + cbase;
 #pragma unroll
                     for (int j = 0; j < 128; j += 4)
                         if (j < hcols) {
@@ -451,9 +493,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync();   // the peer must be done with TMEM and barriers
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, ncols);
+        if constexpr (CG == 2) tmem_dealloc_2sm(tmem_base, ncols);
+        else tmem_dealloc(tmem_base, ncols);
     }
 }
 
