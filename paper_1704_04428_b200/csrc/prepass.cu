@@ -29,30 +29,55 @@ __device__ __forceinline__ void store_split(float* dst, long long base, int c, i
 }
 
 // ------------------------------------------------------------------ NCHW -> NHWC split ----
-// grid (ceil(HW/32), ceil(Cp/32), N), block (32, 8)
-__global__ void nchw_to_nhwc_split_kernel(const float* __restrict__ x, float* __restrict__ xs, int C, int HW,
-                                          int Cp, int planes) {
-    __shared__ float tile[32][33];
+// Tile = 32 channels x 64 pixels of one image, 256 threads.  Loads: each warp reads whole
+// 128-byte channel-row segments (coalesced along pixels).  Stores: the tile's output is, per
+// pixel, one contiguous run of 64 words ([hi16|lo16] x 2 for 3xTF32, 32 hi words for TF32),
+// written by a warp as full 128-byte lines (lane = word).  grid (ceil(HW/64), ceil(Cp/32), N)
+__global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, float* __restrict__ xs,
+                                                                 int C, int HW, int Cp, int planes) {
+    __shared__ float tile[64][33];   // [pixel][channel]
     const int n = blockIdx.z;
-    const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const int p0 = blockIdx.x * 64, c0 = blockIdx.y * 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float* xn = x + (long long)n * C * HW;
-    for (int cc = threadIdx.y; cc < 32; cc += 8) {
-        const int c = c0 + cc, pix = p0 + threadIdx.x;
-        tile[cc][threadIdx.x] = (c < C && pix < HW) ? __ldg(xn + (long long)c * HW + pix) : 0.0f;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int cc = warp + 8 * r;
+        const int c = c0 + cc;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int pix = p0 + lane + 32 * h;
+            tile[lane + 32 * h][cc] = (c < C && pix < HW) ? __ldg(xn + (long long)c * HW + pix) : 0.0f;
+        }
     }
     __syncthreads();
-    const long long row_stride = (long long)planes * Cp;
-    for (int pp = threadIdx.y; pp < 32; pp += 8) {
-        const int pix = p0 + pp, c = c0 + threadIdx.x;
-        if (pix < HW && c < Cp)
-            store_split(xs, ((long long)n * HW + pix) * row_stride, c, Cp, planes, tile[threadIdx.x][pp]);
+    const long long row_words = (long long)planes * Cp;
+    const int words = planes == 2 ? 64 : 32;            // output words per pixel in this tile
+    const int nch = Cp - c0 < 32 ? Cp - c0 : 32;        // channels of this tile inside the padded row
+    const int out_words = planes == 2 ? 2 * nch : nch;
+    for (int pp = warp; pp < 64; pp += 8) {
+        const int pix = p0 + pp;
+        if (pix >= HW) break;
+        float* dst = xs + ((long long)n * HW + pix) * row_words + (long long)planes * c0;
+        for (int o = lane; o < words; o += 32) {
+            if (o >= out_words) continue;
+            if (planes == 2) {
+                const int u = o >> 5, w = o & 31;            // 16-channel block u of this tile
+                const int cc = u * 16 + (w & 15);
+                const float v = tile[pp][cc];
+                const float hi = tf32_rna(v);
+                dst[o] = (w < 16) ? hi : v - hi;
+            } else {
+                dst[o] = tf32_rna(tile[pp][o]);
+            }
+        }
     }
 }
 
 void launch_nchw_to_nhwc_split(const float* x, float* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s) {
-    dim3 grid((HW + 31) / 32, (Cp + 31) / 32, N), block(32, 8);
-    nchw_to_nhwc_split_kernel<<<grid, block, 0, s>>>(x, xs, C, HW, Cp, planes);
+    dim3 grid((HW + 63) / 64, (Cp + 31) / 32, N);
+    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, C, HW, Cp, planes);
     CLB_CUDA(cudaGetLastError());
 }
 

@@ -11,7 +11,7 @@
 using namespace clb;
 
 __global__ void probe(const __grid_constant__ CUtensorMap map, int mode, int box_bytes, int batch, int rounds,
-                      int nrows_total, int box_rows, int issuers, unsigned long long* cycles) {
+                      int nrows_total, int box_rows, int issuers, unsigned long long* cycles, int W) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + batch * box_bytes);
@@ -30,7 +30,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, int mode, int box
         mbar_arrive_expect_tx(&bar[w], per * box_bytes);
         for (int b = 0; b < per; ++b) {
             uint8_t* dst = smem + (w * per + b) * box_bytes;
-            if (mode == 1) tma_load_im2col_4d(&map, &bar[w], dst, 0, row % 56 - 1, (row / 56) % 56 - 1, row / 3136, 1, 1);
+            if (mode == 1) tma_load_im2col_4d(&map, &bar[w], dst, 0, row % W - 1, (row / W) % W - 1, row / (W * W), 1, 1);
             else tma_load_3d(&map, &bar[w], dst, 0, row, 0);
             row += box_rows;
             if (row + box_rows > nrows_total) row = 0;
@@ -54,21 +54,19 @@ int main() {
     cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f2, cudaEnableDefault, &q);
     EncT enc_t = (EncT)f1;
     EncI enc_i = (EncI)f2;
-    const int N = 32, H = 56, W = 56;
-    const int rows = N * H * W;
+    const int rows = 32 * 56 * 56;
     float* buf;
     cudaMalloc(&buf, (size_t)rows * 128);   // 32 fp32 channels per pixel, contiguous pixels
     cudaMemset(buf, 0, (size_t)rows * 128);
     unsigned long long* cyc;
     cudaMalloc(&cyc, 148 * 8);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    struct Case { int mode, box_rows, row_bytes, batch, issuers, ctas; };
+    struct Case { int mode, box_rows, row_bytes, batch, issuers, ctas, W; };
     Case cases[] = {
-        {0, 128, 128, 1, 1, 148}, {0, 128, 128, 2, 1, 148}, {0, 128, 128, 4, 1, 148}, {0, 128, 128, 8, 1, 148},
-        {0, 128, 128, 8, 2, 148}, {0, 128, 128, 8, 4, 148}, {0, 64, 128, 8, 1, 148}, {0, 32, 128, 8, 1, 148},
-        {0, 256, 128, 6, 1, 148}, {0, 128, 64, 8, 1, 148},  {0, 128, 128, 8, 1, 1},
-        {1, 128, 128, 1, 1, 148}, {1, 128, 128, 4, 1, 148}, {1, 128, 128, 8, 1, 148}, {1, 128, 128, 8, 4, 148},
-        {1, 64, 128, 8, 1, 148},  {1, 256, 128, 6, 1, 148}, {1, 128, 64, 8, 1, 148},
+        {0, 128, 128, 8, 1, 148, 56}, {0, 128, 128, 8, 4, 148, 56},
+        {1, 128, 128, 8, 1, 148, 224}, {1, 128, 128, 8, 1, 148, 56}, {1, 128, 128, 8, 1, 148, 28},
+        {1, 128, 128, 8, 1, 148, 14}, {1, 128, 128, 8, 1, 148, 13}, {1, 128, 128, 8, 1, 148, 7},
+        {1, 128, 128, 8, 4, 148, 56}, {1, 128, 128, 8, 4, 148, 13}, {1, 128, 128, 8, 4, 148, 7},
     };
     printf("%-6s %5s %5s %5s %4s %4s %9s %9s %9s %9s\n", "mode", "rows", "rowB", "batch", "iss", "ctas", "ms",
            "TB/s", "B/clk/SM", "clk/load");
@@ -76,6 +74,7 @@ int main() {
         CUtensorMap map;
         const CUtensorMapSwizzle sw = cs.row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
         CUresult r;
+        const int W = cs.W, H = cs.W, N = rows / (W * H);
         if (cs.mode == 1) {
             cuuint64_t dims[4] = {32, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
             cuuint64_t str[3] = {128, 128ull * W, 128ull * W * H};
@@ -96,12 +95,12 @@ int main() {
         const int box_bytes = cs.box_rows * cs.row_bytes;
         const int rounds = 400;
         const int smem = 1024 + cs.batch * box_bytes + 256;
-        probe<<<cs.ctas, 128, smem>>>(map, cs.mode, box_bytes, cs.batch, rounds, rows, cs.box_rows, cs.issuers, cyc);
+        probe<<<cs.ctas, 128, smem>>>(map, cs.mode, box_bytes, cs.batch, rounds, N * H * W, cs.box_rows, cs.issuers, cyc, W);
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        probe<<<cs.ctas, 128, smem>>>(map, cs.mode, box_bytes, cs.batch, rounds, rows, cs.box_rows, cs.issuers, cyc);
+        probe<<<cs.ctas, 128, smem>>>(map, cs.mode, box_bytes, cs.batch, rounds, N * H * W, cs.box_rows, cs.issuers, cyc, W);
         cudaEventRecord(e1);
         cudaError_t err = cudaDeviceSynchronize();
         float ms = 0;
@@ -112,7 +111,7 @@ int main() {
         for (auto v : h) avg += v;
         avg /= cs.ctas;
         const double loads = (double)rounds * cs.batch;
-        printf("%-6s %5d %5d %5d %4d %4d %9.3f %9.2f %9.1f %9.1f %s\n", cs.mode ? "im2col" : "tiled", cs.box_rows,
+        printf("W=%3d %-6s %5d %5d %5d %4d %4d %9.3f %9.2f %9.1f %9.1f %s\n", cs.W, cs.mode ? "im2col" : "tiled", cs.box_rows,
                cs.row_bytes, cs.batch, cs.issuers, cs.ctas, ms, cs.ctas * loads * box_bytes / ms / 1e9,
                loads * box_bytes / avg, avg / loads, err == cudaSuccess ? "" : cudaGetErrorString(err));
     }
