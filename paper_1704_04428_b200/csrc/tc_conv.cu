@@ -119,35 +119,29 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     const int grid = units * cg;
     if (!p.partials || !p.flags) throw Error(6, "stream-K scratch missing");
     CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));
-    // Cooperative launch: the fixup makes CTAs wait on each other, so all must be resident.
+    // The stream-K fixup makes CTAs wait on each other, so all must be resident: grid <= one
+    // CTA per SM at 1 CTA/SM (smem-limited).  CG = 1 additionally asks for a cooperative launch;
+    // CG = 2 uses a plain cluster launch (cooperative + cluster is rejected under ncu).  A CTA
+    // that could never be scheduled would trip the 4 s watchdog (launch error, not a hang).
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    int na = 0;
-    attr[na].id = cudaLaunchAttributeCooperative;
-    attr[na].val.cooperative = 1;
-    ++na;
+    cudaLaunchAttribute attr[1];
     if (cg == 2) {
-        attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = 2;
-        attr[na].val.clusterDim.y = 1;
-        attr[na].val.clusterDim.z = 1;
-        ++na;
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
     }
     cfg.attrs = attr;
-    cfg.numAttrs = na;
+    cfg.numAttrs = 1;
     cudaError_t e = cg == 2 ? cudaLaunchKernelEx(&cfg, tc_conv_kernel<2>, ma, mb, p)
                             : cudaLaunchKernelEx(&cfg, tc_conv_kernel<1>, ma, mb, p);
-    if (e != cudaSuccess && cg == 2) {
-        // clusters + cooperative not accepted: grid = one pair per SM pair is still all-resident
-        cudaGetLastError();
-        cfg.attrs = attr + 1;
-        cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, tc_conv_kernel<2>, ma, mb, p);
-    }
     CLB_CUDA(e);
 }
 

@@ -226,7 +226,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], CG * kEpiThreads);
+            mbar_init(&tempty[a], CG * (kEpiThreads / 32));
         }
         fence_barrier_init();
     }
@@ -256,7 +256,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer ----
-        if (lane_id() == 0) {
+        // whole warp runs the (uniform) loop; one elected lane issues the TMA
+        {
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t tx = (uint32_t)(CG * stage_bytes);   // both CTAs' bytes land on the leader
@@ -278,6 +279,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     const int kc = kb * kRowWords;
                     mbar_wait(&empty[stage], phase ^ 1u);
                     uint8_t* a_st = smem + stage * stage_bytes;
+                    if (elect_one()) {
                     if constexpr (CG == 2) {
                         const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
                         if (leader) mbar_arrive_expect_tx(&full[stage], tx);
@@ -295,6 +297,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
                         load_operand(&map_b, cb, &full[stage], a_st + a_bytes, kc, tap, ti, tj);
                     }
+                    }
+                    __syncwarp();
                     if (++stage == stages) {
                         stage = 0;
                         phase ^= 1u;
@@ -317,7 +321,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // Tensor-core accumulation rounds every update of the running fp32 accumulator
         // (error grows ~linearly in K: 7e-9 K measured), so bounding the chunk to 128
         // K-elements keeps the 3xTF32 result fp32-faithful for any K.
-        if (lane_id() == 0 && leader) {
+        // The whole warp runs the loop (loop state is warp-uniform, so it lives in uniform
+        // registers); one elected lane issues the MMAs and the commits that track them.
+        if (leader) {
             const uint32_t idesc = idesc_tf32((uint32_t)tile_m, (uint32_t)bn);
             int stage = 0;
             uint32_t phase = 0;
@@ -332,6 +338,12 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 if constexpr (CG == 2) mma_commit_2sm_mc(bar, (uint16_t)0x3);
                 else mma_commit(bar);
             };
+            // Descriptors are built once: the start-address field is the low 14 bits (addr >> 4),
+            // so stage / k-step / hi-lo offsets are plain adds on the 64-bit descriptor.  (Building
+            // 4 descriptors per MMA made the single issuing thread slower than an N=192 MMA.)
+            const uint64_t desc0 = umma_desc_kmajor(smem_u32(smem), kRowBytes);
+            const uint64_t st_step = (uint64_t)(stage_bytes >> 4);
+            const uint64_t b_off = (uint64_t)(a_bytes >> 4);
             while (sch.next(pc))
             for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
                 const int c0 = c * ci;
@@ -343,37 +355,35 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 for (int it = c0; it < c1; ++it) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t a_st = smem_u32(smem + stage * stage_bytes);
-                    const uint32_t b_st = a_st + a_bytes;
+                    const uint64_t da = desc0 + (uint64_t)stage * st_step;
+                    const uint64_t db = da + b_off;
+                    const uint32_t first = it > c0 ? 1u : 0u;
+                    if (elect_one()) {
                     if (planes == 2) {
-                        // row = [hi 16 | lo 16]: k-step s (8 tf32 = 32 B) of hi at 32 s, of lo at 64 + 32 s
-#pragma unroll
-                        for (int ks = 0; ks < 2; ++ks) {
-                            const uint32_t off = ks * 32;
-                            const uint64_t dah = umma_desc_kmajor(a_st + off, kRowBytes);
-                            const uint64_t dbh = umma_desc_kmajor(b_st + off, kRowBytes);
-                            const uint64_t dal = umma_desc_kmajor(a_st + 64 + off, kRowBytes);
-                            const uint64_t dbl = umma_desc_kmajor(b_st + 64 + off, kRowBytes);
-                            const uint32_t accum = (it > c0 || ks > 0) ? 1u : 0u;
-                            mma(d_tmem, dal, dbh, accum);   // small cross terms first
-                            mma(d_tmem, dah, dbl, 1u);
-                            mma(d_tmem, dah, dbh, 1u);
-                        }
+                        // row = [hi 16 | lo 16]: k-step s (8 tf32 = 32 B = 2 desc units) of hi at
+                        // +2 s, of lo at +4 + 2 s; small cross terms first
+                        mma(d_tmem, da + 4, db, first);
+                        mma(d_tmem, da, db + 4, 1u);
+                        mma(d_tmem, da, db, 1u);
+                        mma(d_tmem, da + 6, db + 2, 1u);
+                        mma(d_tmem, da + 2, db + 6, 1u);
+                        mma(d_tmem, da + 2, db + 2, 1u);
                     } else {
-#pragma unroll
-                        for (int ks = 0; ks < 4; ++ks) {
-                            const uint32_t off = ks * 32;
-                            mma(d_tmem, umma_desc_kmajor(a_st + off, kRowBytes), umma_desc_kmajor(b_st + off, kRowBytes),
-                                (it > c0 || ks > 0) ? 1u : 0u);
-                        }
+                        mma(d_tmem, da, db, first);
+                        mma(d_tmem, da + 2, db + 2, 1u);
+                        mma(d_tmem, da + 4, db + 4, 1u);
+                        mma(d_tmem, da + 6, db + 6, 1u);
                     }
                     commit(&empty[stage]);          // frees the smem stage(s) once these MMAs retire
+                    }
+                    __syncwarp();
                     if (++stage == stages) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
-                commit(&tfull[buf]);                // chunk complete -> epilogue(s)
+                if (elect_one()) commit(&tfull[buf]);   // chunk complete -> epilogue(s)
+                __syncwarp();
             }
         }
     } else if (warp >= 4) {
@@ -418,8 +428,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             for (int j = 0; j < 16; ++j) sum[(grp + q) * 16 + j] += __uint_as_float(r[q][j]);
                 }
                 tc_fence_before();
-                if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[buf]), 0));
-                else mbar_arrive(&tempty[buf]);
+                __syncwarp();
+                if (lane == 0) {   // one arrive per epilogue warp (count = CG x 8)
+                    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[buf]), 0));
+                    else mbar_arrive(&tempty[buf]);
+                }
             }
             if (pc.c_lo > 0) {
                 // ---- tile tail handled by this CTA: publish the partial for the finisher ----
