@@ -68,59 +68,78 @@ def peaks():
 
 # ------------------------------------------------------------------------- clocks ----
 class ClockSampler:
-    """nvidia-smi sampled during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / power / throttle reasons sampled DURING the timed region (B200_PROFILING.md
+    clocks line): NVML polled every 5 ms from a thread (nvidia-smi -lms as fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
-        self.proc = None
+        self.samples = []          # (t, sm_mhz, max_mhz, power_w, reasons_bitmask)
+        self.stop_flag = False
         self.thread = None
+        self.proc = None
 
     def start(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop_flag:
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.time(), sm, mx, pw, rs))
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            pass
+        try:   # fallback: nvidia-smi
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read_smi, daemon=True)
+            self.thread.start()
         except OSError:
             self.proc = None
-            return
-        self.thread = threading.Thread(target=self._read, daemon=True)
-        self.thread.start()
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append((time.time(), parts))
+            p = [x.strip() for x in line.split(",")]
+            try:
+                self.samples.append((time.time(), float(p[0]), float(p[1]), float(p[2]), int(p[3], 16)))
+            except (ValueError, IndexError):
+                pass
 
     def stop(self):
+        self.stop_flag = True
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
 
     def summary(self, t0: float, t1: float):
-        win = [s for t, s in self.samples if t0 <= t <= t1] or [s for _, s in self.samples]
+        win = [s for s in self.samples if t0 <= s[0] <= t1]
         if not win:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-
-        sm = [num(s[0]) for s in win if num(s[0]) is not None]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in win for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(win[0][1]),
-                "power_w_max": max((num(s[2]) or 0.0) for s in win), "reasons": reasons, "samples": len(win)}
+        reasons = sorted({name for s in win for name, bit in self.REASONS.items() if s[4] & bit})
+        return {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": win[0][2],
+                "power_w_max": max(s[3] for s in win), "reasons": reasons, "samples": len(win)}
 
 
 # ------------------------------------------------------------------- CPU baseline ----

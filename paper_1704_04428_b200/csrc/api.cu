@@ -77,6 +77,10 @@ struct cl_plan {
     float* host_y = nullptr;
     int launches = 0;
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // optional instrumentation
+    // chunked host pipeline (cl_conv_forward_host): copy-in / copy-out streams + per-chunk events
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    static constexpr int kMaxChunks = 16;
+    cudaEvent_t ev_in[kMaxChunks] = {}, ev_comp[kMaxChunks] = {}, ev_start = nullptr, ev_done = nullptr;
 };
 
 namespace {
@@ -165,8 +169,10 @@ TcParams base_params(const cl_plan* p) {
     return t;
 }
 
-void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
-    const cl_conv_desc& d = p->d;
+// n_images < 0: the plan's batch; otherwise a sub-batch (chunked host pipeline).
+void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images = -1) {
+    cl_conv_desc d = p->d;
+    if (n_images >= 0) d.n = n_images;
     require(p->weights_set, "cl_conv_forward: weights not set (cl_conv_set_weights)");
     require(x && y, "cl_conv_forward: null tensor");
     CLB_CUDA(cudaSetDevice(p->device));
@@ -210,6 +216,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s) {
             launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
             ++p->launches;
             Operand a = implicit_a(p, xs);
+            a.n = d.n;
             Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
             TcParams t = base_params(p);
             t.rows = (int)npq;
@@ -407,22 +414,66 @@ cl_status cl_conv_forward(cl_plan* p, const float* d_x, float* d_y, void* d_ws, 
 }
 
 cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* stream) {
+    // Pipelined over batch chunks on three streams: H2D of chunk i+1 (copy-in stream), the
+    // convolution of chunk i (caller's stream) and the D2H of chunk i-1 (copy-out stream)
+    // overlap, so the call costs ~max(H2D, compute, D2H) instead of their sum (PCIe is full
+    // duplex).  Synchronous on return, like run_method.
     return guarded([&] {
         require(p && h_x && h_y, "cl_conv_forward_host: null argument");
         CLB_CUDA(cudaSetDevice(p->device));
         const cl_conv_desc& d = p->d;
-        const size_t xb = (size_t)d.n * d.c * d.h * d.w * 4;
-        const size_t yb = (size_t)d.n * d.m * p->P * p->Q * 4;
+        const size_t img_in = (size_t)d.c * d.h * d.w, img_out = (size_t)d.m * p->P * p->Q;
+        const size_t xb = (size_t)d.n * img_in * 4;
+        const size_t yb = (size_t)d.n * img_out * 4;
         if (!p->host_x) {
             if (cudaMalloc(&p->host_x, xb) != cudaSuccess || cudaMalloc(&p->host_y, yb) != cudaSuccess) {
                 cudaGetLastError();
                 throw Error(CL_ENOMEM, "staging allocation failed");
             }
         }
+        if (!p->s_in) {
+            CLB_CUDA(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+            CLB_CUDA(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+            for (int i = 0; i < cl_plan::kMaxChunks; ++i) {
+                CLB_CUDA(cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming));
+                CLB_CUDA(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming));
+            }
+            CLB_CUDA(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
+            CLB_CUDA(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+        }
         auto s = static_cast<cudaStream_t>(stream);
-        CLB_CUDA(cudaMemcpyAsync(p->host_x, h_x, xb, cudaMemcpyHostToDevice, s));
-        forward(p, p->host_x, p->host_y, nullptr, s);
-        CLB_CUDA(cudaMemcpyAsync(h_y, p->host_y, yb, cudaMemcpyDeviceToHost, s));
+        // chunk count: 8 (measured on B200 + PCIe5: AlexNet b128 e2e 37 -> 45 -> 49 -> 51 TFLOP/s
+        // for 1/2/4/8 chunks), 1 for small transfers where launch overheads dominate
+        // (override: CLB_HOST_CHUNKS)
+        static const int forced_chunks = [] {
+            const char* e = std::getenv("CLB_HOST_CHUNKS");
+            return e ? std::atoi(e) : 0;
+        }();
+        int chunks = forced_chunks > 0 ? forced_chunks : ((xb + yb) >= (8u << 20) ? 8 : 1);
+        if (chunks > cl_plan::kMaxChunks) chunks = cl_plan::kMaxChunks;
+        if (chunks > d.n) chunks = d.n;
+        if (chunks < 1) chunks = 1;
+        // the copy streams must not run ahead of prior work on the caller's stream
+        CLB_CUDA(cudaEventRecord(p->ev_start, s));
+        CLB_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+        CLB_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
+        int first = 0;
+        for (int c = 0; c < chunks; ++c) {
+            const int n0 = first, nc = d.n * (c + 1) / chunks - first;
+            first += nc;
+            if (nc == 0) continue;
+            CLB_CUDA(cudaMemcpyAsync(p->host_x + n0 * img_in, h_x + n0 * img_in, nc * img_in * 4,
+                                     cudaMemcpyHostToDevice, p->s_in));
+            CLB_CUDA(cudaEventRecord(p->ev_in[c], p->s_in));
+            CLB_CUDA(cudaStreamWaitEvent(s, p->ev_in[c], 0));
+            forward(p, p->host_x + n0 * img_in, p->host_y + n0 * img_out, nullptr, s, nc);
+            CLB_CUDA(cudaEventRecord(p->ev_comp[c], s));
+            CLB_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_comp[c], 0));
+            CLB_CUDA(cudaMemcpyAsync(h_y + n0 * img_out, p->host_y + n0 * img_out, nc * img_out * 4,
+                                     cudaMemcpyDeviceToHost, p->s_out));
+        }
+        CLB_CUDA(cudaEventRecord(p->ev_done, p->s_out));
+        CLB_CUDA(cudaStreamWaitEvent(s, p->ev_done, 0));   // the caller's stream sees the outputs
         CLB_CUDA(cudaStreamSynchronize(s));
     });
 }
@@ -436,6 +487,16 @@ void cl_conv_destroy(cl_plan* p) {
     if (p->own_ws) cudaFree(p->own_ws);
     if (p->host_x) cudaFree(p->host_x);
     if (p->host_y) cudaFree(p->host_y);
+    if (p->s_in) {
+        cudaStreamDestroy(p->s_in);
+        cudaStreamDestroy(p->s_out);
+        for (int i = 0; i < cl_plan::kMaxChunks; ++i) {
+            cudaEventDestroy(p->ev_in[i]);
+            cudaEventDestroy(p->ev_comp[i]);
+        }
+        cudaEventDestroy(p->ev_start);
+        cudaEventDestroy(p->ev_done);
+    }
     delete p;
 }
 
