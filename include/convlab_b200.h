@@ -60,7 +60,8 @@ typedef enum cl_method {
     CL_METHOD_KN2COL = 3,        /* transposed: one (NHW x C).(C x k^2 M) GEMM + column shift-add      */
     CL_METHOD_KN2ROW_ACC = 4,    /* accumulating: k^2 shifted GEMM launches summing into the output    */
     CL_METHOD_IM2COL = 5,        /* baseline: patch matrix (NHW x k^2 C) + one GEMM                     */
-    CL_METHOD_CONV1X1 = 6        /* k == 1 only (CL_EINVAL otherwise, methods.cpp:81-85)                */
+    CL_METHOD_CONV1X1 = 6,       /* k == 1 only (CL_EINVAL otherwise, methods.cpp:81-85)                */
+    CL_METHOD_DIRECT = 7         /* fp32 CUDA-core direct loop nest for tiny-C layers (conv_direct.cpp:104-143) */
 } cl_method;
 
 typedef enum cl_precision {

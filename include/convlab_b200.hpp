@@ -43,6 +43,7 @@ enum class ConvMethod {
     Im2colGpu,
     Conv1x1Gpu,
     Auto,
+    DirectGpu,          // fp32 CUDA-core direct loop nest (tiny-C first layers)
 };
 
 enum class Precision { Fp32, Tf32 };

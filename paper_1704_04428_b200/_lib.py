@@ -22,6 +22,7 @@ METHODS = {
     "kn2row-acc-gpu": 4,
     "im2col-gpu": 5,
     "conv1x1-gpu": 6,
+    "direct-gpu": 7,
 }
 METHOD_NAMES = {v: k for k, v in METHODS.items()}
 # cl_precision

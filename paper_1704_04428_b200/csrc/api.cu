@@ -70,6 +70,7 @@ struct cl_plan {
     int bn = 0;
     float* wpack = nullptr;
     size_t wpack_bytes = 0;
+    float* wraw = nullptr;     // direct-gpu: MKKC fp32 weights as given
     bool weights_set = false;
     void* own_ws = nullptr;
     size_t own_ws_bytes = 0;
@@ -88,9 +89,10 @@ namespace {
 cl_method resolve(const cl_conv_desc& d, cl_method m) {
     if (m != CL_METHOD_AUTO) return m;
     // Per-layer selector.  The implicit kernel is the default; tiny-C first layers (VGG
-    // conv1_1, C = 3) waste 13/16 of every 16-channel K block per tap, while im2col packs
-    // all k^2 C taps densely into K (27 -> 32), so it wins there (PAPER.md:484 found a
-    // non-kn2 method best on that layer too).
+    // conv1_1, C = 3) waste 13/16 of every 16-channel K block per tap and are HBM-bound, so
+    // they take the direct CUDA-core kernel (PAPER.md:484 found direct best on that layer
+    // too); im2col remains for small C the direct kernel cannot stage.
+    if (d.c <= 4 && d.stride == 1 && d.k <= 11) return CL_METHOD_DIRECT;
     if (d.k > 1 && d.c * 4 <= 16) return CL_METHOD_IM2COL;
     return CL_METHOD_KN2ROW;
 }
@@ -118,6 +120,8 @@ size_t method_ws_bytes(const cl_plan* p) {
             return xs + kk * d.m * nhw * 4;
         case CL_METHOD_IM2COL:
             return npq * p->planes * p->Kp * 4;
+        case CL_METHOD_DIRECT:
+            return 0;
         default:
             return 0;
     }
@@ -296,6 +300,14 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             tc_done();
             break;
         }
+        case CL_METHOD_DIRECT: {
+            // the dominant (and only) kernel of this method: bracket it for the profile events
+            if (p->ev_begin) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
+            launch_direct_conv(x, p->wraw, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, p->P, p->Q, s);
+            ++p->launches;
+            tc_done();
+            break;
+        }
         default:
             throw Error(CL_EINTERNAL, "unresolved method");
     }
@@ -329,7 +341,11 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         require(P > 0 && Q > 0, "cl_conv_plan: empty output");
         cl_method m = resolve(d, method);
         if (d.k == 1 && (m == CL_METHOD_KN2ROW_EXPLICIT || m == CL_METHOD_KN2COL)) m = CL_METHOD_CONV1X1;
-        if (m != CL_METHOD_IM2COL) {
+        if (m == CL_METHOD_DIRECT) {
+            if (d.stride != 1) throw Error(CL_EUNSUPPORTED, "direct-gpu supports stride 1 only");
+            if (d.k > 11 || direct_smem_bytes(d.c, d.k) > 200 * 1024)
+                throw Error(CL_EUNSUPPORTED, "direct-gpu is for small C (shared-memory halo) and k <= 11");
+        } else if (m != CL_METHOD_IM2COL) {
             if (d.stride != 1) throw Error(CL_EUNSUPPORTED, "kn2 methods support stride 1 only (im2col supports stride)");
             if (d.pad > 127 || d.k - 1 - d.pad > 128)
                 throw Error(CL_EUNSUPPORTED, "padding outside the TMA im2col bounding-box range");
@@ -351,12 +367,14 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         p->Kp = round_up(d.k * d.k * d.c, k_granule(p->planes));
         p->bn = bn_for(d.m);
         if (m == CL_METHOD_IM2COL) p->wpack_bytes = (size_t)d.m * p->planes * p->Kp * 4;
+        else if (m == CL_METHOD_DIRECT) p->wpack_bytes = (size_t)d.m * d.k * d.k * d.c * 4;
         else p->wpack_bytes = (size_t)d.k * d.k * d.m * p->planes * p->Cp * 4;
         if (cudaMalloc(&p->wpack, p->wpack_bytes) != cudaSuccess) {
             cudaGetLastError();
             delete p;
             throw Error(CL_ENOMEM, "packed-weight allocation failed");
         }
+        if (m == CL_METHOD_DIRECT) p->wraw = p->wpack;
         *out_plan = p;
     });
 }
@@ -369,6 +387,8 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
         const cl_conv_desc& d = p->d;
         if (p->method == CL_METHOD_IM2COL)
             launch_rows_split(d_w, p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);   // MKKC == M x k^2C
+        else if (p->method == CL_METHOD_DIRECT)
+            CLB_CUDA(cudaMemcpyAsync(p->wpack, d_w, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
         else
             launch_pack_weights(d_w, p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s);
         p->weights_set = true;
@@ -387,6 +407,8 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
         const cl_conv_desc& d = p->d;
         if (p->method == CL_METHOD_IM2COL)
             launch_rows_split(static_cast<float*>(dw), p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);
+        else if (p->method == CL_METHOD_DIRECT)
+            CLB_CUDA(cudaMemcpyAsync(p->wpack, dw, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
         else
             launch_pack_weights(static_cast<float*>(dw), p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s);
         CLB_CUDA(cudaFreeAsync(dw, s));
@@ -580,13 +602,14 @@ const char* cl_method_name(cl_method m) {
         case CL_METHOD_KN2ROW_ACC: return "kn2row-acc-gpu";
         case CL_METHOD_IM2COL: return "im2col-gpu";
         case CL_METHOD_CONV1X1: return "conv1x1-gpu";
+        case CL_METHOD_DIRECT: return "direct-gpu";
     }
     return "unknown";
 }
 
 int cl_method_from_name(const char* name, cl_method* out) {
     if (!name || !out) return 0;
-    for (int m = CL_METHOD_AUTO; m <= CL_METHOD_CONV1X1; ++m) {
+    for (int m = CL_METHOD_AUTO; m <= CL_METHOD_DIRECT; ++m) {
         if (std::strcmp(name, cl_method_name((cl_method)m)) == 0) {
             *out = (cl_method)m;
             return 1;

@@ -32,6 +32,7 @@ constexpr NameEntry kNames[] = {
     {ConvMethod::Im2colGpu, "im2col-gpu"},
     {ConvMethod::Conv1x1Gpu, "conv1x1-gpu"},
     {ConvMethod::Auto, "auto"},
+    {ConvMethod::DirectGpu, "direct-gpu"},
 };
 
 void check(cl_status s) {
@@ -50,6 +51,7 @@ cl_method to_cl(ConvMethod m) {
         case ConvMethod::Im2colGpu: return CL_METHOD_IM2COL;
         case ConvMethod::Conv1x1Gpu: return CL_METHOD_CONV1X1;
         case ConvMethod::Auto: return CL_METHOD_AUTO;
+        case ConvMethod::DirectGpu: return CL_METHOD_DIRECT;
         default:
             throw std::invalid_argument("method '" + std::string(to_string(m)) +
                                         "' is a reference CPU method; the B200 path runs GPU methods only");
@@ -64,6 +66,7 @@ ConvMethod from_cl(cl_method m) {
         case CL_METHOD_KN2ROW_ACC: return ConvMethod::Kn2rowAccGpu;
         case CL_METHOD_IM2COL: return ConvMethod::Im2colGpu;
         case CL_METHOD_CONV1X1: return ConvMethod::Conv1x1Gpu;
+        case CL_METHOD_DIRECT: return ConvMethod::DirectGpu;
         default: return ConvMethod::Auto;
     }
 }
@@ -117,12 +120,12 @@ CLB_EXPORT std::vector<ConvMethod> parse_method_list(std::string_view csv) {
 
 CLB_EXPORT bool method_requires_1x1(ConvMethod m) { return m == ConvMethod::Conv1x1 || m == ConvMethod::Conv1x1Gpu; }
 
-CLB_EXPORT bool is_gpu_method(ConvMethod m) { return static_cast<int>(m) >= static_cast<int>(ConvMethod::Kn2rowGpu); }
+CLB_EXPORT bool is_gpu_method(ConvMethod m) { return static_cast<int>(m) >= static_cast<int>(ConvMethod::Kn2rowGpu); }  // incl. Auto, DirectGpu
 
 CLB_EXPORT const std::vector<ConvMethod>& default_gpu_methods() {
     static const std::vector<ConvMethod> all = {ConvMethod::Kn2rowGpu, ConvMethod::Kn2rowExplicitGpu,
                                                 ConvMethod::Kn2colGpu, ConvMethod::Kn2rowAccGpu,
-                                                ConvMethod::Im2colGpu};
+                                                ConvMethod::Im2colGpu, ConvMethod::DirectGpu};
     return all;
 }
 

@@ -23,7 +23,8 @@ from . import _lib
 # Reference method names in canonical order (methods.cpp:11-41) -- CPU, reference-only.
 REFERENCE_METHODS = ["direct-sum", "direct-loopnest", "im2col", "im2row", "kn2row", "kn2col", "conv1x1"]
 # GPU methods of this package (the -gpu suffix of SURVEY.md 8b) plus the selector.
-GPU_METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu", "conv1x1-gpu"]
+GPU_METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu", "conv1x1-gpu",
+               "direct-gpu"]
 ALL_METHODS = REFERENCE_METHODS + GPU_METHODS + ["auto"]
 PRECISIONS = ("fp32", "tf32")
 

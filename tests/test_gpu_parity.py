@@ -15,7 +15,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 FP32_L2, FP32_MAX, TF32_L2 = 1e-5, 1e-4, 1e-2
-METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu"]
+METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu", "direct-gpu"]
 
 
 @pytest.fixture(scope="module")
@@ -111,6 +111,17 @@ def test_baseline_shapes_implicit(oracle, clb, torch_cuda, shape):
     _check_fp32(oracle, y, ref, f"auto {shape}")
 
 
+def test_selector_picks_direct_for_tiny_c(oracle, clb, torch_cuda):
+    """auto: C <= 4 -> direct-gpu (VGG conv1_1 shape class), otherwise the implicit kernel."""
+    with clb.ConvPlan(clb.LayerConfig("c3", 3, 32, 32, 64, 3, batch=2), "auto") as plan:
+        assert plan.method == "direct-gpu"
+    with clb.ConvPlan(clb.LayerConfig("c64", 64, 32, 32, 64, 3, batch=2), "auto") as plan:
+        assert plan.method == "kn2row-gpu"
+    for k in (1, 3, 5, 7):   # compile-time and runtime tap paths
+        x, w = oracle.make_problem(2, 3, 19, 23, 20, k, k)
+        _check_fp32(oracle, _run(clb, torch_cuda, "direct-gpu", x, w), oracle.conv_batch(x, w), f"direct k={k}")
+
+
 def test_tf32_fast_mode(oracle, clb, torch_cuda):
     x, w = oracle.make_problem(2, 64, 20, 20, 96, 3, 3)
     ref = oracle.conv_batch(x, w)
@@ -170,7 +181,8 @@ def test_one_contraction_per_call(oracle, clb, torch_cuda):
     torch = torch_cuda
     layer = clb.LayerConfig("l", 3, 6, 6, 2, 3, batch=1)
     x, w = oracle.make_problem(1, 3, 6, 6, 2, 3, 140)
-    expect = {"kn2row-gpu": 2, "kn2row-explicit-gpu": 3, "kn2col-gpu": 3, "im2col-gpu": 2, "kn2row-acc-gpu": 10}
+    expect = {"kn2row-gpu": 2, "kn2row-explicit-gpu": 3, "kn2col-gpu": 3, "im2col-gpu": 2, "kn2row-acc-gpu": 10,
+              "direct-gpu": 1}
     for method, n in expect.items():
         with clb.ConvPlan(layer, method) as plan:
             plan.set_weights(torch.from_numpy(w).cuda())
@@ -228,6 +240,8 @@ def test_run_to_run_bitwise_determinism(oracle, clb, torch_cuda):
     torch = torch_cuda
     x, w = oracle.make_problem(4, 64, 28, 28, 128, 3, 5)
     for method in METHODS:
+        if method == "direct-gpu":   # tiny-C kernel: C=64 exceeds its shared-memory halo
+            continue
         a = _run(clb, torch, method, x, w)
         b = _run(clb, torch, method, x, w)
         assert oracle.fnv1a(a) == oracle.fnv1a(b), method
