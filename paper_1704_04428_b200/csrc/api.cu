@@ -71,6 +71,7 @@ struct cl_plan {
     float* wpack = nullptr;
     size_t wpack_bytes = 0;
     float* wraw = nullptr;     // direct-gpu: MKKC fp32 weights as given
+    unsigned* flags = nullptr; // stream-K fixup flags, zeroed once, self-resetting
     bool weights_set = false;
     void* own_ws = nullptr;
     size_t own_ws_bytes = 0;
@@ -202,9 +203,15 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
     bool began = false;
     void* scratch = scratch_of(p, ws);
     auto tc = [&](const Operand& a, const Operand& b, TcParams t) {
+        // PDL right after the prepass kernel (its launch_dependents trigger lets this
+        // kernel's prologue overlap the prepass tail); an interposed profile event only
+        // removes the overlap, never the ordering
+        t.pdl = !began ? 1 : 0;
         if (p->ev_begin && !began) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
         began = true;
         set_scratch(t, scratch);
+        t.flags = p->flags;
+        t.flags_zeroed = 1;
         launch_tc(a, b, t, s, cta_group_for(t.rows));
         ++p->launches;
     };
@@ -375,6 +382,13 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             throw Error(CL_ENOMEM, "packed-weight allocation failed");
         }
         if (m == CL_METHOD_DIRECT) p->wraw = p->wpack;
+        if (cudaMalloc(&p->flags, kMaxGrid * sizeof(unsigned)) != cudaSuccess ||
+            cudaMemset(p->flags, 0, kMaxGrid * sizeof(unsigned)) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(p->wpack);
+            delete p;
+            throw Error(CL_ENOMEM, "flag allocation failed");
+        }
         *out_plan = p;
     });
 }
@@ -506,6 +520,7 @@ void cl_conv_destroy(cl_plan* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     if (p->wpack) cudaFree(p->wpack);
+    if (p->flags) cudaFree(p->flags);
     if (p->own_ws) cudaFree(p->own_ws);
     if (p->host_x) cudaFree(p->host_x);
     if (p->host_y) cudaFree(p->host_y);

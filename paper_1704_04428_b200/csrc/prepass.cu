@@ -72,6 +72,9 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
             }
         }
     }
+    // let a programmatically dependent consumer (the tcgen05 kernel) start its prologue;
+    // its griddepcontrol.wait still waits for this grid's completion and memory flush
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 void launch_nchw_to_nhwc_split(const float* x, float* xs, int N, int C, int HW, int Cp, int planes,

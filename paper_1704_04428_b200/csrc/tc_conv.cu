@@ -118,7 +118,9 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     p.sk_chunks = (p.num_tiles - p.dp_tiles) * p.chunks_per_tile;
     const int grid = units * cg;
     if (!p.partials || !p.flags) throw Error(6, "stream-K scratch missing");
-    CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));
+    if (!p.flags_zeroed) CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));
+    // PDL only when nothing was enqueued in between (the memset would be the predecessor)
+    if (!p.flags_zeroed) p.pdl = 0;
     // The stream-K fixup makes CTAs wait on each other, so all must be resident: grid <= one
     // CTA per SM at 1 CTA/SM (smem-limited).  CG = 1 additionally asks for a cooperative launch;
     // CG = 2 uses a plain cluster launch (cooperative + cluster is rejected under ncu).  A CTA
@@ -128,18 +130,26 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
+    int na = 0;
     if (cg == 2) {
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 2;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
     } else {
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+    }
+    if (p.pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
     }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     cudaError_t e = cg == 2 ? cudaLaunchKernelEx(&cfg, tc_conv_kernel<2>, ma, mb, p)
                             : cudaLaunchKernelEx(&cfg, tc_conv_kernel<1>, ma, mb, p);
     CLB_CUDA(e);

@@ -78,7 +78,9 @@ struct TcParams {
     int dp_tiles;              // tiles [0, dp_tiles) scheduled whole, round-robin over CTAs
     int sk_chunks;             // chunks of tiles [dp_tiles, num_tiles), split contiguously (stream-K)
     float* partials;           // [gridDim.x][128][bn] tile-tail partial sums
-    unsigned* flags;           // [gridDim.x], zeroed before the launch; 1 = partial ready
+    unsigned* flags;           // [gridDim.x], 0 at launch; 1 = partial ready (the finisher resets it)
+    int flags_zeroed;          // flags are known to be 0 (self-resetting plan buffer): no memset
+    int pdl;                   // launched as a programmatic dependent: wait before touching inputs
 };
 
 // Contiguous chunk range of CTA b: [chunk_start(b), chunk_start(b+1)).
@@ -252,6 +254,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int k_iters = p.taps * p.kblocks;
     const int cpt = p.chunks_per_tile;
     const int ci = p.chunk_iters;
+
+    // Programmatic dependent launch: everything above (barrier init, TMEM alloc, descriptor
+    // prefetch) overlapped the previous kernel's tail; inputs (the split operand, output
+    // buffers) are only touched after this point.
+    if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0) {
@@ -464,6 +471,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             sum[j + 2] += v.z;
                             sum[j + 3] += v.w;
                         }
+                    // every published partial has exactly one finisher: reset its flag so the
+                    // buffer is clean for the next launch (no memset launch needed)
+                    epi_bar_sync();
+                    if (threadIdx.x == 4 * 32) p.flags[slot] = 0u;
                 }
             }
             // ---- store the finished tile ----
