@@ -39,13 +39,16 @@ void require(bool ok, const std::string& what) {
 
 // CTA group of the tcgen05 engine: 2 (CTA pair, M = 256) unless CLB_CTA_GROUP=1 (A/B switch
 // for measurements) or the problem has fewer than 256 rows.
-int cta_group_for(long long rows) {
+int cta_group_for(long long rows, int cols, int bn) {
     static int forced = [] {
         const char* e = std::getenv("CLB_CTA_GROUP");
         return e ? std::atoi(e) : 0;
     }();
     if (forced == 1 || forced == 2) return forced;
-    return rows >= 256 ? 2 : 1;
+    // pairs need at least one wave of 256-row tiles to pay off; small problems want more,
+    // smaller (128-row) tiles instead
+    const long long pair_tiles = (rows + 255) / 256 * ((cols + bn - 1) / bn);
+    return (rows >= 256 && pair_tiles >= num_sms() / 2) ? 2 : 1;
 }
 
 int bn_for(int cols) {
@@ -212,7 +215,12 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         set_scratch(t, scratch);
         t.flags = p->flags;
         t.flags_zeroed = 1;
-        launch_tc(a, b, t, s, cta_group_for(t.rows));
+        const int cg = cta_group_for(t.rows, t.cols, t.bn);
+        // few tiles even at 128 rows: halve the tile N to create more of them (B operand rows
+        // are tiny anyway at these sizes)
+        if (cg == 1 && t.bn >= 64 && (long long)(t.rows + 127) / 128 * ((t.cols + t.bn - 1) / t.bn) < num_sms() / 2)
+            t.bn = round_up(t.bn / 2, 16);
+        launch_tc(a, b, t, s, cg);
         ++p->launches;
     };
     auto tc_done = [&] {
@@ -577,7 +585,7 @@ cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float
         t.out = c;
         t.ld = n;
         set_scratch(t, static_cast<char*>(ws) + align256((size_t)(m + n) * planes * kp * 4));
-        launch_tc(tiled(as, m, 1, kp, planes), tiled(bs, n, 1, kp, planes), t, s, cta_group_for(m));
+        launch_tc(tiled(as, m, 1, kp, planes), tiled(bs, n, 1, kp, planes), t, s, cta_group_for(m, n, t.bn));
         if (own) CLB_CUDA(cudaFreeAsync(own, s));
     });
 }

@@ -109,6 +109,9 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     const int sms = num_sms();
     int units = (sms < kMaxGrid ? sms : kMaxGrid) / cg;      // scheduling units (CTAs or CTA pairs)
     if (total_chunks < units) units = (int)total_chunks;
+    // a split tile is finished by one unit that adds the other pieces' partials serially:
+    // cap the split factor so tiny problems (batch-1 layers) do not drown in fixups
+    if ((long long)units > (long long)p.num_tiles * kMaxSplit) units = p.num_tiles * kMaxSplit;
     // whole-tile waves for all but the last 1-2 waves; stream-K over the rest
     // (a last wave that is >= 95% full stays data-parallel: splitting it costs more than it saves)
     const int waves = p.num_tiles / units;

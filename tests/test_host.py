@@ -173,6 +173,37 @@ dist_.destroy_process_group()
 '''
 
 
+_MSHARD_WORKER = r'''
+import sys, json
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch, torch.distributed as dist_
+from paper_1704_04428_b200 import dist
+from oracle import oracle as O
+info = dist.init("gloo")
+x, w = O.make_problem(2, 3, 6, 5, 7, 3, 4)      # M = 7 over 2 ranks: uneven slices (4 + 3)
+conv = lambda xx, ww: torch.from_numpy(O.conv_batch(xx.numpy(), ww.numpy()))
+y = dist.mshard_conv(torch.from_numpy(x), torch.from_numpy(w), info, conv)
+if info.rank == 0:
+    print(json.dumps({"ok": bool(np.array_equal(y.numpy(), O.conv_batch(x, w))), "shape": list(y.shape)}))
+dist_.destroy_process_group()
+'''
+
+
+def test_two_rank_gloo_channel_sharding(tmp_path):
+    """SURVEY 8(e) output-channel sharding: slices + all-gather + permute == full conv."""
+    import json
+    script = tmp_path / "mshard.py"
+    script.write_text(_MSHARD_WORKER)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29519", str(script), str(ROOT)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=dict(os.environ, OMP_NUM_THREADS="1"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert res == {"ok": True, "shape": [2, 7, 6, 5]}
+    from paper_1704_04428_b200 import dist
+    assert [dist.channel_slice(7, 2, r) for r in (0, 1)] == [(0, 4), (4, 7)]
+
+
 def test_two_rank_gloo_sharding(tmp_path):
     """The N>1 path on CPU: per-rank generation offsets reproduce the global batch,
     MAX/SUM reductions behave, results gather to the single-process answer."""
