@@ -29,44 +29,55 @@ __device__ __forceinline__ void store_split(float* dst, long long base, int c, i
 }
 
 // ------------------------------------------------------------------ NCHW -> NHWC split ----
-// Tile = 32 channels x 64 pixels of one image, 256 threads.  Loads: each warp reads whole
-// 128-byte channel-row segments (coalesced along pixels).  Stores: the tile's output is, per
-// pixel, one contiguous run of 64 words ([hi16|lo16] x 2 for 3xTF32, 32 hi words for TF32),
-// written by a warp as full 128-byte lines (lane = word).  grid (ceil(HW/64), ceil(Cp/32), N)
+// Tile = 32 channels x 128 pixels of one image, 256 threads.  Loads: warp w reads channel
+// rows w, w+8, w+16, w+24 in four 128-byte pieces each -- 16 independent loads in flight per
+// thread (the kernel is HBM-bound; memory-level parallelism is what it needs).  Stores: per
+// pixel the tile's output is one contiguous run of 64 words ([hi16|lo16] x 2 for 3xTF32, 32
+// hi words for TF32), written by a warp as full 128-byte lines (lane = word).
+// grid (ceil(HW/128), ceil(Cp/32), N)
+constexpr int kSplitPx = 128;
+
 __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, float* __restrict__ xs,
                                                                  int C, int HW, int Cp, int planes) {
-    __shared__ float tile[64][33];   // [pixel][channel]
+    __shared__ float tile[kSplitPx][33];   // [pixel][channel]
     const int n = blockIdx.z;
-    const int p0 = blockIdx.x * 64, c0 = blockIdx.y * 32;
+    const int p0 = blockIdx.x * kSplitPx, c0 = blockIdx.y * 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float* xn = x + (long long)n * C * HW;
+    float v[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        const int cc = warp + 8 * r;
-        const int c = c0 + cc;
+        const int c = c0 + warp + 8 * r;
+        const float* row = xn + (long long)c * HW;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 4; ++h) {
             const int pix = p0 + lane + 32 * h;
-            tile[lane + 32 * h][cc] = (c < C && pix < HW) ? __ldg(xn + (long long)c * HW + pix) : 0.0f;
+            v[r][h] = (c < C && pix < HW) ? __ldg(row + pix) : 0.0f;
         }
     }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) tile[lane + 32 * h][warp + 8 * r] = v[r][h];
     __syncthreads();
     const long long row_words = (long long)planes * Cp;
     const int words = planes == 2 ? 64 : 32;            // output words per pixel in this tile
     const int nch = Cp - c0 < 32 ? Cp - c0 : 32;        // channels of this tile inside the padded row
     const int out_words = planes == 2 ? 2 * nch : nch;
-    for (int pp = warp; pp < 64; pp += 8) {
+    for (int pp = warp; pp < kSplitPx; pp += 8) {
         const int pix = p0 + pp;
         if (pix >= HW) break;
         float* dst = xs + ((long long)n * HW + pix) * row_words + (long long)planes * c0;
-        for (int o = lane; o < words; o += 32) {
-            if (o >= out_words) continue;
+#pragma unroll
+        for (int o0 = 0; o0 < 64; o0 += 32) {
+            const int o = o0 + lane;
+            if (o0 >= words || o >= out_words) continue;
             if (planes == 2) {
                 const int u = o >> 5, w = o & 31;            // 16-channel block u of this tile
                 const int cc = u * 16 + (w & 15);
-                const float v = tile[pp][cc];
-                const float hi = tf32_rna(v);
-                dst[o] = (w < 16) ? hi : v - hi;
+                const float val = tile[pp][cc];
+                const float hi = tf32_rna(val);
+                dst[o] = (w < 16) ? hi : val - hi;
             } else {
                 dst[o] = tf32_rna(tile[pp][o]);
             }
@@ -79,7 +90,7 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
 
 void launch_nchw_to_nhwc_split(const float* x, float* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s) {
-    dim3 grid((HW + 63) / 64, (Cp + 31) / 32, N);
+    dim3 grid((HW + kSplitPx - 1) / kSplitPx, (Cp + 31) / 32, N);
     nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, C, HW, Cp, planes);
     CLB_CUDA(cudaGetLastError());
 }
