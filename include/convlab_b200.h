@@ -136,6 +136,10 @@ CL_API cl_status cl_fill_uniform(float* d, uint64_t n, uint64_t seed, uint64_t f
  * caller can time the dominant kernel alone with CUDA events.  NULLs disable. */
 CL_API cl_status cl_conv_set_profile_events(cl_plan* plan, void* ev_begin, void* ev_end);
 
+/* fnv1a over the fp32 bit patterns of a HOST array, bytes low..high (bench.cpp:25-36): the
+ * reference harness's output checksum. */
+CL_API uint64_t cl_checksum_fnv1a(const float* h, uint64_t n);
+
 CL_API const char* cl_last_error(void);
 CL_API const char* cl_method_name(cl_method method);
 CL_API int cl_method_from_name(const char* name, cl_method* out);

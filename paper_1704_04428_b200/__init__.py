@@ -6,6 +6,7 @@ include/convlab_b200.h); this package is its host-side mirror.  Importing it loa
 library and fails loudly when it is missing -- there is no CPU fallback.
 """
 from . import _lib
+from . import harness
 from .methods import (ALL_METHODS, GPU_METHODS, REFERENCE_METHODS, ConvPlan, LayerConfig, footprint, gemm,
                       method_from_name, method_requires_1x1, parse_method_list, parse_network_text, run_method,
                       shift_add_row)

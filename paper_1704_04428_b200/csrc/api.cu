@@ -614,6 +614,19 @@ cl_status cl_conv_set_profile_events(cl_plan* p, void* ev_begin, void* ev_end) {
     return CL_OK;
 }
 
+uint64_t cl_checksum_fnv1a(const float* h, uint64_t n) {
+    uint64_t x = 0xcbf29ce484222325ull;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint32_t bits;
+        std::memcpy(&bits, &h[i], 4);
+        for (int sh = 0; sh < 32; sh += 8) {
+            x ^= (bits >> sh) & 0xffu;
+            x *= 0x100000001b3ull;
+        }
+    }
+    return x;
+}
+
 const char* cl_last_error(void) { return g_err.c_str(); }
 
 const char* cl_method_name(cl_method m) {

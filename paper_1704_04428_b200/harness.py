@@ -1,0 +1,156 @@
+"""Harness mirror for the GPU methods (reference bench.hpp/bench.cpp).
+
+benchmark(layer, method, runs, seed)  <- convlab::benchmark (bench.cpp:87-151):
+    1 untimed warm-up, `runs` timed end-to-end executions of the method (here: the device
+    forward incl. its prepass, CUDA events on the launching stream; input generation and the
+    one-time weight pre-pack excluded -- the north star treats weights as static), mean / min /
+    population stddev, fnv1a checksum of the output (bench.cpp:25-36) and the reference's
+    nondeterminism check on the first timed run (bench.cpp:126-128).
+emit_csv / parse_csv  <- bench.cpp:211-294: the reference's 10 columns first, byte-exact
+    header, shortest round-trip floats; GPU columns appended (batch, pad, precision, gpus,
+    eff_tflops, pct_peak).
+Inputs come from the reference generator on the device (rng.fill_uniform), seeded like
+benchmark(): input split(seed, 0), kernels split(seed, 1) (bench.cpp:109-112).
+"""
+from __future__ import annotations
+
+import io
+import math
+import struct
+from dataclasses import dataclass, field
+from typing import Iterable, List
+
+from .methods import ConvPlan, LayerConfig, footprint
+
+CSV_HEADER = ("layer,method,runs,mean_s,min_s,stddev_s,input_bytes,kernel_bytes,intermediate_bytes,"
+              "output_bytes")
+GPU_COLUMNS = "batch,pad,precision,gpus,eff_tflops,pct_peak"
+PEAK_3XTF32_TFLOPS = 1667.0 / 2 / 3    # MEASURED_PEAKS.json bf16 burst / 2 / 3
+
+
+@dataclass
+class BenchResult:
+    layer: str
+    method: str
+    runs: int
+    mean_s: float
+    min_s: float
+    stddev_s: float
+    input_bytes: int
+    kernel_bytes: int
+    intermediate_bytes: int
+    output_bytes: int
+    batch: int = 1
+    pad: int = 0
+    precision: str = "fp32"
+    gpus: int = 1
+    eff_tflops: float = 0.0
+    pct_peak: float = 0.0
+    samples: List[float] = field(default_factory=list, compare=False)
+    output_checksum: int = field(default=0, compare=False)
+
+    def csv_equal(self, other: "BenchResult") -> bool:
+        keys = ("layer", "method", "runs", "mean_s", "min_s", "stddev_s", "input_bytes", "kernel_bytes",
+                "intermediate_bytes", "output_bytes")
+        return all(getattr(self, k) == getattr(other, k) for k in keys)
+
+
+def fnv1a(t) -> int:
+    """bench.cpp:25-36 over the fp32 bit patterns, bytes low..high (a CUDA or CPU tensor);
+    computed by cl_checksum_fnv1a on a host copy."""
+    import ctypes
+
+    from . import _lib
+    a = t.detach().float().contiguous().cpu()
+    return int(_lib.lib().cl_checksum_fnv1a(ctypes.c_void_p(a.data_ptr()), a.numel()))
+
+
+def benchmark(layer: LayerConfig, method: str = "auto", runs: int = 5, seed: int = 0, precision: str = "fp32",
+              checksum: bool = True, device: int = 0) -> BenchResult:
+    import torch
+
+    from . import rng
+    if runs < 1:
+        raise ValueError("benchmark: runs must be >= 1")
+    if layer.stride != 1 and method != "im2col-gpu":
+        raise ValueError(f"benchmark: strided layer '{layer.name}' is not supported")
+    with ConvPlan(layer, method, precision, device) as plan:
+        x = torch.empty((layer.batch, layer.channels, layer.height, layer.width), device=f"cuda:{device}")
+        w = torch.empty((layer.kernel_count, layer.kernel_size, layer.kernel_size, layer.channels),
+                        device=f"cuda:{device}")
+        rng.fill_uniform(x, rng.split(seed, 0))
+        rng.fill_uniform(w, rng.split(seed, 1))
+        plan.set_weights(w)
+        ws = torch.empty(max(plan.workspace_bytes(), 4), dtype=torch.uint8, device=x.device)
+        y = plan.forward(x, None, ws)                         # warm-up (bench.cpp:115-118)
+        torch.cuda.synchronize()
+        first = fnv1a(y) if checksum else 0
+        samples = []
+        for r in range(runs):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            plan.forward(x, y, ws)
+            e1.record()
+            torch.cuda.synchronize()
+            samples.append(e0.elapsed_time(e1) * 1e-3)
+            if r == 0 and checksum and fnv1a(y) != first:      # bench.cpp:126-128
+                raise RuntimeError(f"benchmark: nondeterministic output for layer '{layer.name}', method {method}")
+        resolved = plan.method
+    mean = sum(samples) / runs
+    std = math.sqrt(sum((s - mean) ** 2 for s in samples) / runs)   # population stddev
+    fp = footprint(layer, resolved)
+    tf = layer.flops() / min(samples) / 1e12
+    return BenchResult(layer.name, resolved, runs, mean, min(samples), std, fp["input_bytes"], fp["kernel_bytes"],
+                       fp["intermediate_bytes"], fp["output_bytes"], layer.batch, layer.pad, precision, 1, tf,
+                       100.0 * tf / PEAK_3XTF32_TFLOPS, samples, first)
+
+
+def _fmt(v: float) -> str:
+    """Shortest round-trip form (the reference uses std::to_chars, bench.cpp:38-42)."""
+    return repr(float(v))
+
+
+def emit_csv(results: Iterable[BenchResult], out=None, gpu_columns: bool = True) -> str:
+    buf = io.StringIO()
+    buf.write(CSV_HEADER + ("," + GPU_COLUMNS if gpu_columns else "") + "\n")
+    for r in results:
+        row = [r.layer, r.method, str(r.runs), _fmt(r.mean_s), _fmt(r.min_s), _fmt(r.stddev_s), str(r.input_bytes),
+               str(r.kernel_bytes), str(r.intermediate_bytes), str(r.output_bytes)]
+        if gpu_columns:
+            row += [str(r.batch), str(r.pad), r.precision, str(r.gpus), _fmt(r.eff_tflops), _fmt(r.pct_peak)]
+        buf.write(",".join(row) + "\n")
+    text = buf.getvalue()
+    if out is not None:
+        out.write(text)
+    return text
+
+
+def parse_csv(text: str) -> List[BenchResult]:
+    """bench.cpp:258-288: header check, 10 (or 16 with GPU columns) fields, numeric errors name
+    the line."""
+    lines = text.splitlines()
+    if not lines:
+        raise RuntimeError("csv: empty input")
+    header = lines[0].rstrip("\r")
+    gpu = header == CSV_HEADER + "," + GPU_COLUMNS
+    if header != CSV_HEADER and not gpu:
+        raise RuntimeError("csv: unexpected header: " + header)
+    want = 16 if gpu else 10
+    out = []
+    for no, line in enumerate(lines[1:], 2):
+        line = line.rstrip("\r")
+        if not line:
+            continue
+        f = line.split(",")
+        if len(f) != want:
+            raise RuntimeError(f"csv line {no}: expected {want} fields, got {len(f)}")
+        try:
+            r = BenchResult(f[0], f[1], int(f[2]), float(f[3]), float(f[4]), float(f[5]), int(f[6]), int(f[7]),
+                            int(f[8]), int(f[9]))
+            if gpu:
+                r.batch, r.pad, r.precision, r.gpus = int(f[10]), int(f[11]), f[12], int(f[13])
+                r.eff_tflops, r.pct_peak = float(f[14]), float(f[15])
+        except ValueError:
+            raise RuntimeError(f"csv line {no}: bad numeric field") from None
+        out.append(r)
+    return out

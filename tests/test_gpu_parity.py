@@ -291,3 +291,19 @@ def test_full_size_sampled_images(oracle, clb, torch_cuda):
         xh = x[picks].cpu().numpy()
         ref = oracle.conv_batch(xh, w.cpu().numpy())
         _check_fp32(oracle, y[picks], ref, layer.name)
+
+
+def test_harness_benchmark_gpu(oracle, clb, torch_cuda):
+    """convlab::benchmark mirror (bench.cpp:87-151): stats, checksum, footprint columns."""
+    from paper_1704_04428_b200 import harness
+    layer = clb.LayerConfig("l1", 16, 20, 20, 32, 3, batch=4)
+    r = harness.benchmark(layer, "kn2row-gpu", runs=3, seed=13)
+    assert r.runs == 3 and len(r.samples) == 3 and r.min_s <= r.mean_s and r.stddev_s >= 0
+    assert (r.input_bytes, r.kernel_bytes, r.intermediate_bytes, r.output_bytes) == (4 * 16 * 400, 4 * 32 * 9 * 16,
+                                                                                      0, 4 * 32 * 400)
+    r2 = harness.benchmark(layer, "kn2row-gpu", runs=1, seed=13)
+    assert r2.output_checksum == r.output_checksum          # deterministic across plans
+    x, w = oracle.make_problem(4, 16, 20, 20, 32, 3, 13)
+    y = clb.run_method("kn2row-gpu", torch_cuda.from_numpy(x).cuda(), torch_cuda.from_numpy(w).cuda())
+    assert harness.fnv1a(y) == r.output_checksum
+    assert harness.parse_csv(harness.emit_csv([r]))[0].csv_equal(r)

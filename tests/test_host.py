@@ -218,3 +218,32 @@ def test_two_rank_gloo_sharding(tmp_path):
     import json
     res = json.loads(line)
     assert res == {"ok": True, "max": 2.0, "sum": 20.0}
+
+
+def test_harness_csv_roundtrip_and_header():
+    """bench.cpp:211-294: byte-exact reference header, 10 reference columns first, GPU columns
+    appended; parse(emit(x)) == x; malformed input errors name the line."""
+    from paper_1704_04428_b200 import harness
+    assert harness.CSV_HEADER == ("layer,method,runs,mean_s,min_s,stddev_s,input_bytes,kernel_bytes,"
+                                  "intermediate_bytes,output_bytes")
+    rs = [harness.BenchResult("l1", "kn2row-gpu", 2, 1.25e-05, 1.1e-05, 1.5e-06, 768, 432, 0, 1024, 8, 1, "fp32", 1,
+                              12.5, 4.5),
+          harness.BenchResult("l3", "im2col-gpu", 3, 0.1, 0.09999999999999999, 0.0, 280, 600, 7000, 420)]
+    for gpu in (True, False):
+        text = harness.emit_csv(rs, gpu_columns=gpu)
+        back = harness.parse_csv(text)
+        assert all(a.csv_equal(b) for a, b in zip(rs, back))
+        assert text.splitlines()[0].startswith(harness.CSV_HEADER)
+    assert harness.parse_csv(harness.emit_csv(rs))[0] == rs[0]
+    with pytest.raises(RuntimeError, match="csv line 2"):
+        harness.parse_csv(harness.CSV_HEADER + "\nl1,x,2,1,1,1,1,1,1\n")
+    with pytest.raises(RuntimeError, match="unexpected header"):
+        harness.parse_csv("layer,method\n")
+
+
+def test_fnv1a_matches_reference_checksum(oracle):
+    import numpy as np
+    import torch
+    from paper_1704_04428_b200 import harness
+    a = oracle.fill(1000, 3)
+    assert harness.fnv1a(torch.from_numpy(a)) == oracle.fnv1a(a)
