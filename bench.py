@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--workload", default="alexnet")
     ap.add_argument("--batch", type=int, default=None, help="override the per-GPU batch")
     ap.add_argument("--method", default="auto")
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline work")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -324,7 +324,7 @@ def main():
     kernel_ms_step = sum(kern_ms)
     tf32_peak = pk["bf16"] / 2.0
     peak_3x = tf32_peak / 3.0
-    mode_peak = peak_3x if args.precision == "fp32" else tf32_peak
+    mode_peak = {"fp32": peak_3x, "tf32": tf32_peak, "bf16": pk["bf16"]}[args.precision]
     achieved = flops_step / (kernel_ms_step * 1e-3) / 1e12
     traffic = None
     try:
@@ -355,13 +355,14 @@ def main():
         "metric": "effective TFLOP/s (2*N*M*C*k^2*P*Q / time), summed over the workload layers",
         "value": value, "unit": "TFLOP/s", "n_gpus": info.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": job_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if args.precision == "fp32" else "tf32",
+        "dtype": {"fp32": "f32", "tf32": "tf32", "bf16": "bf16"}[args.precision],
         "data": "synthetic: reference generator uniform[-1,1) (tensor.cpp:104-134) on device, random-init weights",
         "config": {
             "workload": args.workload, "layers": [l.name for l in layers], "per_gpu_batch": layers[0].batch,
             "global_batch": layers[0].batch * info.world, "method": args.method,
             "resolved_methods": sorted({p.method for p in plans}),
-            "precision": "fp32-faithful 3xTF32" if args.precision == "fp32" else "tf32 (fast mode)",
+            "precision": {"fp32": "fp32-faithful 3xTF32", "tf32": "tf32 (fast mode)",
+                          "bf16": "bf16 operands, fp32 accumulate (fast mode)"}[args.precision],
             "parallelism": f"dp{info.world} (batch-sharded, no data-path collective)",
             "l2": "flushed (256 MiB write) before every timed step", "weights": "pre-packed once, untimed",
         },

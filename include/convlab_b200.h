@@ -66,7 +66,8 @@ typedef enum cl_method {
 
 typedef enum cl_precision {
     CL_PREC_FP32 = 0,  /* fp32-faithful 3xTF32 (rel-L2 <= 1e-5 vs the fp32 oracle)   */
-    CL_PREC_TF32 = 1   /* single TF32 pass (fast mode, 1e-2 tolerance)              */
+    CL_PREC_TF32 = 1,  /* single TF32 pass (fast mode, 1e-2 tolerance)              */
+    CL_PREC_BF16 = 2   /* BF16 operands, fp32 accumulate (fast mode, 1e-2 tolerance) */
 } cl_precision;
 
 typedef struct cl_conv_desc {

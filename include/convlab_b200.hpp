@@ -46,7 +46,7 @@ enum class ConvMethod {
     DirectGpu,          // fp32 CUDA-core direct loop nest (tiny-C first layers)
 };
 
-enum class Precision { Fp32, Tf32 };
+enum class Precision { Fp32, Tf32, Bf16 };
 
 struct LayerConfig {
     std::string name;

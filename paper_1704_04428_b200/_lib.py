@@ -26,7 +26,7 @@ METHODS = {
 }
 METHOD_NAMES = {v: k for k, v in METHODS.items()}
 # cl_precision
-PRECISIONS = {"fp32": 0, "tf32": 1}
+PRECISIONS = {"fp32": 0, "tf32": 1, "bf16": 2}
 
 EXPORTS = [
     "cl_conv_plan", "cl_conv_set_weights", "cl_conv_set_weights_host", "cl_conv_output_dims", "cl_conv_workspace_bytes",

@@ -112,7 +112,7 @@ size_t method_ws_bytes(const cl_plan* p) {
     const cl_conv_desc& d = p->d;
     const size_t nhw = (size_t)d.n * d.h * d.w;
     const size_t npq = (size_t)d.n * p->P * p->Q;
-    const size_t xs = nhw * p->planes * p->Cp * 4;
+    const size_t xs = nhw * row_bytes(p->planes, p->Cp);
     const size_t kk = (size_t)d.k * d.k;
     switch (p->method) {
         case CL_METHOD_KN2ROW:
@@ -123,7 +123,7 @@ size_t method_ws_bytes(const cl_plan* p) {
         case CL_METHOD_KN2COL:
             return xs + kk * d.m * nhw * 4;
         case CL_METHOD_IM2COL:
-            return npq * p->planes * p->Kp * 4;
+            return npq * row_bytes(p->planes, p->Kp);
         case CL_METHOD_DIRECT:
             return 0;
         default:
@@ -143,11 +143,11 @@ void check_device(int device) {
     if (major != 10) throw Error(CL_ENODEVICE, "device is not sm_100 (compute capability 10.x required)");
 }
 
-Operand implicit_a(const cl_plan* p, const float* xs) {
+Operand implicit_a(const cl_plan* p, const void* xs) {
     Operand a;
     a.mode = LOAD_IM2COL;
     a.ptr = xs;
-    a.kw = p->planes * p->Cp;
+    a.kw = (int)row_elems(p->planes, p->Cp);
     a.planes = p->planes;
     a.n = p->d.n;
     a.h = p->d.h;
@@ -157,13 +157,13 @@ Operand implicit_a(const cl_plan* p, const float* xs) {
     return a;
 }
 
-Operand tiled(const float* ptr, long long rows, int taps, int kp, int planes) {
+Operand tiled(const void* ptr, long long rows, int taps, int kp, int planes) {
     Operand o;
     o.mode = LOAD_TILED;
     o.ptr = ptr;
     o.rows = rows;
     o.taps = taps;
-    o.kw = planes * kp;
+    o.kw = (int)row_elems(planes, kp);
     o.planes = planes;
     return o;
 }
@@ -231,7 +231,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         case CL_METHOD_KN2ROW:
         case CL_METHOD_CONV1X1:
         case CL_METHOD_KN2ROW_ACC: {
-            float* xs = wsf;
+            void* xs = wsf;
             launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
             ++p->launches;
             Operand a = implicit_a(p, xs);
@@ -264,8 +264,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         }
         case CL_METHOD_KN2ROW_EXPLICIT:
         case CL_METHOD_KN2COL: {
-            float* xs = wsf;
-            float* inter = wsf + nhw * p->planes * p->Cp;
+            void* xs = wsf;
+            float* inter = reinterpret_cast<float*>(reinterpret_cast<char*>(wsf) + nhw * row_bytes(p->planes, p->Cp));
             launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
             ++p->launches;
             Operand wts = tiled(p->wpack, (long long)taps * d.m, 1, p->Cp, p->planes);
@@ -297,7 +297,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             break;
         }
         case CL_METHOD_IM2COL: {
-            float* pm = wsf;
+            void* pm = wsf;
             launch_im2col_split(x, pm, d.n, d.c, d.h, d.w, d.k, d.pad, d.stride, p->P, p->Q, p->Kp, p->planes, s);
             ++p->launches;
             Operand a = tiled(pm, npq, 1, p->Kp, p->planes);
@@ -348,7 +348,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         require(d.pad != d.k / 2 || d.k <= bound,
                 "ConvProblem: kernel size " + std::to_string(d.k) + " exceeds padded image bound " +
                     std::to_string(bound));
-        require(precision == CL_PREC_FP32 || precision == CL_PREC_TF32, "unknown precision");
+        require(precision == CL_PREC_FP32 || precision == CL_PREC_TF32 || precision == CL_PREC_BF16, "unknown precision");
         if (method == CL_METHOD_CONV1X1)
             require(d.k == 1, "conv1x1 requires a 1x1 kernel, got k = " + std::to_string(d.k));
         const int P = (d.h + 2 * d.pad - d.k) / d.stride + 1;
@@ -376,14 +376,14 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         p->requested = method;
         p->method = m;
         p->prec = precision;
-        p->planes = precision == CL_PREC_FP32 ? 2 : 1;
+        p->planes = precision == CL_PREC_FP32 ? 2 : (precision == CL_PREC_BF16 ? kPlanesBf16 : 1);
         p->device = device;
         p->Cp = round_up(d.c, k_granule(p->planes));
         p->Kp = round_up(d.k * d.k * d.c, k_granule(p->planes));
         p->bn = bn_for(d.m);
-        if (m == CL_METHOD_IM2COL) p->wpack_bytes = (size_t)d.m * p->planes * p->Kp * 4;
+        if (m == CL_METHOD_IM2COL) p->wpack_bytes = (size_t)d.m * row_bytes(p->planes, p->Kp);
         else if (m == CL_METHOD_DIRECT) p->wpack_bytes = (size_t)d.m * d.k * d.k * d.c * 4;
-        else p->wpack_bytes = (size_t)d.k * d.k * d.m * p->planes * p->Cp * 4;
+        else p->wpack_bytes = (size_t)d.k * d.k * d.m * row_bytes(p->planes, p->Cp);
         if (cudaMalloc(&p->wpack, p->wpack_bytes) != cudaSuccess) {
             cudaGetLastError();
             delete p;
@@ -546,9 +546,9 @@ void cl_conv_destroy(cl_plan* p) {
 }
 
 size_t cl_gemm_workspace_bytes(int m, int n, int k, cl_precision precision) {
-    const int planes = precision == CL_PREC_FP32 ? 2 : 1;
+    const int planes = precision == CL_PREC_FP32 ? 2 : (precision == CL_PREC_BF16 ? kPlanesBf16 : 1);
     const size_t kp = (size_t)round_up(k > 0 ? k : 1, k_granule(planes));
-    return align256(((size_t)(m > 0 ? m : 0) + (size_t)(n > 0 ? n : 0)) * planes * kp * 4) + tc_scratch_bytes();
+    return align256(((size_t)(m > 0 ? m : 0) + (size_t)(n > 0 ? n : 0)) * row_bytes(planes, kp)) + tc_scratch_bytes();
 }
 
 cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float* c, cl_precision precision,
@@ -556,12 +556,12 @@ cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float
     return guarded([&] {
         require(m > 0 && n > 0 && k > 0, "gemm: dimensions must be positive");
         require(a && b && c, "gemm: null operand");
-        require(precision == CL_PREC_FP32 || precision == CL_PREC_TF32, "unknown precision");
+        require(precision == CL_PREC_FP32 || precision == CL_PREC_TF32 || precision == CL_PREC_BF16, "unknown precision");
         int dev = 0;
         CLB_CUDA(cudaGetDevice(&dev));
         check_device(dev);
         auto s = static_cast<cudaStream_t>(stream);
-        const int planes = precision == CL_PREC_FP32 ? 2 : 1;
+        const int planes = precision == CL_PREC_FP32 ? 2 : (precision == CL_PREC_BF16 ? kPlanesBf16 : 1);
         const int kp = round_up(k, k_granule(planes));
         const size_t need = cl_gemm_workspace_bytes(m, n, k, precision);
         void* own = nullptr;
@@ -571,8 +571,8 @@ cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float
         } else {
             require(ws_bytes_ >= need, "gemm: workspace too small");
         }
-        float* as = static_cast<float*>(ws);
-        float* bs = as + (size_t)m * planes * kp;
+        char* as = static_cast<char*>(ws);
+        char* bs = as + (size_t)m * row_bytes(planes, kp);
         launch_rows_split(a, as, m, k, kp, planes, s);
         launch_transpose_split(b, bs, k, n, kp, planes, s);
         TcParams t{};
@@ -584,7 +584,7 @@ cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float
         t.epi = EPI_ROWMAJOR;
         t.out = c;
         t.ld = n;
-        set_scratch(t, static_cast<char*>(ws) + align256((size_t)(m + n) * planes * kp * 4));
+        set_scratch(t, static_cast<char*>(ws) + align256((size_t)(m + n) * row_bytes(planes, kp)));
         launch_tc(tiled(as, m, 1, kp, planes), tiled(bs, n, 1, kp, planes), t, s, cta_group_for(m, n, t.bn));
         if (own) CLB_CUDA(cudaFreeAsync(own, s));
     });

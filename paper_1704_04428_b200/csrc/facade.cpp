@@ -158,7 +158,8 @@ CLB_EXPORT FootprintBytes footprint(const LayerConfig& l, ConvMethod m) {
 CLB_EXPORT Plan::Plan(const LayerConfig& layer, ConvMethod method, Precision precision, int device)
     : layer_(layer) {
     const cl_conv_desc d = to_desc(layer);
-    check(cl_conv_plan(&d, to_cl(method), precision == Precision::Fp32 ? CL_PREC_FP32 : CL_PREC_TF32, device,
+    check(cl_conv_plan(&d, to_cl(method),
+                       precision == Precision::Fp32 ? CL_PREC_FP32 : (precision == Precision::Bf16 ? CL_PREC_BF16 : CL_PREC_TF32), device,
                        &plan_));
     int32_t p = 0, q = 0;
     check(cl_conv_output_dims(plan_, &p, &q));

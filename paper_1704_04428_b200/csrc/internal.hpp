@@ -27,23 +27,32 @@ struct Error : std::runtime_error {
     } while (0)
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
-// channel padding granularity of the split layout
-inline int k_granule(int planes) { return planes == 2 ? 16 : 32; }
+// Precision modes ("planes" code carried through the engine):
+//   2 = fp32-faithful 3xTF32 (rows interleave [hi16|lo16] fp32 words per 16 channels)
+//   1 = TF32 fast mode (rows of hi fp32 words)
+//   3 = BF16 fast mode (rows of bf16 elements, kind::f16 MMA)
+constexpr int kPlanesBf16 = 3;
+// channel padding granularity of the split layout (one 128-byte row unit)
+inline int k_granule(int planes) { return planes == 2 ? 16 : (planes == kPlanesBf16 ? 64 : 32); }
+inline int elem_bytes(int planes) { return planes == kPlanesBf16 ? 2 : 4; }
+// elements per operand row of k_pad channels
+inline long long row_elems(int planes, long long kp) { return planes == 2 ? 2 * kp : kp; }
+inline long long row_bytes(int planes, long long kp) { return row_elems(planes, kp) * elem_bytes(planes); }
 
 // ---- pre-pass / post-pass kernels (prepass.cu) -------------------------------------------
 // Split layout of every operand row (k_pad channels): 3xTF32 -> per 16-channel block
 // [hi 16 | lo 16] (row = 2*k_pad words); TF32 -> hi only (row = k_pad words, k_pad % 32 == 0).
 // x NCHW fp32 -> xs[n][h][w][row] (hi = rna_tf32(x), lo = x - hi; zero for c >= C)
-void launch_nchw_to_nhwc_split(const float* x, float* xs, int N, int C, int HW, int Cp, int planes,
+void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s);
 // a[rows][K] -> as[rows][planes][Kp]
-void launch_rows_split(const float* a, float* as, long long rows, int K, int Kp, int planes, cudaStream_t s);
+void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s);
 // b[K][cols] -> bs[cols][planes][Kp]
-void launch_transpose_split(const float* b, float* bs, int K, int cols, int Kp, int planes, cudaStream_t s);
+void launch_transpose_split(const float* b, void* bs, int K, int cols, int Kp, int planes, cudaStream_t s);
 // w MKKC -> wp[tap][M][planes][Cp]
-void launch_pack_weights(const float* w, float* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s);
+void launch_pack_weights(const float* w, void* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s);
 // x NCHW -> patches[n p q][planes][Kp], K index (i*k+j)*C + c  (conv_im2.cpp:19-54 order)
-void launch_im2col_split(const float* x, float* pm, int N, int C, int H, int W, int k, int pad, int stride,
+void launch_im2col_split(const float* x, void* pm, int N, int C, int H, int W, int k, int pad, int stride,
                          int P, int Q, int Kp, int planes, cudaStream_t s);
 // inter[(t*M+m)][N*H*W] -> y NCHW (P x Q)
 void launch_shift_add_row(const float* inter, float* y, int N, int M, int H, int W, int k, int pad, int P,
@@ -63,11 +72,11 @@ void launch_fill_uniform(float* d, unsigned long long n, unsigned long long seed
 // ---- tcgen05 engine (tc_conv.cu) ---------------------------------------------------------
 struct Operand {
     int mode = LOAD_TILED;   // LOAD_TILED: 3-D map (K=planes*Kp, rows, taps); LOAD_IM2COL: NHWC 4-D
-    const float* ptr = nullptr;
+    const void* ptr = nullptr;
     long long rows = 0;      // tiled: rows of the map
     int taps = 1;            // tiled: 3rd dim
-    int kw = 0;              // words per row: 2*Cp (3xTF32 hi|lo interleave) or Cp (TF32)
-    int planes = 2;
+    int kw = 0;              // elements per row: 2*Cp (3xTF32 hi|lo interleave) or Cp (TF32, BF16)
+    int planes = 2;          // precision mode (see k_granule)
     // im2col only
     int n = 0, h = 0, w = 0, k = 1, pad = 0;
 };

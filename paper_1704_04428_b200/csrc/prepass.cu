@@ -4,6 +4,8 @@
 // All are coalesced on both sides (32x32 shared-memory transposes where the layout
 // changes) and grid-stride free: one CTA per 32x32 tile.  None of them does arithmetic
 // beyond the TF32 hi/lo split (hi = cvt.rna.tf32(x), lo = x - hi, exact in fp32).
+#include <cuda_bf16.h>
+
 #include "internal.hpp"
 
 namespace clb {
@@ -16,8 +18,14 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 // Row layout (see internal.hpp): 3xTF32 rows interleave hi|lo per 16-channel block so each
 // 128-byte TMA row carries both halves of 16 channels; TF32 rows hold hi only.
-__device__ __forceinline__ void store_split(float* dst, long long base, int c, int kp, int planes, float v) {
+// `base` = first element of the row (fp32 words, or bf16 elements for the BF16 mode).
+__device__ __forceinline__ void store_split(void* dstv, long long base, int c, int kp, int planes, float v) {
     (void)kp;
+    if (planes == kPlanesBf16) {
+        reinterpret_cast<__nv_bfloat16*>(dstv)[base + c] = __float2bfloat16_rn(v);
+        return;
+    }
+    float* dst = static_cast<float*>(dstv);
     const float hi = tf32_rna(v);
     if (planes == 2) {
         const int u = (c >> 4) << 5, w = c & 15;
@@ -28,6 +36,8 @@ __device__ __forceinline__ void store_split(float* dst, long long base, int c, i
     }
 }
 
+__device__ __forceinline__ long long rowel(int planes, long long kp) { return planes == 2 ? 2 * kp : kp; }
+
 // ------------------------------------------------------------------ NCHW -> NHWC split ----
 // Tile = 32 channels x 128 pixels of one image, 256 threads.  Loads: warp w reads channel
 // rows w, w+8, w+16, w+24 in four 128-byte pieces each -- 16 independent loads in flight per
@@ -37,7 +47,7 @@ __device__ __forceinline__ void store_split(float* dst, long long base, int c, i
 // grid (ceil(HW/128), ceil(Cp/32), N)
 constexpr int kSplitPx = 128;
 
-__global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, float* __restrict__ xs,
+__global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xsv,
                                                                  int C, int HW, int Cp, int planes) {
     __shared__ float tile[kSplitPx][33];   // [pixel][channel]
     const int n = blockIdx.z;
@@ -60,14 +70,25 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
 #pragma unroll
         for (int h = 0; h < 4; ++h) tile[lane + 32 * h][warp + 8 * r] = v[r][h];
     __syncthreads();
-    const long long row_words = (long long)planes * Cp;
-    const int words = planes == 2 ? 64 : 32;            // output words per pixel in this tile
+    const long long row_words = rowel(planes, Cp);
+    const int words = planes == 2 ? 64 : 32;            // output elements per pixel in this tile
     const int nch = Cp - c0 < 32 ? Cp - c0 : 32;        // channels of this tile inside the padded row
     const int out_words = planes == 2 ? 2 * nch : nch;
+    if (planes == kPlanesBf16) {                        // bf16 rows: lane = channel
+        __nv_bfloat16* xb = static_cast<__nv_bfloat16*>(xsv);
+        for (int pp = warp; pp < kSplitPx; pp += 8) {
+            const int pix = p0 + pp;
+            if (pix >= HW) break;
+            if (lane < nch) xb[((long long)n * HW + pix) * row_words + c0 + lane] = __float2bfloat16_rn(tile[pp][lane]);
+        }
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        return;
+    }
+    float* xs = static_cast<float*>(xsv);
     for (int pp = warp; pp < kSplitPx; pp += 8) {
         const int pix = p0 + pp;
         if (pix >= HW) break;
-        float* dst = xs + ((long long)n * HW + pix) * row_words + (long long)planes * c0;
+        float* dst = xs + ((long long)n * HW + pix) * row_words + (long long)(planes == 2 ? 2 : 1) * c0;
 #pragma unroll
         for (int o0 = 0; o0 < 64; o0 += 32) {
             const int o = o0 + lane;
@@ -88,7 +109,7 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-void launch_nchw_to_nhwc_split(const float* x, float* xs, int N, int C, int HW, int Cp, int planes,
+void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s) {
     dim3 grid((HW + kSplitPx - 1) / kSplitPx, (Cp + 31) / 32, N);
     nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, C, HW, Cp, planes);
@@ -97,28 +118,29 @@ void launch_nchw_to_nhwc_split(const float* x, float* xs, int N, int C, int HW, 
 
 // -------------------------------------------------------------------- row-wise split ----
 // grid (ceil(Kp/128), rows), block 128
-__global__ void rows_split_kernel(const float* __restrict__ a, float* __restrict__ as, int K, int Kp,
+__global__ void rows_split_kernel(const float* __restrict__ a, void* __restrict__ as, int K, int Kp,
                                   int planes) {
     const long long r = blockIdx.y;
     const int c = blockIdx.x * 128 + threadIdx.x;
     if (c >= Kp) return;
     const float v = c < K ? __ldg(a + r * K + c) : 0.0f;
-    store_split(as, r * planes * Kp, c, Kp, planes, v);
+    store_split(as, r * rowel(planes, Kp), c, Kp, planes, v);
 }
 
-void launch_rows_split(const float* a, float* as, long long rows, int K, int Kp, int planes, cudaStream_t s) {
+void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s) {
     if (rows <= 0) return;
     for (long long r0 = 0; r0 < rows; r0 += 65535) {
         const long long nr = rows - r0 < 65535 ? rows - r0 : 65535;
         dim3 grid((Kp + 127) / 128, (unsigned)nr);
-        rows_split_kernel<<<grid, 128, 0, s>>>(a + r0 * K, as + r0 * planes * Kp, K, Kp, planes);
+        rows_split_kernel<<<grid, 128, 0, s>>>(a + r0 * K, static_cast<char*>(as) + r0 * row_bytes(planes, Kp), K,
+                                               Kp, planes);
     }
     CLB_CUDA(cudaGetLastError());
 }
 
 // ------------------------------------------------------------- transpose + split (B^T) ----
 // b[K][cols] -> bs[cols][planes][Kp]; grid (ceil(cols/32), ceil(Kp/32)), block (32, 8)
-__global__ void transpose_split_kernel(const float* __restrict__ b, float* __restrict__ bs, int K, int cols,
+__global__ void transpose_split_kernel(const float* __restrict__ b, void* __restrict__ bs, int K, int cols,
                                        int Kp, int planes) {
     __shared__ float tile[32][33];
     const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
@@ -129,11 +151,11 @@ __global__ void transpose_split_kernel(const float* __restrict__ b, float* __res
     __syncthreads();
     for (int nn = threadIdx.y; nn < 32; nn += 8) {
         const int n = n0 + nn, kx = k0 + threadIdx.x;
-        if (n < cols && kx < Kp) store_split(bs, (long long)n * planes * Kp, kx, Kp, planes, tile[threadIdx.x][nn]);
+        if (n < cols && kx < Kp) store_split(bs, (long long)n * rowel(planes, Kp), kx, Kp, planes, tile[threadIdx.x][nn]);
     }
 }
 
-void launch_transpose_split(const float* b, float* bs, int K, int cols, int Kp, int planes, cudaStream_t s) {
+void launch_transpose_split(const float* b, void* bs, int K, int cols, int Kp, int planes, cudaStream_t s) {
     dim3 grid((cols + 31) / 32, (Kp + 31) / 32), block(32, 8);
     transpose_split_kernel<<<grid, block, 0, s>>>(b, bs, K, cols, Kp, planes);
     CLB_CUDA(cudaGetLastError());
@@ -142,7 +164,7 @@ void launch_transpose_split(const float* b, float* bs, int K, int cols, int Kp, 
 // ------------------------------------------------------------------ weight pre-pack ----
 // kn2row_reorder_kernel (conv_kn2.cpp:28-39) fused with the split:
 //   wp[(i*k+j)][m][plane][c] = split(K[m][i][j][c])
-__global__ void pack_weights_kernel(const float* __restrict__ w, float* __restrict__ wp, int M, int k, int C,
+__global__ void pack_weights_kernel(const float* __restrict__ w, void* __restrict__ wp, int M, int k, int C,
                                     int Cp, int planes) {
     const long long total = (long long)k * k * M * Cp;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -152,11 +174,11 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, float* __restri
         const int m = (int)(tm % M);
         const int t = (int)(tm / M);
         const float v = c < C ? w[((long long)m * k * k + t) * C + c] : 0.0f;
-        store_split(wp, tm * planes * Cp, c, Cp, planes, v);
+        store_split(wp, tm * rowel(planes, Cp), c, Cp, planes, v);
     }
 }
 
-void launch_pack_weights(const float* w, float* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s) {
+void launch_pack_weights(const float* w, void* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s) {
     const long long total = (long long)k * k * M * Cp;
     const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
     pack_weights_kernel<<<blocks, 256, 0, s>>>(w, wp, M, k, C, Cp, planes);
@@ -168,7 +190,7 @@ void launch_pack_weights(const float* w, float* wp, int M, int k, int C, int Cp,
 // conv_im2.cpp:56-85 with im2col's K order (i*k+j)*C+c of conv_im2.cpp:19-54):
 //   pm[pix = (n,p,q)][plane][kk = (i*k+j)*C + c] = x[n][c][p*s-pad+i][q*s-pad+j]  (0 if OOB)
 // grid (ceil(NPQ/32), ceil(Kp/32)), block (32, 8): gather coalesced along pixels, write along K.
-__global__ void im2col_split_kernel(const float* __restrict__ x, float* __restrict__ pm, int C, int H, int W,
+__global__ void im2col_split_kernel(const float* __restrict__ x, void* __restrict__ pm, int C, int H, int W,
                                     int k, int pad, int stride, int P, int Q, long long npq, int Kp, int planes) {
     __shared__ float tile[32][33];
     const long long pix0 = (long long)blockIdx.x * 32;
@@ -199,11 +221,11 @@ __global__ void im2col_split_kernel(const float* __restrict__ x, float* __restri
     for (int pp = threadIdx.y; pp < 32; pp += 8) {
         const long long pr = pix0 + pp;
         const int kx = k0 + threadIdx.x;
-        if (pr < npq && kx < Kp) store_split(pm, pr * planes * Kp, kx, Kp, planes, tile[threadIdx.x][pp]);
+        if (pr < npq && kx < Kp) store_split(pm, pr * rowel(planes, Kp), kx, Kp, planes, tile[threadIdx.x][pp]);
     }
 }
 
-void launch_im2col_split(const float* x, float* pm, int N, int C, int H, int W, int k, int pad, int stride,
+void launch_im2col_split(const float* x, void* pm, int N, int C, int H, int W, int k, int pad, int stride,
                          int P, int Q, int Kp, int planes, cudaStream_t s) {
     const long long npq = (long long)N * P * Q;
     dim3 grid((unsigned)((npq + 31) / 32), (Kp + 31) / 32), block(32, 8);

@@ -146,6 +146,17 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, ui
         : "memory");
 }
 
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 operands), fp32 accumulate, one CTA.
+__device__ __forceinline__ void mma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // Arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -235,6 +246,16 @@ __device__ __forceinline__ void mma_tf32_ss_2sm(uint32_t d_tmem, uint64_t a_desc
         : "memory");
 }
 
+__device__ __forceinline__ void mma_bf16_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // commit the leader's MMAs to the same-offset mbarrier of every CTA in `mask`.
 __device__ __forceinline__ void mma_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
     asm volatile(
@@ -258,6 +279,15 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, uint32_
     d |= (uint64_t)1 << 46;                              // [46,48) version = 1 (sm_100)
     d |= layout << 61;                                   // [61,64) swizzle mode
     return d;
+}
+
+// Instruction descriptor: kind::f16 with bf16 A/B, K-major, fp32 accumulator, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N) {
+    return (1u << 4)              // c_format = F32
+           | (1u << 7)            // a_format = BF16
+           | (1u << 10)           // b_format = BF16
+           | ((N >> 3) << 17)     // n_dim
+           | ((M >> 4) << 24);    // m_dim
 }
 
 // Instruction descriptor: kind::tf32, A/B K-major, fp32 accumulator, M x N.

@@ -47,26 +47,30 @@ int num_sms() {
 
 void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows) {
     resolve_driver();
-    const cuuint64_t kdim = (cuuint64_t)op.kw;   // words per row (hi|lo interleaved for 3xTF32)
+    const cuuint64_t kdim = (cuuint64_t)op.kw;   // elements per row (hi|lo interleaved for 3xTF32)
+    const cuuint64_t eb = (cuuint64_t)elem_bytes(op.planes);
+    const CUtensorMapDataType dt = op.planes == kPlanesBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const cuuint32_t unit = (cuuint32_t)(kRowBytes / eb);   // elements per 128-byte row unit
     CUresult r;
     if (op.mode == LOAD_IM2COL) {
         cuuint64_t dims[4] = {kdim, (cuuint64_t)op.w, (cuuint64_t)op.h, (cuuint64_t)op.n};
-        cuuint64_t strides[3] = {kdim * 4, kdim * 4 * op.w, kdim * 4 * op.w * op.h};
+        cuuint64_t strides[3] = {kdim * eb, kdim * eb * op.w, kdim * eb * op.w * op.h};
         // Bounding box: lower corner -pad, upper corner pad-(k-1) in W and H, so the
         // traversal enumerates exactly the P x Q output positions of each image.
         int lower[2] = {-op.pad, -op.pad};
         int upper[2] = {op.pad - (op.k - 1), op.pad - (op.k - 1)};
         cuuint32_t estr[4] = {1, 1, 1, 1};
-        r = g_im2col(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(op.ptr), dims, strides, lower,
-                     upper, (cuuint32_t)kRowWords, (cuuint32_t)box_rows, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        r = g_im2col(map, dt, 4, const_cast<void*>(op.ptr), dims, strides, lower,
+                     upper, unit, (cuuint32_t)box_rows, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
         cuuint64_t dims[3] = {kdim, (cuuint64_t)op.rows, (cuuint64_t)op.taps};
-        cuuint64_t strides[2] = {kdim * 4, kdim * 4 * (cuuint64_t)op.rows};
-        cuuint32_t box[3] = {(cuuint32_t)kRowWords, (cuuint32_t)box_rows, 1};
+        cuuint64_t strides[2] = {kdim * eb, kdim * eb * (cuuint64_t)op.rows};
+        cuuint32_t box[3] = {unit, (cuuint32_t)box_rows, 1};
         cuuint32_t estr[3] = {1, 1, 1};
-        r = g_tiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(op.ptr), dims, strides, box, estr,
+        r = g_tiled(map, dt, 3, const_cast<void*>(op.ptr), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
@@ -78,17 +82,21 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows) {
 void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cg) {
     if (cg != 1 && cg != 2) throw Error(6, "cta group must be 1 or 2");
     if (p.bn % 16 != 0 || p.bn < 16 || p.bn > 256) throw Error(6, "tile N must be a multiple of 16 in [16,256]");
-    if (a.kw != b.kw || a.kw % kRowWords != 0 || a.planes != b.planes) throw Error(6, "operand K layout mismatch");
+    const int unit = kRowBytes / elem_bytes(a.planes);
+    if (a.kw != b.kw || a.kw % unit != 0 || a.planes != b.planes) throw Error(6, "operand K layout mismatch");
     CUtensorMap ma, mb;
     encode_operand_map(&ma, a, kTileM);
     encode_operand_map(&mb, b, p.bn / cg);
     p.planes = a.planes;
-    p.kblocks = a.kw / kRowWords;
+    p.row_elems = unit;
+    p.kblocks = a.kw / unit;
     p.a_mode = a.mode;
     p.b_mode = b.mode;
     p.stages = tc_num_stages(p.bn / cg, p.planes);
     const int k_iters = p.taps * p.kblocks;
-    if (p.chunk_iters <= 0) p.chunk_iters = p.planes == 2 ? kChunkIters : kChunkIters / 2;   // 128 K-elements
+    // 128 K-elements per accumulation chunk for the fp32-faithful mode; coarser for the fast
+    // modes, whose input rounding dominates the accumulator's
+    if (p.chunk_iters <= 0) p.chunk_iters = p.planes == 2 ? kChunkIters : kChunkIters / 2;
     if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
     const int tile_m = kTileM * cg;
     const int row_tiles = (p.rows + tile_m - 1) / tile_m;

@@ -59,7 +59,8 @@ struct TcParams {
     int n_col_tiles, num_tiles;
     int taps, tap_begin, ksize;  // K loop: taps [tap_begin, tap_begin+taps), tap t -> (t/ksize, t%ksize)
     int kblocks;               // 16-channel blocks per tap
-    int planes;                // 2 = 3xTF32 (hi|lo interleaved per 16 channels), 1 = TF32 (hi)
+    int planes;                // 2 = 3xTF32 (hi|lo interleaved per 16 channels), 1 = TF32 (hi), 3 = BF16
+    int row_elems;             // elements per 128-byte row unit (32 fp32 or 64 bf16)
     int stages;
     int chunk_iters;           // k-iterations per TMEM accumulation chunk
     int a_mode, b_mode;        // LOAD_TILED / LOAD_IM2COL
@@ -283,7 +284,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 int kb = it0 - (it0 / p.kblocks) * p.kblocks;
                 int ti = tap / p.ksize, tj = tap - (tap / p.ksize) * p.ksize;
                 for (int it = it0; it < it1; ++it) {
-                    const int kc = kb * kRowWords;
+                    const int kc = kb * p.row_elems;
                     mbar_wait(&empty[stage], phase ^ 1u);
                     uint8_t* a_st = smem + stage * stage_bytes;
                     if (elect_one()) {
@@ -331,7 +332,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // The whole warp runs the loop (loop state is warp-uniform, so it lives in uniform
         // registers); one elected lane issues the MMAs and the commits that track them.
         if (leader) {
-            const uint32_t idesc = idesc_tf32((uint32_t)tile_m, (uint32_t)bn);
+            const uint32_t idesc = planes == 3 ? idesc_bf16((uint32_t)tile_m, (uint32_t)bn)
+                                               : idesc_tf32((uint32_t)tile_m, (uint32_t)bn);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t lg = 0;
@@ -340,6 +342,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
                 if constexpr (CG == 2) mma_tf32_ss_2sm(d, a, b, idesc, acc);
                 else mma_tf32_ss(d, a, b, idesc, acc);
+            };
+            auto mma16 = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {   // kind::f16 (bf16)
+                if constexpr (CG == 2) mma_bf16_ss_2sm(d, a, b, idesc, acc);
+                else mma_bf16_ss(d, a, b, idesc, acc);
             };
             auto commit = [&](uint64_t* bar) {
                 if constexpr (CG == 2) mma_commit_2sm_mc(bar, (uint16_t)0x3);
@@ -375,6 +381,12 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         mma(d_tmem, da + 6, db + 2, 1u);
                         mma(d_tmem, da + 2, db + 6, 1u);
                         mma(d_tmem, da + 2, db + 2, 1u);
+                    } else if (planes == 3) {
+                        // 64 bf16 per row: 4 k-steps of 16 elements (32 B = 2 desc units)
+                        mma16(d_tmem, da, db, first);
+                        mma16(d_tmem, da + 2, db + 2, 1u);
+                        mma16(d_tmem, da + 4, db + 4, 1u);
+                        mma16(d_tmem, da + 6, db + 6, 1u);
                     } else {
                         mma(d_tmem, da, db, first);
                         mma(d_tmem, da + 2, db + 2, 1u);

@@ -26,7 +26,7 @@ REFERENCE_METHODS = ["direct-sum", "direct-loopnest", "im2col", "im2row", "kn2ro
 GPU_METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu", "conv1x1-gpu",
                "direct-gpu"]
 ALL_METHODS = REFERENCE_METHODS + GPU_METHODS + ["auto"]
-PRECISIONS = ("fp32", "tf32")
+PRECISIONS = ("fp32", "tf32", "bf16")
 
 
 def method_from_name(name: str) -> Optional[str]:

@@ -122,12 +122,20 @@ def test_selector_picks_direct_for_tiny_c(oracle, clb, torch_cuda):
         _check_fp32(oracle, _run(clb, torch_cuda, "direct-gpu", x, w), oracle.conv_batch(x, w), f"direct k={k}")
 
 
-def test_tf32_fast_mode(oracle, clb, torch_cuda):
-    x, w = oracle.make_problem(2, 64, 20, 20, 96, 3, 3)
-    ref = oracle.conv_batch(x, w)
-    for method in ("kn2row-gpu", "im2col-gpu", "kn2row-explicit-gpu"):
-        m = oracle.parity_metrics(_run(clb, torch_cuda, method, x, w, "tf32"), ref)
-        assert m["rel_l2"] <= TF32_L2, (method, m)
+@pytest.mark.parametrize("precision", ["tf32", "bf16"])
+def test_fast_modes(oracle, clb, torch_cuda, precision):
+    """TF32 / BF16 fast modes, reported separately at the 1e-2 tolerance of the north star."""
+    for shape in ((2, 64, 20, 20, 96, 3), (2, 200, 13, 13, 72, 5), (3, 16, 9, 9, 24, 1)):
+        x, w = oracle.make_problem(*shape, 3)
+        ref = oracle.conv_batch(x, w)
+        for method in ("kn2row-gpu", "im2col-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu"):
+            m = oracle.parity_metrics(_run(clb, torch_cuda, method, x, w, precision), ref)
+            assert m["rel_l2"] <= TF32_L2 and m["finite"], (precision, method, shape, m)
+            assert m["rel_l2"] > 1e-6, "fast mode must actually round the operands"
+    a = oracle.fill(300 * 150, 1).reshape(300, 150)
+    b = oracle.fill(150 * 70, 2).reshape(150, 70)
+    c = clb.gemm(torch_cuda.from_numpy(a).cuda(), torch_cuda.from_numpy(b).cuda(), precision).cpu().numpy()
+    assert oracle.parity_metrics(c, a.astype(np.float64) @ b.astype(np.float64))["rel_l2"] <= TF32_L2
 
 
 def test_nonstandard_padding(oracle, clb, torch_cuda):
