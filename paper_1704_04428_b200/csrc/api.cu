@@ -75,6 +75,7 @@ struct cl_plan {
     size_t wpack_bytes = 0;
     float* wraw = nullptr;     // direct-gpu: MKKC fp32 weights as given
     unsigned* flags = nullptr; // stream-K fixup flags, zeroed once, self-resetting
+    bool padded_rows = false;  // implicit kn2row in tap-shared (zero-padded row) mode
     bool weights_set = false;
     void* own_ws = nullptr;
     size_t own_ws_bytes = 0;
@@ -118,6 +119,8 @@ size_t method_ws_bytes(const cl_plan* p) {
         case CL_METHOD_KN2ROW:
         case CL_METHOD_CONV1X1:
         case CL_METHOD_KN2ROW_ACC:
+            if (p->padded_rows)
+                return (size_t)d.n * (d.h + 2 * d.pad) * (d.w + 2 * d.pad) * row_bytes(p->planes, p->Cp);
             return xs;
         case CL_METHOD_KN2ROW_EXPLICIT:
         case CL_METHOD_KN2COL:
@@ -232,6 +235,33 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         case CL_METHOD_CONV1X1:
         case CL_METHOD_KN2ROW_ACC: {
             void* xs = wsf;
+            if (p->padded_rows) {
+                // tap-shared mode: zero-padded NHWC rows; each stage loads ONE A box of 128+k-1
+                // rows per kernel row i and feeds its k taps through row-shifted descriptors
+                const int Hp = d.h + 2 * d.pad, Wp = d.w + 2 * d.pad;
+                launch_nchw_to_padded_split(x, xs, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                ++p->launches;
+                Operand a = tiled(xs, (long long)d.n * Hp * Wp, 1, p->Cp, p->planes);
+                Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
+                TcParams t = base_params(p);
+                t.rows = d.n * Hp * Wp;
+                t.cols = d.m;
+                t.bn = p->bn;
+                t.b_tap3 = 1;
+                t.tps = d.k;
+                t.a_row_shift = Wp;
+                t.epi = EPI_NCHW_PADDED;
+                t.epi_hp = Hp;
+                t.epi_wp = Wp;
+                t.epi_n = d.n;
+                t.out = y;
+                t.out_channels = d.m;
+                t.pq_out = p->P * p->Q;
+                t.taps = taps;
+                tc(a, b, t);
+                tc_done();
+                break;
+            }
             launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
             ++p->launches;
             Operand a = implicit_a(p, xs);
@@ -390,6 +420,23 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             throw Error(CL_ENOMEM, "packed-weight allocation failed");
         }
         if (m == CL_METHOD_DIRECT) p->wraw = p->wpack;
+        {
+            // tap-shared (padded-row) mode for the implicit kernel: one A box per kernel row feeds
+            // its k taps through row-shifted descriptors (k x fewer A TMA bytes).  Measured on
+            // B200 it does not speed up small-N tiles -- they are bound by the tensor core's
+            // shared-memory operand reads (tools/mma_probe.cu: N=64 tops out at 63% even with
+            // operands resident), not by TMA -- so it is opt-in (CLB_PADDED_ROWS=1) until the
+            // A operand moves to TMEM.
+            static const int forced_padded = [] {
+                const char* e = std::getenv("CLB_PADDED_ROWS");
+                return e ? std::atoi(e) : -1;
+            }();
+            const double waste = (double)(d.h + 2 * d.pad) * (d.w + 2 * d.pad) / ((double)P * Q) - 1.0;
+            const bool fits = tc_num_stages(p->bn, d.k) >= 2;   // CG1 worst case
+            const bool eligible = m == CL_METHOD_KN2ROW && d.k >= 3 && d.k <= 7 && d.stride == 1 && fits;
+            (void)waste;
+            p->padded_rows = eligible && forced_padded == 1;
+        }
         if (cudaMalloc(&p->flags, kMaxGrid * sizeof(unsigned)) != cudaSuccess ||
             cudaMemset(p->flags, 0, kMaxGrid * sizeof(unsigned)) != cudaSuccess) {
             cudaGetLastError();

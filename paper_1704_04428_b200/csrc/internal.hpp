@@ -45,6 +45,9 @@ inline long long row_bytes(int planes, long long kp) { return row_elems(planes, 
 // x NCHW fp32 -> xs[n][h][w][row] (hi = rna_tf32(x), lo = x - hi; zero for c >= C)
 void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s);
+// same, into the zero-padded image [n][H+2pad][W+2pad][row] (tap-shared kernel mode)
+void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
+                                 cudaStream_t s);
 // a[rows][K] -> as[rows][planes][Kp]
 void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s);
 // b[K][cols] -> bs[cols][planes][Kp]
@@ -81,7 +84,7 @@ struct Operand {
     int n = 0, h = 0, w = 0, k = 1, pad = 0;
 };
 
-void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows);
+void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int box_taps = 1);
 // p.partials / p.flags must point at tc_scratch_bytes() of device scratch (stream-K fixup).
 void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cta_group = 1);
 constexpr int kMaxGrid = 160;   // >= SM count (148 on B200)

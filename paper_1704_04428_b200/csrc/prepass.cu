@@ -47,23 +47,35 @@ __device__ __forceinline__ long long rowel(int planes, long long kp) { return pl
 // grid (ceil(HW/128), ceil(Cp/32), N)
 constexpr int kSplitPx = 128;
 
+// Output pixel space: HW = Hp*Wp pixels per image; with pad > 0 this is the zero-padded
+// image (Hp = H + 2 pad, Wp = W + 2 pad) the tap-shared (padded-row) kernel mode reads.
 __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xsv,
-                                                                 int C, int HW, int Cp, int planes) {
+                                                                 int C, int HW, int Cp, int planes, int H, int W,
+                                                                 int Wp, int pad) {
     __shared__ float tile[kSplitPx][33];   // [pixel][channel]
     const int n = blockIdx.z;
     const int p0 = blockIdx.x * kSplitPx, c0 = blockIdx.y * 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const float* xn = x + (long long)n * C * HW;
+    const float* xn = x + (long long)n * C * H * W;
+    int src[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const int pix = p0 + lane + 32 * h;
+        if (pad == 0) {
+            src[h] = pix < HW ? pix : -1;
+        } else {
+            const int yy = pix / Wp, xx = pix - (pix / Wp) * Wp;
+            const int sy = yy - pad, sx = xx - pad;
+            src[h] = (pix < HW && sy >= 0 && sy < H && sx >= 0 && sx < W) ? sy * W + sx : -1;
+        }
+    }
     float v[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int c = c0 + warp + 8 * r;
-        const float* row = xn + (long long)c * HW;
+        const float* row = xn + (long long)c * H * W;
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const int pix = p0 + lane + 32 * h;
-            v[r][h] = (c < C && pix < HW) ? __ldg(row + pix) : 0.0f;
-        }
+        for (int h = 0; h < 4; ++h) v[r][h] = (c < C && src[h] >= 0) ? __ldg(row + src[h]) : 0.0f;
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r)
@@ -112,7 +124,15 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
 void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s) {
     dim3 grid((HW + kSplitPx - 1) / kSplitPx, (Cp + 31) / 32, N);
-    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, C, HW, Cp, planes);
+    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, C, HW, Cp, planes, 1, HW, HW, 0);
+    CLB_CUDA(cudaGetLastError());
+}
+
+void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
+                                 cudaStream_t s) {
+    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+    dim3 grid((Hp * Wp + kSplitPx - 1) / kSplitPx, (Cp + 31) / 32, N);
+    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, C, Hp * Wp, Cp, planes, H, W, Wp, pad);
     CLB_CUDA(cudaGetLastError());
 }
 

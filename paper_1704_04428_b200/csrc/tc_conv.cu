@@ -45,7 +45,7 @@ int num_sms() {
     return n;
 }
 
-void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows) {
+void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int box_taps) {
     resolve_driver();
     const cuuint64_t kdim = (cuuint64_t)op.kw;   // elements per row (hi|lo interleaved for 3xTF32)
     const cuuint64_t eb = (cuuint64_t)elem_bytes(op.planes);
@@ -68,7 +68,7 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows) {
     } else {
         cuuint64_t dims[3] = {kdim, (cuuint64_t)op.rows, (cuuint64_t)op.taps};
         cuuint64_t strides[2] = {kdim * eb, kdim * eb * (cuuint64_t)op.rows};
-        cuuint32_t box[3] = {unit, (cuuint32_t)box_rows, 1};
+        cuuint32_t box[3] = {unit, (cuuint32_t)box_rows, (cuuint32_t)box_taps};
         cuuint32_t estr[3] = {1, 1, 1};
         r = g_tiled(map, dt, 3, const_cast<void*>(op.ptr), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -84,19 +84,23 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     if (p.bn % 16 != 0 || p.bn < 16 || p.bn > 256) throw Error(6, "tile N must be a multiple of 16 in [16,256]");
     const int unit = kRowBytes / elem_bytes(a.planes);
     if (a.kw != b.kw || a.kw % unit != 0 || a.planes != b.planes) throw Error(6, "operand K layout mismatch");
+    if (p.tps <= 0) p.tps = 1;
     CUtensorMap ma, mb;
-    encode_operand_map(&ma, a, kTileM);
-    encode_operand_map(&mb, b, p.bn / cg);
+    encode_operand_map(&ma, a, tc_a_box_rows(p.tps), 1);
+    encode_operand_map(&mb, b, p.bn / cg, p.tps);
     p.planes = a.planes;
     p.row_elems = unit;
     p.kblocks = a.kw / unit;
     p.a_mode = a.mode;
     p.b_mode = b.mode;
-    p.stages = tc_num_stages(p.bn / cg, p.planes);
-    const int k_iters = p.taps * p.kblocks;
+    p.stages = tc_num_stages(p.bn / cg, p.tps);
+    if (p.stages < 2) throw Error(2, "tile too large for a 2-stage pipeline");
+    if (p.taps % p.tps != 0) throw Error(6, "taps per stage must divide the tap count");
+    const int k_iters = (p.taps / p.tps) * p.kblocks;
     // 128 K-elements per accumulation chunk for the fp32-faithful mode; coarser for the fast
     // modes, whose input rounding dominates the accumulator's
     if (p.chunk_iters <= 0) p.chunk_iters = p.planes == 2 ? kChunkIters : kChunkIters / 2;
+    if (p.tps > 1) p.chunk_iters = p.chunk_iters / p.tps > 0 ? p.chunk_iters / p.tps : 1;   // a stage holds tps taps
     if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
     const int tile_m = kTileM * cg;
     const int row_tiles = (p.rows + tile_m - 1) / tile_m;
@@ -105,7 +109,7 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     if (p.num_tiles <= 0) return;
     p.chunks_per_tile = (k_iters + p.chunk_iters - 1) / p.chunk_iters;
     const long long total_chunks = (long long)p.num_tiles * p.chunks_per_tile;
-    const int smem = tc_smem_bytes(p.bn / cg, p.planes, p.stages);
+    const int smem = tc_smem_bytes(p.bn / cg, p.tps, p.stages);
     static bool configured[3] = {false, false, false};
     if (!configured[cg]) {
         if (cg == 2)

@@ -38,7 +38,7 @@
 namespace clb {
 
 enum : int { LOAD_TILED = 0, LOAD_IM2COL = 1 };
-enum : int { EPI_NCHW = 0, EPI_ROWMAJOR = 1 };
+enum : int { EPI_NCHW = 0, EPI_ROWMAJOR = 1, EPI_NCHW_PADDED = 2 };
 
 constexpr int kTileM = 128;          // UMMA M (D rows per tile)
 // Operand rows are 128-byte units (SWIZZLE_128B, one TMA box per operand per stage):
@@ -68,7 +68,14 @@ struct TcParams {
     // im2col geometry of the row operand (output pixels)
     int P, Q, pad;
     // epilogue
-    int epi;                   // EPI_NCHW (rows = pixels n*P*Q, cols = channels) / EPI_ROWMAJOR
+    int epi;                   // EPI_NCHW (rows = pixels n*P*Q, cols = channels) / EPI_ROWMAJOR /
+                               // EPI_NCHW_PADDED (rows = padded pixels n*Hp*Wp + y*Wp + x)
+    // tap-shared A (padded-row mode): one stage = `tps` taps (a row of the kernel) x one
+    // channel block; A is ONE TMA box of 128 + tps - 1 rows of the zero-padded NHWC input and
+    // tap j reads it through a descriptor shifted by j rows; tap rows step by a_row_shift (Wp).
+    int tps;                   // taps per stage (1 = one tap per stage)
+    int a_row_shift;           // A row offset per tap group (padded row width Wp)
+    int epi_hp, epi_wp, epi_n; // EPI_NCHW_PADDED geometry
     int accumulate;            // out += D (accumulating shifted-GEMM variant)
     float* out;
     long long ld;              // EPI_ROWMAJOR leading dimension
@@ -89,15 +96,19 @@ __host__ __device__ inline int chunk_start(int b, int total, int grid) {
     return (int)(((long long)b * total) / grid);
 }
 
-__host__ __device__ inline int tc_stage_bytes(int bn, int planes) { return (void)planes, (kTileM + bn) * kRowBytes; }
+// A rows of one stage (box) and their smem footprint (1024-aligned for the swizzle atom);
+// B rows = tps taps x (bn / cta group).
+__host__ __device__ inline int tc_a_box_rows(int tps) { return kTileM + tps - 1; }
+__host__ __device__ inline int tc_a_bytes(int tps) { return (tc_a_box_rows(tps) * kRowBytes + 1023) & ~1023; }
+__host__ __device__ inline int tc_stage_bytes(int b_rows, int tps) { return tc_a_bytes(tps) + tps * b_rows * kRowBytes; }
 
-__host__ inline int tc_num_stages(int bn, int planes) {
-    int s = (kSmemBudget - 1024) / tc_stage_bytes(bn, planes);
+__host__ inline int tc_num_stages(int b_rows, int tps) {
+    int s = (kSmemBudget - 1024) / tc_stage_bytes(b_rows, tps);
     return s > 8 ? 8 : s;
 }
 
-__host__ inline int tc_smem_bytes(int bn, int planes, int stages) {
-    return 1024 /*align slack*/ + stages * tc_stage_bytes(bn, planes) + 256 /*barriers*/;
+__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages) {
+    return 1024 /*align slack*/ + stages * tc_stage_bytes(b_rows, tps) + 256 /*barriers*/;
 }
 
 __host__ __device__ inline uint32_t tmem_cols_for(int bn) {
@@ -204,9 +215,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int stages = p.stages;
     const int tile_m = kTileM * CG;               // D rows per tile (the pair's rows for CG = 2)
     const int b_rows = bn / CG;                   // B rows this CTA loads
-    const int a_bytes = kTileM * kRowBytes;       // A rows of one stage
-    const int b_bytes = b_rows * kRowBytes;       // B rows of one stage
+    const int tps = p.tps;
+    const int a_bytes = tc_a_bytes(tps);          // A region of one stage (128 + tps - 1 rows)
+    const int b_bytes = tps * b_rows * kRowBytes; // B rows of one stage (tps taps)
     const int stage_bytes = a_bytes + b_bytes;
+    const uint32_t stage_tx = (uint32_t)((tc_a_box_rows(tps) + tps * b_rows) * kRowBytes);
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;       // scheduling unit
@@ -252,7 +265,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int k_iters = p.taps * p.kblocks;
+    const int k_iters = (p.taps / tps) * p.kblocks;   // stages per tile
     const int cpt = p.chunks_per_tile;
     const int ci = p.chunk_iters;
 
@@ -268,7 +281,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         {
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t tx = (uint32_t)(CG * stage_bytes);   // both CTAs' bytes land on the leader
+            const uint32_t tx = (uint32_t)CG * stage_tx;   // both CTAs' bytes land on the leader
             Sched sch(p, unit, nunits);
             Piece pc;
             while (sch.next(pc)) {
@@ -279,12 +292,14 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const OperandCoord cb = operand_coord(p.b_mode, p.b_tap3, nt * bn + (int)rank * b_rows, p.P, p.Q, p.pad);
                 const int it0 = pc.c_lo * ci;
                 const int it1 = pc.c_hi * ci < k_iters ? pc.c_hi * ci : k_iters;
-                // (tap, channel block) of it0; then walk with counters, no division in the loop
-                int tap = p.tap_begin + it0 / p.kblocks;
+                // (tap group, channel block) of it0; then walk with counters, no division in the loop
+                int grp = p.tap_begin / tps + it0 / p.kblocks;
                 int kb = it0 - (it0 / p.kblocks) * p.kblocks;
+                int tap = grp * tps;
                 int ti = tap / p.ksize, tj = tap - (tap / p.ksize) * p.ksize;
                 for (int it = it0; it < it1; ++it) {
                     const int kc = kb * p.row_elems;
+                    const int arow = ca.c1 + grp * p.a_row_shift;   // padded-row mode: tap row i -> +i Wp
                     mbar_wait(&empty[stage], phase ^ 1u);
                     uint8_t* a_st = smem + stage * stage_bytes;
                     if (elect_one()) {
@@ -294,7 +309,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         if (ca.mode == LOAD_IM2COL)
                             tma_load_im2col_4d_2sm(&map_a, lbar, a_st, kc, ca.c1, ca.c2, ca.c3, (uint16_t)tj, (uint16_t)ti);
                         else
-                            tma_load_3d_2sm(&map_a, lbar, a_st, kc, ca.c1, ca.tap3 ? tap : 0);
+                            tma_load_3d_2sm(&map_a, lbar, a_st, kc, arow, ca.tap3 ? tap : 0);
                         if (cb.mode == LOAD_IM2COL)
                             tma_load_im2col_4d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.c2, cb.c3, (uint16_t)tj,
                                                    (uint16_t)ti);
@@ -302,7 +317,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             tma_load_3d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.tap3 ? tap : 0);
                     } else {
                         mbar_arrive_expect_tx(&full[stage], tx);
-                        load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
+                        if (ca.mode == LOAD_IM2COL)
+                            load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
+                        else
+                            tma_load_3d(&map_a, &full[stage], a_st, kc, arow, ca.tap3 ? tap : 0);
                         load_operand(&map_b, cb, &full[stage], a_st + a_bytes, kc, tap, ti, tj);
                     }
                     }
@@ -313,9 +331,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     }
                     if (++kb == p.kblocks) {
                         kb = 0;
-                        ++tap;
-                        if (++tj == p.ksize) {
-                            tj = 0;
+                        ++grp;
+                        tap += tps;
+                        tj += tps;
+                        while (tj >= p.ksize) {
+                            tj -= p.ksize;
                             ++ti;
                         }
                     }
@@ -368,32 +388,38 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 for (int it = c0; it < c1; ++it) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint64_t da = desc0 + (uint64_t)stage * st_step;
-                    const uint64_t db = da + b_off;
-                    const uint32_t first = it > c0 ? 1u : 0u;
+                    const uint64_t da0 = desc0 + (uint64_t)stage * st_step;
+                    const uint64_t db0 = da0 + b_off;
                     if (elect_one()) {
-                    if (planes == 2) {
-                        // row = [hi 16 | lo 16]: k-step s (8 tf32 = 32 B = 2 desc units) of hi at
-                        // +2 s, of lo at +4 + 2 s; small cross terms first
-                        mma(d_tmem, da + 4, db, first);
-                        mma(d_tmem, da, db + 4, 1u);
-                        mma(d_tmem, da, db, 1u);
-                        mma(d_tmem, da + 6, db + 2, 1u);
-                        mma(d_tmem, da + 2, db + 6, 1u);
-                        mma(d_tmem, da + 2, db + 2, 1u);
-                    } else if (planes == 3) {
-                        // 64 bf16 per row: 4 k-steps of 16 elements (32 B = 2 desc units)
-                        mma16(d_tmem, da, db, first);
-                        mma16(d_tmem, da + 2, db + 2, 1u);
-                        mma16(d_tmem, da + 4, db + 4, 1u);
-                        mma16(d_tmem, da + 6, db + 6, 1u);
-                    } else {
-                        mma(d_tmem, da, db, first);
-                        mma(d_tmem, da + 2, db + 2, 1u);
-                        mma(d_tmem, da + 4, db + 4, 1u);
-                        mma(d_tmem, da + 6, db + 6, 1u);
-                    }
-                    commit(&empty[stage]);          // frees the smem stage(s) once these MMAs retire
+                        for (int t = 0; t < tps; ++t) {
+                            // tap t of the group: A shifted by t rows (8 desc units of 16 B per
+                            // 128 B row), B = the t-th tap's weight tile
+                            const uint64_t da = da0 + (uint64_t)(t * 8);
+                            const uint64_t db = db0 + (uint64_t)(t * b_rows * 8);
+                            const uint32_t first = (it > c0 || t > 0) ? 1u : 0u;
+                            if (planes == 2) {
+                                // row = [hi 16 | lo 16]: k-step s (8 tf32 = 32 B = 2 desc units) of
+                                // hi at +2 s, of lo at +4 + 2 s; small cross terms first
+                                mma(d_tmem, da + 4, db, first);
+                                mma(d_tmem, da, db + 4, 1u);
+                                mma(d_tmem, da, db, 1u);
+                                mma(d_tmem, da + 6, db + 2, 1u);
+                                mma(d_tmem, da + 2, db + 6, 1u);
+                                mma(d_tmem, da + 2, db + 2, 1u);
+                            } else if (planes == 3) {
+                                // 64 bf16 per row: 4 k-steps of 16 elements (32 B = 2 desc units)
+                                mma16(d_tmem, da, db, first);
+                                mma16(d_tmem, da + 2, db + 2, 1u);
+                                mma16(d_tmem, da + 4, db + 4, 1u);
+                                mma16(d_tmem, da + 6, db + 6, 1u);
+                            } else {
+                                mma(d_tmem, da, db, first);
+                                mma(d_tmem, da + 2, db + 2, 1u);
+                                mma(d_tmem, da + 4, db + 4, 1u);
+                                mma(d_tmem, da + 6, db + 6, 1u);
+                            }
+                        }
+                        commit(&empty[stage]);      // frees the smem stage(s) once these MMAs retire
                     }
                     __syncwarp();
                     if (++stage == stages) {
@@ -490,7 +516,26 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 }
             }
             // ---- store the finished tile ----
-            if (row < p.rows) {
+            if (row < p.rows && p.epi == EPI_NCHW_PADDED) {
+                // padded output space: row = n*Hp*Wp + y*Wp + x; only y < P, x < Q are outputs
+                const int hw = p.epi_hp * p.epi_wp;
+                const int n = row / hw;
+                const int rem = row - n * hw;
+                const int y = rem / p.epi_wp;
+                const int xq = rem - y * p.epi_wp;
+                if (n < p.epi_n && y < p.P && xq < p.Q) {
+                    float* dst = p.out + ((long long)n * p.out_channels) * p.pq_out + (long long)y * p.Q + xq;
+#pragma unroll
+                    for (int j = 0; j < 128; ++j) {
+                        const int col = col0 + j;
+                        if (j < hcols && col < p.cols) {
+                            float* o = dst + (long long)col * p.pq_out;
+                            if (p.accumulate) *o += sum[j];
+                            else *o = sum[j];
+                        }
+                    }
+                }
+            } else if (row < p.rows) {
                 if (p.epi == EPI_NCHW) {
                     const int n = row / p.pq_out;
                     const int pq = row - n * p.pq_out;

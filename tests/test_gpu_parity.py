@@ -315,3 +315,43 @@ def test_harness_benchmark_gpu(oracle, clb, torch_cuda):
     y = clb.run_method("kn2row-gpu", torch_cuda.from_numpy(x).cuda(), torch_cuda.from_numpy(w).cuda())
     assert harness.fnv1a(y) == r.output_checksum
     assert harness.parse_csv(harness.emit_csv([r]))[0].csv_equal(r)
+
+
+_PADDED_SCRIPT = r'''
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+from oracle import oracle as O
+import paper_1704_04428_b200 as clb
+out = []
+for (N, C, H, W, M, k, pad) in [(2, 16, 30, 34, 32, 3, 1), (1, 48, 20, 24, 100, 5, 2), (2, 20, 17, 19, 64, 7, 3),
+                                 (2, 24, 21, 23, 40, 3, 0), (3, 64, 12, 12, 64, 3, 2), (64, 8, 5, 6, 16, 3, 1)]:
+    x, w = O.make_problem(N, C, H, W, M, k, N + C)
+    layer = clb.LayerConfig("p", C, H, W, M, k, 1, pad, N)
+    with clb.ConvPlan(layer, "kn2row-gpu") as plan:
+        plan.set_weights(torch.from_numpy(w).cuda())
+        y = plan.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    m = O.parity_metrics(y, O.conv_loopnest(x, w, pad, 1))
+    out.append({"shape": [N, C, H, W, M, k, pad], "rel_l2": m["rel_l2"], "max_rel": m["max_rel"]})
+print(json.dumps(out))
+'''
+
+
+@pytest.mark.parametrize("mode", ["1", "0"])
+def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
+    """The implicit kernel's tap-shared mode (zero-padded NHWC rows, one A box of 128+k-1 rows
+    per kernel row, taps through row-shifted UMMA descriptors), forced on and off via
+    CLB_PADDED_ROWS in a subprocess: k = 3/5/7, pad != k/2, batch-spanning tiles."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    script = tmp_path / "padded.py"
+    script.write_text(_PADDED_SCRIPT)
+    r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, CLB_PADDED_ROWS=mode))
+    assert r.returncode == 0, r.stderr[-3000:]
+    for res in json.loads(r.stdout.strip().splitlines()[-1]):
+        assert res["rel_l2"] <= FP32_L2 and res["max_rel"] <= FP32_MAX, (mode, res)

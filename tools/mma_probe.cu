@@ -1,0 +1,84 @@
+// mma_probe.cu -- raw tcgen05.mma.kind::tf32 throughput vs N with operands resident in smem
+// (no TMA): 148 CTAs, one elected thread issues `iters` x 6 MMAs (the 3xTF32 pattern of one
+// 16-channel stage) back to back, one commit per stage-equivalent; cycles per MMA reported.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "ptx.cuh"
+
+using namespace clb;
+
+__global__ void probe(int n, int iters, int stages_per_commit, unsigned long long* cyc) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    // zero the operand tiles (values irrelevant for timing)
+    for (int i = threadIdx.x; i < (128 + 256) * 32; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 0.0f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 0) tmem_alloc(&tslot, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (warp == 1) {
+        const uint64_t da = umma_desc_kmajor(smem_u32(smem), 128);
+        const uint64_t db = umma_desc_kmajor(smem_u32(smem + 128 * 128), 128);
+        const uint32_t idesc = idesc_tf32(128, (uint32_t)n);
+        uint32_t ph = 0;
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            if (elect_one()) {
+                for (int s = 0; s < stages_per_commit; ++s) {
+                    mma_tf32_ss(tmem, da + 4, db, idesc, (it | s) ? 1u : 0u);
+                    mma_tf32_ss(tmem, da, db + 4, idesc, 1u);
+                    mma_tf32_ss(tmem, da, db, idesc, 1u);
+                    mma_tf32_ss(tmem, da + 6, db + 2, idesc, 1u);
+                    mma_tf32_ss(tmem, da + 2, db + 6, idesc, 1u);
+                    mma_tf32_ss(tmem, da + 2, db + 2, idesc, 1u);
+                }
+                mma_commit(&bar);
+            }
+            __syncwarp();
+            mbar_wait(&bar, ph);   // one batch in flight: cost = batch MMA time + commit round trip
+            ph ^= 1u;
+        }
+        if (lane_id() == 0) cyc[blockIdx.x] = clock64() - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
+int main(int argc, char** argv) {
+    const int only_n = argc > 1 ? atoi(argv[1]) : 0;
+    unsigned long long* cyc;
+    cudaMalloc(&cyc, 148 * 8);
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int spc : {1, 4, 16}) {
+        for (int n : {64, 128, 192, 256}) {
+            if (only_n && n != only_n) continue;
+            const int iters = 2000;
+            probe<<<148, 128, 64 * 1024>>>(n, iters, spc, cyc);
+            cudaError_t e = cudaDeviceSynchronize();
+            std::vector<unsigned long long> h(148);
+            cudaMemcpy(h.data(), cyc, 148 * 8, cudaMemcpyDeviceToHost);
+            double avg = 0;
+            for (auto v : h) avg += v;
+            avg /= 148;
+            const double per_mma = avg / (iters * 6.0 * spc);
+            printf("N=%3d stages/commit=%d: %s  %.1f cycles/MMA (ideal %d)  -> %.0f%% of the tensor-core rate\n", n,
+                   spc, cudaGetErrorString(e), per_mma, n / 2, 100.0 * (n / 2) / per_mma);
+        }
+    }
+    return 0;
+}
