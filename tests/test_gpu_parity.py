@@ -355,3 +355,39 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     assert r.returncode == 0, r.stderr[-3000:]
     for res in json.loads(r.stdout.strip().splitlines()[-1]):
         assert res["rel_l2"] <= FP32_L2 and res["max_rel"] <= FP32_MAX, (mode, res)
+
+
+GUARD_CASES = [(2, 16, 13, 13, 32, 3, 1), (4, 64, 28, 28, 256, 3, 1), (3, 8, 9, 11, 24, 5, 2), (2, 3, 17, 19, 16, 3, 1),
+               (1, 40, 7, 7, 130, 1, 0), (2, 32, 15, 15, 72, 7, 3)]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("method", METHODS)
+def test_guard_bands(oracle, clb, torch_cuda, method, precision):
+    """Out-of-bounds write check (stand-in for a memcheck run): output and workspace live inside
+    larger buffers filled with a NaN-payload sentinel; after the call every guard word must be
+    untouched and the result must still match the oracle."""
+    torch = torch_cuda
+    G = 1 << 16
+    sentinel = np.array([0x7FC0DEAD], dtype=np.uint32).view(np.float32)[0]
+    for N, C, H, W, M, k, pad in GUARD_CASES:
+        if method == "direct-gpu" and (precision != "fp32" or C > 4):
+            continue
+        layer = clb.LayerConfig("guard", C, H, W, M, k, pad=pad, batch=N)
+        x, w = oracle.make_problem(N, C, H, W, M, k, N * 1000 + C)
+        with clb.ConvPlan(layer, method, precision) as plan:
+            plan.set_weights(torch.from_numpy(w).cuda())
+            out = int(np.prod(plan.output_shape()))
+            wsn = (plan.workspace_bytes() + 3) // 4
+            ybuf = torch.full((out + 2 * G,), float(sentinel), device="cuda")
+            wbuf = torch.full((wsn + 2 * G,), float(sentinel), device="cuda")
+            y = ybuf[G:G + out].view(plan.output_shape())
+            plan.forward(torch.from_numpy(x).cuda(), y, wbuf[G:G + wsn] if wsn else None)
+            torch.cuda.synchronize()
+            for name, buf, n in (("output", ybuf, out), ("workspace", wbuf, wsn)):
+                bits = buf.cpu().numpy().view(np.uint32)
+                bad = np.count_nonzero(bits[:G] != 0x7FC0DEAD) + np.count_nonzero(bits[G + n:] != 0x7FC0DEAD)
+                assert bad == 0, (method, precision, (N, C, H, W, M, k, pad), name, bad)
+            ref = oracle.conv_loopnest(x, w, pad, 1)
+            m = oracle.parity_metrics(y.cpu().numpy(), ref)
+            assert m["finite"] and m["rel_l2"] <= (FP32_L2 if precision == "fp32" else TF32_L2), (method, m)
