@@ -391,3 +391,18 @@ def test_guard_bands(oracle, clb, torch_cuda, method, precision):
             ref = oracle.conv_loopnest(x, w, pad, 1)
             m = oracle.parity_metrics(y.cpu().numpy(), ref)
             assert m["finite"] and m["rel_l2"] <= (FP32_L2 if precision == "fp32" else TF32_L2), (method, m)
+
+
+DIRECT_CASES = [(1, 3, 224, 224, 64, 3, 1), (3, 3, 20, 36, 70, 3, 1), (2, 1, 9, 8, 5, 5, 2), (2, 4, 33, 12, 17, 1, 0),
+                (1, 2, 40, 64, 33, 7, 3), (2, 3, 30, 10, 16, 3, 0), (1, 4, 5, 4, 8, 3, 1), (2, 3, 64, 200, 48, 5, 2)]
+
+
+@pytest.mark.parametrize("case", DIRECT_CASES)
+def test_direct_unit_kernel(oracle, clb, torch_cuda, case):
+    """direct-gpu's persistent unit kernel (Q % 4 == 0: 256-group units spanning rows, full-width
+    halos) and its fallback, against the generalised loop nest, incl. pad != k/2."""
+    N, C, H, W, M, k, pad = case
+    x, w = oracle.make_problem(N, C, H, W, M, k, sum(case))
+    ref = oracle.conv_loopnest(x, w, pad, 1)
+    y = _run(clb, torch_cuda, "direct-gpu", x, w, pad=pad)
+    _check_fp32(oracle, y, ref, f"direct {case}")
