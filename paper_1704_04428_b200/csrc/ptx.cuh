@@ -197,7 +197,7 @@ __device__ __forceinline__ void cluster_sync() {
 
 // arrive on an mbarrier of another CTA of the cluster (shared::cluster address)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 // TMA loads whose completion bytes land on the LEADER CTA's mbarrier (cta_group::2).

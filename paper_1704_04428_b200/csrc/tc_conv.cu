@@ -1,6 +1,9 @@
 // tc_conv.cu -- host side of the tcgen05 engine: TMA tensor-map encoding (tiled and
 // im2col) and the persistent launch.  The kernel itself lives in tc_conv.cuh.
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #define CLB_DEFINE_TC_KERNEL 1
 #include "internal.hpp"
@@ -165,9 +168,33 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
+    // CLB_TRACE=1: per-CTA role wait cycles (diagnostics only; synchronises after the launch)
+    static const bool trace = getenv("CLB_TRACE") && atoi(getenv("CLB_TRACE")) != 0;
+    static unsigned long long* trace_buf = nullptr;
+    if (trace) {
+        if (!trace_buf) CLB_CUDA(cudaMalloc(&trace_buf, (size_t)kMaxGrid * 8 * sizeof(unsigned long long)));
+        CLB_CUDA(cudaMemsetAsync(trace_buf, 0, (size_t)kMaxGrid * 8 * sizeof(unsigned long long), s));
+        p.trace = trace_buf;
+        p.pdl = 0;
+        cfg.numAttrs = 1;   // no PDL: the trace needs the launch to be self-contained
+    }
     cudaError_t e = cg == 2 ? cudaLaunchKernelEx(&cfg, tc_conv_kernel<2>, ma, mb, p)
                             : cudaLaunchKernelEx(&cfg, tc_conv_kernel<1>, ma, mb, p);
     CLB_CUDA(e);
+    if (trace) {
+        std::vector<unsigned long long> h((size_t)grid * 8);
+        CLB_CUDA(cudaMemcpyAsync(h.data(), trace_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        CLB_CUDA(cudaStreamSynchronize(s));
+        double avg[8] = {0};
+        for (int b = 0; b < grid; ++b)
+            for (int i = 0; i < 8; ++i) avg[i] += (double)h[(size_t)b * 8 + i] / grid;
+        fprintf(stderr,
+                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stages=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
+                "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
+                "store %.0f%%)\n",
+                p.rows, p.cols, p.bn, cg, p.tps, p.stages, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
+                avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5]);
+    }
 }
 
 size_t tc_scratch_bytes() {

@@ -89,6 +89,7 @@ struct TcParams {
     unsigned* flags;           // [gridDim.x], 0 at launch; 1 = partial ready (the finisher resets it)
     int flags_zeroed;          // flags are known to be 0 (self-resetting plan buffer): no memset
     int pdl;                   // launched as a programmatic dependent: wait before touching inputs
+    unsigned long long* trace; // diagnostics (CLB_TRACE=1): per-CTA role wait cycles, else null
 };
 
 // Contiguous chunk range of CTA b: [chunk_start(b), chunk_start(b+1)).
@@ -197,6 +198,25 @@ struct Sched {
     }
 };
 
+// One D row's columns into NCHW planes: column j lands at o + j * plane.  The accumulate
+// branch is hoisted and the address walks by one plane per column, so each element costs a
+// predicated store and a pointer add (a warp's 32 rows make each store one 128 B line).
+__device__ __forceinline__ void store_nchw(float* o, long long plane, int nvalid, int accumulate, const float* sum) {
+    if (accumulate) {
+#pragma unroll
+        for (int j = 0; j < 128; ++j) {
+            if (j < nvalid) *o += sum[j];
+            o += plane;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 128; ++j) {
+            if (j < nvalid) *o = sum[j];
+            o += plane;
+        }
+    }
+}
+
 // CG = 1: one CTA per 128-row tile (tcgen05 cta_group::1).
 // CG = 2: a CTA pair (cluster of 2) per 256-row tile (cta_group::2): each CTA TMA-loads its
 //         128 A rows and HALF of the BN B rows into its own smem, all completion bytes land
@@ -282,6 +302,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t tx = (uint32_t)CG * stage_tx;   // both CTAs' bytes land on the leader
+            long long w_empty = 0;
+            const long long t_start = clock64();
             Sched sch(p, unit, nunits);
             Piece pc;
             while (sch.next(pc)) {
@@ -300,7 +322,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 for (int it = it0; it < it1; ++it) {
                     const int kc = kb * p.row_elems;
                     const int arow = ca.c1 + grp * p.a_row_shift;   // padded-row mode: tap row i -> +i Wp
-                    mbar_wait(&empty[stage], phase ^ 1u);
+                    if (p.trace) {
+                        const long long t0 = clock64();
+                        mbar_wait(&empty[stage], phase ^ 1u);
+                        w_empty += clock64() - t0;
+                    } else {
+                        mbar_wait(&empty[stage], phase ^ 1u);
+                    }
                     uint8_t* a_st = smem + stage * stage_bytes;
                     if (elect_one()) {
                     if constexpr (CG == 2) {
@@ -341,6 +369,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     }
                 }
             }
+            if (p.trace && lane_id() == 0) {
+                p.trace[blockIdx.x * 8 + 0] = (unsigned long long)(clock64() - t_start);
+                p.trace[blockIdx.x * 8 + 1] = (unsigned long long)w_empty;
+            }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer ----
@@ -377,16 +409,30 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint64_t desc0 = umma_desc_kmajor(smem_u32(smem), kRowBytes);
             const uint64_t st_step = (uint64_t)(stage_bytes >> 4);
             const uint64_t b_off = (uint64_t)(a_bytes >> 4);
+            long long w_full = 0, w_tempty = 0;
+            const long long t_start = clock64();
             while (sch.next(pc))
             for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
                 const int c0 = c * ci;
                 const int c1 = c0 + ci < k_iters ? c0 + ci : k_iters;
                 const uint32_t buf = lg & 1u;
-                mbar_wait(&tempty[buf], ((lg >> 1) & 1u) ^ 1u);
+                if (p.trace) {
+                    const long long t0 = clock64();
+                    mbar_wait(&tempty[buf], ((lg >> 1) & 1u) ^ 1u);
+                    w_tempty += clock64() - t0;
+                } else {
+                    mbar_wait(&tempty[buf], ((lg >> 1) & 1u) ^ 1u);
+                }
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + buf * (ncols / 2);
                 for (int it = c0; it < c1; ++it) {
-                    mbar_wait(&full[stage], phase);
+                    if (p.trace) {
+                        const long long t0 = clock64();
+                        mbar_wait(&full[stage], phase);
+                        w_full += clock64() - t0;
+                    } else {
+                        mbar_wait(&full[stage], phase);
+                    }
                     tc_fence_after();
                     const uint64_t da0 = desc0 + (uint64_t)stage * st_step;
                     const uint64_t db0 = da0 + b_off;
@@ -430,6 +476,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 if (elect_one()) commit(&tfull[buf]);   // chunk complete -> epilogue(s)
                 __syncwarp();
             }
+            if (p.trace && lane_id() == 0) {
+                p.trace[blockIdx.x * 8 + 2] = (unsigned long long)(clock64() - t_start);
+                p.trace[blockIdx.x * 8 + 3] = (unsigned long long)w_full;
+                p.trace[blockIdx.x * 8 + 4] = (unsigned long long)w_tempty;
+            }
         }
     } else if (warp >= 4) {
         // --------------------------------------------------------------- epilogue ----
@@ -443,6 +494,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const int cbase = half * hcols;
         const int trow = quad * 32 + lane;           // row within this CTA's 128 rows
         uint32_t lg = 0;
+        long long w_tfull = 0, w_store = 0;
+        const long long t_start = clock64();
         Sched sch(p, unit, nunits);
         Piece pc;
         while (sch.next(pc)) {
@@ -455,7 +508,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             for (int j = 0; j < 128; ++j) sum[j] = 0.0f;
             for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
                 const uint32_t buf = lg & 1u;
-                mbar_wait(&tfull[buf], (lg >> 1) & 1u);
+                if (p.trace) {
+                    const long long t0 = clock64();
+                    mbar_wait(&tfull[buf], (lg >> 1) & 1u);
+                    w_tfull += clock64() - t0;
+                } else {
+                    mbar_wait(&tfull[buf], (lg >> 1) & 1u);
+                }
                 tc_fence_after();
                 const uint32_t t_addr =
                     tmem_base + ((uint32_t)(quad * 32) << 16) + buf * (ncols / 2) + (uint32_t)cbase;
@@ -516,6 +575,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 }
             }
             // ---- store the finished tile ----
+            const long long t_st = p.trace ? clock64() : 0;
             if (row < p.rows && p.epi == EPI_NCHW_PADDED) {
                 // padded output space: row = n*Hp*Wp + y*Wp + x; only y < P, x < Q are outputs
                 const int hw = p.epi_hp * p.epi_wp;
@@ -523,32 +583,15 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const int rem = row - n * hw;
                 const int y = rem / p.epi_wp;
                 const int xq = rem - y * p.epi_wp;
-                if (n < p.epi_n && y < p.P && xq < p.Q) {
-                    float* dst = p.out + ((long long)n * p.out_channels) * p.pq_out + (long long)y * p.Q + xq;
-#pragma unroll
-                    for (int j = 0; j < 128; ++j) {
-                        const int col = col0 + j;
-                        if (j < hcols && col < p.cols) {
-                            float* o = dst + (long long)col * p.pq_out;
-                            if (p.accumulate) *o += sum[j];
-                            else *o = sum[j];
-                        }
-                    }
-                }
+                if (n < p.epi_n && y < p.P && xq < p.Q)
+                    store_nchw(p.out + ((long long)n * p.out_channels + col0) * p.pq_out + (long long)y * p.Q + xq,
+                               p.pq_out, min(hcols, p.cols - col0), p.accumulate, sum);
             } else if (row < p.rows) {
                 if (p.epi == EPI_NCHW) {
                     const int n = row / p.pq_out;
                     const int pq = row - n * p.pq_out;
-                    float* dst = p.out + ((long long)n * p.out_channels) * p.pq_out + pq;
-#pragma unroll
-                    for (int j = 0; j < 128; ++j) {
-                        const int col = col0 + j;
-                        if (j < hcols && col < p.cols) {
-                            float* o = dst + (long long)col * p.pq_out;
-                            if (p.accumulate) *o += sum[j];
-                            else *o = sum[j];
-                        }
-                    }
+                    store_nchw(p.out + ((long long)n * p.out_channels + col0) * p.pq_out + pq, p.pq_out,
+                               min(hcols, p.cols - col0), p.accumulate, sum);
                 } else {
                     float* dst = p.out + (long long)row * p.ld + col0;
                     const bool vec = (p.ld % 4 == 0) && !p.accumulate;
@@ -569,6 +612,12 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     }
                 }
             }
+            if (p.trace) w_store += clock64() - t_st;
+        }
+        if (p.trace && threadIdx.x == 4 * 32) {
+            p.trace[blockIdx.x * 8 + 5] = (unsigned long long)(clock64() - t_start);
+            p.trace[blockIdx.x * 8 + 6] = (unsigned long long)w_tfull;
+            p.trace[blockIdx.x * 8 + 7] = (unsigned long long)w_store;
         }
     }
 
