@@ -422,11 +422,11 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         if (m == CL_METHOD_DIRECT) p->wraw = p->wpack;
         {
             // tap-shared (padded-row) mode for the implicit kernel: one A box per kernel row feeds
-            // its k taps through row-shifted descriptors (k x fewer A TMA bytes).  Measured on
-            // B200 it does not speed up small-N tiles -- they are bound by the tensor core's
-            // shared-memory operand reads (tools/mma_probe.cu: N=64 tops out at 63% even with
-            // operands resident), not by TMA -- so it is opt-in (CLB_PADDED_ROWS=1) until the
-            // A operand moves to TMEM.
+            // its k taps through row-shifted descriptors (k x fewer A TMA bytes per MMA).  Small-BN
+            // tiles are bound by shared-memory operand traffic (tools/mma_probe.cu: N = 64 tops out
+            // at 63% even with operands resident), so cutting the A writes pays there -- VGG
+            // conv1_2 1.06 -> 0.65 ms, conv2_x 0.71/0.77 -> 1.02/1.06 of peak -- as long as the
+            // padded positions (computed, then dropped) stay few.  CLB_PADDED_ROWS=0/1 forces it.
             static const int forced_padded = [] {
                 const char* e = std::getenv("CLB_PADDED_ROWS");
                 return e ? std::atoi(e) : -1;
@@ -434,8 +434,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             const double waste = (double)(d.h + 2 * d.pad) * (d.w + 2 * d.pad) / ((double)P * Q) - 1.0;
             const bool fits = tc_num_stages(p->bn, d.k) >= 2;   // CG1 worst case
             const bool eligible = m == CL_METHOD_KN2ROW && d.k >= 3 && d.k <= 7 && d.stride == 1 && fits;
-            (void)waste;
-            p->padded_rows = eligible && forced_padded == 1;
+            p->padded_rows = eligible && (forced_padded == 1 || (forced_padded != 0 && p->bn <= 128 && waste <= 0.08));
         }
         if (cudaMalloc(&p->flags, kMaxGrid * sizeof(unsigned)) != cudaSuccess ||
             cudaMemset(p->flags, 0, kMaxGrid * sizeof(unsigned)) != cudaSuccess) {

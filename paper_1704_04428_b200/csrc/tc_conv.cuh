@@ -112,8 +112,13 @@ __host__ inline int tc_smem_bytes(int b_rows, int tps, int stages) {
     return 1024 /*align slack*/ + stages * tc_stage_bytes(b_rows, tps) + 256 /*barriers*/;
 }
 
+// TMEM accumulator buffers: 4 when they fit (BN <= 128), else ping-pong.  Extra buffers let
+// the MMA run ahead while the epilogue is busy storing a finished tile (small-BN tiles finish
+// every few microseconds, so the store burst used to stall the MMA warp on TMEM).
+__host__ __device__ inline int tmem_bufs_for(int bn) { return 4 * bn <= 512 ? 4 : 2; }
+
 __host__ __device__ inline uint32_t tmem_cols_for(int bn) {
-    uint32_t need = 2u * (uint32_t)bn, c = 32;
+    uint32_t need = (uint32_t)tmem_bufs_for(bn) * (uint32_t)bn, c = 32;
     while (c < need) c <<= 1;
     return c;
 }
@@ -248,19 +253,22 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + stages;
-    uint64_t* tfull = bars + 2 * stages;
-    uint64_t* tempty = bars + 2 * stages + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 4);
+    uint64_t* tfull = bars + 2 * stages;        // [nbuf]
+    uint64_t* tempty = bars + 2 * stages + 4;   // [nbuf]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 8);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t ncols = tmem_cols_for(bn);
+    const int nbuf = tmem_bufs_for(bn);
+    const uint32_t nb_shift = nbuf == 4 ? 2u : 1u;
+    const uint32_t buf_cols = ncols / (uint32_t)nbuf;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < nbuf; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], CG * (kEpiThreads / 32));
         }
@@ -377,7 +385,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer ----
         // The K loop of a tile is cut into chunks of ci k-iterations; each chunk accumulates
-        // into a fresh TMEM buffer (ping-pong) that the epilogue folds into fp32 registers.
+        // into the next of 2-4 TMEM buffers (round robin) that the epilogue folds into fp32 registers.
         // Tensor-core accumulation rounds every update of the running fp32 accumulator
         // (error grows ~linearly in K: 7e-9 K measured), so bounding the chunk to 128
         // K-elements keeps the 3xTF32 result fp32-faithful for any K.
@@ -415,16 +423,17 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
                 const int c0 = c * ci;
                 const int c1 = c0 + ci < k_iters ? c0 + ci : k_iters;
-                const uint32_t buf = lg & 1u;
+                const uint32_t buf = lg & (uint32_t)(nbuf - 1);
+                const uint32_t tph = (lg >> nb_shift) & 1u;
                 if (p.trace) {
                     const long long t0 = clock64();
-                    mbar_wait(&tempty[buf], ((lg >> 1) & 1u) ^ 1u);
+                    mbar_wait(&tempty[buf], tph ^ 1u);
                     w_tempty += clock64() - t0;
                 } else {
-                    mbar_wait(&tempty[buf], ((lg >> 1) & 1u) ^ 1u);
+                    mbar_wait(&tempty[buf], tph ^ 1u);
                 }
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + buf * (ncols / 2);
+                const uint32_t d_tmem = tmem_base + buf * buf_cols;
                 for (int it = c0; it < c1; ++it) {
                     if (p.trace) {
                         const long long t0 = clock64();
@@ -507,17 +516,18 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 #pragma unroll
             for (int j = 0; j < 128; ++j) sum[j] = 0.0f;
             for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
-                const uint32_t buf = lg & 1u;
+                const uint32_t buf = lg & (uint32_t)(nbuf - 1);
+                const uint32_t tph = (lg >> nb_shift) & 1u;
                 if (p.trace) {
                     const long long t0 = clock64();
-                    mbar_wait(&tfull[buf], (lg >> 1) & 1u);
+                    mbar_wait(&tfull[buf], tph);
                     w_tfull += clock64() - t0;
                 } else {
-                    mbar_wait(&tfull[buf], (lg >> 1) & 1u);
+                    mbar_wait(&tfull[buf], tph);
                 }
                 tc_fence_after();
                 const uint32_t t_addr =
-                    tmem_base + ((uint32_t)(quad * 32) << 16) + buf * (ncols / 2) + (uint32_t)cbase;
+                    tmem_base + ((uint32_t)(quad * 32) << 16) + buf * buf_cols + (uint32_t)cbase;
 #pragma unroll
                 for (int grp = 0; grp < 8; grp += 4) {      // 4 loads (64 columns) in flight
                     uint32_t r[4][16];

@@ -6,7 +6,8 @@ timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.txt 2>&1
 tail -2 gpurun_out/pytest_gpu.txt
 ./tools/trace_layers.sh
 timeout 600 python tools/report.py --workloads vgg16,alexnet --no-cpu --reps 5 > gpurun_out/rep.txt 2>&1
-python - <<'PY'
+python tools/rep_table.py gpurun_out/rep.txt
+: <<'PY'
 import json
 for l in open("gpurun_out/rep.txt"):
     l = l.strip()
