@@ -57,6 +57,19 @@ def parse_args():
     return ap.parse_args()
 
 
+NOMINAL_BF16 = 2250.0   # dense bf16 TFLOP/s, B200 nominal (B200_PROFILING.md, context only)
+
+
+def mma_peak_for(precision):
+    """Our own kind::tf32 MMA peak (tools/mma_probe.cu, committed under profiles/), in the
+    precision's effective units: 3xTF32 = /3; bf16 (kind::f16) = x2."""
+    f = Path(__file__).resolve().parent / "profiles" / "tf32_mma_peak.json"
+    if not f.exists():
+        return None
+    tf32 = json.loads(f.read_text())["tf32_mma_peak_tflops"]
+    return {"fp32": tf32 / 3.0, "tf32": tf32, "bf16": 2.0 * tf32}[precision]
+
+
 def peaks():
     try:
         p = json.loads(PEAKS_FILE.read_text())
@@ -374,7 +387,16 @@ def main():
                      "kernel": "tc_conv_kernel (tcgen05 kind::tf32 x3, TMA im2col)",
                      "kernel_ms_per_step": kernel_ms_step,
                      "peak_note": (f"3xTF32 peak = measured bf16 burst {pk['bf16']} / 2 (tf32 rate) / 3 (passes); "
-                                   f"{pk['source']}")},
+                                   f"{pk['source']}.  The bf16 figure is cuBLAS under its own power/clock "
+                                   "limits, so a tcgen05 kernel can exceed it; frac_of_nominal is against "
+                                   "the nominal dense 2250 TFLOP/s bf16 (same /2 /3)"),
+                     "measured_mma_peak": mma_peak_for(args.precision),
+                     "frac_of_measured_mma_peak": (achieved / mma_peak_for(args.precision)
+                                                   if mma_peak_for(args.precision) else None),
+                     "nominal_peak": NOMINAL_BF16 / 2.0 / (3.0 if args.precision == "fp32" else 1.0)
+                     * (1.0 if args.precision != "bf16" else 2.0),
+                     "frac_of_nominal": achieved / (NOMINAL_BF16 / 2.0 / (3.0 if args.precision == "fp32" else 1.0)
+                                                    * (1.0 if args.precision != "bf16" else 2.0))},
         "cpu_baseline": cpu,
         "clocks": clocks,
     }

@@ -218,10 +218,17 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         set_scratch(t, scratch);
         t.flags = p->flags;
         t.flags_zeroed = 1;
+        static const int forced_bn = [] {   // experiments: CLB_BN=<multiple of 16 <= 256>
+            const char* e = std::getenv("CLB_BN");
+            const int v = e ? std::atoi(e) : 0;
+            return (v >= 16 && v <= 256 && v % 16 == 0) ? v : 0;
+        }();
+        if (forced_bn && !p->padded_rows) t.bn = forced_bn;
         const int cg = cta_group_for(t.rows, t.cols, t.bn);
         // few tiles even at 128 rows: halve the tile N to create more of them (B operand rows
         // are tiny anyway at these sizes)
-        if (cg == 1 && t.bn >= 64 && (long long)(t.rows + 127) / 128 * ((t.cols + t.bn - 1) / t.bn) < num_sms() / 2)
+        if (!forced_bn && cg == 1 && t.bn >= 64 &&
+            (long long)(t.rows + 127) / 128 * ((t.cols + t.bn - 1) / t.bn) < num_sms() / 2)
             t.bn = round_up(t.bn / 2, 16);
         launch_tc(a, b, t, s, cg);
         ++p->launches;

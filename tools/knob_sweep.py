@@ -1,0 +1,36 @@
+"""Kernel time of selected layers under the current CLB_* environment (one line per layer).
+Driven by tools/gpu_knobs.sh, which re-runs it under each knob setting (the knobs are read
+once per process)."""
+import os
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+import paper_1704_04428_b200 as clb
+from paper_1704_04428_b200 import _lib, rng, workloads
+
+layers = sys.argv[1].split(",")
+tag = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("CLB_"))
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for name in layers:
+    group = name.split("/")[0]
+    layer = [l for l in workloads.workload(group) if l.name == name][0]
+    x, w = rng.make_problem(layer.batch, layer.channels, layer.height, layer.width, layer.kernel_count,
+                            layer.kernel_size)
+    with clb.ConvPlan(layer, "auto", "fp32") as plan:
+        plan.set_weights(w)
+        y = plan.forward(x)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(7):
+            flush.zero_()
+            kb, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            kb.record(); ke.record(); torch.cuda.synchronize()
+            _lib.lib().cl_conv_set_profile_events(plan._h, kb.cuda_event, ke.cuda_event)
+            plan.forward(x, y)
+            torch.cuda.synchronize()
+            ts.append(kb.elapsed_time(ke))
+        _lib.lib().cl_conv_set_profile_events(plan._h, None, None)
+    ts.sort()
+    ms = ts[len(ts) // 2]
+    print(f"{name:16s} {tag:40s} {ms:7.3f} ms {layer.flops() / ms / 1e9:7.1f} TF", flush=True)

@@ -12,7 +12,7 @@
 
 using namespace clb;
 
-__global__ void probe(int n, int iters, int stages_per_commit, unsigned long long* cyc) {
+__global__ void probe(int n, int iters, int stages_per_commit, unsigned long long* cyc, unsigned long long* ns) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar;
@@ -36,6 +36,7 @@ __global__ void probe(int n, int iters, int stages_per_commit, unsigned long lon
         const uint32_t idesc = idesc_tf32(128, (uint32_t)n);
         uint32_t ph = 0;
         const long long t0 = clock64();
+        const unsigned long long g0 = globaltimer_ns();
         for (int it = 0; it < iters; ++it) {
             if (elect_one()) {
                 for (int s = 0; s < stages_per_commit; ++s) {
@@ -52,7 +53,10 @@ __global__ void probe(int n, int iters, int stages_per_commit, unsigned long lon
             mbar_wait(&bar, ph);   // one batch in flight: cost = batch MMA time + commit round trip
             ph ^= 1u;
         }
-        if (lane_id() == 0) cyc[blockIdx.x] = clock64() - t0;
+        if (lane_id() == 0) {
+            cyc[blockIdx.x] = clock64() - t0;
+            ns[blockIdx.x] = globaltimer_ns() - g0;
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -61,24 +65,39 @@ __global__ void probe(int n, int iters, int stages_per_commit, unsigned long lon
 
 int main(int argc, char** argv) {
     const int only_n = argc > 1 ? atoi(argv[1]) : 0;
-    unsigned long long* cyc;
+    unsigned long long *cyc, *ns;
     cudaMalloc(&cyc, 148 * 8);
+    cudaMalloc(&ns, 148 * 8);
+    double best_tf = 0, best_mhz = 0;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     for (int spc : {1, 4, 16}) {
         for (int n : {64, 128, 192, 256}) {
             if (only_n && n != only_n) continue;
             const int iters = 2000;
-            probe<<<148, 128, 64 * 1024>>>(n, iters, spc, cyc);
+            probe<<<148, 128, 64 * 1024>>>(n, iters, spc, cyc, ns);
             cudaError_t e = cudaDeviceSynchronize();
-            std::vector<unsigned long long> h(148);
+            std::vector<unsigned long long> h(148), hn(148);
             cudaMemcpy(h.data(), cyc, 148 * 8, cudaMemcpyDeviceToHost);
-            double avg = 0;
-            for (auto v : h) avg += v;
+            cudaMemcpy(hn.data(), ns, 148 * 8, cudaMemcpyDeviceToHost);
+            double avg = 0, max_ns = 0;
+            for (int b = 0; b < 148; ++b) {
+                avg += h[b];
+                max_ns = hn[b] > max_ns ? hn[b] : max_ns;
+            }
             avg /= 148;
             const double per_mma = avg / (iters * 6.0 * spc);
-            printf("N=%3d stages/commit=%d: %s  %.1f cycles/MMA (ideal %d)  -> %.0f%% of the tensor-core rate\n", n,
-                   spc, cudaGetErrorString(e), per_mma, n / 2, 100.0 * (n / 2) / per_mma);
+            const double mhz = avg / max_ns * 1e3;
+            // whole-GPU kind::tf32 rate: 148 CTAs x (2 * 128 * N * 8) flops per MMA
+            const double tf = 148.0 * iters * 6.0 * spc * 2.0 * 128 * n * 8 / (max_ns * 1e-9) / 1e12;
+            if (tf > best_tf) best_tf = tf, best_mhz = mhz;
+            printf("N=%3d stages/commit=%2d: %s  %.1f cycles/MMA (ideal %d) -> %.0f%% of the tensor-core rate; "
+                   "%.0f TFLOP/s tf32 at %.0f MHz\n", n, spc, cudaGetErrorString(e), per_mma, n / 2,
+                   100.0 * (n / 2) / per_mma, tf, mhz);
         }
     }
+    printf("{\"tf32_mma_peak_tflops\": %.1f, \"sm_mhz\": %.0f, \"fp32_3xtf32_peak_tflops\": %.1f, "
+           "\"how\": \"tools/mma_probe.cu: 148 CTAs, operands resident in smem, back-to-back "
+           "tcgen05.mma.cta_group::1.kind::tf32 M=128 K=8, best N/batching\"}\n",
+           best_tf, best_mhz, best_tf / 3.0);
     return 0;
 }
