@@ -97,7 +97,7 @@ cl_method resolve(const cl_conv_desc& d, cl_method m) {
     // conv1_1, C = 3) waste 13/16 of every 16-channel K block per tap and are HBM-bound, so
     // they take the direct CUDA-core kernel (PAPER.md:484 found direct best on that layer
     // too); im2col remains for small C the direct kernel cannot stage.
-    if (d.c <= 4 && d.stride == 1 && d.k <= 11) return CL_METHOD_DIRECT;
+    if (d.c <= 4 && direct_fast_path(d.c, d.k, d.stride)) return CL_METHOD_DIRECT;
     if (d.k > 1 && d.c * 4 <= 16) return CL_METHOD_IM2COL;
     return CL_METHOD_KN2ROW;
 }
@@ -355,7 +355,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         case CL_METHOD_DIRECT: {
             // the dominant (and only) kernel of this method: bracket it for the profile events
             if (p->ev_begin) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
-            launch_direct_conv(x, p->wraw, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, p->P, p->Q, s);
+            launch_direct_conv(x, p->wraw, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, d.stride, p->P, p->Q, s);
             ++p->launches;
             tc_done();
             break;
@@ -394,9 +394,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         cl_method m = resolve(d, method);
         if (d.k == 1 && (m == CL_METHOD_KN2ROW_EXPLICIT || m == CL_METHOD_KN2COL)) m = CL_METHOD_CONV1X1;
         if (m == CL_METHOD_DIRECT) {
-            if (d.stride != 1) throw Error(CL_EUNSUPPORTED, "direct-gpu supports stride 1 only");
-            if (d.k > 11 || direct_smem_bytes(d.c, d.k) > 200 * 1024)
-                throw Error(CL_EUNSUPPORTED, "direct-gpu is for small C (shared-memory halo) and k <= 11");
+            // any shape: the shared-memory kernels where they fit, else the generic loop nest
         } else if (m != CL_METHOD_IM2COL) {
             if (d.stride != 1) throw Error(CL_EUNSUPPORTED, "kn2 methods support stride 1 only (im2col supports stride)");
             if (d.pad > 127 || d.k - 1 - d.pad > 128)

@@ -66,8 +66,10 @@ void launch_shift_add_col(const float* inter, float* y, int N, int M, int H, int
 
 // direct fp32 convolution for tiny-C layers (direct.cu); weights MKKC, stride 1
 void launch_direct_conv(const float* x, const float* w, float* y, int N, int C, int H, int W, int M, int k, int pad,
+                        int stride,
                         int P, int Q, cudaStream_t s);
 size_t direct_smem_bytes(int C, int k);
+bool direct_fast_path(int C, int k, int stride);   // else the generic loop nest
 
 void launch_fill_uniform(float* d, unsigned long long n, unsigned long long seed,
                          unsigned long long first, cudaStream_t s);

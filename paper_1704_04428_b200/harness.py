@@ -72,6 +72,7 @@ def benchmark(layer: LayerConfig, method: str = "auto", runs: int = 5, seed: int
     from . import rng
     if runs < 1:
         raise ValueError("benchmark: runs must be >= 1")
+    require_device(device)
     if layer.stride != 1 and method != "im2col-gpu":
         raise ValueError(f"benchmark: strided layer '{layer.name}' is not supported")
     with ConvPlan(layer, method, precision, device) as plan:
@@ -154,3 +155,99 @@ def parse_csv(text: str) -> List[BenchResult]:
             raise RuntimeError(f"csv line {no}: bad numeric field") from None
         out.append(r)
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# verify  <- convlab::verify (bench.cpp:158-209; bench.hpp:69-101)
+# ---------------------------------------------------------------------------------------
+VERIFY_DEFAULT_METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu",
+                          "conv1x1-gpu"]
+
+
+@dataclass
+class VerifyEntry:
+    layer: str
+    method: str
+    passed: bool = False
+    max_abs_err: float = 0.0
+    rel_l2: float = 0.0
+    max_rel: float = 0.0
+
+
+@dataclass
+class VerifyReport:
+    entries: List[VerifyEntry] = field(default_factory=list)
+    skipped: List[str] = field(default_factory=list)
+
+    def all_pass(self) -> bool:
+        return all(e.passed for e in self.entries)
+
+
+def require_device(device: int = 0) -> None:
+    """The GPU harness entry points fail loudly without a B200 (no CPU fallback)."""
+    from . import _lib
+    if device >= int(_lib.lib().cl_device_count()):
+        raise _lib.ClError(_lib.CL_ENODEVICE, f"no CUDA device {device} visible (the B200 path has no CPU fallback)")
+
+
+def verify(layers: Iterable[LayerConfig], methods: Iterable[str] = None, seed: int = 0, max_hw: int = 0,
+           precision: str = "fp32", rel: float = 1e-5, abs_tol: float = 1e-6, perturb=None,
+           device: int = 0) -> VerifyReport:
+    """Deterministic data per layer (input stream split(seed, 2 idx), kernels split(seed, 2 idx + 1),
+    bench.cpp:174-177; a batch continues the input stream, so image 0 is the reference's),
+    the library's own direct method as the comparator (the reference uses conv_mcmk_sum,
+    bench.cpp:187 -- here direct-gpu, an fp32 FMA restatement of the same loop nest), and one
+    entry per (layer, method).  fp32 is held to the reference law allclose(rel, abs + rel
+    max|ref|) (bench.cpp:188-192); the TF32/BF16 fast modes to the north star's rel-L2 <= 1e-2.
+    Strided layers and conv1x1 on k != 1 are skipped, not failed (bench.cpp:164-167, 194-198)."""
+    import torch
+
+    from . import rng
+    from .methods import method_requires_1x1
+    methods = list(methods) if methods is not None else list(VERIFY_DEFAULT_METHODS)
+    require_device(device)
+    report = VerifyReport()
+    dev = f"cuda:{device}"
+    for idx, layer in enumerate(layers):
+        if layer.stride != 1:
+            report.skipped.append(f"{layer.name}: stride {layer.stride} (strided convolution is out of scope)")
+            continue
+        h = min(layer.height, max_hw) if max_hw > 0 else layer.height
+        w = min(layer.width, max_hw) if max_hw > 0 else layer.width
+        if layer.kernel_size > min(h, w) + layer.kernel_size // 2:   # ConvProblem (conv_direct.cpp:15-20)
+            report.skipped.append(f"{layer.name}: kernel {layer.kernel_size} too large for {h}x{w}")
+            continue
+        lay = LayerConfig(layer.name, layer.channels, h, w, layer.kernel_count, layer.kernel_size, 1, layer.pad,
+                          layer.batch)
+        x = torch.empty((lay.batch, lay.channels, h, w), device=dev)
+        wt = torch.empty((lay.kernel_count, lay.kernel_size, lay.kernel_size, lay.channels), device=dev)
+        rng.fill_uniform(x, rng.split(seed, 2 * idx))
+        rng.fill_uniform(wt, rng.split(seed, 2 * idx + 1))
+        with ConvPlan(lay, "direct-gpu", "fp32", device) as plan:
+            plan.set_weights(wt)
+            ref = plan.forward(x)
+        ref64 = ref.double()
+        ref_max = ref64.abs().max().item()
+        tol_abs = abs_tol + rel * ref_max                                # scaled_tolerance (tensor.cpp:211-213)
+        for method in methods:
+            if method_requires_1x1(method) and lay.kernel_size != 1:
+                report.skipped.append(f"{lay.name}: conv1x1 needs k == 1, layer has k = {lay.kernel_size}")
+                continue
+            with ConvPlan(lay, method, precision, device) as plan:
+                plan.set_weights(wt)
+                out = plan.forward(x)
+            torch.cuda.synchronize(device)
+            if perturb is not None:
+                perturb(out)
+            d = out.double() - ref64
+            e = VerifyEntry(lay.name, method)
+            e.max_abs_err = d.abs().max().item()
+            e.rel_l2 = (d.norm() / ref64.norm().clamp_min(1e-300)).item()
+            e.max_rel = e.max_abs_err / max(ref_max, 1e-300)
+            finite = bool(torch.isfinite(out).all().item())
+            if precision == "fp32":
+                e.passed = finite and bool((d.abs() <= tol_abs + rel * ref64.abs()).all().item())
+            else:
+                e.passed = finite and e.rel_l2 <= 1e-2
+            report.entries.append(e)
+    return report

@@ -9,6 +9,8 @@ Cases follow the reference's tests: the method x shape grid (conv_kn2_test.cpp:2
 border-dominated shapes (acceptance_main.cpp:182-199), delta kernels, per-tap
 decomposition, k=1 routing, one-contraction-per-call, determinism, and a negative control.
 """
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -406,3 +408,46 @@ def test_direct_unit_kernel(oracle, clb, torch_cuda, case):
     ref = oracle.conv_loopnest(x, w, pad, 1)
     y = _run(clb, torch_cuda, "direct-gpu", x, w, pad=pad)
     _check_fp32(oracle, y, ref, f"direct {case}")
+
+
+@pytest.mark.parametrize("case", [(2, 64, 15, 17, 20, 3, 1, 2), (1, 300, 9, 9, 10, 5, 2, 1), (2, 8, 12, 12, 7, 13, 6, 1),
+                                  (1, 5, 20, 7, 9, 3, 0, 3)])
+def test_direct_generic_loopnest(oracle, clb, torch_cuda, case):
+    """direct-gpu on shapes its shared-memory kernels cannot stage (large C, k > 11, stride):
+    the generic loop nest, against the generalised loop-nest oracle."""
+    N, C, H, W, M, k, pad, stride = case
+    x, w = oracle.make_problem(N, C, H, W, M, k, sum(case))
+    ref = oracle.conv_loopnest(x, w, pad, stride)
+    y = clb.run_method("direct-gpu", torch_cuda.from_numpy(x).cuda(), torch_cuda.from_numpy(w).cuda(), pad=pad,
+                       stride=stride)
+    torch_cuda.cuda.synchronize()
+    _check_fp32(oracle, y.cpu().numpy(), ref, f"direct loop nest {case}")
+
+
+def test_harness_verify_and_negative_control(clb, torch_cuda, tmp_path):
+    """convlab::verify mirror (bench.cpp:158-209) and the CLI: every method passes against the
+    direct comparator; --corrupt (convlab_main.cpp:53-55) must surface as FAIL / exit 1."""
+    from paper_1704_04428_b200 import harness
+    layers = clb.parse_network_text("a 16 13 13 32 3\nb 24 7 7 40 1\nc 8 9 11 16 5 n=2\n")
+    rep = harness.verify(layers, seed=3)
+    assert rep.entries and rep.all_pass(), [(e.layer, e.method, e.max_abs_err) for e in rep.entries if not e.passed]
+    assert {e.method for e in rep.entries} == set(harness.VERIFY_DEFAULT_METHODS)
+    assert any("conv1x1 needs k == 1" in s for s in rep.skipped)
+    fast = harness.verify(layers[:1], ["kn2row-gpu"], precision="bf16")
+    assert fast.all_pass() and fast.entries[0].rel_l2 > 1e-6          # fast mode: looser law, really lossy
+    net = tmp_path / "t.net"
+    net.write_text("a 16 13 13 32 3\n")
+    import subprocess
+    import sys
+    root = str(Path(__file__).resolve().parents[1])
+    ok = subprocess.run([sys.executable, "-m", "paper_1704_04428_b200", "verify", "--net", str(net)], cwd=root,
+                        capture_output=True, text=True, timeout=600)
+    assert ok.returncode == 0 and "0 failures" in ok.stdout, ok.stdout + ok.stderr
+    bad = subprocess.run([sys.executable, "-m", "paper_1704_04428_b200", "verify", "--net", str(net), "--corrupt"],
+                         cwd=root, capture_output=True, text=True, timeout=600)
+    assert bad.returncode == 1 and "FAIL" in bad.stdout, bad.stdout + bad.stderr
+    b = subprocess.run([sys.executable, "-m", "paper_1704_04428_b200", "bench", "--net", str(net), "--runs", "2",
+                        "--out", str(tmp_path / "b.csv")], cwd=root, capture_output=True, text=True, timeout=600)
+    assert b.returncode == 0, b.stderr
+    rows = harness.parse_csv((tmp_path / "b.csv").read_text())
+    assert rows[0].layer == "a" and rows[0].runs == 2 and rows[0].eff_tflops > 0

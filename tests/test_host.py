@@ -247,3 +247,40 @@ def test_fnv1a_matches_reference_checksum(oracle):
     from paper_1704_04428_b200 import harness
     a = oracle.fill(1000, 3)
     assert harness.fnv1a(torch.from_numpy(a)) == oracle.fnv1a(a)
+
+
+def _cli(*args):
+    import subprocess
+    import sys
+    return subprocess.run([sys.executable, "-m", "paper_1704_04428_b200", *args], capture_output=True, text=True,
+                          cwd=str(Path(__file__).resolve().parents[1]), timeout=300)
+
+
+def test_cli_footprint_matches_reference_columns(tmp_path):
+    """convlab_main.cpp run_footprint: one line per (layer, method), CSV with the reference's
+    byte-exact header and runs = 0 rows; reference method names are accepted (closed form)."""
+    net = tmp_path / "p.net"
+    net.write_text("l1 3 16 16 4 3\nl2 8 10 10 6 5  # comment\n")
+    out = tmp_path / "fp.csv"
+    r = _cli("footprint", "--net", str(net), "--methods", "kn2row,im2col-gpu,conv1x1", "--out", str(out))
+    assert r.returncode == 0, r.stderr
+    lines = [l for l in r.stdout.splitlines() if l.startswith("l")]
+    assert lines[0] == "l1  kn2row  input 3072  kernels 432  intermediate 36864  output 4096 bytes"
+    assert len(lines) == 4                               # conv1x1 skipped on k != 1 layers
+    from paper_1704_04428_b200 import harness
+    rows = harness.parse_csv(out.read_text())
+    assert out.read_text().splitlines()[0] == harness.CSV_HEADER
+    assert [(x.layer, x.method, x.runs) for x in rows][:2] == [("l1", "kn2row", 0), ("l1", "im2col-gpu", 0)]
+
+
+def test_cli_usage_and_device_errors(tmp_path):
+    net = tmp_path / "p.net"
+    net.write_text("l1 3 16 16 4 3\n")
+    assert _cli("nonsense").returncode == 2                                  # kExitUsage
+    r = _cli("bench", "--net", str(net), "--methods", "kn2row")              # a CPU method: not runnable here
+    assert r.returncode == 2 and "not a runnable method" in r.stderr
+    assert _cli("footprint", "--net", str(tmp_path / "missing.net")).returncode == 2
+    import torch
+    if not torch.cuda.is_available():
+        r = _cli("verify", "--net", str(net))
+        assert r.returncode == 1 and "no CPU fallback" in r.stderr          # fails loudly, no fallback
