@@ -172,28 +172,72 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     static const bool trace = getenv("CLB_TRACE") && atoi(getenv("CLB_TRACE")) != 0;
     static unsigned long long* trace_buf = nullptr;
     if (trace) {
-        if (!trace_buf) CLB_CUDA(cudaMalloc(&trace_buf, (size_t)kMaxGrid * 8 * sizeof(unsigned long long)));
-        CLB_CUDA(cudaMemsetAsync(trace_buf, 0, (size_t)kMaxGrid * 8 * sizeof(unsigned long long), s));
+        if (!trace_buf) CLB_CUDA(cudaMalloc(&trace_buf, (size_t)kMaxGrid * kTraceSlots * sizeof(unsigned long long)));
+        CLB_CUDA(cudaMemsetAsync(trace_buf, 0, (size_t)kMaxGrid * kTraceSlots * sizeof(unsigned long long), s));
         p.trace = trace_buf;
         p.pdl = 0;
         cfg.numAttrs = 1;   // no PDL: the trace needs the launch to be self-contained
+    }
+    static cudaEvent_t tev[2] = {nullptr, nullptr};
+    if (trace) {
+        if (!tev[0]) {
+            CLB_CUDA(cudaEventCreate(&tev[0]));
+            CLB_CUDA(cudaEventCreate(&tev[1]));
+        }
+        CLB_CUDA(cudaEventRecord(tev[0], s));
     }
     cudaError_t e = cg == 2 ? cudaLaunchKernelEx(&cfg, tc_conv_kernel<2>, ma, mb, p)
                             : cudaLaunchKernelEx(&cfg, tc_conv_kernel<1>, ma, mb, p);
     CLB_CUDA(e);
     if (trace) {
-        std::vector<unsigned long long> h((size_t)grid * 8);
+        CLB_CUDA(cudaEventRecord(tev[1], s));
+        std::vector<unsigned long long> h((size_t)grid * kTraceSlots);
         CLB_CUDA(cudaMemcpyAsync(h.data(), trace_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         CLB_CUDA(cudaStreamSynchronize(s));
-        double avg[8] = {0};
-        for (int b = 0; b < grid; ++b)
-            for (int i = 0; i < 8; ++i) avg[i] += (double)h[(size_t)b * 8 + i] / grid;
+        float ev_ms = 0.0f;
+        CLB_CUDA(cudaEventElapsedTime(&ev_ms, tev[0], tev[1]));
+        double avg[kTraceSlots] = {0};
+        unsigned long long t_in = ~0ull, t_in_max = 0, t_out = 0;
+        for (int b = 0; b < grid; ++b) {
+            for (int i = 0; i < kTraceSlots; ++i) avg[i] += (double)h[(size_t)b * kTraceSlots + i] / grid;
+            t_in = std::min(t_in, h[(size_t)b * kTraceSlots + 9]);
+            t_in_max = std::max(t_in_max, h[(size_t)b * kTraceSlots + 9]);
+            t_out = std::max(t_out, h[(size_t)b * kTraceSlots + 10]);
+        }
         fprintf(stderr,
                 "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stages=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
                 "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
-                "store %.0f%%)\n",
+                "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us\n",
                 p.rows, p.cols, p.bn, cg, p.tps, p.stages, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
-                avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5]);
+                avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5], 100 * avg[11] / avg[5], avg[8], (t_out - t_in) * 1e-3,
+                (t_in_max - t_in) * 1e-3, ev_ms * 1e3);
+        if (const char* dump = getenv("CLB_TRACE_DUMP")) {   // raw per-CTA records, appended
+            if (FILE* f = fopen(dump, "a")) {
+                fprintf(f, "# launch rows=%d cols=%d bn=%d cg=%d grid=%d tiles=%d dp=%d cpt=%d\n", p.rows, p.cols, p.bn, cg,
+                        grid, p.num_tiles, p.dp_tiles, p.chunks_per_tile);
+                for (int b = 0; b < grid; ++b) {
+                    const unsigned long long* r = &h[(size_t)b * kTraceSlots];
+                    auto rel = [&](unsigned long long t) { return t ? (double)(t - t_in) * 1e-3 : -1.0; };
+                    fprintf(f,
+                            "cta %d prod %llu mma %llu epi %llu wtfull %llu wfix %llu nparts %llu | start %.2f "
+                            "mma_end %.2f folded %.2f published %.2f acquired %.2f added %.2f stored %.2f exit %.2f us\n",
+                            b, r[0], r[2], r[5], r[6], r[11], r[14], rel(r[9]), rel(r[12]), rel(r[13]), rel(r[15]),
+                            rel(r[16]), rel(r[17]), rel(r[18]), rel(r[10]));
+                }
+                fclose(f);
+            }
+        }
+        // the slowest CTA (latest exit) decides the kernel time: its own breakdown
+        int slow = 0;
+        for (int b = 1; b < grid; ++b)
+            if (h[(size_t)b * kTraceSlots + 10] > h[(size_t)slow * kTraceSlots + 10]) slow = b;
+        const unsigned long long* r = &h[(size_t)slow * kTraceSlots];
+        int lead = cg == 2 ? (slow & ~1) : slow;   // the MMA runs on the pair's leader
+        const unsigned long long* rl = &h[(size_t)lead * kTraceSlots];
+        fprintf(stderr,
+                "[clb-trace]   slowest CTA %d: exit +%.1f us | producer %llu (wait empty %llu) | mma %llu (wait full "
+                "%llu, wait tmem %llu) | epilogue %llu (wait tfull %llu, store %llu, fixup wait %llu) cyc\n",
+                slow, (r[10] - t_in) * 1e-3, r[0], r[1], rl[2], rl[3], rl[4], r[5], r[6], r[7], r[11]);
     }
 }
 

@@ -123,6 +123,8 @@ __host__ __device__ inline uint32_t tmem_cols_for(int bn) {
     return c;
 }
 
+constexpr int kTraceSlots = 20;   // CLB_TRACE per-CTA record (see launch_tc)
+
 #ifdef CLB_DEFINE_TC_KERNEL
 // Per-tile operand coordinates, computed once per tile so that the K loop of the single
 // producer thread does no integer division (a runtime divide is ~100 cycles of dependent
@@ -234,6 +236,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const long long t_entry = p.trace ? clock64() : 0;
+    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * kTraceSlots + 9] = globaltimer_ns();
 
     const int bn = p.bn;
     const int planes = p.planes;
@@ -312,6 +316,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint32_t tx = (uint32_t)CG * stage_tx;   // both CTAs' bytes land on the leader
             long long w_empty = 0;
             const long long t_start = clock64();
+            if (p.trace && lane_id() == 0) p.trace[blockIdx.x * kTraceSlots + 8] = (unsigned long long)(t_start - t_entry);
             Sched sch(p, unit, nunits);
             Piece pc;
             while (sch.next(pc)) {
@@ -378,8 +383,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 }
             }
             if (p.trace && lane_id() == 0) {
-                p.trace[blockIdx.x * 8 + 0] = (unsigned long long)(clock64() - t_start);
-                p.trace[blockIdx.x * 8 + 1] = (unsigned long long)w_empty;
+                p.trace[blockIdx.x * kTraceSlots + 0] = (unsigned long long)(clock64() - t_start);
+                p.trace[blockIdx.x * kTraceSlots + 1] = (unsigned long long)w_empty;
             }
         }
     } else if (warp == 1) {
@@ -486,9 +491,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 __syncwarp();
             }
             if (p.trace && lane_id() == 0) {
-                p.trace[blockIdx.x * 8 + 2] = (unsigned long long)(clock64() - t_start);
-                p.trace[blockIdx.x * 8 + 3] = (unsigned long long)w_full;
-                p.trace[blockIdx.x * 8 + 4] = (unsigned long long)w_tempty;
+                p.trace[blockIdx.x * kTraceSlots + 2] = (unsigned long long)(clock64() - t_start);
+                p.trace[blockIdx.x * kTraceSlots + 3] = (unsigned long long)w_full;
+                p.trace[blockIdx.x * kTraceSlots + 4] = (unsigned long long)w_tempty;
+                p.trace[blockIdx.x * kTraceSlots + 12] = globaltimer_ns();
             }
         }
     } else if (warp >= 4) {
@@ -503,7 +509,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const int cbase = half * hcols;
         const int trow = quad * 32 + lane;           // row within this CTA's 128 rows
         uint32_t lg = 0;
-        long long w_tfull = 0, w_store = 0;
+        long long w_tfull = 0, w_store = 0, w_fix = 0;
+        unsigned long long n_parts = 0, t_folded = 0, t_pub = 0, t_acq = 0, t_added = 0, t_stored = 0;
         const long long t_start = clock64();
         Sched sch(p, unit, nunits);
         Piece pc;
@@ -515,9 +522,31 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             float sum[128];
 #pragma unroll
             for (int j = 0; j < 128; ++j) sum[j] = 0.0f;
+            // finisher of a split tile (its first chunks, always this CTA's last piece): the
+            // later pieces' partials are acquired while its own last chunk is still in the MMA
+            const bool finisher = pc.c_lo == 0 && pc.c_hi < cpt;
+            int u_end = unit + 1;
+            if (finisher) {
+                const int last = (pc.tile - p.dp_tiles) * cpt + cpt - 1;   // in stream-K chunk space
+                while (u_end < nunits && chunk_start(u_end, p.sk_chunks, nunits) <= last) ++u_end;
+            }
             for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
                 const uint32_t buf = lg & (uint32_t)(nbuf - 1);
                 const uint32_t tph = (lg >> nb_shift) & 1u;
+                if (finisher && c == pc.c_hi - 1) {
+                    const uint64_t t0 = globaltimer_ns();
+                    const long long c0 = p.trace ? clock64() : 0;
+                    for (int u2 = unit + 1; u2 < u_end; ++u2) {
+                        while (ld_acquire_u32(&p.flags[u2 * CG + (int)rank]) == 0u) {
+                            if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+                        }
+                    }
+                    if (p.trace) {
+                        w_fix += clock64() - c0;
+                        n_parts += (unsigned long long)(u_end - unit - 1);
+                        t_acq = globaltimer_ns();
+                    }
+                }
                 if (p.trace) {
                     const long long t0 = clock64();
                     mbar_wait(&tfull[buf], tph);
@@ -548,41 +577,45 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     else mbar_arrive(&tempty[buf]);
                 }
             }
+            if (p.trace) t_folded = globaltimer_ns();
             if (pc.c_lo > 0) {
                 // ---- tile tail handled by this CTA: publish the partial for the finisher ----
-                float* dst = p.partials + ((long long)blockIdx.x * kTileM + trow) * bn + cbase;
+                // lane-contiguous float4 layout [slot][col/4][row]: a warp's store is 512
+                // contiguous bytes (the row-per-thread layout scattered every lane 4 BN bytes
+                // apart and made publish + fixup ~10x slower than the loads themselves)
+                float4* dst = reinterpret_cast<float4*>(p.partials) +
+                              ((long long)blockIdx.x * (bn >> 2) + (cbase >> 2)) * kTileM + trow;
 #pragma unroll
                 for (int j = 0; j < 128; j += 4)
-                    if (j < hcols) *reinterpret_cast<float4*>(dst + j) = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
-                __threadfence();
+                    if (j < hcols) __stcg(dst + (j >> 2) * kTileM, make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]));
+                // the barrier orders every epilogue thread's stores before the single gpu-scope
+                // release (release is cumulative over what the releasing thread has observed)
                 epi_bar_sync();
                 if (threadIdx.x == 4 * 32) st_release_u32(&p.flags[blockIdx.x], 1u);
+                if (p.trace) t_pub = globaltimer_ns();
                 continue;
             }
-            if (pc.c_hi < cpt) {
+            if (finisher) {
                 // ---- finisher of a split tile: add the later pieces' partials in unit order ----
-                const int last = (pc.tile - p.dp_tiles) * cpt + cpt - 1;   // in stream-K chunk space
-                for (int u2 = unit + 1; u2 < nunits && chunk_start(u2, p.sk_chunks, nunits) <= last; ++u2) {
-                    const int slot = u2 * CG + (int)rank;
-                    const uint64_t t0 = globaltimer_ns();
-                    while (ld_acquire_u32(&p.flags[slot]) == 0u) {
-                        if (globaltimer_ns() - t0 > 4000000000ull) __trap();
-                    }
-                    const float* src = p.partials + ((long long)slot * kTileM + trow) * bn + cbase;
+                for (int u2 = unit + 1; u2 < u_end; ++u2) {
+                    const float4* src = reinterpret_cast<const float4*>(p.partials) +
+                                        ((long long)(u2 * CG + (int)rank) * (bn >> 2) + (cbase >> 2)) * kTileM + trow;
 #pragma unroll
                     for (int j = 0; j < 128; j += 4)
                         if (j < hcols) {
-                            const float4 v = __ldcg(reinterpret_cast<const float4*>(src + j));
+                            const float4 v = __ldcg(src + (j >> 2) * kTileM);
                             sum[j] += v.x;
                             sum[j + 1] += v.y;
                             sum[j + 2] += v.z;
                             sum[j + 3] += v.w;
                         }
-                    // every published partial has exactly one finisher: reset its flag so the
-                    // buffer is clean for the next launch (no memset launch needed)
-                    epi_bar_sync();
-                    if (threadIdx.x == 4 * 32) p.flags[slot] = 0u;
                 }
+                if (p.trace) t_added = globaltimer_ns();
+                // every published partial has exactly one finisher: reset its flags so the
+                // buffer is clean for the next launch (no memset launch needed)
+                epi_bar_sync();
+                if (threadIdx.x == 4 * 32)
+                    for (int u2 = unit + 1; u2 < u_end; ++u2) p.flags[u2 * CG + (int)rank] = 0u;
             }
             // ---- store the finished tile ----
             const long long t_st = p.trace ? clock64() : 0;
@@ -622,12 +655,22 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     }
                 }
             }
-            if (p.trace) w_store += clock64() - t_st;
+            if (p.trace) {
+                w_store += clock64() - t_st;
+                t_stored = globaltimer_ns();
+            }
         }
         if (p.trace && threadIdx.x == 4 * 32) {
-            p.trace[blockIdx.x * 8 + 5] = (unsigned long long)(clock64() - t_start);
-            p.trace[blockIdx.x * 8 + 6] = (unsigned long long)w_tfull;
-            p.trace[blockIdx.x * 8 + 7] = (unsigned long long)w_store;
+            p.trace[blockIdx.x * kTraceSlots + 5] = (unsigned long long)(clock64() - t_start);
+            p.trace[blockIdx.x * kTraceSlots + 6] = (unsigned long long)w_tfull;
+            p.trace[blockIdx.x * kTraceSlots + 7] = (unsigned long long)w_store;
+            p.trace[blockIdx.x * kTraceSlots + 11] = (unsigned long long)w_fix;
+            p.trace[blockIdx.x * kTraceSlots + 13] = t_folded;
+            p.trace[blockIdx.x * kTraceSlots + 14] = n_parts;
+            p.trace[blockIdx.x * kTraceSlots + 15] = t_pub;
+            p.trace[blockIdx.x * kTraceSlots + 16] = t_acq;
+            p.trace[blockIdx.x * kTraceSlots + 17] = t_added;
+            p.trace[blockIdx.x * kTraceSlots + 18] = t_stored;
         }
     }
 
@@ -639,6 +682,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         if constexpr (CG == 2) tmem_dealloc_2sm(tmem_base, ncols);
         else tmem_dealloc(tmem_base, ncols);
     }
+    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * kTraceSlots + 10] = globaltimer_ns();
 }
 
 #endif  // CLB_DEFINE_TC_KERNEL
