@@ -124,9 +124,30 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     const int sms = num_sms();
     int units = (sms < kMaxGrid ? sms : kMaxGrid) / cg;      // scheduling units (CTAs or CTA pairs)
     if (total_chunks < units) units = (int)total_chunks;
-    // a split tile is finished by one unit that adds the other pieces' partials serially:
-    // cap the split factor so tiny problems (batch-1 layers) do not drown in fixups
-    if ((long long)units > (long long)p.num_tiles * kMaxSplit) units = p.num_tiles * kMaxSplit;
+    // Fewer tiles than units (latency-bound problems): pick the split s (pieces per tile) by a
+    // cost model in chunk times -- ceil(chunks / units) on the critical path, plus a fixup of
+    // ~3 chunk times and ~0.5 per extra piece whenever tiles are split.  Calibrated on the
+    // batch-1 / GoogLeNet / k-sweep layers (profiles/r01_split_sweep.txt): small-K layers stay
+    // unsplit, big-K ones split up to kMaxSplit.  CLB_MAX_SPLIT caps s for experiments.
+    static const int max_split = [] {
+        const char* e = getenv("CLB_MAX_SPLIT");
+        const int v = e ? atoi(e) : 0;
+        return (v >= 1 && v <= kMaxSplit) ? v : kMaxSplit;
+    }();
+    if (p.num_tiles < units) {
+        double best = 1e30;
+        int best_units = p.num_tiles;
+        for (int sp = 1; sp <= max_split; ++sp) {
+            const long long u = std::min<long long>(units, (long long)p.num_tiles * sp);
+            const double t = (double)((total_chunks + u - 1) / u) + (sp > 1 ? 3.0 + 0.5 * (sp - 1) : 0.0);
+            if (t < best - 1e-9) {
+                best = t;
+                best_units = (int)u;
+            }
+            if (u == units) break;
+        }
+        units = best_units;
+    }
     // whole-tile waves for all but the last 1-2 waves; stream-K over the rest
     // (a last wave that is >= 95% full stays data-parallel: splitting it costs more than it saves)
     const int waves = p.num_tiles / units;

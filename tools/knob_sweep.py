@@ -10,11 +10,12 @@ import paper_1704_04428_b200 as clb
 from paper_1704_04428_b200 import _lib, rng, workloads
 
 layers = sys.argv[1].split(",")
+batch = int(sys.argv[sys.argv.index("--batch") + 1]) if "--batch" in sys.argv else None
 tag = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("CLB_"))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for name in layers:
     group = name.split("/")[0]
-    layer = [l for l in workloads.workload(group) if l.name == name][0]
+    layer = [l for l in workloads.workload(group, batch) if l.name == name][0]
     x, w = rng.make_problem(layer.batch, layer.channels, layer.height, layer.width, layer.kernel_count,
                             layer.kernel_size)
     with clb.ConvPlan(layer, "auto", "fp32") as plan:
@@ -33,4 +34,4 @@ for name in layers:
         _lib.lib().cl_conv_set_profile_events(plan._h, None, None)
     ts.sort()
     ms = ts[len(ts) // 2]
-    print(f"{name:16s} {tag:40s} {ms:7.3f} ms {layer.flops() / ms / 1e9:7.1f} TF", flush=True)
+    print(f"{name + ('-b%d' % layer.batch if batch else ''):16s} {tag:40s} {ms:7.3f} ms {layer.flops() / ms / 1e9:7.1f} TF", flush=True)
