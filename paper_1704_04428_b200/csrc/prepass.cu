@@ -50,32 +50,39 @@ constexpr int kSplitPx = 128;
 // Output pixel space: HW = Hp*Wp pixels per image; with pad > 0 this is the zero-padded
 // image (Hp = H + 2 pad, Wp = W + 2 pad) the tap-shared (padded-row) kernel mode reads.
 __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xsv,
-                                                                 int C, int HW, int Cp, int planes, int H, int W,
-                                                                 int Wp, int pad) {
+                                                                 int N, int C, int HW, int Cp, int planes, int H,
+                                                                 int W, int Wp, int pad) {
     __shared__ float tile[kSplitPx][33];   // [pixel][channel]
-    const int n = blockIdx.z;
-    const int p0 = blockIdx.x * kSplitPx, c0 = blockIdx.y * 32;
+    // pixels are flattened over (image, pixel): a tile may straddle two images, so small maps
+    // (13 x 13 = 169 pixels) do not leave most of a second 128-pixel tile idle
+    const long long NP = (long long)N * HW;
+    const long long g0 = (long long)blockIdx.x * kSplitPx;
+    const int c0 = blockIdx.y * 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const float* xn = x + (long long)n * C * H * W;
-    int src[4];
+    const long long plane = (long long)H * W;
+    long long src[4];                       // element offset of channel 0 of this pixel, or -1
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
-        const int pix = p0 + lane + 32 * h;
-        if (pad == 0) {
-            src[h] = pix < HW ? pix : -1;
-        } else {
-            const int yy = pix / Wp, xx = pix - (pix / Wp) * Wp;
-            const int sy = yy - pad, sx = xx - pad;
-            src[h] = (pix < HW && sy >= 0 && sy < H && sx >= 0 && sx < W) ? sy * W + sx : -1;
+        const long long gp = g0 + lane + 32 * h;
+        src[h] = -1;
+        if (gp < NP) {
+            const int n = NP <= 0x7fffffffLL ? (int)((unsigned)gp / (unsigned)HW) : (int)(gp / HW);
+            const int pix = (int)(gp - (long long)n * HW);
+            int sp = pix;
+            if (pad != 0) {
+                const int yy = pix / Wp, xx = pix - (pix / Wp) * Wp;
+                const int sy = yy - pad, sx = xx - pad;
+                sp = (sy >= 0 && sy < H && sx >= 0 && sx < W) ? sy * W + sx : -1;
+            }
+            if (sp >= 0) src[h] = (long long)n * C * plane + sp;
         }
     }
     float v[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int c = c0 + warp + 8 * r;
-        const float* row = xn + (long long)c * H * W;
 #pragma unroll
-        for (int h = 0; h < 4; ++h) v[r][h] = (c < C && src[h] >= 0) ? __ldg(row + src[h]) : 0.0f;
+        for (int h = 0; h < 4; ++h) v[r][h] = (c < C && src[h] >= 0) ? __ldg(x + src[h] + (long long)c * plane) : 0.0f;
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r)
@@ -89,18 +96,18 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
     if (planes == kPlanesBf16) {                        // bf16 rows: lane = channel
         __nv_bfloat16* xb = static_cast<__nv_bfloat16*>(xsv);
         for (int pp = warp; pp < kSplitPx; pp += 8) {
-            const int pix = p0 + pp;
-            if (pix >= HW) break;
-            if (lane < nch) xb[((long long)n * HW + pix) * row_words + c0 + lane] = __float2bfloat16_rn(tile[pp][lane]);
+            const long long gp = g0 + pp;
+            if (gp >= NP) break;
+            if (lane < nch) xb[gp * row_words + c0 + lane] = __float2bfloat16_rn(tile[pp][lane]);
         }
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         return;
     }
     float* xs = static_cast<float*>(xsv);
     for (int pp = warp; pp < kSplitPx; pp += 8) {
-        const int pix = p0 + pp;
-        if (pix >= HW) break;
-        float* dst = xs + ((long long)n * HW + pix) * row_words + (long long)(planes == 2 ? 2 : 1) * c0;
+        const long long gp = g0 + pp;
+        if (gp >= NP) break;
+        float* dst = xs + gp * row_words + (long long)(planes == 2 ? 2 : 1) * c0;
 #pragma unroll
         for (int o0 = 0; o0 < 64; o0 += 32) {
             const int o = o0 + lane;
@@ -123,16 +130,16 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
 
 void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s) {
-    dim3 grid((HW + kSplitPx - 1) / kSplitPx, (Cp + 31) / 32, N);
-    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, C, HW, Cp, planes, 1, HW, HW, 0);
+    dim3 grid((unsigned)(((long long)N * HW + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
+    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, N, C, HW, Cp, planes, 1, HW, HW, 0);
     CLB_CUDA(cudaGetLastError());
 }
 
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
                                  cudaStream_t s) {
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;
-    dim3 grid((Hp * Wp + kSplitPx - 1) / kSplitPx, (Cp + 31) / 32, N);
-    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, C, Hp * Wp, Cp, planes, H, W, Wp, pad);
+    dim3 grid((unsigned)(((long long)N * Hp * Wp + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
+    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, N, C, Hp * Wp, Cp, planes, H, W, Wp, pad);
     CLB_CUDA(cudaGetLastError());
 }
 
