@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" boundary (include/convlab_b200.h): plans, method dispatch,
 // workspace management, error mapping.  No CPU fallback anywhere: every entry point
 // either enqueues sm_100a kernels or returns an error.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -548,28 +549,57 @@ cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* s
         if (chunks > cl_plan::kMaxChunks) chunks = cl_plan::kMaxChunks;
         if (chunks > d.n) chunks = d.n;
         if (chunks < 1) chunks = 1;
+        // CLB_HOST_TRACE=1: per-chunk timeline (timing events on each stream, printed per call)
+        static const bool htrace = std::getenv("CLB_HOST_TRACE") && std::atoi(std::getenv("CLB_HOST_TRACE")) != 0;
+        static cudaEvent_t tev[3 * cl_plan::kMaxChunks + 1] = {};
+        if (htrace && !tev[0])
+            for (auto& e : tev) CLB_CUDA(cudaEventCreate(&e));
         // the copy streams must not run ahead of prior work on the caller's stream
         CLB_CUDA(cudaEventRecord(p->ev_start, s));
+        if (htrace) CLB_CUDA(cudaEventRecord(tev[0], s));
         CLB_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
         CLB_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
-        int first = 0;
+        // all copy-ins are enqueued first, so the H2D engine streams back to back and never
+        // waits for the host to enqueue a chunk's kernels (that interleaving cost ~25% of the
+        // duplex PCIe rate, measured with CLB_HOST_TRACE)
         for (int c = 0; c < chunks; ++c) {
-            const int n0 = first, nc = d.n * (c + 1) / chunks - first;
-            first += nc;
+            const int n0 = d.n * c / chunks, nc = d.n * (c + 1) / chunks - n0;
             if (nc == 0) continue;
             CLB_CUDA(cudaMemcpyAsync(p->host_x + n0 * img_in, h_x + n0 * img_in, nc * img_in * 4,
                                      cudaMemcpyHostToDevice, p->s_in));
             CLB_CUDA(cudaEventRecord(p->ev_in[c], p->s_in));
+            if (htrace) CLB_CUDA(cudaEventRecord(tev[1 + 3 * c], p->s_in));
+        }
+        for (int c = 0; c < chunks; ++c) {
+            const int n0 = d.n * c / chunks, nc = d.n * (c + 1) / chunks - n0;
+            if (nc == 0) continue;
             CLB_CUDA(cudaStreamWaitEvent(s, p->ev_in[c], 0));
             forward(p, p->host_x + n0 * img_in, p->host_y + n0 * img_out, nullptr, s, nc);
             CLB_CUDA(cudaEventRecord(p->ev_comp[c], s));
+            if (htrace) CLB_CUDA(cudaEventRecord(tev[2 + 3 * c], s));
             CLB_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_comp[c], 0));
             CLB_CUDA(cudaMemcpyAsync(h_y + n0 * img_out, p->host_y + n0 * img_out, nc * img_out * 4,
                                      cudaMemcpyDeviceToHost, p->s_out));
+            if (htrace) CLB_CUDA(cudaEventRecord(tev[3 + 3 * c], p->s_out));
         }
         CLB_CUDA(cudaEventRecord(p->ev_done, p->s_out));
         CLB_CUDA(cudaStreamWaitEvent(s, p->ev_done, 0));   // the caller's stream sees the outputs
         CLB_CUDA(cudaStreamSynchronize(s));
+        if (htrace) {
+            fprintf(stderr, "[clb-host] n=%d c=%d m=%d hw=%dx%d chunks=%d in %.1f MB out %.1f MB |", d.n, d.c, d.m, d.h,
+                    d.w, chunks, xb / 1e6, yb / 1e6);
+            float last_out = 0.0f;
+            for (int c = 0; c < chunks; ++c) {
+                float ti = 0, tc = 0, to = 0;
+                CLB_CUDA(cudaEventElapsedTime(&ti, tev[0], tev[1 + 3 * c]));
+                CLB_CUDA(cudaEventElapsedTime(&tc, tev[0], tev[2 + 3 * c]));
+                CLB_CUDA(cudaEventElapsedTime(&to, tev[0], tev[3 + 3 * c]));
+                fprintf(stderr, " [%d: in %.2f comp %.2f out %.2f]", c, ti, tc, to);
+                last_out = to;
+            }
+            fprintf(stderr, " | total %.2f ms (H2D-only %.2f, D2H-only %.2f ms at 56 GB/s)\n", last_out, xb / 56e6,
+                    yb / 56e6);
+        }
     });
 }
 
