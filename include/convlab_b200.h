@@ -22,6 +22,13 @@
  * Error behaviour mirrors the reference: contract violations (the reference's
  * std::invalid_argument) return CL_EINVAL; unsupported shapes CL_EUNSUPPORTED; CUDA
  * failures CL_ECUDA.  cl_last_error() returns the thread-local message of the last failure.
+ *
+ * Threading / streams (reference SPEC.md:149): entry points are reentrant.  A
+ * plan may be shared by several host threads and streams: calls on one plan are serialised
+ * on the host and execute on the device in call order (a call on a different stream than the
+ * previous one waits for it), because the plan owns per-call state (stream-K fixup flags, its
+ * default workspace, host staging).  For concurrent execution use one plan per stream.
+ * Streams being captured into a CUDA graph are not chained (the graph orders them).
  * No entry point falls back to the CPU: without a usable sm_100 device they fail.
  */
 #ifndef CONVLAB_B200_H

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/convlab_b200.h"
@@ -88,6 +89,13 @@ struct cl_plan {
     cudaStream_t s_in = nullptr, s_out = nullptr;
     static constexpr int kMaxChunks = 16;
     cudaEvent_t ev_in[kMaxChunks] = {}, ev_comp[kMaxChunks] = {}, ev_start = nullptr, ev_done = nullptr;
+    // Sharing: a plan's flags, own workspace and staging buffers are per-plan state, so calls
+    // on one plan are serialised -- host side by `mu`, device side by chaining each call after
+    // the previous call's completion event when it arrives on a different stream.
+    std::mutex mu;
+    cudaEvent_t ev_last = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool has_last = false;
 };
 
 namespace {
@@ -179,6 +187,29 @@ TcParams base_params(const cl_plan* p) {
     t.Q = p->Q;
     t.pad = p->d.pad;
     return t;
+}
+
+// Device-side ordering of calls on a shared plan (caller holds p->mu).
+// (A stream being captured into a CUDA graph is left alone: the graph's own edges order it.)
+bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    CLB_CUDA(cudaStreamIsCapturing(s, &st));
+    return st != cudaStreamCaptureStatusNone;
+}
+
+void order_after_previous(cl_plan* p, cudaStream_t s) {
+    if (p->has_last && p->last_stream != s && !capturing(s)) CLB_CUDA(cudaStreamWaitEvent(s, p->ev_last, 0));
+}
+
+void mark_done(cl_plan* p, cudaStream_t s) {
+    if (capturing(s)) {
+        p->has_last = false;
+        return;
+    }
+    if (!p->ev_last) CLB_CUDA(cudaEventCreateWithFlags(&p->ev_last, cudaEventDisableTiming));
+    CLB_CUDA(cudaEventRecord(p->ev_last, s));
+    p->last_stream = s;
+    p->has_last = true;
 }
 
 // n_images < 0: the plan's batch; otherwise a sub-batch (chunked host pipeline).
@@ -458,6 +489,8 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
         require(p && d_w, "cl_conv_set_weights: null argument");
         CLB_CUDA(cudaSetDevice(p->device));
         auto s = static_cast<cudaStream_t>(stream);
+        std::lock_guard<std::mutex> lock(p->mu);
+        order_after_previous(p, s);
         const cl_conv_desc& d = p->d;
         if (p->method == CL_METHOD_IM2COL)
             launch_rows_split(d_w, p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);   // MKKC == M x k^2C
@@ -466,6 +499,7 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
         else
             launch_pack_weights(d_w, p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s);
         p->weights_set = true;
+        mark_done(p, s);
     });
 }
 
@@ -474,6 +508,8 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
         require(p && h_w, "cl_conv_set_weights_host: null argument");
         CLB_CUDA(cudaSetDevice(p->device));
         auto s = static_cast<cudaStream_t>(stream);
+        std::lock_guard<std::mutex> lock(p->mu);
+        order_after_previous(p, s);
         const size_t bytes = (size_t)p->d.m * p->d.k * p->d.k * p->d.c * 4;
         void* dw = nullptr;
         CLB_CUDA(cudaMallocAsync(&dw, bytes, s));
@@ -488,6 +524,7 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
         CLB_CUDA(cudaFreeAsync(dw, s));
         CLB_CUDA(cudaStreamSynchronize(s));
         p->weights_set = true;
+        mark_done(p, s);
     });
 }
 
@@ -505,7 +542,12 @@ cl_method cl_conv_resolved_method(const cl_plan* p) { return p ? p->method : CL_
 cl_status cl_conv_forward(cl_plan* p, const float* d_x, float* d_y, void* d_ws, void* stream) {
     return guarded([&] {
         require(p, "cl_conv_forward: null plan");
-        forward(p, d_x, d_y, d_ws, static_cast<cudaStream_t>(stream));
+        auto s = static_cast<cudaStream_t>(stream);
+        std::lock_guard<std::mutex> lock(p->mu);
+        CLB_CUDA(cudaSetDevice(p->device));
+        order_after_previous(p, s);
+        forward(p, d_x, d_y, d_ws, s);
+        mark_done(p, s);
     });
 }
 
@@ -517,6 +559,8 @@ cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* s
     return guarded([&] {
         require(p && h_x && h_y, "cl_conv_forward_host: null argument");
         CLB_CUDA(cudaSetDevice(p->device));
+        std::lock_guard<std::mutex> lock(p->mu);
+        order_after_previous(p, static_cast<cudaStream_t>(stream));
         const cl_conv_desc& d = p->d;
         const size_t img_in = (size_t)d.c * d.h * d.w, img_out = (size_t)d.m * p->P * p->Q;
         const size_t xb = (size_t)d.n * img_in * 4;
@@ -584,6 +628,7 @@ cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* s
         }
         CLB_CUDA(cudaEventRecord(p->ev_done, p->s_out));
         CLB_CUDA(cudaStreamWaitEvent(s, p->ev_done, 0));   // the caller's stream sees the outputs
+        mark_done(p, s);
         CLB_CUDA(cudaStreamSynchronize(s));
         if (htrace) {
             fprintf(stderr, "[clb-host] n=%d c=%d m=%d hw=%dx%d chunks=%d in %.1f MB out %.1f MB |", d.n, d.c, d.m, d.h,
@@ -612,6 +657,7 @@ void cl_conv_destroy(cl_plan* p) {
     if (p->flags) cudaFree(p->flags);
     if (p->own_ws) cudaFree(p->own_ws);
     if (p->host_x) cudaFree(p->host_x);
+    if (p->ev_last) cudaEventDestroy(p->ev_last);
     if (p->host_y) cudaFree(p->host_y);
     if (p->s_in) {
         cudaStreamDestroy(p->s_in);

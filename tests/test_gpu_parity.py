@@ -451,3 +451,49 @@ def test_harness_verify_and_negative_control(clb, torch_cuda, tmp_path):
     assert b.returncode == 0, b.stderr
     rows = harness.parse_csv((tmp_path / "b.csv").read_text())
     assert rows[0].layer == "a" and rows[0].runs == 2 and rows[0].eff_tflops > 0
+
+
+def test_shared_plan_two_streams_and_threads(oracle, clb, torch_cuda):
+    """A plan shared by two streams and two host threads: calls serialise in order on the
+    device (the plan's stream-K flags / workspace are per-plan), so every output is exact."""
+    import threading
+    torch = torch_cuda
+    N, C, H, W, M, k = 3, 64, 14, 14, 96, 3     # stream-K tail -> the plan's fixup flags are used
+    layer = clb.LayerConfig("shared", C, H, W, M, k, batch=N)
+    xs = [oracle.make_problem(N, C, H, W, M, k, 50 + i)[0] for i in range(4)]
+    _, w = oracle.make_problem(N, C, H, W, M, k, 7)
+    refs = [oracle.conv_batch(x, w) for x in xs]
+    with clb.ConvPlan(layer, "kn2row-gpu") as plan:
+        plan.set_weights(torch.from_numpy(w).cuda())
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        xd = [torch.from_numpy(x).cuda() for x in xs]
+        torch.cuda.synchronize()
+        outs = [torch.empty(plan.output_shape(), device="cuda") for _ in xs]
+        for rep in range(3):                      # interleave the streams, no host sync between
+            for i, x in enumerate(xd):
+                plan.forward(x, outs[i], stream=streams[i % 2])
+        torch.cuda.synchronize()
+        for y, ref in zip(outs, refs):
+            _check_fp32(oracle, y.cpu().numpy(), ref, "two streams")
+        outs2 = [torch.empty(plan.output_shape(), device="cuda") for _ in xs]
+        errs = []
+
+        def worker(t):
+            try:
+                s = torch.cuda.Stream()
+                for rep in range(4):
+                    for i in range(t, len(xd), 2):
+                        plan.forward(xd[i], outs2[i], stream=s)
+                s.synchronize()
+            except Exception as e:   # surfaced below
+                errs.append(e)
+
+        th = [threading.Thread(target=worker, args=(t,)) for t in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        torch.cuda.synchronize()
+        assert not errs, errs
+        for y, ref in zip(outs2, refs):
+            _check_fp32(oracle, y.cpu().numpy(), ref, "two threads")
