@@ -68,7 +68,9 @@ typedef enum cl_method {
     CL_METHOD_KN2ROW_ACC = 4,    /* accumulating: k^2 shifted GEMM launches summing into the output    */
     CL_METHOD_IM2COL = 5,        /* baseline: patch matrix (NHW x k^2 C) + one GEMM                     */
     CL_METHOD_CONV1X1 = 6,       /* k == 1 only (CL_EINVAL otherwise, methods.cpp:81-85)                */
-    CL_METHOD_DIRECT = 7         /* fp32 CUDA-core direct loop nest for tiny-C layers (conv_direct.cpp:104-143) */
+    CL_METHOD_DIRECT = 7,        /* fp32 CUDA-core direct loop nest for tiny-C layers (conv_direct.cpp:104-143) */
+    CL_METHOD_IM2ROW = 8         /* reference im2row (conv_im2.cpp:56-85, 134-142): on the GPU the same K-major */
+                                 /* patch-rows x weights GEMM as IM2COL (the orientations coincide there)       */
 } cl_method;
 
 typedef enum cl_precision {

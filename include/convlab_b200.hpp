@@ -44,6 +44,7 @@ enum class ConvMethod {
     Conv1x1Gpu,
     Auto,
     DirectGpu,          // fp32 CUDA-core direct loop nest (tiny-C first layers)
+    Im2rowGpu,          // reference im2row; same K-major patch GEMM as Im2colGpu on the GPU
 };
 
 enum class Precision { Fp32, Tf32, Bf16 };

@@ -23,6 +23,7 @@ METHODS = {
     "im2col-gpu": 5,
     "conv1x1-gpu": 6,
     "direct-gpu": 7,
+    "im2row-gpu": 8,
 }
 METHOD_NAMES = {v: k for k, v in METHODS.items()}
 # cl_precision

@@ -16,6 +16,11 @@ namespace {
 
 thread_local std::string g_err;
 
+// im2col and im2row differ on the CPU only in the patch matrix orientation; on the GPU both
+// contract K-major patch rows ([N*P*Q][k^2 C], the im2row layout, with the shared (i*k+j)*C+c
+// K order) against the M x k^2 C weights, so they share one engine path.
+inline bool is_patch_method(cl_method m) { return m == CL_METHOD_IM2COL || m == CL_METHOD_IM2ROW; }
+
 cl_status fail(cl_status s, const std::string& msg) {
     g_err = msg;
     return s;
@@ -135,6 +140,7 @@ size_t method_ws_bytes(const cl_plan* p) {
         case CL_METHOD_KN2COL:
             return xs + kk * d.m * nhw * 4;
         case CL_METHOD_IM2COL:
+        case CL_METHOD_IM2ROW:
             return npq * row_bytes(p->planes, p->Kp);
         case CL_METHOD_DIRECT:
             return 0;
@@ -365,7 +371,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             ++p->launches;
             break;
         }
-        case CL_METHOD_IM2COL: {
+        case CL_METHOD_IM2COL:
+        case CL_METHOD_IM2ROW: {
             void* pm = wsf;
             launch_im2col_split(x, pm, d.n, d.c, d.h, d.w, d.k, d.pad, d.stride, p->P, p->Q, p->Kp, p->planes, s);
             ++p->launches;
@@ -418,6 +425,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
                 "ConvProblem: kernel size " + std::to_string(d.k) + " exceeds padded image bound " +
                     std::to_string(bound));
         require(precision == CL_PREC_FP32 || precision == CL_PREC_TF32 || precision == CL_PREC_BF16, "unknown precision");
+        require(method >= CL_METHOD_AUTO && method <= CL_METHOD_IM2ROW, "unknown method " + std::to_string((int)method));
         if (method == CL_METHOD_CONV1X1)
             require(d.k == 1, "conv1x1 requires a 1x1 kernel, got k = " + std::to_string(d.k));
         const int P = (d.h + 2 * d.pad - d.k) / d.stride + 1;
@@ -427,7 +435,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         if (d.k == 1 && (m == CL_METHOD_KN2ROW_EXPLICIT || m == CL_METHOD_KN2COL)) m = CL_METHOD_CONV1X1;
         if (m == CL_METHOD_DIRECT) {
             // any shape: the shared-memory kernels where they fit, else the generic loop nest
-        } else if (m != CL_METHOD_IM2COL) {
+        } else if (!is_patch_method(m)) {
             if (d.stride != 1) throw Error(CL_EUNSUPPORTED, "kn2 methods support stride 1 only (im2col supports stride)");
             if (d.pad > 127 || d.k - 1 - d.pad > 128)
                 throw Error(CL_EUNSUPPORTED, "padding outside the TMA im2col bounding-box range");
@@ -448,7 +456,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         p->Cp = round_up(d.c, k_granule(p->planes));
         p->Kp = round_up(d.k * d.k * d.c, k_granule(p->planes));
         p->bn = bn_for(d.m);
-        if (m == CL_METHOD_IM2COL) p->wpack_bytes = (size_t)d.m * row_bytes(p->planes, p->Kp);
+        if (is_patch_method(m)) p->wpack_bytes = (size_t)d.m * row_bytes(p->planes, p->Kp);
         else if (m == CL_METHOD_DIRECT) p->wpack_bytes = (size_t)d.m * d.k * d.k * d.c * 4;
         else p->wpack_bytes = (size_t)d.k * d.k * d.m * row_bytes(p->planes, p->Cp);
         if (cudaMalloc(&p->wpack, p->wpack_bytes) != cudaSuccess) {
@@ -492,7 +500,7 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
         std::lock_guard<std::mutex> lock(p->mu);
         order_after_previous(p, s);
         const cl_conv_desc& d = p->d;
-        if (p->method == CL_METHOD_IM2COL)
+        if (is_patch_method(p->method))
             launch_rows_split(d_w, p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);   // MKKC == M x k^2C
         else if (p->method == CL_METHOD_DIRECT)
             CLB_CUDA(cudaMemcpyAsync(p->wpack, d_w, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
@@ -515,7 +523,7 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
         CLB_CUDA(cudaMallocAsync(&dw, bytes, s));
         CLB_CUDA(cudaMemcpyAsync(dw, h_w, bytes, cudaMemcpyHostToDevice, s));
         const cl_conv_desc& d = p->d;
-        if (p->method == CL_METHOD_IM2COL)
+        if (is_patch_method(p->method))
             launch_rows_split(static_cast<float*>(dw), p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);
         else if (p->method == CL_METHOD_DIRECT)
             CLB_CUDA(cudaMemcpyAsync(p->wpack, dw, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
@@ -764,6 +772,7 @@ const char* cl_method_name(cl_method m) {
         case CL_METHOD_KN2COL: return "kn2col-gpu";
         case CL_METHOD_KN2ROW_ACC: return "kn2row-acc-gpu";
         case CL_METHOD_IM2COL: return "im2col-gpu";
+        case CL_METHOD_IM2ROW: return "im2row-gpu";
         case CL_METHOD_CONV1X1: return "conv1x1-gpu";
         case CL_METHOD_DIRECT: return "direct-gpu";
     }
@@ -772,7 +781,7 @@ const char* cl_method_name(cl_method m) {
 
 int cl_method_from_name(const char* name, cl_method* out) {
     if (!name || !out) return 0;
-    for (int m = CL_METHOD_AUTO; m <= CL_METHOD_DIRECT; ++m) {
+    for (int m = CL_METHOD_AUTO; m <= CL_METHOD_IM2ROW; ++m) {
         if (std::strcmp(name, cl_method_name((cl_method)m)) == 0) {
             *out = (cl_method)m;
             return 1;

@@ -33,6 +33,7 @@ constexpr NameEntry kNames[] = {
     {ConvMethod::Conv1x1Gpu, "conv1x1-gpu"},
     {ConvMethod::Auto, "auto"},
     {ConvMethod::DirectGpu, "direct-gpu"},
+    {ConvMethod::Im2rowGpu, "im2row-gpu"},
 };
 
 void check(cl_status s) {
@@ -52,6 +53,7 @@ cl_method to_cl(ConvMethod m) {
         case ConvMethod::Conv1x1Gpu: return CL_METHOD_CONV1X1;
         case ConvMethod::Auto: return CL_METHOD_AUTO;
         case ConvMethod::DirectGpu: return CL_METHOD_DIRECT;
+        case ConvMethod::Im2rowGpu: return CL_METHOD_IM2ROW;
         default:
             throw std::invalid_argument("method '" + std::string(to_string(m)) +
                                         "' is a reference CPU method; the B200 path runs GPU methods only");
@@ -67,6 +69,7 @@ ConvMethod from_cl(cl_method m) {
         case CL_METHOD_IM2COL: return ConvMethod::Im2colGpu;
         case CL_METHOD_CONV1X1: return ConvMethod::Conv1x1Gpu;
         case CL_METHOD_DIRECT: return ConvMethod::DirectGpu;
+        case CL_METHOD_IM2ROW: return ConvMethod::Im2rowGpu;
         default: return ConvMethod::Auto;
     }
 }
@@ -125,7 +128,8 @@ CLB_EXPORT bool is_gpu_method(ConvMethod m) { return static_cast<int>(m) >= stat
 CLB_EXPORT const std::vector<ConvMethod>& default_gpu_methods() {
     static const std::vector<ConvMethod> all = {ConvMethod::Kn2rowGpu, ConvMethod::Kn2rowExplicitGpu,
                                                 ConvMethod::Kn2colGpu, ConvMethod::Kn2rowAccGpu,
-                                                ConvMethod::Im2colGpu, ConvMethod::DirectGpu};
+                                                ConvMethod::Im2colGpu, ConvMethod::Im2rowGpu,
+                                                ConvMethod::DirectGpu};
     return all;
 }
 
@@ -141,6 +145,7 @@ CLB_EXPORT FootprintBytes footprint(const LayerConfig& l, ConvMethod m) {
         case ConvMethod::Im2col:
         case ConvMethod::Im2row:
         case ConvMethod::Im2colGpu:
+        case ConvMethod::Im2rowGpu:
             fp.intermediate_bytes = 4 * k * k * c * h * w;
             break;
         case ConvMethod::Kn2row:

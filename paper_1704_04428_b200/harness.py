@@ -73,7 +73,7 @@ def benchmark(layer: LayerConfig, method: str = "auto", runs: int = 5, seed: int
     if runs < 1:
         raise ValueError("benchmark: runs must be >= 1")
     require_device(device)
-    if layer.stride != 1 and method != "im2col-gpu":
+    if layer.stride != 1 and method not in ("im2col-gpu", "im2row-gpu", "direct-gpu"):
         raise ValueError(f"benchmark: strided layer '{layer.name}' is not supported")
     with ConvPlan(layer, method, precision, device) as plan:
         x = torch.empty((layer.batch, layer.channels, layer.height, layer.width), device=f"cuda:{device}")
@@ -160,7 +160,7 @@ def parse_csv(text: str) -> List[BenchResult]:
 # ---------------------------------------------------------------------------------------
 # verify  <- convlab::verify (bench.cpp:158-209; bench.hpp:69-101)
 # ---------------------------------------------------------------------------------------
-VERIFY_DEFAULT_METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu",
+VERIFY_DEFAULT_METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu", "im2row-gpu",
                           "conv1x1-gpu"]
 
 

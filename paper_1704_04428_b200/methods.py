@@ -23,8 +23,8 @@ from . import _lib
 # Reference method names in canonical order (methods.cpp:11-41) -- CPU, reference-only.
 REFERENCE_METHODS = ["direct-sum", "direct-loopnest", "im2col", "im2row", "kn2row", "kn2col", "conv1x1"]
 # GPU methods of this package (the -gpu suffix of SURVEY.md 8b) plus the selector.
-GPU_METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu", "conv1x1-gpu",
-               "direct-gpu"]
+GPU_METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu", "im2row-gpu",
+               "conv1x1-gpu", "direct-gpu"]
 ALL_METHODS = REFERENCE_METHODS + GPU_METHODS + ["auto"]
 PRECISIONS = ("fp32", "tf32", "bf16")
 
@@ -98,7 +98,7 @@ def footprint(layer: LayerConfig, method: str) -> dict:
     GPU methods report the intermediate they materialise: the implicit kernels none."""
     c, h, w, m, k = layer.channels, layer.height, layer.width, layer.kernel_count, layer.kernel_size
     fp = {"input_bytes": 4 * c * h * w, "kernel_bytes": 4 * m * k * k * c, "output_bytes": 4 * m * h * w}
-    if method in ("im2col", "im2row", "im2col-gpu"):
+    if method in ("im2col", "im2row", "im2col-gpu", "im2row-gpu"):
         inter = 4 * k * k * c * h * w
     elif method in ("kn2row", "kn2col", "kn2row-explicit-gpu", "kn2col-gpu"):
         inter = 4 * k * k * m * h * w

@@ -44,7 +44,7 @@ bool throws(F&& f) {
 static void cpu_tests() {
     // name round trip (methods_test.cpp pattern)
     for (auto m : {ConvMethod::DirectSum, ConvMethod::Kn2row, ConvMethod::Kn2rowGpu, ConvMethod::Im2colGpu,
-                   ConvMethod::Kn2rowAccGpu, ConvMethod::Auto}) {
+                   ConvMethod::Im2rowGpu, ConvMethod::Kn2rowAccGpu, ConvMethod::Auto, ConvMethod::DirectGpu}) {
         auto back = method_from_name(to_string(m));
         CHECK(back.has_value() && *back == m);
     }
@@ -82,6 +82,7 @@ static void gpu_tests() {
         {ConvMethod::Kn2colGpu, {"c", 8, 6, 5, 4, 3, 1, -1, 2}},
         {ConvMethod::Kn2rowAccGpu, {"acc", 8, 9, 9, 12, 3, 1, -1, 1}},
         {ConvMethod::Im2colGpu, {"i", 3, 10, 10, 8, 3, 1, -1, 2}},
+        {ConvMethod::Im2rowGpu, {"r", 5, 9, 7, 6, 3, 1, -1, 2}},
         {ConvMethod::Auto, {"auto", 3, 12, 12, 16, 3, 1, -1, 1}},
     };
     for (const auto& c : cases) {

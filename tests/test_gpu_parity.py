@@ -17,7 +17,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 FP32_L2, FP32_MAX, TF32_L2 = 1e-5, 1e-4, 1e-2
-METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu", "direct-gpu"]
+METHODS = ["kn2row-gpu", "kn2row-explicit-gpu", "kn2col-gpu", "kn2row-acc-gpu", "im2col-gpu", "im2row-gpu",
+           "direct-gpu"]
 
 
 @pytest.fixture(scope="module")
@@ -191,7 +192,8 @@ def test_one_contraction_per_call(oracle, clb, torch_cuda):
     torch = torch_cuda
     layer = clb.LayerConfig("l", 3, 6, 6, 2, 3, batch=1)
     x, w = oracle.make_problem(1, 3, 6, 6, 2, 3, 140)
-    expect = {"kn2row-gpu": 2, "kn2row-explicit-gpu": 3, "kn2col-gpu": 3, "im2col-gpu": 2, "kn2row-acc-gpu": 10,
+    expect = {"kn2row-gpu": 2, "kn2row-explicit-gpu": 3, "kn2col-gpu": 3, "im2col-gpu": 2, "im2row-gpu": 2,
+              "kn2row-acc-gpu": 10,
               "direct-gpu": 1}
     for method, n in expect.items():
         with clb.ConvPlan(layer, method) as plan:

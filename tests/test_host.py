@@ -51,9 +51,8 @@ def test_abi_basics_and_errors_without_gpu():
         assert L.cl_method_name(v).decode() == name
         out = ctypes.c_int()
         assert L.cl_method_from_name(name.encode(), ctypes.byref(out)) == 1 and out.value == v
+    assert _lib.METHODS["im2row-gpu"] == 8 and L.cl_method_name(9) == b"unknown"
     # contract violations are CL_EINVAL (the reference's std::invalid_argument) even without a GPU
-    for bad in (clb.LayerConfig, ):
-        pass
     cases = [
         dict(n=1, c=3, h=8, w=8, m=4, k=2, pad=-1, stride=1),   # even k  (tensor.cpp:64)
         dict(n=1, c=3, h=2, w=2, m=4, k=7, pad=-1, stride=1),   # k > min(H,W)+k/2 (conv_direct.cpp:15-20)
@@ -67,6 +66,8 @@ def test_abi_basics_and_errors_without_gpu():
     d = _lib.ConvDesc(n=1, c=3, h=8, w=8, m=4, k=3, pad=1, stride=1)
     h = ctypes.c_void_p()
     assert L.cl_conv_plan(ctypes.byref(d), 6, 0, 0, ctypes.byref(h)) == _lib.CL_EINVAL   # conv1x1 with k=3
+    assert L.cl_conv_plan(ctypes.byref(d), 42, 0, 0, ctypes.byref(h)) == _lib.CL_EINVAL  # unknown method value
+    assert b"unknown method" in L.cl_last_error()
     if L.cl_device_count() == 0:
         assert L.cl_conv_plan(ctypes.byref(d), 1, 0, 0, ctypes.byref(h)) == _lib.CL_ENODEVICE
         assert b"no CPU fallback" in L.cl_last_error() or b"device" in L.cl_last_error()
