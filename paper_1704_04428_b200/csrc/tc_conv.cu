@@ -115,10 +115,13 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     const int smem = tc_smem_bytes(p.bn / cg, p.tps, p.stages);
     static bool configured[3] = {false, false, false};
     if (!configured[cg]) {
-        if (cg == 2)
-            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        else
-            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        if (cg == 2) {
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        } else {
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        }
         configured[cg] = true;
     }
     const int sms = num_sms();
@@ -207,8 +210,12 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
         }
         CLB_CUDA(cudaEventRecord(tev[0], s));
     }
-    cudaError_t e = cg == 2 ? cudaLaunchKernelEx(&cfg, tc_conv_kernel<2>, ma, mb, p)
-                            : cudaLaunchKernelEx(&cfg, tc_conv_kernel<1>, ma, mb, p);
+    // the traced instantiation carries the diagnostics; the production one has none of their
+    // registers (they were live across the whole epilogue loop)
+    cudaError_t e = trace ? (cg == 2 ? cudaLaunchKernelEx(&cfg, tc_conv_kernel<2, true>, ma, mb, p)
+                                     : cudaLaunchKernelEx(&cfg, tc_conv_kernel<1, true>, ma, mb, p))
+                          : (cg == 2 ? cudaLaunchKernelEx(&cfg, tc_conv_kernel<2, false>, ma, mb, p)
+                                     : cudaLaunchKernelEx(&cfg, tc_conv_kernel<1, false>, ma, mb, p));
     CLB_CUDA(e);
     if (trace) {
         CLB_CUDA(cudaEventRecord(tev[1], s));

@@ -230,14 +230,14 @@ __device__ __forceinline__ void store_nchw(float* o, long long plane, int nvalid
 //         on the leader's barrier, the leader issues M=256 MMAs reading both CTAs' smem and
 //         multicasts its commits; each CTA's TMEM holds its 128 D rows.  Per-SM operand
 //         bytes per MMA drop by BN/2 rows (-33% at BN = 256).
-template <int CG>
+template <int CG, bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const long long t_entry = p.trace ? clock64() : 0;
-    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * kTraceSlots + 9] = globaltimer_ns();
+    const long long t_entry = TRACE ? clock64() : 0;
+    if (TRACE && threadIdx.x == 0) p.trace[blockIdx.x * kTraceSlots + 9] = globaltimer_ns();
 
     const int bn = p.bn;
     const int planes = p.planes;
@@ -316,7 +316,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint32_t tx = (uint32_t)CG * stage_tx;   // both CTAs' bytes land on the leader
             long long w_empty = 0;
             const long long t_start = clock64();
-            if (p.trace && lane_id() == 0) p.trace[blockIdx.x * kTraceSlots + 8] = (unsigned long long)(t_start - t_entry);
+            if (TRACE && lane_id() == 0) p.trace[blockIdx.x * kTraceSlots + 8] = (unsigned long long)(t_start - t_entry);
             Sched sch(p, unit, nunits);
             Piece pc;
             while (sch.next(pc)) {
@@ -335,7 +335,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 for (int it = it0; it < it1; ++it) {
                     const int kc = kb * p.row_elems;
                     const int arow = ca.c1 + grp * p.a_row_shift;   // padded-row mode: tap row i -> +i Wp
-                    if (p.trace) {
+                    if (TRACE) {
                         const long long t0 = clock64();
                         mbar_wait(&empty[stage], phase ^ 1u);
                         w_empty += clock64() - t0;
@@ -382,7 +382,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     }
                 }
             }
-            if (p.trace && lane_id() == 0) {
+            if (TRACE && lane_id() == 0) {
                 p.trace[blockIdx.x * kTraceSlots + 0] = (unsigned long long)(clock64() - t_start);
                 p.trace[blockIdx.x * kTraceSlots + 1] = (unsigned long long)w_empty;
             }
@@ -430,7 +430,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const int c1 = c0 + ci < k_iters ? c0 + ci : k_iters;
                 const uint32_t buf = lg & (uint32_t)(nbuf - 1);
                 const uint32_t tph = (lg >> nb_shift) & 1u;
-                if (p.trace) {
+                if (TRACE) {
                     const long long t0 = clock64();
                     mbar_wait(&tempty[buf], tph ^ 1u);
                     w_tempty += clock64() - t0;
@@ -440,7 +440,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + buf * buf_cols;
                 for (int it = c0; it < c1; ++it) {
-                    if (p.trace) {
+                    if (TRACE) {
                         const long long t0 = clock64();
                         mbar_wait(&full[stage], phase);
                         w_full += clock64() - t0;
@@ -490,7 +490,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 if (elect_one()) commit(&tfull[buf]);   // chunk complete -> epilogue(s)
                 __syncwarp();
             }
-            if (p.trace && lane_id() == 0) {
+            if (TRACE && lane_id() == 0) {
                 p.trace[blockIdx.x * kTraceSlots + 2] = (unsigned long long)(clock64() - t_start);
                 p.trace[blockIdx.x * kTraceSlots + 3] = (unsigned long long)w_full;
                 p.trace[blockIdx.x * kTraceSlots + 4] = (unsigned long long)w_tempty;
@@ -535,19 +535,19 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const uint32_t tph = (lg >> nb_shift) & 1u;
                 if (finisher && c == pc.c_hi - 1) {
                     const uint64_t t0 = globaltimer_ns();
-                    const long long c0 = p.trace ? clock64() : 0;
+                    const long long c0 = TRACE ? clock64() : 0;
                     for (int u2 = unit + 1; u2 < u_end; ++u2) {
                         while (ld_acquire_u32(&p.flags[u2 * CG + (int)rank]) == 0u) {
                             if (globaltimer_ns() - t0 > 4000000000ull) __trap();
                         }
                     }
-                    if (p.trace) {
+                    if (TRACE) {
                         w_fix += clock64() - c0;
                         n_parts += (unsigned long long)(u_end - unit - 1);
                         t_acq = globaltimer_ns();
                     }
                 }
-                if (p.trace) {
+                if (TRACE) {
                     const long long t0 = clock64();
                     mbar_wait(&tfull[buf], tph);
                     w_tfull += clock64() - t0;
@@ -577,7 +577,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     else mbar_arrive(&tempty[buf]);
                 }
             }
-            if (p.trace) t_folded = globaltimer_ns();
+            if (TRACE) t_folded = globaltimer_ns();
             if (pc.c_lo > 0) {
                 // ---- tile tail handled by this CTA: publish the partial for the finisher ----
                 // lane-contiguous float4 layout [slot][col/4][row]: a warp's store is 512
@@ -592,7 +592,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 // release (release is cumulative over what the releasing thread has observed)
                 epi_bar_sync();
                 if (threadIdx.x == 4 * 32) st_release_u32(&p.flags[blockIdx.x], 1u);
-                if (p.trace) t_pub = globaltimer_ns();
+                if (TRACE) t_pub = globaltimer_ns();
                 continue;
             }
             if (finisher) {
@@ -610,7 +610,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             sum[j + 3] += v.w;
                         }
                 }
-                if (p.trace) t_added = globaltimer_ns();
+                if (TRACE) t_added = globaltimer_ns();
                 // every published partial has exactly one finisher: reset its flags so the
                 // buffer is clean for the next launch (no memset launch needed)
                 epi_bar_sync();
@@ -618,7 +618,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     for (int u2 = unit + 1; u2 < u_end; ++u2) p.flags[u2 * CG + (int)rank] = 0u;
             }
             // ---- store the finished tile ----
-            const long long t_st = p.trace ? clock64() : 0;
+            const long long t_st = TRACE ? clock64() : 0;
             if (row < p.rows && p.epi == EPI_NCHW_PADDED) {
                 // padded output space: row = n*Hp*Wp + y*Wp + x; only y < P, x < Q are outputs
                 const int hw = p.epi_hp * p.epi_wp;
@@ -655,12 +655,12 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     }
                 }
             }
-            if (p.trace) {
+            if (TRACE) {
                 w_store += clock64() - t_st;
                 t_stored = globaltimer_ns();
             }
         }
-        if (p.trace && threadIdx.x == 4 * 32) {
+        if (TRACE && threadIdx.x == 4 * 32) {
             p.trace[blockIdx.x * kTraceSlots + 5] = (unsigned long long)(clock64() - t_start);
             p.trace[blockIdx.x * kTraceSlots + 6] = (unsigned long long)w_tfull;
             p.trace[blockIdx.x * kTraceSlots + 7] = (unsigned long long)w_store;
@@ -682,7 +682,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         if constexpr (CG == 2) tmem_dealloc_2sm(tmem_base, ncols);
         else tmem_dealloc(tmem_base, ncols);
     }
-    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * kTraceSlots + 10] = globaltimer_ns();
+    if (TRACE && threadIdx.x == 0) p.trace[blockIdx.x * kTraceSlots + 10] = globaltimer_ns();
 }
 
 #endif  // CLB_DEFINE_TC_KERNEL
