@@ -109,6 +109,14 @@ for wl in args.workloads.split(","):
                 per_img = min(t)
                 row[f"cpu_{m}_s_per_image"] = per_img
                 row[f"cpu_{m}_tflops"] = fl / layer.batch / per_img / 1e12
+            # the reference's single-core backend (GemmBackend::blocked), for the thread scaling
+            # SURVEY 8(d) asks to report beside parallel(T)
+            t0 = time.perf_counter()
+            O.ref_run_method("kn2row", xi, wi, 0)
+            one = time.perf_counter() - t0
+            row["cpu_kn2row_1core_s_per_image"] = one
+            row["cpu_kn2row_1core_tflops"] = fl / layer.batch / one / 1e12
+            row["cpu_kn2row_thread_scaling"] = one / row["cpu_kn2row_s_per_image"]
             row["cpu_threads"] = threads
         rows.append(row)
         print(json.dumps(row), file=sys.stderr, flush=True)

@@ -7,8 +7,8 @@ CFG = {"c1": "C1", "alexnet-b1": "C2 b1", "alexnet": "C2 b128", "vgg16": "C3", "
 txt = open(sys.argv[1]).read()
 d = json.loads(txt[txt.index("{"):])
 print("| config | layer | N | method | GFLOP | kernel µs | eff. TFLOP/s | % of 277.8 | layer roofline % "
-      "| graph fwd µs | rel-L2 | CPU kn2row GFLOP/s | CPU im2col GFLOP/s |")
-print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+      "| graph fwd µs | rel-L2 | CPU kn2row GFLOP/s | CPU im2col GFLOP/s | CPU kn2row 1-core GFLOP/s |")
+print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
 for r in d["rows"]:
     batch1 = r["N"] == 1 or r["workload"] == "googlenet"
     us = (r["graph_forward_ms"] if batch1 else r["kernel_ms"]) * 1e3
@@ -16,4 +16,5 @@ for r in d["rows"]:
     print(f"| {CFG.get(r['workload'], r['workload'])} | {r['layer']} | {r['N']} | {r['method']} | {r['gflop']:.2f} | "
           f"{us:.0f} | {tf:.1f} | {100 * tf / d['peak_3xtf32_tflops']:.0f} | "
           f"{100 * tf / r['roofline_tflops']:.0f} | {r['graph_forward_ms'] * 1e3:.0f} | {r['rel_l2']:.1e} | "
-          f"{r['cpu_kn2row_tflops'] * 1e3:.1f} | {r['cpu_im2col_tflops'] * 1e3:.1f} |")
+          f"{r['cpu_kn2row_tflops'] * 1e3:.1f} | {r['cpu_im2col_tflops'] * 1e3:.1f} | "
+          f"{r.get('cpu_kn2row_1core_tflops', float('nan')) * 1e3:.1f} |")
