@@ -102,7 +102,11 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     const int k_iters = (p.taps / p.tps) * p.kblocks;
     // 128 K-elements per accumulation chunk for the fp32-faithful mode; coarser for the fast
     // modes, whose input rounding dominates the accumulator's
-    if (p.chunk_iters <= 0) p.chunk_iters = p.planes == 2 ? kChunkIters : kChunkIters / 2;
+    // chunk = K slice per TMEM accumulator: 3xTF32 needs <= 128 K-elements per chunk to stay
+    // fp32-faithful (8 stages); the 1e-2 fast modes only chunk for stream-K granularity, and
+    // 16 stages keep the epilogue's fold rate below the MMA's (4 stages had the MMA waiting on
+    // TMEM 11-25 % of the time, CLB_TRACE)
+    if (p.chunk_iters <= 0) p.chunk_iters = p.planes == 2 ? kChunkIters : 2 * kChunkIters;
     if (p.tps > 1) p.chunk_iters = p.chunk_iters / p.tps > 0 ? p.chunk_iters / p.tps : 1;   // a stage holds tps taps
     if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
     const int tile_m = kTileM * cg;
