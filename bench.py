@@ -50,6 +50,9 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=None, help="override the per-GPU batch")
     ap.add_argument("--method", default="auto")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "bf16"])
+    ap.add_argument("--layout", default="nchw", choices=["nchw", "nhwc"],
+                    help="device tensors NCHW (the reference interface, default) or channels-last "
+                         "(cl_conv_forward_nhwc; the e2e leg stays NCHW)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline work")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -251,6 +254,10 @@ def main():
     plans, xs, ys, wss, evs = [], [], [], [], []
     for li, l in enumerate(layers):
         plan = clb.ConvPlan(l, args.method, args.precision, dev)
+        if args.layout == "nhwc" and plan.method not in ("kn2row-gpu", "conv1x1-gpu", "kn2row-acc-gpu"):
+            # channels-last is served by the implicit kernel only: plan that one explicitly
+            plan.close()
+            plan = clb.ConvPlan(l, "kn2row-gpu" if l.kernel_size > 1 else "conv1x1-gpu", args.precision, dev)
         x = torch.empty((l.batch, l.channels, l.height, l.width), device=dev, dtype=torch.float32)
         w = torch.empty((l.kernel_count, l.kernel_size, l.kernel_size, l.channels), device=dev, dtype=torch.float32)
         img = l.channels * l.height * l.width
@@ -259,6 +266,9 @@ def main():
         plan.set_weights(w)
         ws = torch.empty(max(plan.workspace_bytes(), 4), device=dev, dtype=torch.uint8)
         y = torch.empty(plan.output_shape(), device=dev, dtype=torch.float32)
+        if args.layout == "nhwc":   # same values, channels-last storage
+            x = x.permute(0, 2, 3, 1).contiguous()
+            y = y.permute(0, 2, 3, 1).contiguous()
         plans.append(plan)
         xs.append(x)
         ys.append(y)
@@ -271,7 +281,7 @@ def main():
             if record_kernel is not None:
                 b, e = record_kernel[li]
                 _lib.lib().cl_conv_set_profile_events(plan._h, b.cuda_event, e.cuda_event)
-            plan.forward(xs[li], ys[li], wss[li])
+            plan.forward(xs[li], ys[li], wss[li], layout=args.layout)
             if record_kernel is not None:
                 _lib.lib().cl_conv_set_profile_events(plan._h, None, None)
 
@@ -372,6 +382,7 @@ def main():
         "data": "synthetic: reference generator uniform[-1,1) (tensor.cpp:104-134) on device, random-init weights",
         "config": {
             "workload": args.workload, "layers": [l.name for l in layers], "per_gpu_batch": layers[0].batch,
+            "layout": args.layout,
             "global_batch": layers[0].batch * info.world, "method": args.method,
             "resolved_methods": sorted({p.method for p in plans}),
             "precision": {"fp32": "fp32-faithful 3xTF32", "tf32": "tf32 (fast mode)",

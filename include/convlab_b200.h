@@ -116,6 +116,13 @@ CL_API cl_method cl_conv_resolved_method(const cl_plan* plan);
  * allocated workspace.  Asynchronous on `stream`; returns after enqueueing. */
 CL_API cl_status cl_conv_forward(cl_plan* plan, const float* d_x, float* d_y, void* d_ws, void* stream);
 
+/* Channels-last variant: x is [N][H][W][C] and y is [N][P][Q][M] (the reference's HWC
+ * Tensor3 layout, tensor.hpp:86-90, stacked; conv_kn2row accepts HWC input,
+ * conv_kn2.cpp:147-151).  The prepass is an elementwise split (no transpose) and the output
+ * rows are written contiguously.  Implicit kn2row / conv1x1 / kn2row-acc plans only
+ * (CL_EUNSUPPORTED otherwise).  Asynchronous on `stream`. */
+CL_API cl_status cl_conv_forward_nhwc(cl_plan* plan, const float* d_x, float* d_y, void* d_ws, void* stream);
+
 /* Host-buffer end-to-end call (the run_method surface): H2D of x, forward, D2H of y,
  * synchronous.  Host buffers should be pinned for full PCIe bandwidth. */
 CL_API cl_status cl_conv_forward_host(cl_plan* plan, const float* h_x, float* h_y, void* stream);

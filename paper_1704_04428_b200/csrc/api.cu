@@ -219,7 +219,8 @@ void mark_done(cl_plan* p, cudaStream_t s) {
 }
 
 // n_images < 0: the plan's batch; otherwise a sub-batch (chunked host pipeline).
-void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images = -1) {
+// nhwc: channels-last input and output (implicit kn2row / conv1x1 / accumulating only).
+void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images = -1, bool nhwc = false) {
     cl_conv_desc d = p->d;
     if (n_images >= 0) d.n = n_images;
     require(p->weights_set, "cl_conv_forward: weights not set (cl_conv_set_weights)");
@@ -284,7 +285,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 // tap-shared mode: zero-padded NHWC rows; each stage loads ONE A box of 128+k-1
                 // rows per kernel row i and feeds its k taps through row-shifted descriptors
                 const int Hp = d.h + 2 * d.pad, Wp = d.w + 2 * d.pad;
-                launch_nchw_to_padded_split(x, xs, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                else launch_nchw_to_padded_split(x, xs, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
                 ++p->launches;
                 Operand a = tiled(xs, (long long)d.n * Hp * Wp, 1, p->Cp, p->planes);
                 Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
@@ -295,7 +297,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 t.b_tap3 = 1;
                 t.tps = d.k;
                 t.a_row_shift = Wp;
-                t.epi = EPI_NCHW_PADDED;
+                t.epi = nhwc ? EPI_NHWC_PADDED : EPI_NCHW_PADDED;
+                t.ld = d.m;
                 t.epi_hp = Hp;
                 t.epi_wp = Wp;
                 t.epi_n = d.n;
@@ -307,7 +310,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 tc_done();
                 break;
             }
-            launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
+            if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s);
+            else launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
             ++p->launches;
             Operand a = implicit_a(p, xs);
             a.n = d.n;
@@ -317,7 +321,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             t.cols = d.m;
             t.bn = p->bn;
             t.b_tap3 = 1;
-            t.epi = EPI_NCHW;
+            t.epi = nhwc ? EPI_ROWMAJOR : EPI_NCHW;
+            t.ld = d.m;                       // channels-last: D[n*P*Q + pq][m] is the output
             t.out = y;
             t.out_channels = d.m;
             t.pq_out = p->P * p->Q;
@@ -339,6 +344,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         }
         case CL_METHOD_KN2ROW_EXPLICIT:
         case CL_METHOD_KN2COL: {
+            if (nhwc) throw Error(CL_EUNSUPPORTED, "channels-last forward: implicit kn2row / conv1x1 / kn2row-acc only");
             void* xs = wsf;
             float* inter = reinterpret_cast<float*>(reinterpret_cast<char*>(wsf) + nhw * row_bytes(p->planes, p->Cp));
             launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
@@ -373,6 +379,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         }
         case CL_METHOD_IM2COL:
         case CL_METHOD_IM2ROW: {
+            if (nhwc) throw Error(CL_EUNSUPPORTED, "channels-last forward: implicit kn2row / conv1x1 / kn2row-acc only");
             void* pm = wsf;
             launch_im2col_split(x, pm, d.n, d.c, d.h, d.w, d.k, d.pad, d.stride, p->P, p->Q, p->Kp, p->planes, s);
             ++p->launches;
@@ -392,6 +399,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             break;
         }
         case CL_METHOD_DIRECT: {
+            if (nhwc) throw Error(CL_EUNSUPPORTED, "channels-last forward: implicit kn2row / conv1x1 / kn2row-acc only");
             // the dominant (and only) kernel of this method: bracket it for the profile events
             if (p->ev_begin) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
             launch_direct_conv(x, p->wraw, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, d.stride, p->P, p->Q, s);
@@ -557,6 +565,18 @@ cl_status cl_conv_forward(cl_plan* p, const float* d_x, float* d_y, void* d_ws, 
         CLB_CUDA(cudaSetDevice(p->device));
         order_after_previous(p, s);
         forward(p, d_x, d_y, d_ws, s);
+        mark_done(p, s);
+    });
+}
+
+cl_status cl_conv_forward_nhwc(cl_plan* p, const float* d_x, float* d_y, void* d_ws, void* stream) {
+    return guarded([&] {
+        require(p, "cl_conv_forward_nhwc: null plan");
+        auto s = static_cast<cudaStream_t>(stream);
+        std::lock_guard<std::mutex> lock(p->mu);
+        CLB_CUDA(cudaSetDevice(p->device));
+        order_after_previous(p, s);
+        forward(p, d_x, d_y, d_ws, s, -1, true);
         mark_done(p, s);
     });
 }

@@ -46,6 +46,9 @@ inline long long row_bytes(int planes, long long kp) { return row_elems(planes, 
 void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s);
 // same, into the zero-padded image [n][H+2pad][W+2pad][row] (tap-shared kernel mode)
+// NHWC input (channels last) -> split rows; pad > 0 writes the zero-padded grid (tap-shared mode)
+void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
+                       cudaStream_t s);
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
                                  cudaStream_t s);
 // a[rows][K] -> as[rows][planes][Kp]

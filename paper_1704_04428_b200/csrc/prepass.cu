@@ -143,6 +143,94 @@ void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, 
     CLB_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------- NHWC -> split rows ----
+// Channels-last input (the reference's HWC Tensor3 layout, tensor.hpp:86-90, stacked):
+// the split is elementwise along each pixel row, so no transpose: thread = (output row,
+// 4 channels), float4 in, hi / lo float4 out.  The output rows are either the image pixels
+// or (pad > 0) the zero-padded pixel grid of the tap-shared mode.  (row, quad) comes from a
+// multiply-shift divide (n < 2^31): a runtime 32/64-bit division per element costs more
+// issue slots than the bytes it moves.
+struct FastDiv {
+    uint32_t d, m, s;
+};
+
+static FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f{d, 0, 0};
+    while ((1ull << f.s) < d) ++f.s;
+    f.m = (uint32_t)((((1ull << 32) * ((1ull << f.s) - d)) / d) + 1);
+    return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+    return (__umulhi(n, f.m) + n) >> f.s;
+}
+
+__global__ void __launch_bounds__(256) nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xs,
+                                                         uint32_t total, FastDiv q4d, FastDiv pixd, FastDiv wpd, int C,
+                                                         int Cp, int planes, int H, int W, int pad) {
+    const uint32_t i = blockIdx.x * 256u + threadIdx.x;
+    if (i >= total) return;
+    const uint32_t r = fdiv(i, q4d);                 // output row
+    const int c = (int)(i - r * q4d.d) * 4;          // first of 4 channels
+    long long src = r;
+    if (pad > 0) {                                   // padded grid: row = (n, yp, xp)
+        const uint32_t n = fdiv(r, pixd);
+        const uint32_t rem = r - n * pixd.d;
+        const uint32_t yp = fdiv(rem, wpd);
+        const int y = (int)yp - pad, xq = (int)(rem - yp * wpd.d) - pad;
+        src = (y >= 0 && y < H && xq >= 0 && xq < W) ? ((long long)n * H + y) * W + xq : -1;
+    }
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (src >= 0) {
+        const float* px = x + src * C + c;
+        if ((C & 3) == 0 && c + 3 < C) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(px));
+            v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (c + e < C) v[e] = __ldg(px + e);
+        }
+    }
+    if (planes == kPlanesBf16) {
+        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(xs) + (long long)r * Cp + c;
+        __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+        uint2 packed;
+        packed.x = *reinterpret_cast<uint32_t*>(&a);
+        packed.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(dst) = packed;
+        return;
+    }
+    float hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        hi[e] = tf32_rna(v[e]);
+        lo[e] = v[e] - hi[e];
+    }
+    float* dst = static_cast<float*>(xs) + (long long)r * rowel(planes, Cp);
+    if (planes == 2) {
+        const int u = (c >> 4) << 5, w = c & 15;      // 128 B unit [hi 16 | lo 16]
+        *reinterpret_cast<float4*>(dst + u + w) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(dst + u + 16 + w) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    } else {
+        *reinterpret_cast<float4*>(dst + c) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    }
+}
+
+void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
+                       cudaStream_t s) {
+    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+    const long long rows = (long long)N * Hp * Wp;
+    const int q4 = Cp / 4;
+    const long long total = rows * q4;
+    if (total >= (1ll << 31)) throw Error(2, "NHWC prepass: more than 2^31 channel quads (split the batch)");
+    const FastDiv q4d = make_fastdiv((uint32_t)q4), pixd = make_fastdiv((uint32_t)(Hp * Wp)),
+                  wpd = make_fastdiv((uint32_t)Wp);
+    nhwc_split_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(x, xs, (uint32_t)total, q4d, pixd, wpd, C, Cp,
+                                                                      planes, H, W, pad);
+    CLB_CUDA(cudaGetLastError());
+}
+
 // -------------------------------------------------------------------- row-wise split ----
 // grid (ceil(Kp/128), rows), block 128
 __global__ void rows_split_kernel(const float* __restrict__ a, void* __restrict__ as, int K, int Kp,

@@ -38,7 +38,7 @@
 namespace clb {
 
 enum : int { LOAD_TILED = 0, LOAD_IM2COL = 1 };
-enum : int { EPI_NCHW = 0, EPI_ROWMAJOR = 1, EPI_NCHW_PADDED = 2 };
+enum : int { EPI_NCHW = 0, EPI_ROWMAJOR = 1, EPI_NCHW_PADDED = 2, EPI_NHWC_PADDED = 3 };
 
 constexpr int kTileM = 128;          // UMMA M (D rows per tile)
 // Operand rows are 128-byte units (SWIZZLE_128B, one TMA box per operand per stage):
@@ -220,6 +220,27 @@ __device__ __forceinline__ void store_nchw(float* o, long long plane, int nvalid
         for (int j = 0; j < 128; ++j) {
             if (j < nvalid) *o = sum[j];
             o += plane;
+        }
+    }
+}
+
+// One D row's columns into a row-major (channels-last) output row: float4 where aligned.
+__device__ __forceinline__ void store_rowmajor(float* dst, long long ld, int col0, int hcols, int cols, int accumulate,
+                                               const float* sum) {
+    const bool vec = (ld % 4 == 0) && !accumulate && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+#pragma unroll
+    for (int j = 0; j < 128; j += 4) {
+        if (j < hcols) {
+            if (vec && col0 + j + 3 < cols) {
+                *reinterpret_cast<float4*>(dst + j) = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (col0 + j + e < cols) {
+                        if (accumulate) dst[j + e] += sum[j + e];
+                        else dst[j + e] = sum[j + e];
+                    }
+            }
         }
     }
 }
@@ -635,24 +656,18 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     const int pq = row - n * p.pq_out;
                     store_nchw(p.out + ((long long)n * p.out_channels + col0) * p.pq_out + pq, p.pq_out,
                                min(hcols, p.cols - col0), p.accumulate, sum);
+                } else if (p.epi == EPI_NHWC_PADDED) {
+                    // padded pixel space -> channels-last output row (n*P + y)*Q + x
+                    const int hw = p.epi_hp * p.epi_wp;
+                    const int n = row / hw;
+                    const int rem = row - n * hw;
+                    const int y = rem / p.epi_wp;
+                    const int xq = rem - y * p.epi_wp;
+                    if (n < p.epi_n && y < p.P && xq < p.Q)
+                        store_rowmajor(p.out + (((long long)n * p.P + y) * p.Q + xq) * p.ld + col0, p.ld, col0, hcols,
+                                       p.cols, p.accumulate, sum);
                 } else {
-                    float* dst = p.out + (long long)row * p.ld + col0;
-                    const bool vec = (p.ld % 4 == 0) && !p.accumulate;
-#pragma unroll
-                    for (int j = 0; j < 128; j += 4) {
-                        if (j < hcols) {
-                            if (vec && col0 + j + 3 < p.cols) {
-                                *reinterpret_cast<float4*>(dst + j) = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 4; ++e)
-                                    if (col0 + j + e < p.cols) {
-                                        if (p.accumulate) dst[j + e] += sum[j + e];
-                                        else dst[j + e] = sum[j + e];
-                                    }
-                            }
-                        }
-                    }
+                    store_rowmajor(p.out + (long long)row * p.ld + col0, p.ld, col0, hcols, p.cols, p.accumulate, sum);
                 }
             }
             if (TRACE) {

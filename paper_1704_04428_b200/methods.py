@@ -211,16 +211,25 @@ class ConvPlan:
     def output_shape(self):
         return (self.layer.batch, self.layer.kernel_count, *self.out_hw)
 
-    def forward(self, x, y=None, workspace=None, stream=None):
+    def forward(self, x, y=None, workspace=None, stream=None, layout: str = "nchw"):
+        """layout "nchw" (the reference's CHW images stacked) or "nhwc" (channels last, the
+        reference's HWC layout; implicit kn2row / conv1x1 / kn2row-acc plans)."""
         import torch
         L = self.layer
         assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
-        assert tuple(x.shape) == (L.batch, L.channels, L.height, L.width), x.shape
+        if layout not in ("nchw", "nhwc"):
+            raise ValueError(f"layout must be 'nchw' or 'nhwc', got '{layout}'")
+        if layout == "nchw":
+            assert tuple(x.shape) == (L.batch, L.channels, L.height, L.width), x.shape
+            out_shape = self.output_shape()
+        else:
+            assert tuple(x.shape) == (L.batch, L.height, L.width, L.channels), x.shape
+            out_shape = (L.batch, *self.out_hw, L.kernel_count)
         if y is None:
-            y = torch.empty(self.output_shape(), device=x.device, dtype=torch.float32)
+            y = torch.empty(out_shape, device=x.device, dtype=torch.float32)
         ws = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else None
-        _lib.check(_lib.lib().cl_conv_forward(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
-                                              ws, self._stream(stream)))
+        fn = _lib.lib().cl_conv_forward if layout == "nchw" else _lib.lib().cl_conv_forward_nhwc
+        _lib.check(fn(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), ws, self._stream(stream)))
         return y
 
     def forward_host(self, x_host, y_host, stream=None):

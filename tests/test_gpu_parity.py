@@ -506,3 +506,54 @@ def test_shared_plan_two_streams_and_threads(oracle, clb, torch_cuda):
         assert not errs, errs
         for y, ref in zip(outs2, refs):
             _check_fp32(oracle, y.cpu().numpy(), ref, "two threads")
+
+
+NHWC_CASES = [(2, 16, 30, 34, 32, 3, 1), (1, 48, 20, 24, 100, 5, 2), (3, 24, 7, 9, 40, 1, 0), (2, 20, 17, 19, 64, 7, 3),
+              (4, 64, 14, 14, 256, 3, 1), (2, 3, 12, 12, 16, 3, 1), (2, 32, 13, 13, 96, 3, 0)]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32", "bf16"])
+def test_nhwc_forward(oracle, clb, torch_cuda, precision):
+    """cl_conv_forward_nhwc (channels-last in and out, the reference's HWC layout): the
+    elementwise split prepass + row-major epilogue, in both the TMA im2col and the tap-shared
+    mode (forced on and off in subprocess-free form via shapes: padding waste decides)."""
+    torch = torch_cuda
+    for N, C, H, W, M, k, pad in NHWC_CASES:
+        x, w = oracle.make_problem(N, C, H, W, M, k, N * 7 + C)
+        ref = oracle.conv_loopnest(x, w, pad, 1)                       # NCHW
+        layer = clb.LayerConfig("nhwc", C, H, W, M, k, pad=pad, batch=N)
+        for method in ("kn2row-gpu", "kn2row-acc-gpu") if k > 1 else ("conv1x1-gpu",):
+            with clb.ConvPlan(layer, method, precision) as plan:
+                plan.set_weights(torch.from_numpy(w).cuda())
+                xn = torch.from_numpy(np.ascontiguousarray(x.transpose(0, 2, 3, 1))).cuda()
+                y = plan.forward(xn, layout="nhwc")
+                torch.cuda.synchronize()
+                got = y.cpu().numpy().transpose(0, 3, 1, 2)
+            m = oracle.parity_metrics(np.ascontiguousarray(got), ref)
+            if precision == "fp32":
+                assert m["rel_l2"] <= FP32_L2 and m["max_rel"] <= FP32_MAX, (method, (N, C, H, W, M, k, pad), m)
+            else:
+                assert m["rel_l2"] <= TF32_L2, (method, precision, (N, C, H, W, M, k, pad), m)
+
+
+def test_nhwc_unsupported_methods_and_unaligned_output(oracle, clb, torch_cuda):
+    torch = torch_cuda
+    from paper_1704_04428_b200 import _lib
+    N, C, H, W, M, k = 2, 8, 9, 9, 12, 3
+    x, w = oracle.make_problem(N, C, H, W, M, k, 3)
+    layer = clb.LayerConfig("nhwc", C, H, W, M, k, batch=N)
+    xn = torch.from_numpy(np.ascontiguousarray(x.transpose(0, 2, 3, 1))).cuda()
+    for method in ("kn2row-explicit-gpu", "kn2col-gpu", "im2col-gpu", "direct-gpu"):
+        with clb.ConvPlan(layer, method) as plan:
+            plan.set_weights(torch.from_numpy(w).cuda())
+            with pytest.raises(_lib.ClError, match="channels-last"):
+                plan.forward(xn, layout="nhwc")
+    # an output pointer 4 bytes off 16 B alignment takes the scalar store path
+    with clb.ConvPlan(layer, "kn2row-gpu") as plan:
+        plan.set_weights(torch.from_numpy(w).cuda())
+        buf = torch.zeros(N * H * W * M + 1, device="cuda")
+        y = buf[1:].view(N, H, W, M)
+        plan.forward(xn, y, layout="nhwc")
+        torch.cuda.synchronize()
+        got = y.cpu().numpy().transpose(0, 3, 1, 2)
+    _check_fp32(oracle, np.ascontiguousarray(got), oracle.conv_batch(x, w), "unaligned nhwc output")
