@@ -273,7 +273,9 @@ def main():
         xs.append(x)
         ys.append(y)
         wss.append(ws)
-    flush = torch.empty(256 * 1024 * 1024, device=dev, dtype=torch.uint8)
+    # L2 flush between timed steps: a write larger than the 126 MB L2 (MiB, CLB_FLUSH_MB to vary)
+    flush_mb = int(os.environ.get("CLB_FLUSH_MB", "256"))
+    flush = torch.empty(flush_mb * 1024 * 1024, device=dev, dtype=torch.uint8)
     flops_step = workloads.total_flops(layers)
 
     def step(record_kernel=None):
@@ -316,6 +318,8 @@ def main():
     sampler.stop()
 
     step_ms = [st_b[i].elapsed_time(st_e[i]) for i in range(args.steps)]
+    if os.environ.get("CLB_BENCH_STEP_MS"):        # diagnostics: per-step device times
+        print(json.dumps({"step_ms": [round(v, 4) for v in step_ms]}), file=sys.stderr)
     local_ms = sum(step_ms)
     kern_ms = [sum(k_ev[i][li][0].elapsed_time(k_ev[i][li][1]) for i in range(args.steps)) / args.steps
                for li in range(len(plans))]
