@@ -127,6 +127,12 @@ CL_API cl_status cl_conv_forward_nhwc(cl_plan* plan, const float* d_x, float* d_
  * synchronous.  Host buffers should be pinned for full PCIe bandwidth. */
 CL_API cl_status cl_conv_forward_host(cl_plan* plan, const float* h_x, float* h_y, void* stream);
 
+/* Asynchronous variant: returns after enqueueing (pinned host buffers recommended); `stream`
+ * receives the completion (synchronise it before reading h_y).  The copy-in does not wait
+ * for prior work on `stream` -- h_x must hold its data at the call -- only for this plan's
+ * previous call, so consecutive calls on different plans overlap their PCIe transfers. */
+CL_API cl_status cl_conv_forward_host_async(cl_plan* plan, const float* h_x, float* h_y, void* stream);
+
 /* Number of GPU kernel launches the last cl_conv_forward enqueued. */
 CL_API int cl_conv_last_launch_count(const cl_plan* plan);
 

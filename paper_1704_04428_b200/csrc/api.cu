@@ -94,6 +94,7 @@ struct cl_plan {
     cudaStream_t s_in = nullptr, s_out = nullptr;
     static constexpr int kMaxChunks = 16;
     cudaEvent_t ev_in[kMaxChunks] = {}, ev_comp[kMaxChunks] = {}, ev_start = nullptr, ev_done = nullptr;
+    bool host_started = false;   // a host-buffer call has been enqueued (ev_done is live)
     // Sharing: a plan's flags, own workspace and staging buffers are per-plan state, so calls
     // on one plan are serialised -- host side by `mu`, device side by chaining each call after
     // the previous call's completion event when it arrives on a different stream.
@@ -581,11 +582,17 @@ cl_status cl_conv_forward_nhwc(cl_plan* p, const float* d_x, float* d_y, void* d
     });
 }
 
-cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* stream) {
-    // Pipelined over batch chunks on three streams: H2D of chunk i+1 (copy-in stream), the
-    // convolution of chunk i (caller's stream) and the D2H of chunk i-1 (copy-out stream)
-    // overlap, so the call costs ~max(H2D, compute, D2H) instead of their sum (PCIe is full
-    // duplex).  Synchronous on return, like run_method.
+namespace {
+
+// Host-buffer forward, pipelined over batch chunks on three streams: H2D of chunk i+1
+// (copy-in stream), the convolution of chunk i (caller's stream) and the D2H of chunk i-1
+// (copy-out stream) overlap, so a call costs ~max(H2D, compute, D2H) instead of their sum
+// (PCIe is full duplex).  sync: wait for completion on return (like run_method), and let the
+// copy-in wait for prior work on the caller's stream (host buffers it may produce).  async:
+// return after enqueueing; the copy-in waits only for this plan's previous call (its staging
+// buffers), so calls on different plans (layers) overlap their transfers; the caller's
+// stream receives the completion.
+cl_status host_forward(cl_plan* p, const float* h_x, float* h_y, void* stream, bool sync) {
     return guarded([&] {
         require(p && h_x && h_y, "cl_conv_forward_host: null argument");
         CLB_CUDA(cudaSetDevice(p->device));
@@ -628,11 +635,17 @@ cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* s
         static cudaEvent_t tev[3 * cl_plan::kMaxChunks + 1] = {};
         if (htrace && !tev[0])
             for (auto& e : tev) CLB_CUDA(cudaEventCreate(&e));
-        // the copy streams must not run ahead of prior work on the caller's stream
-        CLB_CUDA(cudaEventRecord(p->ev_start, s));
+        if (sync) {
+            // the copy streams must not run ahead of prior work on the caller's stream
+            CLB_CUDA(cudaEventRecord(p->ev_start, s));
+            CLB_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+            CLB_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
+        } else if (p->host_started) {
+            // staging buffers of this plan: the previous call must have drained them
+            CLB_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_done, 0));
+        }
+        p->host_started = true;
         if (htrace) CLB_CUDA(cudaEventRecord(tev[0], s));
-        CLB_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
-        CLB_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
         // all copy-ins are enqueued first, so the H2D engine streams back to back and never
         // waits for the host to enqueue a chunk's kernels (that interleaving cost ~25% of the
         // duplex PCIe rate, measured with CLB_HOST_TRACE)
@@ -659,7 +672,7 @@ cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* s
         CLB_CUDA(cudaEventRecord(p->ev_done, p->s_out));
         CLB_CUDA(cudaStreamWaitEvent(s, p->ev_done, 0));   // the caller's stream sees the outputs
         mark_done(p, s);
-        CLB_CUDA(cudaStreamSynchronize(s));
+        if (sync || htrace) CLB_CUDA(cudaStreamSynchronize(s));
         if (htrace) {
             fprintf(stderr, "[clb-host] n=%d c=%d m=%d hw=%dx%d chunks=%d in %.1f MB out %.1f MB |", d.n, d.c, d.m, d.h,
                     d.w, chunks, xb / 1e6, yb / 1e6);
@@ -676,6 +689,16 @@ cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* s
                     yb / 56e6);
         }
     });
+}
+
+}  // namespace
+
+cl_status cl_conv_forward_host(cl_plan* p, const float* h_x, float* h_y, void* stream) {
+    return host_forward(p, h_x, h_y, stream, true);
+}
+
+cl_status cl_conv_forward_host_async(cl_plan* p, const float* h_x, float* h_y, void* stream) {
+    return host_forward(p, h_x, h_y, stream, false);
 }
 
 int cl_conv_last_launch_count(const cl_plan* p) { return p ? p->launches : 0; }

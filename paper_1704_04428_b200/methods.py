@@ -232,6 +232,13 @@ class ConvPlan:
         _lib.check(fn(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), ws, self._stream(stream)))
         return y
 
+    def forward_host_async(self, x_host, y_host, stream=None):
+        """Host-buffer call that returns after enqueueing (synchronise `stream` before reading
+        y_host); consecutive calls on different plans overlap their transfers."""
+        _lib.check(_lib.lib().cl_conv_forward_host_async(self._h, ctypes.c_void_p(x_host.data_ptr()),
+                                                         ctypes.c_void_p(y_host.data_ptr()), self._stream(stream)))
+        return y_host
+
     def forward_host(self, x_host, y_host, stream=None):
         """End-to-end host-buffer call (H2D + forward + D2H, synchronous)."""
         _lib.check(_lib.lib().cl_conv_forward_host(self._h, ctypes.c_void_p(x_host.data_ptr()),

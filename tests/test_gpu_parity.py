@@ -557,3 +557,34 @@ def test_nhwc_unsupported_methods_and_unaligned_output(oracle, clb, torch_cuda):
         torch.cuda.synchronize()
         got = y.cpu().numpy().transpose(0, 3, 1, 2)
     _check_fp32(oracle, np.ascontiguousarray(got), oracle.conv_batch(x, w), "unaligned nhwc output")
+
+
+def test_forward_host_async_overlapped_plans(oracle, clb, torch_cuda):
+    """cl_conv_forward_host_async: several plans enqueued back to back on one stream, then a
+    single synchronise -- every output equals the synchronous call's (bitwise) and the oracle;
+    repeated calls on one plan reuse its staging buffers safely."""
+    torch = torch_cuda
+    shapes = [(24, 2, 16, 13, 13, 32, 3), (20, 3, 8, 9, 11, 24, 5), (19, 1, 40, 7, 7, 130, 1)]
+    plans, hx, hy, hsync, refs = [], [], [], [], []
+    for seed, N, C, H, W, M, k in shapes:
+        x, w = oracle.make_problem(N, C, H, W, M, k, seed)
+        refs.append(oracle.conv_batch(x, w))
+        layer = clb.LayerConfig(f"a{seed}", C, H, W, M, k, batch=N)
+        plan = clb.ConvPlan(layer)
+        plan.set_weights(torch.from_numpy(w).cuda())
+        plans.append(plan)
+        hx.append(torch.from_numpy(x).pin_memory())
+        hy.append(torch.empty(plan.output_shape()).pin_memory())
+        hs = torch.empty(plan.output_shape()).pin_memory()
+        plan.forward_host(hx[-1], hs)
+        hsync.append(hs)
+    s = torch.cuda.Stream()
+    for rep in range(3):
+        for p, a, b in zip(plans, hx, hy):
+            p.forward_host_async(a, b, s)
+        s.synchronize()
+        for y, ys, ref in zip(hy, hsync, refs):
+            assert torch.equal(y, ys)
+            _check_fp32(oracle, y.numpy(), ref, "forward_host_async")
+    for p in plans:
+        p.close()
