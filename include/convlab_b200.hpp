@@ -98,8 +98,12 @@ public:
     void set_weights_device(const float* d_w_mkkc, void* stream = nullptr);
     void set_weights_host(const float* h_w_mkkc, void* stream = nullptr);
     void forward_device(const float* d_x, float* d_y, void* d_ws = nullptr, void* stream = nullptr);
+    // channels-last device tensors: x [N][H][W][C], y [N][P][Q][M] (implicit kn2row / conv1x1)
+    void forward_device_nhwc(const float* d_x, float* d_y, void* d_ws = nullptr, void* stream = nullptr);
     // host NCHW in / host NCHW out (H2D + forward + D2H)
     std::vector<float> forward_host(const float* h_x, void* stream = nullptr);
+    // same, into a caller buffer, returning after enqueueing (synchronise `stream` before use)
+    void forward_host_async(const float* h_x, float* h_y, void* stream);
 
 private:
     cl_plan* plan_ = nullptr;

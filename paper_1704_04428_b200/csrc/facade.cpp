@@ -202,6 +202,14 @@ CLB_EXPORT void Plan::forward_device(const float* d_x, float* d_y, void* d_ws, v
     check(cl_conv_forward(plan_, d_x, d_y, d_ws, stream));
 }
 
+CLB_EXPORT void Plan::forward_device_nhwc(const float* d_x, float* d_y, void* d_ws, void* stream) {
+    check(cl_conv_forward_nhwc(plan_, d_x, d_y, d_ws, stream));
+}
+
+CLB_EXPORT void Plan::forward_host_async(const float* h_x, float* h_y, void* stream) {
+    check(cl_conv_forward_host_async(plan_, h_x, h_y, stream));
+}
+
 CLB_EXPORT std::vector<float> Plan::forward_host(const float* h_x, void* stream) {
     std::vector<float> y(layer_.batch * layer_.kernel_count * out_h_ * out_w_);
     check(cl_conv_forward_host(plan_, h_x, y.data(), stream));

@@ -109,6 +109,23 @@ static void gpu_tests() {
         std::printf("  %-22s %-5s rel_l2=%.3e\n", std::string(to_string(c.m)).c_str(), l.name.c_str(), rel);
         CHECK(rel <= 1e-5);
     }
+    // Plan: asynchronous host call, completed by a following synchronous call on the same
+    // stream (calls on one plan run in order); both outputs must be bitwise equal
+    {
+        LayerConfig l{"async", 16, 13, 13, 32, 3, 1, -1, 2};
+        const size_t xn = l.batch * l.channels * l.height * l.width;
+        const size_t wn = l.kernel_count * l.kernel_size * l.kernel_size * l.channels;
+        std::vector<float> x(xn), w(wn);
+        orc_fill(x.data(), xn, orc_split(5, 0), 0);
+        orc_fill(w.data(), wn, orc_split(5, 1), 0);
+        Plan plan(l, ConvMethod::Kn2rowGpu);
+        plan.set_weights_host(w.data());
+        std::vector<float> ya(l.batch * l.kernel_count * plan.out_height() * plan.out_width(), -1.0f);
+        plan.forward_host_async(x.data(), ya.data(), nullptr);
+        const std::vector<float> ys = plan.forward_host(x.data());
+        CHECK(ya == ys);
+        std::printf("  Plan::forward_host_async == forward_host: %s\n", ya == ys ? "yes" : "NO");
+    }
 }
 
 int main(int argc, char** argv) {
