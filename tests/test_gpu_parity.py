@@ -588,3 +588,29 @@ def test_forward_host_async_overlapped_plans(oracle, clb, torch_cuda):
             _check_fp32(oracle, y.numpy(), ref, "forward_host_async")
     for p in plans:
         p.close()
+
+
+@pytest.mark.parametrize("layer_name,batch", [("vgg16/conv1_2", 8), ("vgg16/conv3_2", 32), ("alexnet/conv2", 128),
+                                              ("alexnet/conv3", 128), ("scale/56x56", 64)])
+def test_linearity_full_size(clb, torch_cuda, layer_name, batch):
+    """conv_direct_test.cpp:191-217 linearity/additivity, as a size-independent property at
+    the BASELINE shapes (the oracle is too slow there): conv(a x1 + x2) = a conv(x1) + conv(x2)
+    within fp32 rounding, through the tap-shared / im2col-TMA / stream-K paths these shapes take."""
+    torch = torch_cuda
+    from paper_1704_04428_b200 import rng, workloads
+    group = layer_name.split("/")[0]
+    layer = [l for l in workloads.workload(group, batch) if l.name == layer_name][0]
+    x1, w = rng.make_problem(layer.batch, layer.channels, layer.height, layer.width, layer.kernel_count,
+                             layer.kernel_size, seed=1)
+    x2, _ = rng.make_problem(layer.batch, layer.channels, layer.height, layer.width, layer.kernel_count,
+                             layer.kernel_size, seed=2)
+    a = 0.375
+    with clb.ConvPlan(layer) as plan:
+        plan.set_weights(w)
+        y1 = plan.forward(x1)
+        y2 = plan.forward(x2)
+        y12 = plan.forward(a * x1 + x2)
+        torch.cuda.synchronize()
+    lhs, rhs = y12.double(), a * y1.double() + y2.double()
+    rel = ((lhs - rhs).norm() / rhs.norm()).item()
+    assert rel <= 2e-6, (layer_name, rel)
