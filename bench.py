@@ -49,7 +49,9 @@ def parse_args():
     ap.add_argument("--workload", default="alexnet")
     ap.add_argument("--batch", type=int, default=None, help="override the per-GPU batch")
     ap.add_argument("--method", default="auto")
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "bf16"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "bf16"],
+                    help="fp32 = fp32-faithful (rel-L2 <= 1e-5; operand split per CLB_SPLIT: mixed "
+                         "(default) or 3xtf32); tf32 / bf16 = the 1e-2 fast modes")
     ap.add_argument("--layout", default="nchw", choices=["nchw", "nhwc"],
                     help="device tensors NCHW (the reference interface, default) or channels-last "
                          "(cl_conv_forward_nhwc; the e2e leg stays NCHW)")
@@ -65,14 +67,27 @@ def parse_args():
 NOMINAL_BF16 = 2250.0   # dense bf16 TFLOP/s, B200 nominal (B200_PROFILING.md, context only)
 
 
+def fp32_split():
+    """The fp32-faithful operand split the library uses (same switch as api.cu planes_for):
+    'mixed' = hi*Hi in two tf32 MMAs + the two cross terms in one bf16 K=16 MMA each (4
+    tf32-MMA slots per 16 K-elements); '3xtf32' = the classic split (6 slots)."""
+    return "3xtf32" if os.environ.get("CLB_SPLIT") == "3xtf32" else "mixed"
+
+
+def tensor_factor(precision):
+    """Effective-TFLOP/s per tf32 TFLOP/s of the tensor pipe for each precision mode."""
+    if precision == "fp32":
+        return 1.0 / 3.0 if fp32_split() == "3xtf32" else 0.5
+    return {"tf32": 1.0, "bf16": 2.0}[precision]
+
+
 def mma_peak_for(precision):
     """Our own kind::tf32 MMA peak (tools/mma_probe.cu, committed under profiles/), in the
-    precision's effective units: 3xTF32 = /3; bf16 (kind::f16) = x2."""
+    precision's effective units (tensor_factor)."""
     f = Path(__file__).resolve().parent / "profiles" / "tf32_mma_peak.json"
     if not f.exists():
         return None
-    tf32 = json.loads(f.read_text())["tf32_mma_peak_tflops"]
-    return {"fp32": tf32 / 3.0, "tf32": tf32, "bf16": 2.0 * tf32}[precision]
+    return json.loads(f.read_text())["tf32_mma_peak_tflops"] * tensor_factor(precision)
 
 
 def peaks():
@@ -359,8 +374,8 @@ def main():
     # ---- roofline of the dominant kernel (tc_conv_kernel: the tcgen05 contraction) ------
     kernel_ms_step = sum(kern_ms)
     tf32_peak = pk["bf16"] / 2.0
-    peak_3x = tf32_peak / 3.0
-    mode_peak = {"fp32": peak_3x, "tf32": tf32_peak, "bf16": pk["bf16"]}[args.precision]
+    mode_peak = tf32_peak * tensor_factor(args.precision)
+    nominal_peak = NOMINAL_BF16 / 2.0 * tensor_factor(args.precision)
     achieved = flops_step / (kernel_ms_step * 1e-3) / 1e12
     traffic = None
     try:
@@ -398,7 +413,9 @@ def main():
             "layout": args.layout,
             "global_batch": layers[0].batch * info.world, "method": args.method,
             "resolved_methods": sorted({p.method for p in plans}),
-            "precision": {"fp32": "fp32-faithful 3xTF32", "tf32": "tf32 (fast mode)",
+            "precision": {"fp32": ("fp32-faithful (rel-L2 <= 1e-5): hi*Hi tf32 x2 + cross terms bf16 x2"
+                                   if fp32_split() == "mixed" else "fp32-faithful 3xTF32"),
+                          "tf32": "tf32 (fast mode)",
                           "bf16": "bf16 operands, fp32 accumulate (fast mode)"}[args.precision],
             "parallelism": f"dp{info.world} (batch-sharded, no data-path collective)",
             "l2": "flushed (256 MiB write) before every timed step", "weights": "pre-packed once, untimed",
@@ -411,19 +428,24 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": mode_peak, "unit": "TFLOP/s",
                      "frac": achieved / mode_peak, "traffic": traffic,
-                     "kernel": "tc_conv_kernel (tcgen05 kind::tf32 x3, TMA im2col)",
+                     "kernel": {"fp32": ("tc_conv_kernel (tcgen05: hi*Hi kind::tf32 x2 + cross terms kind::f16 x2)"
+                                         if fp32_split() == "mixed" else "tc_conv_kernel (tcgen05 kind::tf32 x3)"),
+                                "tf32": "tc_conv_kernel (tcgen05 kind::tf32)",
+                                "bf16": "tc_conv_kernel (tcgen05 kind::f16, bf16)"}[args.precision],
                      "kernel_ms_per_step": kernel_ms_step,
-                     "peak_note": (f"3xTF32 peak = measured bf16 burst {pk['bf16']} / 2 (tf32 rate) / 3 (passes); "
+                     "peak_note": (f"peak = measured bf16 burst {pk['bf16']} / 2 (tf32 rate) x "
+                                   f"{tensor_factor(args.precision):.3g} (effective flops per tf32 MMA flop: "
+                                   "fp32 split 'mixed' 1/2, '3xtf32' 1/3; tf32 1; bf16 2); "
                                    f"{pk['source']}.  The bf16 figure is cuBLAS under its own power/clock "
-                                   "limits, so a tcgen05 kernel can exceed it; frac_of_nominal is against "
-                                   "the nominal dense 2250 TFLOP/s bf16 (same /2 /3)"),
+                                   "limits, so a tcgen05 kernel can exceed it; measured_mma_peak is our own "
+                                   "kind::tf32 ceiling (tools/mma_probe.cu), nominal_peak the dense 2250 TF "
+                                   "bf16 datasheet figure, both scaled the same way"),
+                     "fp32_split": fp32_split() if args.precision == "fp32" else None,
                      "measured_mma_peak": mma_peak_for(args.precision),
                      "frac_of_measured_mma_peak": (achieved / mma_peak_for(args.precision)
                                                    if mma_peak_for(args.precision) else None),
-                     "nominal_peak": NOMINAL_BF16 / 2.0 / (3.0 if args.precision == "fp32" else 1.0)
-                     * (1.0 if args.precision != "bf16" else 2.0),
-                     "frac_of_nominal": achieved / (NOMINAL_BF16 / 2.0 / (3.0 if args.precision == "fp32" else 1.0)
-                                                    * (1.0 if args.precision != "bf16" else 2.0))},
+                     "nominal_peak": nominal_peak,
+                     "frac_of_nominal": achieved / nominal_peak},
         "cpu_baseline": cpu,
         "clocks": clocks,
     }

@@ -21,6 +21,18 @@ thread_local std::string g_err;
 // K order) against the M x k^2 C weights, so they share one engine path.
 inline bool is_patch_method(cl_method m) { return m == CL_METHOD_IM2COL || m == CL_METHOD_IM2ROW; }
 
+// Operand format of a precision.  fp32-faithful: the mixed 2xTF32 + 2xBF16 split (4 MMA slots
+// per 16 channels) unless CLB_SPLIT=3xtf32 selects the classic 3xTF32 split (6 slots).
+int planes_for(cl_precision precision) {
+    static const bool classic = [] {
+        const char* e = std::getenv("CLB_SPLIT");
+        return e && std::strcmp(e, "3xtf32") == 0;
+    }();
+    if (precision == CL_PREC_BF16) return kPlanesBf16;
+    if (precision == CL_PREC_TF32) return 1;
+    return classic ? 2 : kPlanesMixed;
+}
+
 cl_status fail(cl_status s, const std::string& msg) {
     g_err = msg;
     return s;
@@ -460,7 +472,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         p->requested = method;
         p->method = m;
         p->prec = precision;
-        p->planes = precision == CL_PREC_FP32 ? 2 : (precision == CL_PREC_BF16 ? kPlanesBf16 : 1);
+        p->planes = planes_for(precision);
         p->device = device;
         p->Cp = round_up(d.c, k_granule(p->planes));
         p->Kp = round_up(d.k * d.k * d.c, k_granule(p->planes));
@@ -726,7 +738,7 @@ void cl_conv_destroy(cl_plan* p) {
 }
 
 size_t cl_gemm_workspace_bytes(int m, int n, int k, cl_precision precision) {
-    const int planes = precision == CL_PREC_FP32 ? 2 : (precision == CL_PREC_BF16 ? kPlanesBf16 : 1);
+    const int planes = planes_for(precision);
     const size_t kp = (size_t)round_up(k > 0 ? k : 1, k_granule(planes));
     return align256(((size_t)(m > 0 ? m : 0) + (size_t)(n > 0 ? n : 0)) * row_bytes(planes, kp)) + tc_scratch_bytes();
 }
@@ -741,7 +753,7 @@ cl_status cl_gemm_f32(int m, int n, int k, const float* a, const float* b, float
         CLB_CUDA(cudaGetDevice(&dev));
         check_device(dev);
         auto s = static_cast<cudaStream_t>(stream);
-        const int planes = precision == CL_PREC_FP32 ? 2 : (precision == CL_PREC_BF16 ? kPlanesBf16 : 1);
+        const int planes = planes_for(precision);
         const int kp = round_up(k, k_granule(planes));
         const size_t need = cl_gemm_workspace_bytes(m, n, k, precision);
         void* own = nullptr;

@@ -31,12 +31,18 @@ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 //   2 = fp32-faithful 3xTF32 (rows interleave [hi16|lo16] fp32 words per 16 channels)
 //   1 = TF32 fast mode (rows of hi fp32 words)
 //   3 = BF16 fast mode (rows of bf16 elements, kind::f16 MMA)
+//   4 = fp32-faithful "2xTF32 + 2xBF16": per 16 channels [hi 16 fp32 | hi 16 bf16 | lo 16 bf16]
+//       -- hi*Hi in two tf32 MMAs (exact products), the cross terms hi*Lo and lo*Hi in one
+//       bf16 MMA each (K = 16 per MMA: 4 MMA slots per 16 channels instead of 6)
 constexpr int kPlanesBf16 = 3;
+constexpr int kPlanesMixed = 4;
+// hi|lo split formats: one 128-byte row unit per 16 channels
+__host__ __device__ inline bool is_split(int planes) { return planes == 2 || planes == kPlanesMixed; }
 // channel padding granularity of the split layout (one 128-byte row unit)
-inline int k_granule(int planes) { return planes == 2 ? 16 : (planes == kPlanesBf16 ? 64 : 32); }
+inline int k_granule(int planes) { return is_split(planes) ? 16 : (planes == kPlanesBf16 ? 64 : 32); }
 inline int elem_bytes(int planes) { return planes == kPlanesBf16 ? 2 : 4; }
-// elements per operand row of k_pad channels
-inline long long row_elems(int planes, long long kp) { return planes == 2 ? 2 * kp : kp; }
+// elements (4-byte words for the split formats) per operand row of k_pad channels
+inline long long row_elems(int planes, long long kp) { return is_split(planes) ? 2 * kp : kp; }
 inline long long row_bytes(int planes, long long kp) { return row_elems(planes, kp) * elem_bytes(planes); }
 
 // ---- pre-pass / post-pass kernels (prepass.cu) -------------------------------------------

@@ -19,6 +19,11 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // Row layout (see internal.hpp): 3xTF32 rows interleave hi|lo per 16-channel block so each
 // 128-byte TMA row carries both halves of 16 channels; TF32 rows hold hi only.
 // `base` = first element of the row (fp32 words, or bf16 elements for the BF16 mode).
+__device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
+    __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&t);
+}
+
 __device__ __forceinline__ void store_split(void* dstv, long long base, int c, int kp, int planes, float v) {
     (void)kp;
     if (planes == kPlanesBf16) {
@@ -31,12 +36,19 @@ __device__ __forceinline__ void store_split(void* dstv, long long base, int c, i
         const int u = (c >> 4) << 5, w = c & 15;
         dst[base + u + w] = hi;
         dst[base + u + 16 + w] = v - hi;
+    } else if (planes == kPlanesMixed) {
+        // unit = [hi 16 fp32 | bf16(hi) 16 | bf16(lo) 16]
+        const int u = (c >> 4) << 5, w = c & 15;
+        dst[base + u + w] = hi;
+        __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(dst + base + u);
+        h[32 + w] = __float2bfloat16_rn(hi);
+        h[48 + w] = __float2bfloat16_rn(v - hi);
     } else {
         dst[base + c] = hi;
     }
 }
 
-__device__ __forceinline__ long long rowel(int planes, long long kp) { return planes == 2 ? 2 * kp : kp; }
+__device__ __forceinline__ long long rowel(int planes, long long kp) { return is_split(planes) ? 2 * kp : kp; }
 
 // ------------------------------------------------------------------ NCHW -> NHWC split ----
 // Tile = 32 channels x 128 pixels of one image, 256 threads.  Loads: warp w reads channel
@@ -90,9 +102,9 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
         for (int h = 0; h < 4; ++h) tile[lane + 32 * h][warp + 8 * r] = v[r][h];
     __syncthreads();
     const long long row_words = rowel(planes, Cp);
-    const int words = planes == 2 ? 64 : 32;            // output elements per pixel in this tile
+    const int words = is_split(planes) ? 64 : 32;       // output words per pixel in this tile
     const int nch = Cp - c0 < 32 ? Cp - c0 : 32;        // channels of this tile inside the padded row
-    const int out_words = planes == 2 ? 2 * nch : nch;
+    const int out_words = is_split(planes) ? 2 * nch : nch;
     if (planes == kPlanesBf16) {                        // bf16 rows: lane = channel
         __nv_bfloat16* xb = static_cast<__nv_bfloat16*>(xsv);
         for (int pp = warp; pp < kSplitPx; pp += 8) {
@@ -107,7 +119,7 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
     for (int pp = warp; pp < kSplitPx; pp += 8) {
         const long long gp = g0 + pp;
         if (gp >= NP) break;
-        float* dst = xs + gp * row_words + (long long)(planes == 2 ? 2 : 1) * c0;
+        float* dst = xs + gp * row_words + (long long)(is_split(planes) ? 2 : 1) * c0;
 #pragma unroll
         for (int o0 = 0; o0 < 64; o0 += 32) {
             const int o = o0 + lane;
@@ -118,6 +130,18 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
                 const float val = tile[pp][cc];
                 const float hi = tf32_rna(val);
                 dst[o] = (w < 16) ? hi : val - hi;
+            } else if (planes == kPlanesMixed) {
+                // word w of unit u: [0,16) hi fp32; [16,24) bf16(hi) pairs; [24,32) bf16(lo) pairs
+                const int u = o >> 5, w = o & 31;
+                if (w < 16) {
+                    dst[o] = tf32_rna(tile[pp][u * 16 + w]);
+                } else {
+                    const int cc = u * 16 + ((w & 7) << 1);
+                    const float a = tile[pp][cc], b = tile[pp][cc + 1];
+                    const float ha = tf32_rna(a), hb = tf32_rna(b);
+                    const uint32_t bits = w < 24 ? bf16x2_bits(ha, hb) : bf16x2_bits(a - ha, b - hb);
+                    reinterpret_cast<uint32_t*>(dst)[o] = bits;
+                }
             } else {
                 dst[o] = tf32_rna(tile[pp][o]);
             }
@@ -212,6 +236,12 @@ __global__ void __launch_bounds__(256) nhwc_split_kernel(const float* __restrict
         const int u = (c >> 4) << 5, w = c & 15;      // 128 B unit [hi 16 | lo 16]
         *reinterpret_cast<float4*>(dst + u + w) = make_float4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<float4*>(dst + u + 16 + w) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    } else if (planes == kPlanesMixed) {
+        const int u = (c >> 4) << 5, w = c & 15;      // [hi 16 fp32 | bf16(hi) 16 | bf16(lo) 16]
+        *reinterpret_cast<float4*>(dst + u + w) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        uint32_t* bw = reinterpret_cast<uint32_t*>(dst + u);
+        *reinterpret_cast<uint2*>(bw + 16 + (w >> 1)) = make_uint2(bf16x2_bits(hi[0], hi[1]), bf16x2_bits(hi[2], hi[3]));
+        *reinterpret_cast<uint2*>(bw + 24 + (w >> 1)) = make_uint2(bf16x2_bits(lo[0], lo[1]), bf16x2_bits(lo[2], lo[3]));
     } else {
         *reinterpret_cast<float4*>(dst + c) = make_float4(hi[0], hi[1], hi[2], hi[3]);
     }

@@ -106,7 +106,7 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     // fp32-faithful (8 stages); the 1e-2 fast modes only chunk for stream-K granularity, and
     // 16 stages keep the epilogue's fold rate below the MMA's (4 stages had the MMA waiting on
     // TMEM 11-25 % of the time, CLB_TRACE)
-    if (p.chunk_iters <= 0) p.chunk_iters = p.planes == 2 ? kChunkIters : 2 * kChunkIters;
+    if (p.chunk_iters <= 0) p.chunk_iters = is_split(p.planes) ? kChunkIters : 2 * kChunkIters;
     if (p.tps > 1) p.chunk_iters = p.chunk_iters / p.tps > 0 ? p.chunk_iters / p.tps : 1;   // a stage holds tps taps
     if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
     const int tile_m = kTileM * cg;

@@ -420,6 +420,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         if (leader) {
             const uint32_t idesc = planes == 3 ? idesc_bf16((uint32_t)tile_m, (uint32_t)bn)
                                                : idesc_tf32((uint32_t)tile_m, (uint32_t)bn);
+            const uint32_t idesc16 = idesc_bf16((uint32_t)tile_m, (uint32_t)bn);   // mixed mode corrections
             int stage = 0;
             uint32_t phase = 0;
             uint32_t lg = 0;
@@ -432,6 +433,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             auto mma16 = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {   // kind::f16 (bf16)
                 if constexpr (CG == 2) mma_bf16_ss_2sm(d, a, b, idesc, acc);
                 else mma_bf16_ss(d, a, b, idesc, acc);
+            };
+            auto mma16x = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {   // bf16 corrections (mode 4)
+                if constexpr (CG == 2) mma_bf16_ss_2sm(d, a, b, idesc16, acc);
+                else mma_bf16_ss(d, a, b, idesc16, acc);
             };
             auto commit = [&](uint64_t* bar) {
                 if constexpr (CG == 2) mma_commit_2sm_mc(bar, (uint16_t)0x3);
@@ -486,6 +491,14 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                                 mma(d_tmem, da, db, 1u);
                                 mma(d_tmem, da + 6, db + 2, 1u);
                                 mma(d_tmem, da + 2, db + 6, 1u);
+                                mma(d_tmem, da + 2, db + 2, 1u);
+                            } else if (planes == 4) {
+                                // row = [hi 16 fp32 | bf16(hi) 16 | bf16(lo) 16]: the cross terms
+                                // lo*Hi and hi*Lo as one bf16 K=16 MMA each (bytes 96 / 64 of A
+                                // with 64 / 96 of B), then hi*Hi as two exact tf32 K=8 MMAs
+                                mma16x(d_tmem, da + 6, db + 4, first);
+                                mma16x(d_tmem, da + 4, db + 6, 1u);
+                                mma(d_tmem, da, db, 1u);
                                 mma(d_tmem, da + 2, db + 2, 1u);
                             } else if (planes == 3) {
                                 // 64 bf16 per row: 4 k-steps of 16 elements (32 B = 2 desc units)

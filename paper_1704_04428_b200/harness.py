@@ -25,7 +25,9 @@ from .methods import ConvPlan, LayerConfig, footprint
 CSV_HEADER = ("layer,method,runs,mean_s,min_s,stddev_s,input_bytes,kernel_bytes,intermediate_bytes,"
               "output_bytes")
 GPU_COLUMNS = "batch,pad,precision,gpus,eff_tflops,pct_peak"
-PEAK_3XTF32_TFLOPS = 1667.0 / 2 / 3    # MEASURED_PEAKS.json bf16 burst / 2 / 3
+# fp32-faithful peak: MEASURED_PEAKS.json bf16 burst / 2 (tf32) x 1/2 (mixed split, 4 MMA slots per
+# 16 K-elements; the classic CLB_SPLIT=3xtf32 split would be x 1/3)
+PEAK_3XTF32_TFLOPS = 1667.0 / 2 / 2
 
 
 @dataclass

@@ -158,15 +158,24 @@ def test_im2col_stride(oracle, clb, torch_cuda):
 
 
 def test_delta_kernels_reproduce_input(oracle, clb, torch_cuda):
-    """conv_kn2_test.cpp:148-152: centre-tap identity kernels give the input back (exact:
-    hi+lo of each value is exact and the other taps contribute exact zeros)."""
+    """conv_kn2_test.cpp:148-152: centre-tap identity kernels give the input back.  Exact for
+    the fp32 FMA direct kernel and the classic 3xTF32 split (hi + lo of each value is exact, the
+    other taps contribute exact zeros); the default fp32-faithful split carries the lo*Hi term in
+    bf16, so there each value comes back within 2^-19 of itself (bf16 rounding of lo, which is
+    itself <= 2^-11 of the value) -- asserted elementwise with margin at 2^-18."""
+    import os
     x, _ = oracle.make_problem(2, 3, 5, 5, 3, 3, 137)
     w = np.zeros((3, 3, 3, 3), np.float32)
     for m in range(3):
         w[m, 1, 1, m] = 1.0
+    classic = os.environ.get("CLB_SPLIT") == "3xtf32"
     for method in METHODS:
         y = _run(clb, torch_cuda, method, x, w)
-        assert np.array_equal(y, x), method
+        if method == "direct-gpu" or classic:
+            assert np.array_equal(y, x), method
+        else:
+            err = np.abs(y.astype(np.float64) - x) / np.maximum(np.abs(x), 1e-30)
+            assert err.max() <= 2.0 ** -18, (method, err.max())
 
 
 def test_k1_routing_and_conv1x1(oracle, clb, torch_cuda):
@@ -217,8 +226,8 @@ def test_explicit_intermediate_decomposes_per_tap(oracle, clb, torch_cuda):
         blk = inter[t * M:(t + 1) * M]
         # the two contractions put operands in swapped MMA roles, so equality is to rounding
         assert np.abs(blk - one[0].reshape(M, H * W)).max() <= 1e-6 * max(1.0, np.abs(blk).max()), t
-        assert np.array_equal(blk, oracle.gemm_ref(r, x[0].reshape(C, H * W))[t * M:(t + 1) * M]) or \
-            np.allclose(blk, oracle.gemm_ref(r, x[0].reshape(C, H * W))[t * M:(t + 1) * M], rtol=1e-6, atol=1e-6)
+        # against the reference GEMM (CPU fp32): the north-star fp32-faithful law
+        _check_fp32(oracle, blk, oracle.gemm_ref(r, x[0].reshape(C, H * W))[t * M:(t + 1) * M], f"tap {t}")
 
 
 def test_device_shift_add_known_answers(oracle, clb, torch_cuda):
