@@ -12,7 +12,7 @@
 
 using namespace clb;
 
-__global__ void probe(int n, int iters, int stages_per_commit, unsigned long long* cyc, unsigned long long* ns) {
+__global__ void probe(int m, int n, int iters, int stages_per_commit, unsigned long long* cyc, unsigned long long* ns) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar;
@@ -33,7 +33,7 @@ __global__ void probe(int n, int iters, int stages_per_commit, unsigned long lon
     if (warp == 1) {
         const uint64_t da = umma_desc_kmajor(smem_u32(smem), 128);
         const uint64_t db = umma_desc_kmajor(smem_u32(smem + 128 * 128), 128);
-        const uint32_t idesc = idesc_tf32(128, (uint32_t)n);
+        const uint32_t idesc = idesc_tf32((uint32_t)m, (uint32_t)n);
         uint32_t ph = 0;
         const long long t0 = clock64();
         const unsigned long long g0 = globaltimer_ns();
@@ -65,6 +65,7 @@ __global__ void probe(int n, int iters, int stages_per_commit, unsigned long lon
 
 int main(int argc, char** argv) {
     const int only_n = argc > 1 ? atoi(argv[1]) : 0;
+    const int m_rows = argc > 2 ? atoi(argv[2]) : 128;   // MMA M (64 or 128)
     unsigned long long *cyc, *ns;
     cudaMalloc(&cyc, 148 * 8);
     cudaMalloc(&ns, 148 * 8);
@@ -74,7 +75,7 @@ int main(int argc, char** argv) {
         for (int n : {64, 128, 192, 256}) {
             if (only_n && n != only_n) continue;
             const int iters = 2000;
-            probe<<<148, 128, 64 * 1024>>>(n, iters, spc, cyc, ns);
+            probe<<<148, 128, 64 * 1024>>>(m_rows, n, iters, spc, cyc, ns);
             cudaError_t e = cudaDeviceSynchronize();
             std::vector<unsigned long long> h(148), hn(148);
             cudaMemcpy(h.data(), cyc, 148 * 8, cudaMemcpyDeviceToHost);
@@ -86,13 +87,14 @@ int main(int argc, char** argv) {
             }
             avg /= 148;
             const double per_mma = avg / (iters * 6.0 * spc);
+            const double ideal = (double)n * m_rows / 256.0;   // M=128: N/2 cycles
             const double mhz = avg / max_ns * 1e3;
             // whole-GPU kind::tf32 rate: 148 CTAs x (2 * 128 * N * 8) flops per MMA
-            const double tf = 148.0 * iters * 6.0 * spc * 2.0 * 128 * n * 8 / (max_ns * 1e-9) / 1e12;
+            const double tf = 148.0 * iters * 6.0 * spc * 2.0 * m_rows * n * 8 / (max_ns * 1e-9) / 1e12;
             if (tf > best_tf) best_tf = tf, best_mhz = mhz;
-            printf("N=%3d stages/commit=%2d: %s  %.1f cycles/MMA (ideal %d) -> %.0f%% of the tensor-core rate; "
-                   "%.0f TFLOP/s tf32 at %.0f MHz\n", n, spc, cudaGetErrorString(e), per_mma, n / 2,
-                   100.0 * (n / 2) / per_mma, tf, mhz);
+            printf("M=%3d N=%3d stages/commit=%2d: %s  %.1f cycles/MMA (ideal %.0f) -> %.0f%% of the tensor-core rate; "
+                   "%.0f TFLOP/s tf32 at %.0f MHz\n", m_rows, n, spc, cudaGetErrorString(e), per_mma, ideal,
+                   100.0 * ideal / per_mma, tf, mhz);
         }
     }
     printf("{\"tf32_mma_peak_tflops\": %.1f, \"sm_mhz\": %.0f, \"fp32_3xtf32_peak_tflops\": %.1f, "
