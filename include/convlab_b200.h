@@ -74,7 +74,7 @@ typedef enum cl_method {
 } cl_method;
 
 typedef enum cl_precision {
-    CL_PREC_FP32 = 0,  /* fp32-faithful 3xTF32 (rel-L2 <= 1e-5 vs the fp32 oracle)   */
+    CL_PREC_FP32 = 0,  /* fp32-faithful split products (rel-L2 <= 1e-5 vs the fp32 oracle): hi*Hi tf32 + cross terms bf16; CLB_SPLIT=3xtf32: classic 3xTF32 */
     CL_PREC_TF32 = 1,  /* single TF32 pass (fast mode, 1e-2 tolerance)              */
     CL_PREC_BF16 = 2   /* BF16 operands, fp32 accumulate (fast mode, 1e-2 tolerance) */
 } cl_precision;

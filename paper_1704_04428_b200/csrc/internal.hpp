@@ -46,8 +46,9 @@ inline long long row_elems(int planes, long long kp) { return is_split(planes) ?
 inline long long row_bytes(int planes, long long kp) { return row_elems(planes, kp) * elem_bytes(planes); }
 
 // ---- pre-pass / post-pass kernels (prepass.cu) -------------------------------------------
-// Split layout of every operand row (k_pad channels): 3xTF32 -> per 16-channel block
-// [hi 16 | lo 16] (row = 2*k_pad words); TF32 -> hi only (row = k_pad words, k_pad % 32 == 0).
+// Split layout of every operand row (k_pad channels): per 16-channel block one 128 B unit
+// ([hi 16 fp32 | bf16 hi 16 | bf16 lo 16] mixed, [hi 16 | lo 16] 3xTF32; row = 2*k_pad words);
+// TF32 -> hi only (row = k_pad words, k_pad % 32 == 0); BF16 -> bf16 (k_pad % 64 == 0).
 // x NCHW fp32 -> xs[n][h][w][row] (hi = rna_tf32(x), lo = x - hi; zero for c >= C)
 void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s);
@@ -89,7 +90,7 @@ struct Operand {
     const void* ptr = nullptr;
     long long rows = 0;      // tiled: rows of the map
     int taps = 1;            // tiled: 3rd dim
-    int kw = 0;              // elements per row: 2*Cp (3xTF32 hi|lo interleave) or Cp (TF32, BF16)
+    int kw = 0;              // elements per row: 2*Cp (split formats) or Cp (TF32, BF16)
     int planes = 2;          // precision mode (see k_granule)
     // im2col only
     int n = 0, h = 0, w = 0, k = 1, pad = 0;

@@ -16,7 +16,8 @@ __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float(r);
 }
 
-// Row layout (see internal.hpp): 3xTF32 rows interleave hi|lo per 16-channel block so each
+// Row layout (see internal.hpp): the fp32-faithful split formats pack one 128 B unit per
+// 16-channel block ([hi fp32 | bf16 hi | bf16 lo] mixed, [hi | lo] fp32 for 3xTF32) so each
 // 128-byte TMA row carries both halves of 16 channels; TF32 rows hold hi only.
 // `base` = first element of the row (fp32 words, or bf16 elements for the BF16 mode).
 __device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
@@ -54,7 +55,7 @@ __device__ __forceinline__ long long rowel(int planes, long long kp) { return is
 // Tile = 32 channels x 128 pixels of one image, 256 threads.  Loads: warp w reads channel
 // rows w, w+8, w+16, w+24 in four 128-byte pieces each -- 16 independent loads in flight per
 // thread (the kernel is HBM-bound; memory-level parallelism is what it needs).  Stores: per
-// pixel the tile's output is one contiguous run of 64 words ([hi16|lo16] x 2 for 3xTF32, 32
+// pixel the tile's output is one contiguous run of 64 words (two 16-channel units for the split formats, 32
 // hi words for TF32), written by a warp as full 128-byte lines (lane = word).
 // grid (ceil(HW/128), ceil(Cp/32), N)
 constexpr int kSplitPx = 128;

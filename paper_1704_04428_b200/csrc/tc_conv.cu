@@ -50,7 +50,7 @@ int num_sms() {
 
 void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int box_taps) {
     resolve_driver();
-    const cuuint64_t kdim = (cuuint64_t)op.kw;   // elements per row (hi|lo interleaved for 3xTF32)
+    const cuuint64_t kdim = (cuuint64_t)op.kw;   // elements per row (2 words per channel for the split formats)
     const cuuint64_t eb = (cuuint64_t)elem_bytes(op.planes);
     const CUtensorMapDataType dt = op.planes == kPlanesBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -102,7 +102,7 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     const int k_iters = (p.taps / p.tps) * p.kblocks;
     // 128 K-elements per accumulation chunk for the fp32-faithful mode; coarser for the fast
     // modes, whose input rounding dominates the accumulator's
-    // chunk = K slice per TMEM accumulator: 3xTF32 needs <= 128 K-elements per chunk to stay
+    // chunk = K slice per TMEM accumulator: the fp32-faithful splits need <= 128 K-elements per chunk to stay
     // fp32-faithful (8 stages); the 1e-2 fast modes only chunk for stream-K granularity, and
     // 16 stages keep the epilogue's fold rate below the MMA's (4 stages had the MMA waiting on
     // TMEM 11-25 % of the time, CLB_TRACE)

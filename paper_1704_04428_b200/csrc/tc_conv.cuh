@@ -4,7 +4,8 @@
 //
 // A supplies the 128 D rows of an MMA tile (UMMA M = 128), B the BN columns (UMMA N = BN,
 // a runtime multiple of 16 <= 256).  Both operands are K-major fp32 words holding TF32
-// values, split hi/lo for the fp32-faithful 3xTF32 mode (D += Alo.Bhi + Ahi.Blo + Ahi.Bhi).
+// values, split hi/lo for the fp32-faithful modes (D += Alo.Bhi + Ahi.Blo + Ahi.Bhi; default:
+// Ahi.Bhi in tf32, the two cross terms in bf16 -- see internal.hpp planes 4).
 // Each operand is fetched by TMA either as a plain 3-D tile (k, row, tap) or -- the
 // implicit kn2row path -- as a 4-D im2col box over the NHWC input whose per-tap offsets
 // (j, i) shift the 128 output pixels onto their input taps; taps falling outside the image
@@ -42,9 +43,10 @@ enum : int { EPI_NCHW = 0, EPI_ROWMAJOR = 1, EPI_NCHW_PADDED = 2, EPI_NHWC_PADDE
 
 constexpr int kTileM = 128;          // UMMA M (D rows per tile)
 // Operand rows are 128-byte units (SWIZZLE_128B, one TMA box per operand per stage):
-//   3xTF32: 16 channels as [hi 0..15 | lo 0..15]   (kBlockK = 16 channels per stage)
+//   split formats: 16 channels per 128 B unit   (kBlockK = 16 channels per stage)
+//     mixed (4): [hi 0..15 fp32 | bf16 hi 0..15 | bf16 lo 0..15];  3xTF32 (2): [hi 0..15 | lo 0..15]
 //   TF32  : 32 channels of hi                      (32 channels per stage)
-constexpr int kBlockK = 16;          // channel granularity of the 3xTF32 interleave
+constexpr int kBlockK = 16;          // channel granularity of the split formats
 constexpr int kRowWords = 32;
 constexpr int kRowBytes = kRowWords * 4;
 constexpr int kThreads = 384;             // 4 control warps + 8 epilogue warps
@@ -59,7 +61,7 @@ struct TcParams {
     int n_col_tiles, num_tiles;
     int taps, tap_begin, ksize;  // K loop: taps [tap_begin, tap_begin+taps), tap t -> (t/ksize, t%ksize)
     int kblocks;               // 16-channel blocks per tap
-    int planes;                // 2 = 3xTF32 (hi|lo interleaved per 16 channels), 1 = TF32 (hi), 3 = BF16
+    int planes;                // 4 = mixed split (default fp32), 2 = 3xTF32, 1 = TF32 (hi), 3 = BF16
     int row_elems;             // elements per 128-byte row unit (32 fp32 or 64 bf16)
     int stages;
     int chunk_iters;           // k-iterations per TMEM accumulation chunk
@@ -414,7 +416,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // into the next of 2-4 TMEM buffers (round robin) that the epilogue folds into fp32 registers.
         // Tensor-core accumulation rounds every update of the running fp32 accumulator
         // (error grows ~linearly in K: 7e-9 K measured), so bounding the chunk to 128
-        // K-elements keeps the 3xTF32 result fp32-faithful for any K.
+        // K-elements keeps the split-product result fp32-faithful for any K.
         // The whole warp runs the loop (loop state is warp-uniform, so it lives in uniform
         // registers); one elected lane issues the MMAs and the commits that track them.
         if (leader) {
