@@ -285,3 +285,27 @@ def test_cli_usage_and_device_errors(tmp_path):
     if not torch.cuda.is_available():
         r = _cli("verify", "--net", str(net))
         assert r.returncode == 1 and "no CPU fallback" in r.stderr          # fails loudly, no fallback
+
+
+def test_bench_reference_arm_json_contract():
+    """bench.py --impl reference (CPU only, so it runs here): one JSON line with the driver's
+    keys, the reference arm's own cpu_baseline and an e2e block with zero transfer bytes."""
+    import json
+    import subprocess
+    import sys
+    from oracle import oracle as O
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    root = str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1",
+                        "--workload", "c1"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["cores"] >= 1
