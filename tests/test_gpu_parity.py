@@ -623,3 +623,38 @@ def test_linearity_full_size(clb, torch_cuda, layer_name, batch):
     lhs, rhs = y12.double(), a * y1.double() + y2.double()
     rel = ((lhs - rhs).norm() / rhs.norm()).item()
     assert rel <= 2e-6, (layer_name, rel)
+
+
+@pytest.mark.parametrize("shape", [(4, 64, 28, 28, 256, 3), (2, 16, 13, 13, 32, 3), (1, 256, 28, 28, 256, 5)])
+def test_cuda_graph_capture_and_replay(oracle, clb, torch_cuda, shape):
+    """forward() captured into a CUDA graph (PDL edges, self-resetting stream-K flags, the
+    plan's cross-stream ordering switched off under capture) and replayed with new inputs
+    written into the captured buffer: every replay matches the oracle, and the plan still
+    works eagerly afterwards on another stream."""
+    torch = torch_cuda
+    N, C, H, W, M, k = shape
+    layer = clb.LayerConfig("graph", C, H, W, M, k, batch=N)
+    x0, w = oracle.make_problem(N, C, H, W, M, k, 70)
+    with clb.ConvPlan(layer) as plan:
+        plan.set_weights(torch.from_numpy(w).cuda())
+        xd = torch.from_numpy(x0).cuda()
+        yd = torch.empty(plan.output_shape(), device="cuda")
+        ws = torch.empty(max(plan.workspace_bytes(), 4), dtype=torch.uint8, device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            plan.forward(xd, yd, ws)                       # warm, same stream as the capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            plan.forward(xd, yd, ws)
+        torch.cuda.synchronize()
+        for seed in (71, 72, 73):
+            x, _ = oracle.make_problem(N, C, H, W, M, k, seed)
+            xd.copy_(torch.from_numpy(x))
+            g.replay()
+            torch.cuda.synchronize()
+            _check_fp32(oracle, yd.cpu().numpy(), oracle.conv_batch(x, w), f"graph replay {seed}")
+        y2 = plan.forward(xd, stream=torch.cuda.Stream())  # eager again, different stream
+        torch.cuda.synchronize()
+        _check_fp32(oracle, y2.cpu().numpy(), oracle.conv_batch(x, w), "eager after graph")
