@@ -62,10 +62,18 @@ constexpr int kSplitPx = 128;
 
 // Output pixel space: HW = Hp*Wp pixels per image; with pad > 0 this is the zero-padded
 // image (Hp = H + 2 pad, Wp = W + 2 pad) the tap-shared (padded-row) kernel mode reads.
+// Templated on the operand format so every element is converted exactly once (in the load
+// phase, into shared tiles) and the write phase is plain 32-bit copies: converting per output
+// word made the mixed format's prepass issue-bound (IPC 3.2, DRAM 21 %, ncu on GoogLeNet 1x1).
+template <int PLANES>
 __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xsv,
-                                                                 int N, int C, int HW, int Cp, int planes, int H,
-                                                                 int W, int Wp, int pad) {
-    __shared__ float tile[kSplitPx][33];   // [pixel][channel]
+                                                                 int N, int C, int HW, int Cp, int H, int W, int Wp,
+                                                                 int pad) {
+    constexpr bool kSplit = PLANES == 2 || PLANES == kPlanesMixed;
+    __shared__ float tile[kSplitPx][33];                                   // hi (or raw for bf16 rows)
+    __shared__ float tile_lo[PLANES == 2 ? kSplitPx : 1][33];              // 3xTF32 lo
+    __shared__ uint32_t tile_bh[PLANES == kPlanesMixed ? kSplitPx : 1][17];  // mixed: bf16(hi) pairs
+    __shared__ uint32_t tile_bl[PLANES == kPlanesMixed ? kSplitPx : 1][17];  // mixed: bf16(lo) pairs
     // pixels are flattened over (image, pixel): a tile may straddle two images, so small maps
     // (13 x 13 = 169 pixels) do not leave most of a second 128-pixel tile idle
     const long long NP = (long long)N * HW;
@@ -98,15 +106,28 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
         for (int h = 0; h < 4; ++h) v[r][h] = (c < C && src[h] >= 0) ? __ldg(x + src[h] + (long long)c * plane) : 0.0f;
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < 4; ++r) {
+        const int cc = warp + 8 * r;                   // channel within the tile
 #pragma unroll
-        for (int h = 0; h < 4; ++h) tile[lane + 32 * h][warp + 8 * r] = v[r][h];
+        for (int h = 0; h < 4; ++h) {
+            const int px = lane + 32 * h;
+            if (PLANES == kPlanesBf16) {
+                tile[px][cc] = v[r][h];
+            } else {
+                const float hi = tf32_rna(v[r][h]);
+                tile[px][cc] = hi;
+                if (PLANES == 2) tile_lo[px][cc] = v[r][h] - hi;
+                if (PLANES == kPlanesMixed) {
+                    reinterpret_cast<__nv_bfloat16*>(&tile_bh[px][0])[cc] = __float2bfloat16_rn(hi);
+                    reinterpret_cast<__nv_bfloat16*>(&tile_bl[px][0])[cc] = __float2bfloat16_rn(v[r][h] - hi);
+                }
+            }
+        }
+    }
     __syncthreads();
-    const long long row_words = rowel(planes, Cp);
-    const int words = is_split(planes) ? 64 : 32;       // output words per pixel in this tile
+    const long long row_words = rowel(PLANES, Cp);
     const int nch = Cp - c0 < 32 ? Cp - c0 : 32;        // channels of this tile inside the padded row
-    const int out_words = is_split(planes) ? 2 * nch : nch;
-    if (planes == kPlanesBf16) {                        // bf16 rows: lane = channel
+    if (PLANES == kPlanesBf16) {                        // bf16 rows: lane = channel
         __nv_bfloat16* xb = static_cast<__nv_bfloat16*>(xsv);
         for (int pp = warp; pp < kSplitPx; pp += 8) {
             const long long gp = g0 + pp;
@@ -116,36 +137,28 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         return;
     }
-    float* xs = static_cast<float*>(xsv);
+    const int out_words = kSplit ? 2 * nch : nch;
+    uint32_t* xs = static_cast<uint32_t*>(xsv);
     for (int pp = warp; pp < kSplitPx; pp += 8) {
         const long long gp = g0 + pp;
         if (gp >= NP) break;
-        float* dst = xs + gp * row_words + (long long)(is_split(planes) ? 2 : 1) * c0;
+        uint32_t* dst = xs + gp * row_words + (long long)(kSplit ? 2 : 1) * c0;
 #pragma unroll
-        for (int o0 = 0; o0 < 64; o0 += 32) {
+        for (int o0 = 0; o0 < (kSplit ? 64 : 32); o0 += 32) {
             const int o = o0 + lane;
-            if (o0 >= words || o >= out_words) continue;
-            if (planes == 2) {
-                const int u = o >> 5, w = o & 31;            // 16-channel block u of this tile
-                const int cc = u * 16 + (w & 15);
-                const float val = tile[pp][cc];
-                const float hi = tf32_rna(val);
-                dst[o] = (w < 16) ? hi : val - hi;
-            } else if (planes == kPlanesMixed) {
-                // word w of unit u: [0,16) hi fp32; [16,24) bf16(hi) pairs; [24,32) bf16(lo) pairs
+            if (o >= out_words) continue;
+            uint32_t word;
+            if (PLANES == 2) {                           // unit u = [hi 16 | lo 16]
                 const int u = o >> 5, w = o & 31;
-                if (w < 16) {
-                    dst[o] = tf32_rna(tile[pp][u * 16 + w]);
-                } else {
-                    const int cc = u * 16 + ((w & 7) << 1);
-                    const float a = tile[pp][cc], b = tile[pp][cc + 1];
-                    const float ha = tf32_rna(a), hb = tf32_rna(b);
-                    const uint32_t bits = w < 24 ? bf16x2_bits(ha, hb) : bf16x2_bits(a - ha, b - hb);
-                    reinterpret_cast<uint32_t*>(dst)[o] = bits;
-                }
+                word = __float_as_uint(w < 16 ? tile[pp][u * 16 + w] : tile_lo[pp][u * 16 + w - 16]);
+            } else if (PLANES == kPlanesMixed) {         // unit u = [hi 16 fp32 | bf16 hi 16 | bf16 lo 16]
+                const int u = o >> 5, w = o & 31;
+                word = w < 16 ? __float_as_uint(tile[pp][u * 16 + w])
+                              : (w < 24 ? tile_bh[pp][u * 8 + (w - 16)] : tile_bl[pp][u * 8 + (w - 24)]);
             } else {
-                dst[o] = tf32_rna(tile[pp][o]);
+                word = __float_as_uint(tile[pp][o]);
             }
+            dst[o] = word;
         }
     }
     // let a programmatically dependent consumer (the tcgen05 kernel) start its prologue;
@@ -153,10 +166,20 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+template <typename... Args>
+static void launch_split_kernel(int planes, dim3 grid, cudaStream_t s, Args... args) {
+    switch (planes) {
+        case 1: nchw_to_nhwc_split_kernel<1><<<grid, 256, 0, s>>>(args...); break;
+        case 2: nchw_to_nhwc_split_kernel<2><<<grid, 256, 0, s>>>(args...); break;
+        case kPlanesBf16: nchw_to_nhwc_split_kernel<kPlanesBf16><<<grid, 256, 0, s>>>(args...); break;
+        default: nchw_to_nhwc_split_kernel<kPlanesMixed><<<grid, 256, 0, s>>>(args...);
+    }
+}
+
 void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s) {
     dim3 grid((unsigned)(((long long)N * HW + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
-    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, N, C, HW, Cp, planes, 1, HW, HW, 0);
+    launch_split_kernel(planes, grid, s, x, xs, N, C, HW, Cp, 1, HW, HW, 0);
     CLB_CUDA(cudaGetLastError());
 }
 
@@ -164,7 +187,7 @@ void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, 
                                  cudaStream_t s) {
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;
     dim3 grid((unsigned)(((long long)N * Hp * Wp + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
-    nchw_to_nhwc_split_kernel<<<grid, 256, 0, s>>>(x, xs, N, C, Hp * Wp, Cp, planes, H, W, Wp, pad);
+    launch_split_kernel(planes, grid, s, x, xs, N, C, Hp * Wp, Cp, H, W, Wp, pad);
     CLB_CUDA(cudaGetLastError());
 }
 
