@@ -139,27 +139,28 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
     }
     const int out_words = kSplit ? 2 * nch : nch;
     uint32_t* xs = static_cast<uint32_t*>(xsv);
-    for (int pp = warp; pp < kSplitPx; pp += 8) {
+    // write phase: every lane stores 4 consecutive words of one pixel row (16 B), so a warp
+    // instruction covers 2 pixel rows (split formats, 64 words each) or 4 (TF32, 32 words)
+    constexpr int kLanesPx = (kSplit ? 64 : 32) / 4;
+    constexpr int kPxPerIter = 32 / kLanesPx;
+    const int sub = lane / kLanesPx, o = (lane % kLanesPx) * 4;
+    for (int pp0 = warp * kPxPerIter; pp0 < kSplitPx; pp0 += 8 * kPxPerIter) {
+        const int pp = pp0 + sub;
         const long long gp = g0 + pp;
-        if (gp >= NP) break;
-        uint32_t* dst = xs + gp * row_words + (long long)(kSplit ? 2 : 1) * c0;
-#pragma unroll
-        for (int o0 = 0; o0 < (kSplit ? 64 : 32); o0 += 32) {
-            const int o = o0 + lane;
-            if (o >= out_words) continue;
-            uint32_t word;
-            if (PLANES == 2) {                           // unit u = [hi 16 | lo 16]
-                const int u = o >> 5, w = o & 31;
-                word = __float_as_uint(w < 16 ? tile[pp][u * 16 + w] : tile_lo[pp][u * 16 + w - 16]);
-            } else if (PLANES == kPlanesMixed) {         // unit u = [hi 16 fp32 | bf16 hi 16 | bf16 lo 16]
-                const int u = o >> 5, w = o & 31;
-                word = w < 16 ? __float_as_uint(tile[pp][u * 16 + w])
-                              : (w < 24 ? tile_bh[pp][u * 8 + (w - 16)] : tile_bl[pp][u * 8 + (w - 24)]);
-            } else {
-                word = __float_as_uint(tile[pp][o]);
-            }
-            dst[o] = word;
+        if (gp >= NP || o >= out_words) continue;
+        uint32_t* dst = xs + gp * row_words + (long long)(kSplit ? 2 : 1) * c0 + o;
+        const int u = o >> 5, w = o & 31;
+        const uint32_t* srow;
+        if (PLANES == 2) {                               // unit u = [hi 16 | lo 16]
+            srow = w < 16 ? reinterpret_cast<const uint32_t*>(&tile[pp][u * 16 + w])
+                          : reinterpret_cast<const uint32_t*>(&tile_lo[pp][u * 16 + w - 16]);
+        } else if (PLANES == kPlanesMixed) {             // unit u = [hi 16 fp32 | bf16 hi 16 | bf16 lo 16]
+            srow = w < 16 ? reinterpret_cast<const uint32_t*>(&tile[pp][u * 16 + w])
+                          : (w < 24 ? &tile_bh[pp][u * 8 + (w - 16)] : &tile_bl[pp][u * 8 + (w - 24)]);
+        } else {
+            srow = reinterpret_cast<const uint32_t*>(&tile[pp][o]);
         }
+        *reinterpret_cast<uint4*>(dst) = make_uint4(srow[0], srow[1], srow[2], srow[3]);
     }
     // let a programmatically dependent consumer (the tcgen05 kernel) start its prologue;
     // its griddepcontrol.wait still waits for this grid's completion and memory flush
