@@ -62,13 +62,28 @@ constexpr int kSplitPx = 128;
 
 // Output pixel space: HW = Hp*Wp pixels per image; with pad > 0 this is the zero-padded
 // image (Hp = H + 2 pad, Wp = W + 2 pad) the tap-shared (padded-row) kernel mode reads.
+struct FastDiv {
+    uint32_t d, m, s;
+};
+
+static FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f{d, 0, 0};
+    while ((1ull << f.s) < d) ++f.s;
+    f.m = (uint32_t)((((1ull << 32) * ((1ull << f.s) - d)) / d) + 1);
+    return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+    return (__umulhi(n, f.m) + n) >> f.s;
+}
+
 // Templated on the operand format so every element is converted exactly once (in the load
 // phase, into shared tiles) and the write phase is plain 32-bit copies: converting per output
 // word made the mixed format's prepass issue-bound (IPC 3.2, DRAM 21 %, ncu on GoogLeNet 1x1).
 template <int PLANES>
 __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xsv,
                                                                  int N, int C, int HW, int Cp, int H, int W, int Wp,
-                                                                 int pad) {
+                                                                 int pad, FastDiv hwd, FastDiv wpd) {
     constexpr bool kSplit = PLANES == 2 || PLANES == kPlanesMixed;
     __shared__ float tile[kSplitPx][33];                                   // hi (or raw for bf16 rows)
     __shared__ float tile_lo[PLANES == 2 ? kSplitPx : 1][33];              // 3xTF32 lo
@@ -87,39 +102,48 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
         const long long gp = g0 + lane + 32 * h;
         src[h] = -1;
         if (gp < NP) {
-            const int n = NP <= 0x7fffffffLL ? (int)((unsigned)gp / (unsigned)HW) : (int)(gp / HW);
+            // multiply-shift divisions (host-computed magics); 64-bit divide only past 2^31 pixels
+            const int n = NP <= 0x7fffffffLL ? (int)fdiv((uint32_t)gp, hwd) : (int)(gp / HW);
             const int pix = (int)(gp - (long long)n * HW);
             int sp = pix;
             if (pad != 0) {
-                const int yy = pix / Wp, xx = pix - (pix / Wp) * Wp;
+                const int yy = (int)fdiv((uint32_t)pix, wpd), xx = pix - yy * Wp;
                 const int sy = yy - pad, sx = xx - pad;
                 sp = (sy >= 0 && sy < H && sx >= 0 && sx < W) ? sy * W + sx : -1;
             }
             if (sp >= 0) src[h] = (long long)n * C * plane + sp;
         }
     }
+    // thread (warp, lane) loads channels {2w, 2w+1, 2w+16, 2w+17} of pixels lane + 32 h: each
+    // warp load is 32 consecutive pixels of one channel plane (128 B), and the thread owns
+    // adjacent channel pairs, so the mixed format's bf16 halves go to smem as one 32-bit word
     float v[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        const int c = c0 + warp + 8 * r;
+        const int c = c0 + 2 * warp + (r & 1) + 16 * (r >> 1);
 #pragma unroll
         for (int h = 0; h < 4; ++h) v[r][h] = (c < C && src[h] >= 0) ? __ldg(x + src[h] + (long long)c * plane) : 0.0f;
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int cc = warp + 8 * r;                   // channel within the tile
+    for (int r = 0; r < 4; r += 2) {
+        const int cc = 2 * warp + 16 * (r >> 1);      // even channel within the tile; pair (cc, cc+1)
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const int px = lane + 32 * h;
             if (PLANES == kPlanesBf16) {
                 tile[px][cc] = v[r][h];
+                tile[px][cc + 1] = v[r + 1][h];
             } else {
-                const float hi = tf32_rna(v[r][h]);
-                tile[px][cc] = hi;
-                if (PLANES == 2) tile_lo[px][cc] = v[r][h] - hi;
+                const float h0 = tf32_rna(v[r][h]), h1 = tf32_rna(v[r + 1][h]);
+                tile[px][cc] = h0;
+                tile[px][cc + 1] = h1;
+                if (PLANES == 2) {
+                    tile_lo[px][cc] = v[r][h] - h0;
+                    tile_lo[px][cc + 1] = v[r + 1][h] - h1;
+                }
                 if (PLANES == kPlanesMixed) {
-                    reinterpret_cast<__nv_bfloat16*>(&tile_bh[px][0])[cc] = __float2bfloat16_rn(hi);
-                    reinterpret_cast<__nv_bfloat16*>(&tile_bl[px][0])[cc] = __float2bfloat16_rn(v[r][h] - hi);
+                    tile_bh[px][cc >> 1] = bf16x2_bits(h0, h1);
+                    tile_bl[px][cc >> 1] = bf16x2_bits(v[r][h] - h0, v[r + 1][h] - h1);
                 }
             }
         }
@@ -180,7 +204,8 @@ static void launch_split_kernel(int planes, dim3 grid, cudaStream_t s, Args... a
 void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
                                cudaStream_t s) {
     dim3 grid((unsigned)(((long long)N * HW + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
-    launch_split_kernel(planes, grid, s, x, xs, N, C, HW, Cp, 1, HW, HW, 0);
+    launch_split_kernel(planes, grid, s, x, xs, N, C, HW, Cp, 1, HW, HW, 0, make_fastdiv((uint32_t)HW),
+                        make_fastdiv((uint32_t)HW));
     CLB_CUDA(cudaGetLastError());
 }
 
@@ -188,7 +213,8 @@ void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, 
                                  cudaStream_t s) {
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;
     dim3 grid((unsigned)(((long long)N * Hp * Wp + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
-    launch_split_kernel(planes, grid, s, x, xs, N, C, Hp * Wp, Cp, H, W, Wp, pad);
+    launch_split_kernel(planes, grid, s, x, xs, N, C, Hp * Wp, Cp, H, W, Wp, pad, make_fastdiv((uint32_t)(Hp * Wp)),
+                        make_fastdiv((uint32_t)Wp));
     CLB_CUDA(cudaGetLastError());
 }
 
@@ -199,21 +225,6 @@ void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, 
 // or (pad > 0) the zero-padded pixel grid of the tap-shared mode.  (row, quad) comes from a
 // multiply-shift divide (n < 2^31): a runtime 32/64-bit division per element costs more
 // issue slots than the bytes it moves.
-struct FastDiv {
-    uint32_t d, m, s;
-};
-
-static FastDiv make_fastdiv(uint32_t d) {
-    FastDiv f{d, 0, 0};
-    while ((1ull << f.s) < d) ++f.s;
-    f.m = (uint32_t)((((1ull << 32) * ((1ull << f.s) - d)) / d) + 1);
-    return f;
-}
-
-__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
-    return (__umulhi(n, f.m) + n) >> f.s;
-}
-
 __global__ void __launch_bounds__(256) nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xs,
                                                          uint32_t total, FastDiv q4d, FastDiv pixd, FastDiv wpd, int C,
                                                          int Cp, int planes, int H, int W, int pad) {
