@@ -96,18 +96,42 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     p.kblocks = a.kw / unit;
     p.a_mode = a.mode;
     p.b_mode = b.mode;
-    p.stages = tc_num_stages(p.bn / cg, p.tps);
-    if (p.stages < 2) throw Error(2, "tile too large for a 2-stage pipeline");
     if (p.taps % p.tps != 0) throw Error(6, "taps per stage must divide the tap count");
     const int k_iters = (p.taps / p.tps) * p.kblocks;
-    // 128 K-elements per accumulation chunk for the fp32-faithful mode; coarser for the fast
-    // modes, whose input rounding dominates the accumulator's
-    // chunk = K slice per TMEM accumulator: the fp32-faithful splits need <= 128 K-elements per chunk to stay
-    // fp32-faithful (8 stages); the 1e-2 fast modes only chunk for stream-K granularity, and
-    // 16 stages keep the epilogue's fold rate below the MMA's (4 stages had the MMA waiting on
-    // TMEM 11-25 % of the time, CLB_TRACE)
-    if (p.chunk_iters <= 0) p.chunk_iters = is_split(p.planes) ? kChunkIters : 2 * kChunkIters;
-    if (p.tps > 1) p.chunk_iters = p.chunk_iters / p.tps > 0 ? p.chunk_iters / p.tps : 1;   // a stage holds tps taps
+    const int b_rows = p.bn / cg;
+    // chunk = K slice per TMEM accumulator.  The fp32-faithful splits bound it to kChunkK
+    // K-elements (16 channels x tps taps per k-iteration): tensor-core accumulation error grows
+    // ~linearly with the chunk (rel-L2 8.3e-7 / 1.07e-6 / 1.33e-6 at 128 / 192 / 256, bound 1e-5;
+    // profiles/r01_chunk_accuracy.txt), while short chunks cost the small-N tap-shared layers
+    // 7-9 % (VGG conv1_2-2_2 at 96 vs 192 K).  The 1e-2 fast modes only chunk for stream-K
+    // granularity: 16 iterations keep the epilogue's fold rate below the MMA's (4 had the MMA
+    // waiting on TMEM 11-25 % of the time, CLB_TRACE).
+    if (p.chunk_iters <= 0) {
+        if (is_split(p.planes)) {
+            p.chunk_iters = kChunkK / (16 * p.tps);
+        } else {
+            p.chunk_iters = kFastChunkIters / p.tps;
+        }
+        if (p.chunk_iters < 1) p.chunk_iters = 1;
+        static const int env_chunk = getenv("CLB_CHUNK") ? atoi(getenv("CLB_CHUNK")) : 0;   // experiment knob
+        if (env_chunk > 0) p.chunk_iters = env_chunk;
+    }
+    if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
+    // Stage grouping: bps k-iterations share one full/empty barrier round trip.  Two per stage
+    // are 2-5 % faster on every layer that still keeps >= 3 stages in flight; with only 2
+    // stages left the pipeline runs dry (VGG conv5_x, conv2_1: 3-7 % slower), so stay at 1.
+    if (p.bps <= 0) {
+        static const int env_bps = getenv("CLB_BPS") ? atoi(getenv("CLB_BPS")) : 0;   // experiment knob
+        if (env_bps > 0) p.bps = env_bps;
+        else p.bps = (tc_num_stages(b_rows, p.tps, 2) >= 3 && (p.chunk_iters % 2 == 0 || p.chunk_iters == k_iters)) ? 2 : 1;
+    }
+    p.stages = tc_num_stages(b_rows, p.tps, p.bps);
+    while (p.stages < 2 && p.bps > 1) p.stages = tc_num_stages(b_rows, p.tps, --p.bps);
+    if (p.stages < 2) throw Error(2, "tile too large for a 2-stage pipeline");
+    // chunk boundaries must be stage boundaries: chunk_iters a multiple of bps (a single-chunk
+    // tile is exempt -- its only chunk starts the piece and ends at k_iters)
+    if (p.chunk_iters < k_iters && p.chunk_iters % p.bps != 0)
+        p.chunk_iters = p.chunk_iters >= p.bps ? p.chunk_iters / p.bps * p.bps : p.bps;
     if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
     const int tile_m = kTileM * cg;
     const int row_tiles = (p.rows + tile_m - 1) / tile_m;
@@ -116,7 +140,7 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     if (p.num_tiles <= 0) return;
     p.chunks_per_tile = (k_iters + p.chunk_iters - 1) / p.chunk_iters;
     const long long total_chunks = (long long)p.num_tiles * p.chunks_per_tile;
-    const int smem = tc_smem_bytes(p.bn / cg, p.tps, p.stages);
+    const int smem = tc_smem_bytes(b_rows, p.tps, p.stages, p.bps);
     static bool configured[3] = {false, false, false};
     if (!configured[cg]) {
         if (cg == 2) {
@@ -237,10 +261,10 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
             t_out = std::max(t_out, h[(size_t)b * kTraceSlots + 10]);
         }
         fprintf(stderr,
-                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stages=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
+                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
                 "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
                 "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us\n",
-                p.rows, p.cols, p.bn, cg, p.tps, p.stages, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
+                p.rows, p.cols, p.bn, cg, p.tps, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
                 avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5], 100 * avg[11] / avg[5], avg[8], (t_out - t_in) * 1e-3,
                 (t_in_max - t_in) * 1e-3, ev_ms * 1e3);
         if (const char* dump = getenv("CLB_TRACE_DUMP")) {   // raw per-CTA records, appended

@@ -52,7 +52,8 @@ constexpr int kRowBytes = kRowWords * 4;
 constexpr int kThreads = 384;             // 4 control warps + 8 epilogue warps
 constexpr int kEpiThreads = 256;
 constexpr int kSmemBudget = 200 * 1024;
-constexpr int kChunkIters = 8;      // 8 x 16 = 128 K-elements per TMEM accumulation chunk
+constexpr int kChunkK = 192;          // fp32-faithful splits: K-elements per TMEM accumulation chunk
+constexpr int kFastChunkIters = 16;   // TF32 / BF16 fast modes: k-iterations per chunk
 
 struct TcParams {
     // problem
@@ -76,6 +77,8 @@ struct TcParams {
     // channel block; A is ONE TMA box of 128 + tps - 1 rows of the zero-padded NHWC input and
     // tap j reads it through a descriptor shifted by j rows; tap rows step by a_row_shift (Wp).
     int tps;                   // taps per stage (1 = one tap per stage)
+    int bps;                   // k-iterations ("sub-stages") per pipeline stage: one barrier
+                               // round trip per bps TMA box pairs (chunk_iters % bps == 0)
     int a_row_shift;           // A row offset per tap group (padded row width Wp)
     int epi_hp, epi_wp, epi_n; // EPI_NCHW_PADDED geometry
     int accumulate;            // out += D (accumulating shifted-GEMM variant)
@@ -105,13 +108,13 @@ __host__ __device__ inline int tc_a_box_rows(int tps) { return kTileM + tps - 1;
 __host__ __device__ inline int tc_a_bytes(int tps) { return (tc_a_box_rows(tps) * kRowBytes + 1023) & ~1023; }
 __host__ __device__ inline int tc_stage_bytes(int b_rows, int tps) { return tc_a_bytes(tps) + tps * b_rows * kRowBytes; }
 
-__host__ inline int tc_num_stages(int b_rows, int tps) {
-    int s = (kSmemBudget - 1024) / tc_stage_bytes(b_rows, tps);
+__host__ inline int tc_num_stages(int b_rows, int tps, int bps = 1) {
+    int s = (kSmemBudget - 1024) / (bps * tc_stage_bytes(b_rows, tps));
     return s > 8 ? 8 : s;
 }
 
-__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages) {
-    return 1024 /*align slack*/ + stages * tc_stage_bytes(b_rows, tps) + 256 /*barriers*/;
+__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages, int bps = 1) {
+    return 1024 /*align slack*/ + stages * bps * tc_stage_bytes(b_rows, tps) + 256 /*barriers*/;
 }
 
 // TMEM accumulator buffers: 4 when they fit (BN <= 128), else ping-pong.  Extra buffers let
@@ -270,14 +273,16 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int tps = p.tps;
     const int a_bytes = tc_a_bytes(tps);          // A region of one stage (128 + tps - 1 rows)
     const int b_bytes = tps * b_rows * kRowBytes; // B rows of one stage (tps taps)
-    const int stage_bytes = a_bytes + b_bytes;
+    const int stage_bytes = a_bytes + b_bytes;    // one sub-stage (one k-iteration)
+    const int bps = p.bps;
+    const int group_bytes = bps * stage_bytes;    // one pipeline stage
     const uint32_t stage_tx = (uint32_t)((tc_a_box_rows(tps) + tps * b_rows) * kRowBytes);
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;       // scheduling unit
     const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * group_bytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + stages;
     uint64_t* tfull = bars + 2 * stages;        // [nbuf]
@@ -355,21 +360,22 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 int kb = it0 - (it0 / p.kblocks) * p.kblocks;
                 int tap = grp * tps;
                 int ti = tap / p.ksize, tj = tap - (tap / p.ksize) * p.ksize;
+                int sub = 0;
                 for (int it = it0; it < it1; ++it) {
                     const int kc = kb * p.row_elems;
                     const int arow = ca.c1 + grp * p.a_row_shift;   // padded-row mode: tap row i -> +i Wp
-                    if (TRACE) {
-                        const long long t0 = clock64();
+                    if (sub == 0) {
+                        const long long t0 = TRACE ? clock64() : 0;
                         mbar_wait(&empty[stage], phase ^ 1u);
-                        w_empty += clock64() - t0;
-                    } else {
-                        mbar_wait(&empty[stage], phase ^ 1u);
+                        if (TRACE) w_empty += clock64() - t0;
                     }
-                    uint8_t* a_st = smem + stage * stage_bytes;
+                    // a stage holds min(bps, iterations left in the piece) sub-stages
+                    const uint32_t txs = tx * (uint32_t)(it1 - it < bps ? it1 - it : bps);
+                    uint8_t* a_st = smem + stage * group_bytes + sub * stage_bytes;
                     if (elect_one()) {
                     if constexpr (CG == 2) {
                         const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
-                        if (leader) mbar_arrive_expect_tx(&full[stage], tx);
+                        if (leader && sub == 0) mbar_arrive_expect_tx(&full[stage], txs);
                         if (ca.mode == LOAD_IM2COL)
                             tma_load_im2col_4d_2sm(&map_a, lbar, a_st, kc, ca.c1, ca.c2, ca.c3, (uint16_t)tj, (uint16_t)ti);
                         else
@@ -380,7 +386,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         else
                             tma_load_3d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.tap3 ? tap : 0);
                     } else {
-                        mbar_arrive_expect_tx(&full[stage], tx);
+                        if (sub == 0) mbar_arrive_expect_tx(&full[stage], txs);
                         if (ca.mode == LOAD_IM2COL)
                             load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
                         else
@@ -389,9 +395,12 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     }
                     }
                     __syncwarp();
-                    if (++stage == stages) {
-                        stage = 0;
-                        phase ^= 1u;
+                    if (++sub == bps || it + 1 == it1) {
+                        sub = 0;
+                        if (++stage == stages) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
                     }
                     if (++kb == p.kblocks) {
                         kb = 0;
@@ -415,8 +424,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // The K loop of a tile is cut into chunks of ci k-iterations; each chunk accumulates
         // into the next of 2-4 TMEM buffers (round robin) that the epilogue folds into fp32 registers.
         // Tensor-core accumulation rounds every update of the running fp32 accumulator
-        // (error grows ~linearly in K: 7e-9 K measured), so bounding the chunk to 128
-        // K-elements keeps the split-product result fp32-faithful for any K.
+        // (error grows ~linearly in the chunk length), so bounding the chunk to kChunkK = 192
+        // K-elements keeps the split-product result fp32-faithful for any K (saturates at
+        // rel-L2 ~1.1e-6 against the 1e-5 bound).
         // The whole warp runs the loop (loop state is warp-uniform, so it lives in uniform
         // registers); one elected lane issues the MMAs and the commits that track them.
         if (leader) {
@@ -448,7 +458,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             // so stage / k-step / hi-lo offsets are plain adds on the 64-bit descriptor.  (Building
             // 4 descriptors per MMA made the single issuing thread slower than an N=192 MMA.)
             const uint64_t desc0 = umma_desc_kmajor(smem_u32(smem), kRowBytes);
-            const uint64_t st_step = (uint64_t)(stage_bytes >> 4);
+            const uint64_t st_step = (uint64_t)(group_bytes >> 4);
+            const uint64_t sub_step = (uint64_t)(stage_bytes >> 4);
             const uint64_t b_off = (uint64_t)(a_bytes >> 4);
             long long w_full = 0, w_tempty = 0;
             const long long t_start = clock64();
@@ -467,16 +478,16 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 }
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + buf * buf_cols;
+                int sub = 0;   // chunk starts are stage starts (chunk_iters % bps == 0)
                 for (int it = c0; it < c1; ++it) {
-                    if (TRACE) {
-                        const long long t0 = clock64();
+                    if (sub == 0) {
+                        const long long t0 = TRACE ? clock64() : 0;
                         mbar_wait(&full[stage], phase);
-                        w_full += clock64() - t0;
-                    } else {
-                        mbar_wait(&full[stage], phase);
+                        if (TRACE) w_full += clock64() - t0;
+                        tc_fence_after();
                     }
-                    tc_fence_after();
-                    const uint64_t da0 = desc0 + (uint64_t)stage * st_step;
+                    const bool stage_done = sub + 1 == bps || it + 1 == c1;
+                    const uint64_t da0 = desc0 + (uint64_t)stage * st_step + (uint64_t)sub * sub_step;
                     const uint64_t db0 = da0 + b_off;
                     if (elect_one()) {
                         for (int t = 0; t < tps; ++t) {
@@ -515,12 +526,17 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                                 mma(d_tmem, da + 6, db + 6, 1u);
                             }
                         }
-                        commit(&empty[stage]);      // frees the smem stage(s) once these MMAs retire
+                        if (stage_done) commit(&empty[stage]);   // frees the smem stage once its MMAs retire
                     }
                     __syncwarp();
-                    if (++stage == stages) {
-                        stage = 0;
-                        phase ^= 1u;
+                    if (stage_done) {
+                        sub = 0;
+                        if (++stage == stages) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
+                    } else {
+                        ++sub;
                     }
                 }
                 if (elect_one()) commit(&tfull[buf]);   // chunk complete -> epilogue(s)

@@ -1,20 +1,8 @@
 #!/bin/bash
-# One iteration: full GPU parity suite, traces, per-layer report for VGG16 + AlexNet, bench.
-cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+# one iteration: GPU parity suite, per-layer kernel times, AlexNet + VGG16 bench (30 steps)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
-tail -2 gpurun_out/pytest_gpu.txt
-./tools/trace_layers.sh
-timeout 600 python tools/report.py --workloads vgg16,alexnet --no-cpu --reps 5 > gpurun_out/rep.txt 2>&1
-python tools/rep_table.py gpurun_out/rep.txt
-: <<'PY'
-import json
-for l in open("gpurun_out/rep.txt"):
-    l = l.strip()
-    if l.startswith("{"):
-        d = json.loads(l)
-        if "layer" in d and "kernel_ms" in d:
-            print(f'{d["layer"]:18s} {d["method"]:12s} {d["kernel_ms"]:8.3f} ms  {d["kernel_tflops"]:7.1f} TF  frac {d["frac_of_layer_roofline"]:.2f}')
-PY
-timeout 600 python bench.py --no-cpu-baseline --steps 30 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; cut -c1-300 gpurun_out/bench.json
-timeout 600 python bench.py --workload vgg16 --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/bench_vgg.json 2> gpurun_out/bench_vgg.err; cut -c1-300 gpurun_out/bench_vgg.json
+A=alexnet/conv2,alexnet/conv3,alexnet/conv4,alexnet/conv5
+V=vgg16/conv1_2,vgg16/conv2_1,vgg16/conv2_2,vgg16/conv3_1,vgg16/conv3_2,vgg16/conv3_3,vgg16/conv4_1,vgg16/conv4_2,vgg16/conv4_3,vgg16/conv5_1,vgg16/conv5_2,vgg16/conv5_3
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/iter_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/iter_pytest.txt
+timeout 300 python tools/knob_sweep.py $A,$V > gpurun_out/iter_layers.txt 2>&1
+{ timeout 300 python bench.py --steps 30 --warmup 5; timeout 300 python bench.py --steps 30 --warmup 5 --workload vgg16; } > gpurun_out/iter_bench.txt 2> gpurun_out/iter_bench.err
