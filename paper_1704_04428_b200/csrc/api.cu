@@ -147,7 +147,7 @@ size_t method_ws_bytes(const cl_plan* p) {
         case CL_METHOD_CONV1X1:
         case CL_METHOD_KN2ROW_ACC:
             if (p->padded_rows)
-                return (size_t)d.n * (d.h + 2 * d.pad) * (d.w + 2 * d.pad) * row_bytes(p->planes, p->Cp);
+                return (size_t)d.n * (d.h + d.pad) * (d.w + d.pad) * row_bytes(p->planes, p->Cp);
             return xs;
         case CL_METHOD_KN2ROW_EXPLICIT:
         case CL_METHOD_KN2COL:
@@ -276,12 +276,19 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             return (v >= 16 && v <= 256 && v % 16 == 0) ? v : 0;
         }();
         if (forced_bn && !p->padded_rows) t.bn = forced_bn;
-        const int cg = cta_group_for(t.rows, t.cols, t.bn);
+        int cg = cta_group_for(t.rows, t.cols, t.bn);
         // few tiles even at 128 rows: halve the tile N to create more of them (B operand rows
         // are tiny anyway at these sizes)
         if (!forced_bn && cg == 1 && t.bn >= 64 &&
             (long long)(t.rows + 127) / 128 * ((t.cols + t.bn - 1) / t.bn) < num_sms() / 2)
             t.bn = round_up(t.bn / 2, 16);
+        // a k-tap stage must fit twice: a sub-batch (host-buffer chunks) can drop a padded-row
+        // launch to a single CTA, which holds all of B -- take a pair, or halve the tile N
+        const int tps = t.tps > 0 ? t.tps : 1;
+        while (tc_num_stages(t.bn / cg, tps) < 2 && t.bn > 16) {
+            if (cg == 1 && t.rows >= 256 && t.bn % 32 == 0) cg = 2;
+            else t.bn = round_up(t.bn / 2, 16);
+        }
         launch_tc(a, b, t, s, cg);
         ++p->launches;
     };
@@ -297,7 +304,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             if (p->padded_rows) {
                 // tap-shared mode: zero-padded NHWC rows; each stage loads ONE A box of 128+k-1
                 // rows per kernel row i and feeds its k taps through row-shifted descriptors
-                const int Hp = d.h + 2 * d.pad, Wp = d.w + 2 * d.pad;
+                const int Hp = d.h + d.pad, Wp = d.w + d.pad;   // shared padding (tc_conv.cuh)
                 if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
                 else launch_nchw_to_padded_split(x, xs, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
                 ++p->launches;
@@ -308,8 +315,10 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 t.cols = d.m;
                 t.bn = p->bn;
                 t.b_tap3 = 1;
-                t.tps = d.k;
+                static const bool env_tps1 = getenv("CLB_TPS1") && atoi(getenv("CLB_TPS1")) != 0;   // experiment knob
+                t.tps = env_tps1 ? 1 : d.k;
                 t.a_row_shift = Wp;
+                t.a_row_base = -d.pad * Wp - d.pad;
                 t.epi = nhwc ? EPI_NHWC_PADDED : EPI_NCHW_PADDED;
                 t.ld = d.m;
                 t.epi_hp = Hp;
@@ -491,18 +500,26 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             // its k taps through row-shifted descriptors (k x fewer A TMA bytes per MMA).  Small-BN
             // tiles are bound by shared-memory operand traffic (tools/mma_probe.cu: N = 64 tops out
             // at 63% even with operands resident), so cutting the A writes pays there -- VGG
-            // conv1_2 1.06 -> 0.65 ms, conv2_x 0.71/0.77 -> 1.02/1.06 of peak -- as long as the
-            // padded positions (computed, then dropped) stay below ~1/3: GoogLeNet 28x28 / 14x14
-            // layers (15-31 % waste) gain 5-10 %, 65 % waste loses (profiles/r01_padded_waste_sweep.txt).
-            // CLB_PADDED_ROWS=0/1 forces it.
+            // conv1_2 1.06 -> 0.65 ms, conv2_x 0.71/0.77 -> 1.02/1.06 of peak.  The padded
+            // positions are computed, then dropped.  CLB_PADDED_ROWS=0/1 forces it.
             static const int forced_padded = [] {
                 const char* e = std::getenv("CLB_PADDED_ROWS");
                 return e ? std::atoi(e) : -1;
             }();
-            const double waste = (double)(d.h + 2 * d.pad) * (d.w + 2 * d.pad) / ((double)P * Q) - 1.0;
-            const bool fits = tc_num_stages(p->bn, d.k) >= 2;   // CG1 worst case
-            const bool eligible = m == CL_METHOD_KN2ROW && d.k >= 3 && d.k <= 7 && d.stride == 1 && fits;
-            p->padded_rows = eligible && (forced_padded == 1 || (forced_padded != 0 && p->bn <= 128 && waste <= 0.35));
+            const double waste = (double)(d.h + d.pad) * (d.w + d.pad) / ((double)P * Q) - 1.0;
+            // the CTA group the launch will pick for the padded geometry (a pair holds half of B)
+            const int pcg = cta_group_for((long long)d.n * (d.h + d.pad) * (d.w + d.pad), d.m, p->bn);
+            const bool fits = tc_num_stages(p->bn / pcg, d.k) >= 2;
+            // pad <= k - 1: the P x Q outputs fit the shared-padding grid (H + pad) x (W + pad)
+            const bool eligible = m == CL_METHOD_KN2ROW && d.k >= 3 && d.k <= 7 && d.stride == 1 && d.pad <= d.k - 1 && fits;
+            // With the shared-padding grid ((H + pad) x (W + pad): 16 % waste at 13x13, 7 % at 28x28)
+            // the tiled A boxes beat the TMA im2col loads (tools/tma_probe3.cu: im2col A + tiled B
+            // deliver 37 B/clk per SM, tiled A + B 59) almost everywhere: AlexNet conv3/4 -12/-14 %,
+            // VGG conv3_x/4_x -5..-9 %, GoogLeNet 7x7 layers -27 % even at 31-65 % waste.  It loses
+            // only where BN = 256 meets >= 15 % waste (AlexNet conv2 / conv5: +2-3 %)
+            // (profiles/r01_padded_shared_sweep.txt).
+            const double max_waste = p->bn <= 192 ? 0.70 : 0.10;
+            p->padded_rows = eligible && (forced_padded == 1 || (forced_padded != 0 && waste <= max_waste));
         }
         if (cudaMalloc(&p->flags, kMaxGrid * sizeof(unsigned)) != cudaSuccess ||
             cudaMemset(p->flags, 0, kMaxGrid * sizeof(unsigned)) != cudaSuccess) {

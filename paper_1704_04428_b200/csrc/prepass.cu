@@ -61,7 +61,8 @@ __device__ __forceinline__ long long rowel(int planes, long long kp) { return is
 constexpr int kSplitPx = 128;
 
 // Output pixel space: HW = Hp*Wp pixels per image; with pad > 0 this is the zero-padded
-// image (Hp = H + 2 pad, Wp = W + 2 pad) the tap-shared (padded-row) kernel mode reads.
+// grid (Hp = H + pad, Wp = W + pad, data at (y, x), zeros after each row and image) the
+// tap-shared (padded-row) kernel mode reads.
 struct FastDiv {
     uint32_t d, m, s;
 };
@@ -108,8 +109,7 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
             int sp = pix;
             if (pad != 0) {
                 const int yy = (int)fdiv((uint32_t)pix, wpd), xx = pix - yy * Wp;
-                const int sy = yy - pad, sx = xx - pad;
-                sp = (sy >= 0 && sy < H && sx >= 0 && sx < W) ? sy * W + sx : -1;
+                sp = (yy < H && xx < W) ? yy * W + xx : -1;
             }
             if (sp >= 0) src[h] = (long long)n * C * plane + sp;
         }
@@ -211,7 +211,7 @@ void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, i
 
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
                                  cudaStream_t s) {
-    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+    const int Hp = H + pad, Wp = W + pad;
     dim3 grid((unsigned)(((long long)N * Hp * Wp + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
     launch_split_kernel(planes, grid, s, x, xs, N, C, Hp * Wp, Cp, H, W, Wp, pad, make_fastdiv((uint32_t)(Hp * Wp)),
                         make_fastdiv((uint32_t)Wp));
@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(256) nhwc_split_kernel(const float* __restrict
         const uint32_t n = fdiv(r, pixd);
         const uint32_t rem = r - n * pixd.d;
         const uint32_t yp = fdiv(rem, wpd);
-        const int y = (int)yp - pad, xq = (int)(rem - yp * wpd.d) - pad;
-        src = (y >= 0 && y < H && xq >= 0 && xq < W) ? ((long long)n * H + y) * W + xq : -1;
+        const int y = (int)yp, xq = (int)(rem - yp * wpd.d);
+        src = (y < H && xq < W) ? ((long long)n * H + y) * W + xq : -1;
     }
     float v[4] = {0.f, 0.f, 0.f, 0.f};
     if (src >= 0) {
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(256) nhwc_split_kernel(const float* __restrict
 
 void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
                        cudaStream_t s) {
-    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+    const int Hp = H + pad, Wp = W + pad;   // pad > 0: shared-padding grid (see above)
     const long long rows = (long long)N * Hp * Wp;
     const int q4 = Cp / 4;
     const long long total = rows * q4;

@@ -120,13 +120,15 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     // Stage grouping: bps k-iterations share one full/empty barrier round trip.  Two per stage
     // are 2-5 % faster on every layer that still keeps >= 3 stages in flight; with only 2
     // stages left the pipeline runs dry (VGG conv5_x, conv2_1: 3-7 % slower), so stay at 1.
+    static const int env_smem = getenv("CLB_SMEM_KB") ? atoi(getenv("CLB_SMEM_KB")) * 1024 : 0;   // experiment knob
+    const int budget = env_smem > 0 ? env_smem : kSmemBudget;
     if (p.bps <= 0) {
         static const int env_bps = getenv("CLB_BPS") ? atoi(getenv("CLB_BPS")) : 0;   // experiment knob
         if (env_bps > 0) p.bps = env_bps;
-        else p.bps = (tc_num_stages(b_rows, p.tps, 2) >= 3 && (p.chunk_iters % 2 == 0 || p.chunk_iters == k_iters)) ? 2 : 1;
+        else p.bps = (tc_num_stages(b_rows, p.tps, 2, budget) >= 3 && (p.chunk_iters % 2 == 0 || p.chunk_iters == k_iters)) ? 2 : 1;
     }
-    p.stages = tc_num_stages(b_rows, p.tps, p.bps);
-    while (p.stages < 2 && p.bps > 1) p.stages = tc_num_stages(b_rows, p.tps, --p.bps);
+    p.stages = tc_num_stages(b_rows, p.tps, p.bps, budget);
+    while (p.stages < 2 && p.bps > 1) p.stages = tc_num_stages(b_rows, p.tps, --p.bps, budget);
     if (p.stages < 2) throw Error(2, "tile too large for a 2-stage pipeline");
     // chunk boundaries must be stage boundaries: chunk_iters a multiple of bps (a single-chunk
     // tile is exempt -- its only chunk starts the piece and ends at k_iters)
@@ -260,13 +262,20 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
             t_in_max = std::max(t_in_max, h[(size_t)b * kTraceSlots + 9]);
             t_out = std::max(t_out, h[(size_t)b * kTraceSlots + 10]);
         }
+        double cyc_sum = 0, ns_sum = 0;
+        for (int b = 0; b < grid; ++b) {
+            cyc_sum += (double)h[(size_t)b * kTraceSlots + 19];
+            ns_sum += (double)(h[(size_t)b * kTraceSlots + 10] - h[(size_t)b * kTraceSlots + 9]);
+        }
+        const double mhz = ns_sum > 0 ? 1e3 * cyc_sum / ns_sum : 0.0;
         fprintf(stderr,
                 "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
                 "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
-                "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us\n",
+                "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us | "
+                "SM clock %.0f MHz (CTA cycles / CTA ns)\n",
                 p.rows, p.cols, p.bn, cg, p.tps, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
                 avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5], 100 * avg[11] / avg[5], avg[8], (t_out - t_in) * 1e-3,
-                (t_in_max - t_in) * 1e-3, ev_ms * 1e3);
+                (t_in_max - t_in) * 1e-3, ev_ms * 1e3, mhz);
         if (const char* dump = getenv("CLB_TRACE_DUMP")) {   // raw per-CTA records, appended
             if (FILE* f = fopen(dump, "a")) {
                 fprintf(f, "# launch rows=%d cols=%d bn=%d cg=%d grid=%d tiles=%d dp=%d cpt=%d\n", p.rows, p.cols, p.bn, cg,

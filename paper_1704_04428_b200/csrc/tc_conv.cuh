@@ -32,6 +32,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda.h>
 
 #include "ptx.cuh"
@@ -76,10 +77,15 @@ struct TcParams {
     // tap-shared A (padded-row mode): one stage = `tps` taps (a row of the kernel) x one
     // channel block; A is ONE TMA box of 128 + tps - 1 rows of the zero-padded NHWC input and
     // tap j reads it through a descriptor shifted by j rows; tap rows step by a_row_shift (Wp).
+    // The padded grid is (H + pad) x (W + pad) per image, zeros AFTER each row and image: the
+    // trailing zeros of one row / image are the leading padding of the next (the first image's
+    // leading rows are TMA out-of-bounds zero fill), so output (y, x) sits at row y*Wp + x and
+    // tap (i, j) reads row y*Wp + x + (i - pad)*Wp + (j - pad).
     int tps;                   // taps per stage (1 = one tap per stage)
     int bps;                   // k-iterations ("sub-stages") per pipeline stage: one barrier
                                // round trip per bps TMA box pairs (chunk_iters % bps == 0)
     int a_row_shift;           // A row offset per tap group (padded row width Wp)
+    int a_row_base;            // padded-row mode: A row of output row 0 (-pad*Wp - pad; TMA zero-fills < 0)
     int epi_hp, epi_wp, epi_n; // EPI_NCHW_PADDED geometry
     int accumulate;            // out += D (accumulating shifted-GEMM variant)
     float* out;
@@ -108,8 +114,8 @@ __host__ __device__ inline int tc_a_box_rows(int tps) { return kTileM + tps - 1;
 __host__ __device__ inline int tc_a_bytes(int tps) { return (tc_a_box_rows(tps) * kRowBytes + 1023) & ~1023; }
 __host__ __device__ inline int tc_stage_bytes(int b_rows, int tps) { return tc_a_bytes(tps) + tps * b_rows * kRowBytes; }
 
-__host__ inline int tc_num_stages(int b_rows, int tps, int bps = 1) {
-    int s = (kSmemBudget - 1024) / (bps * tc_stage_bytes(b_rows, tps));
+__host__ inline int tc_num_stages(int b_rows, int tps, int bps = 1, int budget = kSmemBudget) {
+    int s = (budget - 1024 - 256) / (bps * tc_stage_bytes(b_rows, tps));
     return s > 8 ? 8 : s;
 }
 
@@ -363,7 +369,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 int sub = 0;
                 for (int it = it0; it < it1; ++it) {
                     const int kc = kb * p.row_elems;
-                    const int arow = ca.c1 + grp * p.a_row_shift;   // padded-row mode: tap row i -> +i Wp
+                    // padded-row mode: tap (i, j) -> +i Wp + j (j = 0 at a group start when tps = k)
+                    const int arow = p.a_row_shift ? ca.c1 + p.a_row_base + ti * p.a_row_shift + tj : ca.c1;
                     if (sub == 0) {
                         const long long t0 = TRACE ? clock64() : 0;
                         mbar_wait(&empty[stage], phase ^ 1u);
@@ -433,11 +440,6 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint32_t idesc = planes == 3 ? idesc_bf16((uint32_t)tile_m, (uint32_t)bn)
                                                : idesc_tf32((uint32_t)tile_m, (uint32_t)bn);
             const uint32_t idesc16 = idesc_bf16((uint32_t)tile_m, (uint32_t)bn);   // mixed mode corrections
-            int stage = 0;
-            uint32_t phase = 0;
-            uint32_t lg = 0;
-            Sched sch(p, unit, nunits);
-            Piece pc;
             auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
                 if constexpr (CG == 2) mma_tf32_ss_2sm(d, a, b, idesc, acc);
                 else mma_tf32_ss(d, a, b, idesc, acc);
@@ -461,86 +463,119 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint64_t st_step = (uint64_t)(group_bytes >> 4);
             const uint64_t sub_step = (uint64_t)(stage_bytes >> 4);
             const uint64_t b_off = (uint64_t)(a_bytes >> 4);
+            const uint64_t tap_b = (uint64_t)(b_rows * 8);
             long long w_full = 0, w_tempty = 0;
             const long long t_start = clock64();
-            while (sch.next(pc))
-            for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
-                const int c0 = c * ci;
-                const int c1 = c0 + ci < k_iters ? c0 + ci : k_iters;
-                const uint32_t buf = lg & (uint32_t)(nbuf - 1);
-                const uint32_t tph = (lg >> nb_shift) & 1u;
-                if (TRACE) {
-                    const long long t0 = clock64();
-                    mbar_wait(&tempty[buf], tph ^ 1u);
-                    w_tempty += clock64() - t0;
-                } else {
-                    mbar_wait(&tempty[buf], tph ^ 1u);
-                }
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + buf * buf_cols;
-                int sub = 0;   // chunk starts are stage starts (chunk_iters % bps == 0)
-                for (int it = c0; it < c1; ++it) {
-                    if (sub == 0) {
+            // The issue loop is specialised on the split format and on one tap per k-iteration
+            // (compile-time), and one elected block issues a whole stage: at N = 192 the MMAs of a
+            // k-iteration take ~384 tensor cycles, and a generic loop (format dispatch, tap loop,
+            // one elect + reconvergence per k-iteration: ~100 instructions) could not keep up.
+            auto run = [&](auto pl_c, auto t1_c) {
+                constexpr int PL = decltype(pl_c)::value;
+                constexpr bool T1 = decltype(t1_c)::value;
+                // one k-iteration: the taps of the group x the format's MMAs; acc0 = 0 only for the
+                // chunk's first k-iteration (its first MMA starts the accumulator)
+                auto issue = [&](uint32_t d_tmem, uint64_t da0, uint32_t acc0) {
+                    const int ntaps = T1 ? 1 : tps;
+                    for (int t = 0; t < ntaps; ++t) {
+                        // tap t of the group: A shifted by t rows (8 desc units of 16 B per
+                        // 128 B row), B = the t-th tap's weight tile
+                        const uint64_t da = da0 + (uint64_t)(t * 8);
+                        const uint64_t db = da0 + b_off + (uint64_t)t * tap_b;
+                        const uint32_t first = (acc0 | (uint32_t)t) ? 1u : 0u;
+                        if constexpr (PL == 2) {
+                            // row = [hi 16 | lo 16]: k-step s (8 tf32 = 32 B = 2 desc units) of
+                            // hi at +2 s, of lo at +4 + 2 s; small cross terms first
+                            mma(d_tmem, da + 4, db, first);
+                            mma(d_tmem, da, db + 4, 1u);
+                            mma(d_tmem, da, db, 1u);
+                            mma(d_tmem, da + 6, db + 2, 1u);
+                            mma(d_tmem, da + 2, db + 6, 1u);
+                            mma(d_tmem, da + 2, db + 2, 1u);
+                        } else if constexpr (PL == 4) {
+                            // row = [hi 16 fp32 | bf16(hi) 16 | bf16(lo) 16]: the cross terms
+                            // lo*Hi and hi*Lo as one bf16 K=16 MMA each (bytes 96 / 64 of A
+                            // with 64 / 96 of B), then hi*Hi as two exact tf32 K=8 MMAs
+                            mma16x(d_tmem, da + 6, db + 4, first);
+                            mma16x(d_tmem, da + 4, db + 6, 1u);
+                            mma(d_tmem, da, db, 1u);
+                            mma(d_tmem, da + 2, db + 2, 1u);
+                        } else if constexpr (PL == 3) {
+                            // 64 bf16 per row: 4 k-steps of 16 elements (32 B = 2 desc units)
+                            mma16(d_tmem, da, db, first);
+                            mma16(d_tmem, da + 2, db + 2, 1u);
+                            mma16(d_tmem, da + 4, db + 4, 1u);
+                            mma16(d_tmem, da + 6, db + 6, 1u);
+                        } else {
+                            mma(d_tmem, da, db, first);
+                            mma(d_tmem, da + 2, db + 2, 1u);
+                            mma(d_tmem, da + 4, db + 4, 1u);
+                            mma(d_tmem, da + 6, db + 6, 1u);
+                        }
+                    }
+                };
+                int stage = 0;
+                uint32_t phase = 0;
+                uint64_t dstage = desc0;   // descriptor of the current stage's first sub-stage
+                uint32_t lg = 0;
+                Sched sch(p, unit, nunits);
+                Piece pc;
+                while (sch.next(pc))
+                for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
+                    const int c0 = c * ci;
+                    const int c1 = c0 + ci < k_iters ? c0 + ci : k_iters;
+                    const uint32_t buf = lg & (uint32_t)(nbuf - 1);
+                    const uint32_t tph = (lg >> nb_shift) & 1u;
+                    if (TRACE) {
+                        const long long t0 = clock64();
+                        mbar_wait(&tempty[buf], tph ^ 1u);
+                        w_tempty += clock64() - t0;
+                    } else {
+                        mbar_wait(&tempty[buf], tph ^ 1u);
+                    }
+                    tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + buf * buf_cols;
+                    // stages of bps k-iterations (chunk starts are stage starts: ci % bps == 0)
+                    for (int it = c0; it < c1; it += bps) {
+                        const int nsub = c1 - it < bps ? c1 - it : bps;
                         const long long t0 = TRACE ? clock64() : 0;
                         mbar_wait(&full[stage], phase);
                         if (TRACE) w_full += clock64() - t0;
                         tc_fence_after();
-                    }
-                    const bool stage_done = sub + 1 == bps || it + 1 == c1;
-                    const uint64_t da0 = desc0 + (uint64_t)stage * st_step + (uint64_t)sub * sub_step;
-                    const uint64_t db0 = da0 + b_off;
-                    if (elect_one()) {
-                        for (int t = 0; t < tps; ++t) {
-                            // tap t of the group: A shifted by t rows (8 desc units of 16 B per
-                            // 128 B row), B = the t-th tap's weight tile
-                            const uint64_t da = da0 + (uint64_t)(t * 8);
-                            const uint64_t db = db0 + (uint64_t)(t * b_rows * 8);
-                            const uint32_t first = (it > c0 || t > 0) ? 1u : 0u;
-                            if (planes == 2) {
-                                // row = [hi 16 | lo 16]: k-step s (8 tf32 = 32 B = 2 desc units) of
-                                // hi at +2 s, of lo at +4 + 2 s; small cross terms first
-                                mma(d_tmem, da + 4, db, first);
-                                mma(d_tmem, da, db + 4, 1u);
-                                mma(d_tmem, da, db, 1u);
-                                mma(d_tmem, da + 6, db + 2, 1u);
-                                mma(d_tmem, da + 2, db + 6, 1u);
-                                mma(d_tmem, da + 2, db + 2, 1u);
-                            } else if (planes == 4) {
-                                // row = [hi 16 fp32 | bf16(hi) 16 | bf16(lo) 16]: the cross terms
-                                // lo*Hi and hi*Lo as one bf16 K=16 MMA each (bytes 96 / 64 of A
-                                // with 64 / 96 of B), then hi*Hi as two exact tf32 K=8 MMAs
-                                mma16x(d_tmem, da + 6, db + 4, first);
-                                mma16x(d_tmem, da + 4, db + 6, 1u);
-                                mma(d_tmem, da, db, 1u);
-                                mma(d_tmem, da + 2, db + 2, 1u);
-                            } else if (planes == 3) {
-                                // 64 bf16 per row: 4 k-steps of 16 elements (32 B = 2 desc units)
-                                mma16(d_tmem, da, db, first);
-                                mma16(d_tmem, da + 2, db + 2, 1u);
-                                mma16(d_tmem, da + 4, db + 4, 1u);
-                                mma16(d_tmem, da + 6, db + 6, 1u);
-                            } else {
-                                mma(d_tmem, da, db, first);
-                                mma(d_tmem, da + 2, db + 2, 1u);
-                                mma(d_tmem, da + 4, db + 4, 1u);
-                                mma(d_tmem, da + 6, db + 6, 1u);
-                            }
+                        if (elect_one()) {
+                            issue(d_tmem, dstage, it > c0 ? 1u : 0u);
+                            if (nsub > 1) issue(d_tmem, dstage + sub_step, 1u);
+#pragma unroll 1
+                            for (int sb = 2; sb < nsub; ++sb) issue(d_tmem, dstage + (uint64_t)sb * sub_step, 1u);
+                            commit(&empty[stage]);   // frees the smem stage once its MMAs retire
                         }
-                        if (stage_done) commit(&empty[stage]);   // frees the smem stage once its MMAs retire
-                    }
-                    __syncwarp();
-                    if (stage_done) {
-                        sub = 0;
+                        __syncwarp();
                         if (++stage == stages) {
                             stage = 0;
                             phase ^= 1u;
+                            dstage = desc0;
+                        } else {
+                            dstage += st_step;
                         }
-                    } else {
-                        ++sub;
                     }
+                    if (elect_one()) commit(&tfull[buf]);   // chunk complete -> epilogue(s)
+                    __syncwarp();
                 }
-                if (elect_one()) commit(&tfull[buf]);   // chunk complete -> epilogue(s)
-                __syncwarp();
+            };
+            using I1 = std::integral_constant<int, 1>;
+            using I2 = std::integral_constant<int, 2>;
+            using I3 = std::integral_constant<int, 3>;
+            using I4 = std::integral_constant<int, 4>;
+            using BT = std::true_type;
+            using BF = std::false_type;
+            if (planes == 4) {
+                if (tps == 1) run(I4{}, BT{}); else run(I4{}, BF{});
+            } else if (planes == 2) {
+                if (tps == 1) run(I2{}, BT{}); else run(I2{}, BF{});
+            } else if (planes == 3) {
+                if (tps == 1) run(I3{}, BT{}); else run(I3{}, BF{});
+            } else {
+                if (tps == 1) run(I1{}, BT{}); else run(I1{}, BF{});
             }
             if (TRACE && lane_id() == 0) {
                 p.trace[blockIdx.x * kTraceSlots + 2] = (unsigned long long)(clock64() - t_start);
@@ -728,7 +763,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         if constexpr (CG == 2) tmem_dealloc_2sm(tmem_base, ncols);
         else tmem_dealloc(tmem_base, ncols);
     }
-    if (TRACE && threadIdx.x == 0) p.trace[blockIdx.x * kTraceSlots + 10] = globaltimer_ns();
+    if (TRACE && threadIdx.x == 0) {
+        p.trace[blockIdx.x * kTraceSlots + 10] = globaltimer_ns();
+        p.trace[blockIdx.x * kTraceSlots + 19] = (unsigned long long)(clock64() - t_entry);   // SM cycles in the CTA
+    }
 }
 
 #endif  // CLB_DEFINE_TC_KERNEL

@@ -297,6 +297,25 @@ def test_forward_host_matches_device(oracle, clb, torch_cuda):
         _check_fp32(oracle, hy.numpy(), oracle.conv_batch(x, w), f"forward_host n={n}")
 
 
+def test_forward_host_chunks_of_wide_padded_layer(oracle, clb, torch_cuda):
+    """A BN = 256 layer in the padded-row mode (28x28, C = M = 256: the full batch takes CTA
+    pairs) through the host-buffer call, whose sub-batches are small enough for single-CTA
+    launches: a 3-tap stage of 256 B rows must still fit (pair or narrower tile), and the
+    result equals the device call's and the oracle's."""
+    torch = torch_cuda
+    n = 24
+    layer = clb.LayerConfig("wide", 256, 28, 28, 256, 3, batch=n)
+    x, w = oracle.make_problem(n, 256, 28, 28, 256, 3, 11)
+    with clb.ConvPlan(layer, "auto") as plan:
+        plan.set_weights(torch.from_numpy(w).cuda())
+        yd = plan.forward(torch.from_numpy(x).cuda()).cpu()
+        hy = torch.empty(plan.output_shape()).pin_memory()
+        plan.forward_host(torch.from_numpy(x).pin_memory(), hy)
+    assert (hy - yd).abs().max() <= 1e-6 * yd.abs().max()
+    for i in (0, n - 1):
+        _check_fp32(oracle, hy[i:i + 1].numpy(), oracle.conv_batch(x[i:i + 1], w), f"wide padded image {i}")
+
+
 def test_full_size_sampled_images(oracle, clb, torch_cuda):
     """BASELINE full batch sizes: convolve the whole batch on the GPU, check a sample of
     images (0, N-1 and two seeded picks) against the oracle (images are independent)."""

@@ -83,7 +83,8 @@ __global__ void check(const float* a, const float* b, int shift, float* out) {
 }
 
 // timing: 148 CTAs, `taps` row-shifted views of A per stage, 3xTF32 pattern, one commit per
-// 16 stages; ts = 1 copies each view to TMEM first (4 x tcgen05.cp) and runs the .ts MMAs
+// 16 stages; ts = 1 copies each view to TMEM first (4 x tcgen05.cp) and runs the .ts MMAs;
+// ts = 2 runs the same .ts MMAs with A already resident in TMEM (no copies: the MMA rate alone)
 __global__ void timing(int n, int iters, int ts, unsigned long long* cyc) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -114,7 +115,8 @@ __global__ void timing(int n, int iters, int ts, unsigned long long* cyc) {
                     const uint64_t da = da0 + (uint64_t)(t * 8);
                     if (ts) {
                         const uint32_t ta = tmem + 256 + (uint32_t)((s & 1) * 32);
-                        for (int q = 0; q < 4; ++q) tmem_cp_128x256b(ta + 8 * q, da + 2 * q);
+                        if (ts == 1)
+                            for (int q = 0; q < 4; ++q) tmem_cp_128x256b(ta + 8 * q, da + 2 * q);
                         mma_tf32_ts(tmem, ta + 16, db, idesc, (it | s) ? 1u : 0u);
                         mma_tf32_ts(tmem, ta, db + 4, idesc, 1u);
                         mma_tf32_ts(tmem, ta, db, idesc, 1u);
@@ -175,7 +177,7 @@ int main() {
     cudaMalloc(&cyc, 148 * 8);
     cudaFuncSetAttribute(timing, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     for (int n : {64, 128}) {
-        for (int ts = 0; ts < 2; ++ts) {
+        for (int ts = 0; ts < 3; ++ts) {
             const int iters = 1000;
             timing<<<148, 128, 64 * 1024>>>(n, iters, ts, cyc);
             cudaError_t e = cudaDeviceSynchronize();
@@ -185,7 +187,7 @@ int main() {
             for (auto v : h) avg += v;
             avg /= 148;
             const double per = avg / (iters * 16.0 * 6.0);
-            printf("N=%3d %s: %s  %.1f cycles/MMA (ideal %d) -> %.0f%%\n", n, ts ? "A from TMEM (cp + .ts)" : "A from smem (.ss)     ",
+            printf("N=%3d %s: %s  %.1f cycles/MMA (ideal %d) -> %.0f%%\n", n, ts == 2 ? "A resident in TMEM (.ts)" : ts ? "A from TMEM (cp + .ts) " : "A from smem (.ss)       ",
                    cudaGetErrorString(e), per, n / 2, 100.0 * (n / 2) / per);
         }
     }
