@@ -275,7 +275,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             const int v = e ? std::atoi(e) : 0;
             return (v >= 16 && v <= 256 && v % 16 == 0) ? v : 0;
         }();
-        if (forced_bn && !p->padded_rows) t.bn = forced_bn;
+        if (forced_bn) t.bn = forced_bn;
         int cg = cta_group_for(t.rows, t.cols, t.bn);
         // few tiles even at 128 rows: halve the tile N to create more of them (B operand rows
         // are tiny anyway at these sizes)

@@ -120,6 +120,10 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     // Stage grouping: bps k-iterations share one full/empty barrier round trip.  Two per stage
     // are 2-5 % faster on every layer that still keeps >= 3 stages in flight; with only 2
     // stages left the pipeline runs dry (VGG conv5_x, conv2_1: 3-7 % slower), so stay at 1.
+    // A and B loads from two producer warps: 3-8 % on the TMA-im2col layers (AlexNet conv2 / conv5,
+    // VGG conv5_x), neutral on the padded-row ones (profiles/r01_split_issue_sweep.txt)
+    static const int env_split_issue = getenv("CLB_SPLIT_ISSUE") ? atoi(getenv("CLB_SPLIT_ISSUE")) : 1;
+    p.split_issue = env_split_issue;
     static const int env_smem = getenv("CLB_SMEM_KB") ? atoi(getenv("CLB_SMEM_KB")) * 1024 : 0;   // experiment knob
     const int budget = env_smem > 0 ? env_smem : kSmemBudget;
     if (p.bps <= 0) {

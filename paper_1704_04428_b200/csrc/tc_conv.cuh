@@ -82,6 +82,7 @@ struct TcParams {
     // leading rows are TMA out-of-bounds zero fill), so output (y, x) sits at row y*Wp + x and
     // tap (i, j) reads row y*Wp + x + (i - pad)*Wp + (j - pad).
     int tps;                   // taps per stage (1 = one tap per stage)
+    int split_issue;           // A and B TMA loads issued by two warps (0 and 3), 2 arrivals per stage
     int bps;                   // k-iterations ("sub-stages") per pipeline stage: one barrier
                                // round trip per bps TMA box pairs (chunk_iters % bps == 0)
     int a_row_shift;           // A row offset per tap group (padded row width Wp)
@@ -303,7 +304,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], p.split_issue ? 2 : 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < nbuf; ++a) {
@@ -341,16 +342,20 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-    if (warp == 0) {
+    if (warp == 0 || (warp == 3 && p.split_issue)) {
         // ------------------------------------------------------------ TMA producer ----
-        // whole warp runs the (uniform) loop; one elected lane issues the TMA
+        // whole warp runs the (uniform) loop; one elected lane issues the TMA.  With split_issue
+        // warp 0 loads A and warp 3 loads B (TMA im2col boxes are slow to deliver from a single
+        // issuing thread: tools/tma_probe3.cu 37 -> 43 B/clk per SM with two issuers).
         {
+            const bool do_a = warp == 0, do_b = warp == 3 || !p.split_issue;
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t tx = (uint32_t)CG * stage_tx;   // both CTAs' bytes land on the leader
+            const uint32_t a_tx = (uint32_t)(tc_a_box_rows(tps) * kRowBytes);
+            const uint32_t tx = (uint32_t)CG * ((do_a ? a_tx : 0u) + (do_b ? stage_tx - a_tx : 0u));   // both CTAs' bytes land on the leader
             long long w_empty = 0;
             const long long t_start = clock64();
-            if (TRACE && lane_id() == 0) p.trace[blockIdx.x * kTraceSlots + 8] = (unsigned long long)(t_start - t_entry);
+            if (TRACE && lane_id() == 0 && warp == 0) p.trace[blockIdx.x * kTraceSlots + 8] = (unsigned long long)(t_start - t_entry);
             Sched sch(p, unit, nunits);
             Piece pc;
             while (sch.next(pc)) {
@@ -383,22 +388,29 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     if constexpr (CG == 2) {
                         const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
                         if (leader && sub == 0) mbar_arrive_expect_tx(&full[stage], txs);
-                        if (ca.mode == LOAD_IM2COL)
-                            tma_load_im2col_4d_2sm(&map_a, lbar, a_st, kc, ca.c1, ca.c2, ca.c3, (uint16_t)tj, (uint16_t)ti);
-                        else
-                            tma_load_3d_2sm(&map_a, lbar, a_st, kc, arow, ca.tap3 ? tap : 0);
-                        if (cb.mode == LOAD_IM2COL)
-                            tma_load_im2col_4d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.c2, cb.c3, (uint16_t)tj,
-                                                   (uint16_t)ti);
-                        else
-                            tma_load_3d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.tap3 ? tap : 0);
+                        if (do_a) {
+                            if (ca.mode == LOAD_IM2COL)
+                                tma_load_im2col_4d_2sm(&map_a, lbar, a_st, kc, ca.c1, ca.c2, ca.c3, (uint16_t)tj,
+                                                       (uint16_t)ti);
+                            else
+                                tma_load_3d_2sm(&map_a, lbar, a_st, kc, arow, ca.tap3 ? tap : 0);
+                        }
+                        if (do_b) {
+                            if (cb.mode == LOAD_IM2COL)
+                                tma_load_im2col_4d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.c2, cb.c3, (uint16_t)tj,
+                                                       (uint16_t)ti);
+                            else
+                                tma_load_3d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.tap3 ? tap : 0);
+                        }
                     } else {
                         if (sub == 0) mbar_arrive_expect_tx(&full[stage], txs);
-                        if (ca.mode == LOAD_IM2COL)
-                            load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
-                        else
-                            tma_load_3d(&map_a, &full[stage], a_st, kc, arow, ca.tap3 ? tap : 0);
-                        load_operand(&map_b, cb, &full[stage], a_st + a_bytes, kc, tap, ti, tj);
+                        if (do_a) {
+                            if (ca.mode == LOAD_IM2COL)
+                                load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
+                            else
+                                tma_load_3d(&map_a, &full[stage], a_st, kc, arow, ca.tap3 ? tap : 0);
+                        }
+                        if (do_b) load_operand(&map_b, cb, &full[stage], a_st + a_bytes, kc, tap, ti, tj);
                     }
                     }
                     __syncwarp();
@@ -421,7 +433,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     }
                 }
             }
-            if (TRACE && lane_id() == 0) {
+            if (TRACE && lane_id() == 0 && warp == 0) {
                 p.trace[blockIdx.x * kTraceSlots + 0] = (unsigned long long)(clock64() - t_start);
                 p.trace[blockIdx.x * kTraceSlots + 1] = (unsigned long long)w_empty;
             }
