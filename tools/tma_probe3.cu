@@ -3,7 +3,8 @@
 // consumer releases each stage the moment it lands).  Each stage = one A box of 128 rows
 // (im2col over 13x13 NHWC images, or tiled) + one tiled B box of 96 rows, 128 B per row (28 KB),
 // as in AlexNet conv3 (CTA pair, N = 192).  Issuers: 1 = one thread issues both loads;
-// 2 = two warps (A / B), each arriving on the full barrier with its own expect_tx.
+// 2 = two warps (A / B), each arriving on the full barrier with its own expect_tx;
+// 3 = A split into two 64-row boxes from two warps, B from a third.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Ipaper_1704_04428_b200/csrc
 //        tools/tma_probe3.cu -o tools/tma_probe3 -lcuda
 #include <cstdio>
@@ -16,7 +17,8 @@ using namespace clb;
 
 constexpr int kA = 128 * 128, kB = 96 * 128, kStage = kA + kB;
 
-__global__ void ring(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, int a_im2col,
+__global__ void ring(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
+                     const __grid_constant__ CUtensorMap ma64, int a_im2col,
                      int stages, int issuers, int iters, int npix, int W, int nb_rows, unsigned long long* out) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -32,18 +34,23 @@ __global__ void ring(const __grid_constant__ CUtensorMap ma, const __grid_consta
     }
     __syncthreads();
     const long long t0 = clock64();
-    if (warp == 0 || (issuers == 2 && warp == 2)) {
+    if (warp == 0 || (issuers >= 2 && warp == 2) || (issuers == 3 && warp == 3)) {
         if (lane == 0) {
-            const bool do_a = warp == 0, do_b = issuers == 1 || warp == 2;
+            const bool do_a = warp == 0 || warp == 3, do_b = issuers == 1 || warp == 2;
+            const int half = issuers == 3 ? (warp == 3 ? 1 : 0) : -1;   // -1: whole 128-row A box
             int stage = 0;
             uint32_t phase = 0;
             int pix = (blockIdx.x * 977) % npix, brow = (blockIdx.x * 131) % nb_rows;
             for (int it = 0; it < iters; ++it) {
                 mbar_wait(&empty[stage], phase ^ 1u);
                 uint8_t* st = smem + stage * kStage;
-                mbar_arrive_expect_tx(&full[stage], (do_a ? kA : 0) + (do_b ? kB : 0));
+                mbar_arrive_expect_tx(&full[stage], (do_a ? (half < 0 ? kA : kA / 2) : 0) + (do_b ? kB : 0));
                 if (do_a) {
-                    if (a_im2col) {
+                    if (a_im2col && half >= 0) {
+                        const int q = pix + 64 * half;
+                        const int x = q % W, y = (q / W) % W, n = q / (W * W);
+                        tma_load_im2col_4d(&ma64, &full[stage], st + half * (kA / 2), 0, x - 1, y - 1, n, 1, 1);
+                    } else if (a_im2col) {
                         const int x = pix % W, y = (pix / W) % W, n = pix / (W * W);
                         tma_load_im2col_4d(&ma, &full[stage], st, 0, x - 1, y - 1, n, 1, 1);
                     } else {
@@ -95,13 +102,13 @@ int main() {
     cudaMalloc(&bbuf, (size_t)nb_rows * 128);
     cudaMemset(abuf, 0, (size_t)npix * 128);
     cudaMemset(bbuf, 0, (size_t)nb_rows * 128);
-    CUtensorMap ma_i, ma_t, mb;
-    {
+    CUtensorMap ma_i, ma_t, mb, ma_i64;
+    for (int bx : {128, 64}) {
         cuuint64_t dims[4] = {32, (cuuint64_t)W, (cuuint64_t)W, (cuuint64_t)N};
         cuuint64_t str[3] = {128, 128ull * W, 128ull * W * W};
         int lo[2] = {-1, -1}, up[2] = {-1, -1};
         cuuint32_t es[4] = {1, 1, 1, 1};
-        if (enc_i(&ma_i, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, abuf, dims, str, lo, up, 32, 128, es,
+        if (enc_i(bx == 128 ? &ma_i : &ma_i64, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, abuf, dims, str, lo, up, 32, bx, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("encode im2col failed\n"); return 1; }
     }
@@ -122,7 +129,7 @@ int main() {
     cudaFuncSetAttribute(ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     printf("%-7s %6s %4s %9s %9s %10s\n", "A mode", "stages", "iss", "TB/s", "B/clk/SM", "clk/stage");
     struct Case { int im2col, stages, issuers; };
-    const Case cases[] = {{1, 7, 1}, {1, 7, 2}, {1, 4, 1}, {1, 4, 2}, {1, 2, 1}, {0, 7, 1}, {0, 7, 2}, {0, 4, 1}};
+    const Case cases[] = {{1, 7, 1}, {1, 7, 2}, {1, 7, 3}, {1, 4, 3}, {0, 7, 1}, {0, 7, 2}};
     for (const Case& c : cases) {
         const int iters = 2000;
         const int smem = 1024 + c.stages * kStage + 256;
@@ -131,7 +138,7 @@ int main() {
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
             cudaEventRecord(e0);
-            ring<<<148, 128, smem>>>(c.im2col ? ma_i : ma_t, mb, c.im2col, c.stages, c.issuers, iters, npix, W, nb_rows,
+            ring<<<148, 128, smem>>>(c.im2col ? ma_i : ma_t, mb, ma_i64, c.im2col, c.stages, c.issuers, iters, npix, W, nb_rows,
                                      cyc);
             cudaEventRecord(e1);
             cudaError_t err = cudaDeviceSynchronize();
