@@ -95,6 +95,8 @@ struct cl_plan {
     float* wraw = nullptr;     // direct-gpu: MKKC fp32 weights as given
     unsigned* flags = nullptr; // stream-K fixup flags, zeroed once, self-resetting
     bool padded_rows = false;  // implicit kn2row in tap-shared (zero-padded row) mode
+    int stack_k = 1;           // > 1: padded-row mode with the k taps of a kernel row stacked on N
+    int bn_stack = 0;          // its tile N (k x channels per column tile)
     bool weights_set = false;
     void* own_ws = nullptr;
     size_t own_ws_bytes = 0;
@@ -136,6 +138,13 @@ size_t method_ws_bytes(const cl_plan* p);
 size_t ws_bytes(const cl_plan* p) { return align256(method_ws_bytes(p)) + tc_scratch_bytes(); }
 void* scratch_of(const cl_plan* p, void* ws) { return static_cast<char*>(ws) + align256(method_ws_bytes(p)); }
 
+// Tap-stacked mode reads A through an overlapping view whose bounds check covers only the
+// row dimension: zeroed rows before (the first image's leading padding, made real) and after
+// the padded grid keep every read in bounds and every out-of-image tap zero.
+int stack_lead_rows(const cl_plan* p) { return p->stack_k > 1 ? p->d.pad * (p->d.w + p->d.pad) + p->d.pad : 0; }
+int stack_trail_rows(const cl_plan* p) { return p->stack_k > 1 ? 4 * 32 : 0; }
+size_t stack_slack_rows(const cl_plan* p) { return (size_t)stack_lead_rows(p) + stack_trail_rows(p); }
+
 size_t method_ws_bytes(const cl_plan* p) {
     const cl_conv_desc& d = p->d;
     const size_t nhw = (size_t)d.n * d.h * d.w;
@@ -147,7 +156,7 @@ size_t method_ws_bytes(const cl_plan* p) {
         case CL_METHOD_CONV1X1:
         case CL_METHOD_KN2ROW_ACC:
             if (p->padded_rows)
-                return (size_t)d.n * (d.h + d.pad) * (d.w + d.pad) * row_bytes(p->planes, p->Cp);
+                return ((size_t)d.n * (d.h + d.pad) * (d.w + d.pad) + stack_slack_rows(p)) * row_bytes(p->planes, p->Cp);
             return xs;
         case CL_METHOD_KN2ROW_EXPLICIT:
         case CL_METHOD_KN2COL:
@@ -275,11 +284,12 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             const int v = e ? std::atoi(e) : 0;
             return (v >= 16 && v <= 256 && v % 16 == 0) ? v : 0;
         }();
-        if (forced_bn) t.bn = forced_bn;
+        const bool fixed_bn = t.stack_k > 1;   // tap-stacked: N is k x channels, not a free choice
+        if (forced_bn && !fixed_bn) t.bn = forced_bn;
         int cg = cta_group_for(t.rows, t.cols, t.bn);
         // few tiles even at 128 rows: halve the tile N to create more of them (B operand rows
         // are tiny anyway at these sizes)
-        if (!forced_bn && cg == 1 && t.bn >= 64 &&
+        if (!forced_bn && !fixed_bn && cg == 1 && t.bn >= 64 &&
             (long long)(t.rows + 127) / 128 * ((t.cols + t.bn - 1) / t.bn) < num_sms() / 2)
             t.bn = round_up(t.bn / 2, 16);
         // a k-tap stage must fit twice: a sub-batch (host-buffer chunks) can drop a padded-row
@@ -287,6 +297,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         const int tps = t.tps > 0 ? t.tps : 1;
         while (tc_num_stages(t.bn / cg, tps) < 2 && t.bn > 16) {
             if (cg == 1 && t.rows >= 256 && t.bn % 32 == 0) cg = 2;
+            else if (fixed_bn) break;
             else t.bn = round_up(t.bn / 2, 16);
         }
         launch_tc(a, b, t, s, cg);
@@ -305,10 +316,18 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 // tap-shared mode: zero-padded NHWC rows; each stage loads ONE A box of 128+k-1
                 // rows per kernel row i and feeds its k taps through row-shifted descriptors
                 const int Hp = d.h + d.pad, Wp = d.w + d.pad;   // shared padding (tc_conv.cuh)
-                if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
-                else launch_nchw_to_padded_split(x, xs, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                const size_t rb = (size_t)row_bytes(p->planes, p->Cp);
+                const long long grid_rows = (long long)d.n * Hp * Wp;
+                const int lead = stack_lead_rows(p), trail = stack_trail_rows(p);
+                if (lead + trail > 0) {   // tap-stacked slack rows (zero), before the prepass (PDL pairs it with the contraction)
+                    CLB_CUDA(cudaMemsetAsync(xs, 0, (size_t)lead * rb, s));
+                    CLB_CUDA(cudaMemsetAsync(static_cast<char*>(xs) + ((size_t)lead + grid_rows) * rb, 0, (size_t)trail * rb, s));
+                }
+                void* grid = static_cast<char*>(xs) + (size_t)lead * rb;
+                if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
                 ++p->launches;
-                Operand a = tiled(xs, (long long)d.n * Hp * Wp, 1, p->Cp, p->planes);
+                Operand a = tiled(xs, grid_rows, 1, p->Cp, p->planes);
                 Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
                 TcParams t = base_params(p);
                 t.rows = d.n * Hp * Wp;
@@ -317,8 +336,22 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 t.b_tap3 = 1;
                 static const bool env_tps1 = getenv("CLB_TPS1") && atoi(getenv("CLB_TPS1")) != 0;   // experiment knob
                 t.tps = env_tps1 ? 1 : d.k;
+                t.taps = taps;
+                if (p->stack_k > 1) {
+                    // tap-stacked: one k-iteration = kernel row i x one channel block; B rows
+                    // (m, j) of row i, D column m*k + j; A unshifted (the shift-add is in the epilogue)
+                    b = tiled(p->wpack, (long long)d.m * d.k, d.k, p->Cp, p->planes);
+                    a = tiled(xs, lead + grid_rows + trail - 3 * (33 - d.k), 4, p->Cp, p->planes);
+                    a.tap_stride_rows = 33 - d.k;   // quadrant q of a box starts 33 - k rows after q - 1
+                    t.cols = d.m * d.k;
+                    t.bn = p->bn_stack;
+                    t.tps = 1;
+                    t.ksize = 1;      // tap index = kernel row i (ti = i, tj = 0)
+                    t.taps = d.k;
+                    t.stack_k = d.k;
+                }
                 t.a_row_shift = Wp;
-                t.a_row_base = -d.pad * Wp - d.pad;
+                t.a_row_base = lead - d.pad * Wp - d.pad;   // >= 0 in tap-stacked mode
                 t.epi = nhwc ? EPI_NHWC_PADDED : EPI_NCHW_PADDED;
                 t.ld = d.m;
                 t.epi_hp = Hp;
@@ -327,7 +360,6 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 t.out = y;
                 t.out_channels = d.m;
                 t.pq_out = p->P * p->Q;
-                t.taps = taps;
                 tc(a, b, t);
                 tc_done();
                 break;
@@ -520,6 +552,21 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             // (profiles/r01_padded_shared_sweep.txt).
             const double max_waste = p->bn <= 192 ? 0.70 : 0.10;
             p->padded_rows = eligible && (forced_padded == 1 || (forced_padded != 0 && waste <= max_waste));
+            // Tap-stacked: with few output channels the MMA's N = M is small and pays a fixed
+            // cost per instruction (N = 64: 51 cycles vs 32 ideal, tools/mma_probe.cu); stacking
+            // the k taps of a kernel row on N (N = k x M, one A box per row, no tap shifts) and
+            // doing the shift-add in the epilogue issues k x fewer, k x wider MMAs.  Single
+            // column tile only (M <= 80 for k = 3, <= 48 for k = 5).  CLB_STACKED=0/1 forces.
+            static const int forced_stacked = [] {
+                const char* e = std::getenv("CLB_STACKED");
+                return e ? std::atoi(e) : -1;
+            }();
+            const int mt = round_up(d.m, 16);
+            if (p->padded_rows && (d.k == 3 || d.k == 5) && mt * d.k <= 256 && forced_stacked != 0 &&
+                (forced_stacked == 1 || p->bn <= 128)) {
+                p->stack_k = d.k;
+                p->bn_stack = mt * d.k;
+            }
         }
         if (cudaMalloc(&p->flags, kMaxGrid * sizeof(unsigned)) != cudaSuccess ||
             cudaMemset(p->flags, 0, kMaxGrid * sizeof(unsigned)) != cudaSuccess) {
@@ -545,7 +592,7 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
         else if (p->method == CL_METHOD_DIRECT)
             CLB_CUDA(cudaMemcpyAsync(p->wpack, d_w, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
         else
-            launch_pack_weights(d_w, p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s);
+            launch_pack_weights(d_w, p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s, p->stack_k > 1);
         p->weights_set = true;
         mark_done(p, s);
     });
@@ -568,7 +615,7 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
         else if (p->method == CL_METHOD_DIRECT)
             CLB_CUDA(cudaMemcpyAsync(p->wpack, dw, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
         else
-            launch_pack_weights(static_cast<float*>(dw), p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s);
+            launch_pack_weights(static_cast<float*>(dw), p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s, p->stack_k > 1);
         CLB_CUDA(cudaFreeAsync(dw, s));
         CLB_CUDA(cudaStreamSynchronize(s));
         p->weights_set = true;

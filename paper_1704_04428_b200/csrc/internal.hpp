@@ -62,8 +62,9 @@ void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, 
 void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s);
 // b[K][cols] -> bs[cols][planes][Kp]
 void launch_transpose_split(const float* b, void* bs, int K, int cols, int Kp, int planes, cudaStream_t s);
-// w MKKC -> wp[tap][M][planes][Cp]
-void launch_pack_weights(const float* w, void* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s);
+// w MKKC -> wp[tap][M][planes][Cp], or (stacked) wp[i][M][j][planes][Cp]
+void launch_pack_weights(const float* w, void* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s,
+                         bool stacked = false);
 // x NCHW -> patches[n p q][planes][Kp], K index (i*k+j)*C + c  (conv_im2.cpp:19-54 order)
 void launch_im2col_split(const float* x, void* pm, int N, int C, int H, int W, int k, int pad, int stride,
                          int P, int Q, int Kp, int planes, cudaStream_t s);
@@ -90,6 +91,7 @@ struct Operand {
     const void* ptr = nullptr;
     long long rows = 0;      // tiled: rows of the map
     int taps = 1;            // tiled: 3rd dim
+    long long tap_stride_rows = 0;   // tiled: rows between 3rd-dim slices (0 = rows; < rows = overlapping view)
     int kw = 0;              // elements per row: 2*Cp (split formats) or Cp (TF32, BF16)
     int planes = 2;          // precision mode (see k_granule)
     // im2col only

@@ -346,7 +346,7 @@ void launch_transpose_split(const float* b, void* bs, int K, int cols, int Kp, i
 // kn2row_reorder_kernel (conv_kn2.cpp:28-39) fused with the split:
 //   wp[(i*k+j)][m][plane][c] = split(K[m][i][j][c])
 __global__ void pack_weights_kernel(const float* __restrict__ w, void* __restrict__ wp, int M, int k, int C,
-                                    int Cp, int planes) {
+                                    int Cp, int planes, int stacked) {
     const long long total = (long long)k * k * M * Cp;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
@@ -355,14 +355,18 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, void* __restric
         const int m = (int)(tm % M);
         const int t = (int)(tm / M);
         const float v = c < C ? w[((long long)m * k * k + t) * C + c] : 0.0f;
-        store_split(wp, tm * rowel(planes, Cp), c, Cp, planes, v);
+        // tap-major [t][m] rows, or tap-stacked [i][m][j] (the k taps of kernel row i as
+        // adjacent columns of one output channel, tc_conv.cuh stack_k)
+        const long long row = stacked ? ((long long)(t / k) * M + m) * k + (t % k) : tm;
+        store_split(wp, row * rowel(planes, Cp), c, Cp, planes, v);
     }
 }
 
-void launch_pack_weights(const float* w, void* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s) {
+void launch_pack_weights(const float* w, void* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s,
+                         bool stacked) {
     const long long total = (long long)k * k * M * Cp;
     const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-    pack_weights_kernel<<<blocks, 256, 0, s>>>(w, wp, M, k, C, Cp, planes);
+    pack_weights_kernel<<<blocks, 256, 0, s>>>(w, wp, M, k, C, Cp, planes, stacked ? 1 : 0);
     CLB_CUDA(cudaGetLastError());
 }
 

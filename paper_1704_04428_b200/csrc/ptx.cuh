@@ -87,6 +87,14 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
 }
 
 // 3-D tiled load: coords (c0 innermost, c1, c2).
+// L2 prefetch of one tiled box (no smem, no barrier): warms the lines a later load will read
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* m, int32_t c0, int32_t c1, int32_t c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, uint64_t* bar, void* smem, int32_t c0,
                                             int32_t c1, int32_t c2) {
     asm volatile(

@@ -70,7 +70,8 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int b
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
         cuuint64_t dims[3] = {kdim, (cuuint64_t)op.rows, (cuuint64_t)op.taps};
-        cuuint64_t strides[2] = {kdim * eb, kdim * eb * (cuuint64_t)op.rows};
+        const cuuint64_t slice = (cuuint64_t)(op.tap_stride_rows > 0 ? op.tap_stride_rows : op.rows);
+        cuuint64_t strides[2] = {kdim * eb, kdim * eb * slice};
         cuuint32_t box[3] = {unit, (cuuint32_t)box_rows, (cuuint32_t)box_taps};
         cuuint32_t estr[3] = {1, 1, 1};
         r = g_tiled(map, dt, 3, const_cast<void*>(op.ptr), dims, strides, box, estr,
@@ -88,8 +89,20 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     const int unit = kRowBytes / elem_bytes(a.planes);
     if (a.kw != b.kw || a.kw % unit != 0 || a.planes != b.planes) throw Error(6, "operand K layout mismatch");
     if (p.tps <= 0) p.tps = 1;
+    if (p.stack_k <= 1) {
+        p.stack_k = 1;
+        p.row_step = kTileM;
+    } else {
+        if (p.stack_k != 3 && p.stack_k != 5) throw Error(6, "tap-stacked mode supports k = 3 and 5");
+        if ((p.bn / 2) % p.stack_k != 0) throw Error(6, "tap-stacked tile N must hold whole tap groups per half");
+        if (a.mode != LOAD_TILED || p.tps != 1) throw Error(6, "tap-stacked mode needs a tiled A, one tap per stage");
+        p.row_step = 4 * (33 - p.stack_k);
+    }
     CUtensorMap ma, mb;
-    encode_operand_map(&ma, a, tc_a_box_rows(p.tps), 1);
+    // tap-stacked: A = {unit, 32 rows, 4 quadrants} over the overlapping quadrant view
+    if (p.stack_k > 1 && (a.taps != 4 || a.tap_stride_rows != 33 - p.stack_k))
+        throw Error(6, "tap-stacked A must be the 4-quadrant overlapping view");
+    encode_operand_map(&ma, a, p.stack_k > 1 ? 32 : tc_a_box_rows(p.tps), p.stack_k > 1 ? 4 : 1);
     encode_operand_map(&mb, b, p.bn / cg, p.tps);
     p.planes = a.planes;
     p.row_elems = unit;
@@ -124,6 +137,8 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     // VGG conv5_x), neutral on the padded-row ones (profiles/r01_split_issue_sweep.txt)
     static const int env_split_issue = getenv("CLB_SPLIT_ISSUE") ? atoi(getenv("CLB_SPLIT_ISSUE")) : 1;
     p.split_issue = env_split_issue;
+    static const int env_l2_prefetch = getenv("CLB_L2_PREFETCH") ? atoi(getenv("CLB_L2_PREFETCH")) : 1;
+    p.l2_prefetch = env_l2_prefetch;
     static const int env_smem = getenv("CLB_SMEM_KB") ? atoi(getenv("CLB_SMEM_KB")) * 1024 : 0;   // experiment knob
     const int budget = env_smem > 0 ? env_smem : kSmemBudget;
     if (p.bps <= 0) {
@@ -139,7 +154,7 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     if (p.chunk_iters < k_iters && p.chunk_iters % p.bps != 0)
         p.chunk_iters = p.chunk_iters >= p.bps ? p.chunk_iters / p.bps * p.bps : p.bps;
     if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
-    const int tile_m = kTileM * cg;
+    const int tile_m = p.row_step * cg;   // output rows per tile
     const int row_tiles = (p.rows + tile_m - 1) / tile_m;
     p.n_col_tiles = (p.cols + p.bn - 1) / p.bn;
     p.num_tiles = row_tiles * p.n_col_tiles;
@@ -273,11 +288,11 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
         }
         const double mhz = ns_sum > 0 ? 1e3 * cyc_sum / ns_sum : 0.0;
         fprintf(stderr,
-                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
+                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stack=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
                 "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
                 "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us | "
                 "SM clock %.0f MHz (CTA cycles / CTA ns)\n",
-                p.rows, p.cols, p.bn, cg, p.tps, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
+                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
                 avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5], 100 * avg[11] / avg[5], avg[8], (t_out - t_in) * 1e-3,
                 (t_in_max - t_in) * 1e-3, ev_ms * 1e3, mhz);
         if (const char* dump = getenv("CLB_TRACE_DUMP")) {   // raw per-CTA records, appended

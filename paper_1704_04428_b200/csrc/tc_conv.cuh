@@ -83,11 +83,21 @@ struct TcParams {
     // tap (i, j) reads row y*Wp + x + (i - pad)*Wp + (j - pad).
     int tps;                   // taps per stage (1 = one tap per stage)
     int split_issue;           // A and B TMA loads issued by two warps (0 and 3), 2 arrivals per stage
+    int l2_prefetch;           // padded-row modes: L2-prefetch the next piece's A rows (CLB_L2_PREFETCH)
     int bps;                   // k-iterations ("sub-stages") per pipeline stage: one barrier
                                // round trip per bps TMA box pairs (chunk_iters % bps == 0)
     int a_row_shift;           // A row offset per tap group (padded row width Wp)
     int a_row_base;            // padded-row mode: A row of output row 0 (-pad*Wp - pad; TMA zero-fills < 0)
     int epi_hp, epi_wp, epi_n; // EPI_NCHW_PADDED geometry
+    // tap-stacked mode (stack_k = k > 1): the k taps j of a kernel row are k column blocks of
+    // ONE MMA (D column = m * k + j, weights packed [i][m][j]) over an unshifted A operand, and
+    // the kn2row shift-add out[r][m] = sum_j D[r + j][m * k + j] runs in the epilogue as warp
+    // shuffles.  A is ONE 3-D TMA box {unit, 32 rows, 4 quadrants} over an overlapping view of
+    // the padded input (quadrant stride 33 - k rows), so each TMEM lane quadrant holds its own
+    // k - 1 halo rows: 33 - k outputs per quadrant, row_step = 4 (33 - k) per CTA.  For small
+    // M (N = M would be a slow, small MMA).
+    int stack_k;               // 1 = off
+    int row_step;              // output rows per CTA tile (128, or 4 (33 - k) when stacked)
     int accumulate;            // out += D (accumulating shifted-GEMM variant)
     float* out;
     long long ld;              // EPI_ROWMAJOR leading dimension
@@ -257,6 +267,23 @@ __device__ __forceinline__ void store_rowmajor(float* dst, long long ld, int col
     }
 }
 
+// Tap-stacked shift-add (conv_kn2.cpp:94-118 restated on the accumulator): this thread holds
+// D row r = lane of its quadrant, columns c = m * KS + j of its half; afterwards sum[m] =
+// sum_j D[r + j][m * KS + j], row r + j being lane + j of the same warp.  Lanes >= 33 - KS
+// have no complete tap set (their rows are the next quadrant's halo) and are not stored.
+template <int KS>
+__device__ __forceinline__ void shift_add_taps(float* sum, int hcols) {
+#pragma unroll
+    for (int m = 0; m < 128 / KS; ++m) {
+        if (m * KS < hcols) {
+            float v = sum[m * KS];
+#pragma unroll
+            for (int j = 1; j < KS; ++j) v += __shfl_down_sync(0xffffffffu, sum[m * KS + j], j);
+            sum[m] = v;
+        }
+    }
+}
+
 // CG = 1: one CTA per 128-row tile (tcgen05 cta_group::1).
 // CG = 2: a CTA pair (cluster of 2) per 256-row tile (cta_group::2): each CTA TMA-loads its
 //         128 A rows and HALF of the BN B rows into its own smem, all completion bytes land
@@ -276,6 +303,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int planes = p.planes;
     const int stages = p.stages;
     const int tile_m = kTileM * CG;               // D rows per tile (the pair's rows for CG = 2)
+    const int tile_rows = p.row_step * CG;        // output rows per tile (< tile_m when tap-stacked)
     const int b_rows = bn / CG;                   // B rows this CTA loads
     const int tps = p.tps;
     const int a_bytes = tc_a_bytes(tps);          // A region of one stage (128 + tps - 1 rows)
@@ -361,8 +389,22 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             while (sch.next(pc)) {
                 const int mt = pc.tile / p.n_col_tiles;
                 const int nt = pc.tile - mt * p.n_col_tiles;
+                if (p.l2_prefetch && do_a && p.a_mode == LOAD_TILED && p.a_row_shift) {
+                    // padded-row modes: pull the NEXT piece's A rows (all kernel rows, all channel
+                    // blocks) into L2 now, so its loads hit L2 instead of waiting on HBM latency
+                    Sched nx = sch;
+                    Piece pn;
+                    if (nx.next(pn) && elect_one()) {
+                        const int r0 = (pn.tile / p.n_col_tiles) * tile_rows + (int)rank * p.row_step + p.a_row_base;
+                        const int nrow = p.ksize == 1 ? p.taps : p.taps / p.ksize;   // kernel rows
+                        for (int i = 0; i < nrow; ++i)
+                            for (int kb2 = 0; kb2 < p.kblocks; ++kb2)
+                                tma_prefetch_3d(&map_a, kb2 * p.row_elems, r0 + i * p.a_row_shift, 0);
+                    }
+                    __syncwarp();
+                }
                 const OperandCoord ca =
-                    operand_coord(p.a_mode, p.a_tap3, mt * tile_m + (int)rank * kTileM, p.P, p.Q, p.pad);
+                    operand_coord(p.a_mode, p.a_tap3, mt * tile_rows + (int)rank * p.row_step, p.P, p.Q, p.pad);
                 const OperandCoord cb = operand_coord(p.b_mode, p.b_tap3, nt * bn + (int)rank * b_rows, p.P, p.Q, p.pad);
                 const int it0 = pc.c_lo * ci;
                 const int it1 = pc.c_hi * ci < k_iters ? pc.c_hi * ci : k_iters;
@@ -616,8 +658,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         while (sch.next(pc)) {
             const int mt = pc.tile / p.n_col_tiles;
             const int nt = pc.tile - mt * p.n_col_tiles;
-            const int row = mt * tile_m + (int)rank * kTileM + trow;
-            const int col0 = nt * bn + cbase;
+            const int row = mt * tile_rows + (int)rank * p.row_step +
+                            (p.stack_k > 1 ? quad * (33 - p.stack_k) + lane : trow);
+            int col0 = nt * bn + cbase;
             float sum[128];
 #pragma unroll
             for (int j = 0; j < 128; ++j) sum[j] = 0.0f;
@@ -716,9 +759,22 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 if (threadIdx.x == 4 * 32)
                     for (int u2 = unit + 1; u2 < u_end; ++u2) p.flags[u2 * CG + (int)rank] = 0u;
             }
+            // ---- tap-stacked: shift-add the k column blocks across rows ----
+            int ncol = min(hcols, p.cols - col0);   // valid output columns of this half
+            bool row_ok = true;
+            if (p.stack_k > 1) {
+                if (p.stack_k == 3) shift_add_taps<3>(sum, hcols);
+                else if (p.stack_k == 5) shift_add_taps<5>(sum, hcols);
+                const int g = hcols / p.stack_k;    // output channels per half
+                col0 = nt * (bn / p.stack_k) + half * g;
+                ncol = min(g, p.out_channels - col0);
+                row_ok = lane < 33 - p.stack_k;
+            }
             // ---- store the finished tile ----
             const long long t_st = TRACE ? clock64() : 0;
-            if (row < p.rows && p.epi == EPI_NCHW_PADDED) {
+            if (!row_ok || ncol <= 0) {
+                // dropped row (tap-stacked tile tail) or a column half past the last channel
+            } else if (row < p.rows && p.epi == EPI_NCHW_PADDED) {
                 // padded output space: row = n*Hp*Wp + y*Wp + x; only y < P, x < Q are outputs
                 const int hw = p.epi_hp * p.epi_wp;
                 const int n = row / hw;
@@ -727,13 +783,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const int xq = rem - y * p.epi_wp;
                 if (n < p.epi_n && y < p.P && xq < p.Q)
                     store_nchw(p.out + ((long long)n * p.out_channels + col0) * p.pq_out + (long long)y * p.Q + xq,
-                               p.pq_out, min(hcols, p.cols - col0), p.accumulate, sum);
+                               p.pq_out, ncol, p.accumulate, sum);
             } else if (row < p.rows) {
                 if (p.epi == EPI_NCHW) {
                     const int n = row / p.pq_out;
                     const int pq = row - n * p.pq_out;
                     store_nchw(p.out + ((long long)n * p.out_channels + col0) * p.pq_out + pq, p.pq_out,
-                               min(hcols, p.cols - col0), p.accumulate, sum);
+                               ncol, p.accumulate, sum);
                 } else if (p.epi == EPI_NHWC_PADDED) {
                     // padded pixel space -> channels-last output row (n*P + y)*Q + x
                     const int hw = p.epi_hp * p.epi_wp;
@@ -742,10 +798,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     const int y = rem / p.epi_wp;
                     const int xq = rem - y * p.epi_wp;
                     if (n < p.epi_n && y < p.P && xq < p.Q)
-                        store_rowmajor(p.out + (((long long)n * p.P + y) * p.Q + xq) * p.ld + col0, p.ld, col0, hcols,
-                                       p.cols, p.accumulate, sum);
+                        store_rowmajor(p.out + (((long long)n * p.P + y) * p.Q + xq) * p.ld + col0, p.ld, col0, ncol,
+                                       col0 + ncol, p.accumulate, sum);
                 } else {
-                    store_rowmajor(p.out + (long long)row * p.ld + col0, p.ld, col0, hcols, p.cols, p.accumulate, sum);
+                    store_rowmajor(p.out + (long long)row * p.ld + col0, p.ld, col0, ncol, col0 + ncol, p.accumulate, sum);
                 }
             }
             if (TRACE) {

@@ -357,7 +357,9 @@ from oracle import oracle as O
 import paper_1704_04428_b200 as clb
 out = []
 for (N, C, H, W, M, k, pad) in [(2, 16, 30, 34, 32, 3, 1), (1, 48, 20, 24, 100, 5, 2), (2, 20, 17, 19, 64, 7, 3),
-                                 (2, 24, 21, 23, 40, 3, 0), (3, 64, 12, 12, 64, 3, 2), (64, 8, 5, 6, 16, 3, 1)]:
+                                 (2, 24, 21, 23, 40, 3, 0), (3, 64, 12, 12, 64, 3, 2), (64, 8, 5, 6, 16, 3, 1),
+                                 (2, 32, 19, 21, 48, 5, 2), (3, 16, 14, 14, 32, 5, 2), (2, 100, 16, 18, 64, 3, 1),
+                                 (1, 100, 12, 12, 64, 3, 1), (4, 64, 40, 40, 80, 3, 1)]:
     x, w = O.make_problem(N, C, H, W, M, k, N + C)
     ref = O.conv_loopnest(x, w, pad, 1)
     layer = clb.LayerConfig("p", C, H, W, M, k, 1, pad, N)
@@ -372,12 +374,16 @@ print(json.dumps(out))
 '''
 
 
-@pytest.mark.parametrize("mode", ["1", "0"])
+@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked"])
 def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     """The implicit kernel's tap-shared mode (zero-padded NHWC rows, one A box of 128+k-1 rows
     per kernel row, taps through row-shifted UMMA descriptors), forced on and off via
     CLB_PADDED_ROWS in a subprocess: k = 3/5/7, pad != k/2, batch-spanning tiles, all three
-    precisions (the BF16 rows are 64 channels per 128 B unit, so the row shift differs)."""
+    precisions (the BF16 rows are 64 channels per 128 B unit, so the row shift differs).
+    "stacked" forces the tap-stacked variant (the k taps of a kernel row as column blocks of one
+    MMA, shift-add across rows in the epilogue) wherever it applies (k = 3/5, k x M <= 256),
+    including multi-chunk K, stream-K split tiles, M not a multiple of 16 and pad 0 / pad > k/2;
+    the launch trace proves both k = 3 and k = 5 instantiations ran."""
     import json
     import os
     import subprocess
@@ -386,9 +392,14 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     root = Path(__file__).resolve().parent.parent
     script = tmp_path / "padded.py"
     script.write_text(_PADDED_SCRIPT)
+    env = {"1": dict(CLB_PADDED_ROWS="1"), "0": dict(CLB_PADDED_ROWS="0"),
+           "stacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1"),
+           "unstacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="0")}[mode]
     r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
-                       env=dict(os.environ, CLB_PADDED_ROWS=mode))
+                       env=dict(os.environ, **env))
     assert r.returncode == 0, r.stderr[-3000:]
+    if mode == "stacked":
+        assert "stack=3" in r.stderr and "stack=5" in r.stderr, r.stderr[-2000:]
     for res in json.loads(r.stdout.strip().splitlines()[-1]):
         if res["precision"] == "fp32":
             assert res["rel_l2"] <= FP32_L2 and res["max_rel"] <= FP32_MAX, (mode, res)

@@ -15,7 +15,7 @@ tag = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for name in layers:
     group = name.split("/")[0]
-    layer = [l for l in workloads.workload(group, batch) if l.name == name][0]
+    layer = [l for l in workloads.workload(group, batch) if l.name in (name, group)][0]
     x, w = rng.make_problem(layer.batch, layer.channels, layer.height, layer.width, layer.kernel_count,
                             layer.kernel_size)
     with clb.ConvPlan(layer, "auto", "fp32") as plan:
