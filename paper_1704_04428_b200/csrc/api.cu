@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" boundary (include/convlab_b200.h): plans, method dispatch,
 // workspace management, error mapping.  No CPU fallback anywhere: every entry point
 // either enqueues sm_100a kernels or returns an error.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -242,7 +243,10 @@ void mark_done(cl_plan* p, cudaStream_t s) {
 
 // n_images < 0: the plan's batch; otherwise a sub-batch (chunked host pipeline).
 // nhwc: channels-last input and output (implicit kn2row / conv1x1 / accumulating only).
-void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images = -1, bool nhwc = false) {
+// ev_first / ev_last_chunk: record the plan's profile events (begin / end) in this call (a
+// chunked forward brackets all of its chunks with one pair).
+void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images = -1, bool nhwc = false,
+             bool ev_first = true, bool ev_last_chunk = true) {
     cl_conv_desc d = p->d;
     if (n_images >= 0) d.n = n_images;
     require(p->weights_set, "cl_conv_forward: weights not set (cl_conv_set_weights)");
@@ -274,7 +278,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         // kernel's prologue overlap the prepass tail); an interposed profile event only
         // removes the overlap, never the ordering
         t.pdl = !began ? 1 : 0;
-        if (p->ev_begin && !began) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
+        if (p->ev_begin && !began && ev_first) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
         began = true;
         set_scratch(t, scratch);
         t.flags = p->flags;
@@ -304,7 +308,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         ++p->launches;
     };
     auto tc_done = [&] {
-        if (p->ev_end) CLB_CUDA(cudaEventRecord(p->ev_end, s));
+        if (p->ev_end && ev_last_chunk) CLB_CUDA(cudaEventRecord(p->ev_end, s));
     };
 
     switch (p->method) {
@@ -455,7 +459,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         case CL_METHOD_DIRECT: {
             if (nhwc) throw Error(CL_EUNSUPPORTED, "channels-last forward: implicit kn2row / conv1x1 / kn2row-acc only");
             // the dominant (and only) kernel of this method: bracket it for the profile events
-            if (p->ev_begin) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
+            if (p->ev_begin && ev_first) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
             launch_direct_conv(x, p->wraw, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, d.stride, p->P, p->Q, s);
             ++p->launches;
             tc_done();
@@ -464,6 +468,40 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         default:
             throw Error(CL_EINTERNAL, "unresolved method");
     }
+}
+
+// L2-chunked forward: a large implicit-kn2row layer runs as image chunks whose split operand
+// (the prepass output the contraction reads) fits in L2, reusing one workspace region, so the
+// contraction's operand loads hit L2 (tools/tma_probe4.cu: 67-75 vs ~44 B/clk/SM streaming
+// from HBM) and the split tensor never round-trips HBM.  CLB_L2_CHUNK_MB sets the chunk budget
+// (0 = whole batch).
+void forward_chunked(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, bool nhwc) {
+    // Measured 1.3-2x SLOWER on every VGG / AlexNet layer at 16-80 MB chunks (per-launch ramp
+    // and tail waves dominate; profiles/r01_l2_chunked_forward.txt): off unless set.
+    static const double chunk_mb = [] {
+        const char* e = std::getenv("CLB_L2_CHUNK_MB");
+        return e ? std::atof(e) : 0.0;
+    }();
+    const cl_conv_desc& d = p->d;
+    int nc = d.n;
+    const bool implicit = p->method == CL_METHOD_KN2ROW || p->method == CL_METHOD_CONV1X1;
+    if (chunk_mb > 0 && implicit) {
+        const double pix = p->padded_rows ? (double)(d.h + d.pad) * (d.w + d.pad) : (double)d.h * d.w;
+        const double per_img = pix * (double)row_bytes(p->planes, p->Cp);
+        nc = std::max(1, (int)(chunk_mb * 1e6 / per_img));
+    }
+    if (nc >= d.n) {
+        forward(p, x, y, ws, s, -1, nhwc);
+        return;
+    }
+    const size_t img_in = (size_t)d.c * d.h * d.w, img_out = (size_t)d.m * p->P * p->Q;
+    int launches = 0;
+    for (int n0 = 0; n0 < d.n; n0 += nc) {
+        const int cnt = std::min(nc, d.n - n0);
+        forward(p, x + n0 * img_in, y + n0 * img_out, ws, s, cnt, nhwc, n0 == 0, n0 + cnt == d.n);
+        launches += p->launches;
+    }
+    p->launches = launches;
 }
 
 }  // namespace
@@ -556,14 +594,17 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             // cost per instruction (N = 64: 51 cycles vs 32 ideal, tools/mma_probe.cu); stacking
             // the k taps of a kernel row on N (N = k x M, one A box per row, no tap shifts) and
             // doing the shift-add in the epilogue issues k x fewer, k x wider MMAs.  Single
-            // column tile only (M <= 80 for k = 3, <= 48 for k = 5).  CLB_STACKED=0/1 forces.
+            // column tile only (M <= 80 for k = 3, <= 48 for k = 5).  Measured: the MMA work per
+            // tile halves, but these layers then wait on A delivery (latency-bound TMA loads,
+            // tools/tma_probe4.cu), so k = 3 layers gain nothing (VGG conv1_2 -3 %) while the
+            // 5x5 ones gain up to 9 % (GoogLeNet 4a_5x5): auto for k = 5 only.  CLB_STACKED=0/1 forces.
             static const int forced_stacked = [] {
                 const char* e = std::getenv("CLB_STACKED");
                 return e ? std::atoi(e) : -1;
             }();
             const int mt = round_up(d.m, 16);
             if (p->padded_rows && (d.k == 3 || d.k == 5) && mt * d.k <= 256 && forced_stacked != 0 &&
-                (forced_stacked == 1 || p->bn <= 128)) {
+                (forced_stacked == 1 || (d.k == 5 && p->bn <= 128))) {
                 p->stack_k = d.k;
                 p->bn_stack = mt * d.k;
             }
@@ -641,7 +682,7 @@ cl_status cl_conv_forward(cl_plan* p, const float* d_x, float* d_y, void* d_ws, 
         std::lock_guard<std::mutex> lock(p->mu);
         CLB_CUDA(cudaSetDevice(p->device));
         order_after_previous(p, s);
-        forward(p, d_x, d_y, d_ws, s);
+        forward_chunked(p, d_x, d_y, d_ws, s, false);
         mark_done(p, s);
     });
 }
@@ -653,7 +694,7 @@ cl_status cl_conv_forward_nhwc(cl_plan* p, const float* d_x, float* d_y, void* d
         std::lock_guard<std::mutex> lock(p->mu);
         CLB_CUDA(cudaSetDevice(p->device));
         order_after_previous(p, s);
-        forward(p, d_x, d_y, d_ws, s, -1, true);
+        forward_chunked(p, d_x, d_y, d_ws, s, true);
         mark_done(p, s);
     });
 }

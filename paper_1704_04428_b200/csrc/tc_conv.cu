@@ -137,17 +137,34 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     // VGG conv5_x), neutral on the padded-row ones (profiles/r01_split_issue_sweep.txt)
     static const int env_split_issue = getenv("CLB_SPLIT_ISSUE") ? atoi(getenv("CLB_SPLIT_ISSUE")) : 1;
     p.split_issue = env_split_issue;
-    static const int env_l2_prefetch = getenv("CLB_L2_PREFETCH") ? atoi(getenv("CLB_L2_PREFETCH")) : 1;
+    // Weight-stationary B (single column tile, tiled B): CLB_B_RESIDENT=-1 takes it when it
+    // leaves room for >= 3 A stages, =1 whenever >= 2 remain.  Off by default: the A operand of
+    // the small-M layers is latency-bound on bytes in flight, and the resident B takes the smem
+    // that held them (VGG conv1_2 0.55 -> 0.64 ms; profiles/r01_l2_prefetch_bres_stacked.txt).
+    static const int env_bres = getenv("CLB_B_RESIDENT") ? atoi(getenv("CLB_B_RESIDENT")) : 0;
+    int resident_bytes = 0;
+    if (env_bres != 0 && p.b_resident >= 0 && b.mode == LOAD_TILED && (p.cols + p.bn - 1) / p.bn == 1) {
+        const int rb = k_iters * p.tps * b_rows * kRowBytes;
+        const int a_stage = tc_stage_bytes(0, p.tps);
+        const int min_stages = env_bres == 1 ? 2 : 3;   // (env_bres == -1: auto)
+        if (kSmemBudget - rb - 1024 - 256 >= min_stages * a_stage) resident_bytes = rb;
+    }
+    p.b_resident = resident_bytes > 0 ? 1 : 0;
+    if (p.b_resident) p.split_issue = 0;   // one producer warp: resident B first, then A per stage
+    // measured 5-12 % slower on every padded-row layer (the prefetches compete with the loads
+    // for the TMA unit; profiles/r01_l2_prefetch_bres_stacked.txt): off unless CLB_L2_PREFETCH=1
+    static const int env_l2_prefetch = getenv("CLB_L2_PREFETCH") ? atoi(getenv("CLB_L2_PREFETCH")) : 0;
     p.l2_prefetch = env_l2_prefetch;
     static const int env_smem = getenv("CLB_SMEM_KB") ? atoi(getenv("CLB_SMEM_KB")) * 1024 : 0;   // experiment knob
-    const int budget = env_smem > 0 ? env_smem : kSmemBudget;
+    const int budget = (env_smem > 0 ? env_smem : kSmemBudget) - resident_bytes;
+    const int stage_b_rows = p.b_resident ? 0 : b_rows;   // B rows carried per stage
     if (p.bps <= 0) {
         static const int env_bps = getenv("CLB_BPS") ? atoi(getenv("CLB_BPS")) : 0;   // experiment knob
         if (env_bps > 0) p.bps = env_bps;
-        else p.bps = (tc_num_stages(b_rows, p.tps, 2, budget) >= 3 && (p.chunk_iters % 2 == 0 || p.chunk_iters == k_iters)) ? 2 : 1;
+        else p.bps = (tc_num_stages(stage_b_rows, p.tps, 2, budget) >= 3 && (p.chunk_iters % 2 == 0 || p.chunk_iters == k_iters)) ? 2 : 1;
     }
-    p.stages = tc_num_stages(b_rows, p.tps, p.bps, budget);
-    while (p.stages < 2 && p.bps > 1) p.stages = tc_num_stages(b_rows, p.tps, --p.bps, budget);
+    p.stages = tc_num_stages(stage_b_rows, p.tps, p.bps, budget);
+    while (p.stages < 2 && p.bps > 1) p.stages = tc_num_stages(stage_b_rows, p.tps, --p.bps, budget);
     if (p.stages < 2) throw Error(2, "tile too large for a 2-stage pipeline");
     // chunk boundaries must be stage boundaries: chunk_iters a multiple of bps (a single-chunk
     // tile is exempt -- its only chunk starts the piece and ends at k_iters)
@@ -161,7 +178,7 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     if (p.num_tiles <= 0) return;
     p.chunks_per_tile = (k_iters + p.chunk_iters - 1) / p.chunk_iters;
     const long long total_chunks = (long long)p.num_tiles * p.chunks_per_tile;
-    const int smem = tc_smem_bytes(b_rows, p.tps, p.stages, p.bps);
+    const int smem = tc_smem_bytes(stage_b_rows, p.tps, p.stages, p.bps, resident_bytes);
     static bool configured[3] = {false, false, false};
     if (!configured[cg]) {
         if (cg == 2) {
@@ -288,11 +305,11 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
         }
         const double mhz = ns_sum > 0 ? 1e3 * cyc_sum / ns_sum : 0.0;
         fprintf(stderr,
-                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stack=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
+                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stack=%d bres=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
                 "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
                 "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us | "
                 "SM clock %.0f MHz (CTA cycles / CTA ns)\n",
-                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
+                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, p.b_resident, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
                 avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5], 100 * avg[11] / avg[5], avg[8], (t_out - t_in) * 1e-3,
                 (t_in_max - t_in) * 1e-3, ev_ms * 1e3, mhz);
         if (const char* dump = getenv("CLB_TRACE_DUMP")) {   // raw per-CTA records, appended

@@ -84,6 +84,10 @@ struct TcParams {
     int tps;                   // taps per stage (1 = one tap per stage)
     int split_issue;           // A and B TMA loads issued by two warps (0 and 3), 2 arrivals per stage
     int l2_prefetch;           // padded-row modes: L2-prefetch the next piece's A rows (CLB_L2_PREFETCH)
+    // weight-stationary: a single column tile's B (all k-iterations) is loaded once per CTA
+    // into shared memory and only A streams through the stages (B was ~40 % of the stage bytes
+    // on small-M layers, whose operand delivery bounds them)
+    int b_resident;
     int bps;                   // k-iterations ("sub-stages") per pipeline stage: one barrier
                                // round trip per bps TMA box pairs (chunk_iters % bps == 0)
     int a_row_shift;           // A row offset per tap group (padded row width Wp)
@@ -130,8 +134,8 @@ __host__ inline int tc_num_stages(int b_rows, int tps, int bps = 1, int budget =
     return s > 8 ? 8 : s;
 }
 
-__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages, int bps = 1) {
-    return 1024 /*align slack*/ + stages * bps * tc_stage_bytes(b_rows, tps) + 256 /*barriers*/;
+__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages, int bps = 1, int resident_bytes = 0) {
+    return 1024 /*align slack*/ + stages * bps * tc_stage_bytes(b_rows, tps) + resident_bytes + 256 /*barriers*/;
 }
 
 // TMEM accumulator buffers: 4 when they fit (BN <= 128), else ping-pong.  Extra buffers let
@@ -307,22 +311,28 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int b_rows = bn / CG;                   // B rows this CTA loads
     const int tps = p.tps;
     const int a_bytes = tc_a_bytes(tps);          // A region of one stage (128 + tps - 1 rows)
-    const int b_bytes = tps * b_rows * kRowBytes; // B rows of one stage (tps taps)
+    const bool bres = p.b_resident != 0;
+    const int b_unit = tps * b_rows * kRowBytes;  // B rows of one k-iteration (tps taps)
+    const int b_bytes = bres ? 0 : b_unit;        // ... carried in each stage unless resident
     const int stage_bytes = a_bytes + b_bytes;    // one sub-stage (one k-iteration)
     const int bps = p.bps;
     const int group_bytes = bps * stage_bytes;    // one pipeline stage
-    const uint32_t stage_tx = (uint32_t)((tc_a_box_rows(tps) + tps * b_rows) * kRowBytes);
+    const uint32_t stage_tx = (uint32_t)(tc_a_box_rows(tps) * kRowBytes + b_bytes);
+    const int k_iters = (p.taps / tps) * p.kblocks;   // k-iterations per tile
+    uint8_t* const bres_smem = smem + stages * group_bytes;   // resident B: [k-iteration][b_unit]
+    const int bres_bytes = bres ? k_iters * b_unit : 0;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;       // scheduling unit
     const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * group_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * group_bytes + bres_bytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + stages;
     uint64_t* tfull = bars + 2 * stages;        // [nbuf]
     uint64_t* tempty = bars + 2 * stages + 4;   // [nbuf]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 8);
+    uint64_t* bres_full = bars + 2 * stages + 8;   // resident B landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 9);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t ncols = tmem_cols_for(bn);
@@ -339,6 +349,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], CG * (kEpiThreads / 32));
         }
+        mbar_init(bres_full, 1);
         fence_barrier_init();
     }
     if (warp == 0 && lane_id() == 0) {
@@ -360,7 +371,6 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int k_iters = (p.taps / tps) * p.kblocks;   // stages per tile
     const int cpt = p.chunks_per_tile;
     const int ci = p.chunk_iters;
 
@@ -376,7 +386,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // warp 0 loads A and warp 3 loads B (TMA im2col boxes are slow to deliver from a single
         // issuing thread: tools/tma_probe3.cu 37 -> 43 B/clk per SM with two issuers).
         {
-            const bool do_a = warp == 0, do_b = warp == 3 || !p.split_issue;
+            const bool do_a = warp == 0, do_b = !bres && (warp == 3 || !p.split_issue);
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t a_tx = (uint32_t)(tc_a_box_rows(tps) * kRowBytes);
@@ -384,6 +394,28 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             long long w_empty = 0;
             const long long t_start = clock64();
             if (TRACE && lane_id() == 0 && warp == 0) p.trace[blockIdx.x * kTraceSlots + 8] = (unsigned long long)(t_start - t_entry);
+            if (bres && warp == 0) {
+                // weight-stationary: the (single) column tile's B for every k-iteration, once
+                if (elect_one()) {
+                    const OperandCoord cb = operand_coord(p.b_mode, p.b_tap3, (int)rank * b_rows, p.P, p.Q, p.pad);
+                    uint64_t* bar = bres_full;
+                    uint32_t lbar = 0;
+                    if constexpr (CG == 2) {
+                        lbar = mapa_shared(smem_u32(bres_full), 0);
+                        if (leader) mbar_arrive_expect_tx(bres_full, (uint32_t)(CG * bres_bytes));
+                    } else {
+                        mbar_arrive_expect_tx(bres_full, (uint32_t)bres_bytes);
+                    }
+                    for (int it = 0; it < k_iters; ++it) {
+                        const int g2 = p.tap_begin / tps + it / p.kblocks;
+                        const int kb2 = it - (it / p.kblocks) * p.kblocks;
+                        uint8_t* dst = bres_smem + it * b_unit;
+                        if constexpr (CG == 2) tma_load_3d_2sm(&map_b, lbar, dst, kb2 * p.row_elems, cb.c1, cb.tap3 ? g2 * tps : 0);
+                        else tma_load_3d(&map_b, bar, dst, kb2 * p.row_elems, cb.c1, cb.tap3 ? g2 * tps : 0);
+                    }
+                }
+                __syncwarp();
+            }
             Sched sch(p, unit, nunits);
             Piece pc;
             while (sch.next(pc)) {
@@ -517,6 +549,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint64_t st_step = (uint64_t)(group_bytes >> 4);
             const uint64_t sub_step = (uint64_t)(stage_bytes >> 4);
             const uint64_t b_off = (uint64_t)(a_bytes >> 4);
+            const uint64_t bres_desc = umma_desc_kmajor(smem_u32(bres_smem), kRowBytes);
+            const uint64_t bres_step = (uint64_t)(b_unit >> 4);
+            if (bres) mbar_wait(bres_full, 0);
             const uint64_t tap_b = (uint64_t)(b_rows * 8);
             long long w_full = 0, w_tempty = 0;
             const long long t_start = clock64();
@@ -529,13 +564,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 constexpr bool T1 = decltype(t1_c)::value;
                 // one k-iteration: the taps of the group x the format's MMAs; acc0 = 0 only for the
                 // chunk's first k-iteration (its first MMA starts the accumulator)
-                auto issue = [&](uint32_t d_tmem, uint64_t da0, uint32_t acc0) {
+                auto issue = [&](uint32_t d_tmem, uint64_t da0, uint64_t db0, uint32_t acc0) {
                     const int ntaps = T1 ? 1 : tps;
                     for (int t = 0; t < ntaps; ++t) {
                         // tap t of the group: A shifted by t rows (8 desc units of 16 B per
                         // 128 B row), B = the t-th tap's weight tile
                         const uint64_t da = da0 + (uint64_t)(t * 8);
-                        const uint64_t db = da0 + b_off + (uint64_t)t * tap_b;
+                        const uint64_t db = db0 + (uint64_t)t * tap_b;
                         const uint32_t first = (acc0 | (uint32_t)t) ? 1u : 0u;
                         if constexpr (PL == 2) {
                             // row = [hi 16 | lo 16]: k-step s (8 tf32 = 32 B = 2 desc units) of
@@ -597,10 +632,15 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         if (TRACE) w_full += clock64() - t0;
                         tc_fence_after();
                         if (elect_one()) {
-                            issue(d_tmem, dstage, it > c0 ? 1u : 0u);
-                            if (nsub > 1) issue(d_tmem, dstage + sub_step, 1u);
+                            // B of sub-stage sb: in the stage, or the resident copy of k-iteration it + sb
+                            auto dbs = [&](int sb) {
+                                return bres ? bres_desc + (uint64_t)(it + sb) * bres_step
+                                            : dstage + (uint64_t)sb * sub_step + b_off;
+                            };
+                            issue(d_tmem, dstage, dbs(0), it > c0 ? 1u : 0u);
+                            if (nsub > 1) issue(d_tmem, dstage + sub_step, dbs(1), 1u);
 #pragma unroll 1
-                            for (int sb = 2; sb < nsub; ++sb) issue(d_tmem, dstage + (uint64_t)sb * sub_step, 1u);
+                            for (int sb = 2; sb < nsub; ++sb) issue(d_tmem, dstage + (uint64_t)sb * sub_step, dbs(sb), 1u);
                             commit(&empty[stage]);   // frees the smem stage once its MMAs retire
                         }
                         __syncwarp();

@@ -374,7 +374,7 @@ print(json.dumps(out))
 '''
 
 
-@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked"])
+@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs"])
 def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     """The implicit kernel's tap-shared mode (zero-padded NHWC rows, one A box of 128+k-1 rows
     per kernel row, taps through row-shifted UMMA descriptors), forced on and off via
@@ -383,7 +383,10 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     "stacked" forces the tap-stacked variant (the k taps of a kernel row as column blocks of one
     MMA, shift-add across rows in the epilogue) wherever it applies (k = 3/5, k x M <= 256),
     including multi-chunk K, stream-K split tiles, M not a multiple of 16 and pad 0 / pad > k/2;
-    the launch trace proves both k = 3 and k = 5 instantiations ran."""
+    the launch trace proves both k = 3 and k = 5 instantiations ran.  "knobs" turns on the
+    measured-negative, default-off paths so they stay correct: weight-stationary B
+    (CLB_B_RESIDENT), the L2 prefetch of the next piece (CLB_L2_PREFETCH) and the L2-chunked
+    forward (CLB_L2_CHUNK_MB, one image per chunk here)."""
     import json
     import os
     import subprocess
@@ -394,12 +397,16 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     script.write_text(_PADDED_SCRIPT)
     env = {"1": dict(CLB_PADDED_ROWS="1"), "0": dict(CLB_PADDED_ROWS="0"),
            "stacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1"),
-           "unstacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="0")}[mode]
+           "unstacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="0"),
+           "knobs": dict(CLB_PADDED_ROWS="1", CLB_B_RESIDENT="1", CLB_L2_PREFETCH="1", CLB_L2_CHUNK_MB="0.01",
+                         CLB_TRACE="1")}[mode]
     r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, **env))
     assert r.returncode == 0, r.stderr[-3000:]
     if mode == "stacked":
         assert "stack=3" in r.stderr and "stack=5" in r.stderr, r.stderr[-2000:]
+    if mode == "knobs":
+        assert "bres=1" in r.stderr, r.stderr[-2000:]
     for res in json.loads(r.stdout.strip().splitlines()[-1]):
         if res["precision"] == "fp32":
             assert res["rel_l2"] <= FP32_L2 and res["max_rel"] <= FP32_MAX, (mode, res)
