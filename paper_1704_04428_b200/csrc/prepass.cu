@@ -86,6 +86,9 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
                                                                  int N, int C, int HW, int Cp, int H, int W, int Wp,
                                                                  int pad, FastDiv hwd, FastDiv wpd) {
     constexpr bool kSplit = PLANES == 2 || PLANES == kPlanesMixed;
+    // launched as a programmatic dependent of the previous kernel in the stream (typically the
+    // previous layer's contraction, whose output x is): nothing is touched before it completes
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ float tile[kSplitPx][33];                                   // hi (or raw for bf16 rows)
     __shared__ float tile_lo[PLANES == 2 ? kSplitPx : 1][33];              // 3xTF32 lo
     __shared__ uint32_t tile_bh[PLANES == kPlanesMixed ? kSplitPx : 1][17];  // mixed: bf16(hi) pairs
@@ -193,11 +196,25 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
 
 template <typename... Args>
 static void launch_split_kernel(int planes, dim3 grid, cudaStream_t s, Args... args) {
+    // Programmatic dependent launch: the prepass's launch and CTA ramp overlap the tail of the
+    // previous kernel in the stream (the previous layer's contraction); its griddepcontrol.wait
+    // keeps every memory access after that kernel's completion.  CLB_PDL_PREPASS=0 disables.
+    static const bool pdl = !(getenv("CLB_PDL_PREPASS") && atoi(getenv("CLB_PDL_PREPASS")) == 0);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
     switch (planes) {
-        case 1: nchw_to_nhwc_split_kernel<1><<<grid, 256, 0, s>>>(args...); break;
-        case 2: nchw_to_nhwc_split_kernel<2><<<grid, 256, 0, s>>>(args...); break;
-        case kPlanesBf16: nchw_to_nhwc_split_kernel<kPlanesBf16><<<grid, 256, 0, s>>>(args...); break;
-        default: nchw_to_nhwc_split_kernel<kPlanesMixed><<<grid, 256, 0, s>>>(args...);
+        case 1: CLB_CUDA(cudaLaunchKernelEx(&cfg, nchw_to_nhwc_split_kernel<1>, args...)); break;
+        case 2: CLB_CUDA(cudaLaunchKernelEx(&cfg, nchw_to_nhwc_split_kernel<2>, args...)); break;
+        case kPlanesBf16: CLB_CUDA(cudaLaunchKernelEx(&cfg, nchw_to_nhwc_split_kernel<kPlanesBf16>, args...)); break;
+        default: CLB_CUDA(cudaLaunchKernelEx(&cfg, nchw_to_nhwc_split_kernel<kPlanesMixed>, args...));
     }
 }
 
