@@ -151,6 +151,11 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     }
     p.b_resident = resident_bytes > 0 ? 1 : 0;
     if (p.b_resident) p.split_issue = 0;   // one producer warp: resident B first, then A per stage
+    // A boxes of alternate stages issued from two warps (0 and the idle TMEM-allocator warp 2):
+    // +0.5-2 % on the padded-row layers (VGG conv1_2 0.508 -> 0.499 ms), neutral on the TMA-im2col
+    // ones (profiles/r01_a_issuers_ab.txt).  CLB_A_ISSUERS=1 restores one A warp.
+    static const int env_a_iss = getenv("CLB_A_ISSUERS") ? atoi(getenv("CLB_A_ISSUERS")) : 2;
+    p.a_issuers = (env_a_iss == 2 && p.split_issue) ? 2 : 1;
     // measured 5-12 % slower on every padded-row layer (the prefetches compete with the loads
     // for the TMA unit; profiles/r01_l2_prefetch_bres_stacked.txt): off unless CLB_L2_PREFETCH=1
     static const int env_l2_prefetch = getenv("CLB_L2_PREFETCH") ? atoi(getenv("CLB_L2_PREFETCH")) : 0;
@@ -305,11 +310,11 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
         }
         const double mhz = ns_sum > 0 ? 1e3 * cyc_sum / ns_sum : 0.0;
         fprintf(stderr,
-                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stack=%d bres=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
+                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stack=%d bres=%d aiss=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
                 "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
                 "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us | "
                 "SM clock %.0f MHz (CTA cycles / CTA ns)\n",
-                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, p.b_resident, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
+                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, p.b_resident, p.a_issuers, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
                 avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5], 100 * avg[11] / avg[5], avg[8], (t_out - t_in) * 1e-3,
                 (t_in_max - t_in) * 1e-3, ev_ms * 1e3, mhz);
         if (const char* dump = getenv("CLB_TRACE_DUMP")) {   // raw per-CTA records, appended

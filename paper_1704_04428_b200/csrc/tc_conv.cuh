@@ -83,6 +83,7 @@ struct TcParams {
     // tap (i, j) reads row y*Wp + x + (i - pad)*Wp + (j - pad).
     int tps;                   // taps per stage (1 = one tap per stage)
     int split_issue;           // A and B TMA loads issued by two warps (0 and 3), 2 arrivals per stage
+    int a_issuers;             // 2: A loads of alternate stages from warps 0 and 2 (needs split_issue)
     int l2_prefetch;           // padded-row modes: L2-prefetch the next piece's A rows (CLB_L2_PREFETCH)
     // weight-stationary: a single column tile's B (all k-iterations) is loaded once per CTA
     // into shared memory and only A streams through the stages (B was ~40 % of the stage bytes
@@ -380,13 +381,18 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-    if (warp == 0 || (warp == 3 && p.split_issue)) {
+    if (warp == 0 || (warp == 3 && p.split_issue) || (warp == 2 && p.a_issuers == 2)) {
         // ------------------------------------------------------------ TMA producer ----
         // whole warp runs the (uniform) loop; one elected lane issues the TMA.  With split_issue
         // warp 0 loads A and warp 3 loads B (TMA im2col boxes are slow to deliver from a single
         // issuing thread: tools/tma_probe3.cu 37 -> 43 B/clk per SM with two issuers).
         {
-            const bool do_a = warp == 0, do_b = !bres && (warp == 3 || !p.split_issue);
+            const bool do_a = warp == 0 || warp == 2, do_b = !bres && (warp == 3 || !p.split_issue);
+            // two A issuers: warp 0 takes the even stages of the sequence, warp 2 the odd ones
+            // (each stage still gets exactly one A arrival); the B warp takes every stage
+            const uint32_t a_par = warp == 2 ? 1u : 0u;
+            const bool a_alt = do_a && p.a_issuers == 2;
+            uint32_t gs = 0;   // stage sequence number
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t a_tx = (uint32_t)(tc_a_box_rows(tps) * kRowBytes);
@@ -421,7 +427,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             while (sch.next(pc)) {
                 const int mt = pc.tile / p.n_col_tiles;
                 const int nt = pc.tile - mt * p.n_col_tiles;
-                if (p.l2_prefetch && do_a && p.a_mode == LOAD_TILED && p.a_row_shift) {
+                if (p.l2_prefetch && warp == 0 && p.a_mode == LOAD_TILED && p.a_row_shift) {
                     // padded-row modes: pull the NEXT piece's A rows (all kernel rows, all channel
                     // blocks) into L2 now, so its loads hit L2 instead of waiting on HBM latency
                     Sched nx = sch;
@@ -450,7 +456,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     const int kc = kb * p.row_elems;
                     // padded-row mode: tap (i, j) -> +i Wp + j (j = 0 at a group start when tps = k)
                     const int arow = p.a_row_shift ? ca.c1 + p.a_row_base + ti * p.a_row_shift + tj : ca.c1;
-                    if (sub == 0) {
+                    const bool mine = !a_alt || (gs & 1u) == a_par;
+                    if (sub == 0 && mine) {
                         const long long t0 = TRACE ? clock64() : 0;
                         mbar_wait(&empty[stage], phase ^ 1u);
                         if (TRACE) w_empty += clock64() - t0;
@@ -458,7 +465,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     // a stage holds min(bps, iterations left in the piece) sub-stages
                     const uint32_t txs = tx * (uint32_t)(it1 - it < bps ? it1 - it : bps);
                     uint8_t* a_st = smem + stage * group_bytes + sub * stage_bytes;
-                    if (elect_one()) {
+                    if (mine && elect_one()) {
                     if constexpr (CG == 2) {
                         const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
                         if (leader && sub == 0) mbar_arrive_expect_tx(&full[stage], txs);
@@ -490,6 +497,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     __syncwarp();
                     if (++sub == bps || it + 1 == it1) {
                         sub = 0;
+                        ++gs;
                         if (++stage == stages) {
                             stage = 0;
                             phase ^= 1u;

@@ -385,8 +385,8 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     including multi-chunk K, stream-K split tiles, M not a multiple of 16 and pad 0 / pad > k/2;
     the launch trace proves both k = 3 and k = 5 instantiations ran.  "knobs" turns on the
     measured-negative, default-off paths so they stay correct: weight-stationary B
-    (CLB_B_RESIDENT), the L2 prefetch of the next piece (CLB_L2_PREFETCH) and the L2-chunked
-    forward (CLB_L2_CHUNK_MB, one image per chunk here)."""
+    (CLB_B_RESIDENT), the L2 prefetch of the next piece (CLB_L2_PREFETCH), the L2-chunked
+    forward (CLB_L2_CHUNK_MB, one image per chunk here) and a single A-issuing warp."""
     import json
     import os
     import subprocess
@@ -399,7 +399,7 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
            "stacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1"),
            "unstacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="0"),
            "knobs": dict(CLB_PADDED_ROWS="1", CLB_B_RESIDENT="1", CLB_L2_PREFETCH="1", CLB_L2_CHUNK_MB="0.01",
-                         CLB_TRACE="1")}[mode]
+                         CLB_A_ISSUERS="1", CLB_TRACE="1")}[mode]
     r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, **env))
     assert r.returncode == 0, r.stderr[-3000:]
