@@ -1,8 +1,10 @@
 // tc_conv.cu -- host side of the tcgen05 engine: TMA tensor-map encoding (tiled and
 // im2col) and the persistent launch.  The kernel itself lives in tc_conv.cuh.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #define CLB_DEFINE_TC_KERNEL 1
@@ -229,6 +231,52 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     const bool balanced = (long long)(ceil_waves * units - p.num_tiles) * 20 <= (long long)ceil_waves * units;
     p.dp_tiles = balanced ? p.num_tiles : (waves >= 2 ? (waves - 1) * units : 0);
     p.sk_chunks = (p.num_tiles - p.dp_tiles) * p.chunks_per_tile;
+    // Stream-K unit count: with contiguous equal ranges over all units, a tile can straddle
+    // three units whenever a range is shorter than a tile, and a 3-piece tile's finisher waits
+    // for and adds two partials at the very end of the kernel (VGG conv5_1: those CTAs exit
+    // ~8 us after the 2-piece ones; CLB_TRACE_DUMP).  Pick the unit count u <= units that
+    // minimises ceil(chunks / u) + fixup(max pieces per tile), in chunk times: 2 pieces 3,
+    // each further piece +2 (profiles/r01_sk_units.txt).  CLB_SK_UNITS=0 keeps all units.
+    p.sk_units = units;
+    static const int env_sk = getenv("CLB_SK_UNITS") ? atoi(getenv("CLB_SK_UNITS")) : 1;
+    // (memoised per (chunks, chunks per tile, units): a plan's launches repeat the same shape)
+    thread_local std::unordered_map<unsigned long long, int> sk_memo;
+    const unsigned long long sk_key = ((unsigned long long)(unsigned)p.sk_chunks << 32) ^
+                                      ((unsigned long long)(unsigned)p.chunks_per_tile << 12) ^ (unsigned)units;
+    const auto sk_hit = sk_memo.find(sk_key);
+    if (env_sk != 0 && p.sk_chunks > 0 && sk_hit != sk_memo.end()) {
+        p.sk_units = sk_hit->second;
+    } else if (env_sk != 0 && p.sk_chunks > 0) {
+        const int cpt = p.chunks_per_tile, S = p.sk_chunks;
+        auto max_pieces = [&](int u) {
+            int worst = 1;
+            for (int t = 0; t * cpt < S; ++t) {
+                // unit holding chunk c: the b with chunk_start(b) <= c < chunk_start(b + 1)
+                auto unit_of = [&](int c) {
+                    int b = (int)(((long long)c * u) / S);
+                    while (b + 1 < u && chunk_start(b + 1, S, u) <= c) ++b;
+                    while (b > 0 && chunk_start(b, S, u) > c) --b;
+                    return b;
+                };
+                const int pcs = unit_of(std::min(S, (t + 1) * cpt) - 1) - unit_of(t * cpt) + 1;
+                if (pcs > worst) worst = pcs;
+            }
+            return worst;
+        };
+        auto cost = [&](int u) {
+            const int mp = max_pieces(u);
+            return (double)((S + u - 1) / u) + (mp <= 1 ? 0.0 : 3.0 + 2.0 * (mp - 2));
+        };
+        double best = cost(units);
+        for (int u = units - 1; u >= std::max(1, units - 24); --u) {
+            const double c = cost(u);
+            if (c < best - 1e-9) {
+                best = c;
+                p.sk_units = u;
+            }
+        }
+        sk_memo[sk_key] = p.sk_units;
+    }
     const int grid = units * cg;
     if (!p.partials || !p.flags) throw Error(6, "stream-K scratch missing");
     if (!p.flags_zeroed) CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));
@@ -310,11 +358,11 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
         }
         const double mhz = ns_sum > 0 ? 1e3 * cyc_sum / ns_sum : 0.0;
         fprintf(stderr,
-                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stack=%d bres=%d aiss=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d | producer %.0f cyc "
+                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stack=%d bres=%d aiss=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d sku=%d | producer %.0f cyc "
                 "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
                 "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us | "
                 "SM clock %.0f MHz (CTA cycles / CTA ns)\n",
-                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, p.b_resident, p.a_issuers, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, avg[0], 100 * avg[1] / avg[0],
+                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, p.b_resident, p.a_issuers, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, p.sk_units, avg[0], 100 * avg[1] / avg[0],
                 avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5], 100 * avg[11] / avg[5], avg[8], (t_out - t_in) * 1e-3,
                 (t_in_max - t_in) * 1e-3, ev_ms * 1e3, mhz);
         if (const char* dump = getenv("CLB_TRACE_DUMP")) {   // raw per-CTA records, appended

@@ -112,6 +112,8 @@ struct TcParams {
     int chunks_per_tile;       // ceil(k_iters / chunk_iters)
     int dp_tiles;              // tiles [0, dp_tiles) scheduled whole, round-robin over CTAs
     int sk_chunks;             // chunks of tiles [dp_tiles, num_tiles), split contiguously (stream-K)
+    int sk_units;              // scheduling units sharing the stream-K chunks (<= grid units; the
+                               // rest only run data-parallel tiles): chosen so no tile splits 3 ways
     float* partials;           // [gridDim.x][128][bn] tile-tail partial sums
     unsigned* flags;           // [gridDim.x], 0 at launch; 1 = partial ready (the finisher resets it)
     int flags_zeroed;          // flags are known to be 0 (self-resetting plan buffer): no memset
@@ -210,8 +212,8 @@ struct Sched {
     __device__ Sched(const TcParams& p, int b_, int grid_)
         : b(b_), grid(grid_), cpt(p.chunks_per_tile), dp_tiles(p.dp_tiles), i(0) {
         n_dp = dp_tiles > b ? (dp_tiles - b + grid - 1) / grid : 0;
-        g = chunk_start(b, p.sk_chunks, grid);
-        g_end = chunk_start(b + 1, p.sk_chunks, grid);
+        g = b < p.sk_units ? chunk_start(b, p.sk_chunks, p.sk_units) : 0;
+        g_end = b < p.sk_units ? chunk_start(b + 1, p.sk_chunks, p.sk_units) : 0;
     }
     __device__ bool next(Piece& pc) {
         if (i < n_dp) {
@@ -718,7 +720,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             int u_end = unit + 1;
             if (finisher) {
                 const int last = (pc.tile - p.dp_tiles) * cpt + cpt - 1;   // in stream-K chunk space
-                while (u_end < nunits && chunk_start(u_end, p.sk_chunks, nunits) <= last) ++u_end;
+                while (u_end < p.sk_units && chunk_start(u_end, p.sk_chunks, p.sk_units) <= last) ++u_end;
             }
             for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
                 const uint32_t buf = lg & (uint32_t)(nbuf - 1);
