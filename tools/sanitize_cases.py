@@ -9,7 +9,8 @@ from paper_1704_04428_b200 import rng
 cases = [("kn2row-gpu", (2, 16, 13, 13, 32, 3)), ("kn2row-gpu", (4, 64, 28, 28, 256, 3)),   # CG1 / CG2 + stream-K
          ("kn2row-explicit-gpu", (2, 8, 9, 9, 16, 3)), ("kn2col-gpu", (2, 8, 9, 9, 16, 5)),
          ("kn2row-acc-gpu", (2, 8, 9, 9, 16, 3)), ("im2col-gpu", (2, 3, 12, 12, 16, 3)),
-         ("direct-gpu", (2, 3, 20, 20, 16, 3)), ("conv1x1-gpu", (2, 24, 7, 7, 40, 1))]
+         ("direct-gpu", (2, 3, 20, 20, 16, 3)), ("conv1x1-gpu", (2, 24, 7, 7, 40, 1)),
+         ("kn2row-gpu", (3, 32, 19, 21, 48, 5)), ("kn2row-gpu", (2, 64, 30, 30, 64, 3))]   # tap-stacked k = 5 / 3 (CLB_STACKED)
 for method, (N, C, H, W, M, k) in cases:
     for prec in ("fp32", "bf16"):
         if method == "direct-gpu" and prec == "bf16":
