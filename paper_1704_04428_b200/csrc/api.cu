@@ -107,6 +107,7 @@ struct cl_plan {
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // optional instrumentation
     // chunked host pipeline (cl_conv_forward_host): copy-in / copy-out streams + per-chunk events
     cudaStream_t s_in = nullptr, s_out = nullptr;
+    bool shared_streams = false;   // s_in / s_out are the device's shared copy streams (not owned)
     static constexpr int kMaxChunks = 16;
     cudaEvent_t ev_in[kMaxChunks] = {}, ev_comp[kMaxChunks] = {}, ev_start = nullptr, ev_done = nullptr;
     bool host_started = false;   // a host-buffer call has been enqueued (ev_done is live)
@@ -726,8 +727,28 @@ cl_status host_forward(cl_plan* p, const float* h_x, float* h_y, void* stream, b
             }
         }
         if (!p->s_in) {
-            CLB_CUDA(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
-            CLB_CUDA(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+            // CLB_HOST_SHARED_STREAMS=1: copy streams shared by every plan of the device, so a
+            // multi-layer step's copies run in call order (layer 1's input first) instead of all
+            // layers' inputs sharing the H2D engine at once.  Measured mixed, so off by default:
+            // VGG16 e2e 25.9 -> 27.5 TFLOP/s, AlexNet 60.0 -> 59.1 (profiles/r01_e2e_shared_streams.txt).
+            static const bool shared = std::getenv("CLB_HOST_SHARED_STREAMS") &&
+                                       std::atoi(std::getenv("CLB_HOST_SHARED_STREAMS")) == 1;
+            if (shared) {
+                static std::mutex smu;
+                static cudaStream_t dev_in[64] = {}, dev_out[64] = {};
+                std::lock_guard<std::mutex> g(smu);
+                if (p->device < 0 || p->device >= 64) throw Error(CL_EINVAL, "device index out of range");
+                if (!dev_in[p->device]) {
+                    CLB_CUDA(cudaStreamCreateWithFlags(&dev_in[p->device], cudaStreamNonBlocking));
+                    CLB_CUDA(cudaStreamCreateWithFlags(&dev_out[p->device], cudaStreamNonBlocking));
+                }
+                p->s_in = dev_in[p->device];
+                p->s_out = dev_out[p->device];
+                p->shared_streams = true;
+            } else {
+                CLB_CUDA(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+                CLB_CUDA(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+            }
             for (int i = 0; i < cl_plan::kMaxChunks; ++i) {
                 CLB_CUDA(cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming));
                 CLB_CUDA(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming));
@@ -830,8 +851,10 @@ void cl_conv_destroy(cl_plan* p) {
     if (p->ev_last) cudaEventDestroy(p->ev_last);
     if (p->host_y) cudaFree(p->host_y);
     if (p->s_in) {
-        cudaStreamDestroy(p->s_in);
-        cudaStreamDestroy(p->s_out);
+        if (!p->shared_streams) {   // the device's shared copy streams outlive every plan
+            cudaStreamDestroy(p->s_in);
+            cudaStreamDestroy(p->s_out);
+        }
         for (int i = 0; i < cl_plan::kMaxChunks; ++i) {
             cudaEventDestroy(p->ev_in[i]);
             cudaEventDestroy(p->ev_comp[i]);
