@@ -95,6 +95,17 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* m, int32_t c0
                  : "memory");
 }
 
+// one contiguous global -> shared bulk copy (no tensor map), completion on an mbarrier
+__device__ __forceinline__ void bulk_copy_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem)),
+                 "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// order this thread's generic-proxy accesses with its subsequent async-proxy (TMA / bulk) ones
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, uint64_t* bar, void* smem, int32_t c0,
                                             int32_t c1, int32_t c2) {
     asm volatile(

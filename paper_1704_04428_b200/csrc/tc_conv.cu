@@ -239,6 +239,8 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     // each further piece +2 (profiles/r01_sk_units.txt).  CLB_SK_UNITS=0 keeps all units.
     p.sk_units = units;
     static const int env_sk = getenv("CLB_SK_UNITS") ? atoi(getenv("CLB_SK_UNITS")) : 1;
+    static const int env_fix = getenv("CLB_FIXUP_SMEM") ? atoi(getenv("CLB_FIXUP_SMEM")) : 1;
+    p.fixup_smem = env_fix != 0 ? 1 : 0;
     // (memoised per (chunks, chunks per tile, units): a plan's launches repeat the same shape)
     thread_local std::unordered_map<unsigned long long, int> sk_memo;
     const unsigned long long sk_key = ((unsigned long long)(unsigned)p.sk_chunks << 32) ^

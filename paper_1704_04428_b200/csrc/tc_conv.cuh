@@ -89,6 +89,7 @@ struct TcParams {
     // into shared memory and only A streams through the stages (B was ~40 % of the stage bytes
     // on small-M layers, whose operand delivery bounds them)
     int b_resident;
+    int fixup_smem;            // stream-K finisher stages partner partials in smem (bulk copy)
     int bps;                   // k-iterations ("sub-stages") per pipeline stage: one barrier
                                // round trip per bps TMA box pairs (chunk_iters % bps == 0)
     int a_row_shift;           // A row offset per tap group (padded row width Wp)
@@ -335,7 +336,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     uint64_t* tfull = bars + 2 * stages;        // [nbuf]
     uint64_t* tempty = bars + 2 * stages + 4;   // [nbuf]
     uint64_t* bres_full = bars + 2 * stages + 8;   // resident B landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 9);
+    uint64_t* fix_bar = bars + 2 * stages + 9;     // stream-K partial staged in smem (finisher)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 10);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t ncols = tmem_cols_for(bn);
@@ -353,6 +355,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             mbar_init(&tempty[a], CG * (kEpiThreads / 32));
         }
         mbar_init(bres_full, 1);
+        mbar_init(fix_bar, 1);
         fence_barrier_init();
     }
     if (warp == 0 && lane_id() == 0) {
@@ -789,13 +792,33 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             }
             if (finisher) {
                 // ---- finisher of a split tile: add the later pieces' partials in unit order ----
+                // This is the CTA's last piece and all its MMAs have completed, so the pipeline
+                // smem is idle: each partner's partial (one contiguous [col/4][row] float4 block)
+                // is staged there by ONE bulk copy and added from smem.  Per-thread global loads
+                // of the same block were latency-bound (~5 us per 128 KB partial at the tail of
+                // every split layer, CLB_TRACE_DUMP); CLB_FIXUP_SMEM=0 in the launcher keeps them.
+                const uint32_t pbytes = (uint32_t)(kTileM * bn * 4);
+                const bool staged = p.fixup_smem && pbytes <= (uint32_t)(stages * group_bytes);
+                uint32_t fph = 0;
                 for (int u2 = unit + 1; u2 < u_end; ++u2) {
-                    const float4* src = reinterpret_cast<const float4*>(p.partials) +
-                                        ((long long)(u2 * CG + (int)rank) * (bn >> 2) + (cbase >> 2)) * kTileM + trow;
+                    const float4* slot = reinterpret_cast<const float4*>(p.partials) +
+                                         (long long)(u2 * CG + (int)rank) * (bn >> 2) * kTileM;
+                    const float4* src = slot + (long long)(cbase >> 2) * kTileM + trow;
+                    if (staged) {
+                        epi_bar_sync();   // every epilogue thread is done with the previous partner's copy
+                        if (threadIdx.x == 4 * 32) {
+                            fence_proxy_async();   // acquired partial (generic) -> bulk read (async proxy)
+                            mbar_arrive_expect_tx(fix_bar, pbytes);
+                            bulk_copy_g2s(smem, slot, pbytes, fix_bar);
+                        }
+                        mbar_wait(fix_bar, fph);
+                        fph ^= 1u;
+                        src = reinterpret_cast<const float4*>(smem) + (cbase >> 2) * kTileM + trow;
+                    }
 #pragma unroll
                     for (int j = 0; j < 128; j += 4)
                         if (j < hcols) {
-                            const float4 v = __ldcg(src + (j >> 2) * kTileM);
+                            const float4 v = staged ? src[(j >> 2) * kTileM] : __ldcg(src + (j >> 2) * kTileM);
                             sum[j] += v.x;
                             sum[j + 1] += v.y;
                             sum[j + 2] += v.z;
