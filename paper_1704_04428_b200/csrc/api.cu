@@ -532,6 +532,17 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         const int P = (d.h + 2 * d.pad - d.k) / d.stride + 1;
         const int Q = (d.w + 2 * d.pad - d.k) / d.stride + 1;
         require(P > 0 && Q > 0, "cl_conv_plan: empty output");
+        // 32-bit engine coordinates (TMA box coordinates, tile rows): one plan covers fewer than
+        // 2^31 pixel rows in every layout it may use (padded grid + tap-stacked slack included);
+        // larger batches are split by the caller (or by torch.distributed batch sharding)
+        {
+            const long long rows = std::max({(long long)d.n * (d.h + d.pad + 1) * (d.w + d.pad + 1) + 8192,
+                                             (long long)d.n * P * Q, (long long)d.n * d.h * d.w,
+                                             (long long)d.k * d.k * d.m});
+            if (rows >= 0x7fffffffLL)
+                throw Error(CL_EUNSUPPORTED, "layer too large for one plan (" + std::to_string(rows) +
+                                                 " pixel rows >= 2^31): split the batch");
+        }
         cl_method m = resolve(d, method);
         if (d.k == 1 && (m == CL_METHOD_KN2ROW_EXPLICIT || m == CL_METHOD_KN2COL)) m = CL_METHOD_CONV1X1;
         if (m == CL_METHOD_DIRECT) {

@@ -63,8 +63,12 @@ def test_abi_basics_and_errors_without_gpu():
         h = ctypes.c_void_p()
         assert L.cl_conv_plan(ctypes.byref(d), 1, 0, 0, ctypes.byref(h)) == _lib.CL_EINVAL, c
         assert L.cl_last_error()
-    d = _lib.ConvDesc(n=1, c=3, h=8, w=8, m=4, k=3, pad=1, stride=1)
+    # more than 2^31 pixel rows in one plan (32-bit engine coordinates): refused before device work
+    d = _lib.ConvDesc(n=50000, c=3, h=224, w=224, m=4, k=3, pad=1, stride=1)
     h = ctypes.c_void_p()
+    assert L.cl_conv_plan(ctypes.byref(d), 1, 0, 0, ctypes.byref(h)) == _lib.CL_EUNSUPPORTED
+    assert b"split the batch" in L.cl_last_error()
+    d = _lib.ConvDesc(n=1, c=3, h=8, w=8, m=4, k=3, pad=1, stride=1)
     assert L.cl_conv_plan(ctypes.byref(d), 6, 0, 0, ctypes.byref(h)) == _lib.CL_EINVAL   # conv1x1 with k=3
     assert L.cl_conv_plan(ctypes.byref(d), 42, 0, 0, ctypes.byref(h)) == _lib.CL_EINVAL  # unknown method value
     assert b"unknown method" in L.cl_last_error()
