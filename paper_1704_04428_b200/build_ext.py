@@ -26,7 +26,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisib
                   "-I", str(ROOT / "include"), "-I", str(CSRC)]
 CU_SOURCES = ["prepass.cu", "tc_conv.cu", "direct.cu", "api.cu"]
 CXX_SOURCES = ["facade.cpp"]
-HEADERS = ["ptx.cuh", "tc_conv.cuh", "internal.hpp"]
+HEADERS = ["ptx.cuh", "tc_conv.cuh", "split_tile.cuh", "internal.hpp"]
 
 
 def _stale(obj: Path, deps) -> bool:

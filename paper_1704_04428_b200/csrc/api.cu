@@ -244,6 +244,41 @@ void mark_done(cl_plan* p, cudaStream_t s) {
 
 // n_images < 0: the plan's batch; otherwise a sub-batch (chunked host pipeline).
 // nhwc: channels-last input and output (implicit kn2row / conv1x1 / accumulating only).
+// Fused prepass: the implicit kn2row contraction converts its NCHW input itself in a phase 0
+// (tc_conv.cuh) instead of a separate prepass launch.  One CTA per SM converting with its eight
+// epilogue warps has ~6x less memory-level parallelism than the standalone kernel (6 CTAs of
+// 256 threads per SM), so it only pays where the launch it saves dominates: auto for inputs of
+// at most 2 MB (batch-1 layers: C1 30 -> 27 us), while every larger layer measured slower
+// (VGG conv1_2 0.72 -> 1.04 ms, AlexNet conv2 0.31 -> 0.34 ms; profiles/r01_fused_prepass.txt).
+// CLB_FUSED_PREPASS=0 / 1 forces it off / on.
+bool fused_prepass_enabled(const cl_conv_desc& d) {
+    static const int forced = std::getenv("CLB_FUSED_PREPASS") ? std::atoi(std::getenv("CLB_FUSED_PREPASS")) : -1;
+    if (forced == 0 || forced == 1) return forced == 1;
+    return (long long)d.n * d.c * d.h * d.w * 4 <= (2ll << 20);
+}
+
+// phase-0 parameters of the NCHW -> split conversion into `xs` (HW pixels per image; with
+// pad > 0 the shared-padding grid Hp x Wp of the tap-shared modes)
+void set_fused_prepass(TcParams& t, const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp) {
+    t.pre_force = std::getenv("CLB_FUSED_PREPASS") && std::atoi(std::getenv("CLB_FUSED_PREPASS")) == 1;
+    const int Hp = pad > 0 ? H + pad : 1, Wp = pad > 0 ? W + pad : H * W;
+    const int HW = pad > 0 ? Hp * Wp : H * W;
+    t.pre_x = x;
+    t.pre_xs = xs;
+    t.pre_n = N;
+    t.pre_c = C;
+    t.pre_hw = HW;
+    t.pre_cp = Cp;
+    t.pre_h = pad > 0 ? H : 1;
+    t.pre_w = pad > 0 ? W : HW;
+    t.pre_wp = Wp;
+    t.pre_pad = pad;
+    t.pre_hwd = make_fastdiv((uint32_t)HW);
+    t.pre_wpd = make_fastdiv((uint32_t)Wp);
+    t.pre_ntx = (int)(((long long)N * HW + kSplitPx - 1) / kSplitPx);
+    t.pre_nty = (Cp + 31) / 32;
+}
+
 // ev_first / ev_last_chunk: record the plan's profile events (begin / end) in this call (a
 // chunked forward brackets all of its chunks with one pair).
 void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images = -1, bool nhwc = false,
@@ -274,6 +309,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
     p->launches = 0;
     bool began = false;
     void* scratch = scratch_of(p, ws);
+    bool no_pdl = false;   // a non-kernel node (slack memsets) directly precedes the contraction
     auto tc = [&](const Operand& a, const Operand& b, TcParams t) {
         // PDL right after the prepass kernel (its launch_dependents trigger lets this
         // kernel's prologue overlap the prepass tail); an interposed profile event only
@@ -283,7 +319,9 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         began = true;
         set_scratch(t, scratch);
         t.flags = p->flags;
+        t.gbar = p->flags + kMaxGrid;
         t.flags_zeroed = 1;
+        if (no_pdl) t.pdl = 0;
         static const int forced_bn = [] {   // experiments: CLB_BN=<multiple of 16 <= 256>
             const char* e = std::getenv("CLB_BN");
             const int v = e ? std::atoi(e) : 0;
@@ -305,8 +343,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             else if (fixed_bn) break;
             else t.bn = round_up(t.bn / 2, 16);
         }
-        launch_tc(a, b, t, s, cg);
-        ++p->launches;
+        p->launches += launch_tc(a, b, t, s, cg);
     };
     auto tc_done = [&] {
         if (p->ev_end && ev_last_chunk) CLB_CUDA(cudaEventRecord(p->ev_end, s));
@@ -329,9 +366,14 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                     CLB_CUDA(cudaMemsetAsync(static_cast<char*>(xs) + ((size_t)lead + grid_rows) * rb, 0, (size_t)trail * rb, s));
                 }
                 void* grid = static_cast<char*>(xs) + (size_t)lead * rb;
-                if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
-                else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
-                ++p->launches;
+                const bool fused = !nhwc && p->method != CL_METHOD_KN2ROW_ACC && fused_prepass_enabled(d);
+                if (fused) {
+                    no_pdl = lead + trail > 0;
+                } else {
+                    if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                    else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                    ++p->launches;
+                }
                 Operand a = tiled(xs, grid_rows, 1, p->Cp, p->planes);
                 Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
                 TcParams t = base_params(p);
@@ -365,13 +407,17 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 t.out = y;
                 t.out_channels = d.m;
                 t.pq_out = p->P * p->Q;
+                if (fused) set_fused_prepass(t, x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp);
                 tc(a, b, t);
                 tc_done();
                 break;
             }
-            if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s);
-            else launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
-            ++p->launches;
+            const bool fused = !nhwc && p->method != CL_METHOD_KN2ROW_ACC && fused_prepass_enabled(d);
+            if (!fused) {
+                if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s);
+                else launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
+                ++p->launches;
+            }
             Operand a = implicit_a(p, xs);
             a.n = d.n;
             Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
@@ -396,6 +442,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             } else {
                 t.taps = taps;
                 t.tap_begin = 0;
+                if (fused) set_fused_prepass(t, x, xs, d.n, d.c, d.h, d.w, 0, p->Cp);
                 tc(a, b, t);
             }
             tc_done();
@@ -621,8 +668,9 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
                 p->bn_stack = mt * d.k;
             }
         }
-        if (cudaMalloc(&p->flags, kMaxGrid * sizeof(unsigned)) != cudaSuccess ||
-            cudaMemset(p->flags, 0, kMaxGrid * sizeof(unsigned)) != cudaSuccess) {
+        // stream-K flags [kMaxGrid] + the fused prepass's grid barrier (2 words), all self-resetting
+        if (cudaMalloc(&p->flags, (kMaxGrid + 8) * sizeof(unsigned)) != cudaSuccess ||
+            cudaMemset(p->flags, 0, (kMaxGrid + 8) * sizeof(unsigned)) != cudaSuccess) {
             cudaGetLastError();
             cudaFree(p->wpack);
             delete p;

@@ -34,8 +34,7 @@ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 //   4 = fp32-faithful "2xTF32 + 2xBF16": per 16 channels [hi 16 fp32 | hi 16 bf16 | lo 16 bf16]
 //       -- hi*Hi in two tf32 MMAs (exact products), the cross terms hi*Lo and lo*Hi in one
 //       bf16 MMA each (K = 16 per MMA: 4 MMA slots per 16 channels instead of 6)
-constexpr int kPlanesBf16 = 3;
-constexpr int kPlanesMixed = 4;
+// kPlanesBf16 = 3, kPlanesMixed = 4: split_tile.cuh (included through tc_conv.cuh)
 // hi|lo split formats: one 128-byte row unit per 16 channels
 __host__ __device__ inline bool is_split(int planes) { return planes == 2 || planes == kPlanesMixed; }
 // channel padding granularity of the split layout (one 128-byte row unit)
@@ -58,6 +57,9 @@ void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int
                        cudaStream_t s);
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
                                  cudaStream_t s);
+// the same conversion from explicit phase-0 parameters (the fused prepass's fallback)
+void launch_split_tiles(const float* x, void* xs, int N, int C, int HW, int Cp, int H, int W, int Wp, int pad,
+                        FastDiv hwd, FastDiv wpd, int planes, cudaStream_t s);
 // a[rows][K] -> as[rows][planes][Kp]
 void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s);
 // b[K][cols] -> bs[cols][planes][Kp]
@@ -100,7 +102,8 @@ struct Operand {
 
 void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int box_taps = 1);
 // p.partials / p.flags must point at tc_scratch_bytes() of device scratch (stream-K fixup).
-void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cta_group = 1);
+// returns the kernels launched: 1, or 2 when a requested fused prepass ran standalone instead
+int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cta_group = 1);
 constexpr int kMaxGrid = 160;   // >= SM count (148 on B200)
 constexpr int kMaxSplit = 10;   // max stream-K pieces per tile (latency-bound problems)
 size_t tc_scratch_bytes();

@@ -10,21 +10,10 @@
 
 namespace clb {
 
-__device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-
 // Row layout (see internal.hpp): the fp32-faithful split formats pack one 128 B unit per
 // 16-channel block ([hi fp32 | bf16 hi | bf16 lo] mixed, [hi | lo] fp32 for 3xTF32) so each
 // 128-byte TMA row carries both halves of 16 channels; TF32 rows hold hi only.
 // `base` = first element of the row (fp32 words, or bf16 elements for the BF16 mode).
-__device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
-    __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&t);
-}
-
 __device__ __forceinline__ void store_split(void* dstv, long long base, int c, int kp, int planes, float v) {
     (void)kp;
     if (planes == kPlanesBf16) {
@@ -58,137 +47,17 @@ __device__ __forceinline__ long long rowel(int planes, long long kp) { return is
 // pixel the tile's output is one contiguous run of 64 words (two 16-channel units for the split formats, 32
 // hi words for TF32), written by a warp as full 128-byte lines (lane = word).
 // grid (ceil(HW/128), ceil(Cp/32), N)
-constexpr int kSplitPx = 128;
-
-// Output pixel space: HW = Hp*Wp pixels per image; with pad > 0 this is the zero-padded
-// grid (Hp = H + pad, Wp = W + pad, data at (y, x), zeros after each row and image) the
-// tap-shared (padded-row) kernel mode reads.
-struct FastDiv {
-    uint32_t d, m, s;
-};
-
-static FastDiv make_fastdiv(uint32_t d) {
-    FastDiv f{d, 0, 0};
-    while ((1ull << f.s) < d) ++f.s;
-    f.m = (uint32_t)((((1ull << 32) * ((1ull << f.s) - d)) / d) + 1);
-    return f;
-}
-
-__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
-    return (__umulhi(n, f.m) + n) >> f.s;
-}
-
-// Templated on the operand format so every element is converted exactly once (in the load
-// phase, into shared tiles) and the write phase is plain 32-bit copies: converting per output
-// word made the mixed format's prepass issue-bound (IPC 3.2, DRAM 21 %, ncu on GoogLeNet 1x1).
+// (tile body, FastDiv: split_tile.cuh)
 template <int PLANES>
 __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xsv,
                                                                  int N, int C, int HW, int Cp, int H, int W, int Wp,
                                                                  int pad, FastDiv hwd, FastDiv wpd) {
-    constexpr bool kSplit = PLANES == 2 || PLANES == kPlanesMixed;
     // launched as a programmatic dependent of the previous kernel in the stream (typically the
     // previous layer's contraction, whose output x is): nothing is touched before it completes
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    __shared__ float tile[kSplitPx][33];                                   // hi (or raw for bf16 rows)
-    __shared__ float tile_lo[PLANES == 2 ? kSplitPx : 1][33];              // 3xTF32 lo
-    __shared__ uint32_t tile_bh[PLANES == kPlanesMixed ? kSplitPx : 1][17];  // mixed: bf16(hi) pairs
-    __shared__ uint32_t tile_bl[PLANES == kPlanesMixed ? kSplitPx : 1][17];  // mixed: bf16(lo) pairs
-    // pixels are flattened over (image, pixel): a tile may straddle two images, so small maps
-    // (13 x 13 = 169 pixels) do not leave most of a second 128-pixel tile idle
-    const long long NP = (long long)N * HW;
-    const long long g0 = (long long)blockIdx.x * kSplitPx;
-    const int c0 = blockIdx.y * 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long plane = (long long)H * W;
-    long long src[4];                       // element offset of channel 0 of this pixel, or -1
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-        const long long gp = g0 + lane + 32 * h;
-        src[h] = -1;
-        if (gp < NP) {
-            // multiply-shift divisions (host-computed magics); 64-bit divide only past 2^31 pixels
-            const int n = NP <= 0x7fffffffLL ? (int)fdiv((uint32_t)gp, hwd) : (int)(gp / HW);
-            const int pix = (int)(gp - (long long)n * HW);
-            int sp = pix;
-            if (pad != 0) {
-                const int yy = (int)fdiv((uint32_t)pix, wpd), xx = pix - yy * Wp;
-                sp = (yy < H && xx < W) ? yy * W + xx : -1;
-            }
-            if (sp >= 0) src[h] = (long long)n * C * plane + sp;
-        }
-    }
-    // thread (warp, lane) loads channels {2w, 2w+1, 2w+16, 2w+17} of pixels lane + 32 h: each
-    // warp load is 32 consecutive pixels of one channel plane (128 B), and the thread owns
-    // adjacent channel pairs, so the mixed format's bf16 halves go to smem as one 32-bit word
-    float v[4][4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int c = c0 + 2 * warp + (r & 1) + 16 * (r >> 1);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) v[r][h] = (c < C && src[h] >= 0) ? __ldg(x + src[h] + (long long)c * plane) : 0.0f;
-    }
-#pragma unroll
-    for (int r = 0; r < 4; r += 2) {
-        const int cc = 2 * warp + 16 * (r >> 1);      // even channel within the tile; pair (cc, cc+1)
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const int px = lane + 32 * h;
-            if (PLANES == kPlanesBf16) {
-                tile[px][cc] = v[r][h];
-                tile[px][cc + 1] = v[r + 1][h];
-            } else {
-                const float h0 = tf32_rna(v[r][h]), h1 = tf32_rna(v[r + 1][h]);
-                tile[px][cc] = h0;
-                tile[px][cc + 1] = h1;
-                if (PLANES == 2) {
-                    tile_lo[px][cc] = v[r][h] - h0;
-                    tile_lo[px][cc + 1] = v[r + 1][h] - h1;
-                }
-                if (PLANES == kPlanesMixed) {
-                    tile_bh[px][cc >> 1] = bf16x2_bits(h0, h1);
-                    tile_bl[px][cc >> 1] = bf16x2_bits(v[r][h] - h0, v[r + 1][h] - h1);
-                }
-            }
-        }
-    }
-    __syncthreads();
-    const long long row_words = rowel(PLANES, Cp);
-    const int nch = Cp - c0 < 32 ? Cp - c0 : 32;        // channels of this tile inside the padded row
-    if (PLANES == kPlanesBf16) {                        // bf16 rows: lane = channel
-        __nv_bfloat16* xb = static_cast<__nv_bfloat16*>(xsv);
-        for (int pp = warp; pp < kSplitPx; pp += 8) {
-            const long long gp = g0 + pp;
-            if (gp >= NP) break;
-            if (lane < nch) xb[gp * row_words + c0 + lane] = __float2bfloat16_rn(tile[pp][lane]);
-        }
-        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-        return;
-    }
-    const int out_words = kSplit ? 2 * nch : nch;
-    uint32_t* xs = static_cast<uint32_t*>(xsv);
-    // write phase: every lane stores 4 consecutive words of one pixel row (16 B), so a warp
-    // instruction covers 2 pixel rows (split formats, 64 words each) or 4 (TF32, 32 words)
-    constexpr int kLanesPx = (kSplit ? 64 : 32) / 4;
-    constexpr int kPxPerIter = 32 / kLanesPx;
-    const int sub = lane / kLanesPx, o = (lane % kLanesPx) * 4;
-    for (int pp0 = warp * kPxPerIter; pp0 < kSplitPx; pp0 += 8 * kPxPerIter) {
-        const int pp = pp0 + sub;
-        const long long gp = g0 + pp;
-        if (gp >= NP || o >= out_words) continue;
-        uint32_t* dst = xs + gp * row_words + (long long)(kSplit ? 2 : 1) * c0 + o;
-        const int u = o >> 5, w = o & 31;
-        const uint32_t* srow;
-        if (PLANES == 2) {                               // unit u = [hi 16 | lo 16]
-            srow = w < 16 ? reinterpret_cast<const uint32_t*>(&tile[pp][u * 16 + w])
-                          : reinterpret_cast<const uint32_t*>(&tile_lo[pp][u * 16 + w - 16]);
-        } else if (PLANES == kPlanesMixed) {             // unit u = [hi 16 fp32 | bf16 hi 16 | bf16 lo 16]
-            srow = w < 16 ? reinterpret_cast<const uint32_t*>(&tile[pp][u * 16 + w])
-                          : (w < 24 ? &tile_bh[pp][u * 8 + (w - 16)] : &tile_bl[pp][u * 8 + (w - 24)]);
-        } else {
-            srow = reinterpret_cast<const uint32_t*>(&tile[pp][o]);
-        }
-        *reinterpret_cast<uint4*>(dst) = make_uint4(srow[0], srow[1], srow[2], srow[3]);
-    }
+    __shared__ SplitSmem<PLANES> sm;
+    split_tile<PLANES, false>(x, xsv, N, C, HW, Cp, H, W, Wp, pad, hwd, wpd, (int)blockIdx.x, (int)blockIdx.y,
+                              (int)threadIdx.x, sm);
     // let a programmatically dependent consumer (the tcgen05 kernel) start its prologue;
     // its griddepcontrol.wait still waits for this grid's completion and memory flush
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -223,6 +92,13 @@ void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, i
     dim3 grid((unsigned)(((long long)N * HW + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
     launch_split_kernel(planes, grid, s, x, xs, N, C, HW, Cp, 1, HW, HW, 0, make_fastdiv((uint32_t)HW),
                         make_fastdiv((uint32_t)HW));
+    CLB_CUDA(cudaGetLastError());
+}
+
+void launch_split_tiles(const float* x, void* xs, int N, int C, int HW, int Cp, int H, int W, int Wp, int pad,
+                        FastDiv hwd, FastDiv wpd, int planes, cudaStream_t s) {
+    dim3 grid((unsigned)(((long long)N * HW + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
+    launch_split_kernel(planes, grid, s, x, xs, N, C, HW, Cp, H, W, Wp, pad, hwd, wpd);
     CLB_CUDA(cudaGetLastError());
 }
 

@@ -1,0 +1,170 @@
+// split_tile.cuh -- one tile of the NCHW fp32 -> split-operand prepass (128 pixels x 32
+// channels), shared by the standalone prepass kernel (prepass.cu) and the contraction kernel's
+// fused phase 0 (tc_conv.cuh): hi = rna_tf32(x), lo = x - hi (exact in fp32), written as the
+// 128-byte row units the engine's TMA boxes read.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+
+namespace clb {
+
+constexpr int kPlanesBf16 = 3;    // precision codes, see internal.hpp
+constexpr int kPlanesMixed = 4;
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
+    __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&t);
+}
+
+constexpr int kSplitPx = 128;
+
+// Output pixel space: HW = Hp*Wp pixels per image; with pad > 0 this is the zero-padded
+// grid (Hp = H + pad, Wp = W + pad, data at (y, x), zeros after each row and image) the
+// tap-shared (padded-row) kernel mode reads.
+struct FastDiv {
+    uint32_t d, m, s;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f{d, 0, 0};
+    while ((1ull << f.s) < d) ++f.s;
+    f.m = (uint32_t)((((1ull << 32) * ((1ull << f.s) - d)) / d) + 1);
+    return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+    return (__umulhi(n, f.m) + n) >> f.s;
+}
+
+// tile staging: hi (or raw for bf16 rows), 3xTF32 lo, mixed-format bf16(hi) / bf16(lo) pairs
+template <int PLANES>
+struct SplitSmem {
+    float hi[kSplitPx][33];
+    float lo[PLANES == 2 ? kSplitPx : 1][33];
+    uint32_t bh[PLANES == kPlanesMixed ? kSplitPx : 1][17];
+    uint32_t bl[PLANES == kPlanesMixed ? kSplitPx : 1][17];
+};
+
+// the 256 threads converting a tile: a whole CTA (standalone) or the contraction kernel's
+// eight epilogue warps (fused phase 0, named barrier 1)
+template <bool FUSED>
+__device__ __forceinline__ void split_sync() {
+    if (FUSED) asm volatile("bar.sync 1, 256;" ::: "memory");
+    else __syncthreads();
+}
+
+// Templated on the operand format so every element is converted exactly once (in the load
+// phase, into shared tiles) and the write phase is plain 32-bit copies: converting per output
+// word made the mixed format's prepass issue-bound (IPC 3.2, DRAM 21 %, ncu on GoogLeNet 1x1).
+// Tile (bx, by) = pixels [128 bx, 128 bx + 128) flattened over (image, pixel) x channels
+// [32 by, 32 by + 32); tid in [0, 256).
+template <int PLANES, bool FUSED>
+__device__ __forceinline__ void split_tile(const float* __restrict__ x, void* __restrict__ xsv, int N, int C, int HW,
+                                           int Cp, int H, int W, int Wp, int pad, const FastDiv& hwd,
+                                           const FastDiv& wpd, int bx, int by, int tid, SplitSmem<PLANES>& sm) {
+    constexpr bool kSplit = PLANES == 2 || PLANES == kPlanesMixed;
+    // pixels are flattened over (image, pixel): a tile may straddle two images, so small maps
+    // (13 x 13 = 169 pixels) do not leave most of a second 128-pixel tile idle
+    const long long NP = (long long)N * HW;
+    const long long g0 = (long long)bx * kSplitPx;
+    const int c0 = by * 32;
+    const int lane = tid & 31, warp = tid >> 5;
+    const long long plane = (long long)H * W;
+    long long src[4];                       // element offset of channel 0 of this pixel, or -1
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const long long gp = g0 + lane + 32 * h;
+        src[h] = -1;
+        if (gp < NP) {
+            // multiply-shift divisions (host-computed magics); 64-bit divide only past 2^31 pixels
+            const int n = NP <= 0x7fffffffLL ? (int)fdiv((uint32_t)gp, hwd) : (int)(gp / HW);
+            const int pix = (int)(gp - (long long)n * HW);
+            int sp = pix;
+            if (pad != 0) {
+                const int yy = (int)fdiv((uint32_t)pix, wpd), xx = pix - yy * Wp;
+                sp = (yy < H && xx < W) ? yy * W + xx : -1;
+            }
+            if (sp >= 0) src[h] = (long long)n * C * plane + sp;
+        }
+    }
+    // thread (warp, lane) loads channels {2w, 2w+1, 2w+16, 2w+17} of pixels lane + 32 h: each
+    // warp load is 32 consecutive pixels of one channel plane (128 B), and the thread owns
+    // adjacent channel pairs, so the mixed format's bf16 halves go to smem as one 32-bit word
+    float v[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int c = c0 + 2 * warp + (r & 1) + 16 * (r >> 1);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) v[r][h] = (c < C && src[h] >= 0) ? __ldg(x + src[h] + (long long)c * plane) : 0.0f;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; r += 2) {
+        const int cc = 2 * warp + 16 * (r >> 1);      // even channel within the tile; pair (cc, cc+1)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int px = lane + 32 * h;
+            if (PLANES == kPlanesBf16) {
+                sm.hi[px][cc] = v[r][h];
+                sm.hi[px][cc + 1] = v[r + 1][h];
+            } else {
+                const float h0 = tf32_rna(v[r][h]), h1 = tf32_rna(v[r + 1][h]);
+                sm.hi[px][cc] = h0;
+                sm.hi[px][cc + 1] = h1;
+                if (PLANES == 2) {
+                    sm.lo[px][cc] = v[r][h] - h0;
+                    sm.lo[px][cc + 1] = v[r + 1][h] - h1;
+                }
+                if (PLANES == kPlanesMixed) {
+                    sm.bh[px][cc >> 1] = bf16x2_bits(h0, h1);
+                    sm.bl[px][cc >> 1] = bf16x2_bits(v[r][h] - h0, v[r + 1][h] - h1);
+                }
+            }
+        }
+    }
+    split_sync<FUSED>();
+    const long long row_words = kSplit ? 2LL * Cp : (long long)Cp;
+    const int nch = Cp - c0 < 32 ? Cp - c0 : 32;        // channels of this tile inside the padded row
+    if (PLANES == kPlanesBf16) {                        // bf16 rows: lane = channel
+        __nv_bfloat16* xb = static_cast<__nv_bfloat16*>(xsv);
+        for (int pp = warp; pp < kSplitPx; pp += 8) {
+            const long long gp = g0 + pp;
+            if (gp >= NP) break;
+            if (lane < nch) xb[gp * row_words + c0 + lane] = __float2bfloat16_rn(sm.hi[pp][lane]);
+        }
+        return;
+    }
+    const int out_words = kSplit ? 2 * nch : nch;
+    uint32_t* xs = static_cast<uint32_t*>(xsv);
+    // write phase: every lane stores 4 consecutive words of one pixel row (16 B), so a warp
+    // instruction covers 2 pixel rows (split formats, 64 words each) or 4 (TF32, 32 words)
+    constexpr int kLanesPx = (kSplit ? 64 : 32) / 4;
+    constexpr int kPxPerIter = 32 / kLanesPx;
+    const int sub = lane / kLanesPx, o = (lane % kLanesPx) * 4;
+    for (int pp0 = warp * kPxPerIter; pp0 < kSplitPx; pp0 += 8 * kPxPerIter) {
+        const int pp = pp0 + sub;
+        const long long gp = g0 + pp;
+        if (gp >= NP || o >= out_words) continue;
+        uint32_t* dst = xs + gp * row_words + (long long)(kSplit ? 2 : 1) * c0 + o;
+        const int u = o >> 5, w = o & 31;
+        const uint32_t* srow;
+        if (PLANES == 2) {                               // unit u = [hi 16 | lo 16]
+            srow = w < 16 ? reinterpret_cast<const uint32_t*>(&sm.hi[pp][u * 16 + w])
+                          : reinterpret_cast<const uint32_t*>(&sm.lo[pp][u * 16 + w - 16]);
+        } else if (PLANES == kPlanesMixed) {             // unit u = [hi 16 fp32 | bf16 hi 16 | bf16 lo 16]
+            srow = w < 16 ? reinterpret_cast<const uint32_t*>(&sm.hi[pp][u * 16 + w])
+                          : (w < 24 ? &sm.bh[pp][u * 8 + (w - 16)] : &sm.bl[pp][u * 8 + (w - 24)]);
+        } else {
+            srow = reinterpret_cast<const uint32_t*>(&sm.hi[pp][o]);
+        }
+        *reinterpret_cast<uint4*>(dst) = make_uint4(srow[0], srow[1], srow[2], srow[3]);
+    }
+}
+
+}  // namespace clb

@@ -85,7 +85,7 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int b
                            " failed with CUresult " + std::to_string((int)r));
 }
 
-void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cg) {
+int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cg) {
     if (cg != 1 && cg != 2) throw Error(6, "cta group must be 1 or 2");
     if (p.bn % 16 != 0 || p.bn < 16 || p.bn > 256) throw Error(6, "tile N must be a multiple of 16 in [16,256]");
     const int unit = kRowBytes / elem_bytes(a.planes);
@@ -182,10 +182,16 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
     const int row_tiles = (p.rows + tile_m - 1) / tile_m;
     p.n_col_tiles = (p.cols + p.bn - 1) / p.bn;
     p.num_tiles = row_tiles * p.n_col_tiles;
-    if (p.num_tiles <= 0) return;
+    if (p.num_tiles <= 0) return 0;
     p.chunks_per_tile = (k_iters + p.chunk_iters - 1) / p.chunk_iters;
     const long long total_chunks = (long long)p.num_tiles * p.chunks_per_tile;
     const int smem = tc_smem_bytes(stage_b_rows, p.tps, p.stages, p.bps, resident_bytes);
+    if (p.pre_x) {   // the fused prepass stages its tiles in the pipeline smem
+        const int need = p.planes == 4 ? (int)sizeof(SplitSmem<4>) : p.planes == 2 ? (int)sizeof(SplitSmem<2>)
+                                                                                    : (int)sizeof(SplitSmem<1>);
+        if (p.stages * p.bps * tc_stage_bytes(stage_b_rows, p.tps) < need || !p.gbar)
+            throw Error(6, "fused prepass: pipeline smem too small for a conversion tile");
+    }
     static bool configured[3] = {false, false, false};
     if (!configured[cg]) {
         if (cg == 2) {
@@ -280,6 +286,16 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
         sk_memo[sk_key] = p.sk_units;
     }
     const int grid = units * cg;
+    int launched = 1;
+    if (p.pre_x && !p.pre_force && (long long)p.pre_ntx * p.pre_nty > grid) {
+        // the fused conversion would give CTAs several tiles each at 1/6 of the standalone
+        // kernel's memory parallelism (sweep k1: 30 -> 34 us): convert standalone, then PDL
+        launch_split_tiles(p.pre_x, p.pre_xs, p.pre_n, p.pre_c, p.pre_hw, p.pre_cp, p.pre_h, p.pre_w, p.pre_wp,
+                           p.pre_pad, p.pre_hwd, p.pre_wpd, p.planes, s);
+        p.pre_x = nullptr;
+        p.pdl = 1;
+        launched = 2;
+    }
     if (!p.partials || !p.flags) throw Error(6, "stream-K scratch missing");
     if (!p.flags_zeroed) CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));
     // PDL only when nothing was enqueued in between (the memset would be the predecessor)
@@ -395,6 +411,7 @@ void launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, i
                 "%llu, wait tmem %llu) | epilogue %llu (wait tfull %llu, store %llu, fixup wait %llu) cyc\n",
                 slow, (r[10] - t_in) * 1e-3, r[0], r[1], rl[2], rl[3], rl[4], r[5], r[6], r[7], r[11]);
     }
+    return launched;
 }
 
 size_t tc_scratch_bytes() {

@@ -36,6 +36,7 @@
 #include <cuda.h>
 
 #include "ptx.cuh"
+#include "split_tile.cuh"
 
 namespace clb {
 
@@ -120,6 +121,16 @@ struct TcParams {
     int flags_zeroed;          // flags are known to be 0 (self-resetting plan buffer): no memset
     int pdl;                   // launched as a programmatic dependent: wait before touching inputs
     unsigned long long* trace; // diagnostics (CLB_TRACE=1): per-CTA role wait cycles, else null
+    // fused NCHW -> split prepass (phase 0, pre_x != null): the eight epilogue warps of every
+    // CTA convert tiles of 128 pixels x 32 channels (split_tile.cuh) through the still idle
+    // pipeline smem, then a grid barrier publishes the split operand to every CTA's TMA loads
+    const float* pre_x;
+    void* pre_xs;
+    int pre_n, pre_c, pre_hw, pre_cp, pre_h, pre_w, pre_wp, pre_pad;
+    FastDiv pre_hwd, pre_wpd;
+    int pre_ntx, pre_nty;      // tile grid (pixels / 128, padded channels / 32)
+    unsigned* gbar;            // [0] arrivals, [1] sense: self-resetting, plan-owned, zeroed once
+    int pre_force;             // fuse even when CTAs would convert several tiles each
 };
 
 // Contiguous chunk range of CTA b: [chunk_start(b), chunk_start(b+1)).
@@ -197,6 +208,27 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 
 __device__ __forceinline__ void epi_bar_sync() {   // the 8 epilogue warps only
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
+
+// Sense-reversal grid barrier over a persistent grid (every CTA resident: one per SM).  The
+// arrival count returns to 0 and the sense flips once per barrier, so the two words stay valid
+// across launches without a memset.  __threadfence before the arrival publishes the CTA's
+// writes (bar.sync orders its other threads' writes before thread 0's fence).
+__device__ __forceinline__ void grid_barrier(unsigned* gbar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned target = ld_acquire_u32(gbar + 1) ^ 1u;
+        __threadfence();
+        if (atomicAdd(gbar, 1u) == nblocks - 1u) {
+            *reinterpret_cast<volatile unsigned*>(gbar) = 0u;
+            st_release_u32(gbar + 1, target);
+        } else {
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_u32(gbar + 1) != target)
+                if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+        }
+    }
+    __syncthreads();
 }
 
 // A piece = the part of one tile's chunk range [c_lo, c_hi) that falls in this CTA's range.
@@ -384,6 +416,32 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // prefetch) overlapped the previous kernel's tail; inputs (the split operand, output
     // buffers) are only touched after this point.
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    if (p.pre_x) {
+        // ---- phase 0: fused NCHW -> split prepass (replaces the standalone prepass launch) ----
+        if (warp >= 4) {
+            const int tid = (int)threadIdx.x - 4 * 32;
+            const int ntiles = p.pre_ntx * p.pre_nty;
+            auto run_pre = [&](auto pl_c) {
+                constexpr int PL = decltype(pl_c)::value;
+                SplitSmem<PL>& sm = *reinterpret_cast<SplitSmem<PL>*>(smem);
+                for (int t = (int)blockIdx.x; t < ntiles; t += (int)gridDim.x) {
+                    const int by = t / p.pre_ntx, bx = t - by * p.pre_ntx;
+                    split_tile<PL, true>(p.pre_x, p.pre_xs, p.pre_n, p.pre_c, p.pre_hw, p.pre_cp, p.pre_h, p.pre_w,
+                                         p.pre_wp, p.pre_pad, p.pre_hwd, p.pre_wpd, bx, by, tid, sm);
+                    epi_bar_sync();   // the next tile overwrites the staging
+                }
+            };
+            if (planes == 4) run_pre(std::integral_constant<int, 4>{});
+            else if (planes == 2) run_pre(std::integral_constant<int, 2>{});
+            else if (planes == 3) run_pre(std::integral_constant<int, 3>{});
+            else run_pre(std::integral_constant<int, 1>{});
+        }
+        // generic smem / global writes above -> async-proxy (TMA) writes and reads below
+        fence_proxy_async();
+        grid_barrier(p.gbar, gridDim.x);
+        fence_proxy_async();
+    }
 
     if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0 || (warp == 3 && p.split_issue) || (warp == 2 && p.a_issuers == 2)) {
