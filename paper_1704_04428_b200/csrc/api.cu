@@ -244,23 +244,26 @@ void mark_done(cl_plan* p, cudaStream_t s) {
 
 // n_images < 0: the plan's batch; otherwise a sub-batch (chunked host pipeline).
 // nhwc: channels-last input and output (implicit kn2row / conv1x1 / accumulating only).
-// Fused prepass: the implicit kn2row contraction converts its NCHW input itself in a phase 0
-// (tc_conv.cuh) instead of a separate prepass launch.  One CTA per SM converting with its eight
-// epilogue warps has ~6x less memory-level parallelism than the standalone kernel (6 CTAs of
-// 256 threads per SM), so it only pays where the launch it saves dominates: auto for inputs of
-// at most 2 MB (batch-1 layers: C1 30 -> 27 us), while every larger layer measured slower
-// (VGG conv1_2 0.72 -> 1.04 ms, AlexNet conv2 0.31 -> 0.34 ms; profiles/r01_fused_prepass.txt).
-// CLB_FUSED_PREPASS=0 / 1 forces it off / on.
+// Fused prepass (opt-in): the implicit kn2row contraction converts its NCHW input itself in a
+// phase 0 (tc_conv.cuh) instead of a separate prepass launch.  One CTA per SM converting with its
+// eight epilogue warps has ~1/6 of the standalone kernel's memory-level parallelism (6 CTAs of
+// 256 threads per SM), so it is 10-45 % slower on every large layer (VGG conv1_2 0.72 -> 1.04
+// ms); on batch-1 layers it saves a launch's host overhead in eager calls (C1 32 -> 26 us) but
+// costs ~2 us of device time under CUDA-graph replay (C1 17 -> 19 us), which is the device-side
+// measure the report uses -- so it is off by default (profiles/r01_fused_prepass.txt).
+// CLB_FUSED_PREPASS=1: fuse inputs <= 2 MB when every CTA converts at most one tile (else the
+// launcher runs the standalone prepass); =2: always.
 bool fused_prepass_enabled(const cl_conv_desc& d) {
-    static const int forced = std::getenv("CLB_FUSED_PREPASS") ? std::atoi(std::getenv("CLB_FUSED_PREPASS")) : -1;
-    if (forced == 0 || forced == 1) return forced == 1;
-    return (long long)d.n * d.c * d.h * d.w * 4 <= (2ll << 20);
+    static const int mode = std::getenv("CLB_FUSED_PREPASS") ? std::atoi(std::getenv("CLB_FUSED_PREPASS")) : 0;
+    if (mode == 2) return true;
+    if (mode == 1) return (long long)d.n * d.c * d.h * d.w * 4 <= (2ll << 20);
+    return false;
 }
 
 // phase-0 parameters of the NCHW -> split conversion into `xs` (HW pixels per image; with
 // pad > 0 the shared-padding grid Hp x Wp of the tap-shared modes)
 void set_fused_prepass(TcParams& t, const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp) {
-    t.pre_force = std::getenv("CLB_FUSED_PREPASS") && std::atoi(std::getenv("CLB_FUSED_PREPASS")) == 1;
+    t.pre_force = std::getenv("CLB_FUSED_PREPASS") && std::atoi(std::getenv("CLB_FUSED_PREPASS")) == 2;
     const int Hp = pad > 0 ? H + pad : 1, Wp = pad > 0 ? W + pad : H * W;
     const int HW = pad > 0 ? Hp * Wp : H * W;
     t.pre_x = x;

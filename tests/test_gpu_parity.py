@@ -203,9 +203,9 @@ def test_one_contraction_per_call(oracle, clb, torch_cuda):
     torch = torch_cuda
     layer = clb.LayerConfig("l", 3, 6, 6, 2, 3, batch=1)
     x, w = oracle.make_problem(1, 3, 6, 6, 2, 3, 140)
-    # kn2row-gpu: ONE launch -- the NCHW -> split conversion of an input this small runs as the
-    # contraction kernel's fused phase 0 (api.cu fused_prepass_enabled; 2 launches when unfused)
-    fused = os.environ.get("CLB_FUSED_PREPASS", "") != "0"
+    # kn2row-gpu: prepass + contraction, or ONE launch when the opt-in fused prepass folds the
+    # conversion of an input this small into the contraction (api.cu fused_prepass_enabled)
+    fused = os.environ.get("CLB_FUSED_PREPASS", "0") in ("1", "2")
     expect = {"kn2row-gpu": 1 if fused else 2, "kn2row-explicit-gpu": 3, "kn2col-gpu": 3, "im2col-gpu": 2, "im2row-gpu": 2,
               "kn2row-acc-gpu": 10,
               "direct-gpu": 1}
@@ -379,7 +379,7 @@ print(json.dumps(out))
 '''
 
 
-@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs", "fused"])
+@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs", "fused", "fused_auto"])
 def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     """The implicit kernel's tap-shared mode (zero-padded NHWC rows, one A box of 128+k-1 rows
     per kernel row, taps through row-shifted UMMA descriptors), forced on and off via
@@ -391,9 +391,9 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     the launch trace proves both k = 3 and k = 5 instantiations ran.  "knobs" turns on the
     measured-negative, default-off paths so they stay correct: weight-stationary B
     (CLB_B_RESIDENT), the L2 prefetch of the next piece (CLB_L2_PREFETCH), the L2-chunked
-    forward (CLB_L2_CHUNK_MB, one image per chunk here), a single A-issuing warp and the
-    standalone (unfused) NCHW -> split prepass kernel; "fused" forces the contraction's phase-0
-    conversion (grid barrier) on every shape."""
+    forward (CLB_L2_CHUNK_MB, one image per chunk here) and a single A-issuing warp; "fused"
+    forces the contraction's phase-0 conversion (grid barrier) on every shape, "fused_auto" the
+    opt-in small-input rule with its standalone fallback."""
     import json
     import os
     import subprocess
@@ -406,8 +406,8 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
            "stacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1"),
            "unstacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="0"),
            "knobs": dict(CLB_PADDED_ROWS="1", CLB_B_RESIDENT="1", CLB_L2_PREFETCH="1", CLB_L2_CHUNK_MB="0.01",
-                         CLB_A_ISSUERS="1", CLB_FUSED_PREPASS="0", CLB_TRACE="1"),
-           "fused": dict(CLB_FUSED_PREPASS="1")}[mode]
+                         CLB_A_ISSUERS="1", CLB_TRACE="1"),
+           "fused": dict(CLB_FUSED_PREPASS="2"), "fused_auto": dict(CLB_FUSED_PREPASS="1")}[mode]
     r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, **env))
     assert r.returncode == 0, r.stderr[-3000:]
