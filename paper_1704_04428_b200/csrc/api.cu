@@ -7,6 +7,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/convlab_b200.h"
 #include "internal.hpp"
@@ -94,6 +95,7 @@ struct cl_plan {
     float* wpack = nullptr;
     size_t wpack_bytes = 0;
     float* wraw = nullptr;     // direct-gpu: MKKC fp32 weights as given
+    std::vector<float> wparam; // direct-gpu, 3 -> 16/32/64 channels 3x3: host weights [c][i][j][m] (kernel parameter)
     unsigned* flags = nullptr; // stream-K fixup flags, zeroed once, self-resetting
     bool padded_rows = false;  // implicit kn2row in tap-shared (zero-padded row) mode
     int stack_k = 1;           // > 1: padded-row mode with the k taps of a kernel row stacked on N
@@ -511,7 +513,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             if (nhwc) throw Error(CL_EUNSUPPORTED, "channels-last forward: implicit kn2row / conv1x1 / kn2row-acc only");
             // the dominant (and only) kernel of this method: bracket it for the profile events
             if (p->ev_begin && ev_first) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
-            launch_direct_conv(x, p->wraw, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, d.stride, p->P, p->Q, s);
+            launch_direct_conv(x, p->wraw, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, d.stride, p->P, p->Q, s,
+                               p->wparam.empty() ? nullptr : p->wparam.data());
             ++p->launches;
             tc_done();
             break;
@@ -553,6 +556,18 @@ void forward_chunked(cl_plan* p, const float* x, float* y, void* ws, cudaStream_
         launches += p->launches;
     }
     p->launches = launches;
+}
+
+// direct-gpu parameter-weight kernel: MKKC host weights -> [c][i][j][m]
+void pack_param_weights(cl_plan* p, const float* h_w_mkkc) {
+    const cl_conv_desc& d = p->d;
+    p->wparam.assign((size_t)d.c * d.k * d.k * d.m, 0.0f);
+    for (int m = 0; m < d.m; ++m)
+        for (int i = 0; i < d.k; ++i)
+            for (int j = 0; j < d.k; ++j)
+                for (int c = 0; c < d.c; ++c)
+                    p->wparam[(((size_t)c * d.k + i) * d.k + j) * d.m + m] =
+                        h_w_mkkc[(((size_t)m * d.k + i) * d.k + j) * d.c + c];
 }
 
 }  // namespace
@@ -693,9 +708,15 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
         const cl_conv_desc& d = p->d;
         if (is_patch_method(p->method))
             launch_rows_split(d_w, p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);   // MKKC == M x k^2C
-        else if (p->method == CL_METHOD_DIRECT)
+        else if (p->method == CL_METHOD_DIRECT) {
             CLB_CUDA(cudaMemcpyAsync(p->wpack, d_w, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
-        else
+            if (direct_param_shape(d.c, d.k, d.m, d.stride, p->Q)) {   // host copy for the kernel parameter
+                std::vector<float> h(p->wpack_bytes / sizeof(float));
+                CLB_CUDA(cudaMemcpyAsync(h.data(), d_w, p->wpack_bytes, cudaMemcpyDeviceToHost, s));
+                CLB_CUDA(cudaStreamSynchronize(s));
+                pack_param_weights(p, h.data());
+            }
+        } else
             launch_pack_weights(d_w, p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s, p->stack_k > 1);
         p->weights_set = true;
         mark_done(p, s);
@@ -716,8 +737,10 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
         const cl_conv_desc& d = p->d;
         if (is_patch_method(p->method))
             launch_rows_split(static_cast<float*>(dw), p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);
-        else if (p->method == CL_METHOD_DIRECT)
+        else if (p->method == CL_METHOD_DIRECT) {
             CLB_CUDA(cudaMemcpyAsync(p->wpack, dw, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
+            if (direct_param_shape(d.c, d.k, d.m, d.stride, p->Q)) pack_param_weights(p, h_w);
+        }
         else
             launch_pack_weights(static_cast<float*>(dw), p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s, p->stack_k > 1);
         CLB_CUDA(cudaFreeAsync(dw, s));

@@ -18,6 +18,8 @@
 //     16 at a time (64 fp32 accumulators), streaming float4s out (a warp = 512 contiguous B).
 // direct_conv_kernel (fallback when the weights do not fit): the same arithmetic with the
 // halo and a 16-channel weight slice staged per CTA.
+#include <cstring>
+
 #include "internal.hpp"
 
 namespace clb {
@@ -191,6 +193,100 @@ __global__ void __launch_bounds__(kPThreads, 2)
     cp_async_wait_all();
 }
 
+// 3-channel, 3x3 first layers (VGG conv1_1) with M output channels known at compile time:
+// the same persistent unit / halo pipeline as direct_persistent_kernel, but the C*k*k*M
+// weights travel as a __grid_constant__ kernel parameter ([c][i][j][m] order), so with every
+// index a compile-time constant each FFMA takes its weight straight from the constant bank --
+// no shared-memory weight loads (the smem kernel issues one LDS.128 per 16 FFMAs and measured
+// issue-bound, profiles/r01_ncu_vgg16_conv1_1_direct_full.json).
+template <int NW>
+struct ParamWeights {
+    float w[NW];
+};
+
+template <int MT>
+__global__ void __launch_bounds__(kPThreads, 2)
+    direct_param_kernel(const float* __restrict__ x, float* __restrict__ y, int H, int W, int pad, int P, int Q,
+                        int num_units, const __grid_constant__ ParamWeights<27 * MT> wts) {
+    constexpr int C = 3, k = 3;
+    extern __shared__ __align__(16) float sm[];
+    const UnitGeom g = unit_geom(P, Q, k);
+    const int halo = C * g.halo_rows * g.pitch;
+    float* s_in0 = sm;
+    float* s_in1 = s_in0 + halo;
+    const int tid = threadIdx.x;
+    int unit = blockIdx.x;
+    if (unit < num_units) load_halo(s_in0, x, unit, g, C, H, W, k, pad);
+    cp_async_commit();
+    const bool y_aligned = (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+    const long long plane = (long long)P * Q;
+    int buf = 0;
+    for (; unit < num_units; unit += gridDim.x) {
+        cp_async_wait_all();
+        __syncthreads();
+        const int next = unit + gridDim.x;
+        if (next < num_units) load_halo(buf ? s_in0 : s_in1, x, next, g, C, H, W, k, pad);
+        cp_async_commit();
+        const float* s_in = buf ? s_in1 : s_in0;
+        const int n = unit / g.units_img;
+        const int g0 = (unit - n * g.units_img) * kUnit;
+        const int gi = g0 + tid;
+        if (gi < g.groups_img) {
+            const int r_lo = g0 / g.groups_row;
+            const int row = gi / g.groups_row;
+            const int col = (gi - row * g.groups_row) * 4;
+            const float* s_px = s_in + (row - r_lo) * g.pitch + col;
+            float* y_px = y + (long long)n * MT * plane + (long long)gi * 4;
+            // the 27 taps' input rows are loaded once per pixel group and reused for every m
+            float v[C][k][kPx + k - 1];
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+#pragma unroll
+                for (int i = 0; i < k; ++i) {
+                    const float* src = s_px + (c * g.halo_rows + i) * g.pitch;
+                    const float4 v4 = *reinterpret_cast<const float4*>(src);
+                    v[c][i][0] = v4.x, v[c][i][1] = v4.y, v[c][i][2] = v4.z, v[c][i][3] = v4.w;
+                    v[c][i][4] = src[4];
+                    v[c][i][5] = src[5];
+                }
+            // rolled over the 16-channel passes: a fully unrolled M = 64 body (~18k instructions)
+            // measured 30 % slower (instruction-cache bound)
+#pragma unroll 1
+            for (int m0 = 0; m0 < MT; m0 += kMb) {
+                float acc[kMb][kPx];
+#pragma unroll
+                for (int mm = 0; mm < kMb; ++mm)
+#pragma unroll
+                    for (int t = 0; t < kPx; ++t) acc[mm][t] = 0.0f;
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+#pragma unroll
+                    for (int i = 0; i < k; ++i)
+#pragma unroll
+                        for (int j = 0; j < k; ++j)
+#pragma unroll
+                            for (int mm = 0; mm < kMb; ++mm) {
+                                const float wv = wts.w[((c * k + i) * k + j) * MT + m0 + mm];
+#pragma unroll
+                                for (int t = 0; t < kPx; ++t) acc[mm][t] = fmaf(wv, v[c][i][t + j], acc[mm][t]);
+                            }
+#pragma unroll
+                for (int mm = 0; mm < kMb; ++mm) {
+                    float* dst = y_px + (long long)(m0 + mm) * plane;
+                    if (y_aligned) {
+                        st_stream_f4(dst, acc[mm][0], acc[mm][1], acc[mm][2], acc[mm][3]);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < kPx; ++t) dst[t] = acc[mm][t];
+                    }
+                }
+            }
+        }
+        buf ^= 1;
+    }
+    cp_async_wait_all();
+}
+
 // Fallback: KT > 0 fixes the kernel size at compile time; KT == 0 takes any k <= kMaxK.
 template <int KT>
 __global__ void __launch_bounds__(128) direct_conv_kernel(const float* __restrict__ x, const float* __restrict__ w,
@@ -329,8 +425,12 @@ bool direct_fast_path(int C, int k, int stride) {
     return stride == 1 && k <= kMaxK && direct_smem_bytes(C, k) <= 200 * 1024;
 }
 
+bool direct_param_shape(int C, int k, int M, int stride, int Q) {
+    return C == 3 && k == 3 && stride == 1 && Q % 4 == 0 && (M == 16 || M == 32 || M == 64);
+}
+
 void launch_direct_conv(const float* x, const float* w, float* y, int N, int C, int H, int W, int M, int k, int pad,
-                        int stride, int P, int Q, cudaStream_t s) {
+                        int stride, int P, int Q, cudaStream_t s, const float* w_param) {
     if (!direct_fast_path(C, k, stride)) {
         dim3 grid((P * Q + 127) / 128, (M + kLnM - 1) / kLnM, N);
         direct_loopnest_kernel<<<grid, 128, 0, s>>>(x, w, y, C, H, W, M, k, pad, stride, P, Q);
@@ -353,6 +453,33 @@ void launch_direct_conv(const float* x, const float* w, float* y, int N, int C, 
         CLB_CUDA(cudaGetDevice(&dev));
         CLB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         configured = true;
+    }
+    static const bool param_on = !(getenv("CLB_DIRECT_PARAM") && atoi(getenv("CLB_DIRECT_PARAM")) == 0);
+    if (w_param && param_on && direct_param_shape(C, k, M, stride, Q)) {
+        // weights as a kernel parameter (host copy packed [c][i][j][m] by the plan)
+        const UnitGeom g = unit_geom(P, Q, k);
+        const int num_units = N * g.units_img;
+        const size_t psmem = 2 * (size_t)C * g.halo_rows * g.pitch * sizeof(float);
+        if (psmem <= kPersistentSmem / 2 - 1024) {
+            static bool pconf = false;
+            if (!pconf) {
+                set_smem(direct_param_kernel<16>, kPersistentSmem / 2);
+                set_smem(direct_param_kernel<32>, kPersistentSmem / 2);
+                set_smem(direct_param_kernel<64>, kPersistentSmem / 2);
+                pconf = true;
+            }
+            const int grid = std::min(num_units, sms * 2);
+            auto go = [&](auto kernel, auto pw) {
+                decltype(pw) wts;
+                std::memcpy(wts.w, w_param, sizeof(wts.w));
+                kernel<<<grid, kPThreads, psmem, s>>>(x, y, H, W, pad, P, Q, num_units, wts);
+            };
+            if (M == 64) go(direct_param_kernel<64>, ParamWeights<27 * 64>{});
+            else if (M == 32) go(direct_param_kernel<32>, ParamWeights<27 * 32>{});
+            else go(direct_param_kernel<16>, ParamWeights<27 * 16>{});
+            CLB_CUDA(cudaGetLastError());
+            return;
+        }
     }
     const bool unit_ok = Q % 4 == 0 && C <= 4;   // groups of 4 never straddle a row
     const size_t psmem = unit_ok ? persistent_smem_bytes(C, k, M, P, Q) : 0;

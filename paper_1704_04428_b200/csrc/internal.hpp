@@ -78,9 +78,11 @@ void launch_shift_add_col(const float* inter, float* y, int N, int M, int H, int
                           int Q, cudaStream_t s);
 
 // direct fp32 convolution for tiny-C layers (direct.cu); weights MKKC, stride 1
+// w_param (optional): host copy of the weights packed [c][i][j][m] for the parameter-weight
+// kernel (direct_param_shape: C = 3, k = 3, M in {16, 32, 64}, Q % 4 == 0)
 void launch_direct_conv(const float* x, const float* w, float* y, int N, int C, int H, int W, int M, int k, int pad,
-                        int stride,
-                        int P, int Q, cudaStream_t s);
+                        int stride, int P, int Q, cudaStream_t s, const float* w_param = nullptr);
+bool direct_param_shape(int C, int k, int M, int stride, int Q);
 size_t direct_smem_bytes(int C, int k);
 bool direct_fast_path(int C, int k, int stride);   // else the generic loop nest
 

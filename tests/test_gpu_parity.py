@@ -459,13 +459,16 @@ def test_guard_bands(oracle, clb, torch_cuda, method, precision):
 
 
 DIRECT_CASES = [(1, 3, 224, 224, 64, 3, 1), (3, 3, 20, 36, 70, 3, 1), (2, 1, 9, 8, 5, 5, 2), (2, 4, 33, 12, 17, 1, 0),
-                (1, 2, 40, 64, 33, 7, 3), (2, 3, 30, 10, 16, 3, 0), (1, 4, 5, 4, 8, 3, 1), (2, 3, 64, 200, 48, 5, 2)]
+                (1, 2, 40, 64, 33, 7, 3), (2, 3, 30, 10, 16, 3, 0), (1, 4, 5, 4, 8, 3, 1), (2, 3, 64, 200, 48, 5, 2),
+                (2, 3, 17, 20, 32, 3, 1)]
 
 
 @pytest.mark.parametrize("case", DIRECT_CASES)
 def test_direct_unit_kernel(oracle, clb, torch_cuda, case):
     """direct-gpu's persistent unit kernel (Q % 4 == 0: 256-group units spanning rows, full-width
-    halos) and its fallback, against the generalised loop nest, incl. pad != k/2."""
+    halos) and its fallback, against the generalised loop nest, incl. pad != k/2.  C = 3, k = 3
+    with M = 64 / 16 / 32 and Q % 4 == 0 run the parameter-weight kernel (weights in the
+    constant bank)."""
     N, C, H, W, M, k, pad = case
     x, w = oracle.make_problem(N, C, H, W, M, k, sum(case))
     ref = oracle.conv_loopnest(x, w, pad, 1)
