@@ -2,52 +2,72 @@
 """Benchmark of the B200 kn2row hot path -- one JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload alexnet] [--method auto] [--precision fp32]
+                    [--workload vgg16] [--method auto] [--precision fp32] [--scaling auto]
 
-Metric (BASELINE.json): per-layer effective TFLOP/s = 2 N M C k^2 P Q / time, here summed
-over the workload's layers: one STEP is one forward pass of every layer of the workload
-(default: configs[1], the AlexNet stride-1 conv stack at batch 128 per GPU) on synthetic
+Metric (BASELINE.json): per-layer effective TFLOP/s = 2 N M C k^2 P Q / time; the headline
+`value` sums the FLOPs of every layer of the workload over the step time.  One STEP is one
+forward pass of every layer of the workload (default: configs[2], the VGG-16 13-layer stack
+at batch 32 per GPU -- the north-star config and the largest single-GPU one) on synthetic
 uniform[-1,1) data from the reference generator (tensor.cpp:104-134), weights pre-packed
 once outside the timed region (the reference re-packs per call; the north star treats
-weights as static -- stated in DESIGN.md).
+weights as static -- stated in DESIGN.md).  The per-layer table (`layers`) carries each
+layer's dominant-kernel time, its TFLOP/s and its fraction of the tensor-core and layer
+rooflines.
 
 Timing: W untimed warm-up steps, then exactly K steps between a barrier +
 cuda.synchronize on both sides; every step is bracketed by CUDA events on the launching
-stream and L2 is flushed (256 MiB write, untimed) before each step.  Under torchrun each
-rank runs its own batch (weak scaling, no data-path collective) and the job time is the
-MAX over ranks.  `e2e` repeats the workload through the host-buffer C-ABI call
-(cl_conv_forward_host: pinned H2D + forward + D2H).
+stream and L2 is flushed (256 MiB write, untimed) before each step; the job time is the
+MAX over ranks.  `value` = FLOPs of all K steps / that time; `value_median` uses the median
+step.  `e2e` repeats the workload through the host-buffer C-ABI call
+(cl_conv_forward_host_async, pinned host buffers: H2D + forward + D2H inside the timed region).
+
+Multi-GPU: one process per GPU.  `--gpus N` without a torchrun environment re-launches this
+script under `python -m torch.distributed.run --nproc-per-node N` (127.0.0.1).  Images are
+independent, so ranks share nothing on the data path: weak scaling gives every rank the
+per-GPU batch; strong scaling (default for `--workload scale`: global batch 256) splits the
+global batch across ranks.  `--dry-run` goes through the launch and sharding (gloo, no GPU)
+and prints the configuration line without timing anything.
 
 --impl reference times the reference's own CPU kn2row (oracle/_ref = the unmodified
-reference core compiled from /root/reference) with all host threads, on rank 0 only.
+reference core compiled from /root/reference) with all host threads, on rank 0 only, on a
+bounded sample of the same workload (one image of each layer per step).  That arm never
+imports this repo's package.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import threading
 import time
+from dataclasses import dataclass, replace
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
-TRAFFIC_FILE = ROOT / "profiles" / "ncu_traffic.json"
+CONFIG_FILE = ROOT / "configs" / "baseline.net"
+GROUPS = ("c1", "alexnet", "vgg16", "googlenet", "sweep", "scale")
+METRIC = "effective TFLOP/s (2*N*M*C*k^2*P*Q / time), summed over the workload layers"
+NOMINAL_BF16 = 2250.0   # dense bf16 TFLOP/s, B200 nominal (B200_PROFILING.md, context only)
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="alexnet")
-    ap.add_argument("--batch", type=int, default=None, help="override the per-GPU batch")
+    ap.add_argument("--workload", default="vgg16", help=f"one of {GROUPS} (suffix -bN overrides the batch)")
+    ap.add_argument("--batch", type=int, default=None, help="override the batch (per GPU, or global when strong)")
+    ap.add_argument("--scaling", choices=["auto", "weak", "strong"], default="auto",
+                    help="weak: the batch is per GPU; strong: the batch is global and split across ranks "
+                         "(auto: strong for the C5 'scale' workload, weak otherwise)")
     ap.add_argument("--method", default="auto")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "bf16"],
                     help="fp32 = fp32-faithful (rel-L2 <= 1e-5; operand split per CLB_SPLIT: mixed "
@@ -55,18 +75,148 @@ def parse_args():
     ap.add_argument("--layout", default="nchw", choices=["nchw", "nhwc"],
                     help="device tensors NCHW (the reference interface, default) or channels-last "
                          "(cl_conv_forward_nhwc; the e2e leg stays NCHW)")
+    ap.add_argument("--concurrent", action="store_true",
+                    help="run the step's independent layers on concurrent streams (grid-capped launches)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline work")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the CPU-baseline sample")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--e2e-sync", action="store_true",
-                    help="e2e through the synchronous cl_conv_forward_host (one layer at a time)")
-    ap.add_argument("--per-layer", action="store_true", help="add a per-layer table to the JSON line")
-    return ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true", help="launch + sharding only (gloo, no GPU, no timing)")
+    return ap.parse_args(argv)
 
 
-NOMINAL_BF16 = 2250.0   # dense bf16 TFLOP/s, B200 nominal (B200_PROFILING.md, context only)
+# ------------------------------------------------------------------- workloads ----
+# configs/baseline.net in the reference's network grammar (layers.cpp:31-79) plus `pad=` / `n=`
+# columns.  Parsed here without importing the package, so the reference arm never loads it.
+@dataclass(frozen=True)
+class Layer:
+    name: str
+    channels: int
+    height: int
+    width: int
+    kernel_count: int
+    kernel_size: int
+    stride: int = 1
+    pad: int = -1
+    batch: int = 1
+
+    @property
+    def p(self):
+        pad = self.kernel_size // 2 if self.pad < 0 else self.pad
+        return (self.height + 2 * pad - self.kernel_size) // self.stride + 1
+
+    @property
+    def q(self):
+        pad = self.kernel_size // 2 if self.pad < 0 else self.pad
+        return (self.width + 2 * pad - self.kernel_size) // self.stride + 1
+
+    def flops(self, batch=None):
+        n = self.batch if batch is None else batch
+        return 2 * n * self.kernel_count * self.channels * self.kernel_size ** 2 * self.p * self.q
+
+    def bytes(self, batch=None):
+        """Compulsory fp32 HBM bytes 4 (N C H W + M C k^2 + N M P Q)."""
+        n = self.batch if batch is None else batch
+        return 4 * (n * self.channels * self.height * self.width
+                    + self.kernel_count * self.channels * self.kernel_size ** 2 + n * self.kernel_count * self.p * self.q)
 
 
+def load_layers(name: str, batch=None):
+    group, _, suffix = name.partition("-")
+    if group not in GROUPS:
+        raise SystemExit(f"unknown workload '{name}' (choose from {GROUPS})")
+    out = []
+    for raw in CONFIG_FILE.read_text().splitlines():
+        line = raw.split("#", 1)[0].strip()
+        if not line:
+            continue
+        toks = line.split()
+        kv = {}
+        while toks and "=" in toks[-1]:
+            k, _, v = toks.pop().partition("=")
+            kv[k] = int(v)
+        nm = toks[0]
+        if nm != group and not nm.startswith(group + "/"):
+            continue
+        nums = [int(t) for t in toks[1:]]
+        out.append(Layer(nm, nums[0], nums[1], nums[2], nums[3], nums[4], nums[5] if len(nums) == 6 else 1,
+                         kv.get("pad", -1), kv.get("n", 1)))
+    if suffix:
+        batch = int(suffix[1:])
+    if batch is not None:
+        out = [replace(l, batch=batch) for l in out]
+    return out
+
+
+def shard_range(total: int, world: int, rank: int):
+    base, extra = divmod(total, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+@dataclass
+class Run:
+    rank: int
+    world: int
+    local_rank: int
+    scaling: str
+    layers: list            # the workload as configured (batch = per GPU (weak) or global (strong))
+    rank_batch: int         # images this rank convolves per layer
+    image0: int             # first global image index of this rank
+
+    @property
+    def distributed(self):
+        return self.world > 1
+
+
+def setup_run(args) -> Run:
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launch has WORLD_SIZE={world}")
+    layers = load_layers(args.workload, args.batch)
+    scaling = args.scaling
+    if scaling == "auto":
+        scaling = "strong" if args.workload.partition("-")[0] == "scale" else "weak"
+    b = layers[0].batch
+    if any(l.batch != b for l in layers):
+        raise SystemExit("bench.py: a workload's layers share one batch")
+    if scaling == "strong":
+        if b < world:
+            raise SystemExit(f"bench.py: strong scaling needs batch {b} >= {world} ranks")
+        i0, i1 = shard_range(b, world, rank)
+    else:
+        i0, i1 = rank * b, (rank + 1) * b
+    return Run(rank, world, local, scaling, layers, i1 - i0, i0)
+
+
+def config_of(args, run: Run) -> dict:
+    """The `config` object, identical in both arms (the driver compares them)."""
+    layers = run.layers
+    per_gpu = layers[0].batch if run.scaling == "weak" else None
+    glob = layers[0].batch * run.world if run.scaling == "weak" else layers[0].batch
+    return {
+        "workload": args.workload, "layers": [l.name for l in layers],
+        "global_batch": glob, "per_gpu_batch": per_gpu if per_gpu is not None else -(-glob // run.world),
+        "scaling": run.scaling, "layout": args.layout, "method": args.method,
+        "precision": {"fp32": ("fp32-faithful (rel-L2 <= 1e-5): hi*Hi tf32 x2 + cross terms bf16 x2"
+                               if fp32_split() == "mixed" else "fp32-faithful 3xTF32"),
+                      "tf32": "tf32 (fast mode)", "bf16": "bf16 operands, fp32 accumulate (fast mode)"}[args.precision],
+        "parallelism": f"dp{run.world} (batch-sharded, no data-path collective)",
+        "l2": "flushed (256 MiB write) before every timed step", "weights": "pre-packed once, untimed",
+    }
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` without a torchrun environment: one process per GPU via torch.distributed.run."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+# ----------------------------------------------------------------- precision ----
 def fp32_split():
     """The fp32-faithful operand split the library uses (same switch as api.cu planes_for):
     'mixed' = hi*Hi in two tf32 MMAs + the two cross terms in one bf16 K=16 MMA each (4
@@ -82,9 +232,8 @@ def tensor_factor(precision):
 
 
 def mma_peak_for(precision):
-    """Our own kind::tf32 MMA peak (tools/mma_probe.cu, committed under profiles/), in the
-    precision's effective units (tensor_factor)."""
-    f = Path(__file__).resolve().parent / "profiles" / "tf32_mma_peak.json"
+    """Our own kind::tf32 MMA peak (tools/mma_probe.cu, profiles/tf32_mma_peak.json)."""
+    f = ROOT / "profiles" / "tf32_mma_peak.json"
     if not f.exists():
         return None
     return json.loads(f.read_text())["tf32_mma_peak_tflops"] * tensor_factor(precision)
@@ -97,6 +246,20 @@ def peaks():
                 "hbm": float(p["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
     except Exception:
         return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def traffic_for(workload, precision, method):
+    """DRAM bytes per step of the contraction kernels from the committed ncu capture of this
+    workload (profiles/ncu_traffic_<workload>.json, tools/make_traffic.py), or None."""
+    for f in (ROOT / "profiles" / f"ncu_traffic_{workload}.json", ROOT / "profiles" / "ncu_traffic.json"):
+        try:
+            tr = json.loads(f.read_text())
+        except Exception:
+            continue
+        if (tr.get("workload") == workload and tr.get("precision", "fp32") == precision and method == "auto"
+                and tr.get("split", "mixed") == (fp32_split() if precision == "fp32" else tr.get("split", "mixed"))):
+            return tr.get("dram_bytes_per_step"), str(f.relative_to(ROOT))
+    return None, None
 
 
 # ------------------------------------------------------------------------- clocks ----
@@ -176,58 +339,77 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------- CPU baseline ----
-def cpu_reference_sample(layers, seconds: float, threads: int, seed: int = 0):
-    """Times the reference's CPU kn2row (oracle/_ref, convlab::run_method with
-    GemmBackend::parallel(threads)) on ONE image of each layer, repeating the whole sample
-    until ~`seconds` of CPU work.  Returns (TFLOP/s, detail)."""
-    import numpy as np
+def cpu_baseline(layers, threads: int, budget_s: float) -> dict:
+    """The reference's own CPU paths through its public benchmark API (oracle/_ref:
+    convlab::benchmark(layer, method, runs, backend, seed), bench.cpp:87-151 -- 1 untimed
+    warm-up, then timed runs, input generation excluded) on ONE image of every layer of the
+    workload (the reference has no batch dimension: batch-N time = N x per-image time):
+    kn2row and im2col at GemmBackend::parallel(T), kn2row at blocked (1 core), and kn2row's
+    thread scaling 1 -> T over the whole sample.  Returns the cpu_baseline object; `value` is
+    kn2row at parallel(T) (the paper's method, the reference arm's path)."""
     from oracle import oracle as O
 
     if not O.ref_available():
         raise RuntimeError("oracle/_ref (compiled reference) is not available")
-    data = []
-    for li, l in enumerate(layers):
-        x, w = O.make_problem(1, l.channels, l.height, l.width, l.kernel_count, l.kernel_size, seed + li)
-        data.append((l, np.ascontiguousarray(x[0]), w))
-    one_image_flops = sum(l.flops() // l.batch for l in layers)
-    for l, x, w in data:  # warm-up (the reference benchmark()'s untimed run, bench.cpp:115-118)
-        O.ref_run_method("kn2row", x, w, threads)
-    reps, spent = 0, 0.0
-    while reps < 2 or (spent < seconds and reps < 1000):
-        t0 = time.perf_counter()
-        for l, x, w in data:
-            O.ref_run_method("kn2row", x, w, threads)
-        spent += time.perf_counter() - t0
-        reps += 1
-    per_pass = spent / reps
-    return one_image_flops / per_pass / 1e12, {
-        "passes": reps, "seconds": round(spent, 3), "per_image_pass_s": per_pass,
-        "one_image_gflop": one_image_flops / 1e9}
+    img_flops = sum(l.flops(1) for l in layers)
+    t_start = time.perf_counter()
+
+    def run(method, thr):
+        per = []
+        for li, l in enumerate(layers):
+            r = O.ref_benchmark(method, l.channels, l.height, l.width, l.kernel_count, l.kernel_size, 1, thr, li)
+            per.append(r["min_s"])
+        return per
+
+    per_kn = run("kn2row", threads)
+    per_im = run("im2col", threads)
+    per_1c = run("kn2row", 0)             # GemmBackend::blocked(): one core
+    scaling = {"1": img_flops / sum(per_1c) / 1e9}
+    t = 2
+    while t < threads and time.perf_counter() - t_start < budget_s:
+        scaling[str(t)] = img_flops / sum(run("kn2row", t)) / 1e9
+        t *= 2
+    scaling[str(threads)] = img_flops / sum(per_kn) / 1e9
+    spent = time.perf_counter() - t_start
+    return {
+        "value": img_flops / sum(per_kn) / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+        "sample": (f"1 image of each of the {len(layers)} layers ({img_flops / 1e9:.1f} GFLOP), reference "
+                   f"convlab::benchmark (oracle/_ref, the unmodified reference core), 1 warm-up + 1 timed run per "
+                   f"layer and backend; kn2row/im2col at GemmBackend::parallel({threads}), kn2row at blocked (1 core) "
+                   f"and at 2..{threads} threads; {spent:.1f} s of CPU work; batch-N time = N x per-image time"),
+        "kn2row_parallel_tflops": img_flops / sum(per_kn) / 1e12,
+        "im2col_parallel_tflops": img_flops / sum(per_im) / 1e12,
+        "kn2row_1core_tflops": img_flops / sum(per_1c) / 1e12,
+        "kn2row_thread_scaling_gflops": scaling,
+        "kn2row_speedup_1_to_T": sum(per_1c) / sum(per_kn),
+        "per_layer_s": [{"name": l.name, "kn2row_T": a, "im2col_T": b, "kn2row_1core": c}
+                        for l, a, b, c in zip(layers, per_kn, per_im, per_1c)],
+    }
 
 
-def run_reference_arm(args, info, layers, total_flops_per_step):
-    if info.rank != 0:
+def run_reference_arm(args, run: Run) -> int:
+    if run.rank != 0:
         return 0
-    from oracle import oracle as O
+    from oracle import oracle as O   # the CPU checker / reference binding -- not this package
     threads = O.host_threads()
-    cfg = {"workload": args.workload, "layers": [l.name for l in layers], "per_gpu_batch": layers[0].batch,
-           "method": "kn2row (reference CPU)", "backend": f"parallel({threads})"}
+    layers = run.layers
     try:
         # each step: one image through every layer (bounded sample of the workload)
-        import numpy as np
         data = []
         for li, l in enumerate(layers):
             x, w = O.make_problem(1, l.channels, l.height, l.width, l.kernel_count, l.kernel_size, li)
-            data.append((np.ascontiguousarray(x[0]), w))
-        sample_flops = sum(l.flops() // l.batch for l in layers)
+            data.append((x[0].copy(), w))
+        sample_flops = sum(l.flops(1) for l in layers)
         for _ in range(args.warmup):
             for x, w in data:
                 O.ref_run_method("kn2row", x, w, threads)
-        t0 = time.perf_counter()
+        step_s = []
         for _ in range(args.steps):
+            t0 = time.perf_counter()
             for x, w in data:
                 O.ref_run_method("kn2row", x, w, threads)
-        dt = time.perf_counter() - t0
+            step_s.append(time.perf_counter() - t0)
+        dt = sum(step_s)
     except Exception as e:  # pragma: no cover
         print(json.dumps({"impl": "reference", "unavailable": f"reference CPU path failed: {e}"}))
         return 0
@@ -236,49 +418,69 @@ def run_reference_arm(args, info, layers, total_flops_per_step):
               f"(reference convlab::run_method(Kn2row), GemmBackend::parallel({threads})); "
               f"the reference has no batch dim, batch-N time = N x per-image time")
     print(json.dumps({
-        "impl": "reference", "metric": "effective TFLOP/s (2*N*M*C*k^2*P*Q / time), summed over the workload layers",
-        "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (reference generator, uniform[-1,1))", "config": cfg,
+        "impl": "reference", "metric": METRIC,
+        "value": value, "unit": "TFLOP/s", "n_gpus": run.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "step_ms_median": statistics.median(step_s) * 1e3,
+        "higher_is_better": True, "scaling": run.scaling, "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic: reference generator uniform[-1,1) (tensor.cpp:104-134)",
+        "config": config_of(args, run),
+        "device": f"host CPU only ({threads} threads on rank 0; no GPU used by this arm)",
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
     return 0
 
 
+def dry_run(args, run: Run) -> int:
+    import torch.distributed as dist
+    if run.distributed:
+        dist.init_process_group("gloo")
+    batches = [run.rank_batch]
+    if run.distributed:
+        out = [None] * run.world
+        dist.all_gather_object(out, (run.rank, run.image0, run.rank_batch))
+        batches = [b for _, _, b in sorted(out)]
+        dist.barrier()
+        dist.destroy_process_group()
+    if run.rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "value": None, "unit": "TFLOP/s", "n_gpus": run.world,
+                          "scaling": run.scaling, "rank_batches": batches, "config": config_of(args, run)}))
+    return 0
+
+
 # ------------------------------------------------------------------------- our arm ----
-def main():
-    args = parse_args()
-    from paper_1704_04428_b200 import dist, workloads
-
-    info = dist.from_env()
-    layers = workloads.workload(args.workload, args.batch)
-    if args.impl == "reference":
-        return run_reference_arm(args, info, layers, workloads.total_flops(layers))
-
+def run_ours(args, run: Run) -> int:
     import torch
 
     import paper_1704_04428_b200 as clb
-    from paper_1704_04428_b200 import _lib, rng
+    from paper_1704_04428_b200 import _lib, dist, rng
 
-    info = dist.init("nccl")
-    dev = info.local_rank
+    info = dist.RankInfo(run.rank, run.world, run.local_rank)
+    if run.distributed:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")            # NCCL init log (transport, NVLS) to a file
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/clb_nccl.{run.rank}.log")
+    dist.init("nccl")
+    dev = run.local_rank
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
     pk = peaks()
+    rank_layers = [replace(l, batch=run.rank_batch) for l in run.layers]
 
     # ---- setup (untimed): plans, packed weights, resident inputs/outputs/workspaces ----
-    plans, xs, ys, wss, evs = [], [], [], [], []
-    for li, l in enumerate(layers):
-        plan = clb.ConvPlan(l, args.method, args.precision, dev)
+    plans, xs, ys, wss = [], [], [], []
+    for li, l in enumerate(rank_layers):
+        lc = clb.LayerConfig(l.name, l.channels, l.height, l.width, l.kernel_count, l.kernel_size, l.stride,
+                             None if l.pad < 0 else l.pad, l.batch)
+        plan = clb.ConvPlan(lc, args.method, args.precision, dev)
         if args.layout == "nhwc" and plan.method not in ("kn2row-gpu", "conv1x1-gpu", "kn2row-acc-gpu"):
-            # channels-last is served by the implicit kernel only: plan that one explicitly
-            plan.close()
-            plan = clb.ConvPlan(l, "kn2row-gpu" if l.kernel_size > 1 else "conv1x1-gpu", args.precision, dev)
+            plan.close()   # channels-last is served by the implicit kernel only
+            plan = clb.ConvPlan(lc, "kn2row-gpu" if l.kernel_size > 1 else "conv1x1-gpu", args.precision, dev)
         x = torch.empty((l.batch, l.channels, l.height, l.width), device=dev, dtype=torch.float32)
         w = torch.empty((l.kernel_count, l.kernel_size, l.kernel_size, l.channels), device=dev, dtype=torch.float32)
         img = l.channels * l.height * l.width
-        rng.fill_uniform(x, rng.split(li, 0), dist.image_offset(info.rank, l.batch, img))
+        # one global reference stream per layer: this rank's images are images [image0, image0 + batch)
+        rng.fill_uniform(x, rng.split(li, 0), run.image0 * img)
         rng.fill_uniform(w, rng.split(li, 1))
         plan.set_weights(w)
         ws = torch.empty(max(plan.workspace_bytes(), 4), device=dev, dtype=torch.uint8)
@@ -290,12 +492,22 @@ def main():
         xs.append(x)
         ys.append(y)
         wss.append(ws)
-    # L2 flush between timed steps: a write larger than the 126 MB L2 (MiB, CLB_FLUSH_MB to vary)
-    flush_mb = int(os.environ.get("CLB_FLUSH_MB", "256"))
+    flush_mb = int(os.environ.get("CLB_FLUSH_MB", "256"))   # L2 flush: a write larger than the 126 MB L2
     flush = torch.empty(flush_mb * 1024 * 1024, device=dev, dtype=torch.uint8)
-    flops_step = workloads.total_flops(layers)
+    flops_rank = sum(l.flops() for l in rank_layers)
+    flops_job = sum(l.flops() for l in run.layers) * (run.world if run.scaling == "weak" else 1)
+
+    # concurrent layers (--concurrent): each layer on its own stream with an engine grid share
+    # proportional to its FLOPs, forked from / joined into the step stream
+    side = []
+    if args.concurrent:
+        from paper_1704_04428_b200 import concurrency
+        side = concurrency.assign(plans, [l.flops() for l in rank_layers], dev)
 
     def step(record_kernel=None):
+        if side:
+            concurrency.run_step(plans, xs, ys, wss, side, stream, args.layout, record_kernel)
+            return
         for li, plan in enumerate(plans):
             if record_kernel is not None:
                 b, e = record_kernel[li]
@@ -335,18 +547,21 @@ def main():
     sampler.stop()
 
     step_ms = [st_b[i].elapsed_time(st_e[i]) for i in range(args.steps)]
-    if os.environ.get("CLB_BENCH_STEP_MS"):        # diagnostics: per-step device times
-        print(json.dumps({"step_ms": [round(v, 4) for v in step_ms]}), file=sys.stderr)
     local_ms = sum(step_ms)
-    kern_ms = [sum(k_ev[i][li][0].elapsed_time(k_ev[i][li][1]) for i in range(args.steps)) / args.steps
+    kern_ms = [statistics.median(k_ev[i][li][0].elapsed_time(k_ev[i][li][1]) for i in range(args.steps))
                for li in range(len(plans))]
     job_ms = dist.max_over_ranks(local_ms, info, device=dev)
-    total_flops = flops_step * args.steps * info.world
-    value = total_flops / (job_ms * 1e-3) / 1e12
+    med_ms = dist.max_over_ranks(statistics.median(step_ms), info, device=dev)
+    value = flops_job * args.steps / (job_ms * 1e-3) / 1e12
+    value_median = flops_job / (med_ms * 1e-3) / 1e12
 
-    # ---- e2e through the host-buffer C-ABI call ----------------------------------------
-    hx = [x.cpu().pin_memory() for x in xs]
-    hy = [torch.empty(y.shape, dtype=torch.float32).pin_memory() for y in ys]
+    # ---- e2e through the host-buffer C-ABI call (pinned host in / out, every byte timed) ----
+    hx = [x.cpu().pin_memory() for x in xs] if args.layout == "nchw" else \
+         [x.permute(0, 3, 1, 2).contiguous().pin_memory() for x in xs]
+    hy = [torch.empty(p.output_shape(), dtype=torch.float32).pin_memory() for p in plans]
+    # the layers are independent: each is issued on its own stream (the async call orders its
+    # copy-in after prior work on its stream), so their transfers overlap on both copy engines
+    e2e_streams = [torch.cuda.Stream() for _ in plans]
     for li, p in enumerate(plans):
         p.forward_host(hx[li], hy[li])
     e2e_steps = max(1, min(args.e2e_steps, args.steps))
@@ -355,113 +570,116 @@ def main():
     eb, ee = ev(), ev()
     eb.record(stream)
     for _ in range(e2e_steps):
-        if args.e2e_sync:
-            for li, p in enumerate(plans):
-                p.forward_host(hx[li], hy[li])
-        else:
-            # the layers are independent: enqueue all four host-buffer calls, then wait for the
-            # step's outputs (every H2D / D2H byte of the step is inside the timed region)
-            for li, p in enumerate(plans):
-                p.forward_host_async(hx[li], hy[li], stream)
-            stream.synchronize()
+        for li, p in enumerate(plans):
+            p.forward_host_async(hx[li], hy[li], e2e_streams[li])
+        for s in e2e_streams:
+            s.synchronize()
     ee.record(stream)
     torch.cuda.synchronize()
     e2e_ms = dist.max_over_ranks(eb.elapsed_time(ee), info, device=dev)
-    e2e_value = flops_step * e2e_steps * info.world / (e2e_ms * 1e-3) / 1e12
-    h2d = sum(x.numel() * 4 for x in xs)
-    d2h = sum(y.numel() * 4 for y in ys)
+    e2e_value = flops_job * e2e_steps / (e2e_ms * 1e-3) / 1e12
+    h2d = sum(x.numel() * 4 for x in hx)
+    d2h = sum(y.numel() * 4 for y in hy)
 
     # ---- roofline of the dominant kernel (tc_conv_kernel: the tcgen05 contraction) ------
-    kernel_ms_step = sum(kern_ms)
     tf32_peak = pk["bf16"] / 2.0
     mode_peak = tf32_peak * tensor_factor(args.precision)
     nominal_peak = NOMINAL_BF16 / 2.0 * tensor_factor(args.precision)
-    achieved = flops_step / (kernel_ms_step * 1e-3) / 1e12
-    traffic = None
-    try:
-        tr = json.loads(TRAFFIC_FILE.read_text())
-        if tr.get("workload") == args.workload and tr.get("precision", "fp32") == args.precision:
-            traffic = tr.get("dram_bytes_per_step")
-    except Exception:
-        pass
+    hbm = pk["hbm"]
+    tc_idx = [i for i, p in enumerate(plans) if p.method != "direct-gpu"]
+    tc_flops = sum(rank_layers[i].flops() for i in tc_idx)
+    tc_ms = sum(kern_ms[i] for i in tc_idx)
+    achieved = tc_flops / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else None
+    traffic, traffic_src = traffic_for(args.workload, args.precision, args.method)
+    if run.world > 1 or args.batch is not None:
+        traffic, traffic_src = None, None       # the capture is of the 1-GPU default batch
+    layer_rows = []
+    for l, p, km in zip(rank_layers, plans, kern_ms):
+        ai = l.flops() / l.bytes()
+        bound = min(mode_peak, ai * hbm / 1e3)
+        tf = l.flops() / (km * 1e-3) / 1e12
+        layer_rows.append({"name": l.name, "method": p.method, "batch": l.batch, "gflop": round(l.flops() / 1e9, 3),
+                           "kernel_ms": round(km, 4), "kernel_tflops": round(tf, 1),
+                           "frac_of_peak": round(tf / mode_peak, 3),
+                           "layer_roofline_tflops": round(bound, 1), "frac_of_layer_roofline": round(tf / bound, 3),
+                           "bound": "tensor" if bound >= mode_peak else "hbm",
+                           "share_of_step": round(km / statistics.median(step_ms), 3)})
 
-    if info.rank != 0:
+    if run.rank != 0:
+        for p in plans:
+            p.close()
         return 0
 
     cpu = None
-    if not args.no_cpu_baseline and info.world == 1:
+    if not args.no_cpu_baseline and run.world == 1:
         try:
             from oracle import oracle as O
-            threads = O.host_threads()
-            v, det = cpu_reference_sample(layers, args.cpu_seconds, threads)
-            cpu = {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
-                   "sample": (f"1 image of each of the {len(layers)} {args.workload} layers, reference kn2row "
-                              f"(oracle/_ref convlab::run_method, GemmBackend::parallel({threads})), "
-                              f"{det['passes']} passes in {det['seconds']} s; batch-N time = N x per-image time")}
+            cpu = cpu_baseline(run.layers, O.host_threads(), args.cpu_seconds)
         except Exception as e:
             cpu = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
     clocks = sampler.summary(t_wall0, t_wall1)
     out = {
-        "metric": "effective TFLOP/s (2*N*M*C*k^2*P*Q / time), summed over the workload layers",
-        "value": value, "unit": "TFLOP/s", "n_gpus": info.world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": job_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC,
+        "value": value, "unit": "TFLOP/s", "n_gpus": run.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": job_ms / args.steps, "step_ms_median": med_ms, "value_median": value_median,
+        "higher_is_better": True, "scaling": run.scaling, "vs_baseline": None,
         "dtype": {"fp32": "f32", "tf32": "tf32", "bf16": "bf16"}[args.precision],
         "data": "synthetic: reference generator uniform[-1,1) (tensor.cpp:104-134) on device, random-init weights",
-        "config": {
-            "workload": args.workload, "layers": [l.name for l in layers], "per_gpu_batch": layers[0].batch,
-            "layout": args.layout,
-            "global_batch": layers[0].batch * info.world, "method": args.method,
-            "resolved_methods": sorted({p.method for p in plans}),
-            "precision": {"fp32": ("fp32-faithful (rel-L2 <= 1e-5): hi*Hi tf32 x2 + cross terms bf16 x2"
-                                   if fp32_split() == "mixed" else "fp32-faithful 3xTF32"),
-                          "tf32": "tf32 (fast mode)",
-                          "bf16": "bf16 operands, fp32 accumulate (fast mode)"}[args.precision],
-            "parallelism": f"dp{info.world} (batch-sharded, no data-path collective)",
-            "l2": "flushed (256 MiB write) before every timed step", "weights": "pre-packed once, untimed",
-        },
+        "config": config_of(args, run),
+        "rank_batch": run.rank_batch,
+        "resolved_methods": sorted({p.method for p in plans}),
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps,
-                "api": ("cl_conv_forward_host, synchronous per layer" if args.e2e_sync else
-                        "cl_conv_forward_host_async for the 4 layers of a step, then a stream sync per step") +
-                       " (pinned host buffers)"},
+                "api": "cl_conv_forward_host_async per layer, each layer on its own stream, all streams synchronised "
+                       "per step (pinned host buffers)"},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": mode_peak, "unit": "TFLOP/s",
-                     "frac": achieved / mode_peak, "traffic": traffic,
+                     "frac": achieved / mode_peak if achieved else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_step": sum(rank_layers[i].bytes() for i in tc_idx),
                      "kernel": {"fp32": ("tc_conv_kernel (tcgen05: hi*Hi kind::tf32 x2 + cross terms kind::f16 x2)"
                                          if fp32_split() == "mixed" else "tc_conv_kernel (tcgen05 kind::tf32 x3)"),
                                 "tf32": "tc_conv_kernel (tcgen05 kind::tf32)",
                                 "bf16": "tc_conv_kernel (tcgen05 kind::f16, bf16)"}[args.precision],
-                     "kernel_ms_per_step": kernel_ms_step,
+                     "kernel_ms_per_step": tc_ms, "kernel_layers": len(tc_idx),
                      "peak_note": (f"peak = measured bf16 burst {pk['bf16']} / 2 (tf32 rate) x "
                                    f"{tensor_factor(args.precision):.3g} (effective flops per tf32 MMA flop: "
                                    "fp32 split 'mixed' 1/2, '3xtf32' 1/3; tf32 1; bf16 2); "
-                                   f"{pk['source']}.  The bf16 figure is cuBLAS under its own power/clock "
-                                   "limits, so a tcgen05 kernel can exceed it; measured_mma_peak is our own "
-                                   "kind::tf32 ceiling (tools/mma_probe.cu), nominal_peak the dense 2250 TF "
-                                   "bf16 datasheet figure, both scaled the same way"),
+                                   f"{pk['source']}.  achieved = FLOPs of the tcgen05 layers / the median per-step sum "
+                                   "of their CUDA-event-timed contraction launches; the direct-gpu layer (VGG conv1_1, "
+                                   "CUDA cores, HBM-bound) is in `layers` against its own roofline"),
                      "fp32_split": fp32_split() if args.precision == "fp32" else None,
                      "measured_mma_peak": mma_peak_for(args.precision),
                      "frac_of_measured_mma_peak": (achieved / mma_peak_for(args.precision)
-                                                   if mma_peak_for(args.precision) else None),
+                                                   if achieved and mma_peak_for(args.precision) else None),
                      "nominal_peak": nominal_peak,
-                     "frac_of_nominal": achieved / nominal_peak},
+                     "frac_of_nominal": achieved / nominal_peak if achieved else None},
+        "layers": layer_rows,
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
-    if args.per_layer:
-        out["layers"] = [{"name": l.name, "method": p.method, "gflop": l.flops() / 1e9, "kernel_ms": km,
-                          "kernel_tflops": l.flops() / (km * 1e-3) / 1e12,
-                          "frac_of_peak": l.flops() / (km * 1e-3) / 1e12 / mode_peak}
-                         for l, p, km in zip(layers, plans, kern_ms)]
-        out["step_ms_median"] = statistics.median(step_ms)
     print(json.dumps(out))
     for p in plans:
         p.close()
-    if info.distributed:
+    if run.distributed:
         import torch.distributed as tdist
         tdist.destroy_process_group()
     return 0
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
+    run = setup_run(args)
+    if args.dry_run:
+        return dry_run(args, run)
+    if args.impl == "reference":
+        return run_reference_arm(args, run)
+    return run_ours(args, run)
 
 
 if __name__ == "__main__":

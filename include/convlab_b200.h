@@ -128,9 +128,11 @@ CL_API cl_status cl_conv_forward_nhwc(cl_plan* plan, const float* d_x, float* d_
 CL_API cl_status cl_conv_forward_host(cl_plan* plan, const float* h_x, float* h_y, void* stream);
 
 /* Asynchronous variant: returns after enqueueing (pinned host buffers recommended); `stream`
- * receives the completion (synchronise it before reading h_y).  The copy-in does not wait
- * for prior work on `stream` -- h_x must hold its data at the call -- only for this plan's
- * previous call, so consecutive calls on different plans overlap their PCIe transfers. */
+ * receives the completion (synchronise it before reading h_y).  The copy-in is ordered after
+ * prior work on `stream` (so a chain of layers through host buffers on one stream is safe:
+ * layer l's D2H into h_y completes before layer l+1's H2D reads it) and after this plan's
+ * previous call.  Independent layers overlap their PCIe transfers when issued on their own
+ * streams. */
 CL_API cl_status cl_conv_forward_host_async(cl_plan* plan, const float* h_x, float* h_y, void* stream);
 
 /* Number of GPU kernel launches the last cl_conv_forward enqueued. */

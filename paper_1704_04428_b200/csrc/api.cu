@@ -95,7 +95,13 @@ struct cl_plan {
     float* wpack = nullptr;
     size_t wpack_bytes = 0;
     float* wraw = nullptr;     // direct-gpu: MKKC fp32 weights as given
-    std::vector<float> wparam; // direct-gpu, 3 -> 16/32/64 channels 3x3: host weights [c][i][j][m] (kernel parameter)
+    // direct-gpu, 3 -> 16/32/64 channels 3x3: host weights [c][i][j][m] passed as a kernel
+    // parameter (constant-bank FFMA operands).  Only filled by cl_conv_set_weights_host (the host
+    // data is at hand; a device-pointer upload never blocks on a D2H copy) and only used by eager
+    // launches: a CUDA graph captures kernel parameters by value, so a captured launch reads the
+    // device weights instead and picks up later set_weights calls like every other method.
+    std::vector<float> wparam;
+    int max_units = 0;         // engine grid cap (cl_conv_set_max_units; 0 = all co-resident units)
     unsigned* flags = nullptr; // stream-K fixup flags, zeroed once, self-resetting
     bool padded_rows = false;  // implicit kn2row in tap-shared (zero-padded row) mode
     int stack_k = 1;           // > 1: padded-row mode with the k taps of a kernel row stacked on N
@@ -112,7 +118,6 @@ struct cl_plan {
     bool shared_streams = false;   // s_in / s_out are the device's shared copy streams (not owned)
     static constexpr int kMaxChunks = 16;
     cudaEvent_t ev_in[kMaxChunks] = {}, ev_comp[kMaxChunks] = {}, ev_start = nullptr, ev_done = nullptr;
-    bool host_started = false;   // a host-buffer call has been enqueued (ev_done is live)
     // Sharing: a plan's flags, own workspace and staging buffers are per-plan state, so calls
     // on one plan are serialised -- host side by `mu`, device side by chaining each call after
     // the previous call's completion event when it arrives on a different stream.
@@ -246,44 +251,6 @@ void mark_done(cl_plan* p, cudaStream_t s) {
 
 // n_images < 0: the plan's batch; otherwise a sub-batch (chunked host pipeline).
 // nhwc: channels-last input and output (implicit kn2row / conv1x1 / accumulating only).
-// Fused prepass (opt-in): the implicit kn2row contraction converts its NCHW input itself in a
-// phase 0 (tc_conv.cuh) instead of a separate prepass launch.  One CTA per SM converting with its
-// eight epilogue warps has ~1/6 of the standalone kernel's memory-level parallelism (6 CTAs of
-// 256 threads per SM), so it is 10-45 % slower on every large layer (VGG conv1_2 0.72 -> 1.04
-// ms); on batch-1 layers it saves a launch's host overhead in eager calls (C1 32 -> 26 us) but
-// costs ~2 us of device time under CUDA-graph replay (C1 17 -> 19 us), which is the device-side
-// measure the report uses -- so it is off by default (profiles/r01_fused_prepass.txt).
-// CLB_FUSED_PREPASS=1: fuse inputs <= 2 MB when every CTA converts at most one tile (else the
-// launcher runs the standalone prepass); =2: always.
-bool fused_prepass_enabled(const cl_conv_desc& d) {
-    static const int mode = std::getenv("CLB_FUSED_PREPASS") ? std::atoi(std::getenv("CLB_FUSED_PREPASS")) : 0;
-    if (mode == 2) return true;
-    if (mode == 1) return (long long)d.n * d.c * d.h * d.w * 4 <= (2ll << 20);
-    return false;
-}
-
-// phase-0 parameters of the NCHW -> split conversion into `xs` (HW pixels per image; with
-// pad > 0 the shared-padding grid Hp x Wp of the tap-shared modes)
-void set_fused_prepass(TcParams& t, const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp) {
-    t.pre_force = std::getenv("CLB_FUSED_PREPASS") && std::atoi(std::getenv("CLB_FUSED_PREPASS")) == 2;
-    const int Hp = pad > 0 ? H + pad : 1, Wp = pad > 0 ? W + pad : H * W;
-    const int HW = pad > 0 ? Hp * Wp : H * W;
-    t.pre_x = x;
-    t.pre_xs = xs;
-    t.pre_n = N;
-    t.pre_c = C;
-    t.pre_hw = HW;
-    t.pre_cp = Cp;
-    t.pre_h = pad > 0 ? H : 1;
-    t.pre_w = pad > 0 ? W : HW;
-    t.pre_wp = Wp;
-    t.pre_pad = pad;
-    t.pre_hwd = make_fastdiv((uint32_t)HW);
-    t.pre_wpd = make_fastdiv((uint32_t)Wp);
-    t.pre_ntx = (int)(((long long)N * HW + kSplitPx - 1) / kSplitPx);
-    t.pre_nty = (Cp + 31) / 32;
-}
-
 // ev_first / ev_last_chunk: record the plan's profile events (begin / end) in this call (a
 // chunked forward brackets all of its chunks with one pair).
 void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images = -1, bool nhwc = false,
@@ -314,7 +281,6 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
     p->launches = 0;
     bool began = false;
     void* scratch = scratch_of(p, ws);
-    bool no_pdl = false;   // a non-kernel node (slack memsets) directly precedes the contraction
     auto tc = [&](const Operand& a, const Operand& b, TcParams t) {
         // PDL right after the prepass kernel (its launch_dependents trigger lets this
         // kernel's prologue overlap the prepass tail); an interposed profile event only
@@ -324,9 +290,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         began = true;
         set_scratch(t, scratch);
         t.flags = p->flags;
-        t.gbar = p->flags + kMaxGrid;
         t.flags_zeroed = 1;
-        if (no_pdl) t.pdl = 0;
+        t.max_units = p->max_units;
         static const int forced_bn = [] {   // experiments: CLB_BN=<multiple of 16 <= 256>
             const char* e = std::getenv("CLB_BN");
             const int v = e ? std::atoi(e) : 0;
@@ -371,14 +336,9 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                     CLB_CUDA(cudaMemsetAsync(static_cast<char*>(xs) + ((size_t)lead + grid_rows) * rb, 0, (size_t)trail * rb, s));
                 }
                 void* grid = static_cast<char*>(xs) + (size_t)lead * rb;
-                const bool fused = !nhwc && p->method != CL_METHOD_KN2ROW_ACC && fused_prepass_enabled(d);
-                if (fused) {
-                    no_pdl = lead + trail > 0;
-                } else {
-                    if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
-                    else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
-                    ++p->launches;
-                }
+                if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                ++p->launches;
                 Operand a = tiled(xs, grid_rows, 1, p->Cp, p->planes);
                 Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
                 TcParams t = base_params(p);
@@ -386,8 +346,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 t.cols = d.m;
                 t.bn = p->bn;
                 t.b_tap3 = 1;
-                static const bool env_tps1 = getenv("CLB_TPS1") && atoi(getenv("CLB_TPS1")) != 0;   // experiment knob
-                t.tps = env_tps1 ? 1 : d.k;
+                t.tps = d.k;
                 t.taps = taps;
                 if (p->stack_k > 1) {
                     // tap-stacked: one k-iteration = kernel row i x one channel block; B rows
@@ -412,17 +371,13 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 t.out = y;
                 t.out_channels = d.m;
                 t.pq_out = p->P * p->Q;
-                if (fused) set_fused_prepass(t, x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp);
                 tc(a, b, t);
                 tc_done();
                 break;
             }
-            const bool fused = !nhwc && p->method != CL_METHOD_KN2ROW_ACC && fused_prepass_enabled(d);
-            if (!fused) {
-                if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s);
-                else launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
-                ++p->launches;
-            }
+            if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s);
+            else launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
+            ++p->launches;
             Operand a = implicit_a(p, xs);
             a.n = d.n;
             Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
@@ -447,7 +402,6 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             } else {
                 t.taps = taps;
                 t.tap_begin = 0;
-                if (fused) set_fused_prepass(t, x, xs, d.n, d.c, d.h, d.w, 0, p->Cp);
                 tc(a, b, t);
             }
             tc_done();
@@ -513,8 +467,9 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             if (nhwc) throw Error(CL_EUNSUPPORTED, "channels-last forward: implicit kn2row / conv1x1 / kn2row-acc only");
             // the dominant (and only) kernel of this method: bracket it for the profile events
             if (p->ev_begin && ev_first) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
+            const bool param = !p->wparam.empty() && !capturing(s);
             launch_direct_conv(x, p->wraw, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, d.stride, p->P, p->Q, s,
-                               p->wparam.empty() ? nullptr : p->wparam.data());
+                               param ? p->wparam.data() : nullptr);
             ++p->launches;
             tc_done();
             break;
@@ -522,40 +477,6 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         default:
             throw Error(CL_EINTERNAL, "unresolved method");
     }
-}
-
-// L2-chunked forward: a large implicit-kn2row layer runs as image chunks whose split operand
-// (the prepass output the contraction reads) fits in L2, reusing one workspace region, so the
-// contraction's operand loads hit L2 (tools/tma_probe4.cu: 67-75 vs ~44 B/clk/SM streaming
-// from HBM) and the split tensor never round-trips HBM.  CLB_L2_CHUNK_MB sets the chunk budget
-// (0 = whole batch).
-void forward_chunked(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, bool nhwc) {
-    // Measured 1.3-2x SLOWER on every VGG / AlexNet layer at 16-80 MB chunks (per-launch ramp
-    // and tail waves dominate; profiles/r01_l2_chunked_forward.txt): off unless set.
-    static const double chunk_mb = [] {
-        const char* e = std::getenv("CLB_L2_CHUNK_MB");
-        return e ? std::atof(e) : 0.0;
-    }();
-    const cl_conv_desc& d = p->d;
-    int nc = d.n;
-    const bool implicit = p->method == CL_METHOD_KN2ROW || p->method == CL_METHOD_CONV1X1;
-    if (chunk_mb > 0 && implicit) {
-        const double pix = p->padded_rows ? (double)(d.h + d.pad) * (d.w + d.pad) : (double)d.h * d.w;
-        const double per_img = pix * (double)row_bytes(p->planes, p->Cp);
-        nc = std::max(1, (int)(chunk_mb * 1e6 / per_img));
-    }
-    if (nc >= d.n) {
-        forward(p, x, y, ws, s, -1, nhwc);
-        return;
-    }
-    const size_t img_in = (size_t)d.c * d.h * d.w, img_out = (size_t)d.m * p->P * p->Q;
-    int launches = 0;
-    for (int n0 = 0; n0 < d.n; n0 += nc) {
-        const int cnt = std::min(nc, d.n - n0);
-        forward(p, x + n0 * img_in, y + n0 * img_out, ws, s, cnt, nhwc, n0 == 0, n0 + cnt == d.n);
-        launches += p->launches;
-    }
-    p->launches = launches;
 }
 
 // direct-gpu parameter-weight kernel: MKKC host weights -> [c][i][j][m]
@@ -686,7 +607,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
                 p->bn_stack = mt * d.k;
             }
         }
-        // stream-K flags [kMaxGrid] + the fused prepass's grid barrier (2 words), all self-resetting
+        // stream-K flags [kMaxGrid], self-resetting (zeroed once here)
         if (cudaMalloc(&p->flags, (kMaxGrid + 8) * sizeof(unsigned)) != cudaSuccess ||
             cudaMemset(p->flags, 0, (kMaxGrid + 8) * sizeof(unsigned)) != cudaSuccess) {
             cudaGetLastError();
@@ -710,12 +631,7 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
             launch_rows_split(d_w, p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);   // MKKC == M x k^2C
         else if (p->method == CL_METHOD_DIRECT) {
             CLB_CUDA(cudaMemcpyAsync(p->wpack, d_w, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
-            if (direct_param_shape(d.c, d.k, d.m, d.stride, p->Q)) {   // host copy for the kernel parameter
-                std::vector<float> h(p->wpack_bytes / sizeof(float));
-                CLB_CUDA(cudaMemcpyAsync(h.data(), d_w, p->wpack_bytes, cudaMemcpyDeviceToHost, s));
-                CLB_CUDA(cudaStreamSynchronize(s));
-                pack_param_weights(p, h.data());
-            }
+            p->wparam.clear();   // device weights: the kernels read p->wraw (stream-ordered, no host copy)
         } else
             launch_pack_weights(d_w, p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s, p->stack_k > 1);
         p->weights_set = true;
@@ -739,6 +655,7 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
             launch_rows_split(static_cast<float*>(dw), p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);
         else if (p->method == CL_METHOD_DIRECT) {
             CLB_CUDA(cudaMemcpyAsync(p->wpack, dw, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
+            p->wparam.clear();
             if (direct_param_shape(d.c, d.k, d.m, d.stride, p->Q)) pack_param_weights(p, h_w);
         }
         else
@@ -768,7 +685,7 @@ cl_status cl_conv_forward(cl_plan* p, const float* d_x, float* d_y, void* d_ws, 
         std::lock_guard<std::mutex> lock(p->mu);
         CLB_CUDA(cudaSetDevice(p->device));
         order_after_previous(p, s);
-        forward_chunked(p, d_x, d_y, d_ws, s, false);
+        forward(p, d_x, d_y, d_ws, s, -1, false);
         mark_done(p, s);
     });
 }
@@ -780,7 +697,7 @@ cl_status cl_conv_forward_nhwc(cl_plan* p, const float* d_x, float* d_y, void* d
         std::lock_guard<std::mutex> lock(p->mu);
         CLB_CUDA(cudaSetDevice(p->device));
         order_after_previous(p, s);
-        forward_chunked(p, d_x, d_y, d_ws, s, true);
+        forward(p, d_x, d_y, d_ws, s, -1, true);
         mark_done(p, s);
     });
 }
@@ -790,11 +707,12 @@ namespace {
 // Host-buffer forward, pipelined over batch chunks on three streams: H2D of chunk i+1
 // (copy-in stream), the convolution of chunk i (caller's stream) and the D2H of chunk i-1
 // (copy-out stream) overlap, so a call costs ~max(H2D, compute, D2H) instead of their sum
-// (PCIe is full duplex).  sync: wait for completion on return (like run_method), and let the
-// copy-in wait for prior work on the caller's stream (host buffers it may produce).  async:
-// return after enqueueing; the copy-in waits only for this plan's previous call (its staging
-// buffers), so calls on different plans (layers) overlap their transfers; the caller's
-// stream receives the completion.
+// (PCIe is full duplex).  The copy-in waits for prior work on the caller's stream in both
+// modes (a previous call's host output may be this call's input: layer l's D2H into h_y must
+// land before layer l+1's H2D reads it as h_x), and, through the plan's ordering, for this
+// plan's previous call (its staging buffers).  sync: wait for completion on return (like
+// run_method).  async: return after enqueueing; the caller's stream receives the completion,
+// so independent layers issued on their own streams overlap their transfers.
 cl_status host_forward(cl_plan* p, const float* h_x, float* h_y, void* stream, bool sync) {
     return guarded([&] {
         require(p && h_x && h_y, "cl_conv_forward_host: null argument");
@@ -858,16 +776,11 @@ cl_status host_forward(cl_plan* p, const float* h_x, float* h_y, void* stream, b
         static cudaEvent_t tev[3 * cl_plan::kMaxChunks + 1] = {};
         if (htrace && !tev[0])
             for (auto& e : tev) CLB_CUDA(cudaEventCreate(&e));
-        if (sync) {
-            // the copy streams must not run ahead of prior work on the caller's stream
-            CLB_CUDA(cudaEventRecord(p->ev_start, s));
-            CLB_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
-            CLB_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
-        } else if (p->host_started) {
-            // staging buffers of this plan: the previous call must have drained them
-            CLB_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_done, 0));
-        }
-        p->host_started = true;
+        // the copy streams must not run ahead of prior work on the caller's stream (which, after
+        // order_after_previous, includes this plan's previous call)
+        CLB_CUDA(cudaEventRecord(p->ev_start, s));
+        CLB_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+        CLB_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
         if (htrace) CLB_CUDA(cudaEventRecord(tev[0], s));
         // all copy-ins are enqueued first, so the H2D engine streams back to back and never
         // waits for the host to enqueue a chunk's kernels (that interleaving cost ~25% of the

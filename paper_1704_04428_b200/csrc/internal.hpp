@@ -57,9 +57,6 @@ void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int
                        cudaStream_t s);
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
                                  cudaStream_t s);
-// the same conversion from explicit phase-0 parameters (the fused prepass's fallback)
-void launch_split_tiles(const float* x, void* xs, int N, int C, int HW, int Cp, int H, int W, int Wp, int pad,
-                        FastDiv hwd, FastDiv wpd, int planes, cudaStream_t s);
 // a[rows][K] -> as[rows][planes][Kp]
 void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s);
 // b[K][cols] -> bs[cols][planes][Kp]

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
     // previous layer's contraction, whose output x is): nothing is touched before it completes
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ SplitSmem<PLANES> sm;
-    split_tile<PLANES, false>(x, xsv, N, C, HW, Cp, H, W, Wp, pad, hwd, wpd, (int)blockIdx.x, (int)blockIdx.y,
+    split_tile<PLANES>(x, xsv, N, C, HW, Cp, H, W, Wp, pad, hwd, wpd, (int)blockIdx.x, (int)blockIdx.y,
                               (int)threadIdx.x, sm);
     // let a programmatically dependent consumer (the tcgen05 kernel) start its prologue;
     // its griddepcontrol.wait still waits for this grid's completion and memory flush
@@ -92,13 +92,6 @@ void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, i
     dim3 grid((unsigned)(((long long)N * HW + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
     launch_split_kernel(planes, grid, s, x, xs, N, C, HW, Cp, 1, HW, HW, 0, make_fastdiv((uint32_t)HW),
                         make_fastdiv((uint32_t)HW));
-    CLB_CUDA(cudaGetLastError());
-}
-
-void launch_split_tiles(const float* x, void* xs, int N, int C, int HW, int Cp, int H, int W, int Wp, int pad,
-                        FastDiv hwd, FastDiv wpd, int planes, cudaStream_t s) {
-    dim3 grid((unsigned)(((long long)N * HW + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
-    launch_split_kernel(planes, grid, s, x, xs, N, C, HW, Cp, H, W, Wp, pad, hwd, wpd);
     CLB_CUDA(cudaGetLastError());
 }
 

@@ -1,7 +1,6 @@
 // split_tile.cuh -- one tile of the NCHW fp32 -> split-operand prepass (128 pixels x 32
-// channels), shared by the standalone prepass kernel (prepass.cu) and the contraction kernel's
-// fused phase 0 (tc_conv.cuh): hi = rna_tf32(x), lo = x - hi (exact in fp32), written as the
-// 128-byte row units the engine's TMA boxes read.
+// channels) of the prepass kernel (prepass.cu): hi = rna_tf32(x), lo = x - hi (exact in fp32),
+// written as the 128-byte row units the engine's TMA boxes read.
 #pragma once
 
 #include <cstdint>
@@ -52,20 +51,12 @@ struct SplitSmem {
     uint32_t bl[PLANES == kPlanesMixed ? kSplitPx : 1][17];
 };
 
-// the 256 threads converting a tile: a whole CTA (standalone) or the contraction kernel's
-// eight epilogue warps (fused phase 0, named barrier 1)
-template <bool FUSED>
-__device__ __forceinline__ void split_sync() {
-    if (FUSED) asm volatile("bar.sync 1, 256;" ::: "memory");
-    else __syncthreads();
-}
-
 // Templated on the operand format so every element is converted exactly once (in the load
 // phase, into shared tiles) and the write phase is plain 32-bit copies: converting per output
 // word made the mixed format's prepass issue-bound (IPC 3.2, DRAM 21 %, ncu on GoogLeNet 1x1).
 // Tile (bx, by) = pixels [128 bx, 128 bx + 128) flattened over (image, pixel) x channels
 // [32 by, 32 by + 32); tid in [0, 256).
-template <int PLANES, bool FUSED>
+template <int PLANES>
 __device__ __forceinline__ void split_tile(const float* __restrict__ x, void* __restrict__ xsv, int N, int C, int HW,
                                            int Cp, int H, int W, int Wp, int pad, const FastDiv& hwd,
                                            const FastDiv& wpd, int bx, int by, int tid, SplitSmem<PLANES>& sm) {
@@ -128,7 +119,7 @@ __device__ __forceinline__ void split_tile(const float* __restrict__ x, void* __
             }
         }
     }
-    split_sync<FUSED>();
+    __syncthreads();
     const long long row_words = kSplit ? 2LL * Cp : (long long)Cp;
     const int nch = Cp - c0 < 32 ? Cp - c0 : 32;        // channels of this tile inside the padded row
     if (PLANES == kPlanesBf16) {                        // bf16 rows: lane = channel

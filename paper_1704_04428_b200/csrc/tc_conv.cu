@@ -85,6 +85,67 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int b
                            " failed with CUresult " + std::to_string((int)r));
 }
 
+namespace {
+
+// Per-device launch configuration of the engine: the >48 KB dynamic smem opt-in (a per-device
+// function attribute) and the co-resident unit limit per (cluster shape, smem size), computed
+// once each under a lock.
+struct DeviceLimits {
+    int units = 0;
+};
+
+const DeviceLimits& device_limits(int cg, int smem, int max_units) {
+    static std::mutex mu;
+    static std::unordered_map<unsigned long long, DeviceLimits> cache;
+    static bool configured[64][3] = {};
+    int dev = 0;
+    CLB_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) throw Error(6, "device index out of range");
+    const unsigned long long key = ((unsigned long long)dev << 40) | ((unsigned long long)cg << 32) |
+                                   ((unsigned long long)(unsigned)smem << 8) | (unsigned)(max_units & 0xff);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (!configured[dev][cg]) {
+        if (cg == 2) {
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        } else {
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        }
+        configured[dev][cg] = true;
+    }
+    int sms = 0;
+    CLB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int units = (sms < kMaxGrid ? sms : kMaxGrid) / cg;
+    if (cg == 2) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * units);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        CLB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, tc_conv_kernel<2, false>, &cfg));
+        if (clusters < units) units = clusters;
+    } else {
+        int per_sm = 0;
+        CLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc_conv_kernel<1, false>, kThreads, smem));
+        if (per_sm * sms < units) units = per_sm * sms;
+    }
+    if (max_units > 0 && max_units < units) units = max_units;
+    if (units < 1) throw Error(2, "tcgen05 engine: no CTA of this configuration fits on the device");
+    return cache[key] = DeviceLimits{units};
+}
+
+}  // namespace
+
 int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cg) {
     if (cg != 1 && cg != 2) throw Error(6, "cta group must be 1 or 2");
     if (p.bn % 16 != 0 || p.bn < 16 || p.bn > 256) throw Error(6, "tile N must be a multiple of 16 in [16,256]");
@@ -139,32 +200,14 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     // VGG conv5_x), neutral on the padded-row ones (profiles/r01_split_issue_sweep.txt)
     static const int env_split_issue = getenv("CLB_SPLIT_ISSUE") ? atoi(getenv("CLB_SPLIT_ISSUE")) : 1;
     p.split_issue = env_split_issue;
-    // Weight-stationary B (single column tile, tiled B): CLB_B_RESIDENT=-1 takes it when it
-    // leaves room for >= 3 A stages, =1 whenever >= 2 remain.  Off by default: the A operand of
-    // the small-M layers is latency-bound on bytes in flight, and the resident B takes the smem
-    // that held them (VGG conv1_2 0.55 -> 0.64 ms; profiles/r01_l2_prefetch_bres_stacked.txt).
-    static const int env_bres = getenv("CLB_B_RESIDENT") ? atoi(getenv("CLB_B_RESIDENT")) : 0;
-    int resident_bytes = 0;
-    if (env_bres != 0 && p.b_resident >= 0 && b.mode == LOAD_TILED && (p.cols + p.bn - 1) / p.bn == 1) {
-        const int rb = k_iters * p.tps * b_rows * kRowBytes;
-        const int a_stage = tc_stage_bytes(0, p.tps);
-        const int min_stages = env_bres == 1 ? 2 : 3;   // (env_bres == -1: auto)
-        if (kSmemBudget - rb - 1024 - 256 >= min_stages * a_stage) resident_bytes = rb;
-    }
-    p.b_resident = resident_bytes > 0 ? 1 : 0;
-    if (p.b_resident) p.split_issue = 0;   // one producer warp: resident B first, then A per stage
     // A boxes of alternate stages issued from two warps (0 and the idle TMEM-allocator warp 2):
     // +0.5-2 % on the padded-row layers (VGG conv1_2 0.508 -> 0.499 ms), neutral on the TMA-im2col
     // ones (profiles/r01_a_issuers_ab.txt).  CLB_A_ISSUERS=1 restores one A warp.
     static const int env_a_iss = getenv("CLB_A_ISSUERS") ? atoi(getenv("CLB_A_ISSUERS")) : 2;
     p.a_issuers = (env_a_iss == 2 && p.split_issue) ? 2 : 1;
-    // measured 5-12 % slower on every padded-row layer (the prefetches compete with the loads
-    // for the TMA unit; profiles/r01_l2_prefetch_bres_stacked.txt): off unless CLB_L2_PREFETCH=1
-    static const int env_l2_prefetch = getenv("CLB_L2_PREFETCH") ? atoi(getenv("CLB_L2_PREFETCH")) : 0;
-    p.l2_prefetch = env_l2_prefetch;
     static const int env_smem = getenv("CLB_SMEM_KB") ? atoi(getenv("CLB_SMEM_KB")) * 1024 : 0;   // experiment knob
-    const int budget = (env_smem > 0 ? env_smem : kSmemBudget) - resident_bytes;
-    const int stage_b_rows = p.b_resident ? 0 : b_rows;   // B rows carried per stage
+    const int budget = env_smem > 0 ? env_smem : kSmemBudget;
+    const int stage_b_rows = b_rows;   // B rows carried per stage
     if (p.bps <= 0) {
         static const int env_bps = getenv("CLB_BPS") ? atoi(getenv("CLB_BPS")) : 0;   // experiment knob
         if (env_bps > 0) p.bps = env_bps;
@@ -185,26 +228,13 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     if (p.num_tiles <= 0) return 0;
     p.chunks_per_tile = (k_iters + p.chunk_iters - 1) / p.chunk_iters;
     const long long total_chunks = (long long)p.num_tiles * p.chunks_per_tile;
-    const int smem = tc_smem_bytes(stage_b_rows, p.tps, p.stages, p.bps, resident_bytes);
-    if (p.pre_x) {   // the fused prepass stages its tiles in the pipeline smem
-        const int need = p.planes == 4 ? (int)sizeof(SplitSmem<4>) : p.planes == 2 ? (int)sizeof(SplitSmem<2>)
-                                                                                    : (int)sizeof(SplitSmem<1>);
-        if (p.stages * p.bps * tc_stage_bytes(stage_b_rows, p.tps) < need || !p.gbar)
-            throw Error(6, "fused prepass: pipeline smem too small for a conversion tile");
-    }
-    static bool configured[3] = {false, false, false};
-    if (!configured[cg]) {
-        if (cg == 2) {
-            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        } else {
-            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            CLB_CUDA(cudaFuncSetAttribute(tc_conv_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        }
-        configured[cg] = true;
-    }
-    const int sms = num_sms();
-    int units = (sms < kMaxGrid ? sms : kMaxGrid) / cg;      // scheduling units (CTAs or CTA pairs)
+    const int smem = tc_smem_bytes(stage_b_rows, p.tps, p.stages, p.bps);
+    // The stream-K fixup makes CTAs wait on each other, so every CTA of the grid must be
+    // co-resident: the unit count is capped at what the occupancy calculator says fits at once
+    // for this kernel, smem size and cluster shape (on the current device; attributes and
+    // limits are per device, configured once each).
+    const DeviceLimits& lim = device_limits(cg, smem, p.max_units);
+    int units = lim.units;      // scheduling units (CTAs or CTA pairs)
     if (total_chunks < units) units = (int)total_chunks;
     // Fewer tiles than units (latency-bound problems): pick the split s (pieces per tile) by a
     // cost model in chunk times -- ceil(chunks / units) on the critical path, plus a fixup of
@@ -286,24 +316,16 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
         sk_memo[sk_key] = p.sk_units;
     }
     const int grid = units * cg;
-    int launched = 1;
-    if (p.pre_x && !p.pre_force && (long long)p.pre_ntx * p.pre_nty > grid) {
-        // the fused conversion would give CTAs several tiles each at 1/6 of the standalone
-        // kernel's memory parallelism (sweep k1: 30 -> 34 us): convert standalone, then PDL
-        launch_split_tiles(p.pre_x, p.pre_xs, p.pre_n, p.pre_c, p.pre_hw, p.pre_cp, p.pre_h, p.pre_w, p.pre_wp,
-                           p.pre_pad, p.pre_hwd, p.pre_wpd, p.planes, s);
-        p.pre_x = nullptr;
-        p.pdl = 1;
-        launched = 2;
-    }
     if (!p.partials || !p.flags) throw Error(6, "stream-K scratch missing");
     if (!p.flags_zeroed) CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));
     // PDL only when nothing was enqueued in between (the memset would be the predecessor)
     if (!p.flags_zeroed) p.pdl = 0;
-    // The stream-K fixup makes CTAs wait on each other, so all must be resident: grid <= one
-    // CTA per SM at 1 CTA/SM (smem-limited).  CG = 1 additionally asks for a cooperative launch;
-    // CG = 2 uses a plain cluster launch (cooperative + cluster is rejected under ncu).  A CTA
-    // that could never be scheduled would trip the 4 s watchdog (launch error, not a hang).
+    // The stream-K fixup makes CTAs wait on each other, so all must be resident: the grid is
+    // capped at the co-resident limit above.  CG = 1 additionally asks for a cooperative launch
+    // (the driver then refuses a grid that cannot be co-resident); CG = 2 uses a plain cluster
+    // launch (cooperative + cluster is rejected under ncu), sized by
+    // cudaOccupancyMaxActiveClusters.  A CTA that could still never be scheduled (other
+    // kernels holding SMs indefinitely) trips the 4 s watchdog: a launch error, not a hang.
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -380,7 +402,7 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
                 "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
                 "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us | "
                 "SM clock %.0f MHz (CTA cycles / CTA ns)\n",
-                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, p.b_resident, p.a_issuers, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, p.sk_units, avg[0], 100 * avg[1] / avg[0],
+                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, 0, p.a_issuers, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, p.sk_units, avg[0], 100 * avg[1] / avg[0],
                 avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5], 100 * avg[11] / avg[5], avg[8], (t_out - t_in) * 1e-3,
                 (t_in_max - t_in) * 1e-3, ev_ms * 1e3, mhz);
         if (const char* dump = getenv("CLB_TRACE_DUMP")) {   // raw per-CTA records, appended
@@ -411,7 +433,7 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
                 "%llu, wait tmem %llu) | epilogue %llu (wait tfull %llu, store %llu, fixup wait %llu) cyc\n",
                 slow, (r[10] - t_in) * 1e-3, r[0], r[1], rl[2], rl[3], rl[4], r[5], r[6], r[7], r[11]);
     }
-    return launched;
+    return 1;
 }
 
 size_t tc_scratch_bytes() {

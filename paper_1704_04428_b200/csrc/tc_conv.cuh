@@ -85,11 +85,6 @@ struct TcParams {
     int tps;                   // taps per stage (1 = one tap per stage)
     int split_issue;           // A and B TMA loads issued by two warps (0 and 3), 2 arrivals per stage
     int a_issuers;             // 2: A loads of alternate stages from warps 0 and 2 (needs split_issue)
-    int l2_prefetch;           // padded-row modes: L2-prefetch the next piece's A rows (CLB_L2_PREFETCH)
-    // weight-stationary: a single column tile's B (all k-iterations) is loaded once per CTA
-    // into shared memory and only A streams through the stages (B was ~40 % of the stage bytes
-    // on small-M layers, whose operand delivery bounds them)
-    int b_resident;
     int fixup_smem;            // stream-K finisher stages partner partials in smem (bulk copy)
     int bps;                   // k-iterations ("sub-stages") per pipeline stage: one barrier
                                // round trip per bps TMA box pairs (chunk_iters % bps == 0)
@@ -116,21 +111,13 @@ struct TcParams {
     int sk_chunks;             // chunks of tiles [dp_tiles, num_tiles), split contiguously (stream-K)
     int sk_units;              // scheduling units sharing the stream-K chunks (<= grid units; the
                                // rest only run data-parallel tiles): chosen so no tile splits 3 ways
+    int max_units;             // cap on the scheduling units (0 = every co-resident unit): lets
+                               // independent launches share the SMs (concurrent small layers)
     float* partials;           // [gridDim.x][128][bn] tile-tail partial sums
     unsigned* flags;           // [gridDim.x], 0 at launch; 1 = partial ready (the finisher resets it)
     int flags_zeroed;          // flags are known to be 0 (self-resetting plan buffer): no memset
     int pdl;                   // launched as a programmatic dependent: wait before touching inputs
     unsigned long long* trace; // diagnostics (CLB_TRACE=1): per-CTA role wait cycles, else null
-    // fused NCHW -> split prepass (phase 0, pre_x != null): the eight epilogue warps of every
-    // CTA convert tiles of 128 pixels x 32 channels (split_tile.cuh) through the still idle
-    // pipeline smem, then a grid barrier publishes the split operand to every CTA's TMA loads
-    const float* pre_x;
-    void* pre_xs;
-    int pre_n, pre_c, pre_hw, pre_cp, pre_h, pre_w, pre_wp, pre_pad;
-    FastDiv pre_hwd, pre_wpd;
-    int pre_ntx, pre_nty;      // tile grid (pixels / 128, padded channels / 32)
-    unsigned* gbar;            // [0] arrivals, [1] sense: self-resetting, plan-owned, zeroed once
-    int pre_force;             // fuse even when CTAs would convert several tiles each
 };
 
 // Contiguous chunk range of CTA b: [chunk_start(b), chunk_start(b+1)).
@@ -149,8 +136,8 @@ __host__ inline int tc_num_stages(int b_rows, int tps, int bps = 1, int budget =
     return s > 8 ? 8 : s;
 }
 
-__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages, int bps = 1, int resident_bytes = 0) {
-    return 1024 /*align slack*/ + stages * bps * tc_stage_bytes(b_rows, tps) + resident_bytes + 256 /*barriers*/;
+__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages, int bps = 1) {
+    return 1024 /*align slack*/ + stages * bps * tc_stage_bytes(b_rows, tps) + 256 /*barriers*/;
 }
 
 // TMEM accumulator buffers: 4 when they fit (BN <= 128), else ping-pong.  Extra buffers let
@@ -208,27 +195,6 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 
 __device__ __forceinline__ void epi_bar_sync() {   // the 8 epilogue warps only
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-}
-
-// Sense-reversal grid barrier over a persistent grid (every CTA resident: one per SM).  The
-// arrival count returns to 0 and the sense flips once per barrier, so the two words stay valid
-// across launches without a memset.  __threadfence before the arrival publishes the CTA's
-// writes (bar.sync orders its other threads' writes before thread 0's fence).
-__device__ __forceinline__ void grid_barrier(unsigned* gbar, unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned target = ld_acquire_u32(gbar + 1) ^ 1u;
-        __threadfence();
-        if (atomicAdd(gbar, 1u) == nblocks - 1u) {
-            *reinterpret_cast<volatile unsigned*>(gbar) = 0u;
-            st_release_u32(gbar + 1, target);
-        } else {
-            const uint64_t t0 = globaltimer_ns();
-            while (ld_acquire_u32(gbar + 1) != target)
-                if (globaltimer_ns() - t0 > 4000000000ull) __trap();
-        }
-    }
-    __syncthreads();
 }
 
 // A piece = the part of one tile's chunk range [c_lo, c_hi) that falls in this CTA's range.
@@ -347,29 +313,24 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int b_rows = bn / CG;                   // B rows this CTA loads
     const int tps = p.tps;
     const int a_bytes = tc_a_bytes(tps);          // A region of one stage (128 + tps - 1 rows)
-    const bool bres = p.b_resident != 0;
-    const int b_unit = tps * b_rows * kRowBytes;  // B rows of one k-iteration (tps taps)
-    const int b_bytes = bres ? 0 : b_unit;        // ... carried in each stage unless resident
+    const int b_bytes = tps * b_rows * kRowBytes; // B rows of one k-iteration (tps taps)
     const int stage_bytes = a_bytes + b_bytes;    // one sub-stage (one k-iteration)
     const int bps = p.bps;
     const int group_bytes = bps * stage_bytes;    // one pipeline stage
     const uint32_t stage_tx = (uint32_t)(tc_a_box_rows(tps) * kRowBytes + b_bytes);
     const int k_iters = (p.taps / tps) * p.kblocks;   // k-iterations per tile
-    uint8_t* const bres_smem = smem + stages * group_bytes;   // resident B: [k-iteration][b_unit]
-    const int bres_bytes = bres ? k_iters * b_unit : 0;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;       // scheduling unit
     const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * group_bytes + bres_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * group_bytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + stages;
     uint64_t* tfull = bars + 2 * stages;        // [nbuf]
     uint64_t* tempty = bars + 2 * stages + 4;   // [nbuf]
-    uint64_t* bres_full = bars + 2 * stages + 8;   // resident B landed
-    uint64_t* fix_bar = bars + 2 * stages + 9;     // stream-K partial staged in smem (finisher)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 10);
+    uint64_t* fix_bar = bars + 2 * stages + 8;     // stream-K partial staged in smem (finisher)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 9);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t ncols = tmem_cols_for(bn);
@@ -386,7 +347,6 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], CG * (kEpiThreads / 32));
         }
-        mbar_init(bres_full, 1);
         mbar_init(fix_bar, 1);
         fence_barrier_init();
     }
@@ -417,32 +377,6 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // buffers) are only touched after this point.
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
 
-    if (p.pre_x) {
-        // ---- phase 0: fused NCHW -> split prepass (replaces the standalone prepass launch) ----
-        if (warp >= 4) {
-            const int tid = (int)threadIdx.x - 4 * 32;
-            const int ntiles = p.pre_ntx * p.pre_nty;
-            auto run_pre = [&](auto pl_c) {
-                constexpr int PL = decltype(pl_c)::value;
-                SplitSmem<PL>& sm = *reinterpret_cast<SplitSmem<PL>*>(smem);
-                for (int t = (int)blockIdx.x; t < ntiles; t += (int)gridDim.x) {
-                    const int by = t / p.pre_ntx, bx = t - by * p.pre_ntx;
-                    split_tile<PL, true>(p.pre_x, p.pre_xs, p.pre_n, p.pre_c, p.pre_hw, p.pre_cp, p.pre_h, p.pre_w,
-                                         p.pre_wp, p.pre_pad, p.pre_hwd, p.pre_wpd, bx, by, tid, sm);
-                    epi_bar_sync();   // the next tile overwrites the staging
-                }
-            };
-            if (planes == 4) run_pre(std::integral_constant<int, 4>{});
-            else if (planes == 2) run_pre(std::integral_constant<int, 2>{});
-            else if (planes == 3) run_pre(std::integral_constant<int, 3>{});
-            else run_pre(std::integral_constant<int, 1>{});
-        }
-        // generic smem / global writes above -> async-proxy (TMA) writes and reads below
-        fence_proxy_async();
-        grid_barrier(p.gbar, gridDim.x);
-        fence_proxy_async();
-    }
-
     if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0 || (warp == 3 && p.split_issue) || (warp == 2 && p.a_issuers == 2)) {
         // ------------------------------------------------------------ TMA producer ----
@@ -450,7 +384,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // warp 0 loads A and warp 3 loads B (TMA im2col boxes are slow to deliver from a single
         // issuing thread: tools/tma_probe3.cu 37 -> 43 B/clk per SM with two issuers).
         {
-            const bool do_a = warp == 0 || warp == 2, do_b = !bres && (warp == 3 || !p.split_issue);
+            const bool do_a = warp == 0 || warp == 2, do_b = warp == 3 || !p.split_issue;
             // two A issuers: warp 0 takes the even stages of the sequence, warp 2 the odd ones
             // (each stage still gets exactly one A arrival); the B warp takes every stage
             const uint32_t a_par = warp == 2 ? 1u : 0u;
@@ -463,47 +397,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             long long w_empty = 0;
             const long long t_start = clock64();
             if (TRACE && lane_id() == 0 && warp == 0) p.trace[blockIdx.x * kTraceSlots + 8] = (unsigned long long)(t_start - t_entry);
-            if (bres && warp == 0) {
-                // weight-stationary: the (single) column tile's B for every k-iteration, once
-                if (elect_one()) {
-                    const OperandCoord cb = operand_coord(p.b_mode, p.b_tap3, (int)rank * b_rows, p.P, p.Q, p.pad);
-                    uint64_t* bar = bres_full;
-                    uint32_t lbar = 0;
-                    if constexpr (CG == 2) {
-                        lbar = mapa_shared(smem_u32(bres_full), 0);
-                        if (leader) mbar_arrive_expect_tx(bres_full, (uint32_t)(CG * bres_bytes));
-                    } else {
-                        mbar_arrive_expect_tx(bres_full, (uint32_t)bres_bytes);
-                    }
-                    for (int it = 0; it < k_iters; ++it) {
-                        const int g2 = p.tap_begin / tps + it / p.kblocks;
-                        const int kb2 = it - (it / p.kblocks) * p.kblocks;
-                        uint8_t* dst = bres_smem + it * b_unit;
-                        if constexpr (CG == 2) tma_load_3d_2sm(&map_b, lbar, dst, kb2 * p.row_elems, cb.c1, cb.tap3 ? g2 * tps : 0);
-                        else tma_load_3d(&map_b, bar, dst, kb2 * p.row_elems, cb.c1, cb.tap3 ? g2 * tps : 0);
-                    }
-                }
-                __syncwarp();
-            }
             Sched sch(p, unit, nunits);
             Piece pc;
             while (sch.next(pc)) {
                 const int mt = pc.tile / p.n_col_tiles;
                 const int nt = pc.tile - mt * p.n_col_tiles;
-                if (p.l2_prefetch && warp == 0 && p.a_mode == LOAD_TILED && p.a_row_shift) {
-                    // padded-row modes: pull the NEXT piece's A rows (all kernel rows, all channel
-                    // blocks) into L2 now, so its loads hit L2 instead of waiting on HBM latency
-                    Sched nx = sch;
-                    Piece pn;
-                    if (nx.next(pn) && elect_one()) {
-                        const int r0 = (pn.tile / p.n_col_tiles) * tile_rows + (int)rank * p.row_step + p.a_row_base;
-                        const int nrow = p.ksize == 1 ? p.taps : p.taps / p.ksize;   // kernel rows
-                        for (int i = 0; i < nrow; ++i)
-                            for (int kb2 = 0; kb2 < p.kblocks; ++kb2)
-                                tma_prefetch_3d(&map_a, kb2 * p.row_elems, r0 + i * p.a_row_shift, 0);
-                    }
-                    __syncwarp();
-                }
                 const OperandCoord ca =
                     operand_coord(p.a_mode, p.a_tap3, mt * tile_rows + (int)rank * p.row_step, p.P, p.Q, p.pad);
                 const OperandCoord cb = operand_coord(p.b_mode, p.b_tap3, nt * bn + (int)rank * b_rows, p.P, p.Q, p.pad);
@@ -620,9 +518,6 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint64_t st_step = (uint64_t)(group_bytes >> 4);
             const uint64_t sub_step = (uint64_t)(stage_bytes >> 4);
             const uint64_t b_off = (uint64_t)(a_bytes >> 4);
-            const uint64_t bres_desc = umma_desc_kmajor(smem_u32(bres_smem), kRowBytes);
-            const uint64_t bres_step = (uint64_t)(b_unit >> 4);
-            if (bres) mbar_wait(bres_full, 0);
             const uint64_t tap_b = (uint64_t)(b_rows * 8);
             long long w_full = 0, w_tempty = 0;
             const long long t_start = clock64();
@@ -703,11 +598,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         if (TRACE) w_full += clock64() - t0;
                         tc_fence_after();
                         if (elect_one()) {
-                            // B of sub-stage sb: in the stage, or the resident copy of k-iteration it + sb
-                            auto dbs = [&](int sb) {
-                                return bres ? bres_desc + (uint64_t)(it + sb) * bres_step
-                                            : dstage + (uint64_t)sb * sub_step + b_off;
-                            };
+                            auto dbs = [&](int sb) { return dstage + (uint64_t)sb * sub_step + b_off; };   // B of sub-stage sb
                             issue(d_tmem, dstage, dbs(0), it > c0 ? 1u : 0u);
                             if (nsub > 1) issue(d_tmem, dstage + sub_step, dbs(1), 1u);
 #pragma unroll 1

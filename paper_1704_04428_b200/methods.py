@@ -201,46 +201,91 @@ class ConvPlan:
         return int(_lib.lib().cl_conv_last_launch_count(self._h))
 
     def set_weights(self, w, stream=None):
-        import torch
-        assert w.is_cuda and w.dtype == torch.float32 and w.is_contiguous()
         L = self.layer
-        assert tuple(w.shape) == (L.kernel_count, L.kernel_size, L.kernel_size, L.channels), w.shape
+        self._check_device_tensor(w, (L.kernel_count, L.kernel_size, L.kernel_size, L.channels), "w")
         _lib.check(_lib.lib().cl_conv_set_weights(self._h, ctypes.c_void_p(w.data_ptr()), self._stream(stream)))
         self._w = w  # keep alive until the async pack completes
 
+    def set_weights_host(self, w_host, stream=None):
+        """MKKC weights from a host tensor (cl_conv_set_weights_host: synchronous upload)."""
+        L = self.layer
+        self._check_host_tensor(w_host, L.kernel_count * L.kernel_size * L.kernel_size * L.channels, "w_host")
+        _lib.check(_lib.lib().cl_conv_set_weights_host(self._h, ctypes.c_void_p(w_host.data_ptr()),
+                                                       self._stream(stream)))
+
     def output_shape(self):
         return (self.layer.batch, self.layer.kernel_count, *self.out_hw)
+
+    def _check_device_tensor(self, t, shape, what):
+        """Every buffer handed to the C ABI: fp32, contiguous, on this plan's device, exactly the
+        expected shape (a wrong buffer would make the kernels read or write out of bounds)."""
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{what}: expected a torch tensor, got {type(t).__name__}")
+        if not t.is_cuda or t.device.index != self.device:
+            raise ValueError(f"{what}: must be on cuda:{self.device}, got {t.device}")
+        if t.dtype != torch.float32:
+            raise ValueError(f"{what}: must be float32, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what}: must be contiguous")
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{what}: shape {tuple(t.shape)} != expected {tuple(shape)}")
+
+    def _check_host_tensor(self, t, numel, what):
+        import torch
+        if not isinstance(t, torch.Tensor) or t.is_cuda:
+            raise ValueError(f"{what}: expected a host (CPU) torch tensor")
+        if t.dtype != torch.float32 or not t.is_contiguous():
+            raise ValueError(f"{what}: must be contiguous float32")
+        if t.numel() != numel:
+            raise ValueError(f"{what}: {t.numel()} elements != expected {numel}")
+
+    def input_shape(self, layout: str = "nchw"):
+        L = self.layer
+        return ((L.batch, L.channels, L.height, L.width) if layout == "nchw"
+                else (L.batch, L.height, L.width, L.channels))
 
     def forward(self, x, y=None, workspace=None, stream=None, layout: str = "nchw"):
         """layout "nchw" (the reference's CHW images stacked) or "nhwc" (channels last, the
         reference's HWC layout; implicit kn2row / conv1x1 / kn2row-acc plans)."""
         import torch
         L = self.layer
-        assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
         if layout not in ("nchw", "nhwc"):
             raise ValueError(f"layout must be 'nchw' or 'nhwc', got '{layout}'")
-        if layout == "nchw":
-            assert tuple(x.shape) == (L.batch, L.channels, L.height, L.width), x.shape
-            out_shape = self.output_shape()
-        else:
-            assert tuple(x.shape) == (L.batch, L.height, L.width, L.channels), x.shape
-            out_shape = (L.batch, *self.out_hw, L.kernel_count)
+        self._check_device_tensor(x, self.input_shape(layout), "x")
+        out_shape = self.output_shape() if layout == "nchw" else (L.batch, *self.out_hw, L.kernel_count)
         if y is None:
             y = torch.empty(out_shape, device=x.device, dtype=torch.float32)
+        self._check_device_tensor(y, out_shape, "y")
+        if workspace is not None:
+            if not workspace.is_cuda or workspace.device.index != self.device or not workspace.is_contiguous():
+                raise ValueError(f"workspace: must be a contiguous tensor on cuda:{self.device}")
+            have = workspace.numel() * workspace.element_size()
+            if have < self.workspace_bytes():
+                raise ValueError(f"workspace: {have} bytes < required {self.workspace_bytes()}")
         ws = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else None
         fn = _lib.lib().cl_conv_forward if layout == "nchw" else _lib.lib().cl_conv_forward_nhwc
         _lib.check(fn(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), ws, self._stream(stream)))
         return y
 
+    def _check_host_io(self, x_host, y_host):
+        L = self.layer
+        self._check_host_tensor(x_host, L.batch * L.channels * L.height * L.width, "x_host")
+        self._check_host_tensor(y_host, L.batch * L.kernel_count * self.out_hw[0] * self.out_hw[1], "y_host")
+
     def forward_host_async(self, x_host, y_host, stream=None):
         """Host-buffer call that returns after enqueueing (synchronise `stream` before reading
-        y_host); consecutive calls on different plans overlap their transfers."""
+        y_host).  The copy-in is ordered after prior work on `stream` (so a previous layer's
+        host output can be this call's input); independent layers overlap their transfers when
+        each is issued on its own stream."""
+        self._check_host_io(x_host, y_host)
         _lib.check(_lib.lib().cl_conv_forward_host_async(self._h, ctypes.c_void_p(x_host.data_ptr()),
                                                          ctypes.c_void_p(y_host.data_ptr()), self._stream(stream)))
         return y_host
 
     def forward_host(self, x_host, y_host, stream=None):
         """End-to-end host-buffer call (H2D + forward + D2H, synchronous)."""
+        self._check_host_io(x_host, y_host)
         _lib.check(_lib.lib().cl_conv_forward_host(self._h, ctypes.c_void_p(x_host.data_ptr()),
                                                    ctypes.c_void_p(y_host.data_ptr()), self._stream(stream)))
         return y_host

@@ -203,10 +203,8 @@ def test_one_contraction_per_call(oracle, clb, torch_cuda):
     torch = torch_cuda
     layer = clb.LayerConfig("l", 3, 6, 6, 2, 3, batch=1)
     x, w = oracle.make_problem(1, 3, 6, 6, 2, 3, 140)
-    # kn2row-gpu: prepass + contraction, or ONE launch when the opt-in fused prepass folds the
-    # conversion of an input this small into the contraction (api.cu fused_prepass_enabled)
-    fused = os.environ.get("CLB_FUSED_PREPASS", "0") in ("1", "2")
-    expect = {"kn2row-gpu": 1 if fused else 2, "kn2row-explicit-gpu": 3, "kn2col-gpu": 3, "im2col-gpu": 2, "im2row-gpu": 2,
+    # kn2row-gpu: the NCHW -> split prepass + ONE contraction
+    expect = {"kn2row-gpu": 2, "kn2row-explicit-gpu": 3, "kn2col-gpu": 3, "im2col-gpu": 2, "im2row-gpu": 2,
               "kn2row-acc-gpu": 10,
               "direct-gpu": 1}
     for method, n in expect.items():
@@ -379,7 +377,7 @@ print(json.dumps(out))
 '''
 
 
-@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs", "fused", "fused_auto"])
+@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs"])
 def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     """The implicit kernel's tap-shared mode (zero-padded NHWC rows, one A box of 128+k-1 rows
     per kernel row, taps through row-shifted UMMA descriptors), forced on and off via
@@ -388,12 +386,10 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     "stacked" forces the tap-stacked variant (the k taps of a kernel row as column blocks of one
     MMA, shift-add across rows in the epilogue) wherever it applies (k = 3/5, k x M <= 256),
     including multi-chunk K, stream-K split tiles, M not a multiple of 16 and pad 0 / pad > k/2;
-    the launch trace proves both k = 3 and k = 5 instantiations ran.  "knobs" turns on the
-    measured-negative, default-off paths so they stay correct: weight-stationary B
-    (CLB_B_RESIDENT), the L2 prefetch of the next piece (CLB_L2_PREFETCH), the L2-chunked
-    forward (CLB_L2_CHUNK_MB, one image per chunk here) and a single A-issuing warp; "fused"
-    forces the contraction's phase-0 conversion (grid barrier) on every shape, "fused_auto" the
-    opt-in small-input rule with its standalone fallback."""
+    the launch trace proves both k = 3 and k = 5 instantiations ran.  "knobs" turns the
+    remaining A/B switches to their non-default side so they stay correct: one producer warp
+    for A and B (CLB_SPLIT_ISSUE=0), stream-K partials added from global memory
+    (CLB_FIXUP_SMEM=0) and stream-K ranges over all units (CLB_SK_UNITS=0)."""
     import json
     import os
     import subprocess
@@ -405,16 +401,15 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     env = {"1": dict(CLB_PADDED_ROWS="1"), "0": dict(CLB_PADDED_ROWS="0"),
            "stacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1"),
            "unstacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="0"),
-           "knobs": dict(CLB_PADDED_ROWS="1", CLB_B_RESIDENT="1", CLB_L2_PREFETCH="1", CLB_L2_CHUNK_MB="0.01",
-                         CLB_A_ISSUERS="1", CLB_TRACE="1"),
-           "fused": dict(CLB_FUSED_PREPASS="2"), "fused_auto": dict(CLB_FUSED_PREPASS="1")}[mode]
+           "knobs": dict(CLB_PADDED_ROWS="1", CLB_SPLIT_ISSUE="0", CLB_FIXUP_SMEM="0", CLB_SK_UNITS="0",
+                         CLB_TRACE="1")}[mode]
     r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, **env))
     assert r.returncode == 0, r.stderr[-3000:]
     if mode == "stacked":
         assert "stack=3" in r.stderr and "stack=5" in r.stderr, r.stderr[-2000:]
     if mode == "knobs":
-        assert "bres=1" in r.stderr, r.stderr[-2000:]
+        assert "aiss=1" in r.stderr, r.stderr[-2000:]
     for res in json.loads(r.stdout.strip().splitlines()[-1]):
         if res["precision"] == "fp32":
             assert res["rel_l2"] <= FP32_L2 and res["max_rel"] <= FP32_MAX, (mode, res)
@@ -706,3 +701,103 @@ def test_cuda_graph_capture_and_replay(oracle, clb, torch_cuda, shape):
         y2 = plan.forward(xd, stream=torch.cuda.Stream())  # eager again, different stream
         torch.cuda.synchronize()
         _check_fp32(oracle, y2.cpu().numpy(), oracle.conv_batch(x, w), "eager after graph")
+
+
+@pytest.mark.parametrize("method,shape", [("direct-gpu", (2, 3, 16, 24, 64, 3)), ("direct-gpu", (2, 3, 12, 12, 32, 3)),
+                                          ("kn2row-gpu", (2, 32, 14, 14, 64, 3)), ("im2col-gpu", (2, 8, 9, 9, 16, 3))])
+@pytest.mark.parametrize("upload", ["device", "host"])
+def test_graph_replay_sees_new_weights(oracle, clb, torch_cuda, method, shape, upload):
+    """A captured forward replays against the plan's CURRENT weights: set_weights /
+    set_weights_host between replays are picked up (direct-gpu's kernel-parameter weights are
+    never baked into a graph; its eager launches use them only after a host upload)."""
+    torch = torch_cuda
+    N, C, H, W, M, k = shape
+    layer = clb.LayerConfig("gw", C, H, W, M, k, batch=N)
+    x, w0 = oracle.make_problem(N, C, H, W, M, k, 80)
+    _, w1 = oracle.make_problem(N, C, H, W, M, k, 81)
+
+    def upload_w(plan, w):
+        if upload == "device":
+            plan.set_weights(torch.from_numpy(w).cuda())
+        else:
+            plan.set_weights_host(torch.from_numpy(w))
+        torch.cuda.synchronize()
+
+    with clb.ConvPlan(layer, method) as plan:
+        upload_w(plan, w0)
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty(plan.output_shape(), device="cuda")
+        ws = torch.empty(max(plan.workspace_bytes(), 4), dtype=torch.uint8, device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            plan.forward(xd, yd, ws)
+        torch.cuda.synchronize()
+        _check_fp32(oracle, yd.cpu().numpy(), oracle.conv_batch(x, w0), "eager w0")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            plan.forward(xd, yd, ws)
+        g.replay()
+        torch.cuda.synchronize()
+        _check_fp32(oracle, yd.cpu().numpy(), oracle.conv_batch(x, w0), "replay w0")
+        upload_w(plan, w1)
+        g.replay()
+        torch.cuda.synchronize()
+        _check_fp32(oracle, yd.cpu().numpy(), oracle.conv_batch(x, w1), "replay after set_weights")
+        y2 = plan.forward(xd)                                # eager after the update
+        torch.cuda.synchronize()
+        _check_fp32(oracle, y2.cpu().numpy(), oracle.conv_batch(x, w1), "eager w1")
+
+
+def test_plan_rejects_bad_buffers(clb, torch_cuda):
+    """ConvPlan validates every buffer before it reaches the C ABI (shape, dtype, contiguity,
+    device, workspace size, host sizes)."""
+    torch = torch_cuda
+    layer = clb.LayerConfig("v", 8, 10, 10, 16, 3, batch=2)
+    with clb.ConvPlan(layer, "kn2row-gpu") as plan:
+        plan.set_weights(torch.zeros((16, 3, 3, 8), device="cuda"))
+        x = torch.zeros((2, 8, 10, 10), device="cuda")
+        with pytest.raises(ValueError, match="shape"):
+            plan.forward(x, torch.zeros((2, 16, 10, 9), device="cuda"))
+        with pytest.raises(ValueError, match="float32"):
+            plan.forward(x, torch.zeros((2, 16, 10, 10), device="cuda", dtype=torch.float64))
+        with pytest.raises(ValueError, match="contiguous"):
+            plan.forward(x, torch.zeros((2, 10, 10, 16), device="cuda").permute(0, 3, 1, 2))
+        with pytest.raises(ValueError, match="cuda"):
+            plan.forward(x, torch.zeros((2, 16, 10, 10)))
+        with pytest.raises(ValueError, match="workspace"):
+            plan.forward(x, None, torch.zeros(16, dtype=torch.uint8, device="cuda"))
+        with pytest.raises(ValueError, match="x_host"):
+            plan.forward_host(torch.zeros(5), torch.zeros(2 * 16 * 100))
+        with pytest.raises(ValueError, match="y_host"):
+            plan.forward_host(torch.zeros(2 * 8 * 100), torch.zeros(7))
+        with pytest.raises(ValueError, match="shape"):
+            plan.set_weights(torch.zeros((16, 3, 3, 7), device="cuda"))
+
+
+def test_host_async_chain_through_host_buffers(oracle, clb, torch_cuda):
+    """Two layers chained through HOST buffers on one stream: layer 1's D2H into h1 must land
+    before layer 2's H2D reads h1 (cl_conv_forward_host_async orders its copy-in after prior
+    work on the caller's stream).  Repeated with fresh inputs so a stale h1 would show."""
+    torch = torch_cuda
+    l1 = clb.LayerConfig("a", 16, 24, 24, 32, 3, batch=8)
+    l2 = clb.LayerConfig("b", 32, 24, 24, 24, 3, batch=8)
+    _, w1 = oracle.make_problem(8, 16, 24, 24, 32, 3, 90)
+    _, w2 = oracle.make_problem(8, 32, 24, 24, 24, 3, 91)
+    s = torch.cuda.Stream()
+    with clb.ConvPlan(l1) as p1, clb.ConvPlan(l2) as p2:
+        p1.set_weights(torch.from_numpy(w1).cuda())
+        p2.set_weights(torch.from_numpy(w2).cuda())
+        torch.cuda.synchronize()
+        h0 = torch.empty((8, 16, 24, 24)).pin_memory()
+        h1 = torch.zeros((8, 32, 24, 24)).pin_memory()
+        h2 = torch.empty((8, 24, 24, 24)).pin_memory()
+        for seed in (92, 93, 94):
+            x, _ = oracle.make_problem(8, 16, 24, 24, 32, 3, seed)
+            h0.copy_(torch.from_numpy(x))
+            p1.forward_host_async(h0, h1, s)
+            p2.forward_host_async(h1, h2, s)
+            s.synchronize()
+            mid = oracle.conv_batch(x, w1)
+            _check_fp32(oracle, h1.numpy(), mid, f"layer 1 seed {seed}")
+            _check_fp32(oracle, h2.numpy(), oracle.conv_batch(h1.numpy(), w2), f"layer 2 seed {seed}")

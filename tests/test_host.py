@@ -313,3 +313,51 @@ def test_bench_reference_arm_json_contract():
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_bench_reference_arm_never_loads_the_package():
+    """The reference arm times the reference alone: bench.py must not import (and so must not
+    load the .so of) this repo's package on that path."""
+    import json
+    import subprocess
+    import sys
+    from oracle import oracle as O
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    root = str(Path(__file__).resolve().parents[1])
+    code = ("import sys, bench; rc = bench.main(['--impl', 'reference', '--steps', '1', '--warmup', '0', "
+            "'--workload', 'c1']); "
+            "print('LOADED' if any(m.startswith('paper_1704_04428_b200') for m in sys.modules) else 'CLEAN'); "
+            "sys.exit(rc)")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().splitlines()[-1] == "CLEAN", r.stdout
+    ref = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    # same config object as our arm's (the driver compares the two lines)
+    d = subprocess.run([sys.executable, "bench.py", "--dry-run", "--workload", "c1"], cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert d.returncode == 0, d.stderr[-2000:]
+    ours = json.loads([l for l in d.stdout.splitlines() if l.startswith("{")][0])
+    assert ref["config"] == ours["config"]
+
+
+@pytest.mark.parametrize("workload,scaling,batches", [("scale", "strong", [128, 128]), ("c1", "weak", [1, 1])])
+def test_bench_gpus_flag_launches_ranks(workload, scaling, batches):
+    """`bench.py --gpus 2` without torchrun re-launches itself under torch.distributed.run (one
+    process per GPU); --dry-run exercises that launch and the batch sharding on gloo/CPU:
+    strong scaling splits the C5 global batch 256 into 128 per rank, weak keeps the per-GPU
+    batch."""
+    import json
+    import subprocess
+    import sys
+    root = str(Path(__file__).resolve().parents[1])
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--workload", workload, "--dry-run"], cwd=root,
+                       capture_output=True, text=True, timeout=600, env=dict(env, OMP_NUM_THREADS="1"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["rank_batches"] == batches
+    assert d["config"]["per_gpu_batch"] == batches[0]
+    assert d["config"]["global_batch"] == sum(batches)
