@@ -75,6 +75,10 @@ def parse_args(argv=None):
     ap.add_argument("--layout", default="nchw", choices=["nchw", "nhwc"],
                     help="device tensors NCHW (the reference interface, default) or channels-last "
                          "(cl_conv_forward_nhwc; the e2e leg stays NCHW)")
+    ap.add_argument("--shard", choices=["batch", "channels"], default="batch",
+                    help="batch: images split across ranks (no data-path collective); channels: every rank "
+                         "convolves all images with its slice of the kernels and an NCCL all-gather assembles "
+                         "the output (dist.MShardPlan; for batch-1 layers)")
     ap.add_argument("--concurrent", action="store_true",
                     help="run the step's independent layers on concurrent streams (grid-capped launches)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -176,11 +180,15 @@ def setup_run(args) -> Run:
     layers = load_layers(args.workload, args.batch)
     scaling = args.scaling
     if scaling == "auto":
-        scaling = "strong" if args.workload.partition("-")[0] == "scale" else "weak"
+        scaling = "strong" if args.workload.partition("-")[0] == "scale" or args.shard == "channels" else "weak"
     b = layers[0].batch
     if any(l.batch != b for l in layers):
         raise SystemExit("bench.py: a workload's layers share one batch")
-    if scaling == "strong":
+    if args.shard == "channels":
+        if scaling != "strong":
+            raise SystemExit("bench.py: channel sharding is strong scaling (every rank holds the whole batch)")
+        i0, i1 = 0, b
+    elif scaling == "strong":
         if b < world:
             raise SystemExit(f"bench.py: strong scaling needs batch {b} >= {world} ranks")
         i0, i1 = shard_range(b, world, rank)
@@ -201,7 +209,8 @@ def config_of(args, run: Run) -> dict:
         "precision": {"fp32": ("fp32-faithful (rel-L2 <= 1e-5): hi*Hi tf32 x2 + cross terms bf16 x2"
                                if fp32_split() == "mixed" else "fp32-faithful 3xTF32"),
                       "tf32": "tf32 (fast mode)", "bf16": "bf16 operands, fp32 accumulate (fast mode)"}[args.precision],
-        "parallelism": f"dp{run.world} (batch-sharded, no data-path collective)",
+        "parallelism": (f"dp{run.world} (batch-sharded, no data-path collective)" if args.shard == "batch" else
+                        f"mp{run.world} (output channels sharded, NCCL all-gather of the output slices)"),
         "l2": "flushed (256 MiB write) before every timed step", "weights": "pre-packed once, untimed",
     }
 
@@ -472,7 +481,10 @@ def run_ours(args, run: Run) -> int:
     for li, l in enumerate(rank_layers):
         lc = clb.LayerConfig(l.name, l.channels, l.height, l.width, l.kernel_count, l.kernel_size, l.stride,
                              None if l.pad < 0 else l.pad, l.batch)
-        plan = clb.ConvPlan(lc, args.method, args.precision, dev)
+        if args.shard == "channels":
+            plan = dist.MShardPlan(lc, info, args.method, args.precision, dev)
+        else:
+            plan = clb.ConvPlan(lc, args.method, args.precision, dev)
         if args.layout == "nhwc" and plan.method not in ("kn2row-gpu", "conv1x1-gpu", "kn2row-acc-gpu"):
             plan.close()   # channels-last is served by the implicit kernel only
             plan = clb.ConvPlan(lc, "kn2row-gpu" if l.kernel_size > 1 else "conv1x1-gpu", args.precision, dev)
@@ -483,7 +495,8 @@ def run_ours(args, run: Run) -> int:
         rng.fill_uniform(x, rng.split(li, 0), run.image0 * img)
         rng.fill_uniform(w, rng.split(li, 1))
         plan.set_weights(w)
-        ws = torch.empty(max(plan.workspace_bytes(), 4), device=dev, dtype=torch.uint8)
+        base = plan.plan if args.shard == "channels" else plan
+        ws = torch.empty(max(base.workspace_bytes(), 4), device=dev, dtype=torch.uint8)
         y = torch.empty(plan.output_shape(), device=dev, dtype=torch.float32)
         if args.layout == "nhwc":   # same values, channels-last storage
             x = x.permute(0, 2, 3, 1).contiguous()
@@ -494,27 +507,36 @@ def run_ours(args, run: Run) -> int:
         wss.append(ws)
     flush_mb = int(os.environ.get("CLB_FLUSH_MB", "256"))   # L2 flush: a write larger than the 126 MB L2
     flush = torch.empty(flush_mb * 1024 * 1024, device=dev, dtype=torch.uint8)
-    flops_rank = sum(l.flops() for l in rank_layers)
     flops_job = sum(l.flops() for l in run.layers) * (run.world if run.scaling == "weak" else 1)
+    bases = [p.plan if args.shard == "channels" else p for p in plans]   # the ConvPlans this rank runs
+    # FLOPs of this rank's launches (its kernel slice when sharding channels)
+    rank_flops = [l.flops() * ((p.m1 - p.m0) / l.kernel_count if args.shard == "channels" else 1)
+                  for l, p in zip(rank_layers, plans)]
 
-    # concurrent layers (--concurrent): each layer on its own stream with an engine grid share
-    # proportional to its FLOPs, forked from / joined into the step stream
-    side = []
+    # concurrent layers (--concurrent): each layer on its own stream with an SM share proportional
+    # to its standalone time, forked from / joined into the step stream, captured as one CUDA graph
+    conc = None
     if args.concurrent:
+        if args.shard != "batch":
+            raise SystemExit("bench.py: --concurrent runs batch-sharded plans")
         from paper_1704_04428_b200 import concurrency
-        side = concurrency.assign(plans, [l.flops() for l in rank_layers], dev)
+        n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        conc = concurrency.build(plans, xs, ys, wss, stream, n_sms, args.layout)
 
     def step(record_kernel=None):
-        if side:
-            concurrency.run_step(plans, xs, ys, wss, side, stream, args.layout, record_kernel)
+        if conc is not None:
+            conc.replay()                      # the whole fan-out: one graph launch
             return
         for li, plan in enumerate(plans):
             if record_kernel is not None:
                 b, e = record_kernel[li]
-                _lib.lib().cl_conv_set_profile_events(plan._h, b.cuda_event, e.cuda_event)
-            plan.forward(xs[li], ys[li], wss[li], layout=args.layout)
+                _lib.lib().cl_conv_set_profile_events(bases[li]._h, b.cuda_event, e.cuda_event)
+            if args.shard == "channels":
+                ys[li] = plan.forward(xs[li])          # this rank's slice + the NCCL all-gather
+            else:
+                plan.forward(xs[li], ys[li], wss[li], layout=args.layout)
             if record_kernel is not None:
-                _lib.lib().cl_conv_set_profile_events(plan._h, None, None)
+                _lib.lib().cl_conv_set_profile_events(bases[li]._h, None, None)
 
     sampler = ClockSampler(int(os.environ.get("CLB_SMI_INDEX", dev)))
     sampler.start()
@@ -522,13 +544,13 @@ def run_ours(args, run: Run) -> int:
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    launches_per_step = sum(p.launch_count() for p in plans)
+    launches_per_step = sum(p.launch_count() for p in bases)
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     st_b = [ev() for _ in range(args.steps)]
     st_e = [ev() for _ in range(args.steps)]
-    k_ev = [[(ev(), ev()) for _ in plans] for _ in range(args.steps)]
-    for pair in (p for row in k_ev for p in row):   # torch creates CUDA events lazily:
+    k_ev = [[(ev(), ev()) for _ in plans] for _ in range(args.steps)] if conc is None else None
+    for pair in (p for row in (k_ev or []) for p in row):   # torch creates CUDA events lazily:
         pair[0].record(stream)                       # record once so .cuda_event is a live
         pair[1].record(stream)                       # handle the library can record into
     torch.cuda.synchronize()
@@ -539,7 +561,7 @@ def run_ours(args, run: Run) -> int:
     for i in range(args.steps):
         flush.zero_()                       # L2 flush, outside the step events
         st_b[i].record(stream)
-        step(k_ev[i])
+        step(k_ev[i] if k_ev else None)
         st_e[i].record(stream)
     torch.cuda.synchronize()
     dist.barrier(info)
@@ -548,8 +570,11 @@ def run_ours(args, run: Run) -> int:
 
     step_ms = [st_b[i].elapsed_time(st_e[i]) for i in range(args.steps)]
     local_ms = sum(step_ms)
-    kern_ms = [statistics.median(k_ev[i][li][0].elapsed_time(k_ev[i][li][1]) for i in range(args.steps))
-               for li in range(len(plans))]
+    if conc is None:
+        kern_ms = [statistics.median(k_ev[i][li][0].elapsed_time(k_ev[i][li][1]) for i in range(args.steps))
+                   for li in range(len(plans))]
+    else:   # overlapping layers have no per-layer kernel time: their standalone forwards instead
+        kern_ms = list(conc.standalone_ms)
     job_ms = dist.max_over_ranks(local_ms, info, device=dev)
     med_ms = dist.max_over_ranks(statistics.median(step_ms), info, device=dev)
     value = flops_job * args.steps / (job_ms * 1e-3) / 1e12
@@ -562,18 +587,28 @@ def run_ours(args, run: Run) -> int:
     # the layers are independent: each is issued on its own stream (the async call orders its
     # copy-in after prior work on its stream), so their transfers overlap on both copy engines
     e2e_streams = [torch.cuda.Stream() for _ in plans]
-    for li, p in enumerate(plans):
-        p.forward_host(hx[li], hy[li])
+
+    def e2e_step():
+        if args.shard == "channels":
+            # H2D of the input, the sharded forward (slice + NCCL all-gather), D2H of the output
+            for li, p in enumerate(plans):
+                xs[li].copy_(hx[li], non_blocking=True)
+                hy[li].copy_(p.forward(xs[li]), non_blocking=True)
+            stream.synchronize()
+            return
+        for li, p in enumerate(plans):
+            p.forward_host_async(hx[li], hy[li], e2e_streams[li])
+        for s in e2e_streams:
+            s.synchronize()
+
+    e2e_step()
     e2e_steps = max(1, min(args.e2e_steps, args.steps))
     dist.barrier(info)
     torch.cuda.synchronize()
     eb, ee = ev(), ev()
     eb.record(stream)
     for _ in range(e2e_steps):
-        for li, p in enumerate(plans):
-            p.forward_host_async(hx[li], hy[li], e2e_streams[li])
-        for s in e2e_streams:
-            s.synchronize()
+        e2e_step()
     ee.record(stream)
     torch.cuda.synchronize()
     e2e_ms = dist.max_over_ranks(eb.elapsed_time(ee), info, device=dev)
@@ -587,18 +622,20 @@ def run_ours(args, run: Run) -> int:
     nominal_peak = NOMINAL_BF16 / 2.0 * tensor_factor(args.precision)
     hbm = pk["hbm"]
     tc_idx = [i for i, p in enumerate(plans) if p.method != "direct-gpu"]
-    tc_flops = sum(rank_layers[i].flops() for i in tc_idx)
+    tc_flops = sum(rank_flops[i] for i in tc_idx)
     tc_ms = sum(kern_ms[i] for i in tc_idx)
+    if conc is not None:     # concurrent step: the whole step (prepasses and all) is the measure
+        tc_ms = med_ms
     achieved = tc_flops / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else None
     traffic, traffic_src = traffic_for(args.workload, args.precision, args.method)
     if run.world > 1 or args.batch is not None:
         traffic, traffic_src = None, None       # the capture is of the 1-GPU default batch
     layer_rows = []
-    for l, p, km in zip(rank_layers, plans, kern_ms):
+    for l, p, km, fl in zip(rank_layers, plans, kern_ms, rank_flops):
         ai = l.flops() / l.bytes()
         bound = min(mode_peak, ai * hbm / 1e3)
-        tf = l.flops() / (km * 1e-3) / 1e12
-        layer_rows.append({"name": l.name, "method": p.method, "batch": l.batch, "gflop": round(l.flops() / 1e9, 3),
+        tf = fl / (km * 1e-3) / 1e12
+        layer_rows.append({"name": l.name, "method": p.method, "batch": l.batch, "gflop": round(fl / 1e9, 3),
                            "kernel_ms": round(km, 4), "kernel_tflops": round(tf, 1),
                            "frac_of_peak": round(tf / mode_peak, 3),
                            "layer_roofline_tflops": round(bound, 1), "frac_of_layer_roofline": round(tf / bound, 3),
@@ -656,6 +693,12 @@ def run_ours(args, run: Run) -> int:
                      "nominal_peak": nominal_peak,
                      "frac_of_nominal": achieved / nominal_peak if achieved else None},
         "layers": layer_rows,
+        "concurrent": (None if conc is None else
+                       {"sm_caps": conc.caps, "standalone_forward_ms": [round(t, 4) for t in conc.standalone_ms],
+                        "standalone_sum_ms": round(sum(conc.standalone_ms), 4),
+                        "note": "layers on concurrent streams with SM caps proportional to their standalone forward "
+                                "time, captured as one CUDA graph; per-layer rows carry the standalone forward time "
+                                "(prepass + contraction) and roofline.achieved uses the median whole step"}),
         "cpu_baseline": cpu,
         "clocks": clocks,
     }

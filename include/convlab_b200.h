@@ -161,6 +161,15 @@ CL_API cl_status cl_fill_uniform(float* d, uint64_t n, uint64_t seed, uint64_t f
  * caller can time the dominant kernel alone with CUDA events.  NULLs disable. */
 CL_API cl_status cl_conv_set_profile_events(cl_plan* plan, void* ev_begin, void* ev_end);
 
+/* Caps the SMs the plan's tcgen05 launches may occupy (0 = all co-resident units, the
+ * default).  Independent layers on concurrent streams (e.g. GoogLeNet inception branches,
+ * batch-1 stacks) then share the GPU instead of each filling it with a persistent grid whose
+ * fixed costs (prologue, pipeline fill, stream-K tail) serialise.  Keep the caps of kernels
+ * that may run at the same time within the SM count: every CTA of a launch must be
+ * co-resident (its stream-K pieces wait on each other).  No reference counterpart (the
+ * reference runs one layer at a time on the CPU). */
+CL_API cl_status cl_conv_set_max_sms(cl_plan* plan, int max_sms);
+
 /* fnv1a over the fp32 bit patterns of a HOST array, bytes low..high (bench.cpp:25-36): the
  * reference harness's output checksum. */
 CL_API uint64_t cl_checksum_fnv1a(const float* h, uint64_t n);

@@ -101,7 +101,7 @@ struct cl_plan {
     // launches: a CUDA graph captures kernel parameters by value, so a captured launch reads the
     // device weights instead and picks up later set_weights calls like every other method.
     std::vector<float> wparam;
-    int max_units = 0;         // engine grid cap (cl_conv_set_max_units; 0 = all co-resident units)
+    int max_sms = 0;           // engine grid cap in SMs (cl_conv_set_max_sms; 0 = all co-resident units)
     unsigned* flags = nullptr; // stream-K fixup flags, zeroed once, self-resetting
     bool padded_rows = false;  // implicit kn2row in tap-shared (zero-padded row) mode
     int stack_k = 1;           // > 1: padded-row mode with the k taps of a kernel row stacked on N
@@ -291,7 +291,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         set_scratch(t, scratch);
         t.flags = p->flags;
         t.flags_zeroed = 1;
-        t.max_units = p->max_units;
+        t.max_sms = p->max_sms;
         static const int forced_bn = [] {   // experiments: CLB_BN=<multiple of 16 <= 256>
             const char* e = std::getenv("CLB_BN");
             const int v = e ? std::atoi(e) : 0;
@@ -923,6 +923,14 @@ cl_status cl_fill_uniform(float* d, uint64_t n, uint64_t seed, uint64_t first_in
         require(d || n == 0, "cl_fill_uniform: null pointer");
         launch_fill_uniform(d, n, seed, first_index, static_cast<cudaStream_t>(stream));
     });
+}
+
+cl_status cl_conv_set_max_sms(cl_plan* p, int max_sms) {
+    if (!p) return fail(CL_EINVAL, "cl_conv_set_max_sms: null plan");
+    if (max_sms < 0 || max_sms > 255) return fail(CL_EINVAL, "cl_conv_set_max_sms: cap must be in [0, 255]");
+    std::lock_guard<std::mutex> lock(p->mu);
+    p->max_sms = max_sms;
+    return CL_OK;
 }
 
 cl_status cl_conv_set_profile_events(cl_plan* p, void* ev_begin, void* ev_end) {

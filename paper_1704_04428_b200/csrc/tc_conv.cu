@@ -94,7 +94,7 @@ struct DeviceLimits {
     int units = 0;
 };
 
-const DeviceLimits& device_limits(int cg, int smem, int max_units) {
+const DeviceLimits& device_limits(int cg, int smem, int max_sms) {
     static std::mutex mu;
     static std::unordered_map<unsigned long long, DeviceLimits> cache;
     static bool configured[64][3] = {};
@@ -102,7 +102,7 @@ const DeviceLimits& device_limits(int cg, int smem, int max_units) {
     CLB_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64) throw Error(6, "device index out of range");
     const unsigned long long key = ((unsigned long long)dev << 40) | ((unsigned long long)cg << 32) |
-                                   ((unsigned long long)(unsigned)smem << 8) | (unsigned)(max_units & 0xff);
+                                   ((unsigned long long)(unsigned)smem << 8) | (unsigned)(max_sms & 0xff);
     std::lock_guard<std::mutex> g(mu);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
@@ -139,7 +139,7 @@ const DeviceLimits& device_limits(int cg, int smem, int max_units) {
         CLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc_conv_kernel<1, false>, kThreads, smem));
         if (per_sm * sms < units) units = per_sm * sms;
     }
-    if (max_units > 0 && max_units < units) units = max_units;
+    if (max_sms > 0 && std::max(1, max_sms / cg) < units) units = std::max(1, max_sms / cg);
     if (units < 1) throw Error(2, "tcgen05 engine: no CTA of this configuration fits on the device");
     return cache[key] = DeviceLimits{units};
 }
@@ -233,7 +233,7 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     // co-resident: the unit count is capped at what the occupancy calculator says fits at once
     // for this kernel, smem size and cluster shape (on the current device; attributes and
     // limits are per device, configured once each).
-    const DeviceLimits& lim = device_limits(cg, smem, p.max_units);
+    const DeviceLimits& lim = device_limits(cg, smem, p.max_sms);
     int units = lim.units;      // scheduling units (CTAs or CTA pairs)
     if (total_chunks < units) units = (int)total_chunks;
     // Fewer tiles than units (latency-bound problems): pick the split s (pieces per tile) by a

@@ -111,8 +111,8 @@ struct TcParams {
     int sk_chunks;             // chunks of tiles [dp_tiles, num_tiles), split contiguously (stream-K)
     int sk_units;              // scheduling units sharing the stream-K chunks (<= grid units; the
                                // rest only run data-parallel tiles): chosen so no tile splits 3 ways
-    int max_units;             // cap on the scheduling units (0 = every co-resident unit): lets
-                               // independent launches share the SMs (concurrent small layers)
+    int max_sms;               // cap on the SMs the grid may occupy (0 = every co-resident unit):
+                               // lets independent launches share the GPU (concurrent small layers)
     float* partials;           // [gridDim.x][128][bn] tile-tail partial sums
     unsigned* flags;           // [gridDim.x], 0 at launch; 1 = partial ready (the finisher resets it)
     int flags_zeroed;          // flags are known to be 0 (self-resetting plan buffer): no memset

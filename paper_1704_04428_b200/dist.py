@@ -94,23 +94,24 @@ def channel_slice(m: int, world: int, rank: int) -> tuple:
     return shard_range(m, world, rank)
 
 
-def mshard_conv(x, w_mkkc, info: RankInfo, conv_fn):
+def mshard_conv(x, w_mkkc, info: RankInfo, conv_fn, m_total: int = None):
     """y = conv(x, w) with the M dimension sharded over ranks.
 
-    x: [N, C, H, W] (every rank holds all of it), w_mkkc: [M, k, k, C] full weights,
+    x: [N, C, H, W] (every rank holds all of it), w_mkkc: [M, k, k, C] full weights (or None
+    with `m_total` when the callable already holds its slice, as MShardPlan's plan does),
     conv_fn(x, w_slice) -> y_slice [N, M_g, P, Q] runs this rank's share (the B200 plan in
     the product, any callable in tests).  Returns the full y [N, M, P, Q] on every rank.
     """
     import torch
     import torch.distributed as dist
 
-    M = w_mkkc.shape[0]
+    M = w_mkkc.shape[0] if w_mkkc is not None else m_total
     if M < info.world:
         raise ValueError(f"cannot shard {M} kernels over {info.world} ranks")
     b, e = channel_slice(M, info.world, info.rank)
-    y_local = conv_fn(x, w_mkkc[b:e].contiguous())
-    if not info.distributed:
-        return y_local
+    y_local = conv_fn(x, w_mkkc[b:e].contiguous() if w_mkkc is not None else None)
+    if not (dist.is_available() and dist.is_initialized()):
+        return y_local          # single process: the slice is the whole output
     N, _, P, Q = y_local.shape
     # uneven slices: pad every rank's block to the largest slice so one collective suffices
     mg = max(channel_slice(M, info.world, r)[1] - channel_slice(M, info.world, r)[0] for r in range(info.world))
@@ -128,3 +129,56 @@ def mshard_conv(x, w_mkkc, info: RankInfo, conv_fn):
         rb, re_ = channel_slice(M, info.world, r)
         y[:, rb:re_] = gathered[r, :, : re_ - rb]
     return y
+
+
+class MShardPlan:
+    """Output-channel-sharded layer on a real B200 plan (SURVEY.md 8(e) alternative): rank g
+    plans kernels [g M/G, (g+1) M/G) (dist.channel_slice) with its own ConvPlan, convolves the
+    whole input, and `mshard_conv`'s all-gather assembles the NCHW output on every rank --
+    NCCL (all_gather_into_tensor over NVLink / NVSwitch) for device tensors, gloo for the host
+    path.  Weights are sliced and packed once (set_weights).  Optional, off the measured path:
+    it serves batch-1 layers (C1, AlexNet b1, the C5 k-sweep) that batch sharding cannot split.
+    """
+
+    def __init__(self, layer, info: RankInfo, method: str = "auto", precision: str = "fp32", device: int = None):
+        import dataclasses
+        from .methods import ConvPlan
+        if layer.kernel_count < info.world:
+            raise ValueError(f"cannot shard {layer.kernel_count} kernels over {info.world} ranks")
+        self.layer, self.info = layer, info
+        self.m0, self.m1 = channel_slice(layer.kernel_count, info.world, info.rank)
+        self.device = info.local_rank if device is None else device
+        self.plan = ConvPlan(dataclasses.replace(layer, kernel_count=self.m1 - self.m0), method, precision,
+                             self.device)
+
+    @property
+    def method(self):
+        return self.plan.method
+
+    def set_weights(self, w_full):
+        """w_full: the FULL [M, k, k, C] weights (device tensor); this rank keeps its slice."""
+        self.plan.set_weights(w_full[self.m0:self.m1].contiguous())
+
+    def set_weights_host(self, w_full):
+        self.plan.set_weights_host(w_full[self.m0:self.m1].contiguous())
+
+    def output_shape(self):
+        L = self.layer
+        return (L.batch, L.kernel_count, *self.plan.out_hw)
+
+    def forward(self, x):
+        """x: full [N, C, H, W] device tensor on every rank -> full y (NCCL all-gather)."""
+        return mshard_conv(x, None, self.info, lambda xx, _w: self.plan.forward(xx),
+                           m_total=self.layer.kernel_count)
+
+    def forward_host(self, x_host):
+        """Host path: H2D + forward + D2H of this rank's slice, gathered on the host (gloo)."""
+        import torch
+
+        def conv(xx, _w):
+            y = torch.empty((self.layer.batch, self.m1 - self.m0, *self.plan.out_hw), dtype=torch.float32)
+            return self.plan.forward_host(xx.contiguous(), y)
+        return mshard_conv(x_host, None, self.info, conv, m_total=self.layer.kernel_count)
+
+    def close(self):
+        self.plan.close()

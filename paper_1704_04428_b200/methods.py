@@ -197,6 +197,10 @@ class ConvPlan:
     def workspace_bytes(self) -> int:
         return int(_lib.lib().cl_conv_workspace_bytes(self._h))
 
+    def set_max_sms(self, max_sms: int):
+        """Cap the SMs this plan's tcgen05 launches occupy (0 = all; cl_conv_set_max_sms)."""
+        _lib.check(_lib.lib().cl_conv_set_max_sms(self._h, int(max_sms)))
+
     def launch_count(self) -> int:
         return int(_lib.lib().cl_conv_last_launch_count(self._h))
 

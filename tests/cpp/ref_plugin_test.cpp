@@ -4,7 +4,10 @@
 // (register_gemm_backend, gemm.hpp:52-58; compiled into oracle/_ref) and runs the
 // reference's own conv_kn2row / conv_im2col / conv_kn2col (conv_kn2.cpp:145-183,
 // conv_im2.cpp:108-132) with it, against the reference oracle conv_mcmk_sum.  The adapter
-// below is exactly the binding shown in INTEGRATION.md.
+// below is exactly the binding shown in INTEGRATION.md.  Second part: the reference-signature
+// overload convlab_b200::run_method(convlab::ConvMethod, const convlab::ConvProblem&,
+// const convlab::GemmBackend&) of include/convlab_b200_ref.hpp (CHW and HWC inputs, MKKC and
+// MCKK kernels, the k == 1 routing and the conv1x1 contract).
 #include <cstdio>
 #include <stdexcept>
 #include <cuda_runtime.h>
@@ -15,6 +18,7 @@
 #include "convlab/gemm.hpp"
 #include "convlab/methods.hpp"
 #include "convlab_b200.h"
+#include "convlab_b200_ref.hpp"
 
 namespace {
 
@@ -58,6 +62,36 @@ int main() {
                         std::string(convlab::to_string(m)).c_str(), s.c, s.h, s.w, s.m, s.k,
                         convlab::max_abs_diff(out, oracle), ok ? "ok" : "FAIL");
             fails += !ok;
+        }
+    }
+    // ---- the reference signature, served by the B200 path ----
+    for (const auto& s : shapes) {
+        for (int variant = 0; variant < 2; ++variant) {
+            const auto lay = variant ? convlab::Layout::HWC : convlab::Layout::CHW;
+            const auto klay = variant ? convlab::KernelLayout::MCKK : convlab::KernelLayout::MKKC;
+            convlab::ConvProblem p(convlab::random_tensor3(s.c, s.h, s.w, lay, convlab::rng::split(6, 0)),
+                                   convlab::random_kernels(s.m, s.k, s.c, klay, convlab::rng::split(6, 1)));
+            const convlab::Tensor3 oracle = convlab::conv_mcmk_sum(p);
+            const auto tol = convlab::scaled_tolerance({1e-5f, 1e-6f}, convlab::max_abs(oracle));
+            for (auto m : convlab::default_methods()) {
+                const convlab::Tensor3 out = convlab_b200::run_method(m, p, *backend);
+                const bool ok = out.layout() == convlab::Layout::CHW && convlab::allclose(out, oracle, tol);
+                std::printf("  b200 run_method(%-15s %s/%s) C=%zu %zux%zu M=%zu k=%zu  max|err|=%.3e  %s\n",
+                            std::string(convlab::to_string(m)).c_str(), variant ? "HWC" : "CHW",
+                            variant ? "MCKK" : "MKKC", s.c, s.h, s.w, s.m, s.k, convlab::max_abs_diff(out, oracle),
+                            ok ? "ok" : "FAIL");
+                fails += !ok;
+            }
+            bool threw = false;
+            try {
+                (void)convlab_b200::run_method(convlab::ConvMethod::Conv1x1, p, *backend);
+            } catch (const std::invalid_argument&) {
+                threw = true;
+            }
+            if ((s.k != 1) != threw) {
+                std::printf("  conv1x1 contract violated for k=%zu\n", s.k);
+                ++fails;
+            }
         }
     }
     std::printf(fails ? "FAILED (%d)\n" : "PASSED\n", fails);
