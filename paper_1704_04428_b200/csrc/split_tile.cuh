@@ -17,6 +17,14 @@ __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float(r);
 }
 
+// The same rounding in two integer instructions (half an ulp of the 10-bit mantissa added to
+// the magnitude, low 13 bits cleared: ties away from zero; carries into the exponent are the
+// correct rounding up), bit-identical to cvt.rna.tf32.f32 for every finite input -- for the
+// compute-bound in-kernel conversion (cvt.rna.tf32 is several instructions on sm_100).
+__device__ __forceinline__ uint32_t tf32_rna_bits(float x) {
+    return (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+}
+
 __device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
     __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&t);
