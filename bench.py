@@ -276,8 +276,9 @@ class ClockSampler:
     """SM clock / power / throttle reasons sampled DURING the timed region (B200_PROFILING.md
     clocks line): NVML polled every 5 ms from a thread (nvidia-smi -lms as fallback)."""
 
-    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
-               "sw_power_cap": 0x4}
+    REASONS = {"gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+               "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100}
 
     def __init__(self, index: int):
         self.index = index

@@ -120,8 +120,11 @@ def test_selector_picks_direct_for_tiny_c(oracle, clb, torch_cuda):
     """auto: C <= 4 -> direct-gpu (VGG conv1_1 shape class), otherwise the implicit kernel."""
     with clb.ConvPlan(clb.LayerConfig("c3", 3, 32, 32, 64, 3, batch=2), "auto") as plan:
         assert plan.method == "direct-gpu"
+    with clb.ConvPlan(clb.LayerConfig("c64", 64, 56, 56, 64, 3, batch=32), "auto") as plan:
+        assert plan.method == "kn2row-gpu"          # many tiles: the rule, no timing
     with clb.ConvPlan(clb.LayerConfig("c64", 64, 32, 32, 64, 3, batch=2), "auto") as plan:
-        assert plan.method == "kn2row-gpu"
+        # few tiles: implicit vs the paper's explicit kn2row, timed once per descriptor
+        assert plan.method in ("kn2row-gpu", "kn2row-explicit-gpu")
     for k in (1, 3, 5, 7):   # compile-time and runtime tap paths
         x, w = oracle.make_problem(2, 3, 19, 23, 20, k, k)
         _check_fp32(oracle, _run(clb, torch_cuda, "direct-gpu", x, w), oracle.conv_batch(x, w), f"direct k={k}")
@@ -911,3 +914,26 @@ def test_raw_input_contraction(oracle, tmp_path):
         ya, yb = np.load(tmp_path / "r1" / f"raw_{i}.npy"), np.load(tmp_path / "r0" / f"raw_{i}.npy")
         assert np.array_equal(ya, yb), ("raw-input A and prepass paths differ", a["case"])
     assert any(a["launches"] == 1 for a in outs["1"])     # the raw path ran (no prepass launch)
+
+
+def test_selector_timing_cache(oracle, clb, torch_cuda):
+    """`auto` on a batch-1 small-map 3x3 layer (the regime where the paper's explicit kn2row can
+    beat the implicit kernel, profiles/r02_method_table.md) is decided by timing once per
+    descriptor: the choice is one of the two, stable within the process, right against the
+    oracle, and CLB_AUTOTUNE=0 (in a subprocess) leaves the rule's implicit pick."""
+    import subprocess, sys
+    torch = torch_cuda
+    layer = clb.LayerConfig("t", 384, 13, 13, 256, 3, batch=1)
+    picks = set()
+    for _ in range(3):
+        with clb.ConvPlan(layer, "auto") as plan:
+            picks.add(plan.method)
+    assert len(picks) == 1 and picks <= {"kn2row-gpu", "kn2row-explicit-gpu"}, picks
+    x, w = oracle.make_problem(1, 384, 13, 13, 256, 3, 500)
+    _check_fp32(oracle, _run(clb, torch, "auto", x, w), oracle.conv_batch(x, w), f"auto -> {picks}")
+    code = ("import sys; sys.path.insert(0, '.'); import paper_1704_04428_b200 as clb; "
+            "p = clb.ConvPlan(clb.LayerConfig('t', 384, 13, 13, 256, 3, batch=1), 'auto'); print(p.method)")
+    from pathlib import Path
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=str(Path(__file__).resolve().parent.parent), env=dict(os.environ, CLB_AUTOTUNE="0"))
+    assert r.returncode == 0 and r.stdout.strip() == "kn2row-gpu", (r.stdout, r.stderr[-1000:])
