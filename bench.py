@@ -79,6 +79,9 @@ def parse_args(argv=None):
                     help="batch: images split across ranks (no data-path collective); channels: every rank "
                          "convolves all images with its slice of the kernels and an NCCL all-gather assembles "
                          "the output (dist.MShardPlan; for batch-1 layers)")
+    ap.add_argument("--chain", action="store_true",
+                    help="one cl_conv_forward_chain call per step: each layer's prepass rides on the previous "
+                         "layer's contraction (its converter warps), a tail launch finishes it")
     ap.add_argument("--concurrent", action="store_true",
                     help="run the step's independent layers on concurrent streams (grid-capped launches)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -206,6 +209,7 @@ def config_of(args, run: Run) -> dict:
         "workload": args.workload, "layers": [l.name for l in layers],
         "global_batch": glob, "per_gpu_batch": per_gpu if per_gpu is not None else -(-glob // run.world),
         "scaling": run.scaling, "layout": args.layout, "method": args.method,
+        "schedule": "concurrent" if args.concurrent else ("chain" if args.chain else "sequential"),
         "precision": {"fp32": ("fp32-faithful (rel-L2 <= 1e-5): hi*Hi tf32 x2 + cross terms bf16 x2"
                                if fp32_split() == "mixed" else "fp32-faithful 3xTF32"),
                       "tf32": "tf32 (fast mode)", "bf16": "bf16 operands, fp32 accumulate (fast mode)"}[args.precision],
@@ -516,10 +520,12 @@ def run_ours(args, run: Run) -> int:
 
     # concurrent layers (--concurrent): each layer on its own stream with an SM share proportional
     # to its standalone time, forked from / joined into the step stream, captured as one CUDA graph
+    if args.chain and (args.layout != "nchw" or args.shard != "batch"):
+        raise SystemExit("bench.py: --chain runs NCHW batch-sharded plans")
     conc = None
     if args.concurrent:
-        if args.shard != "batch":
-            raise SystemExit("bench.py: --concurrent runs batch-sharded plans")
+        if args.shard != "batch" or args.chain:
+            raise SystemExit("bench.py: --concurrent runs batch-sharded plans, one per stream (no --chain)")
         from paper_1704_04428_b200 import concurrency
         n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
         conc = concurrency.build(plans, xs, ys, wss, stream, n_sms, args.layout)
@@ -527,6 +533,16 @@ def run_ours(args, run: Run) -> int:
     def step(record_kernel=None):
         if conc is not None:
             conc.replay()                      # the whole fan-out: one graph launch
+            return
+        if args.chain:
+            if record_kernel is not None:
+                for li, plan in enumerate(bases):
+                    b, e = record_kernel[li]
+                    _lib.lib().cl_conv_set_profile_events(plan._h, b.cuda_event, e.cuda_event)
+            clb.forward_chain(plans, xs, ys, wss, stream)
+            if record_kernel is not None:
+                for plan in bases:
+                    _lib.lib().cl_conv_set_profile_events(plan._h, None, None)
             return
         for li, plan in enumerate(plans):
             if record_kernel is not None:

@@ -123,6 +123,16 @@ CL_API cl_status cl_conv_forward(cl_plan* plan, const float* d_x, float* d_y, vo
  * (CL_EUNSUPPORTED otherwise).  Asynchronous on `stream`. */
 CL_API cl_status cl_conv_forward_nhwc(cl_plan* plan, const float* d_x, float* d_y, void* d_ws, void* stream);
 
+/* A step of `count` layers on one stream, in order: y_i = conv_i(x_i) for every plan (NCHW device
+ * tensors, workspaces may be NULL).  Where layer i+1 runs the standard NCHW -> split prepass and
+ * layer i is a tcgen05 contraction in the same operand format, layer i's idle converter warps
+ * convert tiles of x_{i+1} while its tensor pipe runs (the prepass is HBM-bound, the contraction
+ * tensor-bound), and a tail launch finishes the tiles left before layer i+1's contraction.
+ * Same results as `count` cl_conv_forward calls (bit-identical operand bytes).  No reference
+ * counterpart (the reference runs one layer per call on the CPU). */
+CL_API cl_status cl_conv_forward_chain(cl_plan* const* plans, const float* const* d_xs, float* const* d_ys,
+                                       void* const* d_wss, int count, void* stream);
+
 /* Host-buffer end-to-end call (the run_method surface): H2D of x, forward, D2H of y,
  * synchronous.  Host buffers should be pinned for full PCIe bandwidth. */
 CL_API cl_status cl_conv_forward_host(cl_plan* plan, const float* h_x, float* h_y, void* stream);

@@ -7,12 +7,12 @@ library and fails loudly when it is missing -- there is no CPU fallback.
 """
 from . import _lib
 from . import harness
-from .methods import (ALL_METHODS, GPU_METHODS, REFERENCE_METHODS, ConvPlan, LayerConfig, footprint, gemm,
+from .methods import (ALL_METHODS, GPU_METHODS, REFERENCE_METHODS, ConvPlan, LayerConfig, footprint, forward_chain, gemm,
                       method_from_name, method_requires_1x1, parse_method_list, parse_network_text, run_method,
                       shift_add_row)
 
 lib = _lib.lib()  # load now: a missing extension is an import error, not a silent fallback
 
-__all__ = ["ConvPlan", "LayerConfig", "run_method", "gemm", "shift_add_row", "footprint", "parse_method_list",
+__all__ = ["ConvPlan", "LayerConfig", "run_method", "forward_chain", "gemm", "shift_add_row", "footprint", "parse_method_list",
            "parse_network_text", "method_from_name", "method_requires_1x1", "ALL_METHODS", "GPU_METHODS",
            "REFERENCE_METHODS", "lib"]

@@ -256,27 +256,56 @@ void mark_done(cl_plan* p, cudaStream_t s) {
 // nhwc: channels-last input and output (implicit kn2row / conv1x1 / accumulating only).
 // ev_first / ev_last_chunk: record the plan's profile events (begin / end) in this call (a
 // chunked forward brackets all of its chunks with one pair).
+// The caller's workspace, or the plan's own (allocated on first use).
+void* resolve_ws(cl_plan* p, void* ws) {
+    const size_t need = ws_bytes(p);
+    if (ws || !need) return ws;
+    if (p->own_ws_bytes < need) {
+        if (p->own_ws) cudaFree(p->own_ws);
+        p->own_ws = nullptr;
+        p->own_ws_bytes = 0;
+        if (cudaMalloc(&p->own_ws, need) != cudaSuccess) {
+            cudaGetLastError();
+            throw Error(CL_ENOMEM, "workspace allocation failed: requires " + std::to_string(need) + " bytes");
+        }
+        p->own_ws_bytes = need;
+    }
+    return p->own_ws;
+}
+
+// Chained prepass (cl_conv_forward_chain): the plan's NCHW -> split prepass as a tile job, when
+// its forward runs the standard prepass (implicit / conv1x1 / accumulating kn2row, fp32-faithful
+// split formats, not the raw-input mode).  The job's counter lives in the plan's flag buffer.
+bool chain_job(cl_plan* p, const float* x, void* ws, SplitJob* out) {
+    const bool implicit = p->method == CL_METHOD_KN2ROW || p->method == CL_METHOD_CONV1X1 ||
+                          p->method == CL_METHOD_KN2ROW_ACC;
+    if (!implicit || !is_split(p->planes) || p->raw_a) return false;
+    const cl_conv_desc& d = p->d;
+    void* xs = ws;
+    int pad = 0;
+    if (p->padded_rows) {
+        xs = static_cast<char*>(ws) + (size_t)stack_lead_rows(p) * row_bytes(p->planes, p->Cp);
+        pad = d.pad;
+    }
+    *out = make_split_job(x, xs, d.n, d.c, d.h, d.w, pad, p->Cp);
+    out->planes = p->planes;
+    out->counter = p->flags + kMaxGrid + 2;
+    return true;
+}
+
 void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images = -1, bool nhwc = false,
-             bool ev_first = true, bool ev_last_chunk = true) {
+             bool ev_first = true, bool ev_last_chunk = true, const SplitJob* next_job = nullptr,
+             bool prepass_partial = false) {
     cl_conv_desc d = p->d;
     if (n_images >= 0) d.n = n_images;
     require(p->weights_set, "cl_conv_forward: weights not set (cl_conv_set_weights)");
     require(x && y, "cl_conv_forward: null tensor");
     CLB_CUDA(cudaSetDevice(p->device));
-    const size_t need = ws_bytes(p);
-    if (!ws && need) {
-        if (p->own_ws_bytes < need) {
-            if (p->own_ws) cudaFree(p->own_ws);
-            p->own_ws = nullptr;
-            p->own_ws_bytes = 0;
-            if (cudaMalloc(&p->own_ws, need) != cudaSuccess) {
-                cudaGetLastError();
-                throw Error(CL_ENOMEM, "workspace allocation failed: requires " + std::to_string(need) + " bytes");
-            }
-            p->own_ws_bytes = need;
-        }
-        ws = p->own_ws;
-    }
+    ws = resolve_ws(p, ws);
+    // chained: this plan's prepass was started by the previous contraction's converter warps
+    SplitJob own_job{};
+    if (prepass_partial && !(n_images < 0 && !nhwc && chain_job(p, x, ws, &own_job)))
+        throw Error(CL_EINTERNAL, "chained prepass on a plan without a chainable prepass");
     const int taps = d.k * d.k;
     const long long nhw = (long long)d.n * d.h * d.w;
     const long long npq = (long long)d.n * p->P * p->Q;
@@ -295,6 +324,10 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         t.flags = p->flags;
         t.flags_zeroed = 1;
         t.max_sms = p->max_sms;
+        if (next_job && is_split(p->planes) && (p->planes == next_job->planes)) {
+            t.nx = *next_job;
+            t.nx_on = 1;
+        }
         static const int forced_bn = [] {   // experiments: CLB_BN=<multiple of 16 <= 256>
             const char* e = std::getenv("CLB_BN");
             const int v = e ? std::atoi(e) : 0;
@@ -342,7 +375,10 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 // raw-input A: the contraction reads the NCHW input itself (TMA boxes + converter
                 // warps), so there is no prepass launch and no split tensor round trip through HBM
                 const bool raw = p->raw_a && !nhwc && reinterpret_cast<uintptr_t>(x) % 16 == 0;
-                if (!raw) {
+                if (prepass_partial) {
+                    launch_split_tail(own_job, p->planes, s);   // the tiles the previous contraction left
+                    ++p->launches;
+                } else if (!raw) {
                     if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
                     else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
                     ++p->launches;
@@ -403,7 +439,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 tc_done();
                 break;
             }
-            if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s);
+            if (prepass_partial) launch_split_tail(own_job, p->planes, s);
+            else if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s);
             else launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
             ++p->launches;
             Operand a = implicit_a(p, xs);
@@ -818,6 +855,55 @@ cl_status cl_conv_forward(cl_plan* p, const float* d_x, float* d_y, void* d_ws, 
         order_after_previous(p, s);
         forward(p, d_x, d_y, d_ws, s, -1, false);
         mark_done(p, s);
+    });
+}
+
+cl_status cl_conv_forward_chain(cl_plan* const* plans, const float* const* xs, float* const* ys, void* const* wss,
+                                int count, void* stream) {
+    return guarded([&] {
+        require(plans && xs && ys && count > 0, "cl_conv_forward_chain: null argument");
+        auto s = static_cast<cudaStream_t>(stream);
+        for (int i = 0; i < count; ++i) {
+            require(plans[i] != nullptr, "cl_conv_forward_chain: null plan");
+            for (int j = 0; j < i; ++j) require(plans[j] != plans[i], "cl_conv_forward_chain: a plan appears twice");
+            require(plans[i]->device == plans[0]->device, "cl_conv_forward_chain: plans on different devices");
+        }
+        std::vector<std::unique_lock<std::mutex>> locks;
+        for (int i = 0; i < count; ++i) locks.emplace_back(plans[i]->mu);
+        CLB_CUDA(cudaSetDevice(plans[0]->device));
+        std::vector<SplitJob> jobs(count);
+        std::vector<char> chainable(count, 0);
+        std::vector<void*> ws(count);
+        for (int i = 0; i < count; ++i) {
+            order_after_previous(plans[i], s);
+            require(plans[i]->weights_set, "cl_conv_forward_chain: weights not set (cl_conv_set_weights)");
+            ws[i] = resolve_ws(plans[i], wss ? wss[i] : nullptr);
+            chainable[i] = chain_job(plans[i], xs[i], ws[i], &jobs[i]) ? 1 : 0;
+        }
+        // layer i+1's prepass rides on layer i's contraction when both use the split operand
+        // format the converters write, layer i's launches are tcgen05 contractions, and layer i's
+        // contraction is long enough to hide anything (estimated >= 50 us at ~400 TF: shorter ones
+        // only add the tail launch -- GoogLeNet b64 6 % slower with every prepass hosted).  Hosting
+        // slows the host contraction by 3-12 % (its converter warps' global traffic shares the
+        // SM's load/store path with the operand stream) and hides most of the next prepass: VGG-16
+        // b32 3.92 -> 3.85 ms per step (profiles/r02_chain_prepass.txt).  CLB_CHAIN_FORCE=1 hosts
+        // every eligible prepass (tests); CLB_CHAIN_MIN_US sets the host threshold.
+        static const double min_us = std::getenv("CLB_CHAIN_MIN_US") ? std::atof(std::getenv("CLB_CHAIN_MIN_US")) : 50.0;
+        static const bool force = std::getenv("CLB_CHAIN_FORCE") && std::atoi(std::getenv("CLB_CHAIN_FORCE")) != 0;
+        auto hosts = [&](int i) {
+            if (!(i + 1 < count && chainable[i + 1] && plans[i]->method != CL_METHOD_DIRECT &&
+                  is_split(plans[i]->planes) && plans[i]->planes == plans[i + 1]->planes))
+                return false;
+            if (force) return true;
+            const cl_conv_desc& a = plans[i]->d;
+            const double t_host_us = 2.0 * a.n * a.m * a.c * a.k * a.k * (double)plans[i]->P * plans[i]->Q / 4.0e8;
+            return t_host_us >= min_us;
+        };
+        for (int i = 0; i < count; ++i) {
+            const bool partial = i > 0 && hosts(i - 1);
+            forward(plans[i], xs[i], ys[i], ws[i], s, -1, false, true, true, hosts(i) ? &jobs[i + 1] : nullptr, partial);
+            mark_done(plans[i], s);
+        }
     });
 }
 

@@ -57,6 +57,10 @@ void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int
                        cudaStream_t s);
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
                                  cudaStream_t s);
+// the same conversion as a tile job (chained mode) and the tail launch that finishes its tiles
+// left by the previous contraction's converter warps (then resets the job's counter)
+SplitJob make_split_job(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp);
+void launch_split_tail(const SplitJob& j, int planes, cudaStream_t s);
 // a[rows][K] -> as[rows][planes][Kp]
 void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s);
 // b[K][cols] -> bs[cols][planes][Kp]

@@ -4,6 +4,7 @@
 // All are coalesced on both sides (32x32 shared-memory transposes where the layout
 // changes) and grid-stride free: one CTA per 32x32 tile.  None of them does arithmetic
 // beyond the TF32 hi/lo split (hi = cvt.rna.tf32(x), lo = x - hi, exact in fp32).
+#include <algorithm>
 #include <cuda_bf16.h>
 
 #include "internal.hpp"
@@ -93,6 +94,69 @@ void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, i
     launch_split_kernel(planes, grid, s, x, xs, N, C, HW, Cp, 1, HW, HW, 0, make_fastdiv((uint32_t)HW),
                         make_fastdiv((uint32_t)HW));
     CLB_CUDA(cudaGetLastError());
+}
+
+// The same conversion as a job over its tile grid (chained mode): the tail kernel takes tiles
+// from the job's counter (left off by the previous contraction's converter warps) until all are
+// done; persistent CTAs, one tile at a time through the smem staging of split_tile.
+SplitJob make_split_job(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp) {
+    SplitJob j{};
+    const int Hp = pad > 0 ? H + pad : H, Wp = pad > 0 ? W + pad : W;
+    j.x = x;
+    j.xs = xs;
+    j.n = N;
+    j.c = C;
+    j.hw = Hp * Wp;
+    j.cp = Cp;
+    j.h = pad > 0 ? H : 1;
+    j.w = pad > 0 ? W : H * W;
+    j.wp = pad > 0 ? Wp : H * W;
+    j.pad = pad;
+    j.hwd = make_fastdiv((uint32_t)j.hw);
+    j.wpd = make_fastdiv((uint32_t)j.wp);
+    j.ntx = (int)(((long long)N * j.hw + kSplitPx - 1) / kSplitPx);
+    j.nty = (Cp + 31) / 32;
+    return j;
+}
+
+template <int PLANES>
+__global__ void __launch_bounds__(256) split_tail_kernel(const SplitJob j) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ SplitSmem<PLANES> sm;
+    __shared__ int tile;
+    const int total = j.ntx * j.nty;
+    for (;;) {
+        if (threadIdx.x == 0) tile = (int)atomicAdd(j.counter, 1u);
+        __syncthreads();
+        const int t = tile;
+        if (t >= total) break;
+        split_tile<PLANES>(j.x, j.xs, j.n, j.c, j.hw, j.cp, j.h, j.w, j.wp, j.pad, j.hwd, j.wpd, t / j.nty, t % j.nty,
+                           (int)threadIdx.x, sm);
+        __syncthreads();   // the staging is reused by the next tile
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+void launch_split_tail(const SplitJob& j, int planes, cudaStream_t s) {
+    int dev = 0, sms = 0;
+    CLB_CUDA(cudaGetDevice(&dev));
+    CLB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const long long total = (long long)j.ntx * j.nty;
+    const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(total, 6LL * sms));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (planes == 2) CLB_CUDA(cudaLaunchKernelEx(&cfg, split_tail_kernel<2>, j));
+    else if (planes == kPlanesMixed) CLB_CUDA(cudaLaunchKernelEx(&cfg, split_tail_kernel<kPlanesMixed>, j));
+    else throw Error(6, "chained prepass: split formats only");
+    // reset the counter for the job's next use (stream-ordered, graph-capturable)
+    CLB_CUDA(cudaMemsetAsync(j.counter, 0, sizeof(unsigned), s));
 }
 
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,

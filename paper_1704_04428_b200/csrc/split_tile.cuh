@@ -50,6 +50,20 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
     return (__umulhi(n, f.m) + n) >> f.s;
 }
 
+// One NCHW -> split-rows conversion (a layer's prepass) as a job over its 128-pixel x
+// 32-channel tile grid, tile t = (bx = t / nty, by = t % nty).  Chained mode (cl_conv_forward_chain):
+// the converter warps of the previous layer's contraction take tiles from `counter` while that
+// contraction runs; a tail launch of the prepass kernel finishes the tiles left.
+struct SplitJob {
+    const float* x;
+    void* xs;
+    int n, c, hw, cp, h, w, wp, pad;   // hw = pixels per image of the output grid (Hp*Wp or H*W)
+    FastDiv hwd, wpd;
+    int ntx, nty;
+    int planes;        // operand format (the converting kernel must share it)
+    unsigned* counter;
+};
+
 // tile staging: hi (or raw for bf16 rows), 3xTF32 lo, mixed-format bf16(hi) / bf16(lo) pairs
 template <int PLANES>
 struct SplitSmem {

@@ -134,6 +134,11 @@ struct TcParams {
     int raw_wp, raw_hpwp;      // padded grid row width Wp and image size Hp*Wp
     FastDiv raw_gd, raw_wd;    // divide by Hp*Wp, by Wp
     const float* raw_x;        // the NCHW input (rare rows of a second image are read directly)
+    // chained prepass (nx_on): while this contraction runs, its converter warps (12-15) convert
+    // tiles of the NEXT layer's input (nx) -- memory-bound work on SMs whose tensor pipe is busy
+    // and whose DRAM traffic is 6-30 % of peak -- until this CTA's epilogue is done
+    SplitJob nx;
+    int nx_on;
     int max_sms;               // cap on the SMs the grid may occupy (0 = every co-resident unit):
                                // lets independent launches share the GPU (concurrent small layers)
     float* partials;           // [gridDim.x][128][bn] tile-tail partial sums
@@ -384,6 +389,66 @@ __device__ __forceinline__ void raw_convert_row(const TcParams& p, uint32_t stg,
     }
 }
 
+// One 128-pixel x 32-channel tile of a SplitJob by one warp, in registers (no shared memory:
+// the contraction owns it): lane = pixel row (4 passes), 16 channels per unit loaded coalesced
+// across the warp (consecutive pixels of one plane), the 128-byte split unit of each row written
+// by its lane.  Same bytes as split_tile (tf32_rna_bits == cvt.rna.tf32 for finite values).
+template <int PL>
+__device__ __forceinline__ void split_tile_warp(const SplitJob& j, int bx, int by, int lane) {
+    const long long NP = (long long)j.n * j.hw;
+    const long long plane = (long long)j.h * j.w;
+    uint32_t* xs = static_cast<uint32_t*>(j.xs);
+    const long long row_words = 2LL * j.cp;
+#pragma unroll 1
+    for (int pass = 0; pass < 4; ++pass) {
+        const long long gp = (long long)bx * kSplitPx + 32 * pass + lane;
+        if (gp >= NP) break;
+        const int n = NP <= 0x7fffffffLL ? (int)fdiv((uint32_t)gp, j.hwd) : (int)(gp / j.hw);
+        const int pix = (int)(gp - (long long)n * j.hw);
+        int sp = pix;
+        if (j.pad != 0) {
+            const int yy = (int)fdiv((uint32_t)pix, j.wpd), xx = pix - yy * j.wp;
+            sp = (yy < j.h && xx < j.w) ? yy * j.w + xx : -1;
+        }
+        const float* src = j.x + (long long)n * j.c * plane + (sp < 0 ? 0 : sp);
+#pragma unroll 1
+        for (int cb = 0; cb < 2; ++cb) {
+            const int c0 = by * 32 + 16 * cb;
+            if (c0 >= j.cp) break;
+            float v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                v[c] = (sp >= 0 && c0 + c < j.c) ? __ldg(src + (long long)(c0 + c) * plane) : 0.0f;
+            uint4* dst = reinterpret_cast<uint4*>(xs + gp * row_words + 2LL * c0);
+            uint32_t hb[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) hb[c] = tf32_rna_bits(v[c]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = make_uint4(hb[4 * q], hb[4 * q + 1], hb[4 * q + 2], hb[4 * q + 3]);
+            if constexpr (PL == 4) {
+                uint32_t w8[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    w8[k] = bf16x2_bits(__uint_as_float(hb[2 * k]), __uint_as_float(hb[2 * k + 1]));
+                dst[4] = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+                dst[5] = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    w8[k] = bf16x2_bits(v[2 * k] - __uint_as_float(hb[2 * k]), v[2 * k + 1] - __uint_as_float(hb[2 * k + 1]));
+                dst[6] = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+                dst[7] = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    dst[4 + q] = make_uint4(__float_as_uint(v[4 * q] - __uint_as_float(hb[4 * q])),
+                                            __float_as_uint(v[4 * q + 1] - __uint_as_float(hb[4 * q + 1])),
+                                            __float_as_uint(v[4 * q + 2] - __uint_as_float(hb[4 * q + 2])),
+                                            __float_as_uint(v[4 * q + 3] - __uint_as_float(hb[4 * q + 3])));
+            }
+        }
+    }
+}
+
 // Row j's source in the staged box of a k-iteration whose rows start at padded-grid row g0 and
 // whose box starts at (image n0, pixel p0): see raw_convert_row.
 __device__ __forceinline__ void raw_row_source(const TcParams& p, int g0, int j, int n0, int p0, int& sidx,
@@ -509,6 +574,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     uint64_t* raw_empty = raw_full + raw_slots;                  // [raw_slots] converted by all 8 epilogue warps
     int4* raw_meta = reinterpret_cast<int4*>(bars + 2 * stages + 10 + 2 * raw_slots);   // [raw_slots], 16-B aligned
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 9 + 2 * raw_slots);
+    volatile int* epi_done = reinterpret_cast<volatile int*>(tmem_slot + 1);   // chained prepass: stop
 
     const int warp = threadIdx.x >> 5;
     const uint32_t ncols = tmem_cols_for(bn);
@@ -533,6 +599,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             mbar_init(&tempty[a], CG * (kEpiThreads / 32));
         }
         mbar_init(fix_bar, 1);
+        *epi_done = 0;
         fence_barrier_init();
     }
     if (warp == 0 && lane_id() == 0) {
@@ -954,6 +1021,22 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 p.trace[blockIdx.x * kTraceSlots + 22] = (unsigned long long)c_empty;
                 p.trace[blockIdx.x * kTraceSlots + 23] = (unsigned long long)c_conv;
             }
+        } else if (p.nx_on) {
+            // chained prepass: tiles of the next layer's input, taken from the job's counter until
+            // the job is done or this CTA's epilogue has finished (a tail launch does the rest)
+            const int lane = (int)lane_id();
+            const int total = p.nx.ntx * p.nx.nty;
+            int tiles = 0;
+            while (!*epi_done) {
+                int t = 0;
+                if (lane == 0) t = (int)atomicAdd(p.nx.counter, 1u);
+                t = __shfl_sync(0xffffffffu, t, 0);
+                if (t >= total) break;
+                if (planes == 4) split_tile_warp<4>(p.nx, t / p.nx.nty, t % p.nx.nty, lane);
+                else split_tile_warp<2>(p.nx, t / p.nx.nty, t % p.nx.nty, lane);
+                ++tiles;
+            }
+            if (TRACE && lane == 0) atomicAdd(&p.trace[blockIdx.x * kTraceSlots + 23], (unsigned long long)tiles);
         }
     } else {
         // --------------------------------------------------------------- epilogue ----
@@ -1146,6 +1229,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 t_stored = globaltimer_ns();
             }
         }
+        if (threadIdx.x == 4 * 32) *epi_done = 1;   // the chained prepass stops taking tiles
         if (TRACE && threadIdx.x == 4 * 32) {
             p.trace[blockIdx.x * kTraceSlots + 5] = (unsigned long long)(clock64() - t_start);
             p.trace[blockIdx.x * kTraceSlots + 6] = (unsigned long long)w_tfull;

@@ -295,6 +295,27 @@ class ConvPlan:
         return y_host
 
 
+def forward_chain(plans: Sequence["ConvPlan"], xs, ys, workspaces=None, stream=None):
+    """One step of independent-or-chained layers on one stream (cl_conv_forward_chain): layer
+    i+1's NCHW -> split prepass rides on layer i's contraction (its converter warps), a tail
+    launch finishes it.  xs / ys: NCHW CUDA tensors per plan; results equal per-plan forwards."""
+    n = len(plans)
+    if not (len(xs) == len(ys) == n) or (workspaces is not None and len(workspaces) != n):
+        raise ValueError("forward_chain: one x, y (and workspace) per plan")
+    for p, x, y, ws in zip(plans, xs, ys, workspaces or [None] * n):
+        p._check_device_tensor(x, p.input_shape("nchw"), "x")
+        p._check_device_tensor(y, p.output_shape(), "y")
+        if ws is not None and ws.numel() * ws.element_size() < p.workspace_bytes():
+            raise ValueError(f"workspace: {ws.numel() * ws.element_size()} bytes < required {p.workspace_bytes()}")
+    arr = ctypes.c_void_p * n
+    ph = arr(*[p._h.value for p in plans])
+    xh = arr(*[x.data_ptr() for x in xs])
+    yh = arr(*[y.data_ptr() for y in ys])
+    wh = arr(*[(w.data_ptr() if w is not None else None) for w in (workspaces or [None] * n)])
+    _lib.check(_lib.lib().cl_conv_forward_chain(ph, xh, yh, wh, n, ConvPlan._stream(stream)))
+    return ys
+
+
 def run_method(method: str, x, w, precision: str = "fp32", pad: Optional[int] = None, stride: int = 1):
     """Functional form of methods.cpp:65-88 for GPU methods: x [N,C,H,W] and w [M,k,k,C]
     torch CUDA tensors -> y [N,M,P,Q].  Applies the reference's k == 1 routing."""

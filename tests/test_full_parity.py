@@ -174,3 +174,42 @@ def test_full_batch_classic_3xtf32_split(oracle, gpu, tmp_path):
             del x
         m = oracle.parity_metrics(yh, _REFS[key])
         assert m["rel_l2"] <= FP32_L2 and m["max_rel"] <= FP32_MAX, (layer.name, "3xtf32", m)
+
+
+@pytest.mark.parametrize("workload", ["vgg16", "alexnet"])
+def test_full_batch_chained_step(oracle, gpu, workload):
+    """The whole workload at its full batch through ONE cl_conv_forward_chain call (each layer's
+    prepass riding on the previous layer's contraction where the heuristic hosts it): every
+    layer's sampled images against the oracle, and bit-identical to the per-layer forwards."""
+    import torch
+    import paper_1704_04428_b200 as clb
+    from paper_1704_04428_b200 import rng
+    layers = [l for wl, l in CASES if wl == workload]
+    plans, xs, ys, ws, solo = [], [], [], [], []
+    for layer in layers:
+        seed = seed_for(layer)
+        x, w = rng.make_problem(layer.batch, layer.channels, layer.height, layer.width, layer.kernel_count,
+                                layer.kernel_size, seed=seed)
+        lc = clb.LayerConfig(layer.name, layer.channels, layer.height, layer.width, layer.kernel_count,
+                             layer.kernel_size, batch=layer.batch)
+        p = clb.ConvPlan(lc, "auto", "fp32")
+        p.set_weights(w)
+        plans.append(p)
+        xs.append(x)
+        ys.append(torch.empty(p.output_shape(), device="cuda"))
+        ws.append(w)
+    clb.forward_chain(plans, xs, ys)
+    torch.cuda.synchronize()
+    for layer, p, x, y, w in zip(layers, plans, xs, ys, ws):
+        y0 = p.forward(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0), layer.name
+        del y0
+        picks = picks_for(layer.batch, seed_for(layer))
+        idx = torch.tensor(picks, device="cuda")
+        xh = x.index_select(0, idx).cpu().numpy()
+        ref = oracle_ref(oracle, layer, xh, w.cpu().numpy())
+        m = oracle.parity_metrics(y.index_select(0, idx).cpu().numpy(), ref)
+        assert m["rel_l2"] <= FP32_L2 and m["max_rel"] <= FP32_MAX, (layer.name, m)
+    for p in plans:
+        p.close()

@@ -937,3 +937,66 @@ def test_selector_timing_cache(oracle, clb, torch_cuda):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
                        cwd=str(Path(__file__).resolve().parent.parent), env=dict(os.environ, CLB_AUTOTUNE="0"))
     assert r.returncode == 0 and r.stdout.strip() == "kn2row-gpu", (r.stdout, r.stderr[-1000:])
+
+
+_CHAIN_SCRIPT = r'''
+import sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+from oracle import oracle as O
+import paper_1704_04428_b200 as clb
+from tests.test_gpu_parity import chain_check
+chain_check(O, clb, torch)
+print("CHAIN_OK")
+'''
+
+
+def test_forward_chain_matches_per_plan_forwards(oracle, clb, torch_cuda, tmp_path):
+    """cl_conv_forward_chain: layer i+1's prepass rides on layer i's contraction (its converter
+    warps take tiles of x_{i+1} while the tensor pipe runs; a tail launch finishes them).  The
+    outputs are BIT-IDENTICAL to per-plan forwards (same operand bytes), right against the oracle,
+    and a second chained step (counters reset by the tails) gives the same bits again.  The chain
+    mixes the padded-row and TMA-im2col geometries, a direct-gpu layer (which cannot host a job)
+    and a layer whose precision differs from its neighbour's (no hosting across formats).  Run
+    with the default hosting heuristic here and with every eligible prepass hosted
+    (CLB_CHAIN_FORCE=1) in a subprocess."""
+    import subprocess, sys
+    from pathlib import Path
+    chain_check(oracle, clb, torch_cuda)
+    script = tmp_path / "chain.py"
+    script.write_text(_CHAIN_SCRIPT)
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, CLB_CHAIN_FORCE="1"), cwd=str(root))
+    assert r.returncode == 0 and "CHAIN_OK" in r.stdout, r.stderr[-3000:]
+
+
+def chain_check(oracle, clb, torch_cuda):
+    torch = torch_cuda
+    shapes = [("c3", 3, 32, 32, 16, 3, "fp32"), ("a", 16, 32, 32, 64, 3, "fp32"), ("b", 64, 32, 32, 128, 3, "fp32"),
+              ("c", 128, 14, 14, 256, 3, "fp32"), ("d", 256, 14, 14, 64, 1, "fp32"), ("e", 64, 14, 14, 96, 5, "fp32"),
+              ("f", 96, 14, 14, 32, 3, "tf32"), ("g", 32, 14, 14, 48, 3, "fp32")]
+    N = 6
+    plans, xs, ys, refs_in = [], [], [], []
+    for i, (name, C, H, W, M, k, prec) in enumerate(shapes):
+        x, w = oracle.make_problem(N, C, H, W, M, k, 600 + i)
+        p = clb.ConvPlan(clb.LayerConfig(name, C, H, W, M, k, batch=N), "auto", prec)
+        p.set_weights(torch.from_numpy(w).cuda())
+        plans.append(p)
+        xs.append(torch.from_numpy(x).cuda())
+        ys.append(torch.full(p.output_shape(), float("nan"), device="cuda"))
+        refs_in.append((x, w, prec))
+    solo = [p.forward(x) for p, x in zip(plans, xs)]
+    torch.cuda.synchronize()
+    for rnd in range(2):
+        for y in ys:
+            y.fill_(float("nan"))
+        clb.forward_chain(plans, xs, ys)
+        torch.cuda.synchronize()
+        for i, (y, y0) in enumerate(zip(ys, solo)):
+            assert torch.equal(y, y0), (shapes[i], rnd)
+    for (x, w, prec), y, s in zip(refs_in, ys, shapes):
+        m = oracle.parity_metrics(y.cpu().numpy(), oracle.conv_batch(x, w))
+        assert m["rel_l2"] <= (FP32_L2 if prec == "fp32" else TF32_L2), (s, m)
+    for p in plans:
+        p.close()
