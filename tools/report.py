@@ -27,8 +27,9 @@ from oracle import oracle as O
 import os
 # fp32-faithful peak: measured bf16 burst / 2 (tf32 rate) x 1/2 for the default mixed split
 # (4 tf32-MMA slots per 16 K-elements) or x 1/3 for CLB_SPLIT=3xtf32 (6 slots)
-PEAK_3X = 1667.0 / 2 / (3 if os.environ.get("CLB_SPLIT") == "3xtf32" else 2)
-HBM = 6550.7                  # GB/s measured
+_pk = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())
+PEAK_3X = float(_pk["bf16_tflops"]) / 2 / (3 if os.environ.get("CLB_SPLIT") == "3xtf32" else 2)
+HBM = float(_pk["hbm_gbs"])   # GB/s measured
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workloads", default="c1,alexnet-b1,alexnet,vgg16,googlenet,sweep,scale")
