@@ -194,14 +194,18 @@ def require_device(device: int = 0) -> None:
 
 def verify(layers: Iterable[LayerConfig], methods: Iterable[str] = None, seed: int = 0, max_hw: int = 0,
            precision: str = "fp32", rel: float = 1e-5, abs_tol: float = 1e-6, perturb=None,
-           device: int = 0) -> VerifyReport:
+           device: int = 0, comparator=None) -> VerifyReport:
     """Deterministic data per layer (input stream split(seed, 2 idx), kernels split(seed, 2 idx + 1),
     bench.cpp:174-177; a batch continues the input stream, so image 0 is the reference's),
     the library's own direct method as the comparator (the reference uses conv_mcmk_sum,
     bench.cpp:187 -- here direct-gpu, an fp32 FMA restatement of the same loop nest), and one
     entry per (layer, method).  fp32 is held to the reference law allclose(rel, abs + rel
     max|ref|) (bench.cpp:188-192); the TF32/BF16 fast modes to the north star's rel-L2 <= 1e-2.
-    Strided layers and conv1x1 on k != 1 are skipped, not failed (bench.cpp:164-167, 194-198)."""
+    Strided layers and conv1x1 on k != 1 are skipped, not failed (bench.cpp:164-167, 194-198).
+
+    `comparator(x, w) -> y` (torch tensors, NCHW / MKKC / NCHW) replaces the direct-gpu
+    comparator: the tests pass the CPU oracle conv_mcmk_sum here (the reference's own comparator,
+    bench.cpp:186), which the package itself never imports (oracle/ is test infrastructure)."""
     import torch
 
     from . import rng
@@ -225,9 +229,12 @@ def verify(layers: Iterable[LayerConfig], methods: Iterable[str] = None, seed: i
         wt = torch.empty((lay.kernel_count, lay.kernel_size, lay.kernel_size, lay.channels), device=dev)
         rng.fill_uniform(x, rng.split(seed, 2 * idx))
         rng.fill_uniform(wt, rng.split(seed, 2 * idx + 1))
-        with ConvPlan(lay, "direct-gpu", "fp32", device) as plan:
-            plan.set_weights(wt)
-            ref = plan.forward(x)
+        if comparator is not None:
+            ref = comparator(x, wt).to(dev)
+        else:
+            with ConvPlan(lay, "direct-gpu", "fp32", device) as plan:
+                plan.set_weights(wt)
+                ref = plan.forward(x)
         ref64 = ref.double()
         ref_max = ref64.abs().max().item()
         tol_abs = abs_tol + rel * ref_max                                # scaled_tolerance (tensor.cpp:211-213)

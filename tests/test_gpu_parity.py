@@ -1000,3 +1000,24 @@ def chain_check(oracle, clb, torch_cuda):
         assert m["rel_l2"] <= (FP32_L2 if prec == "fp32" else TF32_L2), (s, m)
     for p in plans:
         p.close()
+
+
+def test_harness_verify_against_cpu_oracle(oracle, clb, torch_cuda):
+    """The verify mirror with the reference's own comparator: the CPU oracle conv_mcmk_sum
+    (bench.cpp:186), passed in by the test (the package never imports oracle/), on the BASELINE
+    layer shapes at reduced size -- every GPU method holds the reference allclose law."""
+    torch = torch_cuda
+    from paper_1704_04428_b200 import harness, workloads
+
+    def cpu_oracle(x, w):
+        return torch.from_numpy(oracle.conv_batch(x.cpu().numpy(), w.cpu().numpy()))
+
+    layers = [l for l in workloads.all_layers() if l.name in ("c1", "alexnet/conv2", "vgg16/conv3_1",
+                                                               "googlenet/4a_5x5", "googlenet/5b_1x1")]
+    layers = [clb.LayerConfig(l.name, l.channels, l.height, l.width, l.kernel_count, l.kernel_size, batch=2)
+              for l in layers]
+    rep = harness.verify(layers, seed=5, max_hw=14, comparator=cpu_oracle)
+    assert rep.entries and rep.all_pass(), [(e.layer, e.method, e.max_abs_err) for e in rep.entries if not e.passed]
+    bad = harness.verify(layers[:1], ["kn2row-gpu"], seed=5, max_hw=14, comparator=cpu_oracle,
+                         perturb=lambda y: y.view(-1)[7].add_(1.0))
+    assert not bad.all_pass()
