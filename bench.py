@@ -345,11 +345,19 @@ class ClockSampler:
 
     def summary(self, t0: float, t1: float):
         win = [s for s in self.samples if t0 <= s[0] <= t1]
+        note = None
+        if not win and self.samples:
+            # a timed region shorter than the sampling period: the samples nearest to it
+            win = sorted(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))[:2]
+            note = "timed region shorter than the 5 ms sampling period: nearest samples"
         if not win:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         reasons = sorted({name for s in win for name, bit in self.REASONS.items() if s[4] & bit})
-        return {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": win[0][2],
-                "power_w_max": max(s[3] for s in win), "reasons": reasons, "samples": len(win)}
+        out = {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": win[0][2],
+               "power_w_max": max(s[3] for s in win), "reasons": reasons, "samples": len(win)}
+        if note:
+            out["note"] = note
+        return out
 
 
 # ------------------------------------------------------------------- CPU baseline ----
