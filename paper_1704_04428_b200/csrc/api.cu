@@ -868,8 +868,11 @@ cl_status cl_conv_forward_chain(cl_plan* const* plans, const float* const* xs, f
             for (int j = 0; j < i; ++j) require(plans[j] != plans[i], "cl_conv_forward_chain: a plan appears twice");
             require(plans[i]->device == plans[0]->device, "cl_conv_forward_chain: plans on different devices");
         }
+        // every plan's lock, taken in address order (two chains over the same plans never deadlock)
+        std::vector<cl_plan*> order(plans, plans + count);
+        std::sort(order.begin(), order.end());
         std::vector<std::unique_lock<std::mutex>> locks;
-        for (int i = 0; i < count; ++i) locks.emplace_back(plans[i]->mu);
+        for (cl_plan* q : order) locks.emplace_back(q->mu);
         CLB_CUDA(cudaSetDevice(plans[0]->device));
         std::vector<SplitJob> jobs(count);
         std::vector<char> chainable(count, 0);

@@ -361,3 +361,21 @@ def test_bench_gpus_flag_launches_ranks(workload, scaling, batches):
     assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["rank_batches"] == batches
     assert d["config"]["per_gpu_batch"] == batches[0]
     assert d["config"]["global_batch"] == sum(batches)
+
+
+def test_concurrency_sm_shares():
+    """concurrency.sm_shares: caps proportional to the weights, even (CTA pairs), >= 2 each,
+    never above the SM count (every launch's CTAs must stay co-resident), remainder to the
+    heaviest layers."""
+    from paper_1704_04428_b200 import concurrency
+    for weights in ([1.0], [1, 1], [5, 1, 1, 1], [0.05, 0.06, 0.04, 0.04, 0.03, 0.02, 0.03, 0.035, 0.025],
+                    [1e-3] * 40):
+        caps = concurrency.sm_shares(weights, 148)
+        assert len(caps) == len(weights)
+        assert sum(caps) <= 148 and all(c >= 2 and c % 2 == 0 for c in caps), (weights, caps)
+        heavy = max(range(len(weights)), key=lambda i: weights[i])
+        assert caps[heavy] == max(caps)
+    assert concurrency.sm_shares([1.0], 148) == [148]
+    assert sum(concurrency.sm_shares([3, 1], 148)) == 148
+    with pytest.raises(ValueError):
+        concurrency.sm_shares([1.0] * 80, 148)      # 80 layers x 2 SMs do not fit
