@@ -133,6 +133,21 @@ CL_API cl_status cl_conv_forward_nhwc(cl_plan* plan, const float* d_x, float* d_
 CL_API cl_status cl_conv_forward_chain(cl_plan* const* plans, const float* const* d_xs, float* const* d_ys,
                                        void* const* d_wss, int count, void* stream);
 
+/* Fused output-channel all-gather (multi-GPU output-channel sharding): with
+ * n_peers > 0 the plan's NCHW epilogue stores its M output channels into EACH of the n_peers
+ * full [N][m_total][P][Q] tensors at channel offset m_offset -- P2P stores over NVLink /
+ * NVSwitch when the pointers are CUDA-IPC mappings of the other ranks' buffers (one of them the
+ * caller's own) -- instead of into the y argument of cl_conv_forward.  The gather thus overlaps
+ * the contraction tile by tile; the caller synchronises the ranks (stream sync + a barrier)
+ * before reading.  Implicit kn2row / conv1x1 / im2col plans; n_peers = 0 restores the default. */
+CL_API cl_status cl_conv_set_peer_outputs(cl_plan* plan, float* const* d_peer_y, int n_peers, int m_offset,
+                                          int m_total);
+
+/* CUDA IPC helpers for the fused all-gather (64-byte cudaIpcMemHandle_t as opaque bytes). */
+CL_API cl_status cl_ipc_get_mem_handle(const void* d_ptr, void* handle64);
+CL_API cl_status cl_ipc_open_mem_handle(const void* handle64, void** d_ptr);
+CL_API cl_status cl_ipc_close_mem_handle(void* d_ptr);
+
 /* Host-buffer end-to-end call (the run_method surface): H2D of x, forward, D2H of y,
  * synchronous.  Host buffers should be pinned for full PCIe bandwidth. */
 CL_API cl_status cl_conv_forward_host(cl_plan* plan, const float* h_x, float* h_y, void* stream);

@@ -34,7 +34,8 @@ EXPORTS = [
     "cl_conv_resolved_method", "cl_conv_forward", "cl_conv_forward_nhwc", "cl_conv_forward_host", "cl_conv_forward_host_async", "cl_conv_last_launch_count",
     "cl_conv_destroy", "cl_gemm_f32", "cl_gemm_workspace_bytes", "cl_shift_add_row", "cl_last_error",
     "cl_method_name", "cl_method_from_name", "cl_abi_version", "cl_device_count", "cl_fill_uniform",
-    "cl_conv_set_profile_events", "cl_conv_set_max_sms", "cl_conv_forward_chain", "cl_checksum_fnv1a",
+    "cl_conv_set_profile_events", "cl_conv_set_max_sms", "cl_conv_forward_chain", "cl_conv_set_peer_outputs",
+    "cl_ipc_get_mem_handle", "cl_ipc_open_mem_handle", "cl_ipc_close_mem_handle", "cl_checksum_fnv1a",
 ]
 
 
@@ -85,6 +86,10 @@ def lib() -> ctypes.CDLL:
     L.cl_fill_uniform.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, vp]
     L.cl_conv_set_profile_events.argtypes = [vp, vp, vp]
     L.cl_conv_set_max_sms.argtypes = [vp, i32]
+    L.cl_conv_set_peer_outputs.argtypes = [vp, ctypes.POINTER(vp), i32, i32, i32]
+    L.cl_ipc_get_mem_handle.argtypes = [vp, vp]
+    L.cl_ipc_open_mem_handle.argtypes = [vp, ctypes.POINTER(vp)]
+    L.cl_ipc_close_mem_handle.argtypes = [vp]
     L.cl_conv_forward_chain.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
                                         i32, vp]
     L.cl_checksum_fnv1a.restype = ctypes.c_uint64

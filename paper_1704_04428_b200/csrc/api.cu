@@ -104,6 +104,8 @@ struct cl_plan {
     // device weights instead and picks up later set_weights calls like every other method.
     std::vector<float> wparam;
     int max_sms = 0;           // engine grid cap in SMs (cl_conv_set_max_sms; 0 = all co-resident units)
+    std::vector<float*> peers; // fused output all-gather targets (cl_conv_set_peer_outputs)
+    int peer_m0 = 0, peer_M = 0;
     unsigned* flags = nullptr; // stream-K fixup flags, zeroed once, self-resetting
     bool padded_rows = false;  // implicit kn2row in tap-shared (zero-padded row) mode
     bool raw_a = false;        // ... with A converted from the raw NCHW input inside the contraction
@@ -324,6 +326,14 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         t.flags = p->flags;
         t.flags_zeroed = 1;
         t.max_sms = p->max_sms;
+        if (!p->peers.empty()) {
+            if (t.epi != EPI_NCHW && t.epi != EPI_NCHW_PADDED)
+                throw Error(CL_EUNSUPPORTED, "peer outputs: implicit kn2row / conv1x1 / im2col plans, NCHW only");
+            t.n_peers = (int)p->peers.size();
+            for (int r = 0; r < t.n_peers; ++r) t.peers[r] = p->peers[r];
+            t.peer_m0 = p->peer_m0;
+            t.peer_M = p->peer_M;
+        }
         if (next_job && is_split(p->planes) && (p->planes == next_job->planes)) {
             t.nx = *next_job;
             t.nx_on = 1;
@@ -1143,6 +1153,48 @@ cl_status cl_fill_uniform(float* d, uint64_t n, uint64_t seed, uint64_t first_in
         require(d || n == 0, "cl_fill_uniform: null pointer");
         launch_fill_uniform(d, n, seed, first_index, static_cast<cudaStream_t>(stream));
     });
+}
+
+cl_status cl_conv_set_peer_outputs(cl_plan* p, float* const* d_peer_y, int n_peers, int m_offset, int m_total) {
+    return guarded([&] {
+        require(p, "cl_conv_set_peer_outputs: null plan");
+        require(n_peers >= 0 && n_peers <= kMaxPeers, "cl_conv_set_peer_outputs: 0..8 peers");
+        require(n_peers == 0 || d_peer_y, "cl_conv_set_peer_outputs: null peer list");
+        require(n_peers == 0 || (m_offset >= 0 && m_offset + p->d.m <= m_total),
+                "cl_conv_set_peer_outputs: channel slice outside the full output");
+        const bool ok_method = p->method == CL_METHOD_KN2ROW || p->method == CL_METHOD_CONV1X1 ||
+                               p->method == CL_METHOD_IM2COL || p->method == CL_METHOD_IM2ROW;
+        require(n_peers == 0 || (ok_method && p->stack_k == 1),
+                "cl_conv_set_peer_outputs: implicit kn2row / conv1x1 / im2col plans only");
+        std::lock_guard<std::mutex> lock(p->mu);
+        p->peers.assign(d_peer_y, d_peer_y + n_peers);
+        for (float* q : p->peers) require(q != nullptr, "cl_conv_set_peer_outputs: null peer pointer");
+        p->peer_m0 = m_offset;
+        p->peer_M = m_total;
+    });
+}
+
+cl_status cl_ipc_get_mem_handle(const void* d_ptr, void* handle64) {
+    return guarded([&] {
+        require(d_ptr && handle64, "cl_ipc_get_mem_handle: null argument");
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        CLB_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+        std::memcpy(handle64, &h, 64);
+    });
+}
+
+cl_status cl_ipc_open_mem_handle(const void* handle64, void** d_ptr) {
+    return guarded([&] {
+        require(handle64 && d_ptr, "cl_ipc_open_mem_handle: null argument");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, 64);
+        CLB_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+cl_status cl_ipc_close_mem_handle(void* d_ptr) {
+    return guarded([&] { CLB_CUDA(cudaIpcCloseMemHandle(d_ptr)); });
 }
 
 cl_status cl_conv_set_max_sms(cl_plan* p, int max_sms) {

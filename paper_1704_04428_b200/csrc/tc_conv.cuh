@@ -64,6 +64,7 @@ constexpr int kChunkK = 192;          // fp32-faithful splits: K-elements per TM
 constexpr int kRawPx = 140;   // >= 3 (alignment) + 134 rows (k = 7)
 constexpr int kRawSlotBytes = 16 * kRawPx * 4;
 constexpr int kBarrierBytes = 512;
+constexpr int kMaxPeers = 8;     // ranks of a fused output all-gather (one node)
 // TMEM loads (16 columns each) in flight per chunk fold.  2 (not 4) leaves the epilogue warps
 // the registers the raw-input conversion service needs next to their 128 running sums.
 constexpr int kFoldLoads = 2;
@@ -139,6 +140,13 @@ struct TcParams {
     // and whose DRAM traffic is 6-30 % of peak -- until this CTA's epilogue is done
     SplitJob nx;
     int nx_on;
+    // fused output-channel all-gather (dist.MShardPlan fused mode): the NCHW epilogue stores this
+    // plan's output channels [peer_m0, peer_m0 + M_plan) straight into each rank's full
+    // [N][peer_M][P][Q] output (P2P stores over NVLink / NVSwitch through CUDA-IPC-mapped
+    // pointers; one of them is this rank's own), so the gather overlaps the contraction tile by
+    // tile instead of following it as a collective.  n_peers = 0: the plan's own output.
+    float* peers[kMaxPeers];
+    int n_peers, peer_m0, peer_M;
     int max_sms;               // cap on the SMs the grid may occupy (0 = every co-resident unit):
                                // lets independent launches share the GPU (concurrent small layers)
     float* partials;           // [gridDim.x][128][bn] tile-tail partial sums
@@ -1201,15 +1209,25 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const int rem = row - n * hw;
                 const int y = rem / p.epi_wp;
                 const int xq = rem - y * p.epi_wp;
-                if (n < p.epi_n && y < p.P && xq < p.Q)
-                    store_nchw(p.out + ((long long)n * p.out_channels + col0) * p.pq_out + (long long)y * p.Q + xq,
-                               p.pq_out, ncol, p.accumulate, sum);
+                if (n < p.epi_n && y < p.P && xq < p.Q) {
+                    const long long pix = (long long)y * p.Q + xq;
+                    if (p.n_peers == 0)
+                        store_nchw(p.out + ((long long)n * p.out_channels + col0) * p.pq_out + pix, p.pq_out, ncol,
+                                   p.accumulate, sum);
+                    for (int r = 0; r < p.n_peers; ++r)
+                        store_nchw(p.peers[r] + ((long long)n * p.peer_M + p.peer_m0 + col0) * p.pq_out + pix, p.pq_out,
+                                   ncol, p.accumulate, sum);
+                }
             } else if (row < p.rows) {
                 if (p.epi == EPI_NCHW) {
                     const int n = row / p.pq_out;
                     const int pq = row - n * p.pq_out;
-                    store_nchw(p.out + ((long long)n * p.out_channels + col0) * p.pq_out + pq, p.pq_out,
-                               ncol, p.accumulate, sum);
+                    if (p.n_peers == 0)
+                        store_nchw(p.out + ((long long)n * p.out_channels + col0) * p.pq_out + pq, p.pq_out,
+                                   ncol, p.accumulate, sum);
+                    for (int r = 0; r < p.n_peers; ++r)
+                        store_nchw(p.peers[r] + ((long long)n * p.peer_M + p.peer_m0 + col0) * p.pq_out + pq,
+                                   p.pq_out, ncol, p.accumulate, sum);
                 } else if (p.epi == EPI_NHWC_PADDED) {
                     // padded pixel space -> channels-last output row (n*P + y)*Q + x
                     const int hw = p.epi_hp * p.epi_wp;

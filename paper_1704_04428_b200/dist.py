@@ -140,7 +140,8 @@ class MShardPlan:
     it serves batch-1 layers (C1, AlexNet b1, the C5 k-sweep) that batch sharding cannot split.
     """
 
-    def __init__(self, layer, info: RankInfo, method: str = "auto", precision: str = "fp32", device: int = None):
+    def __init__(self, layer, info: RankInfo, method: str = "auto", precision: str = "fp32", device: int = None,
+                 fused: bool = False):
         import dataclasses
         from .methods import ConvPlan
         if layer.kernel_count < info.world:
@@ -148,8 +149,46 @@ class MShardPlan:
         self.layer, self.info = layer, info
         self.m0, self.m1 = channel_slice(layer.kernel_count, info.world, info.rank)
         self.device = info.local_rank if device is None else device
+        if fused and method == "auto":
+            # the fused gather lives in the implicit / conv1x1 epilogue (not the explicit GEMM +
+            # shift-add the timing cache may pick for a small slice)
+            method = "conv1x1-gpu" if layer.kernel_size == 1 else "kn2row-gpu"
         self.plan = ConvPlan(dataclasses.replace(layer, kernel_count=self.m1 - self.m0), method, precision,
                              self.device)
+        self.fused = fused
+        self._opened = []
+        if fused:
+            self._setup_fused()
+
+    def _setup_fused(self):
+        """Fused all-gather: every rank allocates its FULL output, the ranks exchange CUDA IPC handles
+        (over the process group), and this rank's plan writes its channel slice into every rank's
+        output from its epilogue (cl_conv_set_peer_outputs: P2P stores over NVLink / NVSwitch, the
+        gather overlapping the contraction) -- no collective on the data path."""
+        import ctypes
+        import torch
+        import torch.distributed as dist
+        from . import _lib
+        L = self.layer
+        self.y_full = torch.empty((L.batch, L.kernel_count, *self.plan.out_hw), device=f"cuda:{self.device}",
+                                  dtype=torch.float32)
+        h = (ctypes.c_char * 64)()
+        _lib.check(_lib.lib().cl_ipc_get_mem_handle(ctypes.c_void_p(self.y_full.data_ptr()), h))
+        handles = [bytes(h)]
+        if dist.is_available() and dist.is_initialized():
+            handles = [None] * self.info.world
+            dist.all_gather_object(handles, bytes(h))
+        ptrs = []
+        for r, hb in enumerate(handles):
+            if r == self.info.rank:
+                ptrs.append(self.y_full.data_ptr())
+                continue
+            p = ctypes.c_void_p()
+            _lib.check(_lib.lib().cl_ipc_open_mem_handle(ctypes.create_string_buffer(hb, 64), ctypes.byref(p)))
+            self._opened.append(p.value)
+            ptrs.append(p.value)
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        _lib.check(_lib.lib().cl_conv_set_peer_outputs(self.plan._h, arr, len(ptrs), self.m0, L.kernel_count))
 
     @property
     def method(self):
@@ -167,7 +206,23 @@ class MShardPlan:
         return (L.batch, L.kernel_count, *self.plan.out_hw)
 
     def forward(self, x):
-        """x: full [N, C, H, W] device tensor on every rank -> full y (NCCL all-gather)."""
+        """x: full [N, C, H, W] device tensor on every rank -> full y (NCCL all-gather, or the
+        fused epilogue stores + a stream sync and a barrier)."""
+        if self.fused:
+            import ctypes
+            import torch
+            import torch.distributed as dist
+            from . import _lib
+            self.plan._check_device_tensor(x, self.plan.input_shape("nchw"), "x")
+            s = torch.cuda.current_stream()
+            # y_full stands in for the slice output (the epilogue writes the peers' full outputs)
+            _lib.check(_lib.lib().cl_conv_forward(self.plan._h, ctypes.c_void_p(x.data_ptr()),
+                                                  ctypes.c_void_p(self.y_full.data_ptr()), None,
+                                                  ctypes.c_void_p(s.cuda_stream)))
+            s.synchronize()                  # this rank's stores (to every rank) are complete
+            if dist.is_available() and dist.is_initialized():
+                dist.barrier()               # ... and every other rank's into this one
+            return self.y_full
         return mshard_conv(x, None, self.info, lambda xx, _w: self.plan.forward(xx),
                            m_total=self.layer.kernel_count)
 
@@ -181,4 +236,8 @@ class MShardPlan:
         return mshard_conv(x_host, None, self.info, conv, m_total=self.layer.kernel_count)
 
     def close(self):
+        from . import _lib
+        for ptr in self._opened:
+            _lib.lib().cl_ipc_close_mem_handle(ptr)
+        self._opened = []
         self.plan.close()

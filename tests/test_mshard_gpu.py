@@ -4,6 +4,10 @@
                its kernel slice and runs the plan's HOST path; gloo gathers the slices on the host
   ws1 / nccl : the device path through NCCL's all_gather_into_tensor (world size 1 on this
                one-GPU box; the same call spans 8 GPUs over NVLink / NVSwitch)
+  *-fused    : the gather fused into the epilogue (cl_conv_set_peer_outputs): each rank's
+               contraction stores its channel slice into every rank's full output through
+               CUDA-IPC-mapped pointers (ws2: both ranks on cuda:0, the peer buffer mapped from the
+               other process; the kernels never wait on each other -- a barrier after both finish)
 Both against the single-process oracle on the same seeded inputs.
 """
 import json
@@ -27,6 +31,8 @@ from paper_1704_04428_b200 import dist
 from oracle import oracle as O
 info = dist.from_env()
 torch.cuda.set_device(0)
+fused = backend.endswith("-fused")
+backend = backend.replace("-fused", "")
 if backend == "nccl":
     tdist.init_process_group("nccl", device_id=torch.device("cuda:0"))
 else:
@@ -35,8 +41,8 @@ out = []
 for (N, C, H, W, M, k) in [(1, 64, 56, 56, 64, 3), (2, 96, 27, 27, 250, 5), (1, 256, 28, 28, 256, 1), (3, 16, 13, 13, 7, 3)]:
     x, w = O.make_problem(N, C, H, W, M, k, N + M)
     layer = clb.LayerConfig("ms", C, H, W, M, k, batch=N)
-    mp = dist.MShardPlan(layer, info, device=0)
-    if backend == "nccl":
+    mp = dist.MShardPlan(layer, info, device=0, fused=fused)
+    if backend == "nccl" or fused:
         mp.set_weights(torch.from_numpy(w).cuda())
         y = mp.forward(torch.from_numpy(x).cuda()).cpu().numpy()
     else:
@@ -67,7 +73,8 @@ def _launch(tmp_path, nproc, backend, port):
     return json.loads([l for l in r.stdout.splitlines() if l.startswith("[")][-1])
 
 
-@pytest.mark.parametrize("nproc,backend,port", [(2, "gloo", 29531), (1, "nccl", 29533)])
+@pytest.mark.parametrize("nproc,backend,port", [(2, "gloo", 29531), (1, "nccl", 29533), (2, "gloo-fused", 29535),
+                                               (1, "nccl-fused", 29537)])
 def test_mshard_plan(tmp_path, nproc, backend, port):
     res = _launch(tmp_path, nproc, backend, port)
     assert len(res) == 4
