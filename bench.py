@@ -75,10 +75,11 @@ def parse_args(argv=None):
     ap.add_argument("--layout", default="nchw", choices=["nchw", "nhwc"],
                     help="device tensors NCHW (the reference interface, default) or channels-last "
                          "(cl_conv_forward_nhwc; the e2e leg stays NCHW)")
-    ap.add_argument("--shard", choices=["batch", "channels"], default="batch",
+    ap.add_argument("--shard", choices=["batch", "channels", "channels-fused"], default="batch",
                     help="batch: images split across ranks (no data-path collective); channels: every rank "
                          "convolves all images with its slice of the kernels and an NCCL all-gather assembles "
-                         "the output (dist.MShardPlan; for batch-1 layers)")
+                         "the output (dist.MShardPlan; for batch-1 layers); channels-fused: the same with the "
+                         "gather fused into the epilogue (P2P stores into every rank's output over CUDA IPC)")
     ap.add_argument("--chain", action="store_true",
                     help="one cl_conv_forward_chain call per step: each layer's prepass rides on the previous "
                          "layer's contraction (its converter warps), a tail launch finishes it")
@@ -183,11 +184,11 @@ def setup_run(args) -> Run:
     layers = load_layers(args.workload, args.batch)
     scaling = args.scaling
     if scaling == "auto":
-        scaling = "strong" if args.workload.partition("-")[0] == "scale" or args.shard == "channels" else "weak"
+        scaling = "strong" if args.workload.partition("-")[0] == "scale" or args.shard.startswith("channels") else "weak"
     b = layers[0].batch
     if any(l.batch != b for l in layers):
         raise SystemExit("bench.py: a workload's layers share one batch")
-    if args.shard == "channels":
+    if args.shard.startswith("channels"):
         if scaling != "strong":
             raise SystemExit("bench.py: channel sharding is strong scaling (every rank holds the whole batch)")
         i0, i1 = 0, b
@@ -214,7 +215,9 @@ def config_of(args, run: Run) -> dict:
                                if fp32_split() == "mixed" else "fp32-faithful 3xTF32"),
                       "tf32": "tf32 (fast mode)", "bf16": "bf16 operands, fp32 accumulate (fast mode)"}[args.precision],
         "parallelism": (f"dp{run.world} (batch-sharded, no data-path collective)" if args.shard == "batch" else
-                        f"mp{run.world} (output channels sharded, NCCL all-gather of the output slices)"),
+                        f"mp{run.world} (output channels sharded, NCCL all-gather of the output slices)"
+                        if args.shard == "channels" else
+                        f"mp{run.world} (output channels sharded, all-gather fused into the epilogue: P2P stores)"),
         "l2": "flushed (256 MiB write) before every timed step", "weights": "pre-packed once, untimed",
     }
 
@@ -494,8 +497,8 @@ def run_ours(args, run: Run) -> int:
     for li, l in enumerate(rank_layers):
         lc = clb.LayerConfig(l.name, l.channels, l.height, l.width, l.kernel_count, l.kernel_size, l.stride,
                              None if l.pad < 0 else l.pad, l.batch)
-        if args.shard == "channels":
-            plan = dist.MShardPlan(lc, info, args.method, args.precision, dev)
+        if args.shard.startswith("channels"):
+            plan = dist.MShardPlan(lc, info, args.method, args.precision, dev, fused=args.shard == "channels-fused")
         else:
             plan = clb.ConvPlan(lc, args.method, args.precision, dev)
         if args.layout == "nhwc" and plan.method not in ("kn2row-gpu", "conv1x1-gpu", "kn2row-acc-gpu"):
@@ -508,7 +511,7 @@ def run_ours(args, run: Run) -> int:
         rng.fill_uniform(x, rng.split(li, 0), run.image0 * img)
         rng.fill_uniform(w, rng.split(li, 1))
         plan.set_weights(w)
-        base = plan.plan if args.shard == "channels" else plan
+        base = plan.plan if args.shard.startswith("channels") else plan
         ws = torch.empty(max(base.workspace_bytes(), 4), device=dev, dtype=torch.uint8)
         y = torch.empty(plan.output_shape(), device=dev, dtype=torch.float32)
         if args.layout == "nhwc":   # same values, channels-last storage
@@ -521,9 +524,9 @@ def run_ours(args, run: Run) -> int:
     flush_mb = int(os.environ.get("CLB_FLUSH_MB", "256"))   # L2 flush: a write larger than the 126 MB L2
     flush = torch.empty(flush_mb * 1024 * 1024, device=dev, dtype=torch.uint8)
     flops_job = sum(l.flops() for l in run.layers) * (run.world if run.scaling == "weak" else 1)
-    bases = [p.plan if args.shard == "channels" else p for p in plans]   # the ConvPlans this rank runs
+    bases = [p.plan if args.shard.startswith("channels") else p for p in plans]   # the ConvPlans this rank runs
     # FLOPs of this rank's launches (its kernel slice when sharding channels)
-    rank_flops = [l.flops() * ((p.m1 - p.m0) / l.kernel_count if args.shard == "channels" else 1)
+    rank_flops = [l.flops() * ((p.m1 - p.m0) / l.kernel_count if args.shard.startswith("channels") else 1)
                   for l, p in zip(rank_layers, plans)]
 
     # concurrent layers (--concurrent): each layer on its own stream with an SM share proportional
@@ -556,7 +559,7 @@ def run_ours(args, run: Run) -> int:
             if record_kernel is not None:
                 b, e = record_kernel[li]
                 _lib.lib().cl_conv_set_profile_events(bases[li]._h, b.cuda_event, e.cuda_event)
-            if args.shard == "channels":
+            if args.shard.startswith("channels"):
                 ys[li] = plan.forward(xs[li])          # this rank's slice + the NCCL all-gather
             else:
                 plan.forward(xs[li], ys[li], wss[li], layout=args.layout)
@@ -614,7 +617,7 @@ def run_ours(args, run: Run) -> int:
     e2e_streams = [torch.cuda.Stream() for _ in plans]
 
     def e2e_step():
-        if args.shard == "channels":
+        if args.shard.startswith("channels"):
             # H2D of the input, the sharded forward (slice + NCCL all-gather), D2H of the output
             for li, p in enumerate(plans):
                 xs[li].copy_(hx[li], non_blocking=True)

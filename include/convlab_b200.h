@@ -143,10 +143,13 @@ CL_API cl_status cl_conv_forward_chain(cl_plan* const* plans, const float* const
 CL_API cl_status cl_conv_set_peer_outputs(cl_plan* plan, float* const* d_peer_y, int n_peers, int m_offset,
                                           int m_total);
 
-/* CUDA IPC helpers for the fused all-gather (64-byte cudaIpcMemHandle_t as opaque bytes). */
-CL_API cl_status cl_ipc_get_mem_handle(const void* d_ptr, void* handle64);
-CL_API cl_status cl_ipc_open_mem_handle(const void* handle64, void** d_ptr);
-CL_API cl_status cl_ipc_close_mem_handle(void* d_ptr);
+/* CUDA IPC helpers for the fused all-gather (64-byte cudaIpcMemHandle_t as opaque bytes).  The
+ * handle names the whole allocation containing d_ptr; *offset is d_ptr's byte offset in it (a
+ * caching allocator's tensor is a piece of a larger block): the peer opens the handle
+ * (*d_base) and uses d_base + offset, and closes d_base. */
+CL_API cl_status cl_ipc_get_mem_handle(const void* d_ptr, void* handle64, uint64_t* offset);
+CL_API cl_status cl_ipc_open_mem_handle(const void* handle64, void** d_base);
+CL_API cl_status cl_ipc_close_mem_handle(void* d_base);
 
 /* Host-buffer end-to-end call (the run_method surface): H2D of x, forward, D2H of y,
  * synchronous.  Host buffers should be pinned for full PCIe bandwidth. */

@@ -87,7 +87,7 @@ def lib() -> ctypes.CDLL:
     L.cl_conv_set_profile_events.argtypes = [vp, vp, vp]
     L.cl_conv_set_max_sms.argtypes = [vp, i32]
     L.cl_conv_set_peer_outputs.argtypes = [vp, ctypes.POINTER(vp), i32, i32, i32]
-    L.cl_ipc_get_mem_handle.argtypes = [vp, vp]
+    L.cl_ipc_get_mem_handle.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
     L.cl_ipc_open_mem_handle.argtypes = [vp, ctypes.POINTER(vp)]
     L.cl_ipc_close_mem_handle.argtypes = [vp]
     L.cl_conv_forward_chain.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),

@@ -1174,27 +1174,44 @@ cl_status cl_conv_set_peer_outputs(cl_plan* p, float* const* d_peer_y, int n_pee
     });
 }
 
-cl_status cl_ipc_get_mem_handle(const void* d_ptr, void* handle64) {
+cl_status cl_ipc_get_mem_handle(const void* d_ptr, void* handle64, uint64_t* offset) {
     return guarded([&] {
-        require(d_ptr && handle64, "cl_ipc_get_mem_handle: null argument");
+        require(d_ptr && handle64 && offset, "cl_ipc_get_mem_handle: null argument");
         static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
         cudaIpcMemHandle_t h;
         CLB_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
         std::memcpy(handle64, &h, 64);
+        // the handle names the whole allocation (a caching allocator hands out pieces of one):
+        // report where d_ptr sits in it, the opener adds it to the mapped base
+        using PFN_range = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static PFN_range range = [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                fn = nullptr;
+            return reinterpret_cast<PFN_range>(fn);
+        }();
+        if (!range) throw Error(CL_ECUDA, "cuMemGetAddressRange unavailable");
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS)
+            throw Error(CL_ECUDA, "cuMemGetAddressRange failed");
+        *offset = (uint64_t)(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
     });
 }
 
-cl_status cl_ipc_open_mem_handle(const void* handle64, void** d_ptr) {
+cl_status cl_ipc_open_mem_handle(const void* handle64, void** d_base) {
     return guarded([&] {
-        require(handle64 && d_ptr, "cl_ipc_open_mem_handle: null argument");
+        require(handle64 && d_base, "cl_ipc_open_mem_handle: null argument");
         cudaIpcMemHandle_t h;
         std::memcpy(&h, handle64, 64);
-        CLB_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        CLB_CUDA(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess));
     });
 }
 
-cl_status cl_ipc_close_mem_handle(void* d_ptr) {
-    return guarded([&] { CLB_CUDA(cudaIpcCloseMemHandle(d_ptr)); });
+cl_status cl_ipc_close_mem_handle(void* d_base) {
+    return guarded([&] { CLB_CUDA(cudaIpcCloseMemHandle(d_base)); });
 }
 
 cl_status cl_conv_set_max_sms(cl_plan* p, int max_sms) {

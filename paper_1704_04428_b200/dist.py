@@ -173,20 +173,21 @@ class MShardPlan:
         self.y_full = torch.empty((L.batch, L.kernel_count, *self.plan.out_hw), device=f"cuda:{self.device}",
                                   dtype=torch.float32)
         h = (ctypes.c_char * 64)()
-        _lib.check(_lib.lib().cl_ipc_get_mem_handle(ctypes.c_void_p(self.y_full.data_ptr()), h))
-        handles = [bytes(h)]
+        off = ctypes.c_uint64()
+        _lib.check(_lib.lib().cl_ipc_get_mem_handle(ctypes.c_void_p(self.y_full.data_ptr()), h, ctypes.byref(off)))
+        handles = [(bytes(h), off.value)]
         if dist.is_available() and dist.is_initialized():
             handles = [None] * self.info.world
-            dist.all_gather_object(handles, bytes(h))
+            dist.all_gather_object(handles, (bytes(h), off.value))
         ptrs = []
-        for r, hb in enumerate(handles):
+        for r, (hb, offset) in enumerate(handles):
             if r == self.info.rank:
                 ptrs.append(self.y_full.data_ptr())
                 continue
-            p = ctypes.c_void_p()
-            _lib.check(_lib.lib().cl_ipc_open_mem_handle(ctypes.create_string_buffer(hb, 64), ctypes.byref(p)))
-            self._opened.append(p.value)
-            ptrs.append(p.value)
+            base = ctypes.c_void_p()
+            _lib.check(_lib.lib().cl_ipc_open_mem_handle(ctypes.create_string_buffer(hb, 64), ctypes.byref(base)))
+            self._opened.append(base.value)
+            ptrs.append(base.value + offset)   # the peer tensor sits `offset` bytes into its allocation
         arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
         _lib.check(_lib.lib().cl_conv_set_peer_outputs(self.plan._h, arr, len(ptrs), self.m0, L.kernel_count))
 
