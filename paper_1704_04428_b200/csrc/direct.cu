@@ -19,6 +19,7 @@
 // direct_conv_kernel (fallback when the weights do not fit): the same arithmetic with the
 // halo and a 16-channel weight slice staged per CTA.
 #include <cstring>
+#include <mutex>
 
 #include "internal.hpp"
 
@@ -437,9 +438,17 @@ void launch_direct_conv(const float* x, const float* w, float* y, int N, int C, 
         CLB_CUDA(cudaGetLastError());
         return;
     }
-    static bool configured = false;
-    static int sms = 0;
-    if (!configured) {
+    // the >48 KB smem opt-ins are per-device function attributes: configured once per device,
+    // under a lock (a plan may live on any device of the process)
+    static std::mutex mu;
+    static bool configured[64] = {};
+    static int sms_of[64] = {};
+    int cur = 0;
+    CLB_CUDA(cudaGetDevice(&cur));
+    if (cur < 0 || cur >= 64) throw Error(1, "device index out of range");
+    std::lock_guard<std::mutex> guard(mu);
+    const int& sms = sms_of[cur];
+    if (!configured[cur]) {
         set_smem(direct_conv_kernel<0>, 200 * 1024);
         set_smem(direct_conv_kernel<1>, 200 * 1024);
         set_smem(direct_conv_kernel<3>, 200 * 1024);
@@ -449,10 +458,11 @@ void launch_direct_conv(const float* x, const float* w, float* y, int N, int C, 
         set_smem(direct_persistent_kernel<3, 0>, kPersistentSmem);
         set_smem(direct_persistent_kernel<5, 0>, kPersistentSmem);
         set_smem(direct_persistent_kernel<3, 3>, kPersistentSmem);
-        int dev = 0;
-        CLB_CUDA(cudaGetDevice(&dev));
-        CLB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        configured = true;
+        set_smem(direct_param_kernel<16>, kPersistentSmem / 2);
+        set_smem(direct_param_kernel<32>, kPersistentSmem / 2);
+        set_smem(direct_param_kernel<64>, kPersistentSmem / 2);
+        CLB_CUDA(cudaDeviceGetAttribute(&sms_of[cur], cudaDevAttrMultiProcessorCount, cur));
+        configured[cur] = true;
     }
     static const bool param_on = !(getenv("CLB_DIRECT_PARAM") && atoi(getenv("CLB_DIRECT_PARAM")) == 0);
     if (w_param && param_on && direct_param_shape(C, k, M, stride, Q)) {
@@ -461,13 +471,6 @@ void launch_direct_conv(const float* x, const float* w, float* y, int N, int C, 
         const int num_units = N * g.units_img;
         const size_t psmem = 2 * (size_t)C * g.halo_rows * g.pitch * sizeof(float);
         if (psmem <= kPersistentSmem / 2 - 1024) {
-            static bool pconf = false;
-            if (!pconf) {
-                set_smem(direct_param_kernel<16>, kPersistentSmem / 2);
-                set_smem(direct_param_kernel<32>, kPersistentSmem / 2);
-                set_smem(direct_param_kernel<64>, kPersistentSmem / 2);
-                pconf = true;
-            }
             const int grid = std::min(num_units, sms * 2);
             auto go = [&](auto kernel, auto pw) {
                 decltype(pw) wts;
