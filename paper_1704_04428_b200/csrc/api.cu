@@ -912,10 +912,20 @@ cl_status cl_conv_forward_chain(cl_plan* const* plans, const float* const* xs, f
             const double t_host_us = 2.0 * a.n * a.m * a.c * a.k * a.k * (double)plans[i]->P * plans[i]->Q / 4.0e8;
             return t_host_us >= min_us;
         };
-        for (int i = 0; i < count; ++i) {
-            const bool partial = i > 0 && hosts(i - 1);
-            forward(plans[i], xs[i], ys[i], ws[i], s, -1, false, true, true, hosts(i) ? &jobs[i + 1] : nullptr, partial);
-            mark_done(plans[i], s);
+        int i = 0;
+        try {
+            for (; i < count; ++i) {
+                const bool partial = i > 0 && hosts(i - 1);
+                forward(plans[i], xs[i], ys[i], ws[i], s, -1, false, true, true, hosts(i) ? &jobs[i + 1] : nullptr,
+                        partial);
+                mark_done(plans[i], s);
+            }
+        } catch (...) {
+            // a failed layer may leave a hosted job's tile counter part-way (its tail never ran):
+            // reset every counter of this chain so the next call starts clean, then report
+            for (int j = 0; j < count; ++j)
+                if (chainable[j]) cudaMemsetAsync(jobs[j].counter, 0, sizeof(unsigned), s);
+            throw;
         }
     });
 }
