@@ -108,7 +108,6 @@ struct cl_plan {
     int peer_m0 = 0, peer_M = 0;
     unsigned* flags = nullptr; // stream-K fixup flags, zeroed once, self-resetting
     bool padded_rows = false;  // implicit kn2row in tap-shared (zero-padded row) mode
-    bool raw_a = false;        // ... with A converted from the raw NCHW input inside the contraction
     int stack_k = 1;           // > 1: padded-row mode with the k taps of a kernel row stacked on N
     int bn_stack = 0;          // its tile N (k x channels per column tile)
     bool weights_set = false;
@@ -277,11 +276,11 @@ void* resolve_ws(cl_plan* p, void* ws) {
 
 // Chained prepass (cl_conv_forward_chain): the plan's NCHW -> split prepass as a tile job, when
 // its forward runs the standard prepass (implicit / conv1x1 / accumulating kn2row, fp32-faithful
-// split formats, not the raw-input mode).  The job's counter lives in the plan's flag buffer.
+// split formats).  The job's counter lives in the plan's flag buffer.
 bool chain_job(cl_plan* p, const float* x, void* ws, SplitJob* out) {
     const bool implicit = p->method == CL_METHOD_KN2ROW || p->method == CL_METHOD_CONV1X1 ||
                           p->method == CL_METHOD_KN2ROW_ACC;
-    if (!implicit || !is_split(p->planes) || p->raw_a) return false;
+    if (!implicit || !is_split(p->planes)) return false;
     const cl_conv_desc& d = p->d;
     void* xs = ws;
     int pad = 0;
@@ -382,26 +381,15 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                     CLB_CUDA(cudaMemsetAsync(static_cast<char*>(xs) + ((size_t)lead + grid_rows) * rb, 0, (size_t)trail * rb, s));
                 }
                 void* grid = static_cast<char*>(xs) + (size_t)lead * rb;
-                // raw-input A: the contraction reads the NCHW input itself (TMA boxes + converter
-                // warps), so there is no prepass launch and no split tensor round trip through HBM
-                const bool raw = p->raw_a && !nhwc && reinterpret_cast<uintptr_t>(x) % 16 == 0;
                 if (prepass_partial) {
                     launch_split_tail(own_job, p->planes, s);   // the tiles the previous contraction left
                     ++p->launches;
-                } else if (!raw) {
+                } else {
                     if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
                     else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
                     ++p->launches;
                 }
                 Operand a = tiled(xs, grid_rows, 1, p->Cp, p->planes);
-                if (raw) {
-                    a.mode = LOAD_RAW;
-                    a.ptr = x;
-                    a.n = d.n;
-                    a.c = d.c;
-                    a.h = d.h;
-                    a.w = d.w;
-                }
                 Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
                 TcParams t = base_params(p);
                 t.rows = d.n * Hp * Wp;
@@ -425,18 +413,6 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 }
                 t.a_row_shift = Wp;
                 t.a_row_base = lead - d.pad * Wp - d.pad;   // >= 0 in tap-stacked mode
-                if (raw) {
-                    t.raw_c = d.c;
-                    t.raw_h = d.h;
-                    t.raw_w = d.w;
-                    t.raw_n = d.n;
-                    t.raw_hw = d.h * d.w;
-                    t.raw_wp = Wp;
-                    t.raw_hpwp = Hp * Wp;
-                    t.raw_gd = make_fastdiv((uint32_t)(Hp * Wp));
-                    t.raw_wd = make_fastdiv((uint32_t)Wp);
-                    t.raw_x = x;
-                }
                 t.epi = nhwc ? EPI_NHWC_PADDED : EPI_NCHW_PADDED;
                 t.ld = d.m;
                 t.epi_hp = Hp;
@@ -771,19 +747,6 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
                 p->stack_k = d.k;
                 p->bn_stack = mt * d.k;
             }
-            // Raw-input A (tap-shared geometry, fp32-faithful splits, opt-in CLB_RAW_A=1): the
-            // contraction converts the NCHW input itself (TMA boxes of 140 pixels x 16 planes, four
-            // converter warps transposing + splitting into the operand stages), removing the
-            // prepass launch and the split tensor's HBM round trip.  Measured SLOWER on every VGG
-            // layer (conv1_2 0.68 -> 1.32 ms, conv3_2 0.35 -> 0.54 ms whole forward): the
-            // conversion costs ~1700 cycles per k-iteration (four warps, one per SM sub-partition,
-            // issue-latency bound) against 680-1540 cycles of MMA per stage, while the same kernel
-            // with the conversion skipped runs 0.59 / 0.28 ms -- the prepass's cost is the bound
-            // this path would remove if the transpose were free (profiles/r02_raw_input_a.txt).
-            // Its TMA boxes need 16-byte aligned planes (H*W % 4 == 0).
-            static const int env_raw = std::getenv("CLB_RAW_A") ? std::atoi(std::getenv("CLB_RAW_A")) : 0;
-            p->raw_a = env_raw != 0 && p->padded_rows && p->stack_k == 1 && is_split(p->planes) &&
-                       ((long long)d.h * d.w) % 4 == 0 && d.n * (long long)d.c < (1ll << 31);
         }
         // stream-K flags [kMaxGrid], self-resetting (zeroed once here)
         if (cudaMalloc(&p->flags, (kMaxGrid + 8) * sizeof(unsigned)) != cudaSuccess ||

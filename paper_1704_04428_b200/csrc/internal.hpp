@@ -99,8 +99,8 @@ struct Operand {
     long long tap_stride_rows = 0;   // tiled: rows between 3rd-dim slices (0 = rows; < rows = overlapping view)
     int kw = 0;              // elements per row: 2*Cp (split formats) or Cp (TF32, BF16)
     int planes = 2;          // precision mode (see k_granule)
-    // im2col only (n, h, w, k, pad); raw NCHW input (LOAD_RAW): n, c, h, w
-    int n = 0, h = 0, w = 0, k = 1, pad = 0, c = 0;
+    // im2col only
+    int n = 0, h = 0, w = 0, k = 1, pad = 0;
 };
 
 void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int box_taps = 1);

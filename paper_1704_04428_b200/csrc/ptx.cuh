@@ -67,21 +67,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     return ok != 0;
 }
 
-// Non-blocking phase test (mbarrier.test_wait): for polling loops that do other work between
-// tests -- try_wait may suspend the thread for a system-dependent time window when the phase is
-// not complete, which turns a polling loop into a chain of timeouts.
-__device__ __forceinline__ bool mbar_test_wait(uint32_t addr, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P;\n\t}\n"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
 // Protocol debugging (CLB_DEBUG_WAIT=1, launcher): a barrier wait that exceeds the watchdog
 // records (block, warp, barrier smem offset, parity) and GIVES UP instead of trapping, so the
 // kernel finishes with wrong results and the host can print which wait hung.  Per translation
@@ -146,32 +131,6 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, uint64_t* bar,
         " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem)),
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
-}
-
-// 2-D tiled load (CTA-local): coords (c0 innermost, c1)
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* m, uint64_t* bar, void* smem, int32_t c0, int32_t c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem)),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-
-// explicit shared-memory accesses by 32-bit shared-window address (pointers derived through
-// integer alignment arithmetic lose their address space, and generic LD / ST are slower)
-__device__ __forceinline__ float lds_f32(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-
-// this thread's generic-proxy shared-memory writes -> visible to the async proxy (tcgen05.mma
-// operand reads, TMA) once ordered by a subsequent barrier arrive / wait
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // 4-D im2col load over an NHWC tensor: coords (c, w, h, n) of the first traversed pixel
@@ -307,12 +266,6 @@ __device__ __forceinline__ void cluster_sync() {
 // arrive on an mbarrier of another CTA of the cluster (shared::cluster address)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-
-// arrive on the LEADER CTA's mbarrier with cluster-scope release: publishes this CTA's
-// shared-memory operand writes (after fence_proxy_async_smem) to the leader's MMA issue
-__device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 // TMA loads whose completion bytes land on the LEADER CTA's mbarrier (cta_group::2).

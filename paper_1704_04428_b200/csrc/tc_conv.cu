@@ -58,17 +58,7 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int b
                                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const cuuint32_t unit = (cuuint32_t)(kRowBytes / eb);   // elements per 128-byte row unit
     CUresult r;
-    if (op.mode == LOAD_RAW) {
-        // the NCHW fp32 input as [N*C planes][H*W pixels]; one box = kRawPx pixels x 16 planes,
-        // unswizzled; pixels past H*W and planes past N*C are zero-filled
-        cuuint64_t dims[2] = {(cuuint64_t)op.h * op.w, (cuuint64_t)op.n * op.c};
-        cuuint64_t strides[1] = {(cuuint64_t)op.h * op.w * 4};
-        cuuint32_t box[2] = {(cuuint32_t)kRawPx, 16};
-        cuuint32_t estr[2] = {1, 1};
-        r = g_tiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(op.ptr), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    } else if (op.mode == LOAD_IM2COL) {
+    if (op.mode == LOAD_IM2COL) {
         cuuint64_t dims[4] = {kdim, (cuuint64_t)op.w, (cuuint64_t)op.h, (cuuint64_t)op.n};
         cuuint64_t strides[3] = {kdim * eb, kdim * eb * op.w, kdim * eb * op.w * op.h};
         // Bounding box: lower corner -pad, upper corner pad-(k-1) in W and H, so the
@@ -160,16 +150,7 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     if (cg != 1 && cg != 2) throw Error(6, "cta group must be 1 or 2");
     if (p.bn % 16 != 0 || p.bn < 16 || p.bn > 256) throw Error(6, "tile N must be a multiple of 16 in [16,256]");
     const int unit = kRowBytes / elem_bytes(a.planes);
-    if (a.mode == LOAD_RAW) {
-        // raw-input A: the converter warps produce the split operand units of b's layout
-        if (!is_split(b.planes) || p.tps <= 1 || p.stack_k > 1 || !p.a_row_shift)
-            throw Error(6, "raw-input A needs the fp32-faithful split in the tap-shared geometry");
-        if ((long long)a.h * a.w * 4 % 16 != 0 || reinterpret_cast<uintptr_t>(a.ptr) % 16 != 0)
-            throw Error(6, "raw-input A needs 16-byte aligned input planes");
-        p.raw = 1;
-    } else if (a.kw != b.kw || a.kw % unit != 0 || a.planes != b.planes) {
-        throw Error(6, "operand K layout mismatch");
-    }
+    if (a.kw != b.kw || a.kw % unit != 0 || a.planes != b.planes) throw Error(6, "operand K layout mismatch");
     if (p.tps <= 0) p.tps = 1;
     if (p.stack_k <= 1) {
         p.stack_k = 1;
@@ -186,9 +167,9 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
         throw Error(6, "tap-stacked A must be the 4-quadrant overlapping view");
     encode_operand_map(&ma, a, p.stack_k > 1 ? 32 : tc_a_box_rows(p.tps), p.stack_k > 1 ? 4 : 1);
     encode_operand_map(&mb, b, p.bn / cg, p.tps);
-    p.planes = b.planes;
+    p.planes = a.planes;
     p.row_elems = unit;
-    p.kblocks = b.kw / unit;
+    p.kblocks = a.kw / unit;
     p.a_mode = a.mode;
     p.b_mode = b.mode;
     if (p.taps % p.tps != 0) throw Error(6, "taps per stage must divide the tap count");
@@ -218,20 +199,14 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     // A and B loads from two producer warps: 3-8 % on the TMA-im2col layers (AlexNet conv2 / conv5,
     // VGG conv5_x), neutral on the padded-row ones (profiles/r01_split_issue_sweep.txt)
     static const int env_split_issue = getenv("CLB_SPLIT_ISSUE") ? atoi(getenv("CLB_SPLIT_ISSUE")) : 1;
-    p.split_issue = p.raw ? 1 : env_split_issue;   // raw: warp 3 loads B, warp 0 stages the raw A boxes
+    p.split_issue = env_split_issue;
     // A boxes of alternate stages issued from two warps (0 and the idle TMEM-allocator warp 2):
     // +0.5-2 % on the padded-row layers (VGG conv1_2 0.508 -> 0.499 ms), neutral on the TMA-im2col
     // ones (profiles/r01_a_issuers_ab.txt).  CLB_A_ISSUERS=1 restores one A warp.
     static const int env_a_iss = getenv("CLB_A_ISSUERS") ? atoi(getenv("CLB_A_ISSUERS")) : 2;
     p.a_issuers = (env_a_iss == 2 && p.split_issue) ? 2 : 1;
     static const int env_smem = getenv("CLB_SMEM_KB") ? atoi(getenv("CLB_SMEM_KB")) * 1024 : 0;   // experiment knob
-    // raw-input A: the staging ring (raw_slots boxes) comes out of the stage budget
-    static const int env_raw_slots = getenv("CLB_RAW_SLOTS") ? atoi(getenv("CLB_RAW_SLOTS")) : 4;
-    p.raw_slots = p.raw ? (env_raw_slots >= 8 ? 8 : env_raw_slots >= 4 ? 4 : env_raw_slots >= 2 ? 2 : 1) : 0;   // power of two
-    static const int env_raw_dbg = getenv("CLB_RAW_DBG") ? atoi(getenv("CLB_RAW_DBG")) : 0;
-    p.raw_dbg = env_raw_dbg;
-    const int raw_bytes = p.raw_slots * kRawSlotBytes;
-    const int budget = (env_smem > 0 ? env_smem : kSmemBudget) - raw_bytes;
+    const int budget = env_smem > 0 ? env_smem : kSmemBudget;
     const int stage_b_rows = b_rows;   // B rows carried per stage
     if (p.bps <= 0) {
         static const int env_bps = getenv("CLB_BPS") ? atoi(getenv("CLB_BPS")) : 0;   // experiment knob
@@ -253,7 +228,7 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     if (p.num_tiles <= 0) return 0;
     p.chunks_per_tile = (k_iters + p.chunk_iters - 1) / p.chunk_iters;
     const long long total_chunks = (long long)p.num_tiles * p.chunks_per_tile;
-    const int smem = tc_smem_bytes(stage_b_rows, p.tps, p.stages, p.bps, raw_bytes);
+    const int smem = tc_smem_bytes(stage_b_rows, p.tps, p.stages, p.bps);
     // The stream-K fixup makes CTAs wait on each other, so every CTA of the grid must be
     // co-resident: the unit count is capped at what the occupancy calculator says fits at once
     // for this kernel, smem size and cluster shape (on the current device; attributes and
@@ -416,10 +391,10 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
         unsigned long long rec[8];
         CLB_CUDA(cudaMemcpyFromSymbolAsync(rec, clb_dbg_record, sizeof(rec), 0, cudaMemcpyDeviceToHost, s));
         CLB_CUDA(cudaStreamSynchronize(s));
-        fprintf(stderr, "[clb-dbg] rows=%d cols=%d bn=%d cg=%d raw=%d stages=%d bps=%d grid=%d bars at +0x%x "
-                "(full[s], empty[s], tfull[4], tempty[4], fix, raw_full[2 x slots]): %u timed-out waits\n", p.rows,
-                p.cols, p.bn, cg, p.raw, p.stages, p.bps, grid,
-                p.stages * p.bps * tc_stage_bytes(stage_b_rows, p.tps) + raw_bytes, (unsigned)(rec[7] & 0xffffffffu));
+        fprintf(stderr, "[clb-dbg] rows=%d cols=%d bn=%d cg=%d stages=%d bps=%d grid=%d bars at +0x%x "
+                "(full[s], empty[s], tfull[4], tempty[4], fix): %u timed-out waits\n", p.rows, p.cols, p.bn, cg,
+                p.stages, p.bps, grid, p.stages * p.bps * tc_stage_bytes(stage_b_rows, p.tps),
+                (unsigned)(rec[7] & 0xffffffffu));
         for (int i = 0; i < 6 && i < (int)(rec[7] & 0xffffffffu); ++i)
             fprintf(stderr, "[clb-dbg]   block %llu warp %llu bar smem+0x%llx parity %llu\n", rec[i] >> 40,
                     (rec[i] >> 32) & 0xff, (rec[i] & 0xffffffffu) >> 1, rec[i] & 1);
@@ -476,10 +451,8 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
         const unsigned long long* r = &h[(size_t)slow * kTraceSlots];
         int lead = cg == 2 ? (slow & ~1) : slow;   // the MMA runs on the pair's leader
         const unsigned long long* rl = &h[(size_t)lead * kTraceSlots];
-        if (p.raw)
-            fprintf(stderr, "[clb-trace]   converters: total %.0f cyc | wait raw box %.0f%% | wait stage %.0f%% | convert %.0f%% "
-                            "(%.0f cyc per k-iteration)\n", avg[20], 100 * avg[21] / avg[20], 100 * avg[22] / avg[20],
-                    100 * avg[23] / avg[20], avg[23] / std::max(1.0, (double)(p.num_tiles * p.chunks_per_tile * p.chunk_iters) / grid));
+        if (p.nx_on)
+            fprintf(stderr, "[clb-trace]   chained prepass: %.0f tiles per CTA converted by the converter warps\n", avg[23]);
         fprintf(stderr,
                 "[clb-trace]   slowest CTA %d: exit +%.1f us | producer %llu (wait empty %llu) | mma %llu (wait full "
                 "%llu, wait tmem %llu) | epilogue %llu (wait tfull %llu, store %llu, fixup wait %llu) cyc\n",

@@ -41,7 +41,7 @@
 
 namespace clb {
 
-enum : int { LOAD_TILED = 0, LOAD_IM2COL = 1, LOAD_RAW = 2 };
+enum : int { LOAD_TILED = 0, LOAD_IM2COL = 1 };
 enum : int { EPI_NCHW = 0, EPI_ROWMAJOR = 1, EPI_NCHW_PADDED = 2, EPI_NHWC_PADDED = 3 };
 
 constexpr int kTileM = 128;          // UMMA M (D rows per tile)
@@ -54,19 +54,15 @@ constexpr int kRowWords = 32;
 constexpr int kRowBytes = kRowWords * 4;
 constexpr int kThreads = 512;             // 4 control warps + 8 epilogue warps + 4 converter warps
 constexpr int kEpiThreads = 256;
-constexpr int kConvWarps = 4;             // raw-input A converters (warps 12..15, one warpgroup)
+constexpr int kConvWarps = 4;             // converter warpgroup (warps 12..15): the chained prepass
 // registers per thread after setmaxnreg: 4 x 32 x 56 + 8 x 32 x 200 + 4 x 32 x 56 = 65536
 constexpr int kRegsControl = 56, kRegsEpi = 200, kRegsConv = 56;
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kChunkK = 192;          // fp32-faithful splits: K-elements per TMEM accumulation chunk
-// raw-input A (LOAD_RAW): one TMA box of kRawPx consecutive pixels x 16 channel planes of the
-// NCHW fp32 input per k-iteration, staged unswizzled as [plane][pixel]
-constexpr int kRawPx = 140;   // >= 3 (alignment) + 134 rows (k = 7)
-constexpr int kRawSlotBytes = 16 * kRawPx * 4;
 constexpr int kBarrierBytes = 512;
 constexpr int kMaxPeers = 8;     // ranks of a fused output all-gather (one node)
-// TMEM loads (16 columns each) in flight per chunk fold.  2 (not 4) leaves the epilogue warps
-// the registers the raw-input conversion service needs next to their 128 running sums.
+// TMEM loads (16 columns each) in flight per chunk fold (2 keeps the epilogue inside its
+// 200-register budget next to its 128 running sums).
 constexpr int kFoldLoads = 2;
 constexpr int kFastChunkIters = 16;   // TF32 / BF16 fast modes: k-iterations per chunk
 
@@ -124,17 +120,6 @@ struct TcParams {
     int sk_chunks;             // chunks of tiles [dp_tiles, num_tiles), split contiguously (stream-K)
     int sk_units;              // scheduling units sharing the stream-K chunks (<= grid units; the
                                // rest only run data-parallel tiles): chosen so no tile splits 3 ways
-    // raw-input A (raw = 1, tap-shared padded-row geometry): the NCHW fp32 input is read by TMA
-    // boxes (kRawPx pixels x 16 planes) into a staging ring (warp 0 issues them), and the eight
-    // epilogue warps split each staged box into the operand rows (hi / lo formats, SWIZZLE_128B)
-    // while they would otherwise wait -- no prepass kernel, no split tensor in HBM
-    int raw;
-    int raw_slots;             // staging ring slots
-    int raw_dbg;               // debugging bisection (CLB_RAW_DBG): 1 no TMA, 2 no conversion, 4 no proxy fence
-    int raw_c, raw_h, raw_w, raw_n, raw_hw;   // input geometry (C, H, W, N, H*W)
-    int raw_wp, raw_hpwp;      // padded grid row width Wp and image size Hp*Wp
-    FastDiv raw_gd, raw_wd;    // divide by Hp*Wp, by Wp
-    const float* raw_x;        // the NCHW input (rare rows of a second image are read directly)
     // chained prepass (nx_on): while this contraction runs, its converter warps (12-15) convert
     // tiles of the NEXT layer's input (nx) -- memory-bound work on SMs whose tensor pipe is busy
     // and whose DRAM traffic is 6-30 % of peak -- until this CTA's epilogue is done
@@ -172,8 +157,8 @@ __host__ inline int tc_num_stages(int b_rows, int tps, int bps = 1, int budget =
     return s > 8 ? 8 : s;
 }
 
-__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages, int bps = 1, int raw_bytes = 0) {
-    return 1024 /*align slack*/ + stages * bps * tc_stage_bytes(b_rows, tps) + raw_bytes + kBarrierBytes;
+__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages, int bps = 1) {
+    return 1024 /*align slack*/ + stages * bps * tc_stage_bytes(b_rows, tps) + kBarrierBytes;
 }
 
 // TMEM accumulator buffers: 4 when they fit (BN <= 128), else ping-pong.  Extra buffers let
@@ -269,134 +254,6 @@ struct Sched {
     }
 };
 
-// The k-iteration sequence of one CTA in the padded-row (tap-shared) geometry, with the
-// producer's stage bookkeeping: stage / phase / sub-stage and the stage sequence number gs
-// advance exactly as in the TMA producer loop (a stage holds bps k-iterations, or fewer at
-// the end of a piece).  tps = k here, so a tap group is one kernel row i.
-struct KWalk {
-    Sched sch;
-    Piece pc;
-    int it = 0, it1 = 0, kb = 0, ti = 0, row0 = 0;
-    int sub = 0, stage = 0;
-    uint32_t gs = 0, phase = 0;
-    bool have = false;
-    __device__ KWalk(const TcParams& p, int unit, int nunits) : sch(p, unit, nunits) {}
-    __device__ void start(const TcParams& p, int tile_rows, int rank_rows, int k_iters) {
-        have = false;
-        while (sch.next(pc)) {
-            const int mt = pc.tile / p.n_col_tiles;
-            row0 = mt * tile_rows + rank_rows;
-            it = pc.c_lo * p.chunk_iters;
-            it1 = pc.c_hi * p.chunk_iters < k_iters ? pc.c_hi * p.chunk_iters : k_iters;
-            if (it >= it1) continue;
-            ti = it / p.kblocks;
-            kb = it - ti * p.kblocks;
-            have = true;
-            return;
-        }
-    }
-    __device__ bool last_sub(int bps) const { return sub + 1 == bps || it + 1 == it1; }
-    __device__ void advance(const TcParams& p, int tile_rows, int rank_rows, int k_iters, int stages, int bps) {
-        if (last_sub(bps)) {
-            sub = 0;
-            ++gs;
-            if (++stage == stages) {
-                stage = 0;
-                phase ^= 1u;
-            }
-        } else {
-            ++sub;
-        }
-        if (++kb == p.kblocks) {
-            kb = 0;
-            ++ti;
-        }
-        if (++it == it1) start(p, tile_rows, rank_rows, k_iters);
-    }
-};
-
-// First input pixel of a k-iteration's A rows [g0, g0 + rows) in the padded grid: image n0 and
-// pixel y * W + x of the first in-image row, rounded down to a multiple of 4 (p0; every later
-// in-image row of image n0 is the next pixel, since the grid only inserts pad positions).
-// n0 >= N: no input pixel at all.
-__device__ __forceinline__ void raw_first_pixel(const TcParams& p, int g0, int rows, int& n0, int& p0) {
-    const int g = g0 < 0 ? 0 : g0;
-    int n = (int)fdiv((uint32_t)g, p.raw_gd);
-    const int rem = g - n * p.raw_hpwp;
-    int y = (int)fdiv((uint32_t)rem, p.raw_wd);
-    int x = rem - y * p.raw_wp;
-    if (x >= p.raw_w) {
-        x = 0;
-        ++y;
-    }
-    if (y >= p.raw_h) {
-        x = 0;
-        y = 0;
-        ++n;
-    }
-    if (n * p.raw_hpwp + y * p.raw_wp + x > g0 + rows - 1) n = p.raw_n;   // the rows hold padding only
-    n0 = n;
-    // a tiled TMA box must start 16-byte aligned in its innermost dimension (an unaligned start
-    // faults as an illegal instruction, tools/tma2d_probe.cu): round down to 4 pixels -- the
-    // rows (at most 128 + k - 1 <= 134 pixels) then sit at box offsets <= 3 + 133 < kRawPx
-    p0 = (y * p.raw_w + x) & ~3;
-}
-
-// Converts A row j of one k-iteration (one converter thread per row): channels [c0, c0 + 16) of
-// the padded-grid row g0 + j, from the staged box (image n0, pixels [p0, p0 + kRawPx), 16 planes)
-// into the 128-byte operand unit [hi 16 fp32 | bf16(hi) 16 | bf16(lo) 16] (PL = 4) or
-// [hi 16 | lo 16] (PL = 2), SWIZZLE_128B (16-byte chunk q of row j at q ^ (j & 7)): the bytes the
-// prepass + TMA path would have delivered.  `sidx` is the row's staged pixel offset (>= 0), -1 for
-// padding, or -2 for a row of a later image (a tile straddling an image boundary), which is read
-// from global memory at plane offset `goff` (pixel + n * C * H * W).
-template <int PL>
-__device__ __forceinline__ void raw_convert_row(const TcParams& p, uint32_t stg, uint32_t dst, int j, int sidx,
-                                                long long goff, int c0) {
-    const int nv = p.raw_c - c0;   // real channels of this block (>= 16 but for the last block)
-    const uint32_t row = dst + (uint32_t)j * kRowBytes;
-    const uint32_t sw = (uint32_t)(j & 7);
-    float v[16];
-    if (sidx >= 0 && nv >= 16) {          // the common case: a staged row, a full channel block
-        const uint32_t src = stg + (uint32_t)sidx * 4u;
-#pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = lds_f32(src + (uint32_t)(c * kRawPx * 4));   // 16 loads in flight
-    } else {
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-            v[c] = 0.0f;
-            if (c < nv) {
-                if (sidx >= 0) v[c] = lds_f32(stg + (uint32_t)((c * kRawPx + sidx) * 4));
-                else if (sidx == -2) v[c] = __ldg(p.raw_x + goff + (long long)(c0 + c) * p.raw_hw);
-            }
-        }
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        uint32_t hb[8];
-        float hi[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            hb[c] = tf32_rna_bits(v[8 * h + c]);
-            hi[c] = __uint_as_float(hb[c]);
-        }
-        const float* x = v + 8 * h;
-        sts_v4(row + (((2u * h) ^ sw) << 4), hb[0], hb[1], hb[2], hb[3]);
-        sts_v4(row + (((2u * h + 1u) ^ sw) << 4), hb[4], hb[5], hb[6], hb[7]);
-        if constexpr (PL == 4) {
-            sts_v4(row + (((4u + h) ^ sw) << 4), bf16x2_bits(hi[0], hi[1]), bf16x2_bits(hi[2], hi[3]),
-                   bf16x2_bits(hi[4], hi[5]), bf16x2_bits(hi[6], hi[7]));
-            sts_v4(row + (((6u + h) ^ sw) << 4), bf16x2_bits(x[0] - hi[0], x[1] - hi[1]),
-                   bf16x2_bits(x[2] - hi[2], x[3] - hi[3]), bf16x2_bits(x[4] - hi[4], x[5] - hi[5]),
-                   bf16x2_bits(x[6] - hi[6], x[7] - hi[7]));
-        } else {
-            sts_v4(row + (((4u + 2u * h) ^ sw) << 4), __float_as_uint(x[0] - hi[0]), __float_as_uint(x[1] - hi[1]),
-                   __float_as_uint(x[2] - hi[2]), __float_as_uint(x[3] - hi[3]));
-            sts_v4(row + (((5u + 2u * h) ^ sw) << 4), __float_as_uint(x[4] - hi[4]), __float_as_uint(x[5] - hi[5]),
-                   __float_as_uint(x[6] - hi[6]), __float_as_uint(x[7] - hi[7]));
-        }
-    }
-}
-
 // One 128-pixel x 32-channel tile of a SplitJob by one warp, in registers (no shared memory:
 // the contraction owns it): lane = pixel row (4 passes), 16 channels per unit loaded coalesced
 // across the warp (consecutive pixels of one plane), the 128-byte split unit of each row written
@@ -454,28 +311,6 @@ __device__ __forceinline__ void split_tile_warp(const SplitJob& j, int bx, int b
                                             __float_as_uint(v[4 * q + 3] - __uint_as_float(hb[4 * q + 3])));
             }
         }
-    }
-}
-
-// Row j's source in the staged box of a k-iteration whose rows start at padded-grid row g0 and
-// whose box starts at (image n0, pixel p0): see raw_convert_row.
-__device__ __forceinline__ void raw_row_source(const TcParams& p, int g0, int j, int n0, int p0, int& sidx,
-                                               long long& goff) {
-    const int g = g0 + j;
-    sidx = -1;
-    goff = 0;
-    if (g < 0) return;
-    const int n = (int)fdiv((uint32_t)g, p.raw_gd);
-    const int rem = g - n * p.raw_hpwp;
-    const int y = (int)fdiv((uint32_t)rem, p.raw_wd);
-    const int x = rem - y * p.raw_wp;
-    if (n >= p.raw_n || y >= p.raw_h || x >= p.raw_w) return;
-    const int pix = y * p.raw_w + x;
-    if (n == n0) {
-        sidx = pix - p0;
-    } else {
-        sidx = -2;
-        goff = (long long)n * p.raw_c * p.raw_hw + pix;
     }
 }
 
@@ -570,18 +405,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;       // scheduling unit
     const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-    const int raw_slots = p.raw ? p.raw_slots : 0;
-    uint8_t* const raw_smem = smem + stages * group_bytes;   // [slot][16][kRawPx] fp32
-    uint64_t* bars = reinterpret_cast<uint64_t*>(raw_smem + raw_slots * kRawSlotBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * group_bytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + stages;
     uint64_t* tfull = bars + 2 * stages;        // [nbuf]
     uint64_t* tempty = bars + 2 * stages + 4;   // [nbuf]
     uint64_t* fix_bar = bars + 2 * stages + 8;     // stream-K partial staged in smem (finisher)
-    uint64_t* raw_full = bars + 2 * stages + 9;                  // [raw_slots] box staged (TMA bytes)
-    uint64_t* raw_empty = raw_full + raw_slots;                  // [raw_slots] converted by all 8 epilogue warps
-    int4* raw_meta = reinterpret_cast<int4*>(bars + 2 * stages + 10 + 2 * raw_slots);   // [raw_slots], 16-B aligned
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 9 + 2 * raw_slots);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 9);
     volatile int* epi_done = reinterpret_cast<volatile int*>(tmem_slot + 1);   // chained prepass: stop
 
     const int warp = threadIdx.x >> 5;
@@ -591,16 +421,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t buf_cols = ncols / (uint32_t)nbuf;
 
     if (threadIdx.x == 0) {
-        // full: the B TMA warp's expect_tx arrival + the A side (one TMA warp's arrival, or the
-        // converter warp of the stage in each CTA of the group when A is converted from raw input)
-        const uint32_t full_count = p.raw ? 1u + (uint32_t)(CG * kConvWarps) : (p.split_issue ? 2u : 1u);
         for (int s = 0; s < stages; ++s) {
-            mbar_init(&full[s], full_count);
+            mbar_init(&full[s], p.split_issue ? 2 : 1);   // the A and B TMA warps' expect_tx arrivals
             mbar_init(&empty[s], 1);
-        }
-        for (int s = 0; s < raw_slots; ++s) {
-            mbar_init(&raw_full[s], 1);
-            mbar_init(&raw_empty[s], kConvWarps);
         }
         for (int a = 0; a < nbuf; ++a) {
             mbar_init(&tfull[a], 1);
@@ -641,53 +464,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // sits under its own setmaxnreg so ptxas allocates it with that budget).
     if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
-    if (p.raw && (warp == 0 || warp == 2)) {
-        // ------------------------------------------------ raw A issuer (raw-input mode) ----
-        // Warp 0 walks the CTA's k-iterations and, per k-iteration, stages one raw box (kRawPx
-        // pixels x 16 planes of the NCHW input) into the next ring slot once the epilogue warps
-        // have converted that slot's previous box, with the k-iteration's geometry and stage
-        // bookkeeping in the slot's meta record.  It runs up to raw_slots k-iterations ahead of the
-        // conversions, independently of the operand stages.  (Warp 2 has no role here.)
-        if (warp == 0) {
-            const int rows = tc_a_box_rows(tps);
-            const int rank_rows = (int)rank * p.row_step;
-            KWalk iss(p, unit, nunits);
-            iss.start(p, tile_rows, rank_rows, k_iters);
-            uint32_t issued = 0;
-            while (iss.have) {
-                const int slot = (int)(issued & (uint32_t)(raw_slots - 1));   // raw_slots: a power of two
-                const uint32_t lap = issued >> (raw_slots >= 8 ? 3 : raw_slots >= 4 ? 2 : raw_slots >= 2 ? 1 : 0);
-                if (lap > 0) mbar_wait(&raw_empty[slot], (lap - 1u) & 1u);
-                const int g0 = iss.row0 + p.a_row_base + iss.ti * p.a_row_shift;
-                int n0, p0;
-                raw_first_pixel(p, g0, rows, n0, p0);
-                if (elect_one()) {
-                    raw_meta[slot] = make_int4(g0, n0, p0,
-                                               iss.kb | (iss.stage << 16) | (iss.sub << 24) |
-                                                   ((int)iss.last_sub(bps) << 30) | ((int)iss.phase << 31));
-                    if (n0 < p.raw_n && !(p.raw_dbg & 1)) {
-                        mbar_arrive_expect_tx(&raw_full[slot], (uint32_t)kRawSlotBytes);
-                        tma_load_2d(&map_a, &raw_full[slot], raw_smem + slot * kRawSlotBytes, p0,
-                                    n0 * p.raw_c + iss.kb * 16);
-                    } else {
-                        mbar_arrive(&raw_full[slot]);   // padding-only rows: nothing to stage
-                    }
-                }
-                __syncwarp();
-                ++issued;
-                iss.advance(p, tile_rows, rank_rows, k_iters, stages, bps);
-            }
-            // end-of-sequence record for the converters
-            const int slot = (int)(issued & (uint32_t)(raw_slots - 1));
-            const uint32_t lap = issued >> (raw_slots >= 8 ? 3 : raw_slots >= 4 ? 2 : raw_slots >= 2 ? 1 : 0);
-            if (lap > 0) mbar_wait(&raw_empty[slot], (lap - 1u) & 1u);
-            if (elect_one()) {
-                raw_meta[slot] = make_int4(INT_MIN, 0, 0, 0);
-                mbar_arrive(&raw_full[slot]);
-            }
-            __syncwarp();
-        }
-    } else if (warp == 0 || (warp == 3 && p.split_issue) || (warp == 2 && p.a_issuers == 2)) {
+    if (warp == 0 || (warp == 3 && p.split_issue) || (warp == 2 && p.a_issuers == 2)) {
         // ------------------------------------------------------------ TMA producer ----
         // whole warp runs the (uniform) loop; one elected lane issues the TMA.  With split_issue
         // warp 0 loads A and warp 3 loads B (TMA im2col boxes are slow to deliver from a single
@@ -952,84 +729,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     }
     } else if (warp >= 12) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsConv));
-        // ---------------------------------------- A converters (raw-input mode, warps 12-15) ----
-        // Per staged box, in k-iteration order: wait for it to land and (first sub-stage) for its
-        // operand stage to be free, convert -- thread t owns A rows t and t + 128 (< 128 + k - 1),
-        // 16 channels each -- fence the generic writes to the async proxy, release the ring slot and,
-        // after a stage's last k-iteration, arrive on the full barrier of the group's leader CTA
-        // (with the B bytes, the MMA warp's condition).  Row sources are cached while consecutive
-        // boxes cover the same A rows (the channel blocks of one tile row).
-        if (p.raw) {
-            const int t = (int)threadIdx.x - 12 * 32;   // 0..127
-            const int lane = (int)lane_id();
-            const int rows = tc_a_box_rows(tps);
-            const uint32_t rmask = (uint32_t)raw_slots - 1u;
-            const uint32_t rshift = raw_slots >= 8 ? 3u : raw_slots >= 4 ? 2u : raw_slots >= 2 ? 1u : 0u;
-            int last_g0 = INT_MIN, last_n0 = -1, last_p0 = -1;
-            int sidx0 = -1, sidx1 = -1;
-            long long goff0 = 0, goff1 = 0;
-            uint32_t tk = 0;
-            long long c_raw = 0, c_empty = 0, c_conv = 0;
-            const long long c_start = TRACE ? clock64() : 0;
-            while (true) {   // until the issuer's end-of-sequence record (g0 = INT_MIN)
-                const int slot = (int)(tk & rmask);
-                long long c0t = TRACE ? clock64() : 0;
-                mbar_wait(&raw_full[slot], (tk >> rshift) & 1u);
-                const int4 m = raw_meta[slot];
-                if (m.x == INT_MIN) break;
-                const int stage = (m.w >> 16) & 0xff, sub = (m.w >> 24) & 0x3f;
-                if (TRACE) {
-                    const long long c1t = clock64();
-                    c_raw += c1t - c0t;
-                    c0t = c1t;
-                }
-                if (sub == 0) mbar_wait(&empty[stage], (((uint32_t)m.w >> 31) & 1u) ^ 1u);
-                if (TRACE) {
-                    const long long c1t = clock64();
-                    c_empty += c1t - c0t;
-                    c0t = c1t;
-                }
-                if (m.x != last_g0 || m.y != last_n0 || m.z != last_p0) {
-                    last_g0 = m.x;
-                    last_n0 = m.y;
-                    last_p0 = m.z;
-                    raw_row_source(p, m.x, t, m.y, m.z, sidx0, goff0);
-                    if (t + 128 < rows) raw_row_source(p, m.x, t + 128, m.y, m.z, sidx1, goff1);
-                }
-                const uint32_t dst = smem_u32(smem + stage * group_bytes + sub * stage_bytes);
-                const uint32_t stg = smem_u32(raw_smem + slot * kRawSlotBytes);
-                const int c0 = (m.w & 0xffff) * 16;
-                if (!(p.raw_dbg & 2)) {
-                    if (planes == 4) {
-                        raw_convert_row<4>(p, stg, dst, t, sidx0, goff0, c0);
-                        if (t + 128 < rows) raw_convert_row<4>(p, stg, dst, t + 128, sidx1, goff1, c0);
-                    } else {
-                        raw_convert_row<2>(p, stg, dst, t, sidx0, goff0, c0);
-                        if (t + 128 < rows) raw_convert_row<2>(p, stg, dst, t + 128, sidx1, goff1, c0);
-                    }
-                }
-                fence_proxy_async_smem();   // operand writes -> MMA (async proxy); staging reads -> next TMA
-                __syncwarp();
-                if (TRACE) c_conv += clock64() - c0t;
-                if (lane == 0) {
-                    mbar_arrive(&raw_empty[slot]);
-                    if ((m.w >> 30) & 1) {
-                        // CTA-scope release on the leader's barrier: a cluster-scope release makes
-                        // ptxas emit MEMBAR.ALL.GPU; the operand bytes are this warp's own shared-
-                        // memory writes, made visible to the tensor core by the proxy fence above
-                        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&full[stage]), 0));
-                        else mbar_arrive(&full[stage]);
-                    }
-                }
-                ++tk;
-            }
-            if (TRACE && t == 0) {
-                p.trace[blockIdx.x * kTraceSlots + 20] = (unsigned long long)(clock64() - c_start);
-                p.trace[blockIdx.x * kTraceSlots + 21] = (unsigned long long)c_raw;
-                p.trace[blockIdx.x * kTraceSlots + 22] = (unsigned long long)c_empty;
-                p.trace[blockIdx.x * kTraceSlots + 23] = (unsigned long long)c_conv;
-            }
-        } else if (p.nx_on) {
+        // -------------------------------------- converter warpgroup (warps 12-15) ----
+        if (p.nx_on) {
             // chained prepass: tiles of the next layer's input, taken from the job's counter until
             // the job is done or this CTA's epilogue has finished (a tail launch does the rest)
             const int lane = (int)lane_id();

@@ -380,7 +380,7 @@ print(json.dumps(out))
 '''
 
 
-@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs", "raw", "raw_slots1"])
+@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs"])
 def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     """The implicit kernel's tap-shared mode (zero-padded NHWC rows, one A box of 128+k-1 rows
     per kernel row, taps through row-shifted UMMA descriptors), forced on and off via
@@ -405,9 +405,7 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
            "stacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1"),
            "unstacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="0"),
            "knobs": dict(CLB_PADDED_ROWS="1", CLB_SPLIT_ISSUE="0", CLB_FIXUP_SMEM="0", CLB_SK_UNITS="0",
-                         CLB_TRACE="1"),
-           "raw": dict(CLB_PADDED_ROWS="1", CLB_RAW_A="1"),
-           "raw_slots1": dict(CLB_PADDED_ROWS="1", CLB_RAW_A="1", CLB_RAW_SLOTS="1")}[mode]
+                         CLB_TRACE="1")}[mode]
     r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, **env))
     assert r.returncode == 0, r.stderr[-3000:]
@@ -845,75 +843,6 @@ def test_concurrent_layers_graph_matches_oracle(oracle, clb, torch_cuda):
     for p in plans:
         p.close()
 
-
-RAW_CASES = [
-    (2, 64, 56, 56, 64, 3, 1),      # VGG-like, CTA pairs
-    (3, 20, 24, 24, 40, 3, 1),      # C % 16 != 0: the last block's planes past C belong to the next image
-    (40, 16, 4, 4, 32, 3, 1),       # 25-row padded images: most tile rows come from later images (direct loads)
-    (6, 48, 12, 16, 100, 5, 2),     # k = 5, M not a multiple of 16
-    (2, 32, 20, 20, 24, 7, 3),      # k = 7: 134 A rows per box
-    (2, 24, 16, 16, 40, 3, 0),      # pad 0 (P < H)
-    (2, 16, 16, 12, 32, 3, 2),      # pad > k/2
-    (8, 128, 28, 28, 256, 3, 1),    # BN = 256 pairs, multi-chunk K, stream-K
-    (1, 512, 28, 28, 512, 3, 1),    # two column tiles, long K
-]
-
-
-_RAW_SCRIPT = r'''
-import json, sys
-sys.path.insert(0, sys.argv[1])
-import numpy as np, torch
-from oracle import oracle as O
-import paper_1704_04428_b200 as clb
-from tests.test_gpu_parity import RAW_CASES
-out = []
-for case in RAW_CASES:
-    N, C, H, W, M, k, pad = case
-    x, w = O.make_problem(N, C, H, W, M, k, sum(case))
-    layer = clb.LayerConfig("raw", C, H, W, M, k, 1, pad, N)
-    res = {"case": case}
-    for prec in ("fp32",):
-        with clb.ConvPlan(layer, "kn2row-gpu", prec) as plan:
-            plan.set_weights(torch.from_numpy(w).cuda())
-            y = plan.forward(torch.from_numpy(x).cuda())
-            torch.cuda.synchronize()
-            res["launches"] = plan.launch_count()
-        m = O.parity_metrics(y.cpu().numpy(), O.conv_loopnest(x, w, pad, 1))
-        res.update(rel_l2=m["rel_l2"], max_rel=m["max_rel"])
-        np.save(f"{sys.argv[2]}/raw_{len(out)}.npy", y.cpu().numpy())
-    out.append(res)
-print(json.dumps(out))
-'''
-
-
-def test_raw_input_contraction(oracle, tmp_path):
-    """The opt-in raw-input A mode (CLB_RAW_A=1, in a subprocess): the implicit kernel converts its
-    own NCHW input (TMA boxes of 140 pixels x 16 planes, converter warps splitting them into the
-    swizzled operand rows; no prepass kernel) -- against the oracle, with ONE launch where the
-    tap-shared geometry applies, and BIT-IDENTICAL to the default prepass path (same operand bytes,
-    same accumulation order)."""
-    import json, subprocess, sys
-    from pathlib import Path
-    import torch
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    root = Path(__file__).resolve().parent.parent
-    script = tmp_path / "raw.py"
-    script.write_text(_RAW_SCRIPT)
-    outs = {}
-    for raw in ("1", "0"):
-        d = tmp_path / f"r{raw}"
-        d.mkdir()
-        r = subprocess.run([sys.executable, str(script), str(root), str(d)], capture_output=True, text=True,
-                           timeout=900, env=dict(os.environ, CLB_RAW_A=raw), cwd=str(root))
-        assert r.returncode == 0, r.stderr[-3000:]
-        outs[raw] = json.loads(r.stdout.strip().splitlines()[-1])
-    for i, (a, b) in enumerate(zip(outs["1"], outs["0"])):
-        assert a["rel_l2"] <= FP32_L2 and a["max_rel"] <= FP32_MAX, a
-        assert a["launches"] <= b["launches"], (a, b)
-        ya, yb = np.load(tmp_path / "r1" / f"raw_{i}.npy"), np.load(tmp_path / "r0" / f"raw_{i}.npy")
-        assert np.array_equal(ya, yb), ("raw-input A and prepass paths differ", a["case"])
-    assert any(a["launches"] == 1 for a in outs["1"])     # the raw path ran (no prepass launch)
 
 
 def test_selector_timing_cache(oracle, clb, torch_cuda):

@@ -10,6 +10,15 @@
 
 using namespace clb;
 
+// 2-D tiled load (CTA-local): coords (c0 innermost, c1)
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* m, uint64_t* bar, void* smem, int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
 __global__ void probe(const __grid_constant__ CUtensorMap m, float* out, int p0, int plane0, int bytes) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t bar;
