@@ -510,7 +510,12 @@ def run_ours(args, run: Run) -> int:
         # one global reference stream per layer: this rank's images are images [image0, image0 + batch)
         rng.fill_uniform(x, rng.split(li, 0), run.image0 * img)
         rng.fill_uniform(w, rng.split(li, 1))
-        plan.set_weights(w)
+        if plan.method == "direct-gpu" and not args.shard.startswith("channels"):
+            # host upload: the direct kernel's constant-bank weight path is used for weights that
+            # come from the host (a device upload never blocks on a D2H copy; DESIGN 4.1c)
+            plan.set_weights_host(w.cpu())
+        else:
+            plan.set_weights(w)
         base = plan.plan if args.shard.startswith("channels") else plan
         ws = torch.empty(max(base.workspace_bytes(), 4), device=dev, dtype=torch.uint8)
         y = torch.empty(plan.output_shape(), device=dev, dtype=torch.float32)
