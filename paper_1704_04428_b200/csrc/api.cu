@@ -110,6 +110,7 @@ struct cl_plan {
     bool padded_rows = false;  // implicit kn2row in tap-shared (zero-padded row) mode
     int stack_k = 1;           // > 1: padded-row mode with the k taps of a kernel row stacked on N
     int bn_stack = 0;          // its tile N (k x channels per column tile)
+    int msub = 1;              // 2: padded-row mode with two 128-row sub-tiles per B stage (TcParams::msub)
     bool weights_set = false;
     void* own_ws = nullptr;
     size_t own_ws_bytes = 0;
@@ -342,9 +343,15 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
             const int v = e ? std::atoi(e) : 0;
             return (v >= 16 && v <= 256 && v % 16 == 0) ? v : 0;
         }();
-        const bool fixed_bn = t.stack_k > 1;   // tap-stacked: N is k x channels, not a free choice
+        // tap-stacked: N is k x channels; two-sub-tile: N is 2 x the sub-tile's -- not free choices
+        const bool fixed_bn = t.stack_k > 1 || t.msub > 1;
         if (forced_bn && !fixed_bn) t.bn = forced_bn;
-        int cg = cta_group_for(t.rows, t.cols, t.bn);
+        const int ms = t.msub > 1 ? t.msub : 1;
+        int cg = cta_group_for(t.rows / ms, t.cols, t.bn / ms);
+        if (ms > 1 && tc_num_stages(t.bn / ms / cg, t.tps, 1, kSmemBudget, ms) < 3) {   // too few stages: one sub-tile
+            t.msub = 1;
+            t.bn /= ms;
+        }
         // few tiles even at 128 rows: halve the tile N to create more of them (B operand rows
         // are tiny anyway at these sizes)
         if (!forced_bn && !fixed_bn && cg == 1 && t.bn >= 64 &&
@@ -398,6 +405,10 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 t.b_tap3 = 1;
                 t.tps = d.k;
                 t.taps = taps;
+                if (p->msub > 1) {
+                    t.msub = p->msub;
+                    t.bn = p->bn * p->msub;
+                }
                 if (p->stack_k > 1) {
                     // tap-stacked: one k-iteration = kernel row i x one channel block; B rows
                     // (m, j) of row i, D column m*k + j; A unshifted (the shift-add is in the epilogue)
@@ -747,6 +758,22 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
                 p->stack_k = d.k;
                 p->bn_stack = mt * d.k;
             }
+            // Two sub-tiles per B stage (TcParams::msub): each weight stage feeds two 128-row A
+            // boxes, so the operand bytes per MMA drop by 20 % (N = 64) / 14 % (N = 128) at the
+            // cost of a stage (4 instead of 6 at N = 64) and tiles twice as large.  Measured (ms,
+            // tools/gpu_msub.sh): VGG conv1_2 0.556 -> 0.433, conv2_1 0.181 -> 0.166, conv2_2
+            // 0.323 -> 0.305; slower where the bigger tiles leave < 2 waves (GoogLeNet 3a_3x3 0.045
+            // -> 0.052, C1 0.018 -> 0.023), so auto asks for >= 4 waves.  Mixed split only (the
+            // kernel instantiates it there); CLB_MSUB=1/2 forces.
+            static const int forced_msub = [] {
+                const char* e = std::getenv("CLB_MSUB");
+                return e ? std::atoi(e) : -1;
+            }();
+            const long long grid_rows = (long long)d.n * (d.h + d.pad) * (d.w + d.pad);
+            const bool many_tiles = grid_rows / (2LL * kTileM * pcg) >= 4LL * (num_sms() / pcg);
+            if (p->padded_rows && p->stack_k == 1 && p->planes == 4 && p->bn <= 128 && forced_msub != 1 &&
+                (forced_msub == 2 || many_tiles))
+                p->msub = 2;
         }
         // stream-K flags [kMaxGrid], self-resetting (zeroed once here)
         if (cudaMalloc(&p->flags, (kMaxGrid + 8) * sizeof(unsigned)) != cudaSuccess ||

@@ -161,12 +161,19 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
         if (a.mode != LOAD_TILED || p.tps != 1) throw Error(6, "tap-stacked mode needs a tiled A, one tap per stage");
         p.row_step = 4 * (33 - p.stack_k);
     }
+    if (p.msub <= 1) {
+        p.msub = 1;
+    } else if (p.msub != 2 || p.stack_k != 1 || a.mode != LOAD_TILED || p.tps < 2 || a.planes != 4 ||
+               p.bn % 32 != 0) {
+        throw Error(6, "two-sub-tile mode: mixed split, tap-shared tiled A, N a multiple of 16 per sub-tile");
+    }
+    const int mma_n = p.bn / p.msub;
     CUtensorMap ma, mb;
     // tap-stacked: A = {unit, 32 rows, 4 quadrants} over the overlapping quadrant view
     if (p.stack_k > 1 && (a.taps != 4 || a.tap_stride_rows != 33 - p.stack_k))
         throw Error(6, "tap-stacked A must be the 4-quadrant overlapping view");
     encode_operand_map(&ma, a, p.stack_k > 1 ? 32 : tc_a_box_rows(p.tps), p.stack_k > 1 ? 4 : 1);
-    encode_operand_map(&mb, b, p.bn / cg, p.tps);
+    encode_operand_map(&mb, b, mma_n / cg, p.tps);
     p.planes = a.planes;
     p.row_elems = unit;
     p.kblocks = a.kw / unit;
@@ -174,7 +181,7 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     p.b_mode = b.mode;
     if (p.taps % p.tps != 0) throw Error(6, "taps per stage must divide the tap count");
     const int k_iters = (p.taps / p.tps) * p.kblocks;
-    const int b_rows = p.bn / cg;
+    const int b_rows = mma_n / cg;
     // chunk = K slice per TMEM accumulator.  The fp32-faithful splits bound it to kChunkK
     // K-elements (16 channels x tps taps per k-iteration): tensor-core accumulation error grows
     // ~linearly with the chunk (rel-L2 8.3e-7 / 1.07e-6 / 1.33e-6 at 128 / 192 / 256, bound 1e-5;
@@ -211,24 +218,24 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     if (p.bps <= 0) {
         static const int env_bps = getenv("CLB_BPS") ? atoi(getenv("CLB_BPS")) : 0;   // experiment knob
         if (env_bps > 0) p.bps = env_bps;
-        else p.bps = (tc_num_stages(stage_b_rows, p.tps, 2, budget) >= 3 && (p.chunk_iters % 2 == 0 || p.chunk_iters == k_iters)) ? 2 : 1;
+        else p.bps = (tc_num_stages(stage_b_rows, p.tps, 2, budget, p.msub) >= 3 && (p.chunk_iters % 2 == 0 || p.chunk_iters == k_iters)) ? 2 : 1;
     }
-    p.stages = tc_num_stages(stage_b_rows, p.tps, p.bps, budget);
-    while (p.stages < 2 && p.bps > 1) p.stages = tc_num_stages(stage_b_rows, p.tps, --p.bps, budget);
+    p.stages = tc_num_stages(stage_b_rows, p.tps, p.bps, budget, p.msub);
+    while (p.stages < 2 && p.bps > 1) p.stages = tc_num_stages(stage_b_rows, p.tps, --p.bps, budget, p.msub);
     if (p.stages < 2) throw Error(2, "tile too large for a 2-stage pipeline");
     // chunk boundaries must be stage boundaries: chunk_iters a multiple of bps (a single-chunk
     // tile is exempt -- its only chunk starts the piece and ends at k_iters)
     if (p.chunk_iters < k_iters && p.chunk_iters % p.bps != 0)
         p.chunk_iters = p.chunk_iters >= p.bps ? p.chunk_iters / p.bps * p.bps : p.bps;
     if (p.chunk_iters > k_iters) p.chunk_iters = k_iters;
-    const int tile_m = p.row_step * cg;   // output rows per tile
+    const int tile_m = p.row_step * cg * p.msub;   // output rows per tile
     const int row_tiles = (p.rows + tile_m - 1) / tile_m;
-    p.n_col_tiles = (p.cols + p.bn - 1) / p.bn;
+    p.n_col_tiles = (p.cols + mma_n - 1) / mma_n;
     p.num_tiles = row_tiles * p.n_col_tiles;
     if (p.num_tiles <= 0) return 0;
     p.chunks_per_tile = (k_iters + p.chunk_iters - 1) / p.chunk_iters;
     const long long total_chunks = (long long)p.num_tiles * p.chunks_per_tile;
-    const int smem = tc_smem_bytes(stage_b_rows, p.tps, p.stages, p.bps);
+    const int smem = tc_smem_bytes(stage_b_rows, p.tps, p.stages, p.bps, p.msub);
     // The stream-K fixup makes CTAs wait on each other, so every CTA of the grid must be
     // co-resident: the unit count is capped at what the occupancy calculator says fits at once
     // for this kernel, smem size and cluster shape (on the current device; attributes and
@@ -393,7 +400,7 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
         CLB_CUDA(cudaStreamSynchronize(s));
         fprintf(stderr, "[clb-dbg] rows=%d cols=%d bn=%d cg=%d stages=%d bps=%d grid=%d bars at +0x%x "
                 "(full[s], empty[s], tfull[4], tempty[4], fix): %u timed-out waits\n", p.rows, p.cols, p.bn, cg,
-                p.stages, p.bps, grid, p.stages * p.bps * tc_stage_bytes(stage_b_rows, p.tps),
+                p.stages, p.bps, grid, p.stages * p.bps * tc_stage_bytes(stage_b_rows, p.tps, p.msub),
                 (unsigned)(rec[7] & 0xffffffffu));
         for (int i = 0; i < 6 && i < (int)(rec[7] & 0xffffffffu); ++i)
             fprintf(stderr, "[clb-dbg]   block %llu warp %llu bar smem+0x%llx parity %llu\n", rec[i] >> 40,
@@ -421,11 +428,11 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
         }
         const double mhz = ns_sum > 0 ? 1e3 * cyc_sum / ns_sum : 0.0;
         fprintf(stderr,
-                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stack=%d bres=%d aiss=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d sku=%d | producer %.0f cyc "
+                "[clb-trace] rows=%d cols=%d bn=%d cg=%d tps=%d stack=%d msub=%d aiss=%d bps=%d stages=%d cpt=%d grid=%d tiles=%d dp=%d sku=%d | producer %.0f cyc "
                 "(wait empty %.0f%%) | mma %.0f (wait full %.0f%%, wait tmem %.0f%%) | epilogue %.0f (wait tfull %.0f%%, "
                 "store %.0f%%, fixup wait %.0f%%) | setup %.0f cyc | span %.1f us (last CTA start +%.1f us) | events %.1f us | "
                 "SM clock %.0f MHz (CTA cycles / CTA ns)\n",
-                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, 0, p.a_issuers, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, p.sk_units, avg[0], 100 * avg[1] / avg[0],
+                p.rows, p.cols, p.bn, cg, p.tps, p.stack_k, p.msub, p.a_issuers, p.bps, p.stages, p.chunks_per_tile, grid, p.num_tiles, p.dp_tiles, p.sk_units, avg[0], 100 * avg[1] / avg[0],
                 avg[2], 100 * avg[3] / avg[2], 100 * avg[4] / avg[2], avg[5], 100 * avg[6] / avg[5], 100 * avg[7] / avg[5], 100 * avg[11] / avg[5], avg[8], (t_out - t_in) * 1e-3,
                 (t_in_max - t_in) * 1e-3, ev_ms * 1e3, mhz);
         if (const char* dump = getenv("CLB_TRACE_DUMP")) {   // raw per-CTA records, appended

@@ -108,6 +108,13 @@ struct TcParams {
     // k - 1 halo rows: 33 - k outputs per quadrant, row_step = 4 (33 - k) per CTA.  For small
     // M (N = M would be a slow, small MMA).
     int stack_k;               // 1 = off
+    // two-sub-tile mode (msub = 2, padded-row mode, one tap group per stage): each CTA computes
+    // TWO 128-row sub-tiles against every B stage -- sub-tile u is the CTA's rows of the u-th
+    // half of the tile, its own A box in the stage, its own D columns [u * bn / 2, (u + 1) * bn / 2)
+    // (the MMA's N is bn / 2).  The weights a stage carries feed twice the MMA work, so the
+    // operand bytes per MMA drop by a fifth at N = 64 (VGG conv1_2); the epilogue's column
+    // halves ARE the sub-tiles.
+    int msub;                  // 1 = off
     int row_step;              // output rows per CTA tile (128, or 4 (33 - k) when stacked)
     int accumulate;            // out += D (accumulating shifted-GEMM variant)
     float* out;
@@ -150,15 +157,17 @@ __host__ __device__ inline int chunk_start(int b, int total, int grid) {
 // B rows = tps taps x (bn / cta group).
 __host__ __device__ inline int tc_a_box_rows(int tps) { return kTileM + tps - 1; }
 __host__ __device__ inline int tc_a_bytes(int tps) { return (tc_a_box_rows(tps) * kRowBytes + 1023) & ~1023; }
-__host__ __device__ inline int tc_stage_bytes(int b_rows, int tps) { return tc_a_bytes(tps) + tps * b_rows * kRowBytes; }
+__host__ __device__ inline int tc_stage_bytes(int b_rows, int tps, int msub = 1) {
+    return msub * tc_a_bytes(tps) + tps * b_rows * kRowBytes;
+}
 
-__host__ inline int tc_num_stages(int b_rows, int tps, int bps = 1, int budget = kSmemBudget) {
-    int s = (budget - 1024 - kBarrierBytes) / (bps * tc_stage_bytes(b_rows, tps));
+__host__ inline int tc_num_stages(int b_rows, int tps, int bps = 1, int budget = kSmemBudget, int msub = 1) {
+    int s = (budget - 1024 - kBarrierBytes) / (bps * tc_stage_bytes(b_rows, tps, msub));
     return s > 8 ? 8 : s;
 }
 
-__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages, int bps = 1) {
-    return 1024 /*align slack*/ + stages * bps * tc_stage_bytes(b_rows, tps) + kBarrierBytes;
+__host__ inline int tc_smem_bytes(int b_rows, int tps, int stages, int bps = 1, int msub = 1) {
+    return 1024 /*align slack*/ + stages * bps * tc_stage_bytes(b_rows, tps, msub) + kBarrierBytes;
 }
 
 // TMEM accumulator buffers: 4 when they fit (BN <= 128), else ping-pong.  Extra buffers let
@@ -389,16 +398,19 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int bn = p.bn;
     const int planes = p.planes;
     const int stages = p.stages;
-    const int tile_m = kTileM * CG;               // D rows per tile (the pair's rows for CG = 2)
-    const int tile_rows = p.row_step * CG;        // output rows per tile (< tile_m when tap-stacked)
-    const int b_rows = bn / CG;                   // B rows this CTA loads
+    const int msub = p.msub;                      // 128-row sub-tiles per CTA sharing each B stage
+    const int mma_n = bn / msub;                  // N of one MMA (bn = D columns of the tile)
+    const int tile_m = kTileM * CG;               // D rows per MMA (the pair's rows for CG = 2)
+    const int sub_rows = p.row_step * CG;         // output rows per sub-tile (< tile_m when tap-stacked)
+    const int tile_rows = sub_rows * msub;        // output rows per tile
+    const int b_rows = mma_n / CG;                // B rows this CTA loads
     const int tps = p.tps;
-    const int a_bytes = tc_a_bytes(tps);          // A region of one stage (128 + tps - 1 rows)
+    const int a_bytes = tc_a_bytes(tps);          // one A box of a stage (128 + tps - 1 rows)
     const int b_bytes = tps * b_rows * kRowBytes; // B rows of one k-iteration (tps taps)
-    const int stage_bytes = a_bytes + b_bytes;    // one sub-stage (one k-iteration)
+    const int stage_bytes = msub * a_bytes + b_bytes;   // one sub-stage (one k-iteration)
     const int bps = p.bps;
     const int group_bytes = bps * stage_bytes;    // one pipeline stage
-    const uint32_t stage_tx = (uint32_t)(tc_a_box_rows(tps) * kRowBytes + b_bytes);
+    const uint32_t stage_tx = (uint32_t)(msub * tc_a_box_rows(tps) * kRowBytes + b_bytes);
     const int k_iters = (p.taps / tps) * p.kblocks;   // k-iterations per tile
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
@@ -478,7 +490,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             uint32_t gs = 0;   // stage sequence number
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t a_tx = (uint32_t)(tc_a_box_rows(tps) * kRowBytes);
+            const uint32_t a_tx = (uint32_t)(msub * tc_a_box_rows(tps) * kRowBytes);
             const uint32_t tx = (uint32_t)CG * ((do_a ? a_tx : 0u) + (do_b ? stage_tx - a_tx : 0u));   // both CTAs' bytes land on the leader
             long long w_empty = 0;
             const long long t_start = clock64();
@@ -521,14 +533,16 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                                 tma_load_im2col_4d_2sm(&map_a, lbar, a_st, kc, ca.c1, ca.c2, ca.c3, (uint16_t)tj,
                                                        (uint16_t)ti);
                             else
-                                tma_load_3d_2sm(&map_a, lbar, a_st, kc, arow, ca.tap3 ? tap : 0);
+                                for (int u = 0; u < msub; ++u)
+                                    tma_load_3d_2sm(&map_a, lbar, a_st + u * a_bytes, kc, arow + u * sub_rows,
+                                                    ca.tap3 ? tap : 0);
                         }
                         if (do_b) {
                             if (cb.mode == LOAD_IM2COL)
-                                tma_load_im2col_4d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.c2, cb.c3, (uint16_t)tj,
+                                tma_load_im2col_4d_2sm(&map_b, lbar, a_st + msub * a_bytes, kc, cb.c1, cb.c2, cb.c3, (uint16_t)tj,
                                                        (uint16_t)ti);
                             else
-                                tma_load_3d_2sm(&map_b, lbar, a_st + a_bytes, kc, cb.c1, cb.tap3 ? tap : 0);
+                                tma_load_3d_2sm(&map_b, lbar, a_st + msub * a_bytes, kc, cb.c1, cb.tap3 ? tap : 0);
                         }
                     } else {
                         if (sub == 0) mbar_arrive_expect_tx(&full[stage], txs);
@@ -536,9 +550,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             if (ca.mode == LOAD_IM2COL)
                                 load_operand(&map_a, ca, &full[stage], a_st, kc, tap, ti, tj);
                             else
-                                tma_load_3d(&map_a, &full[stage], a_st, kc, arow, ca.tap3 ? tap : 0);
+                                for (int u = 0; u < msub; ++u)
+                                    tma_load_3d(&map_a, &full[stage], a_st + u * a_bytes, kc, arow + u * sub_rows,
+                                                ca.tap3 ? tap : 0);
                         }
-                        if (do_b) load_operand(&map_b, cb, &full[stage], a_st + a_bytes, kc, tap, ti, tj);
+                        if (do_b) load_operand(&map_b, cb, &full[stage], a_st + msub * a_bytes, kc, tap, ti, tj);
                     }
                     }
                     __syncwarp();
@@ -578,9 +594,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // The whole warp runs the loop (loop state is warp-uniform, so it lives in uniform
         // registers); one elected lane issues the MMAs and the commits that track them.
         if (leader) {
-            const uint32_t idesc = planes == 3 ? idesc_bf16((uint32_t)tile_m, (uint32_t)bn)
-                                               : idesc_tf32((uint32_t)tile_m, (uint32_t)bn);
-            const uint32_t idesc16 = idesc_bf16((uint32_t)tile_m, (uint32_t)bn);   // mixed mode corrections
+            const uint32_t idesc = planes == 3 ? idesc_bf16((uint32_t)tile_m, (uint32_t)mma_n)
+                                               : idesc_tf32((uint32_t)tile_m, (uint32_t)mma_n);
+            const uint32_t idesc16 = idesc_bf16((uint32_t)tile_m, (uint32_t)mma_n);   // mixed mode corrections
             auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
                 if constexpr (CG == 2) mma_tf32_ss_2sm(d, a, b, idesc, acc);
                 else mma_tf32_ss(d, a, b, idesc, acc);
@@ -603,7 +619,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint64_t desc0 = umma_desc_kmajor(smem_u32(smem), kRowBytes);
             const uint64_t st_step = (uint64_t)(group_bytes >> 4);
             const uint64_t sub_step = (uint64_t)(stage_bytes >> 4);
-            const uint64_t b_off = (uint64_t)(a_bytes >> 4);
+            const uint64_t b_off = (uint64_t)((msub * a_bytes) >> 4);
+            const uint64_t a_sub = (uint64_t)(a_bytes >> 4);                // next sub-tile's A box
+            const uint32_t d_sub = (uint32_t)mma_n;                         // next sub-tile's D columns
             const uint64_t tap_b = (uint64_t)(b_rows * 8);
             long long w_full = 0, w_tempty = 0;
             const long long t_start = clock64();
@@ -611,14 +629,19 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             // (compile-time), and one elected block issues a whole stage: at N = 192 the MMAs of a
             // k-iteration take ~384 tensor cycles, and a generic loop (format dispatch, tap loop,
             // one elect + reconvergence per k-iteration: ~100 instructions) could not keep up.
-            auto run = [&](auto pl_c, auto t1_c) {
+            auto run = [&](auto pl_c, auto t1_c, auto ms_c) {
                 constexpr int PL = decltype(pl_c)::value;
                 constexpr bool T1 = decltype(t1_c)::value;
+                constexpr int MS = decltype(ms_c)::value;   // == msub
                 // one k-iteration: the taps of the group x the format's MMAs; acc0 = 0 only for the
                 // chunk's first k-iteration (its first MMA starts the accumulator)
-                auto issue = [&](uint32_t d_tmem, uint64_t da0, uint64_t db0, uint32_t acc0) {
+                auto issue = [&](uint32_t d_tmem0, uint64_t da00, uint64_t db0, uint32_t acc0) {
                     const int ntaps = T1 ? 1 : tps;
+#pragma unroll
+                    for (int u = 0; u < MS; ++u)
                     for (int t = 0; t < ntaps; ++t) {
+                        const uint32_t d_tmem = d_tmem0 + (uint32_t)u * d_sub;
+                        const uint64_t da0 = da00 + (uint64_t)u * a_sub;
                         // tap t of the group: A shifted by t rows (8 desc units of 16 B per
                         // 128 B row), B = the t-th tap's weight tile
                         const uint64_t da = da0 + (uint64_t)(t * 8);
@@ -710,14 +733,17 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             using I4 = std::integral_constant<int, 4>;
             using BT = std::true_type;
             using BF = std::false_type;
+            // (two-sub-tile mode: mixed split, tap-shared stages only -- launch_tc enforces it)
             if (planes == 4) {
-                if (tps == 1) run(I4{}, BT{}); else run(I4{}, BF{});
+                if (tps == 1) run(I4{}, BT{}, I1{});
+                else if (msub == 2) run(I4{}, BF{}, I2{});
+                else run(I4{}, BF{}, I1{});
             } else if (planes == 2) {
-                if (tps == 1) run(I2{}, BT{}); else run(I2{}, BF{});
+                if (tps == 1) run(I2{}, BT{}, I1{}); else run(I2{}, BF{}, I1{});
             } else if (planes == 3) {
-                if (tps == 1) run(I3{}, BT{}); else run(I3{}, BF{});
+                if (tps == 1) run(I3{}, BT{}, I1{}); else run(I3{}, BF{}, I1{});
             } else {
-                if (tps == 1) run(I1{}, BT{}); else run(I1{}, BF{});
+                if (tps == 1) run(I1{}, BT{}, I1{}); else run(I1{}, BF{}, I1{});
             }
             if (TRACE && lane_id() == 0) {
                 p.trace[blockIdx.x * kTraceSlots + 2] = (unsigned long long)(clock64() - t_start);
@@ -767,9 +793,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         while (sch.next(pc)) {
             const int mt = pc.tile / p.n_col_tiles;
             const int nt = pc.tile - mt * p.n_col_tiles;
-            const int row = mt * tile_rows + (int)rank * p.row_step +
+            // two-sub-tile mode: column half = sub-tile (rows of the tile's half-th sub_rows)
+            const int row = mt * tile_rows + (msub > 1 ? half * sub_rows : 0) + (int)rank * p.row_step +
                             (p.stack_k > 1 ? quad * (33 - p.stack_k) + lane : trow);
-            int col0 = nt * bn + cbase;
+            int col0 = msub > 1 ? nt * mma_n : nt * bn + cbase;
             float sum[128];
 #pragma unroll
             for (int j = 0; j < 128; ++j) sum[j] = 0.0f;

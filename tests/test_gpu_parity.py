@@ -380,7 +380,7 @@ print(json.dumps(out))
 '''
 
 
-@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs"])
+@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs", "msub", "msub-cg1"])
 def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     """The implicit kernel's tap-shared mode (zero-padded NHWC rows, one A box of 128+k-1 rows
     per kernel row, taps through row-shifted UMMA descriptors), forced on and off via
@@ -389,7 +389,10 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     "stacked" forces the tap-stacked variant (the k taps of a kernel row as column blocks of one
     MMA, shift-add across rows in the epilogue) wherever it applies (k = 3/5, k x M <= 256),
     including multi-chunk K, stream-K split tiles, M not a multiple of 16 and pad 0 / pad > k/2;
-    the launch trace proves both k = 3 and k = 5 instantiations ran.  "knobs" turns the
+    the launch trace proves both k = 3 and k = 5 instantiations ran.  "msub" / "msub-cg1" force
+    the two-sub-tile mode (two 128-row A boxes per weight stage, D column halves = sub-tiles) on
+    every mixed-split padded layer, with CTA pairs and single CTAs: ragged M (16 / 40 / 80),
+    k = 3/5/7, stream-K split tiles.  "knobs" turns the
     remaining A/B switches to their non-default side so they stay correct: one producer warp
     for A and B (CLB_SPLIT_ISSUE=0), stream-K partials added from global memory
     (CLB_FIXUP_SMEM=0) and stream-K ranges over all units (CLB_SK_UNITS=0)."""
@@ -405,7 +408,9 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
            "stacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1"),
            "unstacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="0"),
            "knobs": dict(CLB_PADDED_ROWS="1", CLB_SPLIT_ISSUE="0", CLB_FIXUP_SMEM="0", CLB_SK_UNITS="0",
-                         CLB_TRACE="1")}[mode]
+                         CLB_TRACE="1"),
+           "msub": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="2", CLB_TRACE="1"),
+           "msub-cg1": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="1", CLB_TRACE="1")}[mode]
     r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, **env))
     assert r.returncode == 0, r.stderr[-3000:]
@@ -413,6 +418,9 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
         assert "stack=3" in r.stderr and "stack=5" in r.stderr, r.stderr[-2000:]
     if mode == "knobs":
         assert "aiss=1" in r.stderr, r.stderr[-2000:]
+    if mode.startswith("msub"):
+        assert "msub=2" in r.stderr, r.stderr[-2000:]
+        assert ("cg=1" if mode == "msub-cg1" else "cg=2") in r.stderr, r.stderr[-2000:]
     for res in json.loads(r.stdout.strip().splitlines()[-1]):
         if res["precision"] == "fp32":
             assert res["rel_l2"] <= FP32_L2 and res["max_rel"] <= FP32_MAX, (mode, res)
