@@ -70,8 +70,9 @@ def parse_args(argv=None):
                          "(auto: strong for the C5 'scale' workload, weak otherwise)")
     ap.add_argument("--method", default="auto")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "bf16"],
-                    help="fp32 = fp32-faithful (rel-L2 <= 1e-5; operand split per CLB_SPLIT: mixed "
-                         "(default) or 3xtf32); tf32 / bf16 = the 1e-2 fast modes")
+                    help="fp32 = fp32-faithful (rel-L2 <= 1e-5; operand split per layer: the fp16 split of "
+                         "power-of-2 scaled operands by default, CLB_SPLIT=3xf16|mixed|3xtf32 forces one); "
+                         "tf32 / bf16 = the 1e-2 fast modes")
     ap.add_argument("--layout", default="nchw", choices=["nchw", "nhwc"],
                     help="device tensors NCHW (the reference interface, default) or channels-last "
                          "(cl_conv_forward_nhwc; the e2e leg stays NCHW)")
@@ -211,8 +212,7 @@ def config_of(args, run: Run) -> dict:
         "global_batch": glob, "per_gpu_batch": per_gpu if per_gpu is not None else -(-glob // run.world),
         "scaling": run.scaling, "layout": args.layout, "method": args.method,
         "schedule": "concurrent" if args.concurrent else ("chain" if args.chain else "sequential"),
-        "precision": {"fp32": ("fp32-faithful (rel-L2 <= 1e-5): hi*Hi tf32 x2 + cross terms bf16 x2"
-                               if fp32_split() == "mixed" else "fp32-faithful 3xTF32"),
+        "precision": {"fp32": "fp32-faithful (rel-L2 <= 1e-5): " + SPLIT_TEXT[split_mode()],
                       "tf32": "tf32 (fast mode)", "bf16": "bf16 operands, fp32 accumulate (fast mode)"}[args.precision],
         "parallelism": (f"dp{run.world} (batch-sharded, no data-path collective)" if args.shard == "batch" else
                         f"mp{run.world} (output channels sharded, NCCL all-gather of the output slices)"
@@ -233,26 +233,32 @@ def relaunch_under_torchrun(args) -> int:
 
 
 # ----------------------------------------------------------------- precision ----
-def fp32_split():
-    """The fp32-faithful operand split the library uses (same switch as api.cu planes_for):
-    'mixed' = hi*Hi in two tf32 MMAs + the two cross terms in one bf16 K=16 MMA each (4
-    tf32-MMA slots per 16 K-elements); '3xtf32' = the classic split (6 slots)."""
-    return "3xtf32" if os.environ.get("CLB_SPLIT") == "3xtf32" else "mixed"
+SPLIT_TEXT = {
+    "auto": "fp16 split of power-of-2 scaled operands (lo*Hi + hi*Lo + hi*Hi, kind::f16) for the implicit "
+            "kn2row layers, mixed split (hi*Hi tf32 x2 + cross terms bf16 x2) where C = 16 / 48",
+    "3xf16": "fp16 split of power-of-2 scaled operands (kind::f16 x3) where the method supports it",
+    "mixed": "hi*Hi tf32 x2 + cross terms bf16 x2", "3xtf32": "classic 3xTF32"}
 
 
-def tensor_factor(precision):
-    """Effective-TFLOP/s per tf32 TFLOP/s of the tensor pipe for each precision mode."""
-    if precision == "fp32":
-        return 1.0 / 3.0 if fp32_split() == "3xtf32" else 0.5
-    return {"tf32": 1.0, "bf16": 2.0}[precision]
+def split_mode():
+    """The fp32-faithful split selection in force (api.cu conv_planes_for; CLB_SPLIT forces one)."""
+    e = os.environ.get("CLB_SPLIT")
+    return e if e in ("3xf16", "mixed", "3xtf32") else "auto"
 
 
-def mma_peak_for(precision):
+def split_factor(split):
+    """Effective TFLOP/s per tf32 TFLOP/s of the tensor pipe for an operand format (a plan's
+    `split`): 3xf16 issues 3 f16 MMAs (each half a tf32 MMA's time per K) per product -> 2/3;
+    mixed 4 tf32-MMA slots per 16 K -> 1/2; 3xtf32 6 slots -> 1/3; tf32 1; bf16 2."""
+    return {"3xf16": 2.0 / 3.0, "mixed": 0.5, "3xtf32": 1.0 / 3.0, "tf32": 1.0, "bf16": 2.0}[split]
+
+
+def mma_peak_tf32():
     """Our own kind::tf32 MMA peak (tools/mma_probe.cu, profiles/tf32_mma_peak.json)."""
     f = ROOT / "profiles" / "tf32_mma_peak.json"
     if not f.exists():
         return None
-    return json.loads(f.read_text())["tf32_mma_peak_tflops"] * tensor_factor(precision)
+    return json.loads(f.read_text())["tf32_mma_peak_tflops"]
 
 
 def peaks():
@@ -273,7 +279,7 @@ def traffic_for(workload, precision, method):
         except Exception:
             continue
         if (tr.get("workload") == workload and tr.get("precision", "fp32") == precision and method == "auto"
-                and tr.get("split", "mixed") == (fp32_split() if precision == "fp32" else tr.get("split", "mixed"))):
+                and tr.get("split", "mixed") == (split_mode() if precision == "fp32" else tr.get("split", "mixed"))):
             return tr.get("dram_bytes_per_step"), str(f.relative_to(ROOT))
     return None, None
 
@@ -650,13 +656,23 @@ def run_ours(args, run: Run) -> int:
     d2h = sum(y.numel() * 4 for y in hy)
 
     # ---- roofline of the dominant kernel (tc_conv_kernel: the tcgen05 contraction) ------
+    # each layer against the peak of its own operand format (plan.split); the step's tcgen05
+    # layers against the FLOP-weighted combination (sum of the layers' times at their peaks)
     tf32_peak = pk["bf16"] / 2.0
-    mode_peak = tf32_peak * tensor_factor(args.precision)
-    nominal_peak = NOMINAL_BF16 / 2.0 * tensor_factor(args.precision)
     hbm = pk["hbm"]
     tc_idx = [i for i, p in enumerate(plans) if p.method != "direct-gpu"]
     tc_flops = sum(rank_flops[i] for i in tc_idx)
     tc_ms = sum(kern_ms[i] for i in tc_idx)
+    splits = sorted({plans[i].split for i in tc_idx})
+
+    def combined(peak_tf32):
+        if not tc_idx or not peak_tf32:
+            return None
+        return tc_flops / sum(rank_flops[i] / (peak_tf32 * split_factor(plans[i].split)) for i in tc_idx)
+
+    mode_peak = combined(tf32_peak)
+    nominal_peak = combined(NOMINAL_BF16 / 2.0)
+    mma_peak = combined(mma_peak_tf32())
     if conc is not None:     # concurrent step: the whole step (prepasses and all) is the measure
         tc_ms = med_ms
     achieved = tc_flops / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else None
@@ -666,13 +682,15 @@ def run_ours(args, run: Run) -> int:
     layer_rows = []
     for l, p, km, fl in zip(rank_layers, plans, kern_ms, rank_flops):
         ai = l.flops() / l.bytes()
-        bound = min(mode_peak, ai * hbm / 1e3)
+        lpeak = tf32_peak * split_factor(p.split if p.split in ("3xf16", "mixed", "3xtf32", "tf32", "bf16")
+                                         else {"fp32": "mixed", "tf32": "tf32", "bf16": "bf16"}[args.precision])
+        bound = min(lpeak, ai * hbm / 1e3)
         tf = fl / (km * 1e-3) / 1e12
-        layer_rows.append({"name": l.name, "method": p.method, "batch": l.batch, "gflop": round(fl / 1e9, 3),
-                           "kernel_ms": round(km, 4), "kernel_tflops": round(tf, 1),
-                           "frac_of_peak": round(tf / mode_peak, 3),
+        layer_rows.append({"name": l.name, "method": p.method, "split": p.split, "batch": l.batch,
+                           "gflop": round(fl / 1e9, 3), "kernel_ms": round(km, 4), "kernel_tflops": round(tf, 1),
+                           "peak_tflops": round(lpeak, 1), "frac_of_peak": round(tf / lpeak, 3),
                            "layer_roofline_tflops": round(bound, 1), "frac_of_layer_roofline": round(tf / bound, 3),
-                           "bound": "tensor" if bound >= mode_peak else "hbm",
+                           "bound": "tensor" if bound >= lpeak else "hbm",
                            "share_of_step": round(km / statistics.median(step_ms), 3)})
 
     if run.rank != 0:
@@ -705,26 +723,27 @@ def run_ours(args, run: Run) -> int:
                        "per step (pinned host buffers)"},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": mode_peak, "unit": "TFLOP/s",
-                     "frac": achieved / mode_peak if achieved else None, "traffic": traffic,
+                     "frac": achieved / mode_peak if achieved and mode_peak else None, "traffic": traffic,
                      "traffic_source": traffic_src,
                      "algorithmic_bytes_per_step": sum(rank_layers[i].bytes() for i in tc_idx),
-                     "kernel": {"fp32": ("tc_conv_kernel (tcgen05: hi*Hi kind::tf32 x2 + cross terms kind::f16 x2)"
-                                         if fp32_split() == "mixed" else "tc_conv_kernel (tcgen05 kind::tf32 x3)"),
-                                "tf32": "tc_conv_kernel (tcgen05 kind::tf32)",
-                                "bf16": "tc_conv_kernel (tcgen05 kind::f16, bf16)"}[args.precision],
+                     "kernel": "tc_conv_kernel (tcgen05; operand formats " + ", ".join(splits) + ": " + "; ".join(
+                         {"3xf16": "3xf16 = lo*Hi + hi*Lo + hi*Hi kind::f16 fp16",
+                          "mixed": "mixed = hi*Hi kind::tf32 x2 + cross terms kind::f16 bf16 x2",
+                          "3xtf32": "3xtf32 = kind::tf32 x3", "tf32": "tf32 = kind::tf32",
+                          "bf16": "bf16 = kind::f16 bf16"}[s_] for s_ in splits) + ")",
                      "kernel_ms_per_step": tc_ms, "kernel_layers": len(tc_idx),
-                     "peak_note": (f"peak = measured bf16 burst {pk['bf16']} / 2 (tf32 rate) x "
-                                   f"{tensor_factor(args.precision):.3g} (effective flops per tf32 MMA flop: "
-                                   "fp32 split 'mixed' 1/2, '3xtf32' 1/3; tf32 1; bf16 2); "
-                                   f"{pk['source']}.  achieved = FLOPs of the tcgen05 layers / the median per-step sum "
-                                   "of their CUDA-event-timed contraction launches; the direct-gpu layer (VGG conv1_1, "
-                                   "CUDA cores, HBM-bound) is in `layers` against its own roofline"),
-                     "fp32_split": fp32_split() if args.precision == "fp32" else None,
-                     "measured_mma_peak": mma_peak_for(args.precision),
-                     "frac_of_measured_mma_peak": (achieved / mma_peak_for(args.precision)
-                                                   if achieved and mma_peak_for(args.precision) else None),
+                     "peak_note": (f"peak = measured bf16 burst {pk['bf16']} / 2 (tf32 rate) x the operand format's "
+                                   "effective flops per tf32 MMA flop (3xf16 2/3 = bf16 / 3, mixed 1/2, 3xtf32 1/3, "
+                                   "tf32 1, bf16 2), FLOP-weighted over the layers (sum of the layers' times at "
+                                   f"their peaks); {pk['source']}.  achieved = FLOPs of the tcgen05 layers / the median "
+                                   "per-step sum of their CUDA-event-timed contraction launches; the direct-gpu layer "
+                                   "(VGG conv1_1, CUDA cores, HBM-bound) is in `layers` against its own roofline"),
+                     "fp32_split": split_mode() if args.precision == "fp32" else None,
+                     "operand_splits": splits,
+                     "measured_mma_peak": mma_peak,
+                     "frac_of_measured_mma_peak": achieved / mma_peak if achieved and mma_peak else None,
                      "nominal_peak": nominal_peak,
-                     "frac_of_nominal": achieved / nominal_peak if achieved else None},
+                     "frac_of_nominal": achieved / nominal_peak if achieved and nominal_peak else None},
         "layers": layer_rows,
         "concurrent": (None if conc is None else
                        {"sm_caps": conc.caps, "standalone_forward_ms": [round(t, 4) for t in conc.standalone_ms],

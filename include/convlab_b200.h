@@ -112,6 +112,13 @@ CL_API size_t cl_conv_workspace_bytes(const cl_plan* plan);
 /* The method the plan resolved to (auto -> concrete). */
 CL_API cl_method cl_conv_resolved_method(const cl_plan* plan);
 
+/* The tensor-core operand format the plan computes with (no reference counterpart: the
+ * reference is plain fp32):  "3xf16" (fp32-faithful fp16 split of the power-of-2 scaled
+ * operands, default of the implicit kn2row family), "mixed" (fp32-faithful tf32 hi*Hi + bf16
+ * cross terms), "3xtf32" (classic split), "tf32" / "bf16" (1e-2 fast modes), "fp32-fma" (the
+ * direct CUDA-core kernel).  Static storage. */
+CL_API const char* cl_conv_operand_split(const cl_plan* plan);
+
 /* y[N][M][P][Q] = conv(x[N][C][H][W], w).  d_ws may be NULL: the plan then owns a lazily
  * allocated workspace.  Asynchronous on `stream`; returns after enqueueing. */
 CL_API cl_status cl_conv_forward(cl_plan* plan, const float* d_x, float* d_y, void* d_ws, void* stream);

@@ -31,7 +31,7 @@ PRECISIONS = {"fp32": 0, "tf32": 1, "bf16": 2}
 
 EXPORTS = [
     "cl_conv_plan", "cl_conv_set_weights", "cl_conv_set_weights_host", "cl_conv_output_dims", "cl_conv_workspace_bytes",
-    "cl_conv_resolved_method", "cl_conv_forward", "cl_conv_forward_nhwc", "cl_conv_forward_host", "cl_conv_forward_host_async", "cl_conv_last_launch_count",
+    "cl_conv_resolved_method", "cl_conv_operand_split", "cl_conv_forward", "cl_conv_forward_nhwc", "cl_conv_forward_host", "cl_conv_forward_host_async", "cl_conv_last_launch_count",
     "cl_conv_destroy", "cl_gemm_f32", "cl_gemm_workspace_bytes", "cl_shift_add_row", "cl_last_error",
     "cl_method_name", "cl_method_from_name", "cl_abi_version", "cl_device_count", "cl_fill_uniform",
     "cl_conv_set_profile_events", "cl_conv_set_max_sms", "cl_conv_forward_chain", "cl_conv_set_peer_outputs",
@@ -72,6 +72,8 @@ def lib() -> ctypes.CDLL:
     L.cl_conv_workspace_bytes.restype = sz
     L.cl_conv_workspace_bytes.argtypes = [vp]
     L.cl_conv_resolved_method.argtypes = [vp]
+    L.cl_conv_operand_split.argtypes = [vp]
+    L.cl_conv_operand_split.restype = ctypes.c_char_p
     L.cl_conv_forward.argtypes = [vp, vp, vp, vp, vp]
     L.cl_conv_forward_nhwc.argtypes = [vp, vp, vp, vp, vp]
     L.cl_conv_forward_host.argtypes = [vp, vp, vp, vp]

@@ -37,6 +37,27 @@ int planes_for(cl_precision precision) {
     return classic ? 2 : kPlanesMixed;
 }
 
+// Operand format of a convolution plan.  fp32: the fp16 split (3 MMA slots per 16 channels, half
+// the operand bytes of the mixed split) for the implicit kn2row family wherever
+// it issues fewer MMAs than the mixed split (6 ceil(C/32) < 4 ceil(C/16): not for C = 16, 48),
+// otherwise the mixed split.  CLB_SPLIT=3xtf32 / mixed / 3xf16 forces a split (3xf16: where
+// the method supports it).
+int conv_planes_for(cl_precision precision, cl_method m, int C) {
+    static const int forced = [] {
+        const char* e = std::getenv("CLB_SPLIT");
+        if (!e) return 0;
+        if (std::strcmp(e, "3xtf32") == 0) return 2;
+        if (std::strcmp(e, "mixed") == 0) return kPlanesMixed;
+        if (std::strcmp(e, "3xf16") == 0) return kPlanesF16;
+        return 0;
+    }();
+    if (precision != CL_PREC_FP32) return planes_for(precision);
+    if (forced == 2 || forced == kPlanesMixed) return forced;
+    const bool implicit = m == CL_METHOD_KN2ROW || m == CL_METHOD_CONV1X1 || m == CL_METHOD_KN2ROW_ACC;
+    if (implicit && (forced == kPlanesF16 || 6 * ((C + 31) / 32) < 4 * ((C + 15) / 16))) return kPlanesF16;
+    return kPlanesMixed;
+}
+
 cl_status fail(cl_status s, const std::string& msg) {
     g_err = msg;
     return s;
@@ -96,6 +117,8 @@ struct cl_plan {
     int bn = 0;
     float* wpack = nullptr;
     size_t wpack_bytes = 0;
+    // fp16 split: exponent slots [ew, ex], the absmax pass's counter and partials (device)
+    int* scale = nullptr;
     float* wraw = nullptr;     // direct-gpu: MKKC fp32 weights as given
     // direct-gpu, 3 -> 16/32/64 channels 3x3: host weights [c][i][j][m] passed as a kernel
     // parameter (constant-bank FFMA operands).  Only filled by cl_conv_set_weights_host (the host
@@ -224,6 +247,7 @@ Operand tiled(const void* ptr, long long rows, int taps, int kp, int planes) {
 
 TcParams base_params(const cl_plan* p) {
     TcParams t{};
+    t.sexp = p->planes == kPlanesF16 ? p->scale : nullptr;
     t.ksize = p->d.k;
     t.P = p->P;
     t.Q = p->Q;
@@ -376,6 +400,10 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         case CL_METHOD_CONV1X1:
         case CL_METHOD_KN2ROW_ACC: {
             void* xs = wsf;
+            if (p->planes == kPlanesF16) {   // the input's exponent shift (max|x|) ahead of its split
+                launch_absmax_exp(x, (long long)d.n * d.c * d.h * d.w, p->scale, p->scale + 1, s);
+                ++p->launches;
+            }
             if (p->padded_rows) {
                 // tap-shared mode: zero-padded NHWC rows; each stage loads ONE A box of 128+k-1
                 // rows per kernel row i and feeds its k taps through row-shifted descriptors
@@ -392,8 +420,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                     launch_split_tail(own_job, p->planes, s);   // the tiles the previous contraction left
                     ++p->launches;
                 } else {
-                    if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
-                    else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s);
+                    if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s, p->scale);
+                    else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s, p->scale);
                     ++p->launches;
                 }
                 Operand a = tiled(xs, grid_rows, 1, p->Cp, p->planes);
@@ -437,8 +465,8 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 break;
             }
             if (prepass_partial) launch_split_tail(own_job, p->planes, s);
-            else if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s);
-            else launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s);
+            else if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s, p->scale);
+            else launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s, p->scale);
             ++p->launches;
             Operand a = implicit_a(p, xs);
             a.n = d.n;
@@ -701,7 +729,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         p->requested = method;
         p->method = m;
         p->prec = precision;
-        p->planes = planes_for(precision);
+        p->planes = conv_planes_for(precision, m, d.c);
         p->device = device;
         p->Cp = round_up(d.c, k_granule(p->planes));
         p->Kp = round_up(d.k * d.k * d.c, k_granule(p->planes));
@@ -715,6 +743,16 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             throw Error(CL_ENOMEM, "packed-weight allocation failed");
         }
         if (m == CL_METHOD_DIRECT) p->wraw = p->wpack;
+        if (p->planes == kPlanesF16) {
+            const size_t sb = (size_t)(kScaleSlots + kAbsmaxBlocks) * sizeof(int);
+            if (cudaMalloc(&p->scale, sb) != cudaSuccess || cudaMemset(p->scale, 0, sb) != cudaSuccess) {
+                cudaGetLastError();
+                cudaFree(p->wpack);
+                cudaFree(p->scale);
+                delete p;
+                throw Error(CL_ENOMEM, "scale slot allocation failed");
+            }
+        }
         {
             // tap-shared (padded-row) mode for the implicit kernel: one A box per kernel row feeds
             // its k taps through row-shifted descriptors (k x fewer A TMA bytes per MMA).  Small-BN
@@ -771,7 +809,8 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             }();
             const long long grid_rows = (long long)d.n * (d.h + d.pad) * (d.w + d.pad);
             const bool many_tiles = grid_rows / (2LL * kTileM * pcg) >= 4LL * (num_sms() / pcg);
-            if (p->padded_rows && p->stack_k == 1 && p->planes == 4 && p->bn <= 128 && forced_msub != 1 &&
+            if (p->padded_rows && p->stack_k == 1 && (p->planes == kPlanesMixed || p->planes == kPlanesF16) &&
+                p->bn <= 128 && forced_msub != 1 &&
                 (forced_msub == 2 || many_tiles))
                 p->msub = 2;
         }
@@ -780,6 +819,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             cudaMemset(p->flags, 0, (kMaxGrid + 8) * sizeof(unsigned)) != cudaSuccess) {
             cudaGetLastError();
             cudaFree(p->wpack);
+            cudaFree(p->scale);
             delete p;
             throw Error(CL_ENOMEM, "flag allocation failed");
         }
@@ -800,8 +840,10 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
         else if (p->method == CL_METHOD_DIRECT) {
             CLB_CUDA(cudaMemcpyAsync(p->wpack, d_w, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
             p->wparam.clear();   // device weights: the kernels read p->wraw (stream-ordered, no host copy)
-        } else
-            launch_pack_weights(d_w, p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s, p->stack_k > 1);
+        } else {
+            if (p->planes == kPlanesF16) launch_absmax_exp(d_w, (long long)d.m * d.k * d.k * d.c, p->scale, p->scale, s);
+            launch_pack_weights(d_w, p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s, p->stack_k > 1, p->scale);
+        }
         p->weights_set = true;
         mark_done(p, s);
     });
@@ -826,8 +868,12 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
             p->wparam.clear();
             if (direct_param_shape(d.c, d.k, d.m, d.stride, p->Q)) pack_param_weights(p, h_w);
         }
-        else
-            launch_pack_weights(static_cast<float*>(dw), p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s, p->stack_k > 1);
+        else {
+            if (p->planes == kPlanesF16)
+                launch_absmax_exp(static_cast<float*>(dw), (long long)d.m * d.k * d.k * d.c, p->scale, p->scale, s);
+            launch_pack_weights(static_cast<float*>(dw), p->wpack, d.m, d.k, d.c, p->Cp, p->planes, s, p->stack_k > 1,
+                                p->scale);
+        }
         CLB_CUDA(cudaFreeAsync(dw, s));
         CLB_CUDA(cudaStreamSynchronize(s));
         p->weights_set = true;
@@ -845,6 +891,19 @@ cl_status cl_conv_output_dims(const cl_plan* p, int32_t* P, int32_t* Q) {
 size_t cl_conv_workspace_bytes(const cl_plan* p) { return p ? ws_bytes(p) : 0; }
 
 cl_method cl_conv_resolved_method(const cl_plan* p) { return p ? p->method : CL_METHOD_AUTO; }
+
+const char* cl_conv_operand_split(const cl_plan* p) {
+    if (!p) return "";
+    if (p->method == CL_METHOD_DIRECT) return "fp32-fma";
+    switch (p->planes) {
+        case 1: return "tf32";
+        case 2: return "3xtf32";
+        case kPlanesBf16: return "bf16";
+        case kPlanesMixed: return "mixed";
+        case kPlanesF16: return "3xf16";
+    }
+    return "";
+}
 
 cl_status cl_conv_forward(cl_plan* p, const float* d_x, float* d_y, void* d_ws, void* stream) {
     return guarded([&] {
@@ -1073,6 +1132,7 @@ void cl_conv_destroy(cl_plan* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     if (p->wpack) cudaFree(p->wpack);
+    if (p->scale) cudaFree(p->scale);
     if (p->flags) cudaFree(p->flags);
     if (p->own_ws) cudaFree(p->own_ws);
     if (p->host_x) cudaFree(p->host_x);

@@ -34,9 +34,17 @@ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 //   4 = fp32-faithful "2xTF32 + 2xBF16": per 16 channels [hi 16 fp32 | hi 16 bf16 | lo 16 bf16]
 //       -- hi*Hi in two tf32 MMAs (exact products), the cross terms hi*Lo and lo*Hi in one
 //       bf16 MMA each (K = 16 per MMA: 4 MMA slots per 16 channels instead of 6)
-// kPlanesBf16 = 3, kPlanesMixed = 4: split_tile.cuh (included through tc_conv.cuh)
-// hi|lo split formats: one 128-byte row unit per 16 channels
+//   5 = fp32-faithful fp16 split (implicit kn2row family): the operand is scaled by an exact power
+//       of two 2^e (input: from max|x| per forward; weights: from max|w| at set_weights) so its
+//       largest magnitude lies in [2^14, 2^15), then x = hi + lo with hi = fp16(x), lo = fp16(x - hi)
+//       (22 significant bits); per 32 channels one 128 B unit [hi fp16 32 | lo fp16 32].  D +=
+//       lo*Hi + hi*Lo + hi*Hi as kind::f16 K=16 MMAs (exact products): 3 MMA slots per 16 channels
+//       instead of 4, half the operand bytes; the epilogue multiplies by 2^-(ex + ew).
+// kPlanesBf16 = 3, kPlanesMixed = 4, kPlanesF16 = 5: split_tile.cuh (included through tc_conv.cuh)
+// hi|lo split formats with one 128-byte row unit per 16 channels (two words per channel)
 __host__ __device__ inline bool is_split(int planes) { return planes == 2 || planes == kPlanesMixed; }
+// fp32-faithful formats (chunked accumulation, rel-L2 <= 1e-5)
+__host__ __device__ inline bool is_faithful(int planes) { return is_split(planes) || planes == kPlanesF16; }
 // channel padding granularity of the split layout (one 128-byte row unit)
 inline int k_granule(int planes) { return is_split(planes) ? 16 : (planes == kPlanesBf16 ? 64 : 32); }
 inline int elem_bytes(int planes) { return planes == kPlanesBf16 ? 2 : 4; }
@@ -49,14 +57,22 @@ inline long long row_bytes(int planes, long long kp) { return row_elems(planes, 
 // ([hi 16 fp32 | bf16 hi 16 | bf16 lo 16] mixed, [hi 16 | lo 16] 3xTF32; row = 2*k_pad words);
 // TF32 -> hi only (row = k_pad words, k_pad % 32 == 0); BF16 -> bf16 (k_pad % 64 == 0).
 // x NCHW fp32 -> xs[n][h][w][row] (hi = rna_tf32(x), lo = x - hi; zero for c >= C)
+// sexp (fp16 split only): the plan's exponent slots [ew, ex]; the split reads ex (written by
+// launch_absmax_exp over the same input just before)
 void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
-                               cudaStream_t s);
+                               cudaStream_t s, const int* sexp = nullptr);
 // same, into the zero-padded image [n][H+2pad][W+2pad][row] (tap-shared kernel mode)
 // NHWC input (channels last) -> split rows; pad > 0 writes the zero-padded grid (tap-shared mode)
 void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
-                       cudaStream_t s);
+                       cudaStream_t s, const int* sexp = nullptr);
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
-                                 cudaStream_t s);
+                                 cudaStream_t s, const int* sexp = nullptr);
+// fp16 split scale: exponent e with max|x| * 2^e in [2^14, 2^15) (0 for an all-zero or non-finite
+// tensor; in [-113, 163] otherwise) written to *out_exp.  `slots` = the plan's scale buffer (partials +
+// completion counter, self-resetting).  Stream-ordered, graph-capturable.
+constexpr int kScaleSlots = 8;          // [0] ew, [1] ex, [2] counter, ... then the partial maxima
+constexpr int kAbsmaxBlocks = 1024;
+void launch_absmax_exp(const float* x, long long n, int* slots, int* out_exp, cudaStream_t s);
 // the same conversion as a tile job (chained mode) and the tail launch that finishes its tiles
 // left by the previous contraction's converter warps (then resets the job's counter)
 SplitJob make_split_job(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp);
@@ -67,7 +83,7 @@ void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, 
 void launch_transpose_split(const float* b, void* bs, int K, int cols, int Kp, int planes, cudaStream_t s);
 // w MKKC -> wp[tap][M][planes][Cp], or (stacked) wp[i][M][j][planes][Cp]
 void launch_pack_weights(const float* w, void* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s,
-                         bool stacked = false);
+                         bool stacked = false, const int* sexp = nullptr);
 // x NCHW -> patches[n p q][planes][Kp], K index (i*k+j)*C + c  (conv_im2.cpp:19-54 order)
 void launch_im2col_split(const float* x, void* pm, int N, int C, int H, int W, int k, int pad, int stride,
                          int P, int Q, int Kp, int planes, cudaStream_t s);

@@ -15,10 +15,20 @@ namespace clb {
 // 16-channel block ([hi fp32 | bf16 hi | bf16 lo] mixed, [hi | lo] fp32 for 3xTF32) so each
 // 128-byte TMA row carries both halves of 16 channels; TF32 rows hold hi only.
 // `base` = first element of the row (fp32 words, or bf16 elements for the BF16 mode).
-__device__ __forceinline__ void store_split(void* dstv, long long base, int c, int kp, int planes, float v) {
+__device__ __forceinline__ void store_split(void* dstv, long long base, int c, int kp, int planes, float v,
+                                            Pow2 scale = Pow2{1.0f, 1.0f}) {
     (void)kp;
     if (planes == kPlanesBf16) {
         reinterpret_cast<__nv_bfloat16*>(dstv)[base + c] = __float2bfloat16_rn(v);
+        return;
+    }
+    if (planes == kPlanesF16) {
+        // unit = [hi fp16 32 | lo fp16 32] of the scaled value (32 words per 32 channels)
+        const float xs = apply_pow2(v, scale);
+        const __half hi = __float2half_rn(xs);
+        __half* h = reinterpret_cast<__half*>(static_cast<float*>(dstv) + base + ((c >> 5) << 5));
+        h[c & 31] = hi;
+        h[32 + (c & 31)] = __float2half_rn(xs - __half2float(hi));
         return;
     }
     float* dst = static_cast<float*>(dstv);
@@ -49,16 +59,28 @@ __device__ __forceinline__ long long rowel(int planes, long long kp) { return is
 // hi words for TF32), written by a warp as full 128-byte lines (lane = word).
 // grid (ceil(HW/128), ceil(Cp/32), N)
 // (tile body, FastDiv: split_tile.cuh)
+// fp16 split: a 1-D grid walked in REVERSE (tile t = total - 1 - blockIdx.x, channel blocks of a
+// pixel block adjacent): the absmax pass just streamed x front to back, so the last images are
+// the ones still in L2 -- converting them first turns the second read of x into L2 hits for
+// inputs up to about the L2 size.
 template <int PLANES>
 __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xsv,
                                                                  int N, int C, int HW, int Cp, int H, int W, int Wp,
-                                                                 int pad, FastDiv hwd, FastDiv wpd) {
+                                                                 int pad, FastDiv hwd, FastDiv wpd, const int* sexp) {
     // launched as a programmatic dependent of the previous kernel in the stream (typically the
     // previous layer's contraction, whose output x is): nothing is touched before it completes
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ SplitSmem<PLANES> sm;
-    split_tile<PLANES>(x, xsv, N, C, HW, Cp, H, W, Wp, pad, hwd, wpd, (int)blockIdx.x, (int)blockIdx.y,
-                              (int)threadIdx.x, sm);
+    int bx = (int)blockIdx.x, by = (int)blockIdx.y;
+    Pow2 scale{1.0f, 1.0f};
+    if constexpr (PLANES == kPlanesF16) {
+        const int nty = (Cp + 31) / 32;
+        const int t = (int)gridDim.x - 1 - (int)blockIdx.x;
+        bx = t / nty;
+        by = t - bx * nty;
+        scale = pow2_factors(__ldg(sexp + 1));
+    }
+    split_tile<PLANES>(x, xsv, N, C, HW, Cp, H, W, Wp, pad, hwd, wpd, bx, by, (int)threadIdx.x, sm, scale);
     // let a programmatically dependent consumer (the tcgen05 kernel) start its prologue;
     // its griddepcontrol.wait still waits for this grid's completion and memory flush
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -66,6 +88,7 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_split_kernel(const float* __
 
 template <typename... Args>
 static void launch_split_kernel(int planes, dim3 grid, cudaStream_t s, Args... args) {
+    if (planes == kPlanesF16) grid = dim3(grid.x * grid.y, 1, 1);   // reversed linear tile order
     // Programmatic dependent launch: the prepass's launch and CTA ramp overlap the tail of the
     // previous kernel in the stream (the previous layer's contraction); its griddepcontrol.wait
     // keeps every memory access after that kernel's completion.  CLB_PDL_PREPASS=0 disables.
@@ -84,15 +107,17 @@ static void launch_split_kernel(int planes, dim3 grid, cudaStream_t s, Args... a
         case 1: CLB_CUDA(cudaLaunchKernelEx(&cfg, nchw_to_nhwc_split_kernel<1>, args...)); break;
         case 2: CLB_CUDA(cudaLaunchKernelEx(&cfg, nchw_to_nhwc_split_kernel<2>, args...)); break;
         case kPlanesBf16: CLB_CUDA(cudaLaunchKernelEx(&cfg, nchw_to_nhwc_split_kernel<kPlanesBf16>, args...)); break;
+        case kPlanesF16: CLB_CUDA(cudaLaunchKernelEx(&cfg, nchw_to_nhwc_split_kernel<kPlanesF16>, args...)); break;
         default: CLB_CUDA(cudaLaunchKernelEx(&cfg, nchw_to_nhwc_split_kernel<kPlanesMixed>, args...));
     }
 }
 
 void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, int Cp, int planes,
-                               cudaStream_t s) {
+                               cudaStream_t s, const int* sexp) {
+    if (planes == kPlanesF16 && !sexp) throw Error(6, "fp16 split prepass without its exponent slots");
     dim3 grid((unsigned)(((long long)N * HW + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
     launch_split_kernel(planes, grid, s, x, xs, N, C, HW, Cp, 1, HW, HW, 0, make_fastdiv((uint32_t)HW),
-                        make_fastdiv((uint32_t)HW));
+                        make_fastdiv((uint32_t)HW), sexp);
     CLB_CUDA(cudaGetLastError());
 }
 
@@ -160,11 +185,12 @@ void launch_split_tail(const SplitJob& j, int planes, cudaStream_t s) {
 }
 
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, const int* sexp) {
+    if (planes == kPlanesF16 && !sexp) throw Error(6, "fp16 split prepass without its exponent slots");
     const int Hp = H + pad, Wp = W + pad;
     dim3 grid((unsigned)(((long long)N * Hp * Wp + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
     launch_split_kernel(planes, grid, s, x, xs, N, C, Hp * Wp, Cp, H, W, Wp, pad, make_fastdiv((uint32_t)(Hp * Wp)),
-                        make_fastdiv((uint32_t)Wp));
+                        make_fastdiv((uint32_t)Wp), sexp);
     CLB_CUDA(cudaGetLastError());
 }
 
@@ -177,7 +203,7 @@ void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, 
 // issue slots than the bytes it moves.
 __global__ void __launch_bounds__(256) nhwc_split_kernel(const float* __restrict__ x, void* __restrict__ xs,
                                                          uint32_t total, FastDiv q4d, FastDiv pixd, FastDiv wpd, int C,
-                                                         int Cp, int planes, int H, int W, int pad) {
+                                                         int Cp, int planes, int H, int W, int pad, const int* sexp) {
     const uint32_t i = blockIdx.x * 256u + threadIdx.x;
     if (i >= total) return;
     const uint32_t r = fdiv(i, q4d);                 // output row
@@ -211,6 +237,17 @@ __global__ void __launch_bounds__(256) nhwc_split_kernel(const float* __restrict
         *reinterpret_cast<uint2*>(dst) = packed;
         return;
     }
+    if (planes == kPlanesF16) {                       // [hi fp16 32 | lo fp16 32] per 32 channels
+        const Pow2 sc = pow2_factors(__ldg(sexp + 1));
+        uint32_t h01, l01, h23, l23;
+        f16_split2(apply_pow2(v[0], sc), apply_pow2(v[1], sc), h01, l01);
+        f16_split2(apply_pow2(v[2], sc), apply_pow2(v[3], sc), h23, l23);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(static_cast<float*>(xs) + (long long)r * Cp + ((c >> 5) << 5));
+        const int w = (c & 31) >> 1;                  // word of the channel pair within each half
+        *reinterpret_cast<uint2*>(dst + w) = make_uint2(h01, h23);
+        *reinterpret_cast<uint2*>(dst + 16 + w) = make_uint2(l01, l23);
+        return;
+    }
     float hi[4], lo[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -234,7 +271,8 @@ __global__ void __launch_bounds__(256) nhwc_split_kernel(const float* __restrict
 }
 
 void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
-                       cudaStream_t s) {
+                       cudaStream_t s, const int* sexp) {
+    if (planes == kPlanesF16 && !sexp) throw Error(6, "fp16 split prepass without its exponent slots");
     const int Hp = H + pad, Wp = W + pad;   // pad > 0: shared-padding grid (see above)
     const long long rows = (long long)N * Hp * Wp;
     const int q4 = Cp / 4;
@@ -243,8 +281,95 @@ void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int
     const FastDiv q4d = make_fastdiv((uint32_t)q4), pixd = make_fastdiv((uint32_t)(Hp * Wp)),
                   wpd = make_fastdiv((uint32_t)Wp);
     nhwc_split_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(x, xs, (uint32_t)total, q4d, pixd, wpd, C, Cp,
-                                                                      planes, H, W, pad);
+                                                                      planes, H, W, pad, sexp);
     CLB_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------- fp16 split exponent ----
+// max|x| over the tensor -> the power-of-2 shift of the fp16 split.  Each block reduces a
+// grid-stride share (float4 loads when aligned) to one partial; the last block to finish (a
+// completion counter) reduces the partials, writes the exponent and resets the counter, so the
+// slots need no memset between calls.  |x| as unsigned bits orders like the float (NaN above inf).
+__global__ void __launch_bounds__(256) absmax_exp_kernel(const float* __restrict__ x, long long n, int* slots,
+                                                         int* out_exp) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // x may be the previous kernel's output
+    unsigned* part = reinterpret_cast<unsigned*>(slots + kScaleSlots);
+    unsigned* counter = reinterpret_cast<unsigned*>(slots + 2);
+    unsigned m = 0;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+    auto fold4 = [&](const float4& v) {
+        m = max(max(m, __float_as_uint(v.x) & 0x7fffffffu), __float_as_uint(v.y) & 0x7fffffffu);
+        m = max(max(m, __float_as_uint(v.z) & 0x7fffffffu), __float_as_uint(v.w) & 0x7fffffffu);
+    };
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        // 8 independent 16-byte loads in flight per thread: HBM needs several MB in flight
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const long long n4 = n >> 2;
+        long long i = tid;
+        for (; i + 7 * nth < n4; i += 8 * nth) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(x4 + i + u * nth);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) fold4(v[u]);
+        }
+        for (; i < n4; i += nth) fold4(__ldg(x4 + i));
+        for (long long j = (n4 << 2) + tid; j < n; j += nth) m = max(m, __float_as_uint(__ldg(x + j)) & 0x7fffffffu);
+    } else {
+        for (long long i = tid; i < n; i += nth) m = max(m, __float_as_uint(__ldg(x + i)) & 0x7fffffffu);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ unsigned wm[8];
+    __shared__ bool last;
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) m = max(m, wm[w]);
+        part[blockIdx.x] = m;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        m = 0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += 256) m = max(m, __ldcg(part + b));
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < 8; ++w) m = max(m, wm[w]);
+            int e = 0;
+            if (m != 0 && m < 0x7f800000u) {
+                int ex;
+                frexpf(__uint_as_float(m), &ex);   // max = f 2^ex, f in [0.5, 1)
+                e = 15 - ex;                        // max 2^e in [2^14, 2^15): e in [-113, 163]
+                                                    // for every finite nonzero fp32 max
+            }
+            *out_exp = e;
+            *counter = 0u;
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+void launch_absmax_exp(const float* x, long long n, int* slots, int* out_exp, cudaStream_t s) {
+    int dev = 0, sms = 0;
+    CLB_CUDA(cudaGetDevice(&dev));
+    CLB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const long long want = (n / 4 + 2047) / 2048;   // >= 8 float4 per thread
+    const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, std::min(kAbsmaxBlocks, 4 * sms)));
+    static const bool pdl = !(getenv("CLB_PDL_PREPASS") && atoi(getenv("CLB_PDL_PREPASS")) == 0);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CLB_CUDA(cudaLaunchKernelEx(&cfg, absmax_exp_kernel, x, n, slots, out_exp));
 }
 
 // -------------------------------------------------------------------- row-wise split ----
@@ -296,8 +421,9 @@ void launch_transpose_split(const float* b, void* bs, int K, int cols, int Kp, i
 // kn2row_reorder_kernel (conv_kn2.cpp:28-39) fused with the split:
 //   wp[(i*k+j)][m][plane][c] = split(K[m][i][j][c])
 __global__ void pack_weights_kernel(const float* __restrict__ w, void* __restrict__ wp, int M, int k, int C,
-                                    int Cp, int planes, int stacked) {
+                                    int Cp, int planes, int stacked, const int* sexp) {
     const long long total = (long long)k * k * M * Cp;
+    const Pow2 scale = sexp ? pow2_factors(sexp[0]) : Pow2{1.0f, 1.0f};   // fp16 split: 2^ew
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         const int c = (int)(e % Cp);
@@ -308,15 +434,17 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, void* __restric
         // tap-major [t][m] rows, or tap-stacked [i][m][j] (the k taps of kernel row i as
         // adjacent columns of one output channel, tc_conv.cuh stack_k)
         const long long row = stacked ? ((long long)(t / k) * M + m) * k + (t % k) : tm;
-        store_split(wp, row * rowel(planes, Cp), c, Cp, planes, v);
+        store_split(wp, row * rowel(planes, Cp), c, Cp, planes, v, scale);
     }
 }
 
 void launch_pack_weights(const float* w, void* wp, int M, int k, int C, int Cp, int planes, cudaStream_t s,
-                         bool stacked) {
+                         bool stacked, const int* sexp) {
+    if (planes == kPlanesF16 && !sexp) throw Error(6, "fp16 split weights without their exponent slot");
     const long long total = (long long)k * k * M * Cp;
     const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-    pack_weights_kernel<<<blocks, 256, 0, s>>>(w, wp, M, k, C, Cp, planes, stacked ? 1 : 0);
+    pack_weights_kernel<<<blocks, 256, 0, s>>>(w, wp, M, k, C, Cp, planes, stacked ? 1 : 0,
+                                               planes == kPlanesF16 ? sexp : nullptr);
     CLB_CUDA(cudaGetLastError());
 }
 

@@ -358,6 +358,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N) {
            | ((M >> 4) << 24);    // m_dim
 }
 
+// Instruction descriptor: kind::f16 with fp16 A/B, K-major, fp32 accumulator, M x N.
+__host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N) {
+    return (1u << 4)              // c_format = F32 (a_format = b_format = 0: F16)
+           | ((N >> 3) << 17)     // n_dim
+           | ((M >> 4) << 24);    // m_dim
+}
+
 // Instruction descriptor: kind::tf32, A/B K-major, fp32 accumulator, M x N.
 __host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
     return (1u << 4)              // c_format = F32

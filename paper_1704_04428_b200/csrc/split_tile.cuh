@@ -5,11 +5,40 @@
 
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace clb {
 
 constexpr int kPlanesBf16 = 3;    // precision codes, see internal.hpp
 constexpr int kPlanesMixed = 4;
+constexpr int kPlanesF16 = 5;     // fp32-faithful fp16 split of the power-of-2 scaled operand
+
+// 2^e as a float, e in [-126, 127] (exact; the fp16 split's scale and descale factors)
+__host__ __device__ __forceinline__ float exp2i(int e) {
+    union { uint32_t u; float f; } v;
+    v.u = (uint32_t)(127 + e) << 23;
+    return v.f;
+}
+
+// x * 2^e for any e in [-252, 254] as two exact power-of-2 factors (a single float factor stops
+// at 2^127: subnormal inputs need shifts up to 2^164)
+struct Pow2 {
+    float a, b;
+};
+__host__ __device__ __forceinline__ Pow2 pow2_factors(int e) {
+    const int e1 = e < -126 ? -126 : (e > 127 ? 127 : e);
+    return Pow2{exp2i(e1), exp2i(e - e1)};
+}
+__device__ __forceinline__ float apply_pow2(float v, const Pow2& f) { return (v * f.a) * f.b; }
+
+// fp16 split of one scaled value pair: hi = fp16(x), lo = fp16(x - hi) (x - hi is exact in fp32),
+// packed as the two halves of a 32-bit word each (channel c in the low half, c + 1 in the high)
+__device__ __forceinline__ void f16_split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const __half ha = __float2half_rn(a), hb = __float2half_rn(b);
+    const __half la = __float2half_rn(a - __half2float(ha)), lb = __float2half_rn(b - __half2float(hb));
+    hi = (uint32_t)__half_as_ushort(ha) | ((uint32_t)__half_as_ushort(hb) << 16);
+    lo = (uint32_t)__half_as_ushort(la) | ((uint32_t)__half_as_ushort(lb) << 16);
+}
 
 __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;
@@ -64,24 +93,27 @@ struct SplitJob {
     unsigned* counter;
 };
 
-// tile staging: hi (or raw for bf16 rows), 3xTF32 lo, mixed-format bf16(hi) / bf16(lo) pairs
+// tile staging: hi (or raw for bf16 rows), 3xTF32 lo, mixed-format bf16(hi) / bf16(lo) pairs,
+// fp16-split hi / lo pairs
 template <int PLANES>
 struct SplitSmem {
-    float hi[kSplitPx][33];
+    float hi[PLANES == kPlanesF16 ? 1 : kSplitPx][33];
     float lo[PLANES == 2 ? kSplitPx : 1][33];
-    uint32_t bh[PLANES == kPlanesMixed ? kSplitPx : 1][17];
-    uint32_t bl[PLANES == kPlanesMixed ? kSplitPx : 1][17];
+    uint32_t bh[(PLANES == kPlanesMixed || PLANES == kPlanesF16) ? kSplitPx : 1][17];
+    uint32_t bl[(PLANES == kPlanesMixed || PLANES == kPlanesF16) ? kSplitPx : 1][17];
 };
 
 // Templated on the operand format so every element is converted exactly once (in the load
 // phase, into shared tiles) and the write phase is plain 32-bit copies: converting per output
 // word made the mixed format's prepass issue-bound (IPC 3.2, DRAM 21 %, ncu on GoogLeNet 1x1).
 // Tile (bx, by) = pixels [128 bx, 128 bx + 128) flattened over (image, pixel) x channels
-// [32 by, 32 by + 32); tid in [0, 256).
+// [32 by, 32 by + 32); tid in [0, 256).  `scale` (fp16 split only) = 2^ex, the input's exponent
+// shift (exact, two factors).
 template <int PLANES>
 __device__ __forceinline__ void split_tile(const float* __restrict__ x, void* __restrict__ xsv, int N, int C, int HW,
                                            int Cp, int H, int W, int Wp, int pad, const FastDiv& hwd,
-                                           const FastDiv& wpd, int bx, int by, int tid, SplitSmem<PLANES>& sm) {
+                                           const FastDiv& wpd, int bx, int by, int tid, SplitSmem<PLANES>& sm,
+                                           Pow2 scale = Pow2{1.0f, 1.0f}) {
     constexpr bool kSplit = PLANES == 2 || PLANES == kPlanesMixed;
     // pixels are flattened over (image, pixel): a tile may straddle two images, so small maps
     // (13 x 13 = 169 pixels) do not leave most of a second 128-pixel tile idle
@@ -126,6 +158,9 @@ __device__ __forceinline__ void split_tile(const float* __restrict__ x, void* __
             if (PLANES == kPlanesBf16) {
                 sm.hi[px][cc] = v[r][h];
                 sm.hi[px][cc + 1] = v[r + 1][h];
+            } else if (PLANES == kPlanesF16) {
+                f16_split2(apply_pow2(v[r][h], scale), apply_pow2(v[r + 1][h], scale), sm.bh[px][cc >> 1],
+                           sm.bl[px][cc >> 1]);
             } else {
                 const float h0 = tf32_rna(v[r][h]), h1 = tf32_rna(v[r + 1][h]);
                 sm.hi[px][cc] = h0;
@@ -173,6 +208,8 @@ __device__ __forceinline__ void split_tile(const float* __restrict__ x, void* __
         } else if (PLANES == kPlanesMixed) {             // unit u = [hi 16 fp32 | bf16 hi 16 | bf16 lo 16]
             srow = w < 16 ? reinterpret_cast<const uint32_t*>(&sm.hi[pp][u * 16 + w])
                           : (w < 24 ? &sm.bh[pp][u * 8 + (w - 16)] : &sm.bl[pp][u * 8 + (w - 24)]);
+        } else if (PLANES == kPlanesF16) {               // the tile's unit = [hi fp16 32 | lo fp16 32]
+            srow = o < 16 ? &sm.bh[pp][o] : &sm.bl[pp][o - 16];
         } else {
             srow = reinterpret_cast<const uint32_t*>(&sm.hi[pp][o]);
         }

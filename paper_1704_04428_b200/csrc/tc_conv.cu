@@ -163,9 +163,9 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     }
     if (p.msub <= 1) {
         p.msub = 1;
-    } else if (p.msub != 2 || p.stack_k != 1 || a.mode != LOAD_TILED || p.tps < 2 || a.planes != 4 ||
-               p.bn % 32 != 0) {
-        throw Error(6, "two-sub-tile mode: mixed split, tap-shared tiled A, N a multiple of 16 per sub-tile");
+    } else if (p.msub != 2 || p.stack_k != 1 || a.mode != LOAD_TILED || p.tps < 2 ||
+               (a.planes != kPlanesMixed && a.planes != kPlanesF16) || p.bn % 32 != 0) {
+        throw Error(6, "two-sub-tile mode: mixed / fp16 split, tap-shared tiled A, N a multiple of 16 per sub-tile");
     }
     const int mma_n = p.bn / p.msub;
     CUtensorMap ma, mb;
@@ -175,6 +175,8 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     encode_operand_map(&ma, a, p.stack_k > 1 ? 32 : tc_a_box_rows(p.tps), p.stack_k > 1 ? 4 : 1);
     encode_operand_map(&mb, b, mma_n / cg, p.tps);
     p.planes = a.planes;
+    if (p.planes == kPlanesF16 && !p.sexp) throw Error(6, "fp16 split contraction without its exponent slots");
+    if (p.planes != kPlanesF16) p.sexp = nullptr;
     p.row_elems = unit;
     p.kblocks = a.kw / unit;
     p.a_mode = a.mode;
@@ -190,7 +192,9 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     // granularity: 16 iterations keep the epilogue's fold rate below the MMA's (4 had the MMA
     // waiting on TMEM 11-25 % of the time, CLB_TRACE).
     if (p.chunk_iters <= 0) {
-        if (is_split(p.planes)) {
+        if (p.planes == kPlanesF16) {   // 32 channels per k-iteration and tap
+            p.chunk_iters = kChunkK / (32 * p.tps);
+        } else if (is_split(p.planes)) {
             p.chunk_iters = kChunkK / (16 * p.tps);
         } else {
             p.chunk_iters = kFastChunkIters / p.tps;

@@ -55,8 +55,8 @@ constexpr int kRowBytes = kRowWords * 4;
 constexpr int kThreads = 512;             // 4 control warps + 8 epilogue warps + 4 converter warps
 constexpr int kEpiThreads = 256;
 constexpr int kConvWarps = 4;             // converter warpgroup (warps 12..15): the chained prepass
-// registers per thread after setmaxnreg: 4 x 32 x 56 + 8 x 32 x 200 + 4 x 32 x 56 = 65536
-constexpr int kRegsControl = 56, kRegsEpi = 200, kRegsConv = 56;
+// registers per thread after setmaxnreg: 4 x 32 x 64 + 8 x 32 x 200 + 4 x 32 x 48 = 65536
+constexpr int kRegsControl = 64, kRegsEpi = 200, kRegsConv = 48;
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kChunkK = 192;          // fp32-faithful splits: K-elements per TMEM accumulation chunk
 constexpr int kBarrierBytes = 512;
@@ -117,6 +117,8 @@ struct TcParams {
     int msub;                  // 1 = off
     int row_step;              // output rows per CTA tile (128, or 4 (33 - k) when stacked)
     int accumulate;            // out += D (accumulating shifted-GEMM variant)
+    const int* sexp;           // fp16 split: the operands' exponent shifts [ew, ex] (device); the
+                               // epilogue multiplies D by 2^-(ew + ex).  Null for the other formats.
     float* out;
     long long ld;              // EPI_ROWMAJOR leading dimension
     int out_channels;          // EPI_NCHW: channel count of the output tensor
@@ -594,20 +596,20 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // The whole warp runs the loop (loop state is warp-uniform, so it lives in uniform
         // registers); one elected lane issues the MMAs and the commits that track them.
         if (leader) {
-            const uint32_t idesc = planes == 3 ? idesc_bf16((uint32_t)tile_m, (uint32_t)mma_n)
-                                               : idesc_tf32((uint32_t)tile_m, (uint32_t)mma_n);
-            const uint32_t idesc16 = idesc_bf16((uint32_t)tile_m, (uint32_t)mma_n);   // mixed mode corrections
-            auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
-                if constexpr (CG == 2) mma_tf32_ss_2sm(d, a, b, idesc, acc);
-                else mma_tf32_ss(d, a, b, idesc, acc);
+            // one live instruction descriptor (fp16 A/B); each MMA flavour ORs in its format code
+            const uint32_t idesc0 = idesc_f16((uint32_t)tile_m, (uint32_t)mma_n);
+            constexpr uint32_t kFmtTf32 = (2u << 7) | (2u << 10), kFmtBf16 = (1u << 7) | (1u << 10);
+            auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {     // kind::tf32
+                if constexpr (CG == 2) mma_tf32_ss_2sm(d, a, b, idesc0 | kFmtTf32, acc);
+                else mma_tf32_ss(d, a, b, idesc0 | kFmtTf32, acc);
             };
-            auto mma16 = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {   // kind::f16 (bf16)
-                if constexpr (CG == 2) mma_bf16_ss_2sm(d, a, b, idesc, acc);
-                else mma_bf16_ss(d, a, b, idesc, acc);
+            auto mma16 = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {   // kind::f16, bf16 operands
+                if constexpr (CG == 2) mma_bf16_ss_2sm(d, a, b, idesc0 | kFmtBf16, acc);
+                else mma_bf16_ss(d, a, b, idesc0 | kFmtBf16, acc);
             };
-            auto mma16x = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {   // bf16 corrections (mode 4)
-                if constexpr (CG == 2) mma_bf16_ss_2sm(d, a, b, idesc16, acc);
-                else mma_bf16_ss(d, a, b, idesc16, acc);
+            auto mmah = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {    // kind::f16, fp16 operands
+                if constexpr (CG == 2) mma_bf16_ss_2sm(d, a, b, idesc0, acc);
+                else mma_bf16_ss(d, a, b, idesc0, acc);
             };
             auto commit = [&](uint64_t* bar) {
                 if constexpr (CG == 2) mma_commit_2sm_mc(bar, (uint16_t)0x3);
@@ -660,10 +662,20 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             // row = [hi 16 fp32 | bf16(hi) 16 | bf16(lo) 16]: the cross terms
                             // lo*Hi and hi*Lo as one bf16 K=16 MMA each (bytes 96 / 64 of A
                             // with 64 / 96 of B), then hi*Hi as two exact tf32 K=8 MMAs
-                            mma16x(d_tmem, da + 6, db + 4, first);
-                            mma16x(d_tmem, da + 4, db + 6, 1u);
+                            mma16(d_tmem, da + 6, db + 4, first);
+                            mma16(d_tmem, da + 4, db + 6, 1u);
                             mma(d_tmem, da, db, 1u);
                             mma(d_tmem, da + 2, db + 2, 1u);
+                        } else if constexpr (PL == 5) {
+                            // row = [hi 32 fp16 | lo 32 fp16] of the scaled input: k-step s (16
+                            // fp16 = 32 B = 2 desc units) of hi at +2 s, of lo at +4 + 2 s; the
+                            // cross terms first, then hi*Hi (all products exact in fp32)
+                            mmah(d_tmem, da + 4, db, first);
+                            mmah(d_tmem, da, db + 4, 1u);
+                            mmah(d_tmem, da, db, 1u);
+                            mmah(d_tmem, da + 6, db + 2, 1u);
+                            mmah(d_tmem, da + 2, db + 6, 1u);
+                            mmah(d_tmem, da + 2, db + 2, 1u);
                         } else if constexpr (PL == 3) {
                             // 64 bf16 per row: 4 k-steps of 16 elements (32 B = 2 desc units)
                             mma16(d_tmem, da, db, first);
@@ -731,6 +743,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             using I2 = std::integral_constant<int, 2>;
             using I3 = std::integral_constant<int, 3>;
             using I4 = std::integral_constant<int, 4>;
+            using I5 = std::integral_constant<int, 5>;
             using BT = std::true_type;
             using BF = std::false_type;
             // (two-sub-tile mode: mixed split, tap-shared stages only -- launch_tc enforces it)
@@ -738,6 +751,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 if (tps == 1) run(I4{}, BT{}, I1{});
                 else if (msub == 2) run(I4{}, BF{}, I2{});
                 else run(I4{}, BF{}, I1{});
+            } else if (planes == kPlanesF16) {
+                if (tps == 1) run(I5{}, BT{}, I1{});
+                else if (msub == 2) run(I5{}, BF{}, I2{});
+                else run(I5{}, BF{}, I1{});
             } else if (planes == 2) {
                 if (tps == 1) run(I2{}, BT{}, I1{}); else run(I2{}, BF{}, I1{});
             } else if (planes == 3) {
@@ -784,6 +801,14 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const int hcols = bn >> 1;                   // multiple of 8 (bn % 16 == 0)
         const int cbase = half * hcols;
         const int trow = quad * 32 + lane;           // row within this CTA's 128 rows
+        // fp16 split: D carries the operands' power-of-2 scales; 2^-(ew + ex) as two exact factors
+        // (each a normal float; below 2^-252 every product underflows fp32 anyway), applied once
+        // per finished tile (published partials stay scaled)
+        Pow2 ds{1.0f, 1.0f};
+        if (p.sexp) {
+            const int d = -(p.sexp[0] + p.sexp[1]);
+            ds = pow2_factors(d < -252 ? -252 : d);
+        }
         uint32_t lg = 0;
         long long w_tfull = 0, w_store = 0, w_fix = 0;
         unsigned long long n_parts = 0, t_folded = 0, t_pub = 0, t_acq = 0, t_added = 0, t_stored = 0;
@@ -925,6 +950,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 col0 = nt * (bn / p.stack_k) + half * g;
                 ncol = min(g, p.out_channels - col0);
                 row_ok = lane < 33 - p.stack_k;
+            }
+            if (p.sexp) {
+#pragma unroll
+                for (int j = 0; j < 128; ++j) sum[j] = apply_pow2(sum[j], ds);
             }
             // ---- store the finished tile ----
             const long long t_st = TRACE ? clock64() : 0;

@@ -25,9 +25,12 @@ from .methods import ConvPlan, LayerConfig, footprint
 CSV_HEADER = ("layer,method,runs,mean_s,min_s,stddev_s,input_bytes,kernel_bytes,intermediate_bytes,"
               "output_bytes")
 GPU_COLUMNS = "batch,pad,precision,gpus,eff_tflops,pct_peak"
-# fp32-faithful peak: MEASURED_PEAKS.json bf16 burst / 2 (tf32) x 1/2 (mixed split, 4 MMA slots per
-# 16 K-elements; the classic CLB_SPLIT=3xtf32 split would be x 1/3)
-PEAK_3XTF32_TFLOPS = 1667.0 / 2 / 2
+# tensor-core peak of each operand format (pct_peak column): bf16 burst (MEASURED_PEAKS.json
+# figure) / 3 for the fp16 split (3 f16 MMAs per product), / 4 for the mixed split (4 tf32-MMA
+# slots per 16 K-elements), / 6 for the classic 3xTF32 split; x 1/2 tf32, x 1 bf16 fast modes
+_BF16_PEAK = 1667.0
+SPLIT_PEAK_TFLOPS = {"3xf16": _BF16_PEAK / 3, "mixed": _BF16_PEAK / 4, "3xtf32": _BF16_PEAK / 6,
+                     "tf32": _BF16_PEAK / 2, "bf16": _BF16_PEAK, "fp32-fma": _BF16_PEAK / 4}
 
 
 @dataclass
@@ -99,13 +102,14 @@ def benchmark(layer: LayerConfig, method: str = "auto", runs: int = 5, seed: int
             if r == 0 and checksum and fnv1a(y) != first:      # bench.cpp:126-128
                 raise RuntimeError(f"benchmark: nondeterministic output for layer '{layer.name}', method {method}")
         resolved = plan.method
+        split = plan.split
     mean = sum(samples) / runs
     std = math.sqrt(sum((s - mean) ** 2 for s in samples) / runs)   # population stddev
     fp = footprint(layer, resolved)
     tf = layer.flops() / min(samples) / 1e12
     return BenchResult(layer.name, resolved, runs, mean, min(samples), std, fp["input_bytes"], fp["kernel_bytes"],
                        fp["intermediate_bytes"], fp["output_bytes"], layer.batch, layer.pad, precision, 1, tf,
-                       100.0 * tf / PEAK_3XTF32_TFLOPS, samples, first)
+                       100.0 * tf / SPLIT_PEAK_TFLOPS.get(split, _BF16_PEAK / 4), samples, first)
 
 
 def _fmt(v: float) -> str:

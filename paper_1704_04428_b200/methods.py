@@ -168,6 +168,8 @@ class ConvPlan:
         _lib.check(L.cl_conv_output_dims(h, ctypes.byref(p), ctypes.byref(q)))
         self.out_hw = (p.value, q.value)
         self.method = _lib.METHOD_NAMES[L.cl_conv_resolved_method(h)]
+        # operand format: 3xf16 / mixed / 3xtf32 (fp32-faithful), tf32 / bf16, fp32-fma (direct)
+        self.split = L.cl_conv_operand_split(h).decode()
 
     # -- lifetime ------------------------------------------------------------------------
     def close(self):

@@ -9,9 +9,11 @@ conv_mcmk_sum (oracle/oracle.c, pinned bitwise to the reference).  Inputs come f
 device generator (bit-identical to the reference's, tested in test_gpu_parity.py), one stream
 per layer over the whole N*C*H*W batch.
 
-  fp32-faithful (default mixed split): rel-L2 <= 1e-5 and max|d|/max|ref| <= 1e-4
-  fp32-faithful classic 3xTF32 (CLB_SPLIT=3xtf32, in a subprocess): same bounds, plus the
-      bitwise delta-kernel identity of conv_kn2_test.cpp:148-152 for every GPU method
+  fp32-faithful (default: the fp16 split of power-of-2 scaled operands for the implicit layers,
+      the mixed split where C = 16 / 48): rel-L2 <= 1e-5 and max|d|/max|ref| <= 1e-4
+  fp32-faithful mixed split and classic 3xTF32 on every layer (CLB_SPLIT=mixed / 3xtf32, in a
+      subprocess): same bounds, plus (3xTF32) the bitwise delta-kernel identity of
+      conv_kn2_test.cpp:148-152 for every GPU method
   TF32 / BF16 fast modes: rel-L2 <= 1e-2 (north star), reported separately
 """
 from __future__ import annotations
@@ -59,6 +61,7 @@ def seed_for(layer) -> int:
 
 
 _REFS = {}
+SPLITS = {}   # (layer, batch, precision) -> operand format the plan used
 
 
 def oracle_ref(oracle, layer, x_host_picks, w_host):
@@ -84,6 +87,7 @@ def run_layer(layer, precision="fp32"):
         y = plan.forward(x)
         torch.cuda.synchronize()
         method = plan.method
+        SPLITS[(layer.name, layer.batch, precision)] = plan.split
     picks = picks_for(layer.batch, seed)
     idx = torch.tensor(picks, device=x.device)
     out = (picks, x.index_select(0, idx).cpu().numpy(), w.cpu().numpy(), y.index_select(0, idx).cpu().numpy(), method)
@@ -145,21 +149,24 @@ for method in clb.GPU_METHODS:
         continue
     y = clb.run_method(method, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()).cpu().numpy()
     exact[method] = bool(np.array_equal(y, x))
-print(json.dumps({"methods": out, "delta_exact": exact}))
+print(json.dumps({"methods": out, "delta_exact": exact, "splits": sorted(set(T.SPLITS.values()))}))
 '''
 
 
-def test_full_batch_classic_3xtf32_split(oracle, gpu, tmp_path):
-    """CLB_SPLIT=3xtf32 (the north star's named split, read once per process): every layer at
-    full batch within the fp32-faithful bounds, and the bitwise delta-kernel identity that the
-    default mixed split relaxes to 2^-18 (conv_kn2_test.cpp:148-152)."""
+@pytest.mark.parametrize("split", ["3xtf32", "mixed"])
+def test_full_batch_forced_split(oracle, gpu, tmp_path, split):
+    """CLB_SPLIT=3xtf32 (the north star's named split) and CLB_SPLIT=mixed (read once per
+    process): every layer at full batch within the fp32-faithful bounds; for 3xTF32 also the
+    bitwise delta-kernel identity that the other splits relax to 2^-18 (conv_kn2_test.cpp:148-152)."""
     script = tmp_path / "classic.py"
     script.write_text(_CLASSIC_SCRIPT)
     r = subprocess.run([sys.executable, str(script), str(ROOT), str(tmp_path)], capture_output=True, text=True,
-                       timeout=1800, env=dict(os.environ, CLB_SPLIT="3xtf32"), cwd=str(ROOT))
+                       timeout=1800, env=dict(os.environ, CLB_SPLIT=split), cwd=str(ROOT))
     assert r.returncode == 0, r.stderr[-3000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
-    assert all(res["delta_exact"].values()), res["delta_exact"]
+    assert set(res["splits"]) <= {split, "fp32-fma"}, res["splits"]
+    if split == "3xtf32":
+        assert all(res["delta_exact"].values()), res["delta_exact"]
     import torch
     from paper_1704_04428_b200 import rng
     for _, layer in CASES:
@@ -173,7 +180,7 @@ def test_full_batch_classic_3xtf32_split(oracle, gpu, tmp_path):
             oracle_ref(oracle, layer, x.index_select(0, idx).cpu().numpy(), w.cpu().numpy())
             del x
         m = oracle.parity_metrics(yh, _REFS[key])
-        assert m["rel_l2"] <= FP32_L2 and m["max_rel"] <= FP32_MAX, (layer.name, "3xtf32", m)
+        assert m["rel_l2"] <= FP32_L2 and m["max_rel"] <= FP32_MAX, (layer.name, split, m)
 
 
 @pytest.mark.parametrize("workload", ["vgg16", "alexnet"])

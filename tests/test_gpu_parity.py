@@ -380,7 +380,8 @@ print(json.dumps(out))
 '''
 
 
-@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs", "msub", "msub-cg1"])
+@pytest.mark.parametrize("mode", ["1", "0", "stacked", "unstacked", "knobs", "msub", "msub-cg1", "f16", "mixed",
+                                  "msub-mixed", "stacked-mixed"])
 def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     """The implicit kernel's tap-shared mode (zero-padded NHWC rows, one A box of 128+k-1 rows
     per kernel row, taps through row-shifted UMMA descriptors), forced on and off via
@@ -391,8 +392,11 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     including multi-chunk K, stream-K split tiles, M not a multiple of 16 and pad 0 / pad > k/2;
     the launch trace proves both k = 3 and k = 5 instantiations ran.  "msub" / "msub-cg1" force
     the two-sub-tile mode (two 128-row A boxes per weight stage, D column halves = sub-tiles) on
-    every mixed-split padded layer, with CTA pairs and single CTAs: ragged M (16 / 40 / 80),
-    k = 3/5/7, stream-K split tiles.  "knobs" turns the
+    every fp32 padded layer, with CTA pairs and single CTAs: ragged M (16 / 40 / 80),
+    k = 3/5/7, stream-K split tiles.  "f16" / "mixed" force one fp32-faithful operand format on
+    every shape (CLB_SPLIT; by default C = 8 / 16 / 48 take the mixed split, the others the fp16
+    split), "msub-mixed" / "stacked-mixed" the two-sub-tile and tap-stacked modes under the mixed
+    split.  "knobs" turns the
     remaining A/B switches to their non-default side so they stay correct: one producer warp
     for A and B (CLB_SPLIT_ISSUE=0), stream-K partials added from global memory
     (CLB_FIXUP_SMEM=0) and stream-K ranges over all units (CLB_SK_UNITS=0)."""
@@ -410,11 +414,15 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
            "knobs": dict(CLB_PADDED_ROWS="1", CLB_SPLIT_ISSUE="0", CLB_FIXUP_SMEM="0", CLB_SK_UNITS="0",
                          CLB_TRACE="1"),
            "msub": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="2", CLB_TRACE="1"),
-           "msub-cg1": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="1", CLB_TRACE="1")}[mode]
+           "msub-cg1": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="1", CLB_TRACE="1"),
+           "f16": dict(CLB_PADDED_ROWS="1", CLB_SPLIT="3xf16"),
+           "mixed": dict(CLB_PADDED_ROWS="1", CLB_SPLIT="mixed"),
+           "msub-mixed": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="2", CLB_TRACE="1", CLB_SPLIT="mixed"),
+           "stacked-mixed": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1", CLB_SPLIT="mixed")}[mode]
     r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, **env))
     assert r.returncode == 0, r.stderr[-3000:]
-    if mode == "stacked":
+    if mode.startswith("stacked"):
         assert "stack=3" in r.stderr and "stack=5" in r.stderr, r.stderr[-2000:]
     if mode == "knobs":
         assert "aiss=1" in r.stderr, r.stderr[-2000:]
@@ -426,6 +434,54 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
             assert res["rel_l2"] <= FP32_L2 and res["max_rel"] <= FP32_MAX, (mode, res)
         else:   # TF32 / BF16 fast modes (north star: rel-L2 <= 1e-2)
             assert res["rel_l2"] <= TF32_L2, (mode, res)
+
+
+F16_RANGE_CASES = {
+    "tiny-x": (1e-20, 1.0), "huge-x": (1e20, 1e-3), "tiny-w": (1.0, 1e-30), "large-both": (3e4, 7e4),
+    "subnormal-x": (1e-39, 1e30), "outlier": (1.0, 1.0), "zero-x": (0.0, 1.0),
+}
+
+
+@pytest.mark.parametrize("method", ["kn2row-gpu", "kn2row-acc-gpu", "conv1x1-gpu"])
+@pytest.mark.parametrize("case", sorted(F16_RANGE_CASES))
+def test_f16_split_scaling_range(oracle, clb, torch_cuda, case, method):
+    """The fp16 split (default operand format of the implicit kn2row family) scales each operand
+    by an exact power of two from its max |value| before splitting, and the epilogue undoes it:
+    inputs and weights far outside fp16's range (1e-39 .. 1e20), a lone outlier setting the
+    scale, and an all-zero input must all stay within the fp32-faithful bounds (the zero input
+    exactly zero).  The plan reports the format it used."""
+    sx, sw = F16_RANGE_CASES[case]
+    k = 1 if method == "conv1x1-gpu" else 3
+    x, w = oracle.make_problem(2, 64, 12, 12, 48, k, 321)
+    x = (x * np.float32(sx)).astype(np.float32)
+    w = (w * np.float32(sw)).astype(np.float32)
+    if case == "outlier":
+        x[1, 5, 6, 7] = 1e6
+    ref = oracle.conv_batch(x, w)
+    layer = clb.LayerConfig("r", 64, 12, 12, 48, k, batch=2)
+    with clb.ConvPlan(layer, method, "fp32") as plan:
+        assert plan.split == "3xf16", plan.split
+        plan.set_weights(torch_cuda.from_numpy(w).cuda())
+        y = plan.forward(torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+    if case == "zero-x":
+        assert not np.any(y), "zero input must give an exactly zero output"
+        return
+    _check_fp32(oracle, y, ref, f"{case} {method}")
+
+
+def test_operand_split_selection(clb, torch_cuda):
+    """fp32 plans of the implicit family take the fp16 split where it issues fewer MMAs than the
+    mixed split (C = 16 and 48 keep the mixed split), the other GPU methods the mixed split, the
+    fast modes their own format and the direct kernel fp32 FMA."""
+    def split(c, method="kn2row-gpu", precision="fp32", k=3):
+        with clb.ConvPlan(clb.LayerConfig("s", c, 8, 8, 32, k, batch=1), method, precision) as p:
+            return p.split
+    assert [split(c) for c in (8, 16, 24, 32, 48, 64, 96, 100)] == \
+        ["mixed", "mixed", "3xf16", "3xf16", "mixed", "3xf16", "3xf16", "3xf16"]
+    assert split(64, "kn2row-explicit-gpu") == "mixed" and split(64, "im2col-gpu") == "mixed"
+    assert split(64, "conv1x1-gpu", k=1) == "3xf16" and split(64, "kn2row-acc-gpu") == "3xf16"
+    assert split(64, precision="tf32") == "tf32" and split(64, precision="bf16") == "bf16"
+    assert split(3, "direct-gpu") == "fp32-fma"
 
 
 GUARD_CASES = [(2, 16, 13, 13, 32, 3, 1), (4, 64, 28, 28, 256, 3, 1), (3, 8, 9, 11, 24, 5, 2), (2, 3, 17, 19, 16, 3, 1),

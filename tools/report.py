@@ -25,10 +25,12 @@ from paper_1704_04428_b200 import _lib, rng, workloads
 from oracle import oracle as O
 
 import os
-# fp32-faithful peak: measured bf16 burst / 2 (tf32 rate) x 1/2 for the default mixed split
-# (4 tf32-MMA slots per 16 K-elements) or x 1/3 for CLB_SPLIT=3xtf32 (6 slots)
+# fp32-faithful peak of each plan's operand format: measured bf16 burst / 3 for the fp16 split
+# (3 f16 MMAs per product), / 4 for the mixed split (4 tf32-MMA slots per 16 K-elements), / 6 for
+# CLB_SPLIT=3xtf32; the direct kernel (CUDA cores) is reported against the mixed figure
 _pk = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())
-PEAK_3X = float(_pk["bf16_tflops"]) / 2 / (3 if os.environ.get("CLB_SPLIT") == "3xtf32" else 2)
+SPLIT_PEAK = {"3xf16": float(_pk["bf16_tflops"]) / 3, "mixed": float(_pk["bf16_tflops"]) / 4,
+              "3xtf32": float(_pk["bf16_tflops"]) / 6, "fp32-fma": float(_pk["bf16_tflops"]) / 4}
 HBM = float(_pk["hbm_gbs"])   # GB/s measured
 
 ap = argparse.ArgumentParser()
@@ -65,6 +67,7 @@ for wl in args.workloads.split(","):
                 ft.append(fb.elapsed_time(fe))
             _lib.lib().cl_conv_set_profile_events(plan._h, None, None)
             method = plan.method
+            split = plan.split
             # back-to-back forwards replayed from a CUDA graph: no host launch latency in the
             # measurement (what a serving loop / captured network sees); L2 stays warm
             g = torch.cuda.CUDAGraph()
@@ -92,9 +95,10 @@ for wl in args.workloads.split(","):
         k_ms, f_ms = statistics.median(kt), statistics.median(ft)
         fl = layer.flops()
         ai = fl / layer.algorithmic_bytes()
+        PEAK_3X = SPLIT_PEAK[split]
         bound = min(PEAK_3X, ai * HBM / 1000.0)
         row = {"workload": wl, "layer": layer.name, "N": layer.batch, "C": layer.channels, "HW": layer.height,
-               "M": layer.kernel_count, "k": layer.kernel_size, "method": method, "gflop": fl / 1e9,
+               "M": layer.kernel_count, "k": layer.kernel_size, "method": method, "split": split, "peak_tflops": PEAK_3X, "gflop": fl / 1e9,
                "kernel_ms": k_ms, "forward_ms": f_ms, "kernel_tflops": fl / k_ms / 1e9,
                "forward_tflops": fl / f_ms / 1e9, "graph_forward_ms": graph_ms,
                "graph_forward_tflops": fl / graph_ms / 1e9, "frac_of_fp32_peak": fl / k_ms / 1e9 / PEAK_3X,
@@ -126,5 +130,5 @@ for wl in args.workloads.split(","):
         print(json.dumps(row), file=sys.stderr, flush=True)
         del x, w, y, ws
         torch.cuda.empty_cache()
-print(json.dumps({"peak_fp32_faithful_tflops": PEAK_3X, "fp32_split": os.environ.get("CLB_SPLIT", "mixed"),
+print(json.dumps({"peak_fp32_faithful_tflops": SPLIT_PEAK, "fp32_split": os.environ.get("CLB_SPLIT", "auto"),
                   "hbm_gbs": HBM, "rows": rows}, indent=1))
