@@ -39,10 +39,14 @@ int planes_for(cl_precision precision) {
 
 // Operand format of a convolution plan.  fp32: the fp16 split (3 MMA slots per 16 channels, half
 // the operand bytes of the mixed split) for the implicit kn2row family wherever
-// it issues fewer MMAs than the mixed split (6 ceil(C/32) < 4 ceil(C/16): not for C = 16, 48),
-// otherwise the mixed split.  CLB_SPLIT=3xtf32 / mixed / 3xf16 forces a split (3xf16: where
-// the method supports it).
-int conv_planes_for(cl_precision precision, cl_method m, int C) {
+// it issues fewer MMAs than the mixed split (6 ceil(C/32) < 4 ceil(C/16): not for C = 8, 16, 48)
+// and the layer is large enough (>= 12 GFLOP) to amortise the split's extra pass over the input
+// (max|x|: one launch + 4 B per element, ~3-10 us on these layers): below that the contraction
+// gains 0-2 us (GoogLeNet 3x3 layers, C1, AlexNet b1, the k1-k7 sweep) and the mixed split's
+// single prepass wins (profiles/r02_f16_mode_sweep.txt).
+// Otherwise the mixed split.  CLB_SPLIT=3xtf32 / mixed / 3xf16 forces a split (3xf16: where the
+// method supports it).
+int conv_planes_for(cl_precision precision, cl_method m, int C, double flops) {
     static const int forced = [] {
         const char* e = std::getenv("CLB_SPLIT");
         if (!e) return 0;
@@ -54,8 +58,9 @@ int conv_planes_for(cl_precision precision, cl_method m, int C) {
     if (precision != CL_PREC_FP32) return planes_for(precision);
     if (forced == 2 || forced == kPlanesMixed) return forced;
     const bool implicit = m == CL_METHOD_KN2ROW || m == CL_METHOD_CONV1X1 || m == CL_METHOD_KN2ROW_ACC;
-    if (implicit && (forced == kPlanesF16 || 6 * ((C + 31) / 32) < 4 * ((C + 15) / 16))) return kPlanesF16;
-    return kPlanesMixed;
+    if (!implicit) return kPlanesMixed;
+    if (forced == kPlanesF16) return kPlanesF16;
+    return (6 * ((C + 31) / 32) < 4 * ((C + 15) / 16) && flops >= 12e9) ? kPlanesF16 : kPlanesMixed;
 }
 
 cl_status fail(cl_status s, const std::string& msg) {
@@ -729,7 +734,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         p->requested = method;
         p->method = m;
         p->prec = precision;
-        p->planes = conv_planes_for(precision, m, d.c);
+        p->planes = conv_planes_for(precision, m, d.c, 2.0 * d.n * d.m * d.c * d.k * d.k * (double)P * Q);
         p->device = device;
         p->Cp = round_up(d.c, k_granule(p->planes));
         p->Kp = round_up(d.k * d.k * d.c, k_granule(p->planes));
@@ -776,7 +781,12 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             // VGG conv3_x/4_x -5..-9 %, GoogLeNet 7x7 layers -27 % even at 31-65 % waste.  It loses
             // only where BN = 256 meets >= 15 % waste (AlexNet conv2 / conv5: +2-3 %)
             // (profiles/r01_padded_shared_sweep.txt).
-            const double max_waste = p->bn <= 192 ? 0.70 : 0.10;
+            // With the fp16 split (half the A bytes of the mixed split per MMA) the TMA im2col A loads
+            // keep up at BN > 128, and the padded rows' dropped positions then cost more than they
+            // save: VGG conv3_x / conv4_x -3..-5 %, AlexNet conv3 / conv4 -8 % in im2col mode
+            // (profiles/r02_f16_mode_sweep.txt); at BN <= 128 padded rows still win (conv1_2 1.9x).
+            const double max_waste = p->planes == kPlanesF16 ? (p->bn <= 128 ? 0.70 : -1.0)
+                                                             : (p->bn <= 192 ? 0.70 : 0.10);
             p->padded_rows = eligible && (forced_padded == 1 || (forced_padded != 0 && waste <= max_waste));
             // Tap-stacked: with few output channels the MMA's N = M is small and pays a fixed
             // cost per instruction (N = 64: 51 cycles vs 32 ideal, tools/mma_probe.cu); stacking

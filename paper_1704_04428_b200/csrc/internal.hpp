@@ -123,7 +123,7 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int b
 // p.partials / p.flags must point at tc_scratch_bytes() of device scratch (stream-K fixup).
 // returns the kernels launched: 1, or 2 when a requested fused prepass ran standalone instead
 int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cta_group = 1);
-constexpr int kMaxGrid = 160;   // >= SM count (148 on B200)
+constexpr int kMaxGrid = kMaxUnits;   // >= SM count (148 on B200)
 constexpr int kMaxSplit = 10;   // max stream-K pieces per tile (latency-bound problems)
 size_t tc_scratch_bytes();
 // carve the stream-K scratch out of a workspace pointer

@@ -326,6 +326,8 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
         }
         sk_memo[sk_key] = p.sk_units;
     }
+    if (p.sk_units > kMaxUnits) throw Error(6, "too many scheduling units");
+    for (int b = 0; b <= p.sk_units; ++b) p.sk_start[b] = chunk_start(b, p.sk_chunks, p.sk_units);
     const int grid = units * cg;
     if (!p.partials || !p.flags) throw Error(6, "stream-K scratch missing");
     if (!p.flags_zeroed) CLB_CUDA(cudaMemsetAsync(p.flags, 0, (size_t)grid * sizeof(unsigned), s));

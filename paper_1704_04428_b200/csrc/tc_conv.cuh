@@ -61,6 +61,7 @@ constexpr int kSmemBudget = 200 * 1024;
 constexpr int kChunkK = 192;          // fp32-faithful splits: K-elements per TMEM accumulation chunk
 constexpr int kBarrierBytes = 512;
 constexpr int kMaxPeers = 8;     // ranks of a fused output all-gather (one node)
+constexpr int kMaxUnits = 160;   // scheduling units per launch (>= SM count; = kMaxGrid)
 // TMEM loads (16 columns each) in flight per chunk fold (2 keeps the epilogue inside its
 // 200-register budget next to its 128 running sums).
 constexpr int kFoldLoads = 2;
@@ -129,6 +130,9 @@ struct TcParams {
     int sk_chunks;             // chunks of tiles [dp_tiles, num_tiles), split contiguously (stream-K)
     int sk_units;              // scheduling units sharing the stream-K chunks (<= grid units; the
                                // rest only run data-parallel tiles): chosen so no tile splits 3 ways
+    int sk_start[kMaxUnits + 1];   // chunk_start(b, sk_chunks, sk_units), b = 0..sk_units (host-computed:
+                                   // a 64-bit division in the kernel is a subroutine call, and the
+                                   // registers saved around it spilled into the MMA issue loop)
     // chained prepass (nx_on): while this contraction runs, its converter warps (12-15) convert
     // tiles of the NEXT layer's input (nx) -- memory-bound work on SMs whose tensor pipe is busy
     // and whose DRAM traffic is 6-30 % of peak -- until this CTA's epilogue is done
@@ -243,8 +247,8 @@ struct Sched {
     __device__ Sched(const TcParams& p, int b_, int grid_)
         : b(b_), grid(grid_), cpt(p.chunks_per_tile), dp_tiles(p.dp_tiles), i(0) {
         n_dp = dp_tiles > b ? (dp_tiles - b + grid - 1) / grid : 0;
-        g = b < p.sk_units ? chunk_start(b, p.sk_chunks, p.sk_units) : 0;
-        g_end = b < p.sk_units ? chunk_start(b + 1, p.sk_chunks, p.sk_units) : 0;
+        g = b < p.sk_units ? p.sk_start[b] : 0;
+        g_end = b < p.sk_units ? p.sk_start[b + 1] : 0;
     }
     __device__ bool next(Piece& pc) {
         if (i < n_dp) {
@@ -831,7 +835,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             int u_end = unit + 1;
             if (finisher) {
                 const int last = (pc.tile - p.dp_tiles) * cpt + cpt - 1;   // in stream-K chunk space
-                while (u_end < p.sk_units && chunk_start(u_end, p.sk_chunks, p.sk_units) <= last) ++u_end;
+                while (u_end < p.sk_units && p.sk_start[u_end] <= last) ++u_end;
             }
             for (int c = pc.c_lo; c < pc.c_hi; ++c, ++lg) {
                 const uint32_t buf = lg & (uint32_t)(nbuf - 1);

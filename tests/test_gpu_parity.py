@@ -394,8 +394,8 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     the two-sub-tile mode (two 128-row A boxes per weight stage, D column halves = sub-tiles) on
     every fp32 padded layer, with CTA pairs and single CTAs: ragged M (16 / 40 / 80),
     k = 3/5/7, stream-K split tiles.  "f16" / "mixed" force one fp32-faithful operand format on
-    every shape (CLB_SPLIT; by default C = 8 / 16 / 48 take the mixed split, the others the fp16
-    split), "msub-mixed" / "stacked-mixed" the two-sub-tile and tap-stacked modes under the mixed
+    every shape (CLB_SPLIT; by default these small layers take the mixed split), "stacked" /
+    "msub" / "msub-cg1" run under the fp16 split, "msub-mixed" / "stacked-mixed" under the mixed
     split.  "knobs" turns the
     remaining A/B switches to their non-default side so they stay correct: one producer warp
     for A and B (CLB_SPLIT_ISSUE=0), stream-K partials added from global memory
@@ -409,12 +409,12 @@ def test_tap_shared_padded_row_mode(oracle, tmp_path, mode):
     script = tmp_path / "padded.py"
     script.write_text(_PADDED_SCRIPT)
     env = {"1": dict(CLB_PADDED_ROWS="1"), "0": dict(CLB_PADDED_ROWS="0"),
-           "stacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1"),
+           "stacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="1", CLB_TRACE="1", CLB_SPLIT="3xf16"),
            "unstacked": dict(CLB_PADDED_ROWS="1", CLB_STACKED="0"),
            "knobs": dict(CLB_PADDED_ROWS="1", CLB_SPLIT_ISSUE="0", CLB_FIXUP_SMEM="0", CLB_SK_UNITS="0",
                          CLB_TRACE="1"),
-           "msub": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="2", CLB_TRACE="1"),
-           "msub-cg1": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="1", CLB_TRACE="1"),
+           "msub": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="2", CLB_TRACE="1", CLB_SPLIT="3xf16"),
+           "msub-cg1": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="1", CLB_TRACE="1", CLB_SPLIT="3xf16"),
            "f16": dict(CLB_PADDED_ROWS="1", CLB_SPLIT="3xf16"),
            "mixed": dict(CLB_PADDED_ROWS="1", CLB_SPLIT="mixed"),
            "msub-mixed": dict(CLB_PADDED_ROWS="1", CLB_MSUB="2", CLB_CTA_GROUP="2", CLB_TRACE="1", CLB_SPLIT="mixed"),
@@ -441,45 +441,72 @@ F16_RANGE_CASES = {
     "subnormal-x": (1e-39, 1e30), "outlier": (1.0, 1.0), "zero-x": (0.0, 1.0),
 }
 
+_F16_RANGE_SCRIPT = r'''
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+from oracle import oracle as O
+import paper_1704_04428_b200 as clb
+from tests.test_gpu_parity import F16_RANGE_CASES
+out = []
+for case, (sx, sw) in sorted(F16_RANGE_CASES.items()):
+    for method in ("kn2row-gpu", "kn2row-acc-gpu", "conv1x1-gpu"):
+        k = 1 if method == "conv1x1-gpu" else 3
+        x, w = O.make_problem(2, 64, 12, 12, 48, k, 321)
+        x = (x * np.float32(sx)).astype(np.float32)
+        w = (w * np.float32(sw)).astype(np.float32)
+        if case == "outlier":
+            x[1, 5, 6, 7] = 1e6
+        ref = O.conv_batch(x, w)
+        with clb.ConvPlan(clb.LayerConfig("r", 64, 12, 12, 48, k, batch=2), method, "fp32") as plan:
+            split = plan.split
+            plan.set_weights(torch.from_numpy(w).cuda())
+            y = plan.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+        m = O.parity_metrics(y, ref)
+        out.append({"case": case, "method": method, "split": split, "rel_l2": m["rel_l2"], "max_rel": m["max_rel"],
+                    "finite": m["finite"], "zero": not bool(np.any(y))})
+print(json.dumps(out))
+'''
 
-@pytest.mark.parametrize("method", ["kn2row-gpu", "kn2row-acc-gpu", "conv1x1-gpu"])
-@pytest.mark.parametrize("case", sorted(F16_RANGE_CASES))
-def test_f16_split_scaling_range(oracle, clb, torch_cuda, case, method):
-    """The fp16 split (default operand format of the implicit kn2row family) scales each operand
-    by an exact power of two from its max |value| before splitting, and the epilogue undoes it:
-    inputs and weights far outside fp16's range (1e-39 .. 1e20), a lone outlier setting the
-    scale, and an all-zero input must all stay within the fp32-faithful bounds (the zero input
-    exactly zero).  The plan reports the format it used."""
-    sx, sw = F16_RANGE_CASES[case]
-    k = 1 if method == "conv1x1-gpu" else 3
-    x, w = oracle.make_problem(2, 64, 12, 12, 48, k, 321)
-    x = (x * np.float32(sx)).astype(np.float32)
-    w = (w * np.float32(sw)).astype(np.float32)
-    if case == "outlier":
-        x[1, 5, 6, 7] = 1e6
-    ref = oracle.conv_batch(x, w)
-    layer = clb.LayerConfig("r", 64, 12, 12, 48, k, batch=2)
-    with clb.ConvPlan(layer, method, "fp32") as plan:
-        assert plan.split == "3xf16", plan.split
-        plan.set_weights(torch_cuda.from_numpy(w).cuda())
-        y = plan.forward(torch_cuda.from_numpy(x).cuda()).cpu().numpy()
-    if case == "zero-x":
-        assert not np.any(y), "zero input must give an exactly zero output"
-        return
-    _check_fp32(oracle, y, ref, f"{case} {method}")
+
+def test_f16_split_scaling_range(oracle, tmp_path):
+    """The fp16 split (CLB_SPLIT=3xf16 forces it on these small layers, in a subprocess) scales
+    each operand by an exact power of two from its max |value| before splitting, and the epilogue
+    undoes it: inputs and weights far outside fp16's range (1e-39 .. 1e20), a lone outlier setting
+    the scale, and an all-zero input must all stay within the fp32-faithful bounds (the zero input
+    exactly zero), through implicit kn2row, the accumulating variant and conv1x1."""
+    import json
+    import subprocess
+    import sys
+    root = Path(__file__).resolve().parent.parent
+    script = tmp_path / "f16range.py"
+    script.write_text(_F16_RANGE_SCRIPT)
+    r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, CLB_SPLIT="3xf16"), cwd=str(root))
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert len(res) == 3 * len(F16_RANGE_CASES)
+    for e in res:
+        assert e["split"] == "3xf16", e
+        if e["case"] == "zero-x":
+            assert e["zero"], e
+        else:
+            assert e["finite"] and e["rel_l2"] <= FP32_L2 and e["max_rel"] <= FP32_MAX, e
 
 
 def test_operand_split_selection(clb, torch_cuda):
     """fp32 plans of the implicit family take the fp16 split where it issues fewer MMAs than the
-    mixed split (C = 16 and 48 keep the mixed split), the other GPU methods the mixed split, the
-    fast modes their own format and the direct kernel fp32 FMA."""
-    def split(c, method="kn2row-gpu", precision="fp32", k=3):
-        with clb.ConvPlan(clb.LayerConfig("s", c, 8, 8, 32, k, batch=1), method, precision) as p:
+    mixed split (C = 8, 16 and 48 keep the mixed split) and the layer has >= 12 GFLOP to amortise
+    the split's max|x| pass; smaller layers, the other GPU methods and C = 16 / 48 the mixed
+    split; the fast modes their own format; the direct kernel fp32 FMA."""
+    def split(c, method="kn2row-gpu", precision="fp32", k=3, n=256, hw=56):
+        with clb.ConvPlan(clb.LayerConfig("s", c, hw, hw, 64, k, batch=n), method, precision) as p:
             return p.split
     assert [split(c) for c in (8, 16, 24, 32, 48, 64, 96, 100)] == \
         ["mixed", "mixed", "3xf16", "3xf16", "mixed", "3xf16", "3xf16", "3xf16"]
+    assert split(64, n=1) == "mixed" and split(64, hw=8) == "mixed"          # < 12 GFLOP
     assert split(64, "kn2row-explicit-gpu") == "mixed" and split(64, "im2col-gpu") == "mixed"
-    assert split(64, "conv1x1-gpu", k=1) == "3xf16" and split(64, "kn2row-acc-gpu") == "3xf16"
+    assert split(256, "conv1x1-gpu", k=1) == "3xf16" and split(64, "kn2row-acc-gpu") == "3xf16"
     assert split(64, precision="tf32") == "tf32" and split(64, precision="bf16") == "bf16"
     assert split(3, "direct-gpu") == "fp32-fma"
 
