@@ -405,7 +405,14 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         case CL_METHOD_CONV1X1:
         case CL_METHOD_KN2ROW_ACC: {
             void* xs = wsf;
-            if (p->planes == kPlanesF16) {   // the input's exponent shift (max|x|) ahead of its split
+            // fp16 split: the input's exponent shift.  NCHW input: one speculative pass (the split
+            // reduces max|x| while converting with the previous forward's exponent) + a fixup launch
+            // that re-converts only on a miss; channels-last input (or CLB_F16_SPEC=0): a max|x|
+            // pass ahead of the split
+            static const bool spec_env = !(std::getenv("CLB_F16_SPEC") && std::atoi(std::getenv("CLB_F16_SPEC")) == 0);
+            const bool spec = p->planes == kPlanesF16 && !nhwc && !prepass_partial && spec_env;
+            unsigned* t_reset = nullptr;   // the contraction zeroes the speculative pass's group maxima
+            if (p->planes == kPlanesF16 && !spec) {
                 launch_absmax_exp(x, (long long)d.n * d.c * d.h * d.w, p->scale, p->scale + 1, s);
                 ++p->launches;
             }
@@ -424,6 +431,10 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 if (prepass_partial) {
                     launch_split_tail(own_job, p->planes, s);   // the tiles the previous contraction left
                     ++p->launches;
+                } else if (spec) {
+                    launch_nchw_split_speculative(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->scale, s);
+                    p->launches += 2;
+                    t_reset = spec_reset_slots(p->scale);
                 } else {
                     if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s, p->scale);
                     else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s, p->scale);
@@ -432,6 +443,7 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 Operand a = tiled(xs, grid_rows, 1, p->Cp, p->planes);
                 Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
                 TcParams t = base_params(p);
+                t.reset_slots = t_reset;
                 t.rows = d.n * Hp * Wp;
                 t.cols = d.m;
                 t.bn = p->bn;
@@ -470,13 +482,18 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
                 break;
             }
             if (prepass_partial) launch_split_tail(own_job, p->planes, s);
-            else if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s, p->scale);
+            else if (spec) {
+                launch_nchw_split_speculative(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->scale, s);
+                ++p->launches;
+                t_reset = spec_reset_slots(p->scale);
+            } else if (nhwc) launch_nhwc_split(x, xs, d.n, d.c, d.h, d.w, 0, p->Cp, p->planes, s, p->scale);
             else launch_nchw_to_nhwc_split(x, xs, d.n, d.c, d.h * d.w, p->Cp, p->planes, s, p->scale);
             ++p->launches;
             Operand a = implicit_a(p, xs);
             a.n = d.n;
             Operand b = tiled(p->wpack, d.m, taps, p->Cp, p->planes);
             TcParams t = base_params(p);
+            t.reset_slots = t_reset;
             t.rows = (int)npq;
             t.cols = d.m;
             t.bn = p->bn;
@@ -749,7 +766,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         }
         if (m == CL_METHOD_DIRECT) p->wraw = p->wpack;
         if (p->planes == kPlanesF16) {
-            const size_t sb = (size_t)(kScaleSlots + kAbsmaxBlocks) * sizeof(int);
+            const size_t sb = (size_t)kScaleBufInts * sizeof(int);
             if (cudaMalloc(&p->scale, sb) != cudaSuccess || cudaMemset(p->scale, 0, sb) != cudaSuccess) {
                 cudaGetLastError();
                 cudaFree(p->wpack);

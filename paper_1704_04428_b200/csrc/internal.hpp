@@ -70,9 +70,21 @@ void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, 
 // fp16 split scale: exponent e with max|x| * 2^e in [2^14, 2^15) (0 for an all-zero or non-finite
 // tensor; in [-113, 163] otherwise) written to *out_exp.  `slots` = the plan's scale buffer (partials +
 // completion counter, self-resetting).  Stream-ordered, graph-capturable.
-constexpr int kScaleSlots = 8;          // [0] ew, [1] ex, [2] counter, ... then the partial maxima
-constexpr int kAbsmaxBlocks = 1024;
+constexpr int kScaleSlots = 8;          // [0] ew, [1] ex, [2] counter, [3] e_spec, [4] e_spec valid, [6] e_use
+constexpr int kAbsmaxBlocks = 1024;     // absmax partial maxima [8, 8 + 1024)
+constexpr int kSpecGroups = kSpecGroupSlots;   // speculative prepass: group maxima (zeroed by the contraction)
+constexpr int kSpecStride = kSpecGroupStride;   // ints between group slots (own 64 B sector each)
+constexpr int kScaleBufInts = kScaleSlots + kAbsmaxBlocks + kSpecGroups * kSpecStride;
 void launch_absmax_exp(const float* x, long long n, int* slots, int* out_exp, cudaStream_t s);
+// fp16 split, single pass over x (NCHW input): the prepass converts with the exponent of the
+// plan's previous forward (speculation) while reducing max|x|; its last block writes the exact
+// maxima, and the fixup kernel launched behind it publishes the exact exponent ex and re-converts
+// the whole input with it only when the speculation missed (the first forward, or a changed
+// range), so the operand is always the one the two-pass form writes (bitwise).  The contraction
+// must then zero the group maxima: spec_reset_slots().
+void launch_nchw_split_speculative(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp,
+                                   int* slots, cudaStream_t s);
+inline unsigned* spec_reset_slots(int* slots) { return reinterpret_cast<unsigned*>(slots + kScaleSlots + kAbsmaxBlocks); }
 // the same conversion as a tile job (chained mode) and the tail launch that finishes its tiles
 // left by the previous contraction's converter warps (then resets the job's counter)
 SplitJob make_split_job(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp);

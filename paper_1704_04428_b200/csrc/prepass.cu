@@ -339,14 +339,7 @@ __global__ void __launch_bounds__(256) absmax_exp_kernel(const float* __restrict
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int w = 1; w < 8; ++w) m = max(m, wm[w]);
-            int e = 0;
-            if (m != 0 && m < 0x7f800000u) {
-                int ex;
-                frexpf(__uint_as_float(m), &ex);   // max = f 2^ex, f in [0.5, 1)
-                e = 15 - ex;                        // max 2^e in [2^14, 2^15): e in [-113, 163]
-                                                    // for every finite nonzero fp32 max
-            }
-            *out_exp = e;
+            *out_exp = f16_split_exponent(m);
             *counter = 0u;
         }
     }
@@ -370,6 +363,116 @@ void launch_absmax_exp(const float* x, long long n, int* slots, int* out_exp, cu
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     CLB_CUDA(cudaLaunchKernelEx(&cfg, absmax_exp_kernel, x, n, slots, out_exp));
+}
+
+// ------------------------------------------------ fp16 split, speculative single pass ----
+// Slots: [1] ex (exact exponent of this input, read by the contraction), [3] e_spec / [4] valid
+// (the exponent of the plan's previous forward), [5] unused, [6] e_use (the exponent this
+// forward's split was written with); group maxima after the absmax partials (kSpecGroups: every
+// block folds its max into group blockIdx % kSpecGroups with one fire-and-forget atomicMax, so no
+// address sees more than ~1/64 of the atomics).  The fixup kernel (launched right behind, PDL)
+// folds the groups, publishes ex / e_spec and re-converts the input when e_use != ex; the
+// contraction behind it zeroes the groups for the next forward (TcParams::reset_slots) -- every
+// kernel touching them is then complete.
+struct SpecHook {
+    unsigned* gmax;
+    uint32_t* wmax;   // shared [8]
+    int g;
+    __device__ __forceinline__ void after_load(uint32_t m) {
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
+    }
+    __device__ __forceinline__ void after_sync() {   // after the mid-tile barrier: wmax is complete
+        if (threadIdx.x == 0) {
+            uint32_t m = wmax[0];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) m = max(m, wmax[w]);
+            atomicMax(gmax + g * kSpecStride, m);   // result unused: a RED, no wait
+        }
+    }
+};
+
+__global__ void __launch_bounds__(256) split_spec_kernel(const float* __restrict__ x, void* __restrict__ xsv, int N,
+                                                          int C, int HW, int Cp, int H, int W, int Wp, int pad,
+                                                          FastDiv hwd, FastDiv wpd, int* slots) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ SplitSmem<kPlanesF16> sm;
+    __shared__ uint32_t wmax[8];
+    const int nty = (Cp + 31) / 32;
+    const int t = (int)gridDim.x - 1 - (int)blockIdx.x;     // reversed tile order (see the kernel above)
+    const int bx = t / nty, by = t - bx * nty;
+    const int e_use = slots[4] ? slots[3] : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) slots[6] = e_use;
+    SpecHook hook{reinterpret_cast<unsigned*>(slots + kScaleSlots + kAbsmaxBlocks), wmax,
+                  (int)(blockIdx.x % kSpecGroups)};
+    split_tile<kPlanesF16>(x, xsv, N, C, HW, Cp, H, W, Wp, pad, hwd, wpd, bx, by, (int)threadIdx.x, sm,
+                           pow2_factors(e_use), &hook);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Folds the group maxima into the exact exponent ex (every block computes the same value and
+// publishes it), and re-converts the whole input with ex when the speculative pass used another
+// exponent; otherwise returns at once.  Persistent grid; it always waits for the prepass first,
+// so a contraction launched behind it (PDL) is ordered after both.
+__global__ void __launch_bounds__(256) split_fixup_kernel(const float* __restrict__ x, void* __restrict__ xsv, int N,
+                                                           int C, int HW, int Cp, int H, int W, int Wp, int pad,
+                                                           FastDiv hwd, FastDiv wpd, int* slots, int total) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ int e_sh;
+    const int e_use = __ldcg(slots + 6);   // issued with the group loads (one round trip)
+    if (threadIdx.x < 32) {
+        const unsigned* gmax = reinterpret_cast<const unsigned*>(slots + kScaleSlots + kAbsmaxBlocks);
+        uint32_t a = 0;
+        for (int g = (int)threadIdx.x; g < kSpecGroups; g += 32) a = max(a, __ldcg(gmax + g * kSpecStride));
+        for (int o = 16; o > 0; o >>= 1) a = max(a, __shfl_xor_sync(0xffffffffu, a, o));
+        if (threadIdx.x == 0) {
+            const int e = f16_split_exponent(a);
+            e_sh = e;
+            slots[1] = e;      // identical in every block
+            slots[3] = e;      // the next forward's speculation
+            slots[4] = 1;
+        }
+    }
+    __syncthreads();
+    const int e = e_sh;
+    if (e != e_use) {
+        __shared__ SplitSmem<kPlanesF16> sm;
+        const int nty = (Cp + 31) / 32;
+        const Pow2 sc = pow2_factors(e);
+        for (int t = (int)blockIdx.x; t < total; t += (int)gridDim.x) {
+            const int bx = t / nty, by = t - bx * nty;
+            split_tile<kPlanesF16>(x, xsv, N, C, HW, Cp, H, W, Wp, pad, hwd, wpd, bx, by, (int)threadIdx.x, sm, sc);
+            __syncthreads();   // the staging is reused by the next tile
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+void launch_nchw_split_speculative(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int* slots,
+                                   cudaStream_t s) {
+    // pad > 0: the zero-padded grid of the tap-shared mode; pad == 0: the image pixels
+    const int Hp = pad > 0 ? H + pad : H, Wp = pad > 0 ? W + pad : W;
+    const int HW = Hp * Wp;
+    const long long ntx = ((long long)N * HW + kSplitPx - 1) / kSplitPx, nty = (Cp + 31) / 32;
+    if (ntx * nty >= (1LL << 31)) throw Error(2, "prepass: too many tiles (split the batch)");
+    const int total = (int)(ntx * nty);
+    const FastDiv hwd = make_fastdiv((uint32_t)HW), wpd = make_fastdiv((uint32_t)Wp);
+    const int h = pad > 0 ? H : 1, w = pad > 0 ? W : HW;   // the unpadded path reads rows of HW pixels
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3((unsigned)total);
+    CLB_CUDA(cudaLaunchKernelEx(&cfg, split_spec_kernel, x, xs, N, C, HW, Cp, h, w, Wp, pad, hwd, wpd, slots));
+    int dev = 0, sms = 0;
+    CLB_CUDA(cudaGetDevice(&dev));
+    CLB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cfg.gridDim = dim3((unsigned)std::max(1, std::min(total, sms)));   // one block per SM: a hit reads 64 slots and exits
+    CLB_CUDA(cudaLaunchKernelEx(&cfg, split_fixup_kernel, x, xs, N, C, HW, Cp, h, w, Wp, pad, hwd, wpd, slots, total));
 }
 
 // -------------------------------------------------------------------- row-wise split ----

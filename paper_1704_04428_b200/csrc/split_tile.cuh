@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -30,6 +31,15 @@ __host__ __device__ __forceinline__ Pow2 pow2_factors(int e) {
     return Pow2{exp2i(e1), exp2i(e - e1)};
 }
 __device__ __forceinline__ float apply_pow2(float v, const Pow2& f) { return (v * f.a) * f.b; }
+
+// The fp16 split's exponent shift for a tensor whose max |x| has the (ordered) bits m: max 2^e in
+// [2^14, 2^15), e in [-113, 163] for every finite nonzero max; 0 for zero / non-finite tensors.
+__device__ __forceinline__ int f16_split_exponent(uint32_t m) {
+    if (m == 0 || m >= 0x7f800000u) return 0;
+    int ex;
+    frexpf(__uint_as_float(m), &ex);   // max = f 2^ex, f in [0.5, 1)
+    return 15 - ex;
+}
 
 // fp16 split of one scaled value pair: hi = fp16(x), lo = fp16(x - hi) (x - hi is exact in fp32),
 // packed as the two halves of a 32-bit word each (channel c in the low half, c + 1 in the high)
@@ -109,11 +119,19 @@ struct SplitSmem {
 // Tile (bx, by) = pixels [128 bx, 128 bx + 128) flattened over (image, pixel) x channels
 // [32 by, 32 by + 32); tid in [0, 256).  `scale` (fp16 split only) = 2^ex, the input's exponent
 // shift (exact, two factors).
-template <int PLANES>
+// Optional per-tile hook (the fp16 split's speculative prepass): after_load(max |x| of this
+// thread's values, ordered bits) runs in every thread right after the load phase, after_sync()
+// right after the load / write phase barrier -- so the hook's global atomics overlap the write phase.
+struct NoSplitHook {
+    __device__ __forceinline__ void after_load(uint32_t) {}
+    __device__ __forceinline__ void after_sync() {}
+};
+
+template <int PLANES, class Hook = NoSplitHook>
 __device__ __forceinline__ void split_tile(const float* __restrict__ x, void* __restrict__ xsv, int N, int C, int HW,
                                            int Cp, int H, int W, int Wp, int pad, const FastDiv& hwd,
                                            const FastDiv& wpd, int bx, int by, int tid, SplitSmem<PLANES>& sm,
-                                           Pow2 scale = Pow2{1.0f, 1.0f}) {
+                                           Pow2 scale = Pow2{1.0f, 1.0f}, Hook* hook = nullptr) {
     constexpr bool kSplit = PLANES == 2 || PLANES == kPlanesMixed;
     // pixels are flattened over (image, pixel): a tile may straddle two images, so small maps
     // (13 x 13 = 169 pixels) do not leave most of a second 128-pixel tile idle
@@ -149,6 +167,14 @@ __device__ __forceinline__ void split_tile(const float* __restrict__ x, void* __
 #pragma unroll
         for (int h = 0; h < 4; ++h) v[r][h] = (c < C && src[h] >= 0) ? __ldg(x + src[h] + (long long)c * plane) : 0.0f;
     }
+    if constexpr (!std::is_same<Hook, NoSplitHook>::value) {
+        uint32_t amax = 0;                  // this thread's max |x| (as ordered bits)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int h = 0; h < 4; ++h) amax = max(amax, __float_as_uint(v[r][h]) & 0x7fffffffu);
+        hook->after_load(amax);
+    }
 #pragma unroll
     for (int r = 0; r < 4; r += 2) {
         const int cc = 2 * warp + 16 * (r >> 1);      // even channel within the tile; pair (cc, cc+1)
@@ -177,6 +203,7 @@ __device__ __forceinline__ void split_tile(const float* __restrict__ x, void* __
         }
     }
     __syncthreads();
+    if constexpr (!std::is_same<Hook, NoSplitHook>::value) hook->after_sync();
     const long long row_words = kSplit ? 2LL * Cp : (long long)Cp;
     const int nch = Cp - c0 < 32 ? Cp - c0 : 32;        // channels of this tile inside the padded row
     if (PLANES == kPlanesBf16) {                        // bf16 rows: lane = channel

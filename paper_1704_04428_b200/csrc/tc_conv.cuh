@@ -62,6 +62,8 @@ constexpr int kChunkK = 192;          // fp32-faithful splits: K-elements per TM
 constexpr int kBarrierBytes = 512;
 constexpr int kMaxPeers = 8;     // ranks of a fused output all-gather (one node)
 constexpr int kMaxUnits = 160;   // scheduling units per launch (>= SM count; = kMaxGrid)
+constexpr int kSpecGroupSlots = 64;   // = kSpecGroups (internal.hpp): maxima of the speculative fp16 prepass
+constexpr int kSpecGroupStride = 16;  // ... one per 64 B (spread over L2 slices: every fixup block reads all)
 // TMEM loads (16 columns each) in flight per chunk fold (2 keeps the epilogue inside its
 // 200-register budget next to its 128 running sums).
 constexpr int kFoldLoads = 2;
@@ -120,6 +122,9 @@ struct TcParams {
     int accumulate;            // out += D (accumulating shifted-GEMM variant)
     const int* sexp;           // fp16 split: the operands' exponent shifts [ew, ex] (device); the
                                // epilogue multiplies D by 2^-(ew + ex).  Null for the other formats.
+    unsigned* reset_slots;     // fp16 split, speculative prepass: its group maxima, zeroed by block 0
+                               // once the prepass and its fixup are complete (kSpecGroupSlots words,
+                               // kSpecGroupStride apart)
     float* out;
     long long ld;              // EPI_ROWMAJOR leading dimension
     int out_channels;          // EPI_NCHW: channel count of the output tensor
@@ -477,6 +482,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // prefetch) overlapped the previous kernel's tail; inputs (the split operand, output
     // buffers) are only touched after this point.
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.reset_slots && blockIdx.x == 0 && threadIdx.x < kSpecGroupSlots) p.reset_slots[threadIdx.x * kSpecGroupStride] = 0u;
 
     // Register split per warpgroup (setmaxnreg is warpgroup-aligned, and each role branch below
     // sits under its own setmaxnreg so ptxas allocates it with that budget).

@@ -465,7 +465,25 @@ for case, (sx, sw) in sorted(F16_RANGE_CASES.items()):
         m = O.parity_metrics(y, ref)
         out.append({"case": case, "method": method, "split": split, "rel_l2": m["rel_l2"], "max_rel": m["max_rel"],
                     "finite": m["finite"], "zero": not bool(np.any(y))})
-print(json.dumps(out))
+# speculative single pass: miss (first forward), hit (same data), miss (range x 2^40: the output
+# must be exactly 2^40 x), miss back; every result bitwise equal to the two-pass path's (the
+# channels-last entry point runs the max|x| pass first) and to the oracle within the bounds
+x, w = O.make_problem(3, 64, 20, 20, 80, 3, 99)
+with clb.ConvPlan(clb.LayerConfig("spec", 64, 20, 20, 80, 3, batch=3), "kn2row-gpu", "fp32") as plan:
+    plan.set_weights(torch.from_numpy(w).cuda())
+    xd = torch.from_numpy(x).cuda()
+    y1 = plan.forward(xd).clone()
+    y2 = plan.forward(xd).clone()
+    y3 = plan.forward(xd * 2.0 ** 40).clone()
+    y4 = plan.forward(xd).clone()
+    yn = plan.forward(xd.permute(0, 2, 3, 1).contiguous(), layout="nhwc").permute(0, 3, 1, 2).contiguous()
+    launches = plan.launch_count()
+    torch.cuda.synchronize()
+m = O.parity_metrics(y1.cpu().numpy(), O.conv_batch(x, w))
+spec = {"hit_equal": bool(torch.equal(y1, y2)), "scaled_exact": bool(torch.equal(y3, y1 * 2.0 ** 40)),
+        "back_equal": bool(torch.equal(y4, y1)), "two_pass_equal": bool(torch.equal(yn, y1)),
+        "rel_l2": m["rel_l2"], "max_rel": m["max_rel"]}
+print(json.dumps({"range": out, "spec": spec}))
 '''
 
 
@@ -474,7 +492,10 @@ def test_f16_split_scaling_range(oracle, tmp_path):
     each operand by an exact power of two from its max |value| before splitting, and the epilogue
     undoes it: inputs and weights far outside fp16's range (1e-39 .. 1e20), a lone outlier setting
     the scale, and an all-zero input must all stay within the fp32-faithful bounds (the zero input
-    exactly zero), through implicit kn2row, the accumulating variant and conv1x1."""
+    exactly zero), through implicit kn2row, the accumulating variant and conv1x1.  Also the
+    speculative single pass (the split converts with the previous forward's exponent and a fixup
+    re-converts on a miss): first forward, repeat, a 2^40-scaled input (output exactly 2^40 x)
+    and back all agree bitwise with each other and with the two-pass (channels-last) path."""
     import json
     import subprocess
     import sys
@@ -484,7 +505,10 @@ def test_f16_split_scaling_range(oracle, tmp_path):
     r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, CLB_SPLIT="3xf16"), cwd=str(root))
     assert r.returncode == 0, r.stderr[-3000:]
-    res = json.loads(r.stdout.strip().splitlines()[-1])
+    allres = json.loads(r.stdout.strip().splitlines()[-1])
+    res, spec = allres["range"], allres["spec"]
+    assert spec["hit_equal"] and spec["scaled_exact"] and spec["back_equal"] and spec["two_pass_equal"], spec
+    assert spec["rel_l2"] <= FP32_L2 and spec["max_rel"] <= FP32_MAX, spec
     assert len(res) == 3 * len(F16_RANGE_CASES)
     for e in res:
         assert e["split"] == "3xf16", e
