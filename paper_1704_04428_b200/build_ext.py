@@ -24,7 +24,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                   "-I", str(ROOT / "include"), "-I", str(CSRC)]
-CU_SOURCES = ["prepass.cu", "tc_conv.cu", "direct.cu", "api.cu"]
+CU_SOURCES = ["prepass.cu", "tc_conv.cu", "tc_direct.cu", "direct.cu", "api.cu"]
 CXX_SOURCES = ["facade.cpp"]
 HEADERS = ["ptx.cuh", "tc_conv.cuh", "split_tile.cuh", "internal.hpp"]
 

@@ -124,6 +124,7 @@ struct cl_plan {
     size_t wpack_bytes = 0;
     // fp16 split: exponent slots [ew, ex], the absmax pass's counter and partials (device)
     int* scale = nullptr;
+    bool tc_direct = false;    // direct-gpu on the tensor cores (tc_direct.cu; tiny-C layers, fp32)
     float* wraw = nullptr;     // direct-gpu: MKKC fp32 weights as given
     // direct-gpu, 3 -> 16/32/64 channels 3x3: host weights [c][i][j][m] passed as a kernel
     // parameter (constant-bank FFMA operands).  Only filled by cl_conv_set_weights_host (the host
@@ -577,6 +578,16 @@ void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int
         }
         case CL_METHOD_DIRECT: {
             if (nhwc) throw Error(CL_EUNSUPPORTED, "channels-last forward: implicit kn2row / conv1x1 / kn2row-acc only");
+            if (p->tc_direct) {
+                // tensor cores: the input's exponent (max|x|, a small tensor), then the fused
+                // gather + split + MMA + TMA-store kernel
+                launch_absmax_exp(x, (long long)d.n * d.c * d.h * d.w, p->scale, p->scale + 1, s);
+                if (p->ev_begin && ev_first) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
+                launch_tc_direct(x, p->wpack, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, p->P, p->Q, p->scale, s);
+                p->launches += 2;
+                tc_done();
+                break;
+            }
             // the dominant (and only) kernel of this method: bracket it for the profile events
             if (p->ev_begin && ev_first) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
             const bool param = !p->wparam.empty() && !capturing(s);
@@ -752,11 +763,22 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
         p->method = m;
         p->prec = precision;
         p->planes = conv_planes_for(precision, m, d.c, 2.0 * d.n * d.m * d.c * d.k * d.k * (double)P * Q);
+        {
+            // direct-gpu on the tensor cores where its one-K-block kernel applies (fp32-faithful fp16
+            // split; CLB_DIRECT_TC=0 keeps the CUDA-core kernel): VGG conv1_1 0.154 -> see DESIGN 4.1c
+            static const bool direct_tc = !(std::getenv("CLB_DIRECT_TC") && std::atoi(std::getenv("CLB_DIRECT_TC")) == 0);
+            if (m == CL_METHOD_DIRECT && precision == CL_PREC_FP32 && direct_tc &&
+                tc_direct_shape(d.c, d.k, d.m, d.stride, d.pad, P, Q)) {
+                p->tc_direct = true;
+                p->planes = kPlanesF16;
+            }
+        }
         p->device = device;
         p->Cp = round_up(d.c, k_granule(p->planes));
         p->Kp = round_up(d.k * d.k * d.c, k_granule(p->planes));
         p->bn = bn_for(d.m);
         if (is_patch_method(m)) p->wpack_bytes = (size_t)d.m * row_bytes(p->planes, p->Kp);
+        else if (m == CL_METHOD_DIRECT && p->tc_direct) p->wpack_bytes = (size_t)d.m * kRowBytes;   // [M][32 words]
         else if (m == CL_METHOD_DIRECT) p->wpack_bytes = (size_t)d.m * d.k * d.k * d.c * 4;
         else p->wpack_bytes = (size_t)d.k * d.k * d.m * row_bytes(p->planes, p->Cp);
         if (cudaMalloc(&p->wpack, p->wpack_bytes) != cudaSuccess) {
@@ -764,7 +786,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             delete p;
             throw Error(CL_ENOMEM, "packed-weight allocation failed");
         }
-        if (m == CL_METHOD_DIRECT) p->wraw = p->wpack;
+        if (m == CL_METHOD_DIRECT && !p->tc_direct) p->wraw = p->wpack;
         if (p->planes == kPlanesF16) {
             const size_t sb = (size_t)kScaleBufInts * sizeof(int);
             if (cudaMalloc(&p->scale, sb) != cudaSuccess || cudaMemset(p->scale, 0, sb) != cudaSuccess) {
@@ -864,7 +886,10 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
         const cl_conv_desc& d = p->d;
         if (is_patch_method(p->method))
             launch_rows_split(d_w, p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);   // MKKC == M x k^2C
-        else if (p->method == CL_METHOD_DIRECT) {
+        else if (p->tc_direct) {   // [M][k^2 C] MKKC rows -> fp16-split rows of 32, scaled by 2^ew
+            launch_absmax_exp(d_w, (long long)d.m * d.k * d.k * d.c, p->scale, p->scale, s);
+            launch_rows_split(d_w, p->wpack, d.m, d.k * d.k * d.c, 32, p->planes, s, p->scale);
+        } else if (p->method == CL_METHOD_DIRECT) {
             CLB_CUDA(cudaMemcpyAsync(p->wpack, d_w, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
             p->wparam.clear();   // device weights: the kernels read p->wraw (stream-ordered, no host copy)
         } else {
@@ -890,7 +915,10 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
         const cl_conv_desc& d = p->d;
         if (is_patch_method(p->method))
             launch_rows_split(static_cast<float*>(dw), p->wpack, d.m, d.k * d.k * d.c, p->Kp, p->planes, s);
-        else if (p->method == CL_METHOD_DIRECT) {
+        else if (p->tc_direct) {
+            launch_absmax_exp(static_cast<float*>(dw), (long long)d.m * d.k * d.k * d.c, p->scale, p->scale, s);
+            launch_rows_split(static_cast<float*>(dw), p->wpack, d.m, d.k * d.k * d.c, 32, p->planes, s, p->scale);
+        } else if (p->method == CL_METHOD_DIRECT) {
             CLB_CUDA(cudaMemcpyAsync(p->wpack, dw, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
             p->wparam.clear();
             if (direct_param_shape(d.c, d.k, d.m, d.stride, p->Q)) pack_param_weights(p, h_w);
@@ -921,7 +949,7 @@ cl_method cl_conv_resolved_method(const cl_plan* p) { return p ? p->method : CL_
 
 const char* cl_conv_operand_split(const cl_plan* p) {
     if (!p) return "";
-    if (p->method == CL_METHOD_DIRECT) return "fp32-fma";
+    if (p->method == CL_METHOD_DIRECT && !p->tc_direct) return "fp32-fma";
     switch (p->planes) {
         case 1: return "tf32";
         case 2: return "3xtf32";

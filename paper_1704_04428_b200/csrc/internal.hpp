@@ -90,7 +90,8 @@ inline unsigned* spec_reset_slots(int* slots) { return reinterpret_cast<unsigned
 SplitJob make_split_job(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp);
 void launch_split_tail(const SplitJob& j, int planes, cudaStream_t s);
 // a[rows][K] -> as[rows][planes][Kp]
-void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s);
+void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s,
+                       const int* sexp = nullptr);
 // b[K][cols] -> bs[cols][planes][Kp]
 void launch_transpose_split(const float* b, void* bs, int K, int cols, int Kp, int planes, cudaStream_t s);
 // w MKKC -> wp[tap][M][planes][Cp], or (stacked) wp[i][M][j][planes][Cp]
@@ -132,6 +133,17 @@ struct Operand {
 };
 
 void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int box_taps = 1);
+// a plain (unswizzled) tiled map: the TMA-store output of the tensor-core direct kernel
+void encode_tiled_map(CUtensorMap* map, CUtensorMapDataType dt, int rank, void* ptr, const cuuint64_t* dims,
+                      const cuuint64_t* strides, const cuuint32_t* box, const cuuint32_t* estr);
+
+// ---- tensor-core direct kernel for tiny-C layers (tc_direct.cu) ----------------------------
+// C k^2 <= 32 (C = 1..3 at k = 3, C = 1 at k = 5), stride 1, same padding, M in {16..64} % 16,
+// P Q % 128 == 0.  wpack: [M][32 words] fp16-split rows of the MKKC weights (K index (i k + j) C + c,
+// zero-padded to 32) scaled by 2^ew; sexp = the plan's exponent slots [ew, ex].
+bool tc_direct_shape(int C, int k, int M, int stride, int pad, int P, int Q);
+void launch_tc_direct(const float* x, const void* wpack, float* y, int N, int C, int H, int W, int M, int k, int pad,
+                      int P, int Q, const int* sexp, cudaStream_t s);
 // p.partials / p.flags must point at tc_scratch_bytes() of device scratch (stream-K fixup).
 // returns the kernels launched: 1, or 2 when a requested fused prepass ran standalone instead
 int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cta_group = 1);

@@ -478,21 +478,23 @@ void launch_nchw_split_speculative(const float* x, void* xs, int N, int C, int H
 // -------------------------------------------------------------------- row-wise split ----
 // grid (ceil(Kp/128), rows), block 128
 __global__ void rows_split_kernel(const float* __restrict__ a, void* __restrict__ as, int K, int Kp,
-                                  int planes) {
+                                  int planes, const int* sexp) {
     const long long r = blockIdx.y;
     const int c = blockIdx.x * 128 + threadIdx.x;
     if (c >= Kp) return;
     const float v = c < K ? __ldg(a + r * K + c) : 0.0f;
-    store_split(as, r * rowel(planes, Kp), c, Kp, planes, v);
+    store_split(as, r * rowel(planes, Kp), c, Kp, planes, v, sexp ? pow2_factors(sexp[0]) : Pow2{1.0f, 1.0f});
 }
 
-void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s) {
+void launch_rows_split(const float* a, void* as, long long rows, int K, int Kp, int planes, cudaStream_t s,
+                       const int* sexp) {
     if (rows <= 0) return;
+    if (planes == kPlanesF16 && !sexp) throw Error(6, "fp16 split rows without their exponent slot");
     for (long long r0 = 0; r0 < rows; r0 += 65535) {
         const long long nr = rows - r0 < 65535 ? rows - r0 : 65535;
         dim3 grid((Kp + 127) / 128, (unsigned)nr);
         rows_split_kernel<<<grid, 128, 0, s>>>(a + r0 * K, static_cast<char*>(as) + r0 * row_bytes(planes, Kp), K,
-                                               Kp, planes);
+                                               Kp, planes, planes == kPlanesF16 ? sexp : nullptr);
     }
     CLB_CUDA(cudaGetLastError());
 }

@@ -123,6 +123,26 @@ __device__ __forceinline__ void bulk_copy_g2s(void* smem, const void* gmem, uint
 
 // order this thread's generic-proxy accesses with its subsequent async-proxy (TMA / bulk) ones
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+// this thread's generic-proxy shared-memory writes -> visible to the async proxy (an MMA or a TMA
+// store reading them)
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// TMA tensor store smem -> global (2-D tile; box elements past the tensor's upper bounds are not
+// written -- a box may not start at a negative coordinate), tracked by this thread's bulk group
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* smem, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(smem_u32(smem)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N of this thread's bulk groups still reading their shared-memory source
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// all of this thread's bulk groups complete (writes performed)
+__device__ __forceinline__ void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, uint64_t* bar, void* smem, int32_t c0,
                                             int32_t c1, int32_t c2) {
@@ -137,6 +157,17 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, uint64_t* bar,
 // (output pixel coordinates shifted by the bounding-box lower corner) plus the per-tap
 // offsets (off_w, off_h) in [0, k).  Loads `pixelsPerColumn` pixels x `channelsPerPixel`
 // channels; taps that fall outside the input are zero-filled -- this IS the padding.
+// 4-D tiled load: coords (c0 innermost .. c3); out-of-bounds elements (negative coordinates
+// included) are zero-filled
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* m, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
 __device__ __forceinline__ void tma_load_im2col_4d(const CUtensorMap* m, uint64_t* bar, void* smem,
                                                    int32_t c, int32_t w, int32_t h, int32_t n,
                                                    uint16_t off_w, uint16_t off_h) {

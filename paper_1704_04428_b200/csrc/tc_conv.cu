@@ -85,6 +85,15 @@ void encode_operand_map(CUtensorMap* map, const Operand& op, int box_rows, int b
                            " failed with CUresult " + std::to_string((int)r));
 }
 
+void encode_tiled_map(CUtensorMap* map, CUtensorMapDataType dt, int rank, void* ptr, const cuuint64_t* dims,
+                      const cuuint64_t* strides, const cuuint32_t* box, const cuuint32_t* estr) {
+    resolve_driver();
+    const CUresult r = g_tiled(map, dt, (cuuint32_t)rank, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(3, "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
+}
+
 namespace {
 
 // Per-device launch configuration of the engine: the >48 KB dynamic smem opt-in (a per-device

@@ -580,13 +580,61 @@ DIRECT_CASES = [(1, 3, 224, 224, 64, 3, 1), (3, 3, 20, 36, 70, 3, 1), (2, 1, 9, 
 def test_direct_unit_kernel(oracle, clb, torch_cuda, case):
     """direct-gpu's persistent unit kernel (Q % 4 == 0: 256-group units spanning rows, full-width
     halos) and its fallback, against the generalised loop nest, incl. pad != k/2.  C = 3, k = 3
-    with M = 64 / 16 / 32 and Q % 4 == 0 run the parameter-weight kernel (weights in the
-    constant bank)."""
+    with M = 16 / 32 and Q % 4 == 0 run the parameter-weight kernel (weights in the constant
+    bank); shapes the tensor-core direct kernel takes (the 224 x 224, M = 64 case) run there."""
     N, C, H, W, M, k, pad = case
     x, w = oracle.make_problem(N, C, H, W, M, k, sum(case))
     ref = oracle.conv_loopnest(x, w, pad, 1)
     y = _run(clb, torch_cuda, "direct-gpu", x, w, pad=pad)
     _check_fp32(oracle, y, ref, f"direct {case}")
+
+
+TC_DIRECT_CASES = [(2, 3, 224, 224, 64, 3), (3, 3, 16, 16, 32, 3), (2, 1, 32, 32, 64, 5), (2, 2, 8, 16, 32, 3),
+                   (1, 1, 64, 96, 64, 3), (5, 3, 32, 8, 64, 3)]
+
+_TC_DIRECT_SCRIPT = r'''
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+from oracle import oracle as O
+import paper_1704_04428_b200 as clb
+from tests.test_gpu_parity import TC_DIRECT_CASES
+out = []
+for (N, C, H, W, M, k) in TC_DIRECT_CASES:
+    x, w = O.make_problem(N, C, H, W, M, k, N + C + M)
+    with clb.ConvPlan(clb.LayerConfig("d", C, H, W, M, k, batch=N), "direct-gpu", "fp32") as plan:
+        split = plan.split
+        plan.set_weights(torch.from_numpy(w).cuda())
+        y1 = plan.forward(torch.from_numpy(x).cuda())
+        plan.set_weights_host(torch.from_numpy(w))
+        y2 = plan.forward(torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+    m = O.parity_metrics(y1.cpu().numpy(), O.conv_batch(x, w))
+    out.append({"shape": [N, C, H, W, M, k], "split": split, "rel_l2": m["rel_l2"], "max_rel": m["max_rel"],
+                "finite": m["finite"], "host_weights_equal": bool(torch.equal(y1, y2))})
+print(json.dumps(out))
+'''
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_tc_direct_kernel(oracle, tmp_path, tc):
+    """direct-gpu on the tensor cores (tc_direct.cu: the patch row of every pixel gathered from a
+    TMA-loaded input halo into smem as an fp16-split operand row, 6 kind::f16 MMAs per 128-pixel
+    tile, TMA tensor store of the output): C = 1 / 2 / 3, k = 3 / 5, M = 32 / 64, tiles spanning
+    several image rows, against the oracle; device and host weight uploads agree.  CLB_DIRECT_TC=0
+    (in a subprocess) runs the same shapes on the CUDA-core kernels."""
+    import json
+    import subprocess
+    import sys
+    root = Path(__file__).resolve().parent.parent
+    script = tmp_path / "tcdirect.py"
+    script.write_text(_TC_DIRECT_SCRIPT)
+    r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, CLB_DIRECT_TC=tc), cwd=str(root))
+    assert r.returncode == 0, r.stderr[-3000:]
+    for e in json.loads(r.stdout.strip().splitlines()[-1]):
+        assert e["split"] == ("3xf16" if tc == "1" else "fp32-fma"), e
+        assert e["finite"] and e["rel_l2"] <= FP32_L2 and e["max_rel"] <= FP32_MAX and e["host_weights_equal"], e
 
 
 @pytest.mark.parametrize("case", [(2, 64, 15, 17, 20, 3, 1, 2), (1, 300, 9, 9, 10, 5, 2, 1), (2, 8, 12, 12, 7, 13, 6, 1),
