@@ -767,7 +767,9 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             // direct-gpu on the tensor cores where its one-K-block kernel applies (fp32-faithful fp16
             // split; CLB_DIRECT_TC=0 keeps the CUDA-core kernel): VGG conv1_1 0.154 -> see DESIGN 4.1c
             static const bool direct_tc = !(std::getenv("CLB_DIRECT_TC") && std::atoi(std::getenv("CLB_DIRECT_TC")) == 0);
-            if (m == CL_METHOD_DIRECT && precision == CL_PREC_FP32 && direct_tc &&
+            // (a forced mixed / 3xTF32 split keeps the CUDA-core kernel: the tensor-core one is fp16-split only)
+            const bool f16_allowed = conv_planes_for(precision, CL_METHOD_KN2ROW, 64, 1e30) == kPlanesF16;
+            if (m == CL_METHOD_DIRECT && precision == CL_PREC_FP32 && direct_tc && f16_allowed &&
                 tc_direct_shape(d.c, d.k, d.m, d.stride, d.pad, P, Q)) {
                 p->tc_direct = true;
                 p->planes = kPlanesF16;
