@@ -1,5 +1,7 @@
 #!/bin/bash
-out=gpurun_out/${1:-f16h}; mkdir -p $out
+# GPU test suite + bench lines of every workload (no CPU baseline)
+# usage (gpurun): bash tools/gpu_suite_benches.sh <tag>
+out=gpurun_out/${1:-suite}; mkdir -p $out
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -rf > $out/pytest.log 2>&1; echo "pytest rc=$?" >> $out/pytest.log
 tail -3 $out/pytest.log
 timeout 900 python bench.py --no-cpu-baseline > $out/bench_vgg16.json 2> $out/bench_vgg16.err; echo "bench rc=$?"
