@@ -325,9 +325,26 @@ bool chain_job(cl_plan* p, const float* x, void* ws, SplitJob* out) {
     return true;
 }
 
+void forward_impl(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images, bool nhwc,
+                  bool ev_first, bool ev_last_chunk, const SplitJob* next_job, bool prepass_partial);
+
+// A forward that fails after the fp16 split's speculative prepass was enqueued leaves its group
+// maxima un-zeroed (the contraction zeroes them): zero them here so the next forward's exponent
+// is this input's alone.
 void forward(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images = -1, bool nhwc = false,
              bool ev_first = true, bool ev_last_chunk = true, const SplitJob* next_job = nullptr,
              bool prepass_partial = false) {
+    try {
+        forward_impl(p, x, y, ws, s, n_images, nhwc, ev_first, ev_last_chunk, next_job, prepass_partial);
+    } catch (...) {
+        if (p->scale)
+            cudaMemsetAsync(spec_reset_slots(p->scale), 0, (size_t)kSpecGroups * kSpecStride * sizeof(unsigned), s);
+        throw;
+    }
+}
+
+void forward_impl(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s, int n_images, bool nhwc,
+                  bool ev_first, bool ev_last_chunk, const SplitJob* next_job, bool prepass_partial) {
     cl_conv_desc d = p->d;
     if (n_images >= 0) d.n = n_images;
     require(p->weights_set, "cl_conv_forward: weights not set (cl_conv_set_weights)");
