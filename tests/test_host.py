@@ -379,3 +379,18 @@ def test_concurrency_sm_shares():
     assert sum(concurrency.sm_shares([3, 1], 148)) == 148
     with pytest.raises(ValueError):
         concurrency.sm_shares([1.0] * 80, 148)      # 80 layers x 2 SMs do not fit
+
+
+def test_bench_roofline_peaks_per_operand_split():
+    """bench.py's per-layer peaks follow each plan's operand format (fp16 split = bf16 / 3, mixed =
+    bf16 / 4, 3xTF32 = bf16 / 6, fast modes tf32 / bf16), and the split text covers every
+    CLB_SPLIT selection; no GPU involved."""
+    import bench
+    bf16 = 1653.6
+    tf32 = bf16 / 2
+    assert abs(tf32 * bench.split_factor("3xf16") - bf16 / 3) < 1e-9
+    assert abs(tf32 * bench.split_factor("mixed") - bf16 / 4) < 1e-9
+    assert abs(tf32 * bench.split_factor("3xtf32") - bf16 / 6) < 1e-9
+    assert bench.split_factor("tf32") == 1.0 and bench.split_factor("bf16") == 2.0
+    assert set(bench.SPLIT_TEXT) == {"auto", "3xf16", "mixed", "3xtf32"}
+    assert bench.split_mode() in bench.SPLIT_TEXT
