@@ -600,7 +600,8 @@ void forward_impl(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s
                 // gather + split + MMA + TMA-store kernel
                 launch_absmax_exp(x, (long long)d.n * d.c * d.h * d.w, p->scale, p->scale + 1, s);
                 if (p->ev_begin && ev_first) CLB_CUDA(cudaEventRecord(p->ev_begin, s));
-                launch_tc_direct(x, p->wpack, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, p->P, p->Q, p->scale, s);
+                launch_tc_direct(x, p->wpack, y, d.n, d.c, d.h, d.w, d.m, d.k, d.pad, p->P, p->Q, p->scale, s,
+                                 p->max_sms);
                 p->launches += 2;
                 tc_done();
                 break;

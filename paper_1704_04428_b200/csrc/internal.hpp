@@ -142,8 +142,9 @@ void encode_tiled_map(CUtensorMap* map, CUtensorMapDataType dt, int rank, void* 
 // P Q % 128 == 0.  wpack: [M][32 words] fp16-split rows of the MKKC weights (K index (i k + j) C + c,
 // zero-padded to 32) scaled by 2^ew; sexp = the plan's exponent slots [ew, ex].
 bool tc_direct_shape(int C, int k, int M, int stride, int pad, int P, int Q);
+// max_sms > 0 caps the grid (cl_conv_set_max_sms: concurrent layers)
 void launch_tc_direct(const float* x, const void* wpack, float* y, int N, int C, int H, int W, int M, int k, int pad,
-                      int P, int Q, const int* sexp, cudaStream_t s);
+                      int P, int Q, const int* sexp, cudaStream_t s, int max_sms = 0);
 // p.partials / p.flags must point at tc_scratch_bytes() of device scratch (stream-K fixup).
 // returns the kernels launched: 1, or 2 when a requested fused prepass ran standalone instead
 int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, int cta_group = 1);

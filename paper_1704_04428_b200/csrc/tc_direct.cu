@@ -303,7 +303,7 @@ bool tc_direct_shape(int C, int k, int M, int stride, int pad, int P, int Q) {
 }
 
 void launch_tc_direct(const float* x, const void* wpack, float* y, int N, int C, int H, int W, int M, int k, int pad,
-                      int P, int Q, const int* sexp, cudaStream_t s) {
+                      int P, int Q, const int* sexp, cudaStream_t s, int max_sms) {
     if (!tc_direct_shape(C, k, M, 1, pad, P, Q) || P != H || Q != W)
         throw Error(6, "tensor-core direct kernel: unsupported shape");
     TcDirectParams prm{};
@@ -342,7 +342,8 @@ void launch_tc_direct(const float* x, const void* wpack, float* y, int N, int C,
         cuuint32_t estr[2] = {1, 1};
         encode_tiled_map(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, y, dims, strides, box, estr);
     }
-    const int grid = std::min(prm.tiles, num_sms());
+    const int sms = num_sms();
+    const int grid = std::min(prm.tiles, max_sms > 0 && max_sms < sms ? max_sms : sms);   // one CTA per SM
     const int smem = d_smem_bytes(M);
     if (C == 3) launch_tc_direct_t<3, 3>(mw, mx, my, prm, grid, smem, s);
     else if (C == 2) launch_tc_direct_t<2, 3>(mw, mx, my, prm, grid, smem, s);
