@@ -201,8 +201,15 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     // granularity: 16 iterations keep the epilogue's fold rate below the MMA's (4 had the MMA
     // waiting on TMEM 11-25 % of the time, CLB_TRACE).
     if (p.chunk_iters <= 0) {
-        if (p.planes == kPlanesF16) {   // 32 channels per k-iteration and tap
-            p.chunk_iters = kChunkK / (32 * p.tps);
+        if (p.planes == kPlanesF16) {
+            // 32 channels per k-iteration and tap.  The fp16 split's 22-bit operands leave room for
+            // longer chunks than the other splits: rel-L2 6.7e-7 / 1.3e-6 / 1.9e-6 / 2.7e-6 at
+            // 192 / 384 / 576 / 768 K-elements (bound 1e-5; the reference's own fp32 sum is 1.1e-6
+            // at K = 36864), and fewer TMEM folds per tile are what the epilogue-bound small-N
+            // padded-row layers need: 576 there (VGG conv1_2 0.337 -> 0.310 ms, conv2_1 0.149 ->
+            // 0.126), 384 with one tap per k-iteration (conv3_1 0.134 -> 0.124; 576 coarsens the
+            // stream-K split of conv5_x: 0.077 -> 0.090)  (profiles/r02_f16_chunk.txt)
+            p.chunk_iters = (p.tps > 1 ? kChunkKF16Padded : kChunkKF16) / (32 * p.tps);
         } else if (is_split(p.planes)) {
             p.chunk_iters = kChunkK / (16 * p.tps);
         } else {

@@ -59,6 +59,8 @@ constexpr int kConvWarps = 4;             // converter warpgroup (warps 12..15):
 constexpr int kRegsControl = 64, kRegsEpi = 200, kRegsConv = 48;
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kChunkK = 192;          // fp32-faithful splits: K-elements per TMEM accumulation chunk
+constexpr int kChunkKF16 = 384;       // ... the fp16 split, one tap per k-iteration
+constexpr int kChunkKF16Padded = 576; // ... the fp16 split, tap-shared padded rows
 constexpr int kBarrierBytes = 512;
 constexpr int kMaxPeers = 8;     // ranks of a fused output all-gather (one node)
 constexpr int kMaxUnits = 160;   // scheduling units per launch (>= SM count; = kMaxGrid)
