@@ -595,7 +595,8 @@ void forward_impl(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s
         }
         case CL_METHOD_DIRECT: {
             if (nhwc) throw Error(CL_EUNSUPPORTED, "channels-last forward: implicit kn2row / conv1x1 / kn2row-acc only");
-            if (p->tc_direct) {
+            const bool aligned16 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+            if (p->tc_direct && aligned16) {
                 // tensor cores: the input's exponent (max|x|, a small tensor), then the fused
                 // gather + split + MMA + TMA-store kernel
                 launch_absmax_exp(x, (long long)d.n * d.c * d.h * d.w, p->scale, p->scale + 1, s);
@@ -807,11 +808,20 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             throw Error(CL_ENOMEM, "packed-weight allocation failed");
         }
         if (m == CL_METHOD_DIRECT && !p->tc_direct) p->wraw = p->wpack;
+        if (p->tc_direct && cudaMalloc(&p->wraw, (size_t)d.m * d.k * d.k * d.c * 4) != cudaSuccess) {
+            // the raw MKKC weights too: the CUDA-core kernel serves inputs / outputs the tensor
+            // core kernel's TMA maps cannot address (not 16 B aligned)
+            cudaGetLastError();
+            cudaFree(p->wpack);
+            delete p;
+            throw Error(CL_ENOMEM, "weight allocation failed");
+        }
         if (p->planes == kPlanesF16) {
             const size_t sb = (size_t)kScaleBufInts * sizeof(int);
             if (cudaMalloc(&p->scale, sb) != cudaSuccess || cudaMemset(p->scale, 0, sb) != cudaSuccess) {
                 cudaGetLastError();
                 cudaFree(p->wpack);
+                if (p->tc_direct) cudaFree(p->wraw);
                 cudaFree(p->scale);
                 delete p;
                 throw Error(CL_ENOMEM, "scale slot allocation failed");
@@ -888,6 +898,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
             cudaMemset(p->flags, 0, (kMaxGrid + 8) * sizeof(unsigned)) != cudaSuccess) {
             cudaGetLastError();
             cudaFree(p->wpack);
+            if (p->tc_direct) cudaFree(p->wraw);
             cudaFree(p->scale);
             delete p;
             throw Error(CL_ENOMEM, "flag allocation failed");
@@ -909,6 +920,7 @@ cl_status cl_conv_set_weights(cl_plan* p, const float* d_w, void* stream) {
         else if (p->tc_direct) {   // [M][k^2 C] MKKC rows -> fp16-split rows of 32, scaled by 2^ew
             launch_absmax_exp(d_w, (long long)d.m * d.k * d.k * d.c, p->scale, p->scale, s);
             launch_rows_split(d_w, p->wpack, d.m, d.k * d.k * d.c, 32, p->planes, s, p->scale);
+            CLB_CUDA(cudaMemcpyAsync(p->wraw, d_w, (size_t)d.m * d.k * d.k * d.c * 4, cudaMemcpyDeviceToDevice, s));
         } else if (p->method == CL_METHOD_DIRECT) {
             CLB_CUDA(cudaMemcpyAsync(p->wpack, d_w, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
             p->wparam.clear();   // device weights: the kernels read p->wraw (stream-ordered, no host copy)
@@ -938,6 +950,7 @@ cl_status cl_conv_set_weights_host(cl_plan* p, const float* h_w, void* stream) {
         else if (p->tc_direct) {
             launch_absmax_exp(static_cast<float*>(dw), (long long)d.m * d.k * d.k * d.c, p->scale, p->scale, s);
             launch_rows_split(static_cast<float*>(dw), p->wpack, d.m, d.k * d.k * d.c, 32, p->planes, s, p->scale);
+            CLB_CUDA(cudaMemcpyAsync(p->wraw, dw, bytes, cudaMemcpyDeviceToDevice, s));
         } else if (p->method == CL_METHOD_DIRECT) {
             CLB_CUDA(cudaMemcpyAsync(p->wpack, dw, p->wpack_bytes, cudaMemcpyDeviceToDevice, s));
             p->wparam.clear();
@@ -1207,6 +1220,7 @@ void cl_conv_destroy(cl_plan* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     if (p->wpack) cudaFree(p->wpack);
+    if (p->tc_direct && p->wraw) cudaFree(p->wraw);
     if (p->scale) cudaFree(p->scale);
     if (p->flags) cudaFree(p->flags);
     if (p->own_ws) cudaFree(p->own_ws);

@@ -609,9 +609,18 @@ for (N, C, H, W, M, k) in TC_DIRECT_CASES:
         plan.set_weights_host(torch.from_numpy(w))
         y2 = plan.forward(torch.from_numpy(x).cuda())
         torch.cuda.synchronize()
-    m = O.parity_metrics(y1.cpu().numpy(), O.conv_batch(x, w))
+        # an input 4 B off 16-byte alignment: the TMA maps cannot address it -> the CUDA-core kernel
+        xb = torch.empty(x.size + 1, device="cuda")
+        xm = xb[1:].view(N, C, H, W)
+        xm.copy_(torch.from_numpy(x))
+        y3 = plan.forward(xm)
+        torch.cuda.synchronize()
+    ref = O.conv_batch(x, w)
+    m = O.parity_metrics(y1.cpu().numpy(), ref)
+    m3 = O.parity_metrics(y3.cpu().numpy(), ref)
     out.append({"shape": [N, C, H, W, M, k], "split": split, "rel_l2": m["rel_l2"], "max_rel": m["max_rel"],
-                "finite": m["finite"], "host_weights_equal": bool(torch.equal(y1, y2))})
+                "finite": m["finite"], "host_weights_equal": bool(torch.equal(y1, y2)),
+                "misaligned_rel_l2": m3["rel_l2"], "misaligned_max_rel": m3["max_rel"]})
 print(json.dumps(out))
 '''
 
@@ -621,7 +630,8 @@ def test_tc_direct_kernel(oracle, tmp_path, tc):
     """direct-gpu on the tensor cores (tc_direct.cu: the patch row of every pixel gathered from a
     TMA-loaded input halo into smem as an fp16-split operand row, 6 kind::f16 MMAs per 128-pixel
     tile, TMA tensor store of the output): C = 1 / 2 / 3, k = 3 / 5, M = 32 / 64, tiles spanning
-    several image rows, against the oracle; device and host weight uploads agree.  CLB_DIRECT_TC=0
+    several image rows, against the oracle; device and host weight uploads agree; an input off
+    16-byte alignment (which the kernel's TMA maps cannot address) takes the CUDA-core kernel.  CLB_DIRECT_TC=0
     (in a subprocess) runs the same shapes on the CUDA-core kernels."""
     import json
     import subprocess
@@ -635,6 +645,7 @@ def test_tc_direct_kernel(oracle, tmp_path, tc):
     for e in json.loads(r.stdout.strip().splitlines()[-1]):
         assert e["split"] == ("3xf16" if tc == "1" else "fp32-fma"), e
         assert e["finite"] and e["rel_l2"] <= FP32_L2 and e["max_rel"] <= FP32_MAX and e["host_weights_equal"], e
+        assert e["misaligned_rel_l2"] <= FP32_L2 and e["misaligned_max_rel"] <= FP32_MAX, e
 
 
 @pytest.mark.parametrize("case", [(2, 64, 15, 17, 20, 3, 1, 2), (1, 300, 9, 9, 10, 5, 2, 1), (2, 8, 12, 12, 7, 13, 6, 1),
