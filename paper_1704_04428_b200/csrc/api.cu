@@ -137,6 +137,7 @@ struct cl_plan {
     int peer_m0 = 0, peer_M = 0;
     unsigned* flags = nullptr; // stream-K fixup flags, zeroed once, self-resetting
     bool padded_rows = false;  // implicit kn2row in tap-shared (zero-padded row) mode
+    int wp = 0;                // padded-row mode: padded row width (W + pad; tap-stacked: see tma_store)
     int stack_k = 1;           // > 1: padded-row mode with the k taps of a kernel row stacked on N
     int bn_stack = 0;          // its tile N (k x channels per column tile)
     int msub = 1;              // 2: padded-row mode with two 128-row sub-tiles per B stage (TcParams::msub)
@@ -184,7 +185,7 @@ void* scratch_of(const cl_plan* p, void* ws) { return static_cast<char*>(ws) + a
 // Tap-stacked mode reads A through an overlapping view whose bounds check covers only the
 // row dimension: zeroed rows before (the first image's leading padding, made real) and after
 // the padded grid keep every read in bounds and every out-of-image tap zero.
-int stack_lead_rows(const cl_plan* p) { return p->stack_k > 1 ? p->d.pad * (p->d.w + p->d.pad) + p->d.pad : 0; }
+int stack_lead_rows(const cl_plan* p) { return p->stack_k > 1 ? p->d.pad * p->wp + p->d.pad : 0; }
 int stack_trail_rows(const cl_plan* p) { return p->stack_k > 1 ? 4 * 32 : 0; }
 size_t stack_slack_rows(const cl_plan* p) { return (size_t)stack_lead_rows(p) + stack_trail_rows(p); }
 
@@ -199,7 +200,7 @@ size_t method_ws_bytes(const cl_plan* p) {
         case CL_METHOD_CONV1X1:
         case CL_METHOD_KN2ROW_ACC:
             if (p->padded_rows)
-                return ((size_t)d.n * (d.h + d.pad) * (d.w + d.pad) + stack_slack_rows(p)) * row_bytes(p->planes, p->Cp);
+                return ((size_t)d.n * (d.h + d.pad) * p->wp + stack_slack_rows(p)) * row_bytes(p->planes, p->Cp);
             return xs;
         case CL_METHOD_KN2ROW_EXPLICIT:
         case CL_METHOD_KN2COL:
@@ -311,7 +312,7 @@ void* resolve_ws(cl_plan* p, void* ws) {
 bool chain_job(cl_plan* p, const float* x, void* ws, SplitJob* out) {
     const bool implicit = p->method == CL_METHOD_KN2ROW || p->method == CL_METHOD_CONV1X1 ||
                           p->method == CL_METHOD_KN2ROW_ACC;
-    if (!implicit || !is_split(p->planes)) return false;
+    if (!implicit || !is_split(p->planes) || (p->padded_rows && p->wp != p->d.w + p->d.pad)) return false;
     const cl_conv_desc& d = p->d;
     void* xs = ws;
     int pad = 0;
@@ -437,7 +438,7 @@ void forward_impl(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s
             if (p->padded_rows) {
                 // tap-shared mode: zero-padded NHWC rows; each stage loads ONE A box of 128+k-1
                 // rows per kernel row i and feeds its k taps through row-shifted descriptors
-                const int Hp = d.h + d.pad, Wp = d.w + d.pad;   // shared padding (tc_conv.cuh)
+                const int Hp = d.h + d.pad, Wp = p->wp;   // shared padding (tc_conv.cuh)
                 const size_t rb = (size_t)row_bytes(p->planes, p->Cp);
                 const long long grid_rows = (long long)d.n * Hp * Wp;
                 const int lead = stack_lead_rows(p), trail = stack_trail_rows(p);
@@ -450,12 +451,12 @@ void forward_impl(cl_plan* p, const float* x, float* y, void* ws, cudaStream_t s
                     launch_split_tail(own_job, p->planes, s);   // the tiles the previous contraction left
                     ++p->launches;
                 } else if (spec) {
-                    launch_nchw_split_speculative(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->scale, s);
+                    launch_nchw_split_speculative(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->scale, s, Wp);
                     p->launches += 2;
                     t_reset = spec_reset_slots(p->scale);
                 } else {
-                    if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s, p->scale);
-                    else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s, p->scale);
+                    if (nhwc) launch_nhwc_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s, p->scale, Wp);
+                    else launch_nchw_to_padded_split(x, grid, d.n, d.c, d.h, d.w, d.pad, p->Cp, p->planes, s, p->scale, Wp);
                     ++p->launches;
                 }
                 Operand a = tiled(xs, grid_rows, 1, p->Cp, p->planes);
@@ -875,6 +876,7 @@ cl_status cl_conv_plan(const cl_conv_desc* desc, cl_method method, cl_precision 
                 p->stack_k = d.k;
                 p->bn_stack = mt * d.k;
             }
+            p->wp = d.w + d.pad;   // padded row width (see TcParams::tma_store for the tap-stacked one)
             // Two sub-tiles per B stage (TcParams::msub): each weight stage feeds two 128-row A
             // boxes, so the operand bytes per MMA drop by 20 % (N = 64) / 14 % (N = 128) at the
             // cost of a stage (4 instead of 6 at N = 64) and tiles twice as large.  Measured (ms,

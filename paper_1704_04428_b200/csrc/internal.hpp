@@ -63,10 +63,12 @@ void launch_nchw_to_nhwc_split(const float* x, void* xs, int N, int C, int HW, i
                                cudaStream_t s, const int* sexp = nullptr);
 // same, into the zero-padded image [n][H+2pad][W+2pad][row] (tap-shared kernel mode)
 // NHWC input (channels last) -> split rows; pad > 0 writes the zero-padded grid (tap-shared mode)
+// (padded grids: wp = the padded row width, 0 = W + pad; the trailing wp - W zeros of a row are the
+// next row's leading padding)
 void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
-                       cudaStream_t s, const int* sexp = nullptr);
+                       cudaStream_t s, const int* sexp = nullptr, int wp = 0);
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
-                                 cudaStream_t s, const int* sexp = nullptr);
+                                 cudaStream_t s, const int* sexp = nullptr, int wp = 0);
 // fp16 split scale: exponent e with max|x| * 2^e in [2^14, 2^15) (0 for an all-zero or non-finite
 // tensor; in [-113, 163] otherwise) written to *out_exp.  `slots` = the plan's scale buffer (partials +
 // completion counter, self-resetting).  Stream-ordered, graph-capturable.
@@ -83,7 +85,7 @@ void launch_absmax_exp(const float* x, long long n, int* slots, int* out_exp, cu
 // range), so the operand is always the one the two-pass form writes (bitwise).  The contraction
 // must then zero the group maxima: spec_reset_slots().
 void launch_nchw_split_speculative(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp,
-                                   int* slots, cudaStream_t s);
+                                   int* slots, cudaStream_t s, int wp = 0);
 inline unsigned* spec_reset_slots(int* slots) { return reinterpret_cast<unsigned*>(slots + kScaleSlots + kAbsmaxBlocks); }
 // the same conversion as a tile job (chained mode) and the tail launch that finishes its tiles
 // left by the previous contraction's converter warps (then resets the job's counter)

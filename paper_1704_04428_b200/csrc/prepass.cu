@@ -185,9 +185,9 @@ void launch_split_tail(const SplitJob& j, int planes, cudaStream_t s) {
 }
 
 void launch_nchw_to_padded_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
-                                 cudaStream_t s, const int* sexp) {
+                                 cudaStream_t s, const int* sexp, int wp) {
     if (planes == kPlanesF16 && !sexp) throw Error(6, "fp16 split prepass without its exponent slots");
-    const int Hp = H + pad, Wp = W + pad;
+    const int Hp = H + pad, Wp = wp > 0 ? wp : W + pad;
     dim3 grid((unsigned)(((long long)N * Hp * Wp + kSplitPx - 1) / kSplitPx), (Cp + 31) / 32, 1);
     launch_split_kernel(planes, grid, s, x, xs, N, C, Hp * Wp, Cp, H, W, Wp, pad, make_fastdiv((uint32_t)(Hp * Wp)),
                         make_fastdiv((uint32_t)Wp), sexp);
@@ -271,9 +271,9 @@ __global__ void __launch_bounds__(256) nhwc_split_kernel(const float* __restrict
 }
 
 void launch_nhwc_split(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int planes,
-                       cudaStream_t s, const int* sexp) {
+                       cudaStream_t s, const int* sexp, int wp) {
     if (planes == kPlanesF16 && !sexp) throw Error(6, "fp16 split prepass without its exponent slots");
-    const int Hp = H + pad, Wp = W + pad;   // pad > 0: shared-padding grid (see above)
+    const int Hp = H + pad, Wp = pad > 0 && wp > 0 ? wp : W + pad;   // pad > 0: shared-padding grid (see above)
     const long long rows = (long long)N * Hp * Wp;
     const int q4 = Cp / 4;
     const long long total = rows * q4;
@@ -449,9 +449,10 @@ __global__ void __launch_bounds__(256) split_fixup_kernel(const float* __restric
 }
 
 void launch_nchw_split_speculative(const float* x, void* xs, int N, int C, int H, int W, int pad, int Cp, int* slots,
-                                   cudaStream_t s) {
-    // pad > 0: the zero-padded grid of the tap-shared mode; pad == 0: the image pixels
-    const int Hp = pad > 0 ? H + pad : H, Wp = pad > 0 ? W + pad : W;
+                                   cudaStream_t s, int wp) {
+    // pad > 0: the zero-padded grid of the tap-shared mode (row width wp, default W + pad);
+    // pad == 0: the image pixels
+    const int Hp = pad > 0 ? H + pad : H, Wp = pad > 0 ? (wp > 0 ? wp : W + pad) : W;
     const int HW = Hp * Wp;
     const long long ntx = ((long long)N * HW + kSplitPx - 1) / kSplitPx, nty = (Cp + 31) / 32;
     if (ntx * nty >= (1LL << 31)) throw Error(2, "prepass: too many tiles (split the batch)");
