@@ -298,8 +298,11 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
     // three units whenever a range is shorter than a tile, and a 3-piece tile's finisher waits
     // for and adds two partials at the very end of the kernel (VGG conv5_1: those CTAs exit
     // ~8 us after the 2-piece ones; CLB_TRACE_DUMP).  Pick the unit count u <= units that
-    // minimises ceil(chunks / u) + fixup(max pieces per tile), in chunk times: 2 pieces 3,
-    // each further piece +2 (profiles/r01_sk_units.txt).  CLB_SK_UNITS=0 keeps all units.
+    // minimises ceil(chunks / u) + fixup(max pieces per tile), in chunk times: 2 pieces 2
+    // (3 until the fp16 split's longer chunks: at 3, VGG conv4_1 left 13 of its 74 CTA pairs
+    // idle in the stream-K wave rather than split a tile, 0.137 -> 0.132 ms at 2, every other
+    // BASELINE layer unchanged: profiles/r02c_sk_fixup_cost.txt), each further piece +2
+    // (profiles/r01_sk_units.txt).  CLB_SK_UNITS=0 keeps all units.
     p.sk_units = units;
     static const int env_sk = getenv("CLB_SK_UNITS") ? atoi(getenv("CLB_SK_UNITS")) : 1;
     static const int env_fix = getenv("CLB_FIXUP_SMEM") ? atoi(getenv("CLB_FIXUP_SMEM")) : 1;
@@ -330,7 +333,7 @@ int launch_tc(const Operand& a, const Operand& b, TcParams p, cudaStream_t s, in
         };
         auto cost = [&](int u) {
             const int mp = max_pieces(u);
-            return (double)((S + u - 1) / u) + (mp <= 1 ? 0.0 : 3.0 + 2.0 * (mp - 2));
+            return (double)((S + u - 1) / u) + (mp <= 1 ? 0.0 : 2.0 + 2.0 * (mp - 2));
         };
         double best = cost(units);
         for (int u = units - 1; u >= std::max(1, units - 24); --u) {
