@@ -630,7 +630,7 @@ def run_ours(args, run: Run) -> int:
 
     # ---- e2e through the host-buffer C-ABI call (pinned host in / out, every byte timed) ----
     hx = [x.cpu().pin_memory() for x in xs] if args.layout == "nchw" else \
-         [x.permute(0, 3, 1, 2).contiguous().pin_memory() for x in xs]
+         [x.permute(0, 3, 1, 2).contiguous().cpu().pin_memory() for x in xs]   # the host call takes NCHW
     hy = [torch.empty(p.output_shape(), dtype=torch.float32).pin_memory() for p in plans]
     # the layers are independent: each is issued on its own stream (the async call orders its
     # copy-in after prior work on its stream), so their transfers overlap on both copy engines

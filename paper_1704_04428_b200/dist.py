@@ -195,6 +195,11 @@ class MShardPlan:
     def method(self):
         return self.plan.method
 
+    @property
+    def split(self):
+        """Operand format of this rank's slice plan (bench.py's per-layer peak follows it)."""
+        return self.plan.split
+
     def set_weights(self, w_full):
         """w_full: the FULL [M, k, k, C] weights (device tensor); this rank keeps its slice."""
         self.plan.set_weights(w_full[self.m0:self.m1].contiguous())

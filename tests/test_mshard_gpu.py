@@ -84,3 +84,20 @@ def test_mshard_plan(tmp_path, nproc, backend, port):
         assert r["rel_l2"] <= 1e-5 and r["max_rel"] <= 1e-4, r
     if nproc == 2:
         assert res[3]["slice"] == [0, 4]        # M = 7 over 2 ranks: 4 + 3 (uneven, padded gather)
+
+
+@pytest.mark.parametrize("flags", [["--shard", "channels"], ["--shard", "channels-fused"], ["--concurrent"],
+                                   ["--chain"], ["--layout", "nhwc"], ["--precision", "bf16"]],
+                         ids=lambda f: "".join(f).replace("--", "-").lstrip("-"))
+def test_bench_modes_print_one_line(flags):
+    """Every bench.py mode on the smallest workload (C1): exits 0 and prints the driver's JSON
+    line with a roofline, an e2e and a launch count (a per-plan attribute missing on MShardPlan
+    once broke `--shard channels` without any test noticing)."""
+    r = subprocess.run([sys.executable, "bench.py", "--workload", "c1", "--steps", "3", "--warmup", "3",
+                        "--e2e-steps", "2", "--no-cpu-baseline", *flags], cwd=ROOT, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["value"] > 0 and line["gpu_launches"] > 0 and line["n_gpus"] == 1
+    assert line["roofline"]["achieved"] and line["e2e"]["value"] > 0
+    assert len(line["step_ms"]) == 3
