@@ -235,7 +235,7 @@ def relaunch_under_torchrun(args) -> int:
 # ----------------------------------------------------------------- precision ----
 SPLIT_TEXT = {
     "auto": "fp16 split of power-of-2 scaled operands (lo*Hi + hi*Lo + hi*Hi, kind::f16) for the implicit "
-            "kn2row layers of >= 12 GFLOP (C not 8 / 16 / 48) and the tensor-core direct kernel, mixed split "
+            "kn2row layers of >= 1.2 GFLOP (C not 8 / 16 / 48) and the tensor-core direct kernel, mixed split "
             "(hi*Hi tf32 x2 + cross terms bf16 x2) elsewhere",
     "3xf16": "fp16 split of power-of-2 scaled operands (kind::f16 x3) where the method supports it",
     "mixed": "hi*Hi tf32 x2 + cross terms bf16 x2", "3xtf32": "classic 3xTF32"}

@@ -40,10 +40,13 @@ int planes_for(cl_precision precision) {
 // Operand format of a convolution plan.  fp32: the fp16 split (3 MMA slots per 16 channels, half
 // the operand bytes of the mixed split) for the implicit kn2row family wherever
 // it issues fewer MMAs than the mixed split (6 ceil(C/32) < 4 ceil(C/16): not for C = 8, 16, 48)
-// and the layer is large enough (>= 12 GFLOP) to amortise the split's extra pass over the input
-// (max|x|: one launch + 4 B per element, ~3-10 us on these layers): below that the contraction
-// gains 0-2 us (GoogLeNet 3x3 layers, C1, AlexNet b1, the k1-k7 sweep) and the mixed split's
-// single prepass wins (profiles/r02_f16_mode_sweep.txt).
+// and the layer is large enough (>= 1.2 GFLOP) to amortise the split's extra launch (the fixup
+// behind the speculative single-pass prepass, ~2 us): whole forwards, fp16 vs mixed split
+// (profiles/r02c_f16_small_layers.txt): GoogLeNet 3a/1x1 (1.23 GFLOP) 54 -> 50 us, 3a/3x3 60 ->
+// 54, 4a/1x1 44 -> 42, 5b/1x1 41 -> 38.5, C5 k5 56 -> 54, k7 70 -> 65 (half the operand bytes on
+// HBM-bound 1x1 layers, 3 MMA slots instead of 4); C1, C5 k1 / k3 and the AlexNet b1 layers
+// (<= 0.9 GFLOP) lose 3-7 us and keep the mixed split.  (The bound was 12 GFLOP while the fp16
+// split still needed a max|x| pass ahead of it, profiles/r02_f16_mode_sweep.txt.)
 // Otherwise the mixed split.  CLB_SPLIT=3xtf32 / mixed / 3xf16 forces a split (3xf16: where the
 // method supports it).
 int conv_planes_for(cl_precision precision, cl_method m, int C, double flops) {
@@ -60,7 +63,7 @@ int conv_planes_for(cl_precision precision, cl_method m, int C, double flops) {
     const bool implicit = m == CL_METHOD_KN2ROW || m == CL_METHOD_CONV1X1 || m == CL_METHOD_KN2ROW_ACC;
     if (!implicit) return kPlanesMixed;
     if (forced == kPlanesF16) return kPlanesF16;
-    return (6 * ((C + 31) / 32) < 4 * ((C + 15) / 16) && flops >= 12e9) ? kPlanesF16 : kPlanesMixed;
+    return (6 * ((C + 31) / 32) < 4 * ((C + 15) / 16) && flops >= 1.2e9) ? kPlanesF16 : kPlanesMixed;
 }
 
 cl_status fail(cl_status s, const std::string& msg) {

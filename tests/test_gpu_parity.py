@@ -520,15 +520,16 @@ def test_f16_split_scaling_range(oracle, tmp_path):
 
 def test_operand_split_selection(clb, torch_cuda):
     """fp32 plans of the implicit family take the fp16 split where it issues fewer MMAs than the
-    mixed split (C = 8, 16 and 48 keep the mixed split) and the layer has >= 12 GFLOP to amortise
-    the split's max|x| pass; smaller layers, the other GPU methods and C = 16 / 48 the mixed
+    mixed split (C = 8, 16 and 48 keep the mixed split) and the layer has >= 1.2 GFLOP to amortise
+    the split's extra launch; smaller layers, the other GPU methods and C = 16 / 48 the mixed
     split; the fast modes their own format; the direct kernel fp32 FMA."""
     def split(c, method="kn2row-gpu", precision="fp32", k=3, n=256, hw=56):
         with clb.ConvPlan(clb.LayerConfig("s", c, hw, hw, 64, k, batch=n), method, precision) as p:
             return p.split
     assert [split(c) for c in (8, 16, 24, 32, 48, 64, 96, 100)] == \
         ["mixed", "mixed", "3xf16", "3xf16", "mixed", "3xf16", "3xf16", "3xf16"]
-    assert split(64, n=1) == "mixed" and split(64, hw=8) == "mixed"          # < 12 GFLOP
+    assert split(64, n=1) == "mixed" and split(64, hw=7) == "mixed"          # < 1.2 GFLOP
+    assert split(64, hw=8) == "3xf16"                                        # 1.21 GFLOP
     assert split(64, "kn2row-explicit-gpu") == "mixed" and split(64, "im2col-gpu") == "mixed"
     assert split(256, "conv1x1-gpu", k=1) == "3xf16" and split(64, "kn2row-acc-gpu") == "3xf16"
     assert split(64, precision="tf32") == "tf32" and split(64, precision="bf16") == "bf16"
