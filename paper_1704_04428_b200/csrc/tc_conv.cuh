@@ -339,20 +339,28 @@ __device__ __forceinline__ void split_tile_warp(const SplitJob& j, int bx, int b
 // One D row's columns into NCHW planes: column j lands at o + j * plane.  The accumulate
 // branch is hoisted and the address walks by one plane per column, so each element costs a
 // predicated store and a pointer add (a warp's 32 rows make each store one 128 B line).
-__device__ __forceinline__ void store_nchw(float* o, long long plane, int nvalid, int accumulate, const float* sum) {
+// W = columns this thread can hold for the tile (a narrow tile takes the short loop instead of
+// issuing the predicated-off stores and pointer steps of 128 columns)
+template <int W>
+__device__ __forceinline__ void store_nchw_w(float* o, long long plane, int nvalid, int accumulate, const float* sum) {
     if (accumulate) {
 #pragma unroll
-        for (int j = 0; j < 128; ++j) {
+        for (int j = 0; j < W; ++j) {
             if (j < nvalid) *o += sum[j];
             o += plane;
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < 128; ++j) {
+        for (int j = 0; j < W; ++j) {
             if (j < nvalid) *o = sum[j];
             o += plane;
         }
     }
+}
+__device__ __forceinline__ void store_nchw(float* o, long long plane, int nvalid, int accumulate, const float* sum) {
+    if (nvalid <= 32) store_nchw_w<32>(o, plane, nvalid, accumulate, sum);        // warp-uniform
+    else if (nvalid <= 64) store_nchw_w<64>(o, plane, nvalid, accumulate, sum);
+    else store_nchw_w<128>(o, plane, nvalid, accumulate, sum);
 }
 
 // One D row's columns into a row-major (channels-last) output row: float4 where aligned.
@@ -964,8 +972,16 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 row_ok = lane < 33 - p.stack_k;
             }
             if (p.sexp) {
+                if (hcols <= 32) {   // warp-uniform: a narrow tile scales only the columns it has
 #pragma unroll
-                for (int j = 0; j < 128; ++j) sum[j] = apply_pow2(sum[j], ds);
+                    for (int j = 0; j < 32; ++j) sum[j] = apply_pow2(sum[j], ds);
+                } else if (hcols <= 64) {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) sum[j] = apply_pow2(sum[j], ds);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 128; ++j) sum[j] = apply_pow2(sum[j], ds);
+                }
             }
             // ---- store the finished tile ----
             const long long t_st = TRACE ? clock64() : 0;
