@@ -360,6 +360,7 @@ __device__ __forceinline__ void store_nchw_w(float* o, long long plane, int nval
 __device__ __forceinline__ void store_nchw(float* o, long long plane, int nvalid, int accumulate, const float* sum) {
     if (nvalid <= 32) store_nchw_w<32>(o, plane, nvalid, accumulate, sum);        // warp-uniform
     else if (nvalid <= 64) store_nchw_w<64>(o, plane, nvalid, accumulate, sum);
+    else if (nvalid <= 96) store_nchw_w<96>(o, plane, nvalid, accumulate, sum);
     else store_nchw_w<128>(o, plane, nvalid, accumulate, sum);
 }
 
